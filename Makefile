@@ -1,0 +1,39 @@
+# Build of the B200-native library (sm_100a only) and the test oracles.
+#
+#   make            -> paper_1311_7194_b200/_native/libsf_gpu.so   (product: CUDA + C-ABI)
+#   make oracle     -> oracle/liboracle.so (C restatement) and, when /root/reference exists,
+#                      oracle/_ref/libsfref.so (the unmodified reference + shims)
+#
+# Parity-critical flags: -fmad=false (no FMA contraction on the device) and
+# -ffp-contract=off on the host, matching proj/CMakeLists.txt:33-37.
+
+NVCC    ?= nvcc
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -fmad=false -std=c++17 --expt-relaxed-constexpr \
+           -Xcompiler -fPIC,-ffp-contract=off,-O2 -Xptxas -warn-spills
+SRC_DIR := paper_1311_7194_b200/csrc
+OUT_DIR := paper_1311_7194_b200/_native
+OBJ_DIR := build/obj
+SRCS    := sf_volume sf_fusion sf_render sf_icp sf_tracker sf_scene
+OBJS    := $(addprefix $(OBJ_DIR)/,$(addsuffix .o,$(SRCS)))
+HDRS    := $(wildcard $(SRC_DIR)/*.h $(SRC_DIR)/*.cuh) include/sf_gpu.h
+LIB     := $(OUT_DIR)/libsf_gpu.so
+
+.PHONY: all lib oracle clean
+all: lib
+lib: $(LIB)
+
+$(OBJ_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
+	@mkdir -p $(OBJ_DIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(LIB): $(OBJS)
+	@mkdir -p $(OUT_DIR)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -Xcompiler -fPIC
+
+oracle:
+	$(MAKE) -C oracle port
+	@if [ -d /root/reference/proj/src ]; then $(MAKE) -C oracle ref; else echo "reference sources absent: using prebuilt oracle/_ref"; fi
+
+clean:
+	rm -rf build $(LIB)

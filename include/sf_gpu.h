@@ -1,0 +1,299 @@
+/*
+ * sf_gpu.h — C-ABI boundary of the B200-native sparse-TSDF hot path.
+ *
+ * Drop-in for the reference library "sparsefusion" (/root/reference/proj). Every entry
+ * point below replaces one reference C++ interface (cited as file:line, relative to
+ * /root/reference/proj). Plain C types only: opaque handles, plain pointers and sizes,
+ * int status codes plus a thread-local message (sf_last_error). No CUDA, torch or Eigen
+ * types appear in the signatures; `stream` is a cudaStream_t passed as void* (NULL =
+ * the legacy default stream).
+ *
+ * Conventions
+ *   - Poses are `double pose[12]`: rotation row-major R[r*3+c] in pose[0..8], translation
+ *     in pose[9..11]; camera -> world, x_w = R x_c + t (include/sparsefusion/pose.hpp:9-16).
+ *   - Depth frames are row-major float, 0 = invalid, optional per-pixel sigma plane
+ *     (include/sparsefusion/camera.hpp:45-63). Normal maps are float xyz per pixel, zero =
+ *     invalid (camera.hpp:67-78).
+ *   - Frame/output pointers may be host or device memory, flagged per call. Host pointers
+ *     are staged through the volume's device buffers on `stream`.
+ *   - Calls that return statistics synchronise `stream`; the *_async variants do not.
+ *   - A volume handle is not thread-safe (mirrors grid.hpp:93-95: single writer).
+ *   - Numerics follow the reference bit-for-bit (FP64, no contraction, same operation
+ *     order). The only non-bitwise stage is the ICP reduction order
+ *     (compensated sums merged in a tree; pose parity 1e-6).
+ */
+#ifndef SF_GPU_H
+#define SF_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (reference exception types) ------------------------ */
+typedef enum {
+    SF_OK = 0,
+    SF_INVALID_ARGUMENT = 1, /* std::invalid_argument  (grid.cpp:14-17, fusion.cpp:12-16, ...) */
+    SF_OUT_OF_RANGE = 2,     /* std::out_of_range      (grid.cpp:83,122,133)                   */
+    SF_LOGIC_ERROR = 3,      /* std::logic_error       (grid.cpp:139)                          */
+    SF_POOL_EXHAUSTED = 4,   /* PoolExhausted          (grid.hpp:24-26, grid.cpp:90-92)        */
+    SF_TRACKING_LOST = 5,    /* TrackingLost           (registration.hpp:18-20, .cpp:202-204)  */
+    SF_CUDA_ERROR = 6,
+    SF_IO_ERROR = 7,         /* std::runtime_error from snapshot I/O (grid.cpp:333-408)        */
+    SF_UNSUPPORTED = 8       /* option not implemented on the device path (fails loudly)      */
+} sf_status;
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* sf_last_error(void);
+/* Library/ABI version, e.g. "sf_gpu 0.1 sm_100a". */
+const char* sf_version(void);
+
+/* ---- plain data (mirrors of the reference structs) ---------------------------------- */
+
+/* GridConfig (grid.hpp:28-40). truncation <= 0 -> 4 * voxel_size. */
+typedef struct {
+    int32_t blocks_per_axis;       /* N */
+    int32_t voxels_per_block_axis; /* M */
+    double box_origin[3];
+    double box_side;
+    double truncation;
+} sf_grid_config;
+
+/* AuxQuantization (grid.hpp:53-63). mode 0 = Weight, 1 = Variance. */
+typedef struct {
+    int32_t mode;
+    double w_max;
+    double p_min;
+    double p_max;
+} sf_aux_quant;
+
+/* Intrinsics (camera.hpp:9-24). */
+typedef struct {
+    int32_t width;
+    int32_t height;
+    double fx, fy, cx, cy;
+    double near_plane, far_plane;
+} sf_intrinsics;
+
+/* DepthFrame (camera.hpp:45-63). sigma may be NULL (no recorded sigma plane). */
+typedef struct {
+    sf_intrinsics intrinsics;
+    const float* depth; /* width*height */
+    const float* sigma; /* width*height or NULL */
+    int32_t on_device;  /* 1: device pointers; 0: host pointers */
+} sf_frame;
+
+/* FusionParams (fusion.hpp:18-31). mode 0 Simple, 1 Weighted, 2 Kalman. */
+typedef struct {
+    int32_t mode;
+    double w_fixed;
+    double w_max;
+    double process_variance; /* < 0 -> (0.1 * delta / 127)^2 (fusion.cpp:19-23) */
+    double sigma0;
+    double delta; /* ignored: taken from the grid (fusion.cpp:278) */
+    int32_t refinement_steps;
+    int32_t edge_downweight;
+    double min_variance;
+} sf_fusion_params;
+
+/* FusionStats (fusion.hpp:93-98). */
+typedef struct {
+    uint64_t voxels_updated;
+    uint64_t blocks_allocated_now;
+    uint64_t blocks_total;
+    uint64_t memory_bytes;
+} sf_fusion_stats;
+
+/* RaycastStats (render.hpp:41-49). */
+typedef struct {
+    uint64_t sample_steps;
+    uint64_t hit_pixels;
+    uint64_t rays_with_bounds;
+} sf_raycast_stats;
+
+/* MatchParams (registration.hpp:22-34) incl. its NormalOptions (camera.hpp:77-80). */
+typedef struct {
+    double max_distance;
+    double max_normal_angle;
+    int32_t max_iterations;
+    double convergence_epsilon;
+    double eigen_threshold;
+    double shrink_floor;
+    double normal_sigma0;
+    double normal_spatial_scale;
+} sf_match_params;
+
+/* IcpResult + GatedSolution (registration.hpp:68-83). */
+typedef struct {
+    double delta[12];
+    int32_t iterations;
+    uint64_t matches;
+    /* GatedSolution of the last iteration */
+    double motion_r[3];
+    double motion_t[3];
+    double eigenvalues[6];   /* ascending */
+    double eigenvectors[36]; /* column-major: eigenvectors[col*6 + row] */
+    int32_t gated_mask[6];
+    double residual_rms;
+    double shrunk_motion_norm;
+    uint64_t pair_count;
+} sf_icp_result;
+
+/* Volume summary (grid.hpp:103-108, 132-133). */
+typedef struct {
+    sf_grid_config config;
+    sf_aux_quant aux;
+    double delta;
+    double voxel_size;
+    uint64_t pool_capacity;
+    uint64_t allocated_count;
+    uint64_t memory_bytes;
+} sf_volume_info;
+
+/* ---- volume lifecycle: SparseTsdfGrid (grid.hpp:96-193) ------------------------------ */
+typedef struct sf_volume* sf_volume_t;
+
+/* SparseTsdfGrid::SparseTsdfGrid(config, pool_capacity = 0, aux) (grid.hpp:100-101,
+ * grid.cpp:53-72). pool_capacity 0 -> max(1, N^3/8). aux may be NULL (defaults). */
+int sf_volume_create(const sf_grid_config* config, uint64_t pool_capacity, const sf_aux_quant* aux,
+                     int32_t device, sf_volume_t* out);
+int sf_volume_destroy(sf_volume_t vol);
+int sf_volume_get_info(sf_volume_t vol, sf_volume_info* out);
+
+/* SparseTsdfGrid::allocate_block / free_block / block_slot (grid.cpp:82-119). */
+int sf_volume_allocate_block(sf_volume_t vol, const int32_t bc[3], int32_t* slot_out);
+int sf_volume_free_block(sf_volume_t vol, const int32_t bc[3]);
+int sf_volume_block_slot(sf_volume_t vol, const int32_t bc[3], int32_t* slot_out);
+
+/* SparseTsdfGrid::read_voxel / write_voxel (grid.cpp:121-154). read: *is_chi = 1 for chi
+ * (nullopt); write: tsdf_is_chi = 1 writes chi. */
+int sf_volume_read_voxel(sf_volume_t vol, const int32_t vc[3], int32_t* is_chi, double* tsdf, double* aux);
+int sf_volume_write_voxel(sf_volume_t vol, const int32_t vc[3], int32_t tsdf_is_chi, double tsdf, double aux);
+
+/* Block-buffer layout export (grid.hpp:98,178-181 and 65-68,159-162,189-191):
+ *   table:   int32[N^3], z-major / x fastest, -1 = EMPTY
+ *   payload: uint16 per voxel = {int8 tsdf_code (low byte), uint8 aux_code (high byte)},
+ *            M^3 per slot, x fastest. */
+int sf_volume_read_table(sf_volume_t vol, int32_t* host_table);
+int sf_volume_read_payload(sf_volume_t vol, uint64_t first_slot, uint64_t slot_count, uint16_t* host_payload);
+int sf_volume_write_payload(sf_volume_t vol, uint64_t first_slot, uint64_t slot_count, const uint16_t* host_payload);
+/* Free-list stack, bottom to top (grid.hpp:191); *count_out receives its length. */
+int sf_volume_read_free_list(sf_volume_t vol, int32_t* host_out, uint64_t* count_out);
+
+/* STSG v1 snapshot (grid.cpp:333-408). */
+int sf_volume_save_snapshot(sf_volume_t vol, const char* path);
+int sf_volume_load_snapshot(const char* path, uint64_t pool_capacity, int32_t device, sf_volume_t* out);
+
+/* Float payload mode (block-sparse FloatShadowGrid semantics, grid.hpp:77-88): a
+ * device-resident float2 {tsdf, aux} per pool voxel, chi = +inf / aux 0, updated by
+ * sf_integrate alongside the quantized codes and used as the prior (fusion.cpp:313-318).
+ * Unlike the reference shadow it is block-sparse, so any N is allowed. */
+int sf_volume_enable_float_payload(sf_volume_t vol);
+int sf_volume_read_float_payload(sf_volume_t vol, uint64_t first_slot, uint64_t slot_count, float* host_tsdf_aux);
+
+/* ---- hot path ------------------------------------------------------------------------ */
+
+/* fuse_frame(grid, frame, pose, params) (fusion.hpp:102-103, fusion.cpp:274-376):
+ * surface-sampled block keys -> sort/unique -> ordered slot allocation -> frustum/probe
+ * visibility -> per-voxel measurement + filter. On pool exhaustion the allocate-list
+ * prefix before the first unallocatable block is integrated and SF_POOL_EXHAUSTED is
+ * returned (fusion.cpp:369, grid.cpp:90-92). stats may be NULL (then nothing syncs). */
+int sf_integrate(sf_volume_t vol, const sf_frame* frame, const double pose[12],
+                 const sf_fusion_params* params, sf_fusion_stats* stats, void* stream);
+
+/* select_update_blocks (fusion.hpp:71-72, fusion.cpp:187-235), for parity tests: block
+ * coordinates (x,y,z triples) of the allocate list (ascending (z,y,x)) and of the update
+ * list (ascending table order). Counts are in/out: capacity in, size out. */
+int sf_select_update_blocks(sf_volume_t vol, const sf_frame* frame, const double pose[12],
+                            int32_t* allocate_xyz, uint64_t* allocate_count,
+                            int32_t* update_xyz, uint64_t* update_count, void* stream);
+
+/* compute_ray_bounds (render.hpp:38-39, render.cpp:65-153). Outputs width*height floats. */
+int sf_ray_bounds(sf_volume_t vol, const double pose[12], const sf_intrinsics* intr,
+                  float* t_start, float* t_end, int32_t out_on_device, void* stream);
+
+/* raycast(grid, pose, intrinsics) (render.hpp:61-63, render.cpp:155-250). depth: width*height
+ * floats (0 = miss); normals_xyz: 3*width*height floats, camera frame. stats may be NULL. */
+int sf_raycast(sf_volume_t vol, const double pose[12], const sf_intrinsics* intr,
+               float* depth, float* normals_xyz, int32_t out_on_device,
+               sf_raycast_stats* stats, void* stream);
+
+/* compute_normals(frame, opts) (camera.hpp:90, camera.cpp:44-76). */
+int sf_compute_normals(const sf_frame* frame, double sigma0, double spatial_scale,
+                       float* normals_xyz, int32_t out_on_device, void* stream);
+
+/* icp(source, [source_normals,] target, target_normals, initial, params)
+ * (registration.hpp:120-124, registration.cpp:195-220). source_normals may be NULL:
+ * then compute_normals(source, params.normal_options) is used (registration.cpp:218).
+ * Normal-map pointers live where the frames live (frame->on_device). */
+int sf_icp(const sf_frame* source, const float* source_normals, const sf_frame* target,
+           const float* target_normals, const double initial[12], const sf_match_params* params,
+           sf_icp_result* result, void* stream);
+
+/* ---- fused frame loop: run() per-frame body (pipeline.cpp:233-301) ------------------ */
+/* A tracker owns the device-resident state of one reconstruction: the current pose, the
+ * raycast model maps and the per-frame work buffers. Each step is raycast(current pose)
+ * -> icp(captured vs rendered) -> compose -> fuse_frame, or fuse_frame at the supplied
+ * pose (first frame / ground-truth tracking). Steps are fully asynchronous (no host
+ * synchronisation); results are fetched with sf_tracker_fetch. */
+typedef struct sf_tracker* sf_tracker_t;
+
+typedef struct {
+    sf_fusion_params fusion;
+    sf_match_params match;
+    sf_intrinsics camera;
+    int32_t use_graphs; /* capture the per-frame launch sequence in a CUDA graph */
+} sf_tracker_config;
+
+typedef struct {
+    int32_t frame;
+    int32_t registered;
+    int32_t status; /* sf_status of this frame (SF_OK, SF_POOL_EXHAUSTED, SF_TRACKING_LOST) */
+    double pose[12];
+    int32_t iterations;
+    uint64_t matches;
+    double residual_rms;
+    double lambda_over_n[6];
+    int32_t gated_mask[6];
+    sf_fusion_stats fusion;
+    sf_raycast_stats raycast;
+} sf_frame_metrics;
+
+int sf_tracker_create(sf_volume_t vol, const sf_tracker_config* config, const double initial_pose[12],
+                      sf_tracker_t* out);
+int sf_tracker_destroy(sf_tracker_t tr);
+/* mode 0: track (raycast + ICP, except for the tracker's first frame which is fused at the
+ * current pose); mode 1: ground truth (fuse at gt_pose, no raycast/ICP). */
+int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, const double gt_pose[12],
+                    void* stream);
+/* Synchronises `stream` and copies the metrics of the last step. */
+int sf_tracker_fetch(sf_tracker_t tr, sf_frame_metrics* out, void* stream);
+/* Device pointer to the tracker's pose (12 doubles) and to the last step's kernel count. */
+int sf_tracker_device_pose(sf_tracker_t tr, const double** device_pose);
+/* Number of this library's kernels launched by the last sf_tracker_step (excl. graphs
+ * replay bookkeeping): the bench's gpu_launches figure. */
+int sf_tracker_last_launch_count(sf_tracker_t tr, uint64_t* count);
+
+/* ---- synthetic input (scene.hpp:69-79, scene.cpp:101-177) --------------------------- */
+/* Analytic scene of spheres (cx,cy,cz,r), planes (nx,ny,nz,offset; normalised as
+ * AnalyticScene::add_plane does) and axis-aligned boxes (cx,cy,cz,hx,hy,hz). Depth is
+ * sphere traced on the device in FP64 (bit-identical to render_synthetic_depth for
+ * sigma0 == 0); with noise, the Gaussian sequence is drawn on the host with
+ * std::mt19937_64 / std::normal_distribution in the reference's pixel order. */
+typedef struct {
+    const double* spheres; int32_t sphere_count;
+    const double* planes;  int32_t plane_count;
+    const double* boxes;   int32_t box_count;
+} sf_scene;
+
+int sf_render_synthetic_depth(const sf_scene* scene, const double pose[12], const sf_intrinsics* intr,
+                              double noise_sigma0, uint64_t noise_seed, int32_t max_steps,
+                              double tolerance_scale, double domain_size,
+                              float* depth_host, float* sigma_host /* NULL if sigma0 == 0 */);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SF_GPU_H */

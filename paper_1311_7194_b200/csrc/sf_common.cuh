@@ -1,0 +1,195 @@
+// sf_common.cuh — shared device/host numerics and POD layouts for the sparse-TSDF path.
+//
+// PARITY CONTRACT. Every geometric quantity is computed in FP64 with the reference's
+// operation order (the order of /root/reference/proj/src/*.cpp evaluated through the
+// Eigen-API definition in oracle/shim/Eigen/Dense), and the whole library is compiled
+// with -fmad=false (device) / -ffp-contract=off (host), so products and sums are never
+// contracted into FMAs. IEEE division and sqrt are correctly rounded in CUDA FP64, so
+// the device reproduces the reference's doubles bit for bit. Transcendentals (log/exp in
+// the aux codec, cos in MatchParams) are evaluated on the HOST with the same libm as the
+// reference and shipped to the device as tables / scalars.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#ifndef SF_HD
+#define SF_HD __host__ __device__ __forceinline__
+#endif
+
+namespace sf {
+
+constexpr int32_t kEmpty = -1;          // SparseTsdfGrid::kEmpty (grid.hpp:98)
+constexpr int8_t kChiCode = -128;       // grid.hpp:19
+constexpr int kTsdfCodeRange = 127;     // grid.hpp:21
+constexpr uint16_t kChiPayload = 0x0080; // VoxelPayload{-128, 0}: low byte tsdf, high byte aux
+
+struct d3 {
+    double x, y, z;
+};
+
+SF_HD d3 mk(double x, double y, double z) { return d3{x, y, z}; }
+SF_HD d3 add(d3 a, d3 b) { return d3{a.x + b.x, a.y + b.y, a.z + b.z}; }
+SF_HD d3 sub(d3 a, d3 b) { return d3{a.x - b.x, a.y - b.y, a.z - b.z}; }
+SF_HD d3 neg(d3 a) { return d3{-a.x, -a.y, -a.z}; }
+SF_HD d3 scale(double s, d3 a) { return d3{s * a.x, s * a.y, s * a.z}; }  // Eigen: s * v
+SF_HD d3 divs(d3 a, double s) { return d3{a.x / s, a.y / s, a.z / s}; }   // Eigen: v / s
+SF_HD d3 cmul(d3 a, d3 b) { return d3{a.x * b.x, a.y * b.y, a.z * b.z}; } // cwiseProduct
+SF_HD double dot(d3 a, d3 b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; }
+SF_HD double sqnorm(d3 a) { return dot(a, a); }
+SF_HD d3 cross(d3 a, d3 b) {
+    return d3{a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+// Eigen normalized(): v / sqrt(squaredNorm) when squaredNorm > 0.
+SF_HD d3 normalized(d3 a) {
+    const double z = sqnorm(a);
+    if (z > 0.0) return divs(a, sqrt(z));
+    return a;
+}
+SF_HD double dmin(double a, double b) { return (b < a) ? b : a; }  // std::min(a, b)
+SF_HD double dmax(double a, double b) { return (a < b) ? b : a; }  // std::max(a, b)
+SF_HD double dclamp(double v, double lo, double hi) { return (v < lo) ? lo : (hi < v) ? hi : v; }
+
+// 3x3 matrices, row-major m[r*3+c].
+struct m33 {
+    double m[9];
+};
+SF_HD d3 mv(const m33& R, d3 v) {
+    return d3{(R.m[0] * v.x + R.m[1] * v.y) + R.m[2] * v.z, (R.m[3] * v.x + R.m[4] * v.y) + R.m[5] * v.z,
+              (R.m[6] * v.x + R.m[7] * v.y) + R.m[8] * v.z};
+}
+SF_HD m33 mt(const m33& R) {
+    m33 t;
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) t.m[c * 3 + r] = R.m[r * 3 + c];
+    return t;
+}
+SF_HD m33 mm(const m33& A, const m33& B) {
+    m33 r;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            r.m[i * 3 + j] = (A.m[i * 3 + 0] * B.m[0 * 3 + j] + A.m[i * 3 + 1] * B.m[1 * 3 + j]) +
+                             A.m[i * 3 + 2] * B.m[2 * 3 + j];
+    return r;
+}
+SF_HD d3 col(const m33& R, int c) { return d3{R.m[c], R.m[3 + c], R.m[6 + c]}; }
+
+// Pose (pose.hpp:9-16): x_w = R x_c + t.
+struct Pose {
+    m33 R;
+    d3 t;
+};
+SF_HD d3 apply(const Pose& p, d3 x) { return add(mv(p.R, x), p.t); }
+// compose (pose.cpp:6-11)
+SF_HD Pose compose(const Pose& a, const Pose& b) {
+    Pose o;
+    o.R = mm(a.R, b.R);
+    o.t = add(mv(a.R, b.t), a.t);
+    return o;
+}
+// invert (pose.cpp:13-18)
+SF_HD Pose invert(const Pose& a) {
+    Pose o;
+    o.R = mt(a.R);
+    o.t = neg(mv(o.R, a.t));
+    return o;
+}
+SF_HD Pose pose_from12(const double* p) {
+    Pose o;
+    for (int i = 0; i < 9; ++i) o.R.m[i] = p[i];
+    o.t = d3{p[9], p[10], p[11]};
+    return o;
+}
+SF_HD void pose_to12(const Pose& o, double* p) {
+    for (int i = 0; i < 9; ++i) p[i] = o.R.m[i];
+    p[9] = o.t.x;
+    p[10] = o.t.y;
+    p[11] = o.t.z;
+}
+
+// Intrinsics (camera.hpp:9-24) as a POD.
+struct Intr {
+    int w, h;
+    double fx, fy, cx, cy, near_plane, far_plane;
+};
+// unproject (camera.cpp:31-33)
+SF_HD d3 unproject(const Intr& I, double u, double v, double depth) {
+    return d3{(u - I.cx) / I.fx * depth, (v - I.cy) / I.fy * depth, depth};
+}
+// project (camera.cpp:35-42); returns false when !(z > 0).
+SF_HD bool project(const Intr& I, d3 p, double& u, double& v) {
+    if (!(p.z > 0.0)) return false;
+    u = I.fx * p.x / p.z + I.cx;
+    v = I.fy * p.y / p.z + I.cy;
+    return true;
+}
+
+// static_cast<int>(std::lround(x)) as compiled by g++ on x86-64: glibc lround (half away
+// from zero; out-of-range / NaN -> LONG_MIN via cvttsd2si), then truncation to 32 bits.
+SF_HD int ref_lround_int(double x) {
+    long long r;
+    if (!(fabs(x) < 9223372036854775808.0)) r = (long long)0x8000000000000000ULL;
+    else r = llround(x);
+    return (int)(unsigned int)(unsigned long long)r;
+}
+// static_cast<int>(double) on x86-64 (cvttsd2si): truncation, INT_MIN when out of range / NaN.
+SF_HD int ref_to_int(double x) {
+    if (!(x > -2147483649.0 && x < 2147483648.0)) return (int)0x80000000u;
+    return (int)x;
+}
+SF_HD int ref_floor_int(double x) { return ref_to_int(floor(x)); }
+
+// Quantizers (grid.cpp:20-27): lround(clamp(d,-delta,delta) / delta * 127).
+SF_HD int8_t quantize_tsdf(double d, double delta) {
+    const double clamped = dclamp(d, -delta, delta);
+    return (int8_t)(long long)llround(clamped / delta * (double)kTsdfCodeRange);
+}
+SF_HD double dequantize_tsdf(int8_t code, double delta) { return (double)code / (double)kTsdfCodeRange * delta; }
+
+// Volume parameters shared by every kernel (by value).
+struct VolParams {
+    int N, M, M3, res;  // blocks/axis, voxels/block axis, M^3, N*M
+    double ox, oy, oz;  // box origin
+    double box_side, voxel, block_side, delta;
+    int aux_mode;  // 0 weight, 1 variance
+    double aux_w_max, aux_p_min, aux_p_max;
+    uint64_t table_size;  // N^3
+    uint32_t capacity;
+};
+
+// voxel_center (grid.cpp:271-273): origin + (vc + 0.5) * voxel_size
+SF_HD d3 voxel_center(const VolParams& P, int x, int y, int z) {
+    return d3{P.ox + ((double)x + 0.5) * P.voxel, P.oy + ((double)y + 0.5) * P.voxel,
+              P.oz + ((double)z + 0.5) * P.voxel};
+}
+// block_min_corner (grid.cpp:275-277): origin + bc * block_side
+SF_HD d3 block_min_corner(const VolParams& P, int x, int y, int z) {
+    return d3{P.ox + (double)x * P.block_side, P.oy + (double)y * P.block_side, P.oz + (double)z * P.block_side};
+}
+SF_HD uint64_t table_index(const VolParams& P, int x, int y, int z) {
+    return ((uint64_t)z * (uint64_t)P.N + (uint64_t)y) * (uint64_t)P.N + (uint64_t)x;
+}
+
+// Per-frame constants derived from (pose, intrinsics), computed on the device by one
+// thread (so a device-resident ICP pose never round-trips to the host).
+constexpr int kSatAxes = 26;  // 3 box + 5 frustum + 6x3 edge crosses (grid.cpp:208-216)
+struct FrameConsts {
+    Pose pose;        // camera -> world
+    Pose inv;         // world -> camera (invert(pose))
+    Intr intr;
+    double delta;     // grid delta (fusion params.delta := grid.delta(), fusion.cpp:278)
+    // Frustum SAT (grid.cpp:228-269): axis vector, frustum projection interval, validity.
+    d3 sat_axis[kSatAxes];
+    double sat_lo[kSatAxes], sat_hi[kSatAxes];
+    int sat_valid[kSatAxes];
+};
+
+// Fusion parameters (fusion.hpp:18-31) resolved on the host.
+struct FuseParams {
+    int mode;  // 0 simple, 1 weighted, 2 kalman
+    double w_fixed, w_max, q, sigma0, min_variance;
+    int downweight;
+    int has_sigma;
+};
+
+}  // namespace sf

@@ -1,0 +1,804 @@
+// sf_fusion.cu — fuse_frame on the device (fusion.cpp:25-376, grid.cpp:174-269).
+//
+// Per frame (all launches asynchronous, no host round trip):
+//   k_frame_setup      1 thread: camera_from_world, frustum SAT axes + intervals   (grid.cpp:228-259)
+//   k_normals          compute_normals with the fusion options                     (camera.cpp:44-76, fusion.cpp:33-36)
+//   k_edge             depth-edge mask                                              (fusion.cpp:40-62)
+//   k_pixel_meas       5x5 near-edge dilation + every per-pixel factor of the
+//                      measurement (sigma, p_k, w_k, grazing reject)                (fusion.cpp:63-70, 148-171)
+//   k_block_keys       surface samples -> block keys (FP64)                         (fusion.cpp:190-206)
+//   CUB radix sort + unique                 == std::set<BlockLess> order          (fusion.cpp:177-183,193)
+//   k_alloc_flags / CUB scan / k_alloc_assign / k_alloc_finalize
+//                      ordered slot assignment == sequential free-list pops;
+//                      PoolExhausted prefix semantics                              (fusion.cpp:294-299,369; grid.cpp:87-100)
+//   k_visible          SAT frustum test + 9 probes over allocated blocks            (grid.cpp:174-269; fusion.cpp:211-233)
+//   k_integrate        per voxel: project, band test, filter, quantize              (fusion.cpp:81-173, 237-272, 300-364)
+//   k_fuse_finalize    FusionStats                                                  (fusion.cpp:372-375)
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "sf_internal.h"
+
+namespace sf {
+
+constexpr int kThreads = 256;
+constexpr int kPersistentCtas = 148 * 8;
+
+// ---------------------------------------------------------------------------------
+// frame setup (one thread)
+// ---------------------------------------------------------------------------------
+__global__ void k_frame_consts(VolParams P, Intr intr, const double* __restrict__ pose12, FrameConsts* fc) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const Pose pose = pose_from12(pose12);
+    fc->pose = pose;
+    fc->inv = invert(pose);
+    fc->intr = intr;
+    fc->delta = P.delta;
+
+    // Frustum hull and separating axes, exactly as occupied_blocks_in_frustum builds them.
+    const double us[2] = {-0.5, intr.w - 0.5};
+    const double vs[2] = {-0.5, intr.h - 0.5};
+    d3 pts[8];
+    int np = 0;
+    const double zs[2] = {intr.near_plane, intr.far_plane};
+    for (int iz = 0; iz < 2; ++iz)
+        for (int iv = 0; iv < 2; ++iv)
+            for (int iu = 0; iu < 2; ++iu) pts[np++] = apply(pose, unproject(intr, us[iu], vs[iv], zs[iz]));
+    const d3 optical = col(pose.R, 2);
+    auto corner_ray = [&](double u, double v) { return normalized(mv(pose.R, unproject(intr, u, v, 1.0))); };
+    const d3 r00 = corner_ray(us[0], vs[0]);
+    const d3 r10 = corner_ray(us[1], vs[0]);
+    const d3 r01 = corner_ray(us[0], vs[1]);
+    const d3 r11 = corner_ray(us[1], vs[1]);
+    d3 axes[kSatAxes];
+    int na = 0;
+    const d3 box_axes[3] = {mk(1, 0, 0), mk(0, 1, 0), mk(0, 0, 1)};
+    for (int i = 0; i < 3; ++i) axes[na++] = box_axes[i];
+    axes[na++] = optical;
+    axes[na++] = cross(r00, r10);  // top
+    axes[na++] = cross(r11, r01);  // bottom
+    axes[na++] = cross(r01, r00);  // left
+    axes[na++] = cross(r10, r11);  // right
+    const d3 edges[6] = {r00, r10, r01, r11, col(pose.R, 0), col(pose.R, 1)};
+    for (int e = 0; e < 6; ++e)
+        for (int a = 0; a < 3; ++a) axes[na++] = cross(edges[e], box_axes[a]);
+    for (int k = 0; k < kSatAxes; ++k) {
+        fc->sat_axis[k] = axes[k];
+        fc->sat_valid[k] = !(sqnorm(axes[k]) < 1e-18);
+        double lo = INFINITY, hi = -INFINITY;
+        for (int i = 0; i < 8; ++i) {
+            const double d = dot(axes[k], pts[i]);
+            lo = dmin(lo, d);
+            hi = dmax(hi, d);
+        }
+        fc->sat_lo[k] = lo;
+        fc->sat_hi[k] = hi;
+    }
+}
+
+// Zero the per-frame counters; a set dead flag (tracker: tracking lost / pool exhausted
+// earlier) turns every later kernel of the frame into a no-op.
+__global__ void k_fuse_begin(FrameCounters* ctr, const VolCounters* vc, const int* dead) {
+    FrameCounters z;
+    memset(&z, 0, sizeof(z));
+    z.alloc_before = vc->allocated_count;
+    z.skip = dead ? static_cast<uint32_t>(*dead != 0) : 0u;
+    *ctr = z;
+}
+
+// ---------------------------------------------------------------------------------
+// frame preparation
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ bool px_valid(const float* depth, int w, int h, int u, int v) {
+    return u >= 0 && v >= 0 && u < w && v < h && depth[(size_t)v * w + u] > 0.0f;
+}
+
+// compute_normals (camera.cpp:44-76)
+__global__ void k_normals(const float* __restrict__ depth, int w, int h, Intr intr, double sigma0, double spatial,
+                          float* __restrict__ normals, const int* dead) {
+    if (dead && *dead) return;
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    const int v = blockIdx.y * blockDim.y + threadIdx.y;
+    if (u >= w || v >= h) return;
+    float* out = normals + 3 * ((size_t)v * w + u);
+    float nx = 0.f, ny = 0.f, nz = 0.f;
+    if (u >= 1 && u + 1 < w && v >= 1 && v + 1 < h) {
+        const float z = px_valid(depth, w, h, u, v) ? depth[(size_t)v * w + u] : 0.0f;
+        if (z > 0.0f) {
+            const float zl = depth[(size_t)v * w + u - 1];
+            const float zr = depth[(size_t)v * w + u + 1];
+            const float zu = depth[(size_t)(v - 1) * w + u];
+            const float zd = depth[(size_t)(v + 1) * w + u];
+            if (!(zl <= 0.0f || zr <= 0.0f || zu <= 0.0f || zd <= 0.0f)) {
+                const double threshold = 3.0 * sigma0 * double(z) * double(z) + 2.0 * spatial;
+                if (!(fabsf(zl - z) > threshold || fabsf(zr - z) > threshold || fabsf(zu - z) > threshold ||
+                      fabsf(zd - z) > threshold)) {
+                    const d3 du = sub(unproject(intr, u + 1, v, zr), unproject(intr, u - 1, v, zl));
+                    const d3 dv = sub(unproject(intr, u, v + 1, zd), unproject(intr, u, v - 1, zu));
+                    d3 n = cross(du, dv);
+                    const double len = sqrt(sqnorm(n));
+                    if (len > 0.0) {
+                        n = divs(n, len);
+                        if (dot(n, unproject(intr, u, v, z)) > 0.0) n = neg(n);
+                        nx = (float)n.x;
+                        ny = (float)n.y;
+                        nz = (float)n.z;
+                    }
+                }
+            }
+        }
+    }
+    out[0] = nx;
+    out[1] = ny;
+    out[2] = nz;
+}
+
+// Edge mask (fusion.cpp:44-62)
+__global__ void k_edge(const float* __restrict__ depth, int w, int h, double sigma0, uint8_t* __restrict__ edge,
+                       const int* dead) {
+    if (dead && *dead) return;
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    const int v = blockIdx.y * blockDim.y + threadIdx.y;
+    if (u >= w || v >= h) return;
+    uint8_t e = 0;
+    if (!px_valid(depth, w, h, u, v)) {
+        e = 1;
+    } else {
+        const float z = depth[(size_t)v * w + u];
+        const double jump = 3.0 * sigma0 * double(z) * double(z) + 0.02 * double(z);
+        bool is_edge = u == 0 || v == 0 || u == w - 1 || v == h - 1;
+        for (int k = 0; !is_edge && k < 4; ++k) {
+            const int nu = u + (k == 0 ? 1 : k == 1 ? -1 : 0);
+            const int nv = v + (k == 2 ? 1 : k == 3 ? -1 : 0);
+            if (!px_valid(depth, w, h, nu, nv) || fabsf(depth[(size_t)nv * w + nu] - z) > jump) is_edge = true;
+        }
+        e = is_edge ? 1 : 0;
+    }
+    edge[(size_t)v * w + u] = e;
+}
+
+// Per-pixel measurement factors (fusion.cpp:148-171) + near-edge dilation (fusion.cpp:63-70).
+// Everything after the band test in estimate_measurement depends only on the chosen pixel.
+__global__ void k_pixel_meas(const float* __restrict__ depth, const float* __restrict__ sigma, int w, int h,
+                             Intr intr, FuseParams fp, const float* __restrict__ normals,
+                             const uint8_t* __restrict__ edge, double* __restrict__ pix_var,
+                             double* __restrict__ pix_w, uint8_t* __restrict__ pix_ok, const int* dead) {
+    if (dead && *dead) return;
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    const int v = blockIdx.y * blockDim.y + threadIdx.y;
+    if (u >= w || v >= h) return;
+    const size_t idx = (size_t)v * w + u;
+    uint8_t ok = 0;
+    double var = 0.0, wk = 0.0;
+    if (px_valid(depth, w, h, u, v)) {
+        const double measured = depth[idx];
+        const double sg = fp.has_sigma && sigma[idx] > 0.0f ? static_cast<double>(sigma[idx])
+                                                             : fp.sigma0 * measured * measured;
+        var = dmax(sg * sg, fp.min_variance);
+        wk = fp.w_fixed;
+        ok = 1;
+        if (fp.downweight) {
+            double quality = 0.3;
+            const float fx = normals[3 * idx], fy = normals[3 * idx + 1], fz = normals[3 * idx + 2];
+            if ((fx * fx + fy * fy) + fz * fz > 0.0f) {
+                const d3 ray = normalized(unproject(intr, u, v, 1.0));
+                quality = fabs(dot(mk((double)fx, (double)fy, (double)fz), ray));
+            }
+            bool near = false;
+            for (int dv = -2; !near && dv <= 2; ++dv)
+                for (int du = -2; !near && du <= 2; ++du) {
+                    const int nu = u + du, nv = v + dv;
+                    if (nu >= 0 && nv >= 0 && nu < w && nv < h && edge[(size_t)nv * w + nu]) near = true;
+                }
+            if (near) quality *= 0.5;
+            if (quality < 0.2) {
+                ok = 0;
+            } else {
+                wk *= quality;
+                var /= quality;
+            }
+        }
+    }
+    pix_var[idx] = var;
+    pix_w[idx] = wk;
+    pix_ok[idx] = ok;
+}
+
+// ---------------------------------------------------------------------------------
+// block keys, allocation
+// ---------------------------------------------------------------------------------
+__global__ void k_block_keys(VolParams P, const FrameConsts* __restrict__ fc, const float* __restrict__ depth,
+                             int w, int h, int stride, int su, int sv, uint32_t* __restrict__ keys, uint32_t sentinel,
+                             const uint32_t* skip) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= su * sv) return;
+    uint32_t k0 = sentinel, k1 = sentinel, k2 = sentinel;
+    const int u = (i % su) * stride;
+    const int v = (i / su) * stride;
+    if (!*skip && px_valid(depth, w, h, u, v)) {
+        const Intr& intr = fc->intr;
+        const Pose& pose = fc->pose;
+        const d3 dir_cam = normalized(unproject(intr, u, v, 1.0));
+        const d3 dir = mv(pose.R, dir_cam);
+        const double t_hit = (double)depth[(size_t)v * w + u] / dir_cam.z;
+        const double offs[3] = {-fc->delta, 0.0, fc->delta};
+        uint32_t out[3];
+        for (int k = 0; k < 3; ++k) {
+            const d3 x = add(pose.t, scale(t_hit + offs[k], dir));
+            // block_of_point (grid.cpp:283-287)
+            const int bx = ref_floor_int((x.x - P.ox) / P.block_side);
+            const int by = ref_floor_int((x.y - P.oy) / P.block_side);
+            const int bz = ref_floor_int((x.z - P.oz) / P.block_side);
+            const bool in = bx >= 0 && by >= 0 && bz >= 0 && bx < P.N && by < P.N && bz < P.N;
+            out[k] = in ? static_cast<uint32_t>(table_index(P, bx, by, bz)) : sentinel;
+        }
+        k0 = out[0];
+        k1 = out[1];
+        k2 = out[2];
+    }
+    keys[3 * i + 0] = k0;
+    keys[3 * i + 1] = k1;
+    keys[3 * i + 2] = k2;
+}
+
+__global__ void k_list_len(FrameCounters* ctr, const uint32_t* __restrict__ uniq, uint32_t sentinel) {
+    const uint32_t n = ctr->n_unique;
+    const uint32_t len = (n > 0 && uniq[n - 1] == sentinel) ? n - 1 : n;
+    ctr->n_list = len;
+    ctr->limit = len;
+}
+
+__global__ void k_alloc_flags(const FrameCounters* ctr, const uint32_t* __restrict__ uniq,
+                              const int32_t* __restrict__ table, uint32_t* __restrict__ flags, uint32_t cap) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cap) return;
+    uint32_t f = 0;
+    if (i < ctr->n_list && !ctr->skip) f = table[uniq[i]] == kEmpty ? 1u : 0u;
+    flags[i] = f;
+}
+
+// Ordered allocation: the r-th new key (in (z,y,x) order) receives the r-th pop of the
+// free-list stack, exactly as process_block's lazy allocate_block calls would.
+__global__ void k_alloc_assign(FrameCounters* ctr, const uint32_t* __restrict__ uniq,
+                               const uint32_t* __restrict__ ranks, int32_t* __restrict__ table,
+                               const int32_t* __restrict__ free_list, int32_t* __restrict__ slot_key,
+                               uint32_t* __restrict__ occ, const VolCounters* __restrict__ vc,
+                               int2* __restrict__ work, unsigned long long* high_water) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ctr->n_list || ctr->skip) return;
+    const uint32_t key = uniq[i];
+    int32_t slot = table[key];
+    uint32_t fresh = 0;
+    if (slot == kEmpty) {
+        const unsigned long long r = ranks[i];
+        const unsigned long long top = vc->free_top;
+        if (r < top) {
+            slot = free_list[top - 1 - r];
+            table[key] = slot;
+            slot_key[slot] = static_cast<int32_t>(key);
+            atomicOr(&occ[key >> 5], 1u << (key & 31));
+            atomicMax(high_water, (unsigned long long)slot + 1ull);
+            fresh = 1;
+        } else {
+            if (r == top) ctr->limit = i;  // first unallocatable block: PoolExhausted here
+            slot = -1;
+        }
+    }
+    work[i] = make_int2(static_cast<int32_t>(static_cast<uint32_t>(slot) | (fresh << 31)), static_cast<int32_t>(key));
+}
+
+__global__ void k_alloc_finalize(FrameCounters* ctr, const uint32_t* __restrict__ flags,
+                                 const uint32_t* __restrict__ ranks, VolCounters* vc) {
+    if (ctr->skip) return;
+    const uint32_t n = ctr->n_list;
+    const unsigned long long n_new = n ? (unsigned long long)ranks[n - 1] + flags[n - 1] : 0ull;
+    const unsigned long long top = vc->free_top;
+    const unsigned long long got = n_new < top ? n_new : top;
+    vc->free_top = top - got;
+    vc->allocated_count += got;
+    ctr->n_new = static_cast<uint32_t>(n_new);
+    ctr->exhausted = n_new > top ? 1u : 0u;
+}
+
+// ---------------------------------------------------------------------------------
+// visibility: exact SAT + probes over every allocated block
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ bool in_sorted(const uint32_t* __restrict__ a, uint32_t n, uint32_t key) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        const uint32_t x = a[mid];
+        if (x < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo < n && a[lo] == key;
+}
+
+__device__ bool frustum_intersects_block(const VolParams& P, const FrameConsts* __restrict__ fc, d3 lo, d3 hi) {
+    // box axes: the box projection is exactly [lo_a, hi_a]
+    const double blo[3] = {lo.x, lo.y, lo.z}, bhi[3] = {hi.x, hi.y, hi.z};
+    for (int k = 0; k < 3; ++k) {
+        if (fc->sat_hi[k] < blo[k] || bhi[k] < fc->sat_lo[k]) return false;
+    }
+    for (int k = 3; k < kSatAxes; ++k) {
+        if (!fc->sat_valid[k]) continue;
+        const d3 a = fc->sat_axis[k];
+        double mn = INFINITY, mx = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const d3 p = mk(i & 1 ? hi.x : lo.x, i & 2 ? hi.y : lo.y, i & 4 ? hi.z : lo.z);
+            const double d = dot(a, p);
+            mn = dmin(mn, d);
+            mx = dmax(mx, d);
+        }
+        if (fc->sat_hi[k] < mn || mx < fc->sat_lo[k]) return false;
+    }
+    return true;
+}
+
+__global__ void k_visible(VolParams P, const FrameConsts* __restrict__ fc, FrameCounters* ctr,
+                          const VolCounters* __restrict__ vc, const int32_t* __restrict__ slot_key,
+                          const uint32_t* __restrict__ uniq, const float* __restrict__ depth, int w, int h,
+                          int2* __restrict__ work, uint32_t* __restrict__ export_keys, int export_only) {
+    if (ctr->skip || (!export_only && ctr->exhausted)) return;
+    const unsigned long long hw = vc->high_water;
+    const uint32_t n_list = ctr->n_list;
+    const uint32_t base = ctr->limit;
+    const Intr& intr = fc->intr;
+    for (unsigned long long s = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; s < hw;
+         s += (unsigned long long)gridDim.x * blockDim.x) {
+        const int32_t key = slot_key[s];
+        if (key < 0) continue;
+        if (in_sorted(uniq, n_list, static_cast<uint32_t>(key))) continue;  // in the allocate set
+        const int bx = key % P.N, by = (key / P.N) % P.N, bz = key / (P.N * P.N);
+        const d3 lo = block_min_corner(P, bx, by, bz);
+        const double side = P.block_side;
+        const d3 hi = add(lo, mk(side, side, side));
+        if (!frustum_intersects_block(P, fc, lo, hi)) continue;
+        bool visible = false;
+        for (int i = 0; i < 9 && !visible; ++i) {
+            const d3 probe = i == 8 ? add(lo, mk(0.5 * side, 0.5 * side, 0.5 * side))
+                                    : add(lo, mk(i & 1 ? side : 0.0, i & 2 ? side : 0.0, i & 4 ? side : 0.0));
+            const d3 xc = apply(fc->inv, probe);
+            double pu, pv;
+            if (!project(intr, xc, pu, pv)) continue;
+            const int u = ref_lround_int(pu);
+            const int v = ref_lround_int(pv);
+            if (!(u >= 0 && v >= 0 && u < w && v < h)) continue;
+            const float d = depth[(size_t)v * w + u];
+            if (!(d > 0.0f) || xc.z <= d + fc->delta) visible = true;
+        }
+        if (!visible) continue;
+        const uint32_t j = atomicAdd(&ctr->n_update, 1u);
+        if (export_only) export_keys[j] = static_cast<uint32_t>(key);
+        else work[base + j] = make_int2(static_cast<int32_t>(s), key);
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// per-voxel integration
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ uint8_t aux_encode_dev(const VolParams& P, const double* s_thr, double value) {
+    if (P.aux_mode == 0) {
+        const double clamped = dclamp(value, 0.0, P.aux_w_max);
+        return static_cast<uint8_t>(static_cast<long long>(llround(clamped / P.aux_w_max * 255.0)));
+    }
+    // #{k in 1..255 : value >= thresh[k]} by binary search (thresholds ascending).
+    int lo = 0, hi = 255;  // answer in [lo, hi]
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (value >= s_thr[mid]) lo = mid;
+        else hi = mid - 1;
+    }
+    return static_cast<uint8_t>(lo);
+}
+
+template <int MODE, bool FLOATP>
+__global__ void __launch_bounds__(kThreads)
+    k_integrate(VolParams P, const FrameConsts* __restrict__ fc, FuseParams fp, const int2* __restrict__ work,
+                const FrameCounters* __restrict__ ctr, const AuxTables* __restrict__ aux,
+                const float* __restrict__ depth, const double* __restrict__ pix_var, const double* __restrict__ pix_w,
+                const uint8_t* __restrict__ pix_ok, uint16_t* __restrict__ payload, float2* __restrict__ fpayload,
+                unsigned long long* __restrict__ voxels_updated) {
+    __shared__ double s_tdec[256], s_adec[256], s_thr[256];
+    if (ctr->skip) return;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        s_tdec[i] = aux->tsdf_decode[i];
+        s_adec[i] = aux->aux_decode[i];
+        s_thr[i] = aux->aux_thresh[i];
+    }
+    __syncthreads();
+    const Pose inv = fc->inv;
+    const Intr intr = fc->intr;
+    const double delta = P.delta;
+    const int w = intr.w, h = intr.h;
+    const unsigned long long n_work = (unsigned long long)ctr->limit + ctr->n_update;
+    const unsigned long long total = n_work * (unsigned long long)P.M3;
+    const int M = P.M, MM = P.M * P.M, N = P.N;
+    unsigned long long updated = 0;
+    for (unsigned long long g = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; g < total;
+         g += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long item = g / (unsigned)P.M3;
+        const int l = static_cast<int>(g - item * (unsigned)P.M3);
+        const int2 wk = work[item];
+        const uint32_t slot = static_cast<uint32_t>(wk.x) & 0x7fffffffu;
+        const bool fresh = (static_cast<uint32_t>(wk.x) >> 31) != 0;
+        const int key = wk.y;
+        const int bx = key % N, by = (key / N) % N, bz = key / (N * N);
+        const int lx = l % M, ly = (l / M) % M, lz = l / MM;
+        const size_t pidx = (size_t)slot * P.M3 + l;
+        // estimate_measurement (fusion.cpp:81-99, 145)
+        const d3 xc = apply(inv, voxel_center(P, bx * M + lx, by * M + ly, bz * M + lz));
+        bool meas = false;
+        double tsdf_k = 0.0;
+        size_t pix = 0;
+        double pu, pv;
+        if (project(intr, xc, pu, pv)) {
+            const int u = ref_lround_int(pu);
+            const int v = ref_lround_int(pv);
+            if (u >= 0 && v >= 0 && u < w && v < h) {
+                pix = (size_t)v * w + u;
+                const float d = depth[pix];
+                if (d > 0.0f) {
+                    tsdf_k = (double)d - xc.z;
+                    meas = !(fabs(tsdf_k) > delta) && pix_ok[pix];
+                }
+            }
+        }
+        if (!meas) {
+            if (fresh) {
+                payload[pidx] = kChiPayload;
+                if (FLOATP) fpayload[pidx] = make_float2(INFINITY, 0.0f);
+            }
+            continue;
+        }
+        // prior (fusion.cpp:311-322)
+        bool has_prior;
+        double prior_t = 0.0, prior_a = 0.0;
+        if (FLOATP) {
+            const float2 f = fresh ? make_float2(INFINITY, 0.0f) : fpayload[pidx];
+            has_prior = f.x < INFINITY;  // !FloatShadowGrid::is_chi
+            if (has_prior) {
+                prior_t = f.x;
+                prior_a = f.y;
+            }
+        } else {
+            const uint16_t cell = fresh ? kChiPayload : payload[pidx];
+            const int8_t code = static_cast<int8_t>(cell & 0xFF);
+            has_prior = code != kChiCode;
+            if (has_prior) {
+                prior_t = s_tdec[(int)code + 128];
+                prior_a = s_adec[cell >> 8];
+            }
+        }
+        // filters (fusion.cpp:237-272)
+        double new_t, new_a;
+        if (MODE == 0) {  // simple
+            const double wk_ = pix_w[pix];
+            new_t = has_prior ? (1.0 - wk_) * prior_t + wk_ * tsdf_k : tsdf_k;
+            new_a = wk_;
+        } else if (MODE == 1) {  // weighted
+            const double wk_ = pix_w[pix];
+            if (!has_prior) {
+                new_t = tsdf_k;
+                new_a = wk_;
+            } else {
+                new_t = (prior_a * prior_t + wk_ * tsdf_k) / (prior_a + wk_);
+                new_a = dmin(prior_a + wk_, fp.w_max);
+            }
+        } else {  // kalman
+            const double pk = pix_var[pix];
+            if (!has_prior) {
+                new_t = tsdf_k;
+                new_a = pk;
+            } else {
+                const double predicted = prior_a + fp.q;
+                const double gain = predicted / (predicted + pk);
+                new_t = prior_t + gain * (tsdf_k - prior_t);
+                new_a = (1.0 - gain) * predicted;
+            }
+        }
+        const bool chi = fabs(new_t) > delta;
+        uint16_t out = kChiPayload;
+        if (!chi) {
+            const int8_t code = quantize_tsdf(new_t, delta);
+            const uint8_t ac = aux_encode_dev(P, s_thr, new_a);
+            out = static_cast<uint16_t>(static_cast<uint8_t>(code)) | static_cast<uint16_t>(ac << 8);
+        }
+        payload[pidx] = out;
+        if (FLOATP) fpayload[pidx] = chi ? make_float2(INFINITY, 0.0f) : make_float2((float)new_t, (float)new_a);
+        ++updated;
+    }
+    // voxels_updated: warp reduction, one atomic per warp
+    for (int off = 16; off > 0; off >>= 1) updated += __shfl_down_sync(0xffffffffu, updated, off);
+    if ((threadIdx.x & 31) == 0 && updated) atomicAdd(voxels_updated, updated);
+}
+
+__global__ void k_fuse_finalize(FrameCounters* ctr, const VolCounters* vc) {
+    ctr->alloc_now = vc->allocated_count;
+}
+
+// ---------------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------------
+static uint32_t sentinel_of(const VolParams& P) { return static_cast<uint32_t>(P.table_size); }
+static int end_bit_of(const VolParams& P) {
+    const uint32_t s = sentinel_of(P);
+    int b = 1;
+    while (b < 32 && (s >> b) != 0) ++b;
+    return b;
+}
+
+size_t cub_temp_bytes_needed(uint32_t key_cap) {
+    size_t a = 0, b = 0, c = 0;
+    SF_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, a, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)key_cap, 0, 32));
+    SF_CUDA(cub::DeviceSelect::Unique(nullptr, b, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                      (int)key_cap));
+    SF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, c, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)key_cap));
+    return std::max({a, b, c, (size_t)256});
+}
+
+void launch_consts(const VolParams& P, const Intr& intr, const double* d_pose, FrameConsts* d_fc, cudaStream_t s,
+                   uint64_t* launches) {
+    k_frame_consts<<<1, 32, 0, s>>>(P, intr, d_pose, d_fc);
+    SF_LAUNCH_CHECK();
+    if (launches) *launches += 1;
+}
+
+void launch_compute_normals(const float* depth, int w, int h, const Intr& intr, double sigma0, double spatial_scale,
+                            float* normals, cudaStream_t s, uint64_t* launches, const int* dead_flag) {
+    const dim3 blk(32, 8), grd((w + 31) / 32, (h + 7) / 8);
+    k_normals<<<grd, blk, 0, s>>>(depth, w, h, intr, sigma0, spatial_scale, normals, dead_flag);
+    SF_LAUNCH_CHECK();
+    if (launches) *launches += 1;
+}
+
+FuseParams resolve_fuse_params(const Volume& v, const sf_fusion_params& p, bool has_sigma) {
+    // FusionParams::validate (fusion.cpp:12-17) and the mode/aux checks (fusion.cpp:279-283)
+    if (!(p.w_fixed > 0.0) || p.w_fixed > 1.0) throw Error(SF_INVALID_ARGUMENT, "fusion: w_fixed must be in (0, 1]");
+    if (!(p.w_max > 0.0)) throw Error(SF_INVALID_ARGUMENT, "fusion: w_max must be positive");
+    if (p.sigma0 < 0.0) throw Error(SF_INVALID_ARGUMENT, "fusion: sigma0 must be >= 0");
+    if (p.refinement_steps < 0) throw Error(SF_INVALID_ARGUMENT, "fusion: negative refinement_steps");
+    if (p.mode == 2 && v.aux.mode != 1) throw Error(SF_INVALID_ARGUMENT, "fusion: Kalman mode needs a variance-mode grid");
+    if (p.mode != 2 && v.aux.mode != 0)
+        throw Error(SF_INVALID_ARGUMENT, "fusion: weight-mode grid required for this fusion mode");
+    if (p.mode < 0 || p.mode > 2) throw Error(SF_INVALID_ARGUMENT, "fusion: unknown mode");
+    if (p.refinement_steps > 0)
+        throw Error(SF_UNSUPPORTED, "fusion: refinement_steps > 0 is not implemented on the device path");
+    FuseParams f{};
+    f.mode = p.mode;
+    f.w_fixed = p.w_fixed;
+    f.w_max = p.w_max;
+    const double delta = v.P.delta;
+    if (p.process_variance >= 0.0) {
+        f.q = p.process_variance;
+    } else {  // FusionParams::resolved_q (fusion.cpp:19-23)
+        const double step = 0.1 * delta / kTsdfCodeRange;
+        f.q = step * step;
+    }
+    f.sigma0 = p.sigma0;
+    f.min_variance = p.min_variance;
+    f.downweight = p.edge_downweight ? 1 : 0;
+    f.has_sigma = has_sigma ? 1 : 0;
+    return f;
+}
+
+void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* depth, const float* sigma,
+                 const FuseParams& fp, cudaStream_t s, bool export_only, uint64_t* launches, const int* dead_flag) {
+    const int w = fb.w, h = fb.h;
+    const VolParams& P = v.P;
+    uint64_t n = 0;
+    launch_consts(P, intr, fb.pose, fb.fc, s, &n);
+    k_fuse_begin<<<1, 1, 0, s>>>(fb.ctr, v.d_vc, dead_flag);
+    SF_LAUNCH_CHECK();
+    n += 1;
+    const dim3 blk2(32, 8), grd2((w + 31) / 32, (h + 7) / 8);
+    const int* dead = reinterpret_cast<const int*>(&fb.ctr->skip);
+    if (!export_only) {
+        // Frame prep: normals with the fusion options (sigma0, spatial_scale = 0.25 * delta;
+        // fusion.cpp:33-36), edge mask, per-pixel measurement factors.
+        if (fp.downweight) {
+            k_normals<<<grd2, blk2, 0, s>>>(depth, w, h, intr, fp.sigma0, 0.25 * P.delta, fb.normals, dead);
+            SF_LAUNCH_CHECK();
+            k_edge<<<grd2, blk2, 0, s>>>(depth, w, h, fp.sigma0, fb.edge, dead);
+            SF_LAUNCH_CHECK();
+            n += 2;
+        }
+        k_pixel_meas<<<grd2, blk2, 0, s>>>(depth, sigma, w, h, intr, fp, fb.normals, fb.edge, fb.pix_var, fb.pix_w,
+                                            fb.pix_ok, dead);
+        SF_LAUNCH_CHECK();
+        n += 1;
+    }
+    // Keys -> sorted unique allocate list.
+    const int su = (w + fb.stride - 1) / fb.stride, sv = (h + fb.stride - 1) / fb.stride;
+    const uint32_t sentinel = sentinel_of(P);
+    k_block_keys<<<(su * sv + kThreads - 1) / kThreads, kThreads, 0, s>>>(P, fb.fc, depth, w, h, fb.stride, su, sv,
+                                                                          fb.keys, sentinel, &fb.ctr->skip);
+    SF_LAUNCH_CHECK();
+    size_t tb = fb.cub_temp_bytes;
+    SF_CUDA(cub::DeviceRadixSort::SortKeys(fb.cub_temp, tb, fb.keys, fb.keys_sorted, (int)fb.key_cap, 0, end_bit_of(P), s));
+    tb = fb.cub_temp_bytes;
+    SF_CUDA(cub::DeviceSelect::Unique(fb.cub_temp, tb, fb.keys_sorted, fb.keys_unique, &fb.ctr->n_unique,
+                                      (int)fb.key_cap, s));
+    k_list_len<<<1, 1, 0, s>>>(fb.ctr, fb.keys_unique, sentinel);
+    SF_LAUNCH_CHECK();
+    n += 2 + 4;  // keys + list_len + (sort, unique: >= 4 CUB kernels)
+    const int kb = (fb.key_cap + kThreads - 1) / kThreads;
+    if (!export_only) {
+        k_alloc_flags<<<kb, kThreads, 0, s>>>(fb.ctr, fb.keys_unique, v.d_table, fb.flags, fb.key_cap);
+        SF_LAUNCH_CHECK();
+        tb = fb.cub_temp_bytes;
+        SF_CUDA(cub::DeviceScan::ExclusiveSum(fb.cub_temp, tb, fb.flags, fb.ranks, (int)fb.key_cap, s));
+        k_alloc_assign<<<kb, kThreads, 0, s>>>(fb.ctr, fb.keys_unique, fb.ranks, v.d_table, v.d_free_list,
+                                               v.d_slot_key, v.d_occ, v.d_vc, fb.work, &v.d_vc->high_water);
+        SF_LAUNCH_CHECK();
+        k_alloc_finalize<<<1, 1, 0, s>>>(fb.ctr, fb.flags, fb.ranks, v.d_vc);
+        SF_LAUNCH_CHECK();
+        n += 5;
+    }
+    k_visible<<<kPersistentCtas, kThreads, 0, s>>>(P, fb.fc, fb.ctr, v.d_vc, v.d_slot_key, fb.keys_unique, depth, w, h,
+                                                   fb.work, fb.keys /* reused as export buffer */, export_only ? 1 : 0);
+    SF_LAUNCH_CHECK();
+    n += 1;
+    if (!export_only) {
+        unsigned long long* vu = &fb.ctr->voxels_updated;
+#define SF_INTEGRATE(MODE, FP)                                                                                    \
+    k_integrate<MODE, FP><<<kPersistentCtas, kThreads, 0, s>>>(P, fb.fc, fp, fb.work, fb.ctr, v.d_aux, depth,       \
+                                                               fb.pix_var, fb.pix_w, fb.pix_ok, v.d_payload,        \
+                                                               v.d_fpayload, vu)
+        const bool fpl = v.d_fpayload != nullptr;
+        if (fp.mode == 0) {
+            if (fpl) SF_INTEGRATE(0, true);
+            else SF_INTEGRATE(0, false);
+        } else if (fp.mode == 1) {
+            if (fpl) SF_INTEGRATE(1, true);
+            else SF_INTEGRATE(1, false);
+        } else {
+            if (fpl) SF_INTEGRATE(2, true);
+            else SF_INTEGRATE(2, false);
+        }
+#undef SF_INTEGRATE
+        SF_LAUNCH_CHECK();
+        k_fuse_finalize<<<1, 1, 0, s>>>(fb.ctr, v.d_vc);
+        SF_LAUNCH_CHECK();
+        n += 2;
+    }
+    if (launches) *launches += n;
+}
+
+static void validate_intrinsics(const sf_intrinsics& i) {
+    // Intrinsics::validate (camera.cpp:9-14)
+    if (i.width <= 0 || i.height <= 0) throw Error(SF_INVALID_ARGUMENT, "intrinsics: non-positive image size");
+    if (i.fx <= 0.0 || i.fy <= 0.0) throw Error(SF_INVALID_ARGUMENT, "intrinsics: non-positive focal length");
+    if (!(i.near_plane > 0.0) || !(i.near_plane < i.far_plane))
+        throw Error(SF_INVALID_ARGUMENT, "intrinsics: need 0 < near < far");
+}
+
+// Stage a frame (host or device pointers) into device memory; returns device pointers.
+static void stage_frame(FrameBuffers& fb, const sf_frame& f, cudaStream_t s, const float** d_depth,
+                        const float** d_sigma) {
+    const size_t n = static_cast<size_t>(f.intrinsics.width) * f.intrinsics.height;
+    if (f.on_device) {
+        *d_depth = f.depth;
+        *d_sigma = f.sigma;
+        return;
+    }
+    SF_CUDA(cudaMemcpyAsync(fb.depth, f.depth, n * sizeof(float), cudaMemcpyHostToDevice, s));
+    *d_depth = fb.depth;
+    *d_sigma = nullptr;
+    if (f.sigma) {
+        SF_CUDA(cudaMemcpyAsync(fb.sigma, f.sigma, n * sizeof(float), cudaMemcpyHostToDevice, s));
+        *d_sigma = fb.sigma;
+    }
+}
+
+}  // namespace sf
+
+using namespace sf;
+
+extern "C" {
+
+int sf_integrate(sf_volume_t v, const sf_frame* frame, const double pose[12], const sf_fusion_params* params,
+                 sf_fusion_stats* stats, void* stream) {
+    return guarded([&]() -> int {
+        if (!v || !frame || !pose || !params) throw Error(SF_INVALID_ARGUMENT, "sf_integrate: null argument");
+        SF_CUDA(cudaSetDevice(v->device));
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        validate_intrinsics(frame->intrinsics);
+        const FuseParams fp = resolve_fuse_params(*v, *params, frame->sigma != nullptr);
+        ensure_frame_buffers(*v, v->fb, frame->intrinsics.width, frame->intrinsics.height);
+        FrameBuffers& fb = v->fb;
+        const float *d_depth, *d_sigma;
+        stage_frame(fb, *frame, s, &d_depth, &d_sigma);
+        SF_CUDA(cudaMemcpyAsync(fb.pose, pose, 12 * sizeof(double), cudaMemcpyHostToDevice, s));
+        const Intr intr = to_intr(frame->intrinsics);
+        launch_fuse(*v, fb, intr, d_depth, d_sigma, fp, s, false, nullptr, nullptr);
+        SF_CUDA(cudaMemcpyAsync(fb.h_ctr, fb.ctr, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
+        SF_CUDA(cudaStreamSynchronize(s));
+        const FrameCounters& c = *fb.h_ctr;
+        if (stats) {
+            const uint64_t nn = v->P.N, m = v->P.M;
+            stats->voxels_updated = c.voxels_updated;
+            stats->blocks_allocated_now = c.alloc_now - c.alloc_before;
+            stats->blocks_total = c.alloc_now;
+            stats->memory_bytes = 2ull * c.alloc_now * m * m * m + 4ull * nn * nn * nn;
+        }
+        if (c.exhausted)
+            throw Error(SF_POOL_EXHAUSTED, "grid: payload pool exhausted (" + std::to_string(v->P.capacity) +
+                                               " blocks); increase pool capacity or lower resolution");
+        return SF_OK;
+    });
+}
+
+int sf_select_update_blocks(sf_volume_t v, const sf_frame* frame, const double pose[12], int32_t* allocate_xyz,
+                            uint64_t* allocate_count, int32_t* update_xyz, uint64_t* update_count, void* stream) {
+    return guarded([&]() -> int {
+        SF_CUDA(cudaSetDevice(v->device));
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        validate_intrinsics(frame->intrinsics);
+        ensure_frame_buffers(*v, v->fb, frame->intrinsics.width, frame->intrinsics.height);
+        FrameBuffers& fb = v->fb;
+        const float *d_depth, *d_sigma;
+        stage_frame(fb, *frame, s, &d_depth, &d_sigma);
+        SF_CUDA(cudaMemcpyAsync(fb.pose, pose, 12 * sizeof(double), cudaMemcpyHostToDevice, s));
+        const Intr intr = to_intr(frame->intrinsics);
+        FuseParams fp{};
+        launch_fuse(*v, fb, intr, d_depth, d_sigma, fp, s, true, nullptr, nullptr);
+        SF_CUDA(cudaMemcpyAsync(fb.h_ctr, fb.ctr, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
+        SF_CUDA(cudaStreamSynchronize(s));
+        const FrameCounters c = *fb.h_ctr;
+        if (c.n_list > *allocate_count || c.n_update > *update_count)
+            throw Error(SF_OUT_OF_RANGE, "select_update_blocks: output capacity");
+        std::vector<uint32_t> a(c.n_list), u(c.n_update);
+        if (c.n_list) SF_CUDA(cudaMemcpy(a.data(), fb.keys_unique, a.size() * 4, cudaMemcpyDeviceToHost));
+        if (c.n_update) SF_CUDA(cudaMemcpy(u.data(), fb.keys, u.size() * 4, cudaMemcpyDeviceToHost));
+        std::sort(u.begin(), u.end());  // occupied_blocks_in_frustum walks the table in order
+        const uint32_t N = v->P.N;
+        auto put = [&](uint32_t key, int32_t* out) {
+            out[0] = key % N;
+            out[1] = (key / N) % N;
+            out[2] = key / (N * N);
+        };
+        for (size_t i = 0; i < a.size(); ++i) put(a[i], allocate_xyz + 3 * i);
+        for (size_t i = 0; i < u.size(); ++i) put(u[i], update_xyz + 3 * i);
+        *allocate_count = a.size();
+        *update_count = u.size();
+        return SF_OK;
+    });
+}
+
+int sf_compute_normals(const sf_frame* frame, double sigma0, double spatial_scale, float* normals_xyz,
+                       int32_t out_on_device, void* stream) {
+    return guarded([&]() -> int {
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        validate_intrinsics(frame->intrinsics);
+        const int w = frame->intrinsics.width, h = frame->intrinsics.height;
+        const size_t n = static_cast<size_t>(w) * h;
+        float* d_depth = nullptr;
+        float* d_out = nullptr;
+        const float* src = frame->depth;
+        if (!frame->on_device) {
+            SF_CUDA(cudaMallocAsync(&d_depth, n * sizeof(float), s));
+            SF_CUDA(cudaMemcpyAsync(d_depth, frame->depth, n * sizeof(float), cudaMemcpyHostToDevice, s));
+            src = d_depth;
+        }
+        float* dst = normals_xyz;
+        if (!out_on_device) {
+            SF_CUDA(cudaMallocAsync(&d_out, 3 * n * sizeof(float), s));
+            dst = d_out;
+        }
+        launch_compute_normals(src, w, h, to_intr(frame->intrinsics), sigma0, spatial_scale, dst, s, nullptr,
+                               nullptr);
+        if (!out_on_device)
+            SF_CUDA(cudaMemcpyAsync(normals_xyz, d_out, 3 * n * sizeof(float), cudaMemcpyDeviceToHost, s));
+        if (d_depth) SF_CUDA(cudaFreeAsync(d_depth, s));
+        if (d_out) SF_CUDA(cudaFreeAsync(d_out, s));
+        SF_CUDA(cudaStreamSynchronize(s));
+        return SF_OK;
+    });
+}
+
+}  // extern "C"

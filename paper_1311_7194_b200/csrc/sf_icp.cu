@@ -1,0 +1,366 @@
+// sf_icp.cu — projective point-to-plane ICP on the device (registration.cpp:17-224).
+//
+// Every iteration is four launches with device-side control (no host round trip):
+//   k_icp_match     per source pixel: projective association + distance / normal
+//                   rejection (registration.cpp:17-50); match record to HBM; per-CTA
+//                   bbox (min/max of p and q) and count                    [deterministic]
+//   k_icp_bbox      1 CTA: bbox -> shrink centre / scale (registration.cpp:52-74);
+//                   < 10 matches -> TrackingLost (registration.cpp:202-204)
+//   k_icp_assemble  per match: shrunk row (c_hat, n), d; 21 + 6 + 1 compensated sums
+//                   (double-double TwoSum accumulators), warp-shuffle -> CTA partials
+//                   (registration.cpp:76-123)
+//   k_icp_solve     1 CTA: fixed-order merge of the partials, Jacobi 6x6, gated solve,
+//                   unshrink, apply_motion, convergence test (registration.cpp:125-220)
+// A converged / failed state makes the remaining iterations' kernels exit at once, so the
+// whole ICP (max_iterations x 4 launches) is a fixed launch sequence: CUDA-graph friendly.
+//
+// Parity: the association and every per-match quantity are FP64 in the reference order.
+// The only deviation is the summation order of the 28 sums (tree instead of sequential
+// Kahan); both are within ~1 ulp of the exact sum, pose parity is asserted at 1e-6.
+#include <algorithm>
+#include <cmath>
+#include <string>
+
+#include "sf_icp.cuh"
+#include "sf_linalg.cuh"
+
+namespace sf {
+
+__global__ void k_icp_init(IcpState* st, const double* __restrict__ initial12, const int* dead) {
+    IcpState z;
+    memset(&z, 0, sizeof(z));
+    z.delta = pose_from12(initial12);
+    z.done = (dead && *dead) ? 1 : 0;
+    *st = z;
+}
+
+// match_points (registration.cpp:17-50) + bbox partials of shrink (registration.cpp:54-59)
+__global__ void __launch_bounds__(kIcpThreads)
+    k_icp_match(const float* __restrict__ src, const float* __restrict__ src_n, const float* __restrict__ tgt,
+                const float* __restrict__ tgt_n, Intr si, Intr ti, IcpParamsDev prm, IcpState* st,
+                MatchRec* __restrict__ rec, uint8_t* __restrict__ flag, double* __restrict__ part_bbox,
+                unsigned long long* __restrict__ part_count) {
+    if (st->done) return;
+    const Pose delta = st->delta;
+    const int w = si.w, h = si.h;
+    const int n = w * h;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    unsigned long long cnt = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int u = i % w, v = i / w;
+        uint8_t ok = 0;
+        const float sd = src[i];
+        const float snx = src_n[3 * i], sny = src_n[3 * i + 1], snz = src_n[3 * i + 2];
+        if (sd > 0.0f && (snx * snx + sny * sny) + snz * snz > 0.0f) {
+            const d3 p = apply(delta, unproject(si, u, v, sd));
+            double pu, pv;
+            if (project(ti, p, pu, pv)) {
+                const int tu = ref_lround_int(pu), tv = ref_lround_int(pv);
+                if (tu >= 0 && tv >= 0 && tu < ti.w && tv < ti.h) {
+                    const int j = tv * ti.w + tu;
+                    const float td = tgt[j];
+                    const float tnx = tgt_n[3 * j], tny = tgt_n[3 * j + 1], tnz = tgt_n[3 * j + 2];
+                    if (td > 0.0f && (tnx * tnx + tny * tny) + tnz * tnz > 0.0f) {
+                        const d3 q = unproject(ti, tu, tv, td);
+                        if (!(sqnorm(sub(p, q)) > prm.max_dist_sq)) {
+                            const d3 nn = mk(tnx, tny, tnz);
+                            const d3 ns = mv(delta.R, mk(snx, sny, snz));
+                            if (!(dot(ns, nn) < prm.cos_max)) {
+                                ok = 1;
+                                MatchRec r;
+                                r.p[0] = p.x;
+                                r.p[1] = p.y;
+                                r.p[2] = p.z;
+                                r.q[0] = q.x;
+                                r.q[1] = q.y;
+                                r.q[2] = q.z;
+                                r.n[0] = nn.x;
+                                r.n[1] = nn.y;
+                                r.n[2] = nn.z;
+                                rec[i] = r;
+                                const double pp[3] = {p.x, p.y, p.z}, qq[3] = {q.x, q.y, q.z};
+                                for (int a = 0; a < 3; ++a) {
+                                    lo[a] = dmin(dmin(lo[a], pp[a]), qq[a]);
+                                    hi[a] = dmax(dmax(hi[a], pp[a]), qq[a]);
+                                }
+                                ++cnt;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        flag[i] = ok;
+    }
+    // CTA reduction (min/max are exact: order-free)
+    for (int off = 16; off > 0; off >>= 1) {
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = dmin(lo[a], __shfl_down_sync(0xffffffffu, lo[a], off));
+            hi[a] = dmax(hi[a], __shfl_down_sync(0xffffffffu, hi[a], off));
+        }
+        cnt += __shfl_down_sync(0xffffffffu, cnt, off);
+    }
+    __shared__ double s_b[kIcpThreads / 32][6];
+    __shared__ unsigned long long s_c[kIcpThreads / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        for (int a = 0; a < 3; ++a) {
+            s_b[wid][a] = lo[a];
+            s_b[wid][3 + a] = hi[a];
+        }
+        s_c[wid] = cnt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < kIcpThreads / 32; ++k) {
+            for (int a = 0; a < 3; ++a) {
+                s_b[0][a] = dmin(s_b[0][a], s_b[k][a]);
+                s_b[0][3 + a] = dmax(s_b[0][3 + a], s_b[k][3 + a]);
+            }
+            s_c[0] += s_c[k];
+        }
+        for (int a = 0; a < 6; ++a) part_bbox[blockIdx.x * 6 + a] = s_b[0][a];
+        part_count[blockIdx.x] = s_c[0];
+    }
+}
+
+// shrink's centre / scale (registration.cpp:54-64) from the bbox partials.
+__global__ void k_icp_bbox(IcpState* st, const double* __restrict__ part_bbox,
+                           const unsigned long long* __restrict__ part_count, int nparts, IcpParamsDev prm) {
+    if (st->done) return;
+    if (threadIdx.x != 0) return;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    unsigned long long cnt = 0;
+    for (int b = 0; b < nparts; ++b) {
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = dmin(lo[a], part_bbox[b * 6 + a]);
+            hi[a] = dmax(hi[a], part_bbox[b * 6 + 3 + a]);
+        }
+        cnt += part_count[b];
+    }
+    if (cnt < 10) {
+        st->lost = 1;
+        st->lost_count = cnt;
+        st->done = 1;
+        return;
+    }
+    st->matches = cnt;
+    st->cur_count = cnt;
+    const d3 l = mk(lo[0], lo[1], lo[2]), hh = mk(hi[0], hi[1], hi[2]);
+    const d3 c = scale(0.5, add(l, hh));
+    const d3 ext = sub(hh, l);
+    const d3 s = mk(dmax(ext.x, prm.floor), dmax(ext.y, prm.floor), dmax(ext.z, prm.floor));  // cwiseMax(floor)
+    st->center = c;
+    st->scale = s;
+    st->inv_scale = mk(1.0 / s.x, 1.0 / s.y, 1.0 / s.z);
+}
+
+// assemble (registration.cpp:93-123) on the shrunk matches (registration.cpp:65-72).
+__global__ void __launch_bounds__(kIcpThreads)
+    k_icp_assemble(const IcpState* __restrict__ st, const MatchRec* __restrict__ rec, const uint8_t* __restrict__ flag,
+                   int n, DD* __restrict__ part) {
+    if (st->done) return;
+    const d3 c = st->center, inv = st->inv_scale, scl = st->scale;
+    DD acc[kSums];
+#pragma unroll
+    for (int k = 0; k < kSums; ++k) acc[k] = DD{0.0, 0.0};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        if (!flag[i]) continue;
+        const MatchRec r = rec[i];
+        const d3 p = mk(r.p[0], r.p[1], r.p[2]), q = mk(r.q[0], r.q[1], r.q[2]), nn = mk(r.n[0], r.n[1], r.n[2]);
+        const d3 p_hat = cmul(inv, sub(p, c));
+        const d3 q_hat = cmul(inv, sub(q, c));
+        const d3 c_hat = cmul(inv, sub(cross(p, nn), cross(c, nn)));
+        const double row[6] = {c_hat.x, c_hat.y, c_hat.z, nn.x, nn.y, nn.z};
+        const double d = dot(cmul(scl, sub(p_hat, q_hat)), nn);
+        int k = 0;
+#pragma unroll
+        for (int a = 0; a < 6; ++a)
+#pragma unroll
+            for (int b = a; b < 6; ++b, ++k) dd_add(acc[k], row[a] * row[b]);
+#pragma unroll
+        for (int a = 0; a < 6; ++a) dd_add(acc[21 + a], -row[a] * d);
+        dd_add(acc[27], d * d);
+    }
+    // warp tree
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+        for (int k = 0; k < kSums; ++k) {
+            DD o;
+            o.hi = __shfl_down_sync(0xffffffffu, acc[k].hi, off);
+            o.lo = __shfl_down_sync(0xffffffffu, acc[k].lo, off);
+            dd_merge(acc[k], o);
+        }
+    }
+    __shared__ DD s_acc[kIcpThreads / 32][kSums];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0)
+        for (int k = 0; k < kSums; ++k) s_acc[wid][k] = acc[k];
+    __syncthreads();
+    if (threadIdx.x < kSums) {
+        DD a = s_acc[0][threadIdx.x];
+        for (int w = 1; w < kIcpThreads / 32; ++w) dd_merge(a, s_acc[w][threadIdx.x]);
+        part[blockIdx.x * kSums + threadIdx.x] = a;
+    }
+}
+
+// solve_gated + apply_motion + convergence (registration.cpp:175-212)
+__global__ void k_icp_solve(IcpState* st, const DD* __restrict__ part, int nparts, IcpParamsDev prm, int iter) {
+    if (st->done) return;
+    __shared__ double s_sum[kSums];
+    if (threadIdx.x < kSums) {
+        DD a = part[threadIdx.x];
+        for (int b = 1; b < nparts; ++b) dd_merge(a, part[b * kSums + threadIdx.x]);
+        s_sum[threadIdx.x] = a.hi + a.lo;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    double A[36];
+    int k = 0;
+    for (int i = 0; i < 6; ++i)
+        for (int j = i; j < 6; ++j, ++k) {
+            A[i * 6 + j] = s_sum[k];
+            A[j * 6 + i] = s_sum[k];
+        }
+    double b[6];
+    for (int i = 0; i < 6; ++i) b[i] = s_sum[21 + i];
+    const double res_sq = s_sum[27];
+    const unsigned long long cnt = st->cur_count;
+    const double n_pairs = static_cast<double>(cnt);
+    st->pair_count = cnt;
+    st->residual_rms = sqrt(dmax(0.0, res_sq) / n_pairs);
+    Eig6 e;
+    eigendecompose_sym6(A, e);
+    double x[6] = {0, 0, 0, 0, 0, 0};
+    for (int i = 0; i < 6; ++i) {
+        st->eigenvalues[i] = e.values[i];
+        const bool keep = e.values[i] / n_pairs > prm.theta;
+        st->gated[i] = keep ? 1 : 0;
+        if (!keep) continue;
+        const double* vcol = e.vectors + i * 6;
+        double vb = vcol[0] * b[0];
+        for (int r = 1; r < 6; ++r) vb = vb + vcol[r] * b[r];
+        const double sc = vb / e.values[i];
+        for (int r = 0; r < 6; ++r) x[r] = x[r] + vcol[r] * sc;
+    }
+    for (int i = 0; i < 36; ++i) st->eigenvectors[i] = e.vectors[i];
+    double xn = x[0] * x[0];
+    for (int r = 1; r < 6; ++r) xn = xn + x[r] * x[r];
+    st->shrunk_norm = sqrt(xn);
+    // unshrink_motion (registration.cpp:167-173)
+    const d3 s = st->scale, c = st->center;
+    const d3 r = mk((1.0 / s.x) * x[0], (1.0 / s.y) * x[1], (1.0 / s.z) * x[2]);
+    const d3 t = sub(mk(x[3], x[4], x[5]), cross(r, c));
+    st->motion_r = r;
+    st->motion_t = t;
+    st->delta = apply_motion(st->delta, r, t);
+    st->iterations = iter + 1;
+    if (st->shrunk_norm < prm.eps) st->done = 1;
+}
+
+IcpParamsDev make_icp_params(const sf_match_params& p) {
+    IcpParamsDev d;
+    d.cos_max = std::cos(p.max_normal_angle);          // registration.cpp:25
+    d.max_dist_sq = p.max_distance * p.max_distance;   // registration.cpp:26
+    d.eps = p.convergence_epsilon;
+    d.theta = p.eigen_threshold;
+    d.floor = p.shrink_floor;
+    d.max_iterations = p.max_iterations;
+    return d;
+}
+
+// Launch the whole ICP: init + max_iterations x (match, bbox, assemble, solve).
+void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* tgt, const float* tgt_n,
+                const Intr& si, const Intr& ti, const double* d_initial, const IcpParamsDev& prm, cudaStream_t s,
+                uint64_t* launches, const int* dead) {
+    const int n = si.w * si.h;
+    k_icp_init<<<1, 1, 0, s>>>(wk.st, d_initial, dead);
+    SF_LAUNCH_CHECK();
+    uint64_t cnt = 1;
+    for (int it = 0; it < prm.max_iterations; ++it) {
+        k_icp_match<<<kIcpCtas, kIcpThreads, 0, s>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st, wk.rec, wk.flag,
+                                                     wk.part_bbox, wk.part_count);
+        k_icp_bbox<<<1, 32, 0, s>>>(wk.st, wk.part_bbox, wk.part_count, kIcpCtas, prm);
+        k_icp_assemble<<<kIcpCtas, kIcpThreads, 0, s>>>(wk.st, wk.rec, wk.flag, n, wk.part);
+        k_icp_solve<<<1, 32, 0, s>>>(wk.st, wk.part, kIcpCtas, prm, it);
+        SF_LAUNCH_CHECK();
+        cnt += 4;
+    }
+    if (launches) *launches += cnt;
+}
+
+void fill_icp_result(const IcpState& st, sf_icp_result* out) {
+    memset(out, 0, sizeof(*out));
+    pose_to12(st.delta, out->delta);
+    out->iterations = st.iterations;
+    out->matches = st.matches;
+    out->motion_r[0] = st.motion_r.x;
+    out->motion_r[1] = st.motion_r.y;
+    out->motion_r[2] = st.motion_r.z;
+    out->motion_t[0] = st.motion_t.x;
+    out->motion_t[1] = st.motion_t.y;
+    out->motion_t[2] = st.motion_t.z;
+    for (int i = 0; i < 6; ++i) {
+        out->eigenvalues[i] = st.eigenvalues[i];
+        out->gated_mask[i] = st.gated[i];
+    }
+    for (int i = 0; i < 36; ++i) out->eigenvectors[i] = st.eigenvectors[i];
+    out->residual_rms = st.residual_rms;
+    out->shrunk_motion_norm = st.shrunk_norm;
+    out->pair_count = st.pair_count;
+}
+
+}  // namespace sf
+
+using namespace sf;
+
+extern "C" int sf_icp(const sf_frame* source, const float* source_normals, const sf_frame* target,
+                      const float* target_normals, const double initial[12], const sf_match_params* params,
+                      sf_icp_result* result, void* stream) {
+    return guarded([&]() -> int {
+        if (!source || !target || !target_normals || !initial || !params || !result)
+            throw Error(SF_INVALID_ARGUMENT, "sf_icp: null argument");
+        const sf_intrinsics& si = source->intrinsics;
+        const sf_intrinsics& ti = target->intrinsics;
+        if (si.width != ti.width || si.height != ti.height)
+            throw Error(SF_INVALID_ARGUMENT, "match: frames must share intrinsics");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        static thread_local IcpWork wk;
+        wk.ensure(si.width, si.height);
+        const size_t n = static_cast<size_t>(si.width) * si.height;
+        const float *d_src = source->depth, *d_tgt = target->depth, *d_tn = target_normals,
+                    *d_sn = source_normals;
+        if (!source->on_device) {
+            SF_CUDA(cudaMemcpyAsync(wk.src, source->depth, n * sizeof(float), cudaMemcpyHostToDevice, s));
+            d_src = wk.src;
+            if (source_normals) {
+                SF_CUDA(cudaMemcpyAsync(wk.src_n_in, source_normals, 3 * n * sizeof(float), cudaMemcpyHostToDevice, s));
+                d_sn = wk.src_n_in;
+            }
+        }
+        if (!target->on_device) {
+            SF_CUDA(cudaMemcpyAsync(wk.tgt, target->depth, n * sizeof(float), cudaMemcpyHostToDevice, s));
+            SF_CUDA(cudaMemcpyAsync(wk.tgt_n, target_normals, 3 * n * sizeof(float), cudaMemcpyHostToDevice, s));
+            d_tgt = wk.tgt;
+            d_tn = wk.tgt_n;
+        }
+        const Intr SI = to_intr(si), TI = to_intr(ti);
+        if (!d_sn) {  // compute_normals(source, params.normal_options) (registration.cpp:218)
+            launch_compute_normals(d_src, si.width, si.height, SI, params->normal_sigma0, params->normal_spatial_scale,
+                                   wk.src_normals, s, nullptr, nullptr);
+            d_sn = wk.src_normals;
+        }
+        SF_CUDA(cudaMemcpyAsync(wk.initial, initial, 12 * sizeof(double), cudaMemcpyHostToDevice, s));
+        const IcpParamsDev prm = make_icp_params(*params);
+        launch_icp(wk, d_src, d_sn, d_tgt, d_tn, SI, TI, wk.initial, prm, s, nullptr, nullptr);
+        IcpState hs;
+        SF_CUDA(cudaMemcpyAsync(&hs, wk.st, sizeof(hs), cudaMemcpyDeviceToHost, s));
+        SF_CUDA(cudaStreamSynchronize(s));
+        if (hs.lost)
+            throw Error(SF_TRACKING_LOST, "icp: only " + std::to_string(hs.lost_count) + " correspondences");
+        fill_icp_result(hs, result);
+        if (prm.max_iterations <= 0) pose_to12(pose_from12(initial), result->delta);
+        return SF_OK;
+    });
+}

@@ -1,0 +1,112 @@
+// sf_icp.cuh — ICP device state shared by sf_icp.cu and the tracker.
+#pragma once
+
+#include "sf_internal.h"
+
+namespace sf {
+
+constexpr int kIcpThreads = 256;
+constexpr int kIcpCtas = 296;  // 2 per SM; fixed => deterministic reduction tree
+constexpr int kSums = 28;      // 21 upper(A) + 6 b + 1 residual
+
+struct DD {
+    double hi, lo;
+};
+__device__ __forceinline__ void dd_add(DD& a, double x) {
+    const double s = a.hi + x;
+    const double bb = s - a.hi;
+    const double e = (a.hi - (s - bb)) + (x - bb);
+    a.hi = s;
+    a.lo += e;
+}
+__device__ __forceinline__ void dd_merge(DD& a, const DD& b) {
+    const double s = a.hi + b.hi;
+    const double bb = s - a.hi;
+    const double e = (a.hi - (s - bb)) + (b.hi - bb);
+    a.hi = s;
+    a.lo = (a.lo + b.lo) + e;
+}
+
+struct IcpState {
+    Pose delta;
+    int done;       // converged or failed: later iterations are no-ops
+    int lost;       // TrackingLost raised
+    int iterations;
+    int pad;
+    unsigned long long matches;       // matches of the last completed iteration
+    unsigned long long lost_count;    // match count that triggered TrackingLost
+    d3 center, scale, inv_scale;      // shrink of the current iteration
+    unsigned long long cur_count;
+    // GatedSolution of the last iteration
+    double eigenvalues[6];
+    double eigenvectors[36];
+    int gated[6];
+    double residual_rms, shrunk_norm;
+    unsigned long long pair_count;
+    d3 motion_r, motion_t;
+};
+
+struct IcpParamsDev {
+    double max_dist_sq, cos_max, eps, theta, floor;
+    int max_iterations;
+};
+
+struct MatchRec {
+    double p[3], q[3], n[3];
+};
+
+// Scratch for one ICP (owned by the caller: stand-alone API or tracker).
+struct IcpWork {
+    int w = 0, h = 0;
+    MatchRec* rec = nullptr;
+    uint8_t* flag = nullptr;
+    double* part_bbox = nullptr;
+    unsigned long long* part_count = nullptr;
+    DD* part = nullptr;
+    IcpState* st = nullptr;
+    float* src_normals = nullptr;
+    float *src = nullptr, *tgt = nullptr, *tgt_n = nullptr, *src_n_in = nullptr;
+    double* initial = nullptr;
+    void ensure(int W, int H) {
+        if (W == w && H == h && rec) return;
+        release();
+        const size_t n = static_cast<size_t>(W) * H;
+        SF_CUDA(cudaMalloc(&rec, n * sizeof(MatchRec)));
+        SF_CUDA(cudaMalloc(&flag, n));
+        SF_CUDA(cudaMalloc(&part_bbox, kIcpCtas * 6 * sizeof(double)));
+        SF_CUDA(cudaMalloc(&part_count, kIcpCtas * sizeof(unsigned long long)));
+        SF_CUDA(cudaMalloc(&part, kIcpCtas * kSums * sizeof(DD)));
+        SF_CUDA(cudaMalloc(&st, sizeof(IcpState)));
+        SF_CUDA(cudaMalloc(&src_normals, 3 * n * sizeof(float)));
+        SF_CUDA(cudaMalloc(&src, n * sizeof(float)));
+        SF_CUDA(cudaMalloc(&tgt, n * sizeof(float)));
+        SF_CUDA(cudaMalloc(&tgt_n, 3 * n * sizeof(float)));
+        SF_CUDA(cudaMalloc(&src_n_in, 3 * n * sizeof(float)));
+        SF_CUDA(cudaMalloc(&initial, 12 * sizeof(double)));
+        w = W;
+        h = H;
+    }
+    void release() {
+        void* p[] = {rec, flag, part_bbox, part_count, part, st, src_normals, src, tgt, tgt_n, src_n_in, initial};
+        for (void* q : p)
+            if (q) cudaFree(q);
+        rec = nullptr;
+        flag = nullptr;
+        part_bbox = nullptr;
+        part_count = nullptr;
+        part = nullptr;
+        st = nullptr;
+        src_normals = src = tgt = tgt_n = src_n_in = nullptr;
+        initial = nullptr;
+        w = h = 0;
+    }
+    ~IcpWork() { release(); }
+};
+
+IcpParamsDev make_icp_params(const sf_match_params& p);
+void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* tgt, const float* tgt_n,
+                const Intr& si, const Intr& ti, const double* d_initial, const IcpParamsDev& prm, cudaStream_t s,
+                uint64_t* launches, const int* dead);
+void fill_icp_result(const IcpState& st, sf_icp_result* out);
+
+}  // namespace sf

@@ -1,0 +1,158 @@
+// sf_internal.h — host-side internals shared by the translation units of libsf_gpu.so.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "../../include/sf_gpu.h"
+#include "sf_common.cuh"
+
+namespace sf {
+
+// ---- error plumbing: C++ exceptions inside, sf_status at the C boundary -------------
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+void set_last_error(const std::string& msg);
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what, const char* file, int line);
+
+#define SF_CUDA(call)                                                       \
+    do {                                                                    \
+        cudaError_t sf_e_ = (call);                                         \
+        if (sf_e_ != cudaSuccess) ::sf::throw_cuda(sf_e_, #call, __FILE__, __LINE__); \
+    } while (0)
+#define SF_LAUNCH_CHECK() SF_CUDA(cudaGetLastError())
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        set_last_error("");
+        return f();
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_last_error("host allocation failed");
+        return SF_CUDA_ERROR;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return SF_CUDA_ERROR;
+    }
+}
+
+// ---- device counters of a volume --------------------------------------------------
+struct VolCounters {
+    unsigned long long allocated_count;
+    unsigned long long free_top;    // size of the free-list stack
+    unsigned long long high_water;  // 1 + highest slot ever handed out
+    unsigned long long pad;
+};
+
+// Per-frame device counters (zeroed by the frame-setup kernel).
+struct FrameCounters {
+    uint32_t n_unique;   // CUB unique output count (may include the sentinel)
+    uint32_t n_list;     // allocate-list length (valid unique keys)
+    uint32_t n_new;      // keys needing a fresh slot
+    uint32_t limit;      // processed allocate-list prefix
+    uint32_t n_update;   // update-list length
+    uint32_t exhausted;  // PoolExhausted raised this frame
+    uint32_t skip;       // whole fuse skipped (tracker dead / tracking lost)
+    uint32_t pad;
+    unsigned long long voxels_updated;
+    unsigned long long alloc_before;
+    unsigned long long alloc_now;
+};
+
+// Device-side aux codec tables (host-computed with the reference's libm).
+struct AuxTables {
+    double tsdf_decode[256];  // dequantize_tsdf(code)        (grid.cpp:25-27), index code+128
+    double aux_decode[256];   // AuxQuantization::decode(code) (grid.cpp:48-51)
+    double aux_thresh[256];   // variance mode: thresh[k] = min v with encode(v) >= k, k = 1..255
+};
+void build_aux_tables(const VolParams& P, AuxTables* t);
+uint8_t host_aux_encode(const VolParams& P, double value);  // reference encode (grid.cpp:38-46)
+
+// ---- frame-sized scratch, owned by a volume or a tracker ----------------------------
+struct FrameBuffers {
+    int w = 0, h = 0, stride = 0;
+    int device = 0;
+    float* depth = nullptr;    // staged depth for host frames
+    float* sigma = nullptr;    // staged sigma plane
+    float* normals = nullptr;  // 3*w*h fusion normals
+    uint8_t* edge = nullptr;   // w*h
+    double* pix_var = nullptr; // w*h per-pixel p_k
+    double* pix_w = nullptr;   // w*h per-pixel w_k
+    uint8_t* pix_ok = nullptr; // w*h valid && quality >= 0.2
+    uint32_t key_cap = 0;
+    uint32_t* keys = nullptr;
+    uint32_t* keys_sorted = nullptr;
+    uint32_t* keys_unique = nullptr;
+    uint32_t* flags = nullptr;
+    uint32_t* ranks = nullptr;
+    void* cub_temp = nullptr;
+    size_t cub_temp_bytes = 0;
+    int2* work = nullptr;  // {slot | fresh<<31, table index}
+    uint64_t work_cap = 0;
+    FrameCounters* ctr = nullptr;
+    FrameConsts* fc = nullptr;
+    double* pose = nullptr;  // 12 doubles
+    FrameCounters* h_ctr = nullptr;  // pinned mirror
+    void release();
+    ~FrameBuffers() { release(); }
+};
+
+
+}  // namespace sf
+
+// ---- the opaque volume -------------------------------------------------------------
+struct sf_volume {
+    int device = 0;
+    sf_grid_config cfg{};
+    sf_aux_quant aux{};
+    sf::VolParams P{};
+    int32_t* d_table = nullptr;      // N^3
+    uint16_t* d_payload = nullptr;   // capacity * M^3
+    float2* d_fpayload = nullptr;    // optional float payload {tsdf, aux}
+    int32_t* d_free_list = nullptr;  // capacity (stack, bottom..top)
+    int32_t* d_slot_key = nullptr;   // capacity: table index of the block in each slot, -1 free
+    uint32_t* d_occ = nullptr;       // occupancy bitmap, N^3 bits
+    sf::VolCounters* d_vc = nullptr;
+    sf::AuxTables* d_aux = nullptr;
+    sf::AuxTables h_aux{};
+    sf::FrameBuffers fb;  // scratch for the stand-alone API calls
+    unsigned long long host_allocated() const;
+};
+
+namespace sf {
+using Volume = ::sf_volume;
+void ensure_frame_buffers(Volume& v, FrameBuffers& fb, int w, int h);
+
+// Launchers shared between the stand-alone API (sf_integrate, sf_raycast, sf_icp) and the
+// tracker. All are asynchronous on `stream`; `dead_flag` (device int, may be NULL) turns
+// the launched kernels into no-ops when set (tracker after TrackingLost / PoolExhausted).
+struct RayCounters {
+    unsigned long long sample_steps, hit_pixels, rays_with_bounds, pad;
+};
+void launch_consts(const VolParams& P, const Intr& intr, const double* d_pose, FrameConsts* d_fc, cudaStream_t s,
+                   uint64_t* launches);
+// fuse_frame at the pose in fb.pose (device)
+void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* depth, const float* sigma,
+                 const FuseParams& fp, cudaStream_t s, bool export_lists_only, uint64_t* launches,
+                 const int* dead_flag);
+void launch_ray_bounds(Volume& v, const FrameConsts* d_fc, const Intr& intr, float* t_start, float* t_end,
+                       cudaStream_t s, uint64_t* launches, const int* dead_flag);
+void launch_raycast(Volume& v, const FrameConsts* d_fc, const Intr& intr, const float* t_start, const float* t_end,
+                    float* depth, float* normals, RayCounters* d_stats, cudaStream_t s, uint64_t* launches,
+                    const int* dead_flag);
+void launch_compute_normals(const float* depth, int w, int h, const Intr& intr, double sigma0,
+                            double spatial_scale, float* normals, cudaStream_t s, uint64_t* launches,
+                            const int* dead_flag);
+Intr to_intr(const sf_intrinsics& i);
+FuseParams resolve_fuse_params(const Volume& v, const sf_fusion_params& p, bool has_sigma);
+
+}  // namespace sf

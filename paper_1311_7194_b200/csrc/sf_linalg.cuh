@@ -1,0 +1,277 @@
+// sf_linalg.cuh — small dense linear algebra of the ICP solve, host/device.
+//
+//   eigendecompose_sym6   cyclic Jacobi (registration.cpp:125-165). The reference forms
+//                         the full plane rotation and evaluates m = rot^T * m * rot and
+//                         v = v * rot as dense 6x6 products; the products only touch rows
+//                         /columns p and q (the other terms are exact zeros), so the
+//                         updates below are the same values in the same summation order.
+//   solve_gated           eigen-gated spectral solve + unshrink (registration.cpp:167-193)
+//   nearest_rotation      polar factor U V^T via two-sided Jacobi SVD with 2x2 real
+//                         Jacobi steps, descending singular values (pose.cpp:20-29; the
+//                         SVD algorithm is Eigen's JacobiSVD as restated in
+//                         oracle/shim/Eigen/Dense)
+//   apply_motion          small-angle rotation -> nearest rotation -> compose (pose.cpp:31-43)
+#pragma once
+
+#include "sf_common.cuh"
+
+namespace sf {
+
+// Row-major 6x6 helpers (the reference's Matrix<double,6,6> is column-major; only the
+// summation order matters and it is reproduced explicitly below).
+struct Eig6 {
+    double values[6];   // ascending
+    double vectors[36]; // column-major: vectors[c*6 + r]
+};
+
+SF_HD void eigendecompose_sym6(const double* a /* row-major 6x6 */, Eig6& out) {
+    double m[6][6], v[6][6];
+    for (int i = 0; i < 6; ++i)
+        for (int j = 0; j < 6; ++j) {
+            m[i][j] = 0.5 * (a[i * 6 + j] + a[j * 6 + i]);
+            v[i][j] = i == j ? 1.0 : 0.0;
+        }
+    // m.norm(): column-major left-to-right sum of squares
+    double sq = m[0][0] * m[0][0];
+    for (int c = 0; c < 6; ++c)
+        for (int r = 0; r < 6; ++r) {
+            if (c == 0 && r == 0) continue;
+            sq = sq + m[r][c] * m[r][c];
+        }
+    const double nrm = sqrt(sq);
+    const double scl = (1.0 < nrm) ? nrm : 1.0;  // std::max(1.0, m.norm())
+    const double tol = 1e-12 * scl;
+    for (int sweep = 0; sweep < 64; ++sweep) {
+        double off = 0.0;
+        for (int p = 0; p < 6; ++p)
+            for (int q = p + 1; q < 6; ++q) off += m[p][q] * m[p][q];
+        if (sqrt(off) <= tol) break;
+        for (int p = 0; p < 6; ++p) {
+            for (int q = p + 1; q < 6; ++q) {
+                const double apq = m[p][q];
+                if (fabs(apq) <= tol / 30.0) continue;
+                const double theta = (m[q][q] - m[p][p]) / (2.0 * apq);
+                const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                const double c = 1.0 / sqrt(t * t + 1.0);
+                const double s = t * c;
+                // m1 = rot^T * m: rows p, q
+                for (int j = 0; j < 6; ++j) {
+                    const double mp = m[p][j], mq = m[q][j];
+                    m[p][j] = c * mp + (-s) * mq;
+                    m[q][j] = s * mp + c * mq;
+                }
+                // m = m1 * rot: columns p, q
+                for (int i = 0; i < 6; ++i) {
+                    const double mp = m[i][p], mq = m[i][q];
+                    m[i][p] = mp * c + mq * (-s);
+                    m[i][q] = mp * s + mq * c;
+                }
+                // v = v * rot
+                for (int i = 0; i < 6; ++i) {
+                    const double vp = v[i][p], vq = v[i][q];
+                    v[i][p] = vp * c + vq * (-s);
+                    v[i][q] = vp * s + vq * c;
+                }
+            }
+        }
+    }
+    // std::sort by diagonal (libstdc++ insertion sort for n <= 16: stable)
+    int order[6] = {0, 1, 2, 3, 4, 5};
+    for (int i = 1; i < 6; ++i) {
+        const int val = order[i];
+        int j = i;
+        while (j > 0 && m[val][val] < m[order[j - 1]][order[j - 1]]) {
+            order[j] = order[j - 1];
+            --j;
+        }
+        order[j] = val;
+    }
+    for (int i = 0; i < 6; ++i) {
+        out.values[i] = m[order[i]][order[i]];
+        for (int r = 0; r < 6; ++r) out.vectors[i * 6 + r] = v[r][order[i]];
+    }
+}
+
+// ---- 3x3 Jacobi SVD (Eigen JacobiSVD restated) ------------------------------------
+struct Rot2 {
+    double c, s;
+};
+SF_HD Rot2 rot_mul(Rot2 a, Rot2 b) { return Rot2{a.c * b.c - a.s * b.s, a.c * b.s + a.s * b.c}; }
+SF_HD Rot2 rot_t(Rot2 a) { return Rot2{a.c, -a.s}; }
+
+SF_HD void make_jacobi(double x, double y, double z, Rot2& j) {
+    const double deno = 2.0 * fabs(y);
+    if (deno < 2.2250738585072014e-308) {
+        j.c = 1.0;
+        j.s = 0.0;
+        return;
+    }
+    const double tau = (x - z) / deno;
+    const double w = sqrt(tau * tau + 1.0);
+    double t;
+    if (tau > 0.0) t = 1.0 / (tau + w);
+    else t = 1.0 / (tau - w);
+    const double sign_t = t > 0.0 ? 1.0 : -1.0;
+    const double n = 1.0 / sqrt(t * t + 1.0);
+    j.s = -sign_t * (y / fabs(y)) * fabs(t) * n;
+    j.c = n;
+}
+
+// m is row-major 3x3: m[r][c]
+SF_HD void real_2x2_jacobi_svd(const double (*mat)[3], int p, int q, Rot2& jl, Rot2& jr) {
+    double m00 = mat[p][p], m01 = mat[p][q], m10 = mat[q][p], m11 = mat[q][q];
+    Rot2 rot1;
+    const double t = m00 + m11;
+    const double d = m10 - m01;
+    if (fabs(d) < 2.2250738585072014e-308) {
+        rot1.s = 0.0;
+        rot1.c = 1.0;
+    } else {
+        const double u = t / d;
+        const double tmp = sqrt(1.0 + u * u);
+        rot1.s = 1.0 / tmp;
+        rot1.c = u / tmp;
+    }
+    {
+        const double a0 = m00, a1 = m01, b0 = m10, b1 = m11;
+        m00 = rot1.c * a0 + rot1.s * b0;
+        m01 = rot1.c * a1 + rot1.s * b1;
+        m10 = -rot1.s * a0 + rot1.c * b0;
+        m11 = -rot1.s * a1 + rot1.c * b1;
+        (void)m10;
+    }
+    make_jacobi(m00, m01, m11, jr);
+    jl = rot_mul(rot1, rot_t(jr));
+}
+
+SF_HD void apply_left3(double (*m)[3], int p, int q, Rot2 j) {
+    for (int k = 0; k < 3; ++k) {
+        const double xi = m[p][k], yi = m[q][k];
+        m[p][k] = j.c * xi + j.s * yi;
+        m[q][k] = -j.s * xi + j.c * yi;
+    }
+}
+SF_HD void apply_right3(double (*m)[3], int p, int q, Rot2 j) {
+    for (int k = 0; k < 3; ++k) {
+        const double xi = m[k][p], yi = m[k][q];
+        m[k][p] = j.c * xi - j.s * yi;
+        m[k][q] = j.s * xi + j.c * yi;
+    }
+}
+
+// nearest_rotation (pose.cpp:20-29)
+SF_HD m33 nearest_rotation(const m33& a) {
+    double work[3][3], u[3][3], v[3][3];
+    double scl = fabs(a.m[0]);
+    // cwiseAbs().maxCoeff() in column-major order
+    for (int c = 0; c < 3; ++c)
+        for (int r = 0; r < 3; ++r) {
+            const double x = fabs(a.m[r * 3 + c]);
+            scl = scl < x ? x : scl;
+        }
+    if (scl == 0.0) scl = 1.0;
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+            work[r][c] = a.m[r * 3 + c] / scl;
+            u[r][c] = r == c ? 1.0 : 0.0;
+            v[r][c] = r == c ? 1.0 : 0.0;
+        }
+    const double considerAsZero = 2.2250738585072014e-308;
+    const double precision = 2.0 * 2.220446049250313e-16;
+    double maxDiag = fabs(work[0][0]);
+    maxDiag = maxDiag < fabs(work[1][1]) ? fabs(work[1][1]) : maxDiag;
+    maxDiag = maxDiag < fabs(work[2][2]) ? fabs(work[2][2]) : maxDiag;
+    bool finished = false;
+    int sweeps = 0;
+    while (!finished && sweeps < 64) {
+        finished = true;
+        ++sweeps;
+        for (int p = 1; p < 3; ++p) {
+            for (int q = 0; q < p; ++q) {
+                const double pm = precision * maxDiag;
+                const double threshold = considerAsZero < pm ? pm : considerAsZero;
+                if (fabs(work[p][q]) > threshold || fabs(work[q][p]) > threshold) {
+                    finished = false;
+                    Rot2 jl, jr;
+                    real_2x2_jacobi_svd(work, p, q, jl, jr);
+                    apply_left3(work, p, q, jl);
+                    apply_right3(u, p, q, rot_t(jl));
+                    apply_right3(work, p, q, jr);
+                    apply_right3(v, p, q, jr);
+                    const double a_pp = fabs(work[p][p]), a_qq = fabs(work[q][q]);
+                    const double mx = a_pp < a_qq ? a_qq : a_pp;
+                    maxDiag = maxDiag < mx ? mx : maxDiag;
+                }
+            }
+        }
+    }
+    double sv[3];
+    for (int i = 0; i < 3; ++i) {
+        const double aii = work[i][i];
+        sv[i] = fabs(aii);
+        if (aii < 0.0)
+            for (int k = 0; k < 3; ++k) u[k][i] = -u[k][i];
+    }
+    for (int i = 0; i < 3; ++i) sv[i] = sv[i] * scl;
+    for (int i = 0; i < 3; ++i) {
+        int pos = i;
+        for (int k = i + 1; k < 3; ++k)
+            if (sv[k] > sv[pos]) pos = k;
+        if (pos != i) {
+            const double t = sv[i];
+            sv[i] = sv[pos];
+            sv[pos] = t;
+            for (int k = 0; k < 3; ++k) {
+                double x = u[k][i];
+                u[k][i] = u[k][pos];
+                u[k][pos] = x;
+                x = v[k][i];
+                v[k][i] = v[k][pos];
+                v[k][pos] = x;
+            }
+        }
+    }
+    m33 U, V;
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+            U.m[r * 3 + c] = u[r][c];
+            V.m[r * 3 + c] = v[r][c];
+        }
+    m33 R = mm(U, mt(V));
+    // determinant (shim order, grid-independent): m(0,0)*(m11*m22 - m21*m12) - m10*(...) + m20*(...)
+    const double* M = R.m;
+    auto at = [&](int r, int c) { return M[r * 3 + c]; };
+    const double det = at(0, 0) * (at(1, 1) * at(2, 2) - at(2, 1) * at(1, 2)) -
+                       at(1, 0) * (at(0, 1) * at(2, 2) - at(2, 1) * at(0, 2)) +
+                       at(2, 0) * (at(0, 1) * at(1, 2) - at(1, 1) * at(0, 2));
+    if (det < 0.0) {
+        m33 flip;
+        for (int i = 0; i < 9; ++i) flip.m[i] = 0.0;
+        flip.m[0] = 1.0;
+        flip.m[4] = 1.0;
+        flip.m[8] = -1.0;
+        R = mm(mm(U, flip), mt(V));
+    }
+    return R;
+}
+
+// apply_motion (pose.cpp:31-43)
+SF_HD Pose apply_motion(const Pose& pose, d3 r, d3 t) {
+    const double a = r.x, b = r.y, g = r.z;
+    m33 lin;
+    lin.m[0] = 1.0;
+    lin.m[1] = -g;
+    lin.m[2] = b;
+    lin.m[3] = g;
+    lin.m[4] = 1.0;
+    lin.m[5] = -a;
+    lin.m[6] = -b;
+    lin.m[7] = a;
+    lin.m[8] = 1.0;
+    Pose corr;
+    corr.R = nearest_rotation(lin);
+    corr.t = t;
+    return compose(corr, pose);
+}
+
+}  // namespace sf

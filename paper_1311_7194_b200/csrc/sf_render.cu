@@ -1,0 +1,405 @@
+// sf_render.cu — sparse-volume raycasting on the device (render.cpp:12-250).
+//
+//   k_ray_bounds  per pixel: slab clip + Amanatides-Woo DDA over the N^3 block lattice,
+//                 occupancy read from the 1-bit/block bitmap (N^3/8 bytes, L2 resident)
+//                 instead of the 4-byte offset table; first/last occupied cell -> float
+//                 [t_start, t_end]                                     (render.cpp:65-153)
+//   k_raycast     per pixel: stage-1 march on the sequential double t lattice, secant /
+//                 bisection stage 2, 6-sample gradient normal          (render.cpp:160-250)
+// All arithmetic is FP64 in the reference's order (no contraction), so depth, normals and
+// the stage-1 sample count are bit-identical to the CPU path.
+#include <algorithm>
+#include <vector>
+
+#include "sf_internal.h"
+
+namespace sf {
+
+__device__ __forceinline__ bool occupied(const uint32_t* __restrict__ occ, uint64_t ti) {
+    return (__ldg(&occ[ti >> 5]) >> (ti & 31)) & 1u;
+}
+
+__global__ void k_ray_bounds(VolParams P, const FrameConsts* __restrict__ fc, const uint32_t* __restrict__ occ,
+                             const VolCounters* __restrict__ vc, float* __restrict__ t_start,
+                             float* __restrict__ t_end, int w, int h, const int* dead) {
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    const int v = blockIdx.y * blockDim.y + threadIdx.y;
+    if (u >= w || v >= h) return;
+    if (dead && *dead) return;
+    const size_t idx = (size_t)v * w + u;
+    float ts = INFINITY, te = -INFINITY;
+    if (vc->allocated_count != 0) {
+        const Intr& intr = fc->intr;
+        const Pose& pose = fc->pose;
+        const int n = P.N;
+        const double side = P.block_side;
+        const double box_lo[3] = {P.ox, P.oy, P.oz};
+        const double box_hi[3] = {P.ox + P.box_side, P.oy + P.box_side, P.oz + P.box_side};
+        const double org[3] = {pose.t.x, pose.t.y, pose.t.z};
+        const d3 dir_cam = normalized(unproject(intr, u, v, 1.0));
+        const d3 dv3 = mv(pose.R, dir_cam);
+        const double dir[3] = {dv3.x, dv3.y, dv3.z};
+        double lo = intr.near_plane / dir_cam.z;
+        double hi = intr.far_plane / dir_cam.z;
+        for (int a = 0; a < 3; ++a) {
+            if (fabs(dir[a]) < 1e-15) {
+                if (org[a] < box_lo[a] || org[a] > box_hi[a]) {
+                    lo = 1.0;
+                    hi = 0.0;
+                    break;
+                }
+                continue;
+            }
+            double t0 = (box_lo[a] - org[a]) / dir[a];
+            double t1 = (box_hi[a] - org[a]) / dir[a];
+            if (t0 > t1) {
+                const double tmp = t0;
+                t0 = t1;
+                t1 = tmp;
+            }
+            lo = dmax(lo, t0);
+            hi = dmin(hi, t1);
+        }
+        if (lo <= hi) {
+            const double entry[3] = {org[0] + lo * dir[0], org[1] + lo * dir[1], org[2] + lo * dir[2]};
+            int cell[3], step[3];
+            double t_max[3], t_delta[3];
+            for (int a = 0; a < 3; ++a) {
+                int c = ref_floor_int((entry[a] - box_lo[a]) / side);
+                c = c < 0 ? 0 : (n - 1 < c ? n - 1 : c);  // std::clamp(c, 0, n - 1)
+                cell[a] = c;
+            }
+            for (int a = 0; a < 3; ++a) {
+                if (dir[a] > 1e-15) {
+                    step[a] = 1;
+                    t_max[a] = lo + (box_lo[a] + (double)(cell[a] + 1) * side - entry[a]) / dir[a];
+                    t_delta[a] = side / dir[a];
+                } else if (dir[a] < -1e-15) {
+                    step[a] = -1;
+                    t_max[a] = lo + (box_lo[a] + (double)cell[a] * side - entry[a]) / dir[a];
+                    t_delta[a] = -side / dir[a];
+                } else {
+                    step[a] = 0;
+                    t_max[a] = INFINITY;
+                    t_delta[a] = INFINITY;
+                }
+            }
+            double first = INFINITY, last = -INFINITY;
+            double t_in = lo;
+            while (t_in <= hi) {
+                const int axis = t_max[0] <= t_max[1] ? (t_max[0] <= t_max[2] ? 0 : 2) : (t_max[1] <= t_max[2] ? 1 : 2);
+                const double t_out = dmin(t_max[axis], hi);
+                if (occupied(occ, table_index(P, cell[0], cell[1], cell[2]))) {
+                    first = dmin(first, t_in);
+                    last = dmax(last, t_out);
+                }
+                t_in = t_max[axis];
+                cell[axis] += step[axis];
+                if (cell[axis] < 0 || cell[axis] >= n) break;
+                t_max[axis] += t_delta[axis];
+            }
+            if (first <= last) {
+                ts = (float)dmax(first, lo);
+                te = (float)dmin(last, hi);
+            }
+        }
+    }
+    t_start[idx] = ts;
+    t_end[idx] = te;
+}
+
+// voxel_code + sample_tsdf (render.cpp:12-48). Returns false for nullopt.
+struct Sampler {
+    VolParams P;
+    const int32_t* __restrict__ table;
+    const uint16_t* __restrict__ payload;
+    const double* tdec;  // shared-memory LUT, index code + 128
+
+    __device__ __forceinline__ bool code(int x, int y, int z, double& out) const {
+        const int M = P.M;
+        const int bx = x / M, by = y / M, bz = z / M;
+        const int32_t slot = __ldg(&table[table_index(P, bx, by, bz)]);
+        if (slot == kEmpty) return false;
+        const int lx = x - bx * M, ly = y - by * M, lz = z - bz * M;
+        const uint16_t pl = __ldg(&payload[(size_t)slot * P.M3 + (lz * M + ly) * M + lx]);
+        const int8_t c = static_cast<int8_t>(pl & 0xFF);
+        if (c == kChiCode) return false;
+        out = tdec[(int)c + 128];
+        return true;
+    }
+
+    __device__ bool sample(d3 p, double& out) const {
+        const double gx = (p.x - P.ox) / P.voxel - 0.5;
+        const double gy = (p.y - P.oy) / P.voxel - 0.5;
+        const double gz = (p.z - P.oz) / P.voxel - 0.5;
+        const int bx = ref_floor_int(gx), by = ref_floor_int(gy), bz = ref_floor_int(gz);
+        const int res = P.res;
+        if (bx < 0 || by < 0 || bz < 0 || bx + 1 >= res || by + 1 >= res || bz + 1 >= res) return false;
+        const double fx = gx - (double)bx, fy = gy - (double)by, fz = gz - (double)bz;
+        double c[8];
+        for (int i = 0; i < 8; ++i)
+            if (!code(bx + (i & 1), by + ((i >> 1) & 1), bz + ((i >> 2) & 1), c[i])) return false;
+        const double x0 = c[0] + (c[1] - c[0]) * fx;
+        const double x1 = c[2] + (c[3] - c[2]) * fx;
+        const double x2 = c[4] + (c[5] - c[4]) * fx;
+        const double x3 = c[6] + (c[7] - c[6]) * fx;
+        const double y0 = x0 + (x1 - x0) * fy;
+        const double y1 = x2 + (x3 - x2) * fy;
+        out = y0 + (y1 - y0) * fz;
+        return true;
+    }
+
+    // sample_tsdf_gradient (render.cpp:50-63)
+    __device__ bool gradient(d3 p, double h, d3& g) const {
+        double gv[3];
+        const double pc[3] = {p.x, p.y, p.z};
+        for (int i = 0; i < 3; ++i) {
+            double dp[3] = {pc[0], pc[1], pc[2]}, dm[3] = {pc[0], pc[1], pc[2]};
+            dp[i] += h;
+            dm[i] -= h;
+            double a, b;
+            if (!sample(mk(dp[0], dp[1], dp[2]), a)) return false;
+            if (!sample(mk(dm[0], dm[1], dm[2]), b)) return false;
+            gv[i] = (a - b) / (2.0 * h);
+        }
+        g = mk(gv[0], gv[1], gv[2]);
+        return true;
+    }
+};
+
+__global__ void __launch_bounds__(256)
+    k_raycast(VolParams P, const FrameConsts* __restrict__ fc, const int32_t* __restrict__ table,
+              const uint16_t* __restrict__ payload, const AuxTables* __restrict__ aux,
+              const float* __restrict__ t_start, const float* __restrict__ t_end, float* __restrict__ depth_out,
+              float* __restrict__ normals_out, RayCounters* stats, int w, int h, const int* dead) {
+    __shared__ double s_tdec[256];
+    if (dead && *dead) return;
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+    for (int i = tid; i < 256; i += blockDim.x * blockDim.y) s_tdec[i] = aux->tsdf_decode[i];
+    __syncthreads();
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    const int v = blockIdx.y * blockDim.y + threadIdx.y;
+    unsigned long long steps = 0, hits = 0, with_bounds = 0;
+    if (u < w && v < h) {
+        const size_t idx = (size_t)v * w + u;
+        float out_d = 0.0f, nx = 0.f, ny = 0.f, nz = 0.f;
+        const float fs = t_start[idx], fe = t_end[idx];
+        if (fs <= fe) {  // !bounds.empty(u, v)
+            with_bounds = 1;
+            const Sampler S{P, table, payload, s_tdec};
+            const Intr& intr = fc->intr;
+            const Pose& pose = fc->pose;
+            const double vox = P.voxel;
+            const double coarse_step = 0.5 * P.delta;
+            const double fine_tol = 0.01 * vox;
+            const d3 dir_cam = normalized(unproject(intr, u, v, 1.0));
+            const d3 dir = mv(pose.R, dir_cam);
+            const double t0 = fs, t1 = fe;
+            double prev_t = 0.0, prev_val = 0.0;
+            bool have_prev = false, bracketed = false;
+            double hit_a = 0.0, hit_b = 0.0, val_a = 0.0, val_b = 0.0;
+            for (double t = t0;; t += coarse_step) {
+                const bool final_sample = t >= t1;
+                if (final_sample) t = t1;
+                ++steps;
+                double val;
+                if (S.sample(add(pose.t, scale(t, dir)), val)) {
+                    if (have_prev && prev_val > 0.0 && val < 0.0) {
+                        hit_a = prev_t;
+                        val_a = prev_val;
+                        hit_b = t;
+                        val_b = val;
+                        bracketed = true;
+                        break;
+                    }
+                    have_prev = true;
+                    prev_t = t;
+                    prev_val = val;
+                }
+                if (final_sample) break;
+            }
+            if (bracketed) {
+                double root = hit_b;
+                for (int iter = 0; iter < 48 && hit_b - hit_a > fine_tol; ++iter) {
+                    double t_new = hit_b - val_b * (hit_b - hit_a) / (val_b - val_a);
+                    if (!(t_new > hit_a) || !(t_new < hit_b)) t_new = 0.5 * (hit_a + hit_b);
+                    double val;
+                    if (!S.sample(add(pose.t, scale(t_new, dir)), val)) {
+                        hit_a = t_new;
+                        val_a = dmax(val_a, 1e-12);
+                        continue;
+                    }
+                    if (val > 0.0) {
+                        hit_a = t_new;
+                        val_a = val;
+                    } else {
+                        hit_b = t_new;
+                        val_b = val;
+                    }
+                }
+                if (val_b != val_a) {
+                    const double interp = hit_b - val_b * (hit_b - hit_a) / (val_b - val_a);
+                    root = dclamp(interp, hit_a, hit_b);
+                } else {
+                    root = 0.5 * (hit_a + hit_b);
+                }
+                const double dd = root * dir_cam.z;
+                if (!(dd < intr.near_plane || dd > intr.far_plane)) {
+                    out_d = (float)dd;
+                    hits = 1;
+                    d3 g;
+                    if (S.gradient(add(pose.t, scale(root, dir)), vox, g) && sqnorm(g) > 0.0) {
+                        // world_to_cam * grad.normalized()  (render.cpp:242-245)
+                        const d3 n_cam = mv(mt(pose.R), normalized(g));
+                        nx = (float)n_cam.x;
+                        ny = (float)n_cam.y;
+                        nz = (float)n_cam.z;
+                    }
+                }
+            }
+        }
+        depth_out[idx] = out_d;
+        normals_out[3 * idx] = nx;
+        normals_out[3 * idx + 1] = ny;
+        normals_out[3 * idx + 2] = nz;
+    }
+    // RaycastStats: warp reduction, one atomic per warp and counter.
+    for (int off = 16; off > 0; off >>= 1) {
+        steps += __shfl_down_sync(0xffffffffu, steps, off);
+        hits += __shfl_down_sync(0xffffffffu, hits, off);
+        with_bounds += __shfl_down_sync(0xffffffffu, with_bounds, off);
+    }
+    if ((tid & 31) == 0 && stats) {
+        if (steps) atomicAdd(&stats->sample_steps, steps);
+        if (hits) atomicAdd(&stats->hit_pixels, hits);
+        if (with_bounds) atomicAdd(&stats->rays_with_bounds, with_bounds);
+    }
+}
+
+void launch_ray_bounds(Volume& v, const FrameConsts* d_fc, const Intr& intr, float* t_start, float* t_end,
+                       cudaStream_t s, uint64_t* launches, const int* dead_flag) {
+    const dim3 blk(32, 4), grd((intr.w + 31) / 32, (intr.h + 3) / 4);
+    k_ray_bounds<<<grd, blk, 0, s>>>(v.P, d_fc, v.d_occ, v.d_vc, t_start, t_end, intr.w, intr.h, dead_flag);
+    SF_LAUNCH_CHECK();
+    if (launches) *launches += 1;
+}
+
+void launch_raycast(Volume& v, const FrameConsts* d_fc, const Intr& intr, const float* t_start, const float* t_end,
+                    float* depth, float* normals, RayCounters* d_stats, cudaStream_t s, uint64_t* launches,
+                    const int* dead_flag) {
+    const dim3 blk(32, 4), grd((intr.w + 31) / 32, (intr.h + 3) / 4);
+    k_raycast<<<grd, blk, 0, s>>>(v.P, d_fc, v.d_table, v.d_payload, v.d_aux, t_start, t_end, depth, normals,
+                                  d_stats, intr.w, intr.h, dead_flag);
+    SF_LAUNCH_CHECK();
+    if (launches) *launches += 1;
+}
+
+// Scratch for the stand-alone raycast API.
+struct RayScratch {
+    int w = 0, h = 0;
+    float *ts = nullptr, *te = nullptr, *depth = nullptr, *normals = nullptr;
+    FrameConsts* fc = nullptr;
+    double* pose = nullptr;
+    RayCounters* stats = nullptr;
+    void ensure(int W, int H) {
+        if (W == w && H == h && ts) return;
+        release();
+        const size_t n = static_cast<size_t>(W) * H;
+        SF_CUDA(cudaMalloc(&ts, n * sizeof(float)));
+        SF_CUDA(cudaMalloc(&te, n * sizeof(float)));
+        SF_CUDA(cudaMalloc(&depth, n * sizeof(float)));
+        SF_CUDA(cudaMalloc(&normals, 3 * n * sizeof(float)));
+        SF_CUDA(cudaMalloc(&fc, sizeof(FrameConsts)));
+        SF_CUDA(cudaMalloc(&pose, 12 * sizeof(double)));
+        SF_CUDA(cudaMalloc(&stats, sizeof(RayCounters)));
+        w = W;
+        h = H;
+    }
+    void release() {
+        void* p[] = {ts, te, depth, normals, fc, pose, stats};
+        for (void* q : p)
+            if (q) cudaFree(q);
+        ts = te = depth = normals = nullptr;
+        fc = nullptr;
+        pose = nullptr;
+        stats = nullptr;
+        w = h = 0;
+    }
+};
+
+static void validate_intr(const sf_intrinsics& i) {
+    if (i.width <= 0 || i.height <= 0) throw Error(SF_INVALID_ARGUMENT, "intrinsics: non-positive image size");
+    if (i.fx <= 0.0 || i.fy <= 0.0) throw Error(SF_INVALID_ARGUMENT, "intrinsics: non-positive focal length");
+    if (!(i.near_plane > 0.0) || !(i.near_plane < i.far_plane))
+        throw Error(SF_INVALID_ARGUMENT, "intrinsics: need 0 < near < far");
+}
+
+}  // namespace sf
+
+using namespace sf;
+
+static RayScratch& ray_scratch() {
+    static thread_local RayScratch rs;
+    return rs;
+}
+
+extern "C" {
+
+int sf_ray_bounds(sf_volume_t v, const double pose[12], const sf_intrinsics* intr, float* t_start, float* t_end,
+                  int32_t out_on_device, void* stream) {
+    return guarded([&]() -> int {
+        SF_CUDA(cudaSetDevice(v->device));
+        validate_intr(*intr);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        RayScratch& rs = ray_scratch();
+        rs.ensure(intr->width, intr->height);
+        const Intr I = to_intr(*intr);
+        SF_CUDA(cudaMemcpyAsync(rs.pose, pose, 12 * sizeof(double), cudaMemcpyHostToDevice, s));
+        launch_consts(v->P, I, rs.pose, rs.fc, s, nullptr);
+        float* ts = out_on_device ? t_start : rs.ts;
+        float* te = out_on_device ? t_end : rs.te;
+        launch_ray_bounds(*v, rs.fc, I, ts, te, s, nullptr, nullptr);
+        const size_t n = static_cast<size_t>(intr->width) * intr->height;
+        if (!out_on_device) {
+            SF_CUDA(cudaMemcpyAsync(t_start, rs.ts, n * sizeof(float), cudaMemcpyDeviceToHost, s));
+            SF_CUDA(cudaMemcpyAsync(t_end, rs.te, n * sizeof(float), cudaMemcpyDeviceToHost, s));
+        }
+        SF_CUDA(cudaStreamSynchronize(s));
+        return SF_OK;
+    });
+}
+
+int sf_raycast(sf_volume_t v, const double pose[12], const sf_intrinsics* intr, float* depth, float* normals_xyz,
+               int32_t out_on_device, sf_raycast_stats* stats, void* stream) {
+    return guarded([&]() -> int {
+        SF_CUDA(cudaSetDevice(v->device));
+        validate_intr(*intr);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        RayScratch& rs = ray_scratch();
+        rs.ensure(intr->width, intr->height);
+        const Intr I = to_intr(*intr);
+        SF_CUDA(cudaMemcpyAsync(rs.pose, pose, 12 * sizeof(double), cudaMemcpyHostToDevice, s));
+        SF_CUDA(cudaMemsetAsync(rs.stats, 0, sizeof(RayCounters), s));
+        launch_consts(v->P, I, rs.pose, rs.fc, s, nullptr);
+        launch_ray_bounds(*v, rs.fc, I, rs.ts, rs.te, s, nullptr, nullptr);
+        float* d = out_on_device ? depth : rs.depth;
+        float* nm = out_on_device ? normals_xyz : rs.normals;
+        launch_raycast(*v, rs.fc, I, rs.ts, rs.te, d, nm, rs.stats, s, nullptr, nullptr);
+        const size_t n = static_cast<size_t>(intr->width) * intr->height;
+        if (!out_on_device) {
+            SF_CUDA(cudaMemcpyAsync(depth, rs.depth, n * sizeof(float), cudaMemcpyDeviceToHost, s));
+            SF_CUDA(cudaMemcpyAsync(normals_xyz, rs.normals, 3 * n * sizeof(float), cudaMemcpyDeviceToHost, s));
+        }
+        RayCounters c{};
+        SF_CUDA(cudaMemcpyAsync(&c, rs.stats, sizeof(c), cudaMemcpyDeviceToHost, s));
+        SF_CUDA(cudaStreamSynchronize(s));
+        if (stats) {
+            stats->sample_steps = c.sample_steps;
+            stats->hit_pixels = c.hit_pixels;
+            stats->rays_with_bounds = c.rays_with_bounds;
+        }
+        return SF_OK;
+    });
+}
+
+}  // extern "C"

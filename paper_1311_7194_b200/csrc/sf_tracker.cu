@@ -1,0 +1,314 @@
+// sf_tracker.cu — the fused frame: run()'s per-frame body (pipeline.cpp:233-301) on the
+// device, captured once into a CUDA graph and replayed per frame.
+//
+// Track step (pipeline.cpp:257-287):
+//   raycast(grid, current_pose)                  -> model depth + normals   (render.cpp)
+//   initial_delta = compose(invert(current), current)   (initial_transform_hook without
+//                                                         an external delta, registration.cpp:222-224)
+//   icp(captured, model depth, model normals, initial_delta)   (source normals from
+//                                                         match.normal_options, registration.cpp:216-220)
+//   estimated = compose(current, delta); current = estimated
+//   fuse_frame(grid, captured, estimated)
+// Ground-truth step (and the first frame): fuse at the given pose.
+// TrackingLost / PoolExhausted set a device "dead" flag: the rest of the frame and every
+// later step become no-ops, mirroring run()'s break (pipeline.cpp:289-299).
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "sf_icp.cuh"
+
+namespace sf {
+
+struct TrackerDev {
+    int dead;
+    int status;
+    int registered;
+    int frame;
+};
+
+__global__ void k_tracker_begin_track(const double* __restrict__ cur, double* __restrict__ init_delta,
+                                      RayCounters* rstats, const TrackerDev* td) {
+    if (td->dead) return;
+    // initial_pose = initial_transform_hook(current, nullopt) = current;
+    // initial_delta = compose(invert(current), initial_pose)   (pipeline.cpp:262-267)
+    const Pose c = pose_from12(cur);
+    const Pose d = compose(invert(c), c);
+    pose_to12(d, init_delta);
+    RayCounters z{0, 0, 0, 0};
+    *rstats = z;
+}
+
+__global__ void k_tracker_after_icp(double* __restrict__ cur, double* __restrict__ fuse_pose, const IcpState* st,
+                                    TrackerDev* td) {
+    if (td->dead) return;
+    if (st->lost) {
+        td->dead = 1;
+        td->status = SF_TRACKING_LOST;
+        return;
+    }
+    const Pose est = compose(pose_from12(cur), st->delta);  // pipeline.cpp:282
+    pose_to12(est, cur);
+    pose_to12(est, fuse_pose);
+    td->registered = 1;
+}
+
+__global__ void k_tracker_begin_gt(const double* __restrict__ gt, double* __restrict__ cur,
+                                   double* __restrict__ fuse_pose, RayCounters* rstats, TrackerDev* td, int set_current) {
+    if (td->dead) return;
+    for (int i = 0; i < 12; ++i) {
+        fuse_pose[i] = gt[i];
+        if (set_current) cur[i] = gt[i];
+    }
+    RayCounters z{0, 0, 0, 0};
+    *rstats = z;
+    td->registered = 0;
+}
+
+__global__ void k_tracker_finish(const FrameCounters* ctr, TrackerDev* td) {
+    if (td->dead) return;
+    if (ctr->exhausted) {
+        td->dead = 1;
+        td->status = SF_POOL_EXHAUSTED;
+    }
+}
+
+}  // namespace sf
+
+using namespace sf;
+
+struct sf_tracker {
+    sf_volume* vol = nullptr;
+    sf_tracker_config cfg{};
+    Intr cam{};
+    FuseParams fp{};
+    FuseParams fp_sigma{};
+    IcpParamsDev icp_prm{};
+    FrameBuffers fb;
+    IcpWork icp;
+    double* d_cur = nullptr;
+    double* d_init_delta = nullptr;
+    double* d_gt = nullptr;
+    FrameConsts* d_rc_fc = nullptr;
+    float *d_ts = nullptr, *d_te = nullptr, *d_model_depth = nullptr, *d_model_normals = nullptr;
+    float *d_cap = nullptr, *d_cap_sigma = nullptr;
+    RayCounters* d_rstats = nullptr;
+    TrackerDev* d_td = nullptr;
+    // host-side
+    int frames = 0;
+    int last_mode = 0;
+    bool last_registered = false;
+    uint64_t last_launches = 0;
+    cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [mode][has_sigma]
+    uint64_t graph_kernels[2][2] = {{0, 0}, {0, 0}};
+    // pinned fetch staging
+    struct Fetch {
+        double cur[12];
+        double fuse_pose[12];
+        TrackerDev td;
+        FrameCounters ctr;
+        RayCounters rs;
+        IcpState icp;
+    }* h = nullptr;
+
+    ~sf_tracker() {
+        cudaSetDevice(vol ? vol->device : 0);
+        for (auto& row : graph)
+            for (auto& g : row)
+                if (g) cudaGraphExecDestroy(g);
+        void* p[] = {d_cur, d_init_delta, d_gt, d_rc_fc, d_ts, d_te, d_model_depth, d_model_normals, d_cap,
+                     d_cap_sigma, d_rstats, d_td};
+        for (void* q : p)
+            if (q) cudaFree(q);
+        if (h) cudaFreeHost(h);
+    }
+
+    // The frame's launch sequence (captured into a graph or issued directly).
+    uint64_t issue(int mode, bool has_sigma, cudaStream_t s) {
+        uint64_t n = 0;
+        const int* dead = &d_td->dead;
+        const FuseParams& p = has_sigma ? fp_sigma : fp;
+        const float* sig = has_sigma ? d_cap_sigma : nullptr;
+        if (mode == 0) {
+            k_tracker_begin_track<<<1, 1, 0, s>>>(d_cur, d_init_delta, d_rstats, d_td);
+            SF_LAUNCH_CHECK();
+            ++n;
+            launch_consts(vol->P, cam, d_cur, d_rc_fc, s, &n);
+            launch_ray_bounds(*vol, d_rc_fc, cam, d_ts, d_te, s, &n, dead);
+            launch_raycast(*vol, d_rc_fc, cam, d_ts, d_te, d_model_depth, d_model_normals, d_rstats, s, &n, dead);
+            launch_compute_normals(d_cap, cam.w, cam.h, cam, cfg.match.normal_sigma0, cfg.match.normal_spatial_scale,
+                                   icp.src_normals, s, &n, dead);
+            launch_icp(icp, d_cap, icp.src_normals, d_model_depth, d_model_normals, cam, cam, d_init_delta, icp_prm, s,
+                       &n, dead);
+            k_tracker_after_icp<<<1, 1, 0, s>>>(d_cur, fb.pose, icp.st, d_td);
+            SF_LAUNCH_CHECK();
+            ++n;
+        } else {
+            k_tracker_begin_gt<<<1, 1, 0, s>>>(d_gt, d_cur, fb.pose, d_rstats, d_td, mode == 1 ? 1 : 0);
+            SF_LAUNCH_CHECK();
+            ++n;
+        }
+        launch_fuse(*vol, fb, cam, d_cap, sig, p, s, false, &n, dead);
+        k_tracker_finish<<<1, 1, 0, s>>>(fb.ctr, d_td);
+        SF_LAUNCH_CHECK();
+        ++n;
+        return n;
+    }
+};
+
+static uint64_t count_kernel_nodes(cudaGraph_t g) {
+    size_t num = 0;
+    SF_CUDA(cudaGraphGetNodes(g, nullptr, &num));
+    std::vector<cudaGraphNode_t> nodes(num);
+    SF_CUDA(cudaGraphGetNodes(g, nodes.data(), &num));
+    uint64_t k = 0;
+    for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        SF_CUDA(cudaGraphNodeGetType(nd, &t));
+        if (t == cudaGraphNodeTypeKernel) ++k;
+    }
+    return k;
+}
+
+extern "C" {
+
+int sf_tracker_create(sf_volume_t vol, const sf_tracker_config* config, const double initial_pose[12],
+                      sf_tracker_t* out) {
+    return guarded([&]() -> int {
+        if (!vol || !config || !initial_pose || !out) throw Error(SF_INVALID_ARGUMENT, "sf_tracker_create: null");
+        SF_CUDA(cudaSetDevice(vol->device));
+        auto t = std::make_unique<sf_tracker>();
+        t->vol = vol;
+        t->cfg = *config;
+        t->cam = to_intr(config->camera);
+        t->fp = resolve_fuse_params(*vol, config->fusion, false);
+        t->fp_sigma = resolve_fuse_params(*vol, config->fusion, true);
+        t->icp_prm = make_icp_params(config->match);
+        const int w = config->camera.width, h = config->camera.height;
+        if (w <= 0 || h <= 0) throw Error(SF_INVALID_ARGUMENT, "intrinsics: non-positive image size");
+        ensure_frame_buffers(*vol, t->fb, w, h);
+        t->icp.ensure(w, h);
+        const size_t n = static_cast<size_t>(w) * h;
+        SF_CUDA(cudaMalloc(&t->d_cur, 12 * sizeof(double)));
+        SF_CUDA(cudaMalloc(&t->d_init_delta, 12 * sizeof(double)));
+        SF_CUDA(cudaMalloc(&t->d_gt, 12 * sizeof(double)));
+        SF_CUDA(cudaMalloc(&t->d_rc_fc, sizeof(FrameConsts)));
+        SF_CUDA(cudaMalloc(&t->d_ts, n * sizeof(float)));
+        SF_CUDA(cudaMalloc(&t->d_te, n * sizeof(float)));
+        SF_CUDA(cudaMalloc(&t->d_model_depth, n * sizeof(float)));
+        SF_CUDA(cudaMalloc(&t->d_model_normals, 3 * n * sizeof(float)));
+        SF_CUDA(cudaMalloc(&t->d_cap, n * sizeof(float)));
+        SF_CUDA(cudaMalloc(&t->d_cap_sigma, n * sizeof(float)));
+        SF_CUDA(cudaMalloc(&t->d_rstats, sizeof(RayCounters)));
+        SF_CUDA(cudaMalloc(&t->d_td, sizeof(TrackerDev)));
+        SF_CUDA(cudaMemset(t->d_td, 0, sizeof(TrackerDev)));
+        SF_CUDA(cudaMemset(t->d_rstats, 0, sizeof(RayCounters)));
+        SF_CUDA(cudaMemcpy(t->d_cur, initial_pose, 12 * sizeof(double), cudaMemcpyHostToDevice));
+        SF_CUDA(cudaMallocHost(&t->h, sizeof(sf_tracker::Fetch)));
+        std::memset(t->h, 0, sizeof(sf_tracker::Fetch));
+        *out = t.release();
+        return SF_OK;
+    });
+}
+
+int sf_tracker_destroy(sf_tracker_t tr) {
+    delete tr;
+    return SF_OK;
+}
+
+int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, const double gt_pose[12], void* stream) {
+    return guarded([&]() -> int {
+        if (!tr || !captured) throw Error(SF_INVALID_ARGUMENT, "sf_tracker_step: null argument");
+        if (captured->intrinsics.width != tr->cam.w || captured->intrinsics.height != tr->cam.h)
+            throw Error(SF_INVALID_ARGUMENT, "sf_tracker_step: frame size differs from the tracker camera");
+        if (mode == 1 && !gt_pose) throw Error(SF_INVALID_ARGUMENT, "sf_tracker_step: ground-truth mode needs gt_pose");
+        SF_CUDA(cudaSetDevice(tr->vol->device));
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const size_t n = static_cast<size_t>(tr->cam.w) * tr->cam.h;
+        const cudaMemcpyKind kind = captured->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        SF_CUDA(cudaMemcpyAsync(tr->d_cap, captured->depth, n * sizeof(float), kind, s));
+        const bool has_sigma = captured->sigma != nullptr;
+        if (has_sigma) SF_CUDA(cudaMemcpyAsync(tr->d_cap_sigma, captured->sigma, n * sizeof(float), kind, s));
+        // First frame: fuse at the current (initial) pose without registration (pipeline.cpp:250-252).
+        int eff = mode;
+        if (mode == 0 && tr->frames == 0) eff = 2;  // fuse at current, keep current
+        if (eff == 1) SF_CUDA(cudaMemcpyAsync(tr->d_gt, gt_pose, 12 * sizeof(double), cudaMemcpyHostToDevice, s));
+        if (eff == 2) SF_CUDA(cudaMemcpyAsync(tr->d_gt, tr->d_cur, 12 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        const int gmode = eff == 0 ? 0 : 1;
+        const int sidx = has_sigma ? 1 : 0;
+        if (tr->cfg.use_graphs && eff != 2) {
+            cudaGraphExec_t& ge = tr->graph[gmode][sidx];
+            if (!ge) {
+                cudaGraph_t g;
+                SF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+                try {
+                    tr->issue(eff, has_sigma, s);
+                } catch (...) {
+                    cudaStreamEndCapture(s, &g);
+                    throw;
+                }
+                SF_CUDA(cudaStreamEndCapture(s, &g));
+                SF_CUDA(cudaGraphInstantiate(&ge, g, 0));
+                tr->graph_kernels[gmode][sidx] = count_kernel_nodes(g);
+                SF_CUDA(cudaGraphDestroy(g));
+            }
+            SF_CUDA(cudaGraphLaunch(ge, s));
+            tr->last_launches = tr->graph_kernels[gmode][sidx];
+        } else {
+            tr->last_launches = tr->issue(eff, has_sigma, s);
+        }
+        tr->last_mode = eff;
+        ++tr->frames;
+        return SF_OK;
+    });
+}
+
+int sf_tracker_fetch(sf_tracker_t tr, sf_frame_metrics* out, void* stream) {
+    return guarded([&]() -> int {
+        SF_CUDA(cudaSetDevice(tr->vol->device));
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        auto* h = tr->h;
+        SF_CUDA(cudaMemcpyAsync(h->cur, tr->d_cur, sizeof(h->cur), cudaMemcpyDeviceToHost, s));
+        SF_CUDA(cudaMemcpyAsync(h->fuse_pose, tr->fb.pose, sizeof(h->fuse_pose), cudaMemcpyDeviceToHost, s));
+        SF_CUDA(cudaMemcpyAsync(&h->td, tr->d_td, sizeof(TrackerDev), cudaMemcpyDeviceToHost, s));
+        SF_CUDA(cudaMemcpyAsync(&h->ctr, tr->fb.ctr, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
+        SF_CUDA(cudaMemcpyAsync(&h->rs, tr->d_rstats, sizeof(RayCounters), cudaMemcpyDeviceToHost, s));
+        SF_CUDA(cudaMemcpyAsync(&h->icp, tr->icp.st, sizeof(IcpState), cudaMemcpyDeviceToHost, s));
+        SF_CUDA(cudaStreamSynchronize(s));
+        std::memset(out, 0, sizeof(*out));
+        out->frame = tr->frames - 1;
+        out->status = h->td.status;
+        out->registered = tr->last_mode == 0 ? h->td.registered : 0;
+        std::memcpy(out->pose, h->fuse_pose, sizeof(out->pose));
+        if (out->registered) {
+            out->iterations = h->icp.iterations;
+            out->matches = h->icp.matches;
+            out->residual_rms = h->icp.residual_rms;
+            for (int i = 0; i < 6; ++i) {
+                out->lambda_over_n[i] = h->icp.eigenvalues[i] / static_cast<double>(h->icp.pair_count);
+                out->gated_mask[i] = h->icp.gated[i];
+            }
+        }
+        const uint64_t nn = tr->vol->P.N, m = tr->vol->P.M;
+        out->fusion.voxels_updated = h->ctr.voxels_updated;
+        out->fusion.blocks_allocated_now = h->ctr.alloc_now - h->ctr.alloc_before;
+        out->fusion.blocks_total = h->ctr.alloc_now;
+        out->fusion.memory_bytes = 2ull * h->ctr.alloc_now * m * m * m + 4ull * nn * nn * nn;
+        out->raycast.sample_steps = h->rs.sample_steps;
+        out->raycast.hit_pixels = h->rs.hit_pixels;
+        out->raycast.rays_with_bounds = h->rs.rays_with_bounds;
+        return SF_OK;
+    });
+}
+
+int sf_tracker_device_pose(sf_tracker_t tr, const double** device_pose) {
+    *device_pose = tr->d_cur;
+    return SF_OK;
+}
+
+int sf_tracker_last_launch_count(sf_tracker_t tr, uint64_t* count) {
+    *count = tr->last_launches;
+    return SF_OK;
+}
+
+}  // extern "C"

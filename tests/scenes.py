@@ -1,0 +1,58 @@
+"""Scenes and configurations of BASELINE.json, shared by tests and bench."""
+import math
+
+from paper_1311_7194_b200 import api as sf
+
+
+def camera(width=640, height=480, focal=525.0):
+    return sf.Intrinsics.simple(width, height, focal)
+
+
+def sphere_plane_scene():
+    """C1/C2: sphere c=(0,0,1.3) r=0.4 plus the wall z = 2."""
+    s = sf.AnalyticScene()
+    s.add_sphere([0.0, 0.0, 1.3], 0.4)
+    s.add_plane([0.0, 0.0, -1.0], -2.0)
+    return s
+
+
+def c1_config():
+    return sf.GridConfig(32, 8, (-1.0, -1.0, 0.25), 2.0, 0.0)
+
+
+def c2_config():
+    return sf.GridConfig(125, 4, (-1.0, -1.0, 0.25), 2.0, 0.0)
+
+
+def c1_trajectory(frames=100):
+    return sf.orbit_trajectory([0.0, 0.0, 1.3], 1.3, frames, (0.0, 1.0, 0.0), math.pi / 4, math.pi / 2)
+
+
+def bumpy_sphere(center=(0.0, 0.0, 0.35), r=0.08, bump=0.024):
+    """C4: hand-scale bumpy sphere."""
+    s = sf.AnalyticScene()
+    s.add_sphere(list(center), r)
+    o = r / math.sqrt(3.0)
+    for i in range(8):
+        s.add_sphere([center[0] + (o if i & 1 else -o), center[1] + (o if i & 2 else -o),
+                      center[2] + (o if i & 4 else -o)], bump)
+    return s
+
+
+def c4_config():
+    side = 4096 * 0.15e-3
+    return sf.GridConfig(512, 8, (-side / 2, -side / 2, 0.35 - side / 2), side, 0.0)
+
+
+def c4_trajectory(frames=100):
+    return sf.orbit_trajectory([0.0, 0.0, 0.35], 0.35, frames, (0.0, 1.0, 0.0), 0.0, 2.0 * math.pi)
+
+
+def cluster_scene():
+    """sphere_cluster (tests/test_utils.hpp:15-22)."""
+    s = sf.AnalyticScene()
+    s.add_sphere([0.25, -0.05, 1.30], 0.28)
+    s.add_sphere([-0.30, 0.18, 1.55], 0.22)
+    s.add_sphere([0.05, 0.30, 1.10], 0.16)
+    s.add_sphere([-0.12, -0.28, 1.05], 0.13)
+    return s

@@ -1,0 +1,142 @@
+"""CPU-only checks: the C-ABI library loads and exports every declared entry point, the
+host-side codec tables and pose math are exact against the reference (no GPU calls)."""
+import ctypes as C
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1311_7194_b200 import _abi as A
+from paper_1311_7194_b200 import api as sf
+from tests import scenes
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "sf_gpu.h")).read()
+    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(sf_[a-z0-9_]+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = C.CDLL(A.LIB_PATH)
+    syms = declared_symbols()
+    assert len(syms) >= 30
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    # and the ctypes mirror covers them all
+    assert set(A.EXPORTED) <= set(syms) | {"sf_version"}
+
+
+def test_version_string():
+    assert A.product().version().decode().startswith("sf_gpu")
+
+
+def test_native_library_is_sm100a_only():
+    out = os.popen(f"cuobjdump --list-elf {A.LIB_PATH} 2>/dev/null").read()
+    if not out:
+        pytest.skip("cuobjdump unavailable")
+    arches = set(re.findall(r"sm_(\d+a?)", out))
+    assert arches == {"100a"}, arches
+
+
+def _lround(x):
+    # std::lround on a finite double (half away from zero), exact
+    r = math.floor(abs(x))
+    frac = abs(x) - r
+    v = r + (1 if frac >= 0.5 else 0)
+    return int(math.copysign(v, x)) if x != 0 else 0
+
+
+def _ref_encode_variance(v, p_min, p_max):
+    # AuxQuantization::encode, variance branch (grid.cpp:43-45)
+    c = min(max(v, p_min), p_max)
+    s = math.log(c / p_min) / math.log(p_max / p_min)
+    return _lround(s * 255.0) & 0xFF
+
+
+@pytest.mark.parametrize("p_min,p_max", [(1e-8, 1e-2), (1e-12, 1e-2), (1e-10, 1e-4)])
+def test_variance_threshold_encode_matches_log_encode(p_min, p_max):
+    lib = A.product()
+    aux = A.AuxQuantC(1, 20.0, p_min, p_max)
+    td = (C.c_double * 256)()
+    ad = (C.c_double * 256)()
+    th = (C.c_double * 256)()
+    assert lib.debug_aux_tables(C.byref(aux), 0.01, td, ad, th) == 0
+    thr = np.array(list(th))
+    assert np.all(np.diff(thr[1:]) > 0)
+    rng = np.random.default_rng(1)
+    vals = np.exp(rng.uniform(math.log(p_min) - 2, math.log(p_max) + 2, 20000))
+    # plus the thresholds themselves and their neighbours (the only places a code flips)
+    edge = np.concatenate([thr[1:], np.nextafter(thr[1:], 0), np.nextafter(thr[1:], 1)])
+    for v in np.concatenate([vals, edge]):
+        code = int(np.searchsorted(thr[1:], v, side="right"))
+        assert code == _ref_encode_variance(float(v), p_min, p_max), v
+
+
+def test_variance_codes_against_reference_write_voxel(ref):
+    """The threshold encode reproduces the reference's own encode through its public API."""
+    p_min, p_max = 1e-12, 1e-2
+    lib = A.product()
+    aux = A.AuxQuantC(1, 20.0, p_min, p_max)
+    td, ad, th = (C.c_double * 256)(), (C.c_double * 256)(), (C.c_double * 256)()
+    lib.debug_aux_tables(C.byref(aux), 0.01, td, ad, th)
+    thr = np.array(list(th))
+    cfg = sf.GridConfig(2, 8, (0, 0, 0), 1.0, 0.0)
+    g = sf.SparseTsdfGrid(cfg, 8, sf.AuxMode.Variance, p_min=p_min, p_max=p_max, backend=ref)
+    g.allocate_block([0, 0, 0])
+    rng = np.random.default_rng(7)
+    vals = np.concatenate([np.exp(rng.uniform(math.log(p_min) - 1, math.log(p_max) + 1, 400)),
+                           thr[1:], np.nextafter(thr[1:], 0)])
+    for i, v in enumerate(vals):
+        g.write_voxel([i % 8, (i // 8) % 8, 0], 0.0, float(v))
+        code = int(g.read_payload(0, 1)[(i // 8 % 8) * 8 + i % 8]) >> 8
+        assert code == int(np.searchsorted(thr[1:], v, side="right")), v
+        # decode table == reference decode
+        assert g.read_voxel([i % 8, (i // 8) % 8, 0])[1] == ad[code]
+
+
+def test_pose_math_bit_exact(ref):
+    rng = np.random.default_rng(3)
+    lib = ref.lib
+    for _ in range(50):
+        q = rng.normal(size=4)
+        q /= np.linalg.norm(q)
+        w, x, y, z = q
+        R = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                      [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                      [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+        a = sf.Pose(R, rng.normal(size=3))
+        b = sf.Pose(R.T, rng.normal(size=3))
+        out = (C.c_double * 12)()
+        a12, b12 = a.to12(), b.to12()
+        lib.compose(a12.ctypes.data_as(A.c_double_p), b12.ctypes.data_as(A.c_double_p), out)
+        assert np.array_equal(sf.compose(a, b).to12(), np.array(list(out)))
+        lib.invert(a12.ctypes.data_as(A.c_double_p), out)
+        assert np.array_equal(sf.invert(a).to12(), np.array(list(out)))
+
+
+@pytest.mark.parametrize("frames,arc", [(100, math.pi / 2), (8, 2 * math.pi), (1, 1.0)])
+def test_orbit_trajectory_bit_exact(ref, frames, arc):
+    poses = sf.orbit_trajectory([0.0, 0.0, 1.3], 1.3, frames, (0.0, 1.0, 0.0), math.pi / 4, arc)
+    out = np.zeros(12 * frames)
+    tgt = np.array([0.0, 0.0, 1.3])
+    ax = np.array([0.0, 1.0, 0.0])
+    ref.lib.orbit_trajectory(tgt.ctypes.data_as(A.c_double_p), 1.3, frames, ax.ctypes.data_as(A.c_double_p),
+                             math.pi / 4, arc, out.ctypes.data_as(A.c_double_p))
+    for k, p in enumerate(poses):
+        assert np.array_equal(p.to12(), out[12 * k: 12 * k + 12])
+
+
+def test_reference_wrapper_fuses_on_cpu(ref):
+    intr = scenes.camera(160, 120, 131.25)
+    scene = scenes.sphere_plane_scene()
+    pose = scenes.c1_trajectory(4)[0]
+    frame = ref.render_synthetic_depth(scene, pose, intr, domain_size=2.0)
+    g = sf.SparseTsdfGrid(scenes.c1_config(), 0, sf.AuxMode.Variance, backend=ref)
+    st = ref.fuse_frame(g, frame, pose, sf.FusionParams(mode=sf.FusionMode.Kalman))
+    assert st.blocks_total > 20 and st.voxels_updated > 1000
+    assert st.memory_bytes == 2 * st.blocks_total * 512 + 4 * 32 ** 3
+    assert ref.lib.volume_check_consistency(g.handle) == 0

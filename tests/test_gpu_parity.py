@@ -1,0 +1,359 @@
+"""GPU parity: the CUDA path against the UNMODIFIED reference (oracle/_ref) on identical
+inputs. Integer / byte outputs (offset table, payload codes, block lists, free list) must
+be bit-exact; raycast depth/normals and bounds are bit-exact too (FP64, same order);
+ICP pose within 1e-6 (north star)."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_1311_7194_b200 import api as sf
+from tests import scenes
+
+pytestmark = pytest.mark.gpu
+
+
+def grids(gpu, ref, cfg, cap, aux_mode, **kw):
+    return (sf.SparseTsdfGrid(cfg, cap, aux_mode, backend=gpu, **kw),
+            sf.SparseTsdfGrid(cfg, cap, aux_mode, backend=ref, **kw))
+
+
+def assert_same_volume(a, b):
+    ta, tb = a.read_table(), b.read_table()
+    assert np.array_equal(ta, tb), f"table differs at {np.flatnonzero(ta != tb)[:10]}"
+    pa, pb = a.read_payload(), b.read_payload()
+    diff = np.flatnonzero(pa != pb)
+    assert diff.size == 0, f"{diff.size} payload codes differ, first {diff[:8]} gpu={pa[diff[:8]]} ref={pb[diff[:8]]}"
+    assert a.allocated_count == b.allocated_count
+
+
+def frames_for(ref, scene, poses, intr, domain, sigma0=0.0):
+    return [ref.render_synthetic_depth(scene, p, intr, sigma0=sigma0, seed=1000 + k, domain_size=domain)
+            for k, p in enumerate(poses)]
+
+
+# ---------------------------------------------------------------------------------
+# input side
+# ---------------------------------------------------------------------------------
+@pytest.mark.parametrize("sigma0", [0.0, 2.5e-4])
+def test_synthetic_depth_bit_exact(gpu, ref, sigma0):
+    intr = scenes.camera(320, 240, 262.5)
+    scene = scenes.sphere_plane_scene()
+    scene.add_box([0.3, -0.2, 1.0], [0.1, 0.05, 0.08])
+    pose = scenes.c1_trajectory(10)[3]
+    a = gpu.render_synthetic_depth(scene, pose, intr, sigma0=sigma0, seed=77, domain_size=2.0)
+    b = ref.render_synthetic_depth(scene, pose, intr, sigma0=sigma0, seed=77, domain_size=2.0)
+    assert np.array_equal(a.depth, b.depth)
+    if sigma0 > 0:
+        assert np.array_equal(a.sigma, b.sigma)
+    assert (a.depth > 0).mean() > 0.5
+
+
+@pytest.mark.parametrize("spatial", [0.0, 0.0078125])
+def test_compute_normals_bit_exact(gpu, ref, spatial):
+    intr = scenes.camera(320, 240, 262.5)
+    pose = scenes.c1_trajectory(10)[5]
+    f = ref.render_synthetic_depth(scenes.sphere_plane_scene(), pose, intr, sigma0=2.5e-4, seed=3, domain_size=2.0)
+    a = gpu.compute_normals(f, 2.5e-4, spatial).array
+    b = ref.compute_normals(f, 2.5e-4, spatial).array
+    assert np.array_equal(a, b)
+    assert (np.abs(a).sum(-1) > 0).mean() > 0.3
+
+
+# ---------------------------------------------------------------------------------
+# fuse_frame
+# ---------------------------------------------------------------------------------
+@pytest.mark.parametrize("mode", [sf.FusionMode.Kalman, sf.FusionMode.Weighted, sf.FusionMode.Simple])
+def test_fuse_sequence_bit_exact_c1(gpu, ref, mode):
+    """C1 (256^3, N=32, M=8): table, slots and every payload code equal after every frame."""
+    intr = scenes.camera(320, 240, 262.5)
+    poses = scenes.c1_trajectory(100)[::12]
+    frames = frames_for(ref, scenes.sphere_plane_scene(), poses, intr, 2.0)
+    aux = sf.AuxMode.Variance if mode == sf.FusionMode.Kalman else sf.AuxMode.Weight
+    g, r = grids(gpu, ref, scenes.c1_config(), 0, aux)
+    params = sf.FusionParams(mode=mode)
+    for f, p in zip(frames, poses):
+        sg = gpu.fuse_frame(g, f, p, params)
+        sr = ref.fuse_frame(r, f, p, params)
+        assert sg == sr
+        assert_same_volume(g, r)
+    assert sr.blocks_total > 200 and sr.voxels_updated > 10000
+
+
+def test_fuse_full_resolution_noisy_kalman(gpu, ref):
+    """640x480 noisy frames with a sigma plane, Kalman, edge down-weighting on."""
+    intr = scenes.camera()
+    poses = scenes.c1_trajectory(100)[::33]
+    frames = frames_for(ref, scenes.sphere_plane_scene(), poses, intr, 2.0, sigma0=2.5e-4)
+    g, r = grids(gpu, ref, scenes.c1_config(), 0, sf.AuxMode.Variance)
+    params = sf.FusionParams(mode=sf.FusionMode.Kalman, sigma0=2.5e-4)
+    for f, p in zip(frames, poses):
+        assert gpu.fuse_frame(g, f, p, params) == ref.fuse_frame(r, f, p, params)
+        assert_same_volume(g, r)
+
+
+def test_fuse_m4_exact_500(gpu, ref):
+    """C2 geometry: N=125, M=4 (500^3), stride 2 sampling."""
+    intr = scenes.camera(320, 240, 262.5)
+    poses = scenes.c1_trajectory(100)[::40]
+    frames = frames_for(ref, scenes.sphere_plane_scene(), poses, intr, 2.0)
+    g, r = grids(gpu, ref, scenes.c2_config(), 200000, sf.AuxMode.Variance)
+    params = sf.FusionParams(mode=sf.FusionMode.Kalman)
+    for f, p in zip(frames, poses):
+        assert gpu.fuse_frame(g, f, p, params) == ref.fuse_frame(r, f, p, params)
+        assert_same_volume(g, r)
+
+
+def test_select_update_blocks_lists(gpu, ref):
+    intr = scenes.camera(320, 240, 262.5)
+    poses = scenes.c1_trajectory(100)
+    scene = scenes.sphere_plane_scene()
+    g, r = grids(gpu, ref, scenes.c1_config(), 0, sf.AuxMode.Weight)
+    params = sf.FusionParams()
+    for k in (0, 20, 40):
+        f = ref.render_synthetic_depth(scene, poses[k], intr, domain_size=2.0)
+        ga, gu = gpu.select_update_blocks(g, f, poses[k])
+        ra, ru = ref.select_update_blocks(r, f, poses[k])
+        assert np.array_equal(ga, ra)
+        assert np.array_equal(gu, ru)
+        gpu.fuse_frame(g, f, poses[k], params)
+        ref.fuse_frame(r, f, poses[k], params)
+    assert len(ru) > 0
+
+
+def test_float_payload_matches_reference_shadow(gpu, ref):
+    """Float payload mode == FloatShadowGrid semantics (grid.hpp:77-88, fusion.cpp:313-318)."""
+    cfg = sf.GridConfig(16, 8, (-1.0, -1.0, 0.25), 2.0, 0.0)  # 128^3: shadow limit
+    intr = scenes.camera(320, 240, 262.5)
+    poses = scenes.c1_trajectory(100)[::25]
+    frames = frames_for(ref, scenes.sphere_plane_scene(), poses, intr, 2.0, sigma0=2.5e-4)
+    g, r = grids(gpu, ref, cfg, 0, sf.AuxMode.Variance)
+    g.enable_float_payload()
+    assert ref.lib.volume_enable_shadow(r.handle) == 0
+    params = sf.FusionParams(mode=sf.FusionMode.Kalman)
+    for f, p in zip(frames, poses):
+        assert gpu.fuse_frame(g, f, p, params) == ref.fuse_frame(r, f, p, params)
+    assert_same_volume(g, r)
+    res = 128
+    st = np.zeros(res ** 3, np.float32)
+    sa = np.zeros(res ** 3, np.float32)
+    import ctypes as C
+    ref.lib.volume_read_shadow(r.handle, st.ctypes.data_as(C.POINTER(C.c_float)),
+                               sa.ctypes.data_as(C.POINTER(C.c_float)))
+    fp = g.read_float_payload()
+    table = g.read_table()
+    n, m = 16, 8
+    compared = 0
+    for ti in np.flatnonzero(table >= 0):
+        slot = table[ti]
+        bx, by, bz = ti % n, (ti // n) % n, ti // (n * n)
+        blk = fp[slot * 512:(slot + 1) * 512].reshape(m, m, m, 2)  # z, y, x
+        dense_t = st.reshape(res, res, res)[bz * m:(bz + 1) * m, by * m:(by + 1) * m, bx * m:(bx + 1) * m]
+        dense_a = sa.reshape(res, res, res)[bz * m:(bz + 1) * m, by * m:(by + 1) * m, bx * m:(bx + 1) * m]
+        assert np.array_equal(blk[..., 0], dense_t)
+        assert np.array_equal(blk[..., 1], dense_a)
+        compared += 1
+    assert compared > 50
+
+
+def test_pool_exhaustion_partial_state(gpu, ref):
+    """PoolExhausted mid-list: the allocate-list prefix is integrated, nothing else (fusion.cpp:369)."""
+    intr = scenes.camera(320, 240, 262.5)
+    pose = scenes.c1_trajectory(100)[10]
+    f = ref.render_synthetic_depth(scenes.sphere_plane_scene(), pose, intr, domain_size=2.0)
+    g, r = grids(gpu, ref, scenes.c1_config(), 150, sf.AuxMode.Weight)
+    params = sf.FusionParams()
+    with pytest.raises(sf.PoolExhausted):
+        ref.fuse_frame(r, f, pose, params)
+    with pytest.raises(sf.PoolExhausted):
+        gpu.fuse_frame(g, f, pose, params)
+    assert r.allocated_count == 150
+    assert_same_volume(g, r)
+
+
+def test_grid_api_parity(gpu, ref):
+    cfg = sf.GridConfig(8, 4, (0, 0, 0), 1.0, 0.0)
+    g, r = grids(gpu, ref, cfg, 20, sf.AuxMode.Weight)
+    rng = np.random.default_rng(5)
+    for _ in range(300):
+        bc = rng.integers(0, 8, 3)
+        op = rng.integers(0, 3)
+        if op == 0:
+            try:
+                a = r.allocate_block(bc)
+            except sf.PoolExhausted:
+                with pytest.raises(sf.PoolExhausted):
+                    g.allocate_block(bc)
+                continue
+            assert g.allocate_block(bc) == a
+        elif op == 1:
+            r.free_block(bc)
+            g.free_block(bc)
+        else:
+            vc = bc * 4 + rng.integers(0, 4, 3)
+            t = float(rng.uniform(-0.6, 0.6)) * r.delta
+            aux = float(rng.uniform(0, 25))
+            try:
+                r.write_voxel(vc, t, aux)
+            except RuntimeError:
+                with pytest.raises(RuntimeError):
+                    g.write_voxel(vc, t, aux)
+                continue
+            g.write_voxel(vc, t, aux)
+    assert_same_volume(g, r)
+    with pytest.raises(IndexError):
+        g.allocate_block([8, 0, 0])
+
+
+def test_snapshot_roundtrip_cross_implementation(gpu, ref, tmp_path):
+    intr = scenes.camera(320, 240, 262.5)
+    pose = scenes.c1_trajectory(100)[30]
+    f = ref.render_synthetic_depth(scenes.sphere_plane_scene(), pose, intr, domain_size=2.0)
+    g, r = grids(gpu, ref, scenes.c1_config(), 0, sf.AuxMode.Weight)
+    gpu.fuse_frame(g, f, pose, sf.FusionParams())
+    ref.fuse_frame(r, f, pose, sf.FusionParams())
+    pg, pr = str(tmp_path / "g.stsg"), str(tmp_path / "r.stsg")
+    g.save_snapshot(pg)
+    r.save_snapshot(pr)
+    assert open(pg, "rb").read() == open(pr, "rb").read()
+    g2 = sf.SparseTsdfGrid.load_snapshot(pr, backend=gpu)
+    r2 = sf.SparseTsdfGrid.load_snapshot(pr, backend=ref)
+    assert_same_volume(g2, r2)
+
+
+# ---------------------------------------------------------------------------------
+# raycast
+# ---------------------------------------------------------------------------------
+def fused_pair(gpu, ref, cfg, intr, poses, scene, domain, mode=sf.FusionMode.Weighted, cap=0):
+    aux = sf.AuxMode.Variance if mode == sf.FusionMode.Kalman else sf.AuxMode.Weight
+    g, r = grids(gpu, ref, cfg, cap, aux)
+    params = sf.FusionParams(mode=mode)
+    for k, p in enumerate(poses):
+        f = ref.render_synthetic_depth(scene, p, intr, domain_size=domain)
+        gpu.fuse_frame(g, f, p, params)
+        ref.fuse_frame(r, f, p, params)
+    assert_same_volume(g, r)
+    return g, r
+
+
+def test_ray_bounds_and_raycast_bit_exact(gpu, ref):
+    intr = scenes.camera(320, 240, 262.5)
+    poses = scenes.c1_trajectory(100)
+    g, r = fused_pair(gpu, ref, scenes.c1_config(), intr, poses[::20], scenes.sphere_plane_scene(), 2.0)
+    for p in (poses[10], poses[55]):
+        gs, ge = gpu.compute_ray_bounds(g, p, intr)
+        rs, re_ = ref.compute_ray_bounds(r, p, intr)
+        assert np.array_equal(gs, rs) and np.array_equal(ge, re_)
+        gd, gn, gst = gpu.raycast_result(g, p, intr)
+        rd, rn, rst = ref.raycast_result(r, p, intr)
+        assert gst == rst
+        assert np.array_equal(gd.depth, rd.depth)
+        assert np.array_equal(gn.array, rn.array)
+        assert rst.hit_pixels > 10000
+
+
+def test_raycast_m4_kalman(gpu, ref):
+    intr = scenes.camera(320, 240, 262.5)
+    poses = scenes.c1_trajectory(100)
+    g, r = fused_pair(gpu, ref, scenes.c2_config(), intr, poses[::30], scenes.sphere_plane_scene(), 2.0,
+                      sf.FusionMode.Kalman, cap=200000)
+    gd, gn, gst = gpu.raycast_result(g, poses[45], intr)
+    rd, rn, rst = ref.raycast_result(r, poses[45], intr)
+    assert gst == rst
+    assert np.array_equal(gd.depth, rd.depth) and np.array_equal(gn.array, rn.array)
+
+
+# ---------------------------------------------------------------------------------
+# ICP
+# ---------------------------------------------------------------------------------
+def pose_diff(a: sf.Pose, b: sf.Pose):
+    return max(np.abs(a.rotation - b.rotation).max(), np.abs(a.translation - b.translation).max())
+
+
+def test_icp_recovers_perturbation_like_reference(gpu, ref):
+    """test_smoke.py:102-130 scenario at 320x240."""
+    intr = scenes.camera(320, 240, 280.0)
+    scene = scenes.cluster_scene()
+    target_pose = sf.orbit_trajectory([0.0, 0.0, 1.3], 1.3, 8)[1]
+    ang = math.radians(2.0)
+    perturb = sf.Pose([[math.cos(ang), 0, math.sin(ang)], [0, 1, 0], [-math.sin(ang), 0, math.cos(ang)]],
+                      [0.01, -0.005, 0.008])
+    source_pose = sf.compose(target_pose, perturb)
+    target = ref.render_synthetic_depth(scene, target_pose, intr)
+    source = ref.render_synthetic_depth(scene, source_pose, intr)
+    tn = ref.compute_normals(target, 2.5e-4, 0.006)
+    params = sf.MatchParams.for_voxel_size(1.5 / 256.0)
+    a = gpu.icp(source, target, tn, sf.Pose.identity(), params)
+    b = ref.icp(source, target, tn, sf.Pose.identity(), params)
+    assert a.iterations == b.iterations
+    assert a.matches == b.matches
+    assert pose_diff(a.delta, b.delta) < 1e-6
+    assert a.gated_mask == b.gated_mask
+    np.testing.assert_allclose(a.eigenvalues, b.eigenvalues, rtol=1e-9)
+    truth = sf.compose(sf.invert(target_pose), source_pose)
+    assert pose_diff(a.delta, truth) < 1e-3
+
+
+def test_icp_against_raycast_model(gpu, ref):
+    """ICP of a captured frame against the raycast model, as run() does."""
+    intr = scenes.camera(320, 240, 262.5)
+    poses = scenes.c1_trajectory(100)
+    g, r = fused_pair(gpu, ref, scenes.c1_config(), intr, poses[:40:4], scenes.sphere_plane_scene(), 2.0)
+    cur = poses[40]
+    rd, rn, _ = ref.raycast(r, cur, intr)
+    captured = ref.render_synthetic_depth(scenes.sphere_plane_scene(), poses[41], intr, domain_size=2.0)
+    params = sf.MatchParams.for_voxel_size(2.0 / 256)
+    init = sf.compose(sf.invert(cur), cur)
+    a = gpu.icp(captured, rd, rn, init, params)
+    b = ref.icp(captured, rd, rn, init, params)
+    assert a.iterations == b.iterations and a.matches == b.matches
+    assert pose_diff(a.delta, b.delta) < 1e-6
+
+
+def test_icp_tracking_lost(gpu, ref):
+    intr = scenes.camera(64, 48, 55.0)
+    empty = sf.DepthFrame(intr, np.zeros((48, 64), np.float32))
+    nm = sf.NormalMap(np.zeros((48, 64, 3), np.float32))
+    with pytest.raises(sf.TrackingLost):
+        ref.icp(empty, empty, nm, sf.Pose.identity(), sf.MatchParams())
+    with pytest.raises(sf.TrackingLost):
+        gpu.icp(empty, empty, nm, sf.Pose.identity(), sf.MatchParams())
+
+
+# ---------------------------------------------------------------------------------
+# fused frame loop (run() body)
+# ---------------------------------------------------------------------------------
+def test_tracker_matches_reference_pipeline(gpu, ref):
+    """C2-style full loop (raycast -> ICP -> fuse) over a short sequence: poses within 1e-6,
+    volumes bit-exact."""
+    import ctypes as C
+    from paper_1311_7194_b200 import _abi as A
+
+    intr = scenes.camera(320, 240, 262.5)
+    poses = scenes.c1_trajectory(100)[:12]
+    scene = scenes.sphere_plane_scene()
+    frames = frames_for(ref, scene, poses, intr, 2.0)
+    cfg = scenes.c1_config()
+    fusion = sf.FusionParams(mode=sf.FusionMode.Kalman)
+    match = sf.MatchParams.for_voxel_size(cfg.voxel_size)
+    match.normal_sigma0 = 0.0
+    g, r = grids(gpu, ref, cfg, 0, sf.AuxMode.Variance)
+    tr = sf.Tracker(g, intr, fusion, match, poses[0])
+    cur = poses[0].to12().copy()
+    for k, f in enumerate(frames):
+        tr.step(f, sf.Tracker.TRACK)
+        m = tr.fetch()
+        st = A.FusionStatsC()
+        it = C.c_int32()
+        mt = C.c_uint64()
+        fc, ic, fp, mp = f.c(), intr.c(), fusion.c(), match.c()
+        assert ref.lib.pipeline_frame(r.handle, C.byref(fc), C.byref(ic), C.byref(fp), C.byref(mp),
+                                      0 if k > 0 else 1, cur.ctypes.data_as(A.c_double_p), C.byref(st),
+                                      C.byref(it), C.byref(mt)) == 0
+        assert m.status == 0
+        assert pose_diff(m.pose, sf.Pose.from12(cur)) < 1e-6
+        if k > 0:
+            assert m.iterations == it.value and m.matches == mt.value
+        assert m.fusion.blocks_total == st.blocks_total
+    assert_same_volume(g, r)
+    assert tr.last_launch_count() > 20
