@@ -1,0 +1,397 @@
+#!/usr/bin/env python3
+"""Fused-frame benchmark (BASELINE.json metric: fused depth frames/s and voxel updates/s at
+4096^3 sparse, % HBM roofline).
+
+Workload (the configuration the metric is quoted on): hand-scale bumpy
+sphere, 4096^3 sparse volume at 0.15 mm (N=512, M=8), 640x480 noisy synthetic depth
+(sigma0 = 4e-4, recorded sigma plane), Kalman fusion with p_min = 1e-12, full loop per
+frame: raycast(current pose) -> point-to-plane ICP -> fuse_frame. One "step" = one fused
+frame of the sequence.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Timing: per-step CUDA events on the launching stream, L2 flushed (400 MB write) between
+steps outside the timed events, max over ranks. `e2e` repeats the sequence through the
+public API with pinned HOST frames (H2D inside the step) and a metrics read-back per step.
+N > 1: independent replicas per GPU (weak scaling).
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0
+
+C4 = dict(N=512, M=8, voxel=0.15e-3, center=(0.0, 0.0, 0.35), r=0.08, bump=0.024, orbit_radius=0.35,
+          orbit_arc=0.3, frames=100, width=640, height=480, focal=525.0, sigma0=4e-4, p_min=1e-12,
+          pool=512 * 1024, max_distance=4e-3)
+
+
+def workload_config():
+    c = dict(C4)
+    side = c["N"] * c["M"] * c["voxel"]
+    c["box_side"] = side
+    c["box_origin"] = (c["center"][0] - side / 2, c["center"][1] - side / 2, c["center"][2] - side / 2)
+    return c
+
+
+def make_scene(sf, c):
+    s = sf.AnalyticScene()
+    s.add_sphere(list(c["center"]), c["r"])
+    o = c["r"] / math.sqrt(3.0)
+    for i in range(8):
+        s.add_sphere([c["center"][0] + (o if i & 1 else -o), c["center"][1] + (o if i & 2 else -o),
+                      c["center"][2] + (o if i & 4 else -o)], c["bump"])
+    return s
+
+
+def make_params(sf, c):
+    grid_cfg = sf.GridConfig(c["N"], c["M"], c["box_origin"], c["box_side"], 0.0)
+    intr = sf.Intrinsics.simple(c["width"], c["height"], c["focal"])
+    fusion = sf.FusionParams(mode=sf.FusionMode.Kalman, sigma0=c["sigma0"])
+    match = sf.MatchParams.for_voxel_size(grid_cfg.voxel_size)
+    match.max_distance = c["max_distance"]
+    match.normal_sigma0 = c["sigma0"]
+    return grid_cfg, intr, fusion, match
+
+
+def make_frames(sf, c, count, intr):
+    poses = sf.orbit_trajectory(list(c["center"]), c["orbit_radius"], c["frames"], (0.0, 1.0, 0.0), 0.0,
+                                c["orbit_arc"])[:count]
+    scene = make_scene(sf, c)
+    frames = [sf.render_synthetic_depth(scene, p, intr, sigma0=c["sigma0"], seed=1000 + k,
+                                        domain_size=c["box_side"]) for k, p in enumerate(poses)]
+    return poses, frames
+
+
+def hbm_peak():
+    try:
+        with open(MEASURED_PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+           0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+           0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=open(self.path, "w"),
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 3:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    mx = max(mx, float(parts[1]))
+                    bits = int(parts[2], 16)
+                except ValueError:
+                    continue
+                for b, name in REASONS.items():
+                    if bits & b and name != "gpu_idle":
+                        reasons.add(name)
+        except FileNotFoundError:
+            pass
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------------
+# reference (CPU) arm
+# ---------------------------------------------------------------------------------
+def reference_frames_per_s(sf, c, poses, frames, steps, warmup, budget_s):
+    """The unmodified reference (oracle/_ref) on the box's host cores, single-threaded as
+    shipped: frame 0 fused at its pose, then raycast -> icp -> fuse per frame."""
+    import ctypes as C
+
+    from paper_1311_7194_b200 import _abi as A
+    from tests import oracle_backends
+
+    ref = oracle_backends.reference()
+    if ref is None:
+        return None
+    grid_cfg, intr, fusion, match = make_params(sf, c)
+    g = sf.SparseTsdfGrid(grid_cfg, c["pool"], sf.AuxMode.Variance, p_min=c["p_min"], backend=ref)
+    cur = poses[0].to12().copy()
+    ic, fp, mp = intr.c(), fusion.c(), match.c()
+    times, vox = [], 0
+
+    def one(k, mode):
+        st = A.FusionStatsC()
+        it, mt = C.c_int32(), C.c_uint64()
+        fc = frames[k].c()
+        t0 = time.perf_counter()
+        rc = ref.lib.pipeline_frame(g.handle, C.byref(fc), C.byref(ic), C.byref(fp), C.byref(mp), mode,
+                                    cur.ctypes.data_as(A.c_double_p), C.byref(st), C.byref(it), C.byref(mt))
+        dt = time.perf_counter() - t0
+        if rc != 0:
+            raise RuntimeError("reference pipeline failed: " + ref.lib.error())
+        return dt, st.voxels_updated
+
+    one(0, 1)
+    start = time.perf_counter()
+    k = 1
+    for _ in range(warmup):
+        if time.perf_counter() - start > budget_s / 3:
+            break
+        one(k, 0)
+        k += 1
+    t_start = time.perf_counter()
+    while len(times) < steps and k < len(frames) and time.perf_counter() - t_start < budget_s:
+        dt, v = one(k, 0)
+        times.append(dt)
+        vox += v
+        k += 1
+    total = sum(times)
+    return {"frames_per_s": len(times) / total, "voxel_updates_per_s": vox / total, "frames": len(times),
+            "seconds": total, "first_frame": k - len(times)}
+
+
+# ---------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------
+def run_ours(args, world, rank, local):
+    import torch
+
+    import paper_1311_7194_b200 as sf
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = workload_config()
+    grid_cfg, intr, fusion, match = make_params(sf, c)
+    nframes = min(c["frames"], 1 + args.warmup + args.steps)
+    steps = nframes - 1 - args.warmup
+    poses, frames = make_frames(sf, c, nframes, intr)
+    dev = torch.device("cuda", local)
+    dframes = [sf.DepthFrame(intr, torch.from_numpy(f.depth).to(dev), torch.from_numpy(f.sigma).to(dev))
+               for f in frames]
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    flush = torch.empty(400 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    grid = sf.SparseTsdfGrid(grid_cfg, c["pool"], sf.AuxMode.Variance, p_min=c["p_min"], device=local)
+    tracker = sf.Tracker(grid, intr, fusion, match, poses[0])
+    tracker.step(dframes[0], sf.Tracker.TRACK, stream=sp)  # frame 0: fused at the first pose
+    for k in range(1, 1 + args.warmup):
+        tracker.step(dframes[k], sf.Tracker.TRACK, stream=sp)
+    m = tracker.fetch(stream=sp)
+    if m.status != 0:
+        raise RuntimeError(f"warm-up failed with status {m.status}")
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    stage, metrics = [], []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for i in range(steps):
+            k = 1 + args.warmup + i
+            flush.fill_(i & 0xFF)  # evict L2 (126 MB) between timed steps
+            ev0[i].record(stream)
+            tracker.step(dframes[k], sf.Tracker.TRACK, stream=sp)
+            ev1[i].record(stream)
+            metrics.append(tracker.fetch(stream=sp))  # synchronises (outside the events)
+            stage.append(tracker.stage_times())
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    step_ms = [ev0[i].elapsed_time(ev1[i]) for i in range(steps)]
+    total_ms = sum(step_ms)
+    launches_per_step = tracker.last_launch_count()
+    statuses = [mm.status for mm in metrics]
+    if any(statuses):
+        raise RuntimeError(f"tracking failed during the timed region: {statuses}")
+    vox_updated = sum(mm.fusion.voxels_updated for mm in metrics)
+    blocks = [mm.blocks_processed for mm in metrics]
+    # ground-truth tracking error of the last frame (sanity, not a parity claim)
+    gt = poses[nframes - 1]
+    pose_err = float(max(np.abs(metrics[-1].pose.rotation - gt.rotation).max(),
+                         np.abs(metrics[-1].pose.translation - gt.translation).max()))
+
+    # integrate kernel roofline: algorithmic bytes per launch / its event time
+    m3 = c["M"] ** 3
+    px = c["width"] * c["height"]
+    integ_ms = [s[3] for s in stage]
+    integ_bytes = [b * (m3 * 4 + 8) + px * (4 + 8 + 1) for b in blocks]
+    achieved = sum(integ_bytes) / (sum(integ_ms) * 1e-3) / 1e9
+    peak, peak_kind = hbm_peak()
+
+    # e2e: fresh volume, pinned HOST frames, H2D inside the step + metrics read-back
+    grid2 = sf.SparseTsdfGrid(grid_cfg, c["pool"], sf.AuxMode.Variance, p_min=c["p_min"], device=local)
+    tr2 = sf.Tracker(grid2, intr, fusion, match, poses[0])
+    pinned = []
+    for f in frames:
+        d = torch.from_numpy(f.depth).pin_memory()
+        s = torch.from_numpy(f.sigma).pin_memory()
+        pinned.append((sf.DepthFrame(intr, d.numpy(), s.numpy()), d, s))
+    for k in range(0, 1 + args.warmup):
+        tr2.step(pinned[k][0], sf.Tracker.TRACK, stream=sp)
+    tr2.fetch(stream=sp)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(steps):
+        tr2.step(pinned[1 + args.warmup + i][0], sf.Tracker.TRACK, stream=sp)
+        tr2.fetch(stream=sp)
+    e2e_s = time.perf_counter() - t0
+    h2d, d2h = tr2.io_bytes(True)
+
+    times = torch.tensor([total_ms, e2e_s * 1e3], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(times, op=dist.ReduceOp.MAX)
+    total_ms, e2e_ms = times.tolist()
+    value = world * steps / (total_ms * 1e-3)
+    result = {
+        "metric": "fused depth frames/s (raycast+ICP+integrate, 640x480) at 4096^3 sparse",
+        "value": value,
+        "unit": "frames/s",
+        "n_gpus": world,
+        "steps": steps,
+        "warmup": args.warmup,
+        "ms_per_step": total_ms / steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (GPU sphere-traced bumpy sphere, sigma0=4e-4 noise + sigma plane)",
+        "config": {
+            "workload": "C4: hand-scale bumpy sphere, 4096^3 sparse @ 0.15 mm (N=512, M=8), 640x480, "
+                        "Kalman (p_min 1e-12), full loop raycast->ICP->fuse per frame",
+            "blocks_per_axis": c["N"], "voxels_per_block_axis": c["M"], "voxel_m": c["voxel"],
+            "pool_capacity": c["pool"], "frames": nframes, "orbit_arc_rad": c["orbit_arc"],
+            "l2": "flushed (400 MB write) between timed steps", "parallelism": f"replicas x{world}",
+        },
+        "voxel_updates_per_s": world * vox_updated / (total_ms * 1e-3),
+        "stage_ms_mean": dict(zip(["raycast", "icp", "fuse_prologue", "integrate", "total"],
+                                  [sum(s[j] for s in stage) / steps for j in range(5)])),
+        "blocks_processed_mean": sum(blocks) / steps,
+        "icp_iterations_mean": sum(mm.iterations for mm in metrics) / steps,
+        "tracking_error_last_frame": pose_err,
+        "roofline": {"bound": "hbm", "kernel": "k_integrate<Kalman>", "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "bytes_per_launch_mean": sum(integ_bytes) / steps,
+                     "ms_per_launch_mean": sum(integ_ms) / steps},
+        "e2e": {"value": world * steps / (e2e_ms * 1e-3), "unit": "frames/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches_per_step * steps,
+        "clocks": clocks.summary(),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = reference_frames_per_s(sf, c, poses, frames, steps=3, warmup=0, budget_s=25.0)
+        if cpu:
+            result["cpu_baseline"] = {"value": cpu["frames_per_s"], "unit": "frames/s", "cores": 1,
+                                      "kind": "reference",
+                                      "sample": f"{cpu['frames']} fused frames (frames {cpu['first_frame']}.."
+                                                f"{cpu['first_frame'] + cpu['frames'] - 1} of the same C4 "
+                                                f"sequence), {cpu['seconds']:.1f} s, single thread",
+                                      "voxel_updates_per_s": cpu["voxel_updates_per_s"]}
+    if rank == 0:
+        print(json.dumps(result))
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_reference(args, world, rank, local):
+    if rank != 0:
+        return
+    import paper_1311_7194_b200 as sf
+
+    c = workload_config()
+    grid_cfg, intr, fusion, match = make_params(sf, c)
+    nframes = min(c["frames"], 1 + args.warmup + args.steps)
+    poses, frames = make_frames(sf, c, nframes, intr)
+    budget = float(os.environ.get("SF_REFERENCE_BUDGET_S", "150"))
+    r = reference_frames_per_s(sf, c, poses, frames, steps=args.steps, warmup=min(args.warmup, 1), budget_s=budget)
+    if r is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libsfref.so not built"}))
+        return
+    nthreads = 1
+    out = {
+        "impl": "reference",
+        "metric": "fused depth frames/s (raycast+ICP+integrate, 640x480) at 4096^3 sparse",
+        "value": r["frames_per_s"],
+        "unit": "frames/s",
+        "n_gpus": world,
+        "steps": r["frames"],
+        "warmup": min(args.warmup, 1),
+        "ms_per_step": 1e3 / r["frames_per_s"],
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (same frames as the GPU arm)",
+        "config": {"workload": "C4 (see our arm); reference CPU path, single-threaded as shipped",
+                   "requested_steps": args.steps},
+        "voxel_updates_per_s": r["voxel_updates_per_s"],
+        "cpu_baseline": {"value": r["frames_per_s"], "unit": "frames/s", "cores": nthreads, "kind": "reference",
+                         "sample": f"{r['frames']} fused frames in {r['seconds']:.1f} s (time-bounded)"},
+        "e2e": {"value": r["frames_per_s"], "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank, local)
+    else:
+        run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -258,6 +258,8 @@ typedef struct {
     int32_t gated_mask[6];
     sf_fusion_stats fusion;
     sf_raycast_stats raycast;
+    uint64_t blocks_processed; /* allocate-list prefix + update list integrated this frame */
+    uint64_t voxels_visited;   /* blocks_processed * M^3 */
 } sf_frame_metrics;
 
 int sf_tracker_create(sf_volume_t vol, const sf_tracker_config* config, const double initial_pose[12],
@@ -269,11 +271,19 @@ int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, con
                     void* stream);
 /* Synchronises `stream` and copies the metrics of the last step. */
 int sf_tracker_fetch(sf_tracker_t tr, sf_frame_metrics* out, void* stream);
-/* Device pointer to the tracker's pose (12 doubles) and to the last step's kernel count. */
+/* Device-timed stages of the last step, in ms (CUDA events recorded inside the step /
+ * graph): [0] raycast (bounds + march), [1] ICP (source normals + all iterations),
+ * [2] fuse prologue (frame prep, keys, sort/unique, allocation, visibility),
+ * [3] the per-voxel integrate kernel, [4] whole step. Call after sf_tracker_fetch. */
+int sf_tracker_stage_times(sf_tracker_t tr, float ms[5]);
+/* Device pointer to the tracker's pose (12 doubles). */
 int sf_tracker_device_pose(sf_tracker_t tr, const double** device_pose);
 /* Number of this library's kernels launched by the last sf_tracker_step (excl. graphs
  * replay bookkeeping): the bench's gpu_launches figure. */
 int sf_tracker_last_launch_count(sf_tracker_t tr, uint64_t* count);
+/* Bytes one step moves across PCIe when the frame is a host frame (depth [+ sigma]) and
+ * bytes sf_tracker_fetch reads back. */
+int sf_tracker_io_bytes(sf_tracker_t tr, int32_t has_sigma, uint64_t* h2d, uint64_t* d2h);
 
 /* ---- synthetic input (scene.hpp:69-79, scene.cpp:101-177) --------------------------- */
 /* Analytic scene of spheres (cx,cy,cz,r), planes (nx,ny,nz,offset; normalised as

@@ -152,6 +152,8 @@ class FrameMetricsC(C.Structure):
         ("gated_mask", C.c_int32 * 6),
         ("fusion", FusionStatsC),
         ("raycast", RaycastStatsC),
+        ("blocks_processed", C.c_uint64),
+        ("voxels_visited", C.c_uint64),
     ]
 
 
@@ -212,6 +214,8 @@ PRODUCT_ONLY = {
     "tracker_fetch": (C.c_int, [vp, P(FrameMetricsC), vp]),
     "tracker_device_pose": (C.c_int, [vp, P(c_double_p)]),
     "tracker_last_launch_count": (C.c_int, [vp, u64p]),
+    "tracker_stage_times": (C.c_int, [vp, P(C.c_float)]),
+    "tracker_io_bytes": (C.c_int, [vp, i32, u64p, u64p]),
     "debug_aux_tables": (C.c_int, [P(AuxQuantC), C.c_double, c_double_p, c_double_p, c_double_p]),
 }
 

@@ -672,6 +672,8 @@ class FrameMetrics:
     gated_mask: List[bool]
     fusion: FusionStats
     raycast: RaycastStats
+    blocks_processed: int = 0
+    voxels_visited: int = 0
 
 
 class Tracker:
@@ -714,7 +716,20 @@ class Tracker:
         return FrameMetrics(m.frame, bool(m.registered), m.status, Pose.from12(list(m.pose)), m.iterations,
                             m.matches, m.residual_rms, list(m.lambda_over_n), [bool(x) for x in m.gated_mask],
                             FusionStats(f.voxels_updated, f.blocks_allocated_now, f.blocks_total, f.memory_bytes),
-                            RaycastStats(r.sample_steps, r.hit_pixels, r.rays_with_bounds))
+                            RaycastStats(r.sample_steps, r.hit_pixels, r.rays_with_bounds),
+                            m.blocks_processed, m.voxels_visited)
+
+    def stage_times(self):
+        """Device-timed stages of the last step (ms): raycast, icp, fuse prologue, integrate, total."""
+        ms = (C.c_float * 5)()
+        self.grid.backend.check(self._lib.tracker_stage_times(self.handle, ms))
+        return list(ms)
+
+    def io_bytes(self, has_sigma: bool):
+        """(h2d, d2h) bytes of one host-frame step + fetch."""
+        a, b = C.c_uint64(), C.c_uint64()
+        self._lib.tracker_io_bytes(self.handle, 1 if has_sigma else 0, C.byref(a), C.byref(b))
+        return a.value, b.value
 
     def last_launch_count(self) -> int:
         c = C.c_uint64()

@@ -1,7 +1,7 @@
 // sf_fusion.cu — fuse_frame on the device (fusion.cpp:25-376, grid.cpp:174-269).
 //
 // Per frame (all launches asynchronous, no host round trip):
-//   k_frame_setup      1 thread: camera_from_world, frustum SAT axes + intervals   (grid.cpp:228-259)
+//   k_frame_consts     1 thread: camera_from_world, frustum SAT axes + intervals   (grid.cpp:228-259)
 //   k_normals          compute_normals with the fusion options                     (camera.cpp:44-76, fusion.cpp:33-36)
 //   k_edge             depth-edge mask                                              (fusion.cpp:40-62)
 //   k_pixel_meas       5x5 near-edge dilation + every per-pixel factor of the
@@ -587,7 +587,8 @@ FuseParams resolve_fuse_params(const Volume& v, const sf_fusion_params& p, bool 
 }
 
 void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* depth, const float* sigma,
-                 const FuseParams& fp, cudaStream_t s, bool export_only, uint64_t* launches, const int* dead_flag) {
+                 const FuseParams& fp, cudaStream_t s, bool export_only, uint64_t* launches, const int* dead_flag,
+                 const FuseEvents* events) {
     const int w = fb.w, h = fb.h;
     const VolParams& P = v.P;
     uint64_t n = 0;
@@ -650,6 +651,7 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
                                                                fb.pix_var, fb.pix_w, fb.pix_ok, v.d_payload,        \
                                                                v.d_fpayload, vu)
         const bool fpl = v.d_fpayload != nullptr;
+        if (events && events->before_integrate) record_event(events->before_integrate, s);
         if (fp.mode == 0) {
             if (fpl) SF_INTEGRATE(0, true);
             else SF_INTEGRATE(0, false);
@@ -662,6 +664,7 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
         }
 #undef SF_INTEGRATE
         SF_LAUNCH_CHECK();
+        if (events && events->after_integrate) record_event(events->after_integrate, s);
         k_fuse_finalize<<<1, 1, 0, s>>>(fb.ctr, v.d_vc);
         SF_LAUNCH_CHECK();
         n += 2;

@@ -28,6 +28,14 @@ void set_last_error(const std::string& msg);
     } while (0)
 #define SF_LAUNCH_CHECK() SF_CUDA(cudaGetLastError())
 
+// Timing event usable both eagerly and under stream capture (as an event-record node).
+inline void record_event(cudaEvent_t ev, cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    SF_CUDA(cudaStreamIsCapturing(s, &st));
+    if (st == cudaStreamCaptureStatusActive) SF_CUDA(cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal));
+    else SF_CUDA(cudaEventRecord(ev, s));
+}
+
 template <typename F>
 int guarded(F&& f) {
     try {
@@ -141,9 +149,12 @@ struct RayCounters {
 void launch_consts(const VolParams& P, const Intr& intr, const double* d_pose, FrameConsts* d_fc, cudaStream_t s,
                    uint64_t* launches);
 // fuse_frame at the pose in fb.pose (device)
+struct FuseEvents {
+    cudaEvent_t before_integrate = nullptr, after_integrate = nullptr;
+};
 void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* depth, const float* sigma,
                  const FuseParams& fp, cudaStream_t s, bool export_lists_only, uint64_t* launches,
-                 const int* dead_flag);
+                 const int* dead_flag, const FuseEvents* events = nullptr);
 void launch_ray_bounds(Volume& v, const FrameConsts* d_fc, const Intr& intr, float* t_start, float* t_end,
                        cudaStream_t s, uint64_t* launches, const int* dead_flag);
 void launch_raycast(Volume& v, const FrameConsts* d_fc, const Intr& intr, const float* t_start, const float* t_end,

@@ -99,6 +99,8 @@ struct sf_tracker {
     int last_mode = 0;
     bool last_registered = false;
     uint64_t last_launches = 0;
+    cudaStream_t capture_stream = nullptr;  // graphs are captured here (the legacy stream cannot capture)
+    cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // stage timing (graph nodes)
     cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [mode][has_sigma]
     uint64_t graph_kernels[2][2] = {{0, 0}, {0, 0}};
     // pinned fetch staging
@@ -121,6 +123,9 @@ struct sf_tracker {
         for (void* q : p)
             if (q) cudaFree(q);
         if (h) cudaFreeHost(h);
+        if (capture_stream) cudaStreamDestroy(capture_stream);
+        for (auto e : ev)
+            if (e) cudaEventDestroy(e);
     }
 
     // The frame's launch sequence (captured into a graph or issued directly).
@@ -129,6 +134,7 @@ struct sf_tracker {
         const int* dead = &d_td->dead;
         const FuseParams& p = has_sigma ? fp_sigma : fp;
         const float* sig = has_sigma ? d_cap_sigma : nullptr;
+        record_event(ev[0], s);
         if (mode == 0) {
             k_tracker_begin_track<<<1, 1, 0, s>>>(d_cur, d_init_delta, d_rstats, d_td);
             SF_LAUNCH_CHECK();
@@ -136,6 +142,7 @@ struct sf_tracker {
             launch_consts(vol->P, cam, d_cur, d_rc_fc, s, &n);
             launch_ray_bounds(*vol, d_rc_fc, cam, d_ts, d_te, s, &n, dead);
             launch_raycast(*vol, d_rc_fc, cam, d_ts, d_te, d_model_depth, d_model_normals, d_rstats, s, &n, dead);
+            record_event(ev[1], s);
             launch_compute_normals(d_cap, cam.w, cam.h, cam, cfg.match.normal_sigma0, cfg.match.normal_spatial_scale,
                                    icp.src_normals, s, &n, dead);
             launch_icp(icp, d_cap, icp.src_normals, d_model_depth, d_model_normals, cam, cam, d_init_delta, icp_prm, s,
@@ -143,15 +150,22 @@ struct sf_tracker {
             k_tracker_after_icp<<<1, 1, 0, s>>>(d_cur, fb.pose, icp.st, d_td);
             SF_LAUNCH_CHECK();
             ++n;
+            record_event(ev[2], s);
         } else {
             k_tracker_begin_gt<<<1, 1, 0, s>>>(d_gt, d_cur, fb.pose, d_rstats, d_td, mode == 1 ? 1 : 0);
             SF_LAUNCH_CHECK();
             ++n;
+            record_event(ev[1], s);
+            record_event(ev[2], s);
         }
-        launch_fuse(*vol, fb, cam, d_cap, sig, p, s, false, &n, dead);
+        FuseEvents fe;
+        fe.before_integrate = ev[3];
+        fe.after_integrate = ev[4];
+        launch_fuse(*vol, fb, cam, d_cap, sig, p, s, false, &n, dead, &fe);
         k_tracker_finish<<<1, 1, 0, s>>>(fb.ctr, d_td);
         SF_LAUNCH_CHECK();
         ++n;
+        record_event(ev[5], s);
         return n;
     }
 };
@@ -205,6 +219,7 @@ int sf_tracker_create(sf_volume_t vol, const sf_tracker_config* config, const do
         SF_CUDA(cudaMemset(t->d_rstats, 0, sizeof(RayCounters)));
         SF_CUDA(cudaMemcpy(t->d_cur, initial_pose, 12 * sizeof(double), cudaMemcpyHostToDevice));
         SF_CUDA(cudaMallocHost(&t->h, sizeof(sf_tracker::Fetch)));
+        for (auto& e : t->ev) SF_CUDA(cudaEventCreate(&e));
         std::memset(t->h, 0, sizeof(sf_tracker::Fetch));
         *out = t.release();
         return SF_OK;
@@ -240,14 +255,16 @@ int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, con
             cudaGraphExec_t& ge = tr->graph[gmode][sidx];
             if (!ge) {
                 cudaGraph_t g;
-                SF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+                if (!tr->capture_stream) SF_CUDA(cudaStreamCreateWithFlags(&tr->capture_stream, cudaStreamNonBlocking));
+                cudaStream_t cs = tr->capture_stream;
+                SF_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
                 try {
-                    tr->issue(eff, has_sigma, s);
+                    tr->issue(eff, has_sigma, cs);
                 } catch (...) {
-                    cudaStreamEndCapture(s, &g);
+                    cudaStreamEndCapture(cs, &g);
                     throw;
                 }
-                SF_CUDA(cudaStreamEndCapture(s, &g));
+                SF_CUDA(cudaStreamEndCapture(cs, &g));
                 SF_CUDA(cudaGraphInstantiate(&ge, g, 0));
                 tr->graph_kernels[gmode][sidx] = count_kernel_nodes(g);
                 SF_CUDA(cudaGraphDestroy(g));
@@ -297,12 +314,31 @@ int sf_tracker_fetch(sf_tracker_t tr, sf_frame_metrics* out, void* stream) {
         out->raycast.sample_steps = h->rs.sample_steps;
         out->raycast.hit_pixels = h->rs.hit_pixels;
         out->raycast.rays_with_bounds = h->rs.rays_with_bounds;
+        out->blocks_processed = static_cast<uint64_t>(h->ctr.limit) + h->ctr.n_update;
+        if (h->ctr.skip) out->blocks_processed = 0;
+        out->voxels_visited = out->blocks_processed * m * m * m;
+        return SF_OK;
+    });
+}
+
+int sf_tracker_stage_times(sf_tracker_t tr, float ms[5]) {
+    return guarded([&]() -> int {
+        const int pairs[5][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {0, 5}};
+        for (int i = 0; i < 5; ++i) SF_CUDA(cudaEventElapsedTime(&ms[i], tr->ev[pairs[i][0]], tr->ev[pairs[i][1]]));
         return SF_OK;
     });
 }
 
 int sf_tracker_device_pose(sf_tracker_t tr, const double** device_pose) {
     *device_pose = tr->d_cur;
+    return SF_OK;
+}
+
+int sf_tracker_io_bytes(sf_tracker_t tr, int32_t has_sigma, uint64_t* h2d, uint64_t* d2h) {
+    const uint64_t n = static_cast<uint64_t>(tr->cam.w) * tr->cam.h;
+    *h2d = n * sizeof(float) * (has_sigma ? 2 : 1);
+    const sf_tracker::Fetch* f = nullptr;
+    *d2h = sizeof(f->cur) + sizeof(f->fuse_pose) + sizeof(f->td) + sizeof(f->ctr) + sizeof(f->rs) + sizeof(f->icp);
     return SF_OK;
 }
 
