@@ -244,6 +244,13 @@ typedef struct {
     sf_match_params match;
     sf_intrinsics camera;
     int32_t use_graphs; /* capture the per-frame launch sequence in a CUDA graph */
+    /* 0 (default): reference-exact pose chain. The reference forms
+     * initial_delta = compose(invert(current), current) and current = compose(current, delta)
+     * (pipeline.cpp:262-282), which multiplies the rotation's departure from orthonormality by
+     * ~3 per tracked frame (R R^T R); after ~30 frames tracking collapses in the reference and
+     * here alike. 1: project the estimated rotation back onto SO(3) (nearest_rotation) after
+     * every registration — a numerical fix that departs from reference bits. */
+    int32_t orthonormalize;
 } sf_tracker_config;
 
 typedef struct {
@@ -266,9 +273,13 @@ int sf_tracker_create(sf_volume_t vol, const sf_tracker_config* config, const do
                       sf_tracker_t* out);
 int sf_tracker_destroy(sf_tracker_t tr);
 /* mode 0: track (raycast + ICP, except for the tracker's first frame which is fused at the
- * current pose); mode 1: ground truth (fuse at gt_pose, no raycast/ICP). */
+ * current pose); mode 1: ground truth (fuse at gt_pose, no raycast/ICP); mode 2: track with
+ * an external initial delta passed in gt_pose (tracking.mode = icp_with_hook: ICP starts
+ * from compose(current, external), pipeline.cpp:262-267, registration.cpp:222-224). */
 int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, const double gt_pose[12],
                     void* stream);
+/* Re-seed the tracker's current pose (relocalisation; asynchronous on `stream`). */
+int sf_tracker_set_pose(sf_tracker_t tr, const double pose[12], void* stream);
 /* Synchronises `stream` and copies the metrics of the last step. */
 int sf_tracker_fetch(sf_tracker_t tr, sf_frame_metrics* out, void* stream);
 /* Device-timed stages of the last step, in ms (CUDA events recorded inside the step /

@@ -490,18 +490,21 @@ int sfref_apply_motion(const double pose[12], const double r[3], const double t[
 
 // One run() frame body (pipeline.cpp:250-287) without acquisition, for the fused-frame
 // reference timing and tracking parity: track = raycast(current) -> icp -> compose -> fuse.
+// mode 0: track; 1: fuse at current_pose; 2: track with external initial delta (icp_with_hook).
 int sfref_pipeline_frame(sfref_volume* v, const sf_frame* captured, const sf_intrinsics* camera,
                          const sf_fusion_params* fparams, const sf_match_params* mparams, int32_t mode,
-                         double current_pose[12], sf_fusion_stats* stats, int32_t* iterations,
-                         uint64_t* matches) {
+                         const double* external, double current_pose[12], sf_fusion_stats* stats,
+                         int32_t* iterations, uint64_t* matches) {
     return guarded([&]() -> int {
         const DepthFrame f = to_frame(captured);
         Pose current = to_pose(current_pose);
         *iterations = 0;
         *matches = 0;
-        if (mode == 0) {
+        if (mode == 0 || mode == 2) {
             const RaycastResult rendered = raycast(*v->grid, current, to_intr(camera));
-            const Pose initial_pose = initial_transform_hook(current, std::nullopt);
+            std::optional<Pose> ext;
+            if (mode == 2) ext = to_pose(external);
+            const Pose initial_pose = initial_transform_hook(current, ext);
             const Pose initial_delta = compose(invert(current), initial_pose);
             const IcpResult r = icp(f, rendered.depth, rendered.normals, initial_delta, to_match(mparams));
             *iterations = r.iterations;

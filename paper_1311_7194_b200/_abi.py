@@ -136,6 +136,7 @@ class TrackerConfigC(C.Structure):
         ("match", MatchParamsC),
         ("camera", IntrinsicsC),
         ("use_graphs", C.c_int32),
+        ("orthonormalize", C.c_int32),
     ]
 
 
@@ -212,6 +213,7 @@ PRODUCT_ONLY = {
     "tracker_destroy": (C.c_int, [vp]),
     "tracker_step": (C.c_int, [vp, P(FrameC), i32, c_double_p, vp]),
     "tracker_fetch": (C.c_int, [vp, P(FrameMetricsC), vp]),
+    "tracker_set_pose": (C.c_int, [vp, c_double_p, vp]),
     "tracker_device_pose": (C.c_int, [vp, P(c_double_p)]),
     "tracker_last_launch_count": (C.c_int, [vp, u64p]),
     "tracker_stage_times": (C.c_int, [vp, P(C.c_float)]),
@@ -233,7 +235,8 @@ REF_ONLY = {
     "apply_motion": (C.c_int, [c_double_p, c_double_p, c_double_p, c_double_p]),
     "pipeline_frame": (
         C.c_int,
-        [vp, P(FrameC), P(IntrinsicsC), P(FusionParamsC), P(MatchParamsC), i32, c_double_p, P(FusionStatsC), i32p, u64p],
+        [vp, P(FrameC), P(IntrinsicsC), P(FusionParamsC), P(MatchParamsC), i32, c_double_p, c_double_p,
+         P(FusionStatsC), i32p, u64p],
     ),
 }
 

@@ -682,14 +682,16 @@ class Tracker:
 
     TRACK = 0
     GROUND_TRUTH = 1
+    TRACK_WITH_HOOK = 2  # gt_pose carries the external initial delta (tracking.mode = icp_with_hook)
 
     def __init__(self, grid: SparseTsdfGrid, camera: Intrinsics, fusion: FusionParams, match: MatchParams,
-                 initial_pose: Pose, use_graphs: bool = True):
+                 initial_pose: Pose, use_graphs: bool = True, orthonormalize: bool = False):
         self.grid = grid
         self.camera = camera
         lib = grid.backend.lib
         self._lib = lib
-        cfg = A.TrackerConfigC(fusion.c(), match.c(), camera.c(), 1 if use_graphs else 0)
+        cfg = A.TrackerConfigC(fusion.c(), match.c(), camera.c(), 1 if use_graphs else 0,
+                               1 if orthonormalize else 0)
         h = C.c_void_p()
         p12 = initial_pose.to12()
         grid.backend.check(lib.tracker_create(grid.handle, C.byref(cfg), _dptr(p12), C.byref(h)))
@@ -707,6 +709,11 @@ class Tracker:
         fc = frame.c()
         g = _dptr(gt_pose.to12()) if gt_pose is not None else None
         self.grid.backend.check(self._lib.tracker_step(self.handle, C.byref(fc), mode, g, stream))
+
+    def set_pose(self, pose: Pose, stream=None):
+        """Re-seed the current pose (relocalisation)."""
+        p12 = pose.to12()
+        self.grid.backend.check(self._lib.tracker_set_pose(self.handle, _dptr(p12), stream))
 
     def fetch(self, stream=None) -> FrameMetrics:
         m = A.FrameMetricsC()

@@ -155,7 +155,21 @@ struct VolParams {
     double aux_w_max, aux_p_min, aux_p_max;
     uint64_t table_size;  // N^3
     uint32_t capacity;
+    int mshift;               // log2(M) when M is a power of two, else -1
+    int Nc;                   // coarse occupancy lattice: ceil(N / 16) super-blocks per axis
+    uint64_t occ_fine_words;  // uint32 words of the fine (per-block) bitmap; coarse bits follow
 };
+
+constexpr int kCoarseShift = 4;  // super-block = 16^3 blocks
+
+// Occupancy bitmaps (fine: 1 bit per block; coarse: 1 bit per 16^3 super-block, set when
+// any block in it was ever allocated — a conservative filter, never cleared on free).
+__device__ __forceinline__ void occ_set(const VolParams& P, uint32_t* occ, uint64_t key) {
+    atomicOr(&occ[key >> 5], 1u << (key & 31));
+    const uint64_t x = key % P.N, y = (key / P.N) % P.N, z = key / ((uint64_t)P.N * P.N);
+    const uint64_t c = ((z >> kCoarseShift) * P.Nc + (y >> kCoarseShift)) * P.Nc + (x >> kCoarseShift);
+    atomicOr(&occ[P.occ_fine_words + (c >> 5)], 1u << (c & 31));
+}
 
 // voxel_center (grid.cpp:271-273): origin + (vc + 0.5) * voxel_size
 SF_HD d3 voxel_center(const VolParams& P, int x, int y, int z) {

@@ -262,7 +262,7 @@ __global__ void k_alloc_flags(const FrameCounters* ctr, const uint32_t* __restri
 
 // Ordered allocation: the r-th new key (in (z,y,x) order) receives the r-th pop of the
 // free-list stack, exactly as process_block's lazy allocate_block calls would.
-__global__ void k_alloc_assign(FrameCounters* ctr, const uint32_t* __restrict__ uniq,
+__global__ void k_alloc_assign(VolParams P, FrameCounters* ctr, const uint32_t* __restrict__ uniq,
                                const uint32_t* __restrict__ ranks, int32_t* __restrict__ table,
                                const int32_t* __restrict__ free_list, int32_t* __restrict__ slot_key,
                                uint32_t* __restrict__ occ, const VolCounters* __restrict__ vc,
@@ -279,7 +279,7 @@ __global__ void k_alloc_assign(FrameCounters* ctr, const uint32_t* __restrict__ 
             slot = free_list[top - 1 - r];
             table[key] = slot;
             slot_key[slot] = static_cast<int32_t>(key);
-            atomicOr(&occ[key >> 5], 1u << (key & 31));
+            occ_set(P, occ, key);
             atomicMax(high_water, (unsigned long long)slot + 1ull);
             fresh = 1;
         } else {
@@ -633,7 +633,7 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
         SF_LAUNCH_CHECK();
         tb = fb.cub_temp_bytes;
         SF_CUDA(cub::DeviceScan::ExclusiveSum(fb.cub_temp, tb, fb.flags, fb.ranks, (int)fb.key_cap, s));
-        k_alloc_assign<<<kb, kThreads, 0, s>>>(fb.ctr, fb.keys_unique, fb.ranks, v.d_table, v.d_free_list,
+        k_alloc_assign<<<kb, kThreads, 0, s>>>(P, fb.ctr, fb.keys_unique, fb.ranks, v.d_table, v.d_free_list,
                                                v.d_slot_key, v.d_occ, v.d_vc, fb.work, &v.d_vc->high_water);
         SF_LAUNCH_CHECK();
         k_alloc_finalize<<<1, 1, 0, s>>>(fb.ctr, fb.flags, fb.ranks, v.d_vc);

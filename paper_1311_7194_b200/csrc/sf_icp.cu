@@ -1,18 +1,19 @@
 // sf_icp.cu — projective point-to-plane ICP on the device (registration.cpp:17-224).
 //
-// Every iteration is four launches with device-side control (no host round trip):
+// Every iteration is two launches with device-side control (no host round trip):
 //   k_icp_match     per source pixel: projective association + distance / normal
-//                   rejection (registration.cpp:17-50); match record to HBM; per-CTA
-//                   bbox (min/max of p and q) and count                    [deterministic]
-//   k_icp_bbox      1 CTA: bbox -> shrink centre / scale (registration.cpp:52-74);
-//                   < 10 matches -> TrackingLost (registration.cpp:202-204)
+//                   rejection (registration.cpp:17-50); match record to HBM/L2; per-CTA
+//                   bbox (min/max of p and q) and count. The last CTA to finish merges the
+//                   partials -> shrink centre / scale (registration.cpp:52-74), or
+//                   TrackingLost below 10 matches (registration.cpp:202-204).
 //   k_icp_assemble  per match: shrunk row (c_hat, n), d; 21 + 6 + 1 compensated sums
-//                   (double-double TwoSum accumulators), warp-shuffle -> CTA partials
-//                   (registration.cpp:76-123)
-//   k_icp_solve     1 CTA: fixed-order merge of the partials, Jacobi 6x6, gated solve,
-//                   unshrink, apply_motion, convergence test (registration.cpp:125-220)
+//                   (double-double TwoSum accumulators), warp shuffle -> CTA partials
+//                   (registration.cpp:76-123). The last CTA merges the partials in a fixed
+//                   order and runs Jacobi 6x6, gated solve, unshrink, apply_motion and the
+//                   convergence test (registration.cpp:125-220) — one thread, registers only.
 // A converged / failed state makes the remaining iterations' kernels exit at once, so the
-// whole ICP (max_iterations x 4 launches) is a fixed launch sequence: CUDA-graph friendly.
+// whole ICP (max_iterations x 2 launches) is a fixed launch sequence: CUDA-graph friendly.
+// Partials are merged in a fixed order, so results are deterministic run to run.
 //
 // Parity: the association and every per-match quantity are FP64 in the reference order.
 // The only deviation is the summation order of the 28 sums (tree instead of sequential
@@ -34,12 +35,78 @@ __global__ void k_icp_init(IcpState* st, const double* __restrict__ initial12, c
     *st = z;
 }
 
+// Returns true in every thread of the CTA that finished last (all partials visible).
+__device__ __forceinline__ bool last_cta(unsigned int* counter) {
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last) __threadfence();
+    return s_last;
+}
+
+// shrink's centre / scale (registration.cpp:54-64) from the bbox partials (min/max and
+// integer counts are exact in any order).
+__device__ void bbox_finalize(IcpState* st, const double* __restrict__ part_bbox,
+                              const unsigned long long* __restrict__ part_count, int nparts, const IcpParamsDev& prm) {
+    double b[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    unsigned long long cnt = 0;
+    for (int p = threadIdx.x; p < nparts; p += blockDim.x) {
+        const volatile double* pb = part_bbox + p * 6;
+        for (int a = 0; a < 3; ++a) {
+            b[a] = dmin(b[a], pb[a]);
+            b[3 + a] = dmax(b[3 + a], pb[3 + a]);
+        }
+        cnt += ((const volatile unsigned long long*)part_count)[p];
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        for (int a = 0; a < 3; ++a) {
+            b[a] = dmin(b[a], __shfl_down_sync(0xffffffffu, b[a], off));
+            b[3 + a] = dmax(b[3 + a], __shfl_down_sync(0xffffffffu, b[3 + a], off));
+        }
+        cnt += __shfl_down_sync(0xffffffffu, cnt, off);
+    }
+    __shared__ double s_b[kIcpThreads / 32][6];
+    __shared__ unsigned long long s_c[kIcpThreads / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        for (int a = 0; a < 6; ++a) s_b[wid][a] = b[a];
+        s_c[wid] = cnt;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int k = 1; k < (int)(blockDim.x / 32); ++k) {
+        for (int a = 0; a < 3; ++a) {
+            s_b[0][a] = dmin(s_b[0][a], s_b[k][a]);
+            s_b[0][3 + a] = dmax(s_b[0][3 + a], s_b[k][3 + a]);
+        }
+        s_c[0] += s_c[k];
+    }
+    cnt = s_c[0];
+    if (cnt < 10) {
+        st->lost = 1;
+        st->lost_count = cnt;
+        st->done = 1;
+        return;
+    }
+    st->matches = cnt;
+    st->cur_count = cnt;
+    const d3 l = mk(s_b[0][0], s_b[0][1], s_b[0][2]), hh = mk(s_b[0][3], s_b[0][4], s_b[0][5]);
+    const d3 c = scale(0.5, add(l, hh));
+    const d3 ext = sub(hh, l);
+    const d3 s = mk(dmax(ext.x, prm.floor), dmax(ext.y, prm.floor), dmax(ext.z, prm.floor));  // cwiseMax(floor)
+    st->center = c;
+    st->scale = s;
+    st->inv_scale = mk(1.0 / s.x, 1.0 / s.y, 1.0 / s.z);
+}
+
 // match_points (registration.cpp:17-50) + bbox partials of shrink (registration.cpp:54-59)
 __global__ void __launch_bounds__(kIcpThreads)
     k_icp_match(const float* __restrict__ src, const float* __restrict__ src_n, const float* __restrict__ tgt,
                 const float* __restrict__ tgt_n, Intr si, Intr ti, IcpParamsDev prm, IcpState* st,
                 MatchRec* __restrict__ rec, uint8_t* __restrict__ flag, double* __restrict__ part_bbox,
-                unsigned long long* __restrict__ part_count) {
+                unsigned long long* __restrict__ part_count, unsigned int* counter) {
     if (st->done) return;
     const Pose delta = st->delta;
     const int w = si.w, h = si.h;
@@ -122,43 +189,72 @@ __global__ void __launch_bounds__(kIcpThreads)
         for (int a = 0; a < 6; ++a) part_bbox[blockIdx.x * 6 + a] = s_b[0][a];
         part_count[blockIdx.x] = s_c[0];
     }
+    if (last_cta(counter)) {
+        bbox_finalize(st, part_bbox, part_count, gridDim.x, prm);
+        if (threadIdx.x == 0) *counter = 0;
+    }
 }
 
-// shrink's centre / scale (registration.cpp:54-64) from the bbox partials.
-__global__ void k_icp_bbox(IcpState* st, const double* __restrict__ part_bbox,
-                           const unsigned long long* __restrict__ part_count, int nparts, IcpParamsDev prm) {
-    if (st->done) return;
-    if (threadIdx.x != 0) return;
-    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-    unsigned long long cnt = 0;
-    for (int b = 0; b < nparts; ++b) {
-        for (int a = 0; a < 3; ++a) {
-            lo[a] = dmin(lo[a], part_bbox[b * 6 + a]);
-            hi[a] = dmax(hi[a], part_bbox[b * 6 + 3 + a]);
+// solve_gated + apply_motion + convergence (registration.cpp:175-212), one thread.
+__device__ __noinline__ void solve_finalize(IcpState* st, const double* s_sum, const IcpParamsDev& prm, int iter) {
+    double A[36];
+    int k = 0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+        for (int j = i; j < 6; ++j, ++k) {
+            A[i * 6 + j] = s_sum[k];
+            A[j * 6 + i] = s_sum[k];
         }
-        cnt += part_count[b];
+    double b[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) b[i] = s_sum[21 + i];
+    const double res_sq = s_sum[27];
+    const unsigned long long cnt = st->cur_count;
+    const double n_pairs = static_cast<double>(cnt);
+    st->pair_count = cnt;
+    st->residual_rms = sqrt(dmax(0.0, res_sq) / n_pairs);
+    Eig6 e;
+    eigendecompose_sym6(A, e);
+    double x[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+        st->eigenvalues[i] = e.values[i];
+        const bool keep = e.values[i] / n_pairs > prm.theta;
+        st->gated[i] = keep ? 1 : 0;
+        if (keep) {
+            const double* vcol = e.vectors + i * 6;
+            double vb = vcol[0] * b[0];
+#pragma unroll
+            for (int r = 1; r < 6; ++r) vb = vb + vcol[r] * b[r];
+            const double sc = vb / e.values[i];
+#pragma unroll
+            for (int r = 0; r < 6; ++r) x[r] = x[r] + vcol[r] * sc;
+        }
     }
-    if (cnt < 10) {
-        st->lost = 1;
-        st->lost_count = cnt;
-        st->done = 1;
-        return;
-    }
-    st->matches = cnt;
-    st->cur_count = cnt;
-    const d3 l = mk(lo[0], lo[1], lo[2]), hh = mk(hi[0], hi[1], hi[2]);
-    const d3 c = scale(0.5, add(l, hh));
-    const d3 ext = sub(hh, l);
-    const d3 s = mk(dmax(ext.x, prm.floor), dmax(ext.y, prm.floor), dmax(ext.z, prm.floor));  // cwiseMax(floor)
-    st->center = c;
-    st->scale = s;
-    st->inv_scale = mk(1.0 / s.x, 1.0 / s.y, 1.0 / s.z);
+#pragma unroll
+    for (int i = 0; i < 36; ++i) st->eigenvectors[i] = e.vectors[i];
+    double xn = x[0] * x[0];
+#pragma unroll
+    for (int r = 1; r < 6; ++r) xn = xn + x[r] * x[r];
+    st->shrunk_norm = sqrt(xn);
+    // unshrink_motion (registration.cpp:167-173)
+    const d3 s = st->scale, c = st->center;
+    const d3 r = mk((1.0 / s.x) * x[0], (1.0 / s.y) * x[1], (1.0 / s.z) * x[2]);
+    const d3 t = sub(mk(x[3], x[4], x[5]), cross(r, c));
+    st->motion_r = r;
+    st->motion_t = t;
+    st->delta = apply_motion(st->delta, r, t);
+    st->iterations = iter + 1;
+    if (st->shrunk_norm < prm.eps) st->done = 1;
 }
+
+constexpr int kMergeLanes = 8;  // threads per sum in the final merge (224 of 256 threads busy)
 
 // assemble (registration.cpp:93-123) on the shrunk matches (registration.cpp:65-72).
 __global__ void __launch_bounds__(kIcpThreads)
-    k_icp_assemble(const IcpState* __restrict__ st, const MatchRec* __restrict__ rec, const uint8_t* __restrict__ flag,
-                   int n, DD* __restrict__ part) {
+    k_icp_assemble(IcpState* st, const MatchRec* __restrict__ rec, const uint8_t* __restrict__ flag, int n,
+                   DD* __restrict__ part, unsigned int* counter, IcpParamsDev prm, int iter) {
     if (st->done) return;
     const d3 c = st->center, inv = st->inv_scale, scl = st->scale;
     DD acc[kSums];
@@ -203,60 +299,40 @@ __global__ void __launch_bounds__(kIcpThreads)
         for (int w = 1; w < kIcpThreads / 32; ++w) dd_merge(a, s_acc[w][threadIdx.x]);
         part[blockIdx.x * kSums + threadIdx.x] = a;
     }
-}
-
-// solve_gated + apply_motion + convergence (registration.cpp:175-212)
-__global__ void k_icp_solve(IcpState* st, const DD* __restrict__ part, int nparts, IcpParamsDev prm, int iter) {
-    if (st->done) return;
+    if (!last_cta(counter)) return;
+    // Fixed-order merge of all CTA partials: sum k, lane j takes partials j, j+8, ...
+    __shared__ DD s_m[kSums][kMergeLanes];
     __shared__ double s_sum[kSums];
+    const int nparts = gridDim.x;
+    if (threadIdx.x < kSums * kMergeLanes) {
+        const int k = threadIdx.x / kMergeLanes, j = threadIdx.x % kMergeLanes;
+        const volatile DD* vp = part;
+        DD a{0.0, 0.0};
+        bool first = true;
+        for (int p = j; p < nparts; p += kMergeLanes) {
+            DD b;
+            b.hi = vp[p * kSums + k].hi;
+            b.lo = vp[p * kSums + k].lo;
+            if (first) {
+                a = b;
+                first = false;
+            } else {
+                dd_merge(a, b);
+            }
+        }
+        s_m[k][j] = a;
+    }
+    __syncthreads();
     if (threadIdx.x < kSums) {
-        DD a = part[threadIdx.x];
-        for (int b = 1; b < nparts; ++b) dd_merge(a, part[b * kSums + threadIdx.x]);
+        DD a = s_m[threadIdx.x][0];
+        for (int j = 1; j < kMergeLanes; ++j) dd_merge(a, s_m[threadIdx.x][j]);
         s_sum[threadIdx.x] = a.hi + a.lo;
     }
     __syncthreads();
-    if (threadIdx.x != 0) return;
-    double A[36];
-    int k = 0;
-    for (int i = 0; i < 6; ++i)
-        for (int j = i; j < 6; ++j, ++k) {
-            A[i * 6 + j] = s_sum[k];
-            A[j * 6 + i] = s_sum[k];
-        }
-    double b[6];
-    for (int i = 0; i < 6; ++i) b[i] = s_sum[21 + i];
-    const double res_sq = s_sum[27];
-    const unsigned long long cnt = st->cur_count;
-    const double n_pairs = static_cast<double>(cnt);
-    st->pair_count = cnt;
-    st->residual_rms = sqrt(dmax(0.0, res_sq) / n_pairs);
-    Eig6 e;
-    eigendecompose_sym6(A, e);
-    double x[6] = {0, 0, 0, 0, 0, 0};
-    for (int i = 0; i < 6; ++i) {
-        st->eigenvalues[i] = e.values[i];
-        const bool keep = e.values[i] / n_pairs > prm.theta;
-        st->gated[i] = keep ? 1 : 0;
-        if (!keep) continue;
-        const double* vcol = e.vectors + i * 6;
-        double vb = vcol[0] * b[0];
-        for (int r = 1; r < 6; ++r) vb = vb + vcol[r] * b[r];
-        const double sc = vb / e.values[i];
-        for (int r = 0; r < 6; ++r) x[r] = x[r] + vcol[r] * sc;
+    if (threadIdx.x == 0) {
+        solve_finalize(st, s_sum, prm, iter);
+        *counter = 0;
     }
-    for (int i = 0; i < 36; ++i) st->eigenvectors[i] = e.vectors[i];
-    double xn = x[0] * x[0];
-    for (int r = 1; r < 6; ++r) xn = xn + x[r] * x[r];
-    st->shrunk_norm = sqrt(xn);
-    // unshrink_motion (registration.cpp:167-173)
-    const d3 s = st->scale, c = st->center;
-    const d3 r = mk((1.0 / s.x) * x[0], (1.0 / s.y) * x[1], (1.0 / s.z) * x[2]);
-    const d3 t = sub(mk(x[3], x[4], x[5]), cross(r, c));
-    st->motion_r = r;
-    st->motion_t = t;
-    st->delta = apply_motion(st->delta, r, t);
-    st->iterations = iter + 1;
-    if (st->shrunk_norm < prm.eps) st->done = 1;
 }
 
 IcpParamsDev make_icp_params(const sf_match_params& p) {
@@ -270,7 +346,7 @@ IcpParamsDev make_icp_params(const sf_match_params& p) {
     return d;
 }
 
-// Launch the whole ICP: init + max_iterations x (match, bbox, assemble, solve).
+// Launch the whole ICP: init + max_iterations x (match, assemble).
 void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* tgt, const float* tgt_n,
                 const Intr& si, const Intr& ti, const double* d_initial, const IcpParamsDev& prm, cudaStream_t s,
                 uint64_t* launches, const int* dead) {
@@ -280,12 +356,11 @@ void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* 
     uint64_t cnt = 1;
     for (int it = 0; it < prm.max_iterations; ++it) {
         k_icp_match<<<kIcpCtas, kIcpThreads, 0, s>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st, wk.rec, wk.flag,
-                                                     wk.part_bbox, wk.part_count);
-        k_icp_bbox<<<1, 32, 0, s>>>(wk.st, wk.part_bbox, wk.part_count, kIcpCtas, prm);
-        k_icp_assemble<<<kIcpCtas, kIcpThreads, 0, s>>>(wk.st, wk.rec, wk.flag, n, wk.part);
-        k_icp_solve<<<1, 32, 0, s>>>(wk.st, wk.part, kIcpCtas, prm, it);
+                                                     wk.part_bbox, wk.part_count, wk.counters);
+        k_icp_assemble<<<kIcpCtas, kIcpThreads, 0, s>>>(wk.st, wk.rec, wk.flag, n, wk.part, wk.counters + 1, prm,
+                                                        it);
         SF_LAUNCH_CHECK();
-        cnt += 4;
+        cnt += 2;
     }
     if (launches) *launches += cnt;
 }

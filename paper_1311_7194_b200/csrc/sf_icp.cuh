@@ -67,10 +67,13 @@ struct IcpWork {
     float* src_normals = nullptr;
     float *src = nullptr, *tgt = nullptr, *tgt_n = nullptr, *src_n_in = nullptr;
     double* initial = nullptr;
+    unsigned int* counters = nullptr;  // "last CTA" tickets of the two fused reductions
     void ensure(int W, int H) {
         if (W == w && H == h && rec) return;
         release();
         const size_t n = static_cast<size_t>(W) * H;
+        SF_CUDA(cudaMalloc(&counters, 4 * sizeof(unsigned int)));
+        SF_CUDA(cudaMemset(counters, 0, 4 * sizeof(unsigned int)));
         SF_CUDA(cudaMalloc(&rec, n * sizeof(MatchRec)));
         SF_CUDA(cudaMalloc(&flag, n));
         SF_CUDA(cudaMalloc(&part_bbox, kIcpCtas * 6 * sizeof(double)));
@@ -87,9 +90,11 @@ struct IcpWork {
         h = H;
     }
     void release() {
-        void* p[] = {rec, flag, part_bbox, part_count, part, st, src_normals, src, tgt, tgt_n, src_n_in, initial};
+        void* p[] = {rec, flag, part_bbox, part_count, part, st, src_normals, src, tgt, tgt_n, src_n_in, initial,
+                     counters};
         for (void* q : p)
             if (q) cudaFree(q);
+        counters = nullptr;
         rec = nullptr;
         flag = nullptr;
         part_bbox = nullptr;

@@ -24,16 +24,21 @@ struct Eig6 {
     double vectors[36]; // column-major: vectors[c*6 + r]
 };
 
+// All loops over fixed index ranges are fully unrolled so m and v live in registers.
 SF_HD void eigendecompose_sym6(const double* a /* row-major 6x6 */, Eig6& out) {
     double m[6][6], v[6][6];
+#pragma unroll
     for (int i = 0; i < 6; ++i)
+#pragma unroll
         for (int j = 0; j < 6; ++j) {
             m[i][j] = 0.5 * (a[i * 6 + j] + a[j * 6 + i]);
             v[i][j] = i == j ? 1.0 : 0.0;
         }
     // m.norm(): column-major left-to-right sum of squares
     double sq = m[0][0] * m[0][0];
+#pragma unroll
     for (int c = 0; c < 6; ++c)
+#pragma unroll
         for (int r = 0; r < 6; ++r) {
             if (c == 0 && r == 0) continue;
             sq = sq + m[r][c] * m[r][c];
@@ -43,52 +48,80 @@ SF_HD void eigendecompose_sym6(const double* a /* row-major 6x6 */, Eig6& out) {
     const double tol = 1e-12 * scl;
     for (int sweep = 0; sweep < 64; ++sweep) {
         double off = 0.0;
+#pragma unroll
         for (int p = 0; p < 6; ++p)
+#pragma unroll
             for (int q = p + 1; q < 6; ++q) off += m[p][q] * m[p][q];
         if (sqrt(off) <= tol) break;
+#pragma unroll
         for (int p = 0; p < 6; ++p) {
+#pragma unroll
             for (int q = p + 1; q < 6; ++q) {
                 const double apq = m[p][q];
-                if (fabs(apq) <= tol / 30.0) continue;
-                const double theta = (m[q][q] - m[p][p]) / (2.0 * apq);
-                const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-                const double c = 1.0 / sqrt(t * t + 1.0);
-                const double s = t * c;
-                // m1 = rot^T * m: rows p, q
-                for (int j = 0; j < 6; ++j) {
-                    const double mp = m[p][j], mq = m[q][j];
-                    m[p][j] = c * mp + (-s) * mq;
-                    m[q][j] = s * mp + c * mq;
-                }
-                // m = m1 * rot: columns p, q
-                for (int i = 0; i < 6; ++i) {
-                    const double mp = m[i][p], mq = m[i][q];
-                    m[i][p] = mp * c + mq * (-s);
-                    m[i][q] = mp * s + mq * c;
-                }
-                // v = v * rot
-                for (int i = 0; i < 6; ++i) {
-                    const double vp = v[i][p], vq = v[i][q];
-                    v[i][p] = vp * c + vq * (-s);
-                    v[i][q] = vp * s + vq * c;
+                if (!(fabs(apq) <= tol / 30.0)) {
+                    const double theta = (m[q][q] - m[p][p]) / (2.0 * apq);
+                    const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                    const double c = 1.0 / sqrt(t * t + 1.0);
+                    const double s = t * c;
+                    // m1 = rot^T * m: rows p, q
+#pragma unroll
+                    for (int j = 0; j < 6; ++j) {
+                        const double mp = m[p][j], mq = m[q][j];
+                        m[p][j] = c * mp + (-s) * mq;
+                        m[q][j] = s * mp + c * mq;
+                    }
+                    // m = m1 * rot: columns p, q
+#pragma unroll
+                    for (int i = 0; i < 6; ++i) {
+                        const double mp = m[i][p], mq = m[i][q];
+                        m[i][p] = mp * c + mq * (-s);
+                        m[i][q] = mp * s + mq * c;
+                    }
+                    // v = v * rot
+#pragma unroll
+                    for (int i = 0; i < 6; ++i) {
+                        const double vp = v[i][p], vq = v[i][q];
+                        v[i][p] = vp * c + vq * (-s);
+                        v[i][q] = vp * s + vq * c;
+                    }
                 }
             }
         }
     }
-    // std::sort by diagonal (libstdc++ insertion sort for n <= 16: stable)
+    // std::sort by diagonal (libstdc++ insertion sort for n <= 16: stable), on a register copy
+    double d[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) d[i] = m[i][i];
     int order[6] = {0, 1, 2, 3, 4, 5};
     for (int i = 1; i < 6; ++i) {
         const int val = order[i];
+        double dv = 0.0;
+#pragma unroll
+        for (int k = 0; k < 6; ++k)
+            if (k == val) dv = d[k];
         int j = i;
-        while (j > 0 && m[val][val] < m[order[j - 1]][order[j - 1]]) {
-            order[j] = order[j - 1];
+        while (j > 0) {
+            double dp = 0.0;
+            const int o = order[j - 1];
+#pragma unroll
+            for (int k = 0; k < 6; ++k)
+                if (k == o) dp = d[k];
+            if (!(dv < dp)) break;
+            order[j] = o;
             --j;
         }
         order[j] = val;
     }
+#pragma unroll
     for (int i = 0; i < 6; ++i) {
-        out.values[i] = m[order[i]][order[i]];
-        for (int r = 0; r < 6; ++r) out.vectors[i * 6 + r] = v[r][order[i]];
+        const int o = order[i];
+#pragma unroll
+        for (int k = 0; k < 6; ++k)
+            if (k == o) {
+                out.values[i] = d[k];
+#pragma unroll
+                for (int r = 0; r < 6; ++r) out.vectors[i * 6 + r] = v[r][k];
+            }
     }
 }
 
@@ -186,7 +219,9 @@ SF_HD m33 nearest_rotation(const m33& a) {
     while (!finished && sweeps < 64) {
         finished = true;
         ++sweeps;
+#pragma unroll
         for (int p = 1; p < 3; ++p) {
+#pragma unroll
             for (int q = 0; q < p; ++q) {
                 const double pm = precision * maxDiag;
                 const double threshold = considerAsZero < pm ? pm : considerAsZero;
@@ -213,21 +248,31 @@ SF_HD m33 nearest_rotation(const m33& a) {
             for (int k = 0; k < 3; ++k) u[k][i] = -u[k][i];
     }
     for (int i = 0; i < 3; ++i) sv[i] = sv[i] * scl;
+#pragma unroll
     for (int i = 0; i < 3; ++i) {
+        // first maximum of sv[i..2] (Eigen maxCoeff(&pos)), swapped into place
         int pos = i;
+        double best = sv[i];
+#pragma unroll
         for (int k = i + 1; k < 3; ++k)
-            if (sv[k] > sv[pos]) pos = k;
-        if (pos != i) {
+            if (sv[k] > best) {
+                pos = k;
+                best = sv[k];
+            }
+#pragma unroll
+        for (int c = i + 1; c < 3; ++c) {
+            if (c != pos) continue;
             const double t = sv[i];
-            sv[i] = sv[pos];
-            sv[pos] = t;
+            sv[i] = sv[c];
+            sv[c] = t;
+#pragma unroll
             for (int k = 0; k < 3; ++k) {
                 double x = u[k][i];
-                u[k][i] = u[k][pos];
-                u[k][pos] = x;
+                u[k][i] = u[k][c];
+                u[k][c] = x;
                 x = v[k][i];
-                v[k][i] = v[k][pos];
-                v[k][pos] = x;
+                v[k][i] = v[k][c];
+                v[k][c] = x;
             }
         }
     }

@@ -22,10 +22,21 @@ __device__ __forceinline__ bool occupied(const uint32_t* __restrict__ occ, uint6
 __global__ void k_ray_bounds(VolParams P, const FrameConsts* __restrict__ fc, const uint32_t* __restrict__ occ,
                              const VolCounters* __restrict__ vc, float* __restrict__ t_start,
                              float* __restrict__ t_end, int w, int h, const int* dead) {
+    // Coarse occupancy (1 bit per 16^3 blocks) staged in shared memory: the DDA only reads
+    // the fine bitmap (L2) inside super-blocks that ever held a block. Exact: a clear coarse
+    // bit implies every block of the super-block is EMPTY.
+    extern __shared__ uint32_t s_coarse[];
+    if (dead && *dead) return;
+    {
+        const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+        const uint64_t nc = P.Nc;
+        const int cwords = static_cast<int>((nc * nc * nc + 31) / 32);
+        for (int i = tid; i < cwords; i += blockDim.x * blockDim.y) s_coarse[i] = __ldg(&occ[P.occ_fine_words + i]);
+        __syncthreads();
+    }
     const int u = blockIdx.x * blockDim.x + threadIdx.x;
     const int v = blockIdx.y * blockDim.y + threadIdx.y;
     if (u >= w || v >= h) return;
-    if (dead && *dead) return;
     const size_t idx = (size_t)v * w + u;
     float ts = INFINITY, te = -INFINITY;
     if (vc->allocated_count != 0) {
@@ -89,7 +100,10 @@ __global__ void k_ray_bounds(VolParams P, const FrameConsts* __restrict__ fc, co
             while (t_in <= hi) {
                 const int axis = t_max[0] <= t_max[1] ? (t_max[0] <= t_max[2] ? 0 : 2) : (t_max[1] <= t_max[2] ? 1 : 2);
                 const double t_out = dmin(t_max[axis], hi);
-                if (occupied(occ, table_index(P, cell[0], cell[1], cell[2]))) {
+                const int cc = ((cell[2] >> kCoarseShift) * P.Nc + (cell[1] >> kCoarseShift)) * P.Nc +
+                               (cell[0] >> kCoarseShift);
+                if (((s_coarse[cc >> 5] >> (cc & 31)) & 1u) &&
+                    occupied(occ, table_index(P, cell[0], cell[1], cell[2]))) {
                     first = dmin(first, t_in);
                     last = dmax(last, t_out);
                 }
@@ -113,11 +127,14 @@ struct Sampler {
     VolParams P;
     const int32_t* __restrict__ table;
     const uint16_t* __restrict__ payload;
+    const uint32_t* __restrict__ occ;
     const double* tdec;  // shared-memory LUT, index code + 128
+
+    __device__ __forceinline__ int blk(int x) const { return P.mshift >= 0 ? (x >> P.mshift) : x / P.M; }
 
     __device__ __forceinline__ bool code(int x, int y, int z, double& out) const {
         const int M = P.M;
-        const int bx = x / M, by = y / M, bz = z / M;
+        const int bx = blk(x), by = blk(y), bz = blk(z);
         const int32_t slot = __ldg(&table[table_index(P, bx, by, bz)]);
         if (slot == kEmpty) return false;
         const int lx = x - bx * M, ly = y - by * M, lz = z - bz * M;
@@ -135,6 +152,9 @@ struct Sampler {
         const int bx = ref_floor_int(gx), by = ref_floor_int(gy), bz = ref_floor_int(gz);
         const int res = P.res;
         if (bx < 0 || by < 0 || bz < 0 || bx + 1 >= res || by + 1 >= res || bz + 1 >= res) return false;
+        // The base corner's block EMPTY => voxel_code fails => nullopt (render.cpp:14-15,39):
+        // decided from the 1-bit occupancy map without touching the 4-byte table.
+        if (!occupied(occ, table_index(P, blk(bx), blk(by), blk(bz)))) return false;
         const double fx = gx - (double)bx, fy = gy - (double)by, fz = gz - (double)bz;
         double c[8];
         for (int i = 0; i < 8; ++i)
@@ -169,7 +189,7 @@ struct Sampler {
 
 __global__ void __launch_bounds__(256)
     k_raycast(VolParams P, const FrameConsts* __restrict__ fc, const int32_t* __restrict__ table,
-              const uint16_t* __restrict__ payload, const AuxTables* __restrict__ aux,
+              const uint16_t* __restrict__ payload, const uint32_t* __restrict__ occ, const AuxTables* __restrict__ aux,
               const float* __restrict__ t_start, const float* __restrict__ t_end, float* __restrict__ depth_out,
               float* __restrict__ normals_out, RayCounters* stats, int w, int h, const int* dead) {
     __shared__ double s_tdec[256];
@@ -186,7 +206,7 @@ __global__ void __launch_bounds__(256)
         const float fs = t_start[idx], fe = t_end[idx];
         if (fs <= fe) {  // !bounds.empty(u, v)
             with_bounds = 1;
-            const Sampler S{P, table, payload, s_tdec};
+            const Sampler S{P, table, payload, occ, s_tdec};
             const Intr& intr = fc->intr;
             const Pose& pose = fc->pose;
             const double vox = P.voxel;
@@ -278,8 +298,11 @@ __global__ void __launch_bounds__(256)
 
 void launch_ray_bounds(Volume& v, const FrameConsts* d_fc, const Intr& intr, float* t_start, float* t_end,
                        cudaStream_t s, uint64_t* launches, const int* dead_flag) {
-    const dim3 blk(32, 4), grd((intr.w + 31) / 32, (intr.h + 3) / 4);
-    k_ray_bounds<<<grd, blk, 0, s>>>(v.P, d_fc, v.d_occ, v.d_vc, t_start, t_end, intr.w, intr.h, dead_flag);
+    const dim3 blk(32, 8), grd((intr.w + 31) / 32, (intr.h + 7) / 8);
+    const uint64_t nc = v.P.Nc;
+    const size_t smem = ((nc * nc * nc + 31) / 32) * sizeof(uint32_t);
+    if (smem > 48 * 1024) SF_CUDA(cudaFuncSetAttribute(k_ray_bounds, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_ray_bounds<<<grd, blk, smem, s>>>(v.P, d_fc, v.d_occ, v.d_vc, t_start, t_end, intr.w, intr.h, dead_flag);
     SF_LAUNCH_CHECK();
     if (launches) *launches += 1;
 }
@@ -288,7 +311,7 @@ void launch_raycast(Volume& v, const FrameConsts* d_fc, const Intr& intr, const 
                     float* depth, float* normals, RayCounters* d_stats, cudaStream_t s, uint64_t* launches,
                     const int* dead_flag) {
     const dim3 blk(32, 4), grd((intr.w + 31) / 32, (intr.h + 3) / 4);
-    k_raycast<<<grd, blk, 0, s>>>(v.P, d_fc, v.d_table, v.d_payload, v.d_aux, t_start, t_end, depth, normals,
+    k_raycast<<<grd, blk, 0, s>>>(v.P, d_fc, v.d_table, v.d_payload, v.d_occ, v.d_aux, t_start, t_end, depth, normals,
                                   d_stats, intr.w, intr.h, dead_flag);
     SF_LAUNCH_CHECK();
     if (launches) *launches += 1;

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "sf_icp.cuh"
+#include "sf_linalg.cuh"
 
 namespace sf {
 
@@ -27,27 +28,30 @@ struct TrackerDev {
     int frame;
 };
 
-__global__ void k_tracker_begin_track(const double* __restrict__ cur, double* __restrict__ init_delta,
-                                      RayCounters* rstats, const TrackerDev* td) {
+__global__ void k_tracker_begin_track(const double* __restrict__ cur, const double* __restrict__ external,
+                                      double* __restrict__ init_delta, RayCounters* rstats, const TrackerDev* td) {
     if (td->dead) return;
-    // initial_pose = initial_transform_hook(current, nullopt) = current;
-    // initial_delta = compose(invert(current), initial_pose)   (pipeline.cpp:262-267)
+    // initial_pose = initial_transform_hook(current, external) = external ? compose(current,
+    // *external) : current (registration.cpp:222-224); initial_delta = compose(invert(current),
+    // initial_pose) (pipeline.cpp:262-267)
     const Pose c = pose_from12(cur);
-    const Pose d = compose(invert(c), c);
+    const Pose init = external ? compose(c, pose_from12(external)) : c;
+    const Pose d = compose(invert(c), init);
     pose_to12(d, init_delta);
     RayCounters z{0, 0, 0, 0};
     *rstats = z;
 }
 
 __global__ void k_tracker_after_icp(double* __restrict__ cur, double* __restrict__ fuse_pose, const IcpState* st,
-                                    TrackerDev* td) {
+                                    TrackerDev* td, int orthonormalize) {
     if (td->dead) return;
     if (st->lost) {
         td->dead = 1;
         td->status = SF_TRACKING_LOST;
         return;
     }
-    const Pose est = compose(pose_from12(cur), st->delta);  // pipeline.cpp:282
+    Pose est = compose(pose_from12(cur), st->delta);  // pipeline.cpp:282
+    if (orthonormalize) est.R = nearest_rotation(est.R);
     pose_to12(est, cur);
     pose_to12(est, fuse_pose);
     td->registered = 1;
@@ -101,8 +105,8 @@ struct sf_tracker {
     uint64_t last_launches = 0;
     cudaStream_t capture_stream = nullptr;  // graphs are captured here (the legacy stream cannot capture)
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // stage timing (graph nodes)
-    cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [mode][has_sigma]
-    uint64_t graph_kernels[2][2] = {{0, 0}, {0, 0}};
+    cudaGraphExec_t graph[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};  // [mode][sigma]
+    uint64_t graph_kernels[3][2] = {{0, 0}, {0, 0}, {0, 0}};
     // pinned fetch staging
     struct Fetch {
         double cur[12];
@@ -135,8 +139,8 @@ struct sf_tracker {
         const FuseParams& p = has_sigma ? fp_sigma : fp;
         const float* sig = has_sigma ? d_cap_sigma : nullptr;
         record_event(ev[0], s);
-        if (mode == 0) {
-            k_tracker_begin_track<<<1, 1, 0, s>>>(d_cur, d_init_delta, d_rstats, d_td);
+        if (mode == 0 || mode == 3) {
+            k_tracker_begin_track<<<1, 1, 0, s>>>(d_cur, mode == 3 ? d_gt : nullptr, d_init_delta, d_rstats, d_td);
             SF_LAUNCH_CHECK();
             ++n;
             launch_consts(vol->P, cam, d_cur, d_rc_fc, s, &n);
@@ -147,7 +151,7 @@ struct sf_tracker {
                                    icp.src_normals, s, &n, dead);
             launch_icp(icp, d_cap, icp.src_normals, d_model_depth, d_model_normals, cam, cam, d_init_delta, icp_prm, s,
                        &n, dead);
-            k_tracker_after_icp<<<1, 1, 0, s>>>(d_cur, fb.pose, icp.st, d_td);
+            k_tracker_after_icp<<<1, 1, 0, s>>>(d_cur, fb.pose, icp.st, d_td, cfg.orthonormalize);
             SF_LAUNCH_CHECK();
             ++n;
             record_event(ev[2], s);
@@ -236,7 +240,9 @@ int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, con
         if (!tr || !captured) throw Error(SF_INVALID_ARGUMENT, "sf_tracker_step: null argument");
         if (captured->intrinsics.width != tr->cam.w || captured->intrinsics.height != tr->cam.h)
             throw Error(SF_INVALID_ARGUMENT, "sf_tracker_step: frame size differs from the tracker camera");
-        if (mode == 1 && !gt_pose) throw Error(SF_INVALID_ARGUMENT, "sf_tracker_step: ground-truth mode needs gt_pose");
+        if ((mode == 1 || mode == 2) && !gt_pose)
+            throw Error(SF_INVALID_ARGUMENT, "sf_tracker_step: this mode needs a pose argument");
+        if (mode < 0 || mode > 2) throw Error(SF_INVALID_ARGUMENT, "sf_tracker_step: unknown mode");
         SF_CUDA(cudaSetDevice(tr->vol->device));
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         const size_t n = static_cast<size_t>(tr->cam.w) * tr->cam.h;
@@ -245,11 +251,14 @@ int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, con
         const bool has_sigma = captured->sigma != nullptr;
         if (has_sigma) SF_CUDA(cudaMemcpyAsync(tr->d_cap_sigma, captured->sigma, n * sizeof(float), kind, s));
         // First frame: fuse at the current (initial) pose without registration (pipeline.cpp:250-252).
-        int eff = mode;
-        if (mode == 0 && tr->frames == 0) eff = 2;  // fuse at current, keep current
-        if (eff == 1) SF_CUDA(cudaMemcpyAsync(tr->d_gt, gt_pose, 12 * sizeof(double), cudaMemcpyHostToDevice, s));
+        // internal modes: 0 track, 1 ground truth, 2 fuse at current (first frame), 3 track with
+        // an external initial delta (tracking.mode = icp_with_hook, pipeline.cpp:262-266)
+        int eff = mode == 2 ? 3 : mode;
+        if (mode != 1 && tr->frames == 0) eff = 2;  // fuse at current, keep current
+        if (eff == 1 || eff == 3)
+            SF_CUDA(cudaMemcpyAsync(tr->d_gt, gt_pose, 12 * sizeof(double), cudaMemcpyHostToDevice, s));
         if (eff == 2) SF_CUDA(cudaMemcpyAsync(tr->d_gt, tr->d_cur, 12 * sizeof(double), cudaMemcpyDeviceToDevice, s));
-        const int gmode = eff == 0 ? 0 : 1;
+        const int gmode = eff == 0 ? 0 : eff == 1 ? 1 : 2;
         const int sidx = has_sigma ? 1 : 0;
         if (tr->cfg.use_graphs && eff != 2) {
             cudaGraphExec_t& ge = tr->graph[gmode][sidx];
@@ -280,6 +289,15 @@ int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, con
     });
 }
 
+int sf_tracker_set_pose(sf_tracker_t tr, const double pose[12], void* stream) {
+    return guarded([&]() -> int {
+        SF_CUDA(cudaSetDevice(tr->vol->device));
+        SF_CUDA(cudaMemcpyAsync(tr->d_cur, pose, 12 * sizeof(double), cudaMemcpyHostToDevice,
+                                static_cast<cudaStream_t>(stream)));
+        return SF_OK;
+    });
+}
+
 int sf_tracker_fetch(sf_tracker_t tr, sf_frame_metrics* out, void* stream) {
     return guarded([&]() -> int {
         SF_CUDA(cudaSetDevice(tr->vol->device));
@@ -295,7 +313,7 @@ int sf_tracker_fetch(sf_tracker_t tr, sf_frame_metrics* out, void* stream) {
         std::memset(out, 0, sizeof(*out));
         out->frame = tr->frames - 1;
         out->status = h->td.status;
-        out->registered = tr->last_mode == 0 ? h->td.registered : 0;
+        out->registered = (tr->last_mode == 0 || tr->last_mode == 3) ? h->td.registered : 0;
         std::memcpy(out->pose, h->fuse_pose, sizeof(out->pose));
         if (out->registered) {
             out->iterations = h->icp.iterations;

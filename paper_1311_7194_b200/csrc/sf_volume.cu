@@ -6,7 +6,8 @@
 //   d_free_list  int32[cap]        free-list stack, lowest slot on top (grid.cpp:68-71)
 //   d_slot_key   int32[cap]        inverse map slot -> table index (-1 = free), lets the
 //                                  visibility pass walk allocated blocks without an N^3 scan
-//   d_occ        uint32[N^3/32]    occupancy bitmap for the ray-bounds DDA (L2 resident)
+//   d_occ        uint32[N^3/32]    occupancy bitmap for the ray-bounds DDA (L2 resident), followed
+//                                  by a coarse 1-bit-per-16^3-blocks bitmap (shared-memory resident)
 //   d_fpayload   float2[cap*M^3]   optional float payload (FloatShadowGrid semantics)
 #include <algorithm>
 #include <cmath>
@@ -192,7 +193,7 @@ __global__ void k_allocate_one(VolParams P, int32_t* table, int32_t* free_list, 
                 if ((unsigned long long)slot + 1 > vc->high_water) vc->high_water = slot + 1;
                 table[tidx] = slot;
                 slot_key[slot] = static_cast<int32_t>(tidx);
-                occ[tidx >> 5] |= 1u << (tidx & 31);
+                occ_set(P, occ, tidx);
                 out[1] = 1;  // fresh
             }
         }
@@ -235,7 +236,7 @@ __global__ void k_rebuild_index(VolParams P, const int32_t* table, int32_t* slot
         const int32_t s = table[i];
         if (s != kEmpty) {
             slot_key[s] = static_cast<int32_t>(i);
-            atomicOr(&occ[i >> 5], 1u << (i & 31));
+            occ_set(P, occ, i);
         }
     }
 }
@@ -269,6 +270,11 @@ static VolParams make_params(const sf_grid_config& c, const sf_aux_quant& a, uin
     P.aux_p_max = a.p_max;
     P.table_size = static_cast<uint64_t>(P.N) * P.N * P.N;
     P.capacity = capacity;
+    P.Nc = (P.N + (1 << kCoarseShift) - 1) >> kCoarseShift;
+    P.mshift = -1;
+    for (int b = 0; b < 16; ++b)
+        if ((1 << b) == P.M) P.mshift = b;
+    P.occ_fine_words = (P.table_size + 31) / 32;
     return P;
 }
 
@@ -303,7 +309,8 @@ static void volume_init_device(Volume& v) {
     SF_CUDA(cudaMalloc(&v.d_payload, std::max<uint64_t>(pool_voxels, 1) * sizeof(uint16_t)));
     SF_CUDA(cudaMalloc(&v.d_free_list, std::max<uint32_t>(P.capacity, 1) * sizeof(int32_t)));
     SF_CUDA(cudaMalloc(&v.d_slot_key, std::max<uint32_t>(P.capacity, 1) * sizeof(int32_t)));
-    const uint64_t occ_words = (P.table_size + 31) / 32;
+    const uint64_t nc = static_cast<uint64_t>(P.Nc);
+    const uint64_t occ_words = P.occ_fine_words + (nc * nc * nc + 31) / 32;
     SF_CUDA(cudaMalloc(&v.d_occ, occ_words * sizeof(uint32_t)));
     SF_CUDA(cudaMalloc(&v.d_vc, sizeof(VolCounters)));
     SF_CUDA(cudaMalloc(&v.d_aux, sizeof(AuxTables)));

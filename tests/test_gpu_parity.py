@@ -348,7 +348,7 @@ def test_tracker_matches_reference_pipeline(gpu, ref):
         mt = C.c_uint64()
         fc, ic, fp, mp = f.c(), intr.c(), fusion.c(), match.c()
         assert ref.lib.pipeline_frame(r.handle, C.byref(fc), C.byref(ic), C.byref(fp), C.byref(mp),
-                                      0 if k > 0 else 1, cur.ctypes.data_as(A.c_double_p), C.byref(st),
+                                      0 if k > 0 else 1, None, cur.ctypes.data_as(A.c_double_p), C.byref(st),
                                       C.byref(it), C.byref(mt)) == 0
         assert m.status == 0
         assert pose_diff(m.pose, sf.Pose.from12(cur)) < 1e-6
@@ -362,3 +362,64 @@ def test_tracker_matches_reference_pipeline(gpu, ref):
     pa, pb = g.read_payload(), r.read_payload()
     assert (pa == pb).mean() > 0.9999
     assert tr.last_launch_count() > 20
+
+
+def test_tracker_hook_mode_matches_reference(gpu, ref):
+    """tracking.mode = icp_with_hook (pipeline.cpp:262-266) plus relocalisation via set_pose."""
+    import ctypes as C
+    from paper_1311_7194_b200 import _abi as A
+
+    intr = scenes.camera(320, 240, 262.5)
+    poses = scenes.c1_trajectory(100)[:10]
+    frames = frames_for(ref, scenes.sphere_plane_scene(), poses, intr, 2.0, sigma0=2.5e-4)
+    cfg = scenes.c1_config()
+    fusion = sf.FusionParams(mode=sf.FusionMode.Weighted, sigma0=2.5e-4)
+    match = sf.MatchParams.for_voxel_size(cfg.voxel_size)
+    g, r = grids(gpu, ref, cfg, 0, sf.AuxMode.Weight)
+    tr = sf.Tracker(g, intr, fusion, match, poses[0])
+    cur = poses[0].to12().copy()
+    for k, f in enumerate(frames):
+        ext = sf.compose(sf.invert(poses[k - 1]), poses[k]) if k else sf.Pose.identity()
+        if k == 6:  # relocalise both
+            tr.set_pose(poses[5])
+            cur[:] = poses[5].to12()
+        tr.step(f, sf.Tracker.TRACK_WITH_HOOK, ext)
+        m = tr.fetch()
+        st, it, mt = A.FusionStatsC(), C.c_int32(), C.c_uint64()
+        fc, ic, fp, mp = f.c(), intr.c(), fusion.c(), match.c()
+        e12 = ext.to12()
+        assert ref.lib.pipeline_frame(r.handle, C.byref(fc), C.byref(ic), C.byref(fp), C.byref(mp),
+                                      2 if k else 1, e12.ctypes.data_as(A.c_double_p),
+                                      cur.ctypes.data_as(A.c_double_p), C.byref(st), C.byref(it), C.byref(mt)) == 0
+        assert m.status == 0
+        assert pose_diff(m.pose, sf.Pose.from12(cur)) < 1e-6
+        assert m.fusion.blocks_total == st.blocks_total
+        if k:
+            assert m.registered and m.iterations == it.value
+    assert np.array_equal(g.read_table(), r.read_table())
+
+
+def test_reference_pose_chain_instability_and_fix(gpu):
+    """The reference pose chain (pipeline.cpp:262-282) triples the rotation's departure from
+    orthonormality every tracked frame; `orthonormalize` removes it."""
+    intr = scenes.camera(160, 120, 131.25)
+    poses = scenes.c1_trajectory(100)[:30]
+    scene = scenes.sphere_plane_scene()
+    frames = [gpu.render_synthetic_depth(scene, p, intr, domain_size=2.0) for p in poses]
+    cfg = scenes.c1_config()
+    fusion = sf.FusionParams(mode=sf.FusionMode.Weighted)
+    match = sf.MatchParams.for_voxel_size(cfg.voxel_size)
+    match.max_iterations = 0  # isolate the pose chain: delta = hook = exact ground-truth motion
+    orth = {}
+    for fix in (False, True):
+        g = sf.SparseTsdfGrid(cfg, 0, sf.AuxMode.Weight)
+        tr = sf.Tracker(g, intr, fusion, match, poses[0], orthonormalize=fix)
+        errs = []
+        for k, f in enumerate(frames):
+            ext = sf.compose(sf.invert(poses[k - 1]), poses[k]) if k else sf.Pose.identity()
+            tr.step(f, sf.Tracker.TRACK_WITH_HOOK, ext)
+            R = tr.fetch().pose.rotation
+            errs.append(np.abs(R.T @ R - np.eye(3)).max())
+        orth[fix] = errs
+    assert orth[False][25] > 1e4 * max(orth[False][3], 1e-16)  # exponential growth
+    assert max(orth[True]) < 1e-14
