@@ -157,18 +157,31 @@ struct VolParams {
     uint32_t capacity;
     int mshift;               // log2(M) when M is a power of two, else -1
     int Nc;                   // coarse occupancy lattice: ceil(N / 16) super-blocks per axis
-    uint64_t occ_fine_words;  // uint32 words of the fine (per-block) bitmap; coarse bits follow
+    uint64_t occ_fine_words;    // uint32 words of the fine (per-block) bitmap; coarse bits follow
+    uint64_t occ_coarse_words;  // uint32 words of the coarse bitmap; 6 ints of bounding box follow
 };
 
 constexpr int kCoarseShift = 4;  // super-block = 16^3 blocks
 
 // Occupancy bitmaps (fine: 1 bit per block; coarse: 1 bit per 16^3 super-block, set when
 // any block in it was ever allocated — a conservative filter, never cleared on free).
+// Block-coordinate bounding box of every block ever allocated: {xlo, ylo, zlo, xhi, yhi, zhi}
+// (empty: lo > hi). Grown on allocation, never shrunk: a conservative filter like the coarse bits.
+SF_HD const int* occ_bbox(const VolParams& P, const uint32_t* occ) {
+    return reinterpret_cast<const int*>(occ + P.occ_fine_words + P.occ_coarse_words);
+}
 __device__ __forceinline__ void occ_set(const VolParams& P, uint32_t* occ, uint64_t key) {
     atomicOr(&occ[key >> 5], 1u << (key & 31));
     const uint64_t x = key % P.N, y = (key / P.N) % P.N, z = key / ((uint64_t)P.N * P.N);
     const uint64_t c = ((z >> kCoarseShift) * P.Nc + (y >> kCoarseShift)) * P.Nc + (x >> kCoarseShift);
     atomicOr(&occ[P.occ_fine_words + (c >> 5)], 1u << (c & 31));
+    int* bb = reinterpret_cast<int*>(occ + P.occ_fine_words + P.occ_coarse_words);
+    atomicMin(&bb[0], (int)x);
+    atomicMin(&bb[1], (int)y);
+    atomicMin(&bb[2], (int)z);
+    atomicMax(&bb[3], (int)x);
+    atomicMax(&bb[4], (int)y);
+    atomicMax(&bb[5], (int)z);
 }
 
 // voxel_center (grid.cpp:271-273): origin + (vc + 0.5) * voxel_size

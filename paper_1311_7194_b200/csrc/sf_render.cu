@@ -71,46 +71,91 @@ __global__ void k_ray_bounds(VolParams P, const FrameConsts* __restrict__ fc, co
             lo = dmax(lo, t0);
             hi = dmin(hi, t1);
         }
-        if (lo <= hi) {
-            const double entry[3] = {org[0] + lo * dir[0], org[1] + lo * dir[1], org[2] + lo * dir[2]};
-            int cell[3], step[3];
-            double t_max[3], t_delta[3];
+        // Conservative reject: a ray missing the occupied bounding box (grown by one block)
+        // meets no allocated block, so its DDA would find nothing.
+        const int* bb = occ_bbox(P, occ);
+        const int bx0 = bb[0], by0 = bb[1], bz0 = bb[2], bx1 = bb[3], by1 = bb[4], bz1 = bb[5];
+        if (lo <= hi && bx0 <= bx1) {
+            double rlo = lo, rhi = hi;
+            const int bl[3] = {bx0, by0, bz0}, bh[3] = {bx1, by1, bz1};
+#pragma unroll
             for (int a = 0; a < 3; ++a) {
-                int c = ref_floor_int((entry[a] - box_lo[a]) / side);
-                c = c < 0 ? 0 : (n - 1 < c ? n - 1 : c);  // std::clamp(c, 0, n - 1)
-                cell[a] = c;
-            }
-            for (int a = 0; a < 3; ++a) {
-                if (dir[a] > 1e-15) {
-                    step[a] = 1;
-                    t_max[a] = lo + (box_lo[a] + (double)(cell[a] + 1) * side - entry[a]) / dir[a];
-                    t_delta[a] = side / dir[a];
-                } else if (dir[a] < -1e-15) {
-                    step[a] = -1;
-                    t_max[a] = lo + (box_lo[a] + (double)cell[a] * side - entry[a]) / dir[a];
-                    t_delta[a] = -side / dir[a];
-                } else {
-                    step[a] = 0;
-                    t_max[a] = INFINITY;
-                    t_delta[a] = INFINITY;
+                const double wlo = box_lo[a] + (double)(bl[a] - 1) * side;
+                const double whi = box_lo[a] + (double)(bh[a] + 2) * side;
+                if (fabs(dir[a]) < 1e-300) {
+                    if (org[a] < wlo || org[a] > whi) rhi = -INFINITY;
+                    continue;
                 }
+                double t0 = (wlo - org[a]) / dir[a], t1 = (whi - org[a]) / dir[a];
+                if (t0 > t1) {
+                    const double tmp = t0;
+                    t0 = t1;
+                    t1 = tmp;
+                }
+                rlo = dmax(rlo, t0);
+                rhi = dmin(rhi, t1);
             }
+            if (!(rlo <= rhi)) lo = 1.0, hi = 0.0;
+        }
+        if (lo <= hi && bx0 <= bx1) {
+            // Scalar (register-resident) Amanatides-Woo state; same operations as render.cpp:103-144.
+            const double ex = org[0] + lo * dir[0], ey = org[1] + lo * dir[1], ez = org[2] + lo * dir[2];
+            auto clampc = [n](int c) { return c < 0 ? 0 : (n - 1 < c ? n - 1 : c); };  // std::clamp(c, 0, n-1)
+            int cx = clampc(ref_floor_int((ex - box_lo[0]) / side));
+            int cy = clampc(ref_floor_int((ey - box_lo[1]) / side));
+            int cz = clampc(ref_floor_int((ez - box_lo[2]) / side));
+            auto init_axis = [&](double d, double blo, int c, double e, int& st, double& tm, double& td) {
+                if (d > 1e-15) {
+                    st = 1;
+                    tm = lo + (blo + (double)(c + 1) * side - e) / d;
+                    td = side / d;
+                } else if (d < -1e-15) {
+                    st = -1;
+                    tm = lo + (blo + (double)c * side - e) / d;
+                    td = -side / d;
+                } else {
+                    st = 0;
+                    tm = INFINITY;
+                    td = INFINITY;
+                }
+            };
+            int sx, sy, sz;
+            double tmx, tmy, tmz, tdx, tdy, tdz;
+            init_axis(dir[0], box_lo[0], cx, ex, sx, tmx, tdx);
+            init_axis(dir[1], box_lo[1], cy, ey, sy, tmy, tdy);
+            init_axis(dir[2], box_lo[2], cz, ez, sz, tmz, tdz);
             double first = INFINITY, last = -INFINITY;
             double t_in = lo;
             while (t_in <= hi) {
-                const int axis = t_max[0] <= t_max[1] ? (t_max[0] <= t_max[2] ? 0 : 2) : (t_max[1] <= t_max[2] ? 1 : 2);
-                const double t_out = dmin(t_max[axis], hi);
-                const int cc = ((cell[2] >> kCoarseShift) * P.Nc + (cell[1] >> kCoarseShift)) * P.Nc +
-                               (cell[0] >> kCoarseShift);
-                if (((s_coarse[cc >> 5] >> (cc & 31)) & 1u) &&
-                    occupied(occ, table_index(P, cell[0], cell[1], cell[2]))) {
-                    first = dmin(first, t_in);
-                    last = dmax(last, t_out);
+                // Past the occupied box in the direction of travel: no later cell can be
+                // allocated (cells move monotonically per axis), so first/last are final.
+                if ((sx >= 0 && cx > bx1) || (sx <= 0 && cx < bx0) || (sy >= 0 && cy > by1) || (sy <= 0 && cy < by0) ||
+                    (sz >= 0 && cz > bz1) || (sz <= 0 && cz < bz0))
+                    break;
+                const int axis = tmx <= tmy ? (tmx <= tmz ? 0 : 2) : (tmy <= tmz ? 1 : 2);
+                const double tm = axis == 0 ? tmx : (axis == 1 ? tmy : tmz);
+                const double t_out = dmin(tm, hi);
+                if (cx >= bx0 && cx <= bx1 && cy >= by0 && cy <= by1 && cz >= bz0 && cz <= bz1) {
+                    const int cc = ((cz >> kCoarseShift) * P.Nc + (cy >> kCoarseShift)) * P.Nc + (cx >> kCoarseShift);
+                    if (((s_coarse[cc >> 5] >> (cc & 31)) & 1u) && occupied(occ, table_index(P, cx, cy, cz))) {
+                        first = dmin(first, t_in);
+                        last = dmax(last, t_out);
+                    }
                 }
-                t_in = t_max[axis];
-                cell[axis] += step[axis];
-                if (cell[axis] < 0 || cell[axis] >= n) break;
-                t_max[axis] += t_delta[axis];
+                t_in = tm;
+                if (axis == 0) {
+                    cx += sx;
+                    if (cx < 0 || cx >= n) break;
+                    tmx += tdx;
+                } else if (axis == 1) {
+                    cy += sy;
+                    if (cy < 0 || cy >= n) break;
+                    tmy += tdy;
+                } else {
+                    cz += sz;
+                    if (cz < 0 || cz >= n) break;
+                    tmz += tdz;
+                }
             }
             if (first <= last) {
                 ts = (float)dmax(first, lo);
@@ -171,18 +216,14 @@ struct Sampler {
 
     // sample_tsdf_gradient (render.cpp:50-63)
     __device__ bool gradient(d3 p, double h, d3& g) const {
-        double gv[3];
-        const double pc[3] = {p.x, p.y, p.z};
-        for (int i = 0; i < 3; ++i) {
-            double dp[3] = {pc[0], pc[1], pc[2]}, dm[3] = {pc[0], pc[1], pc[2]};
-            dp[i] += h;
-            dm[i] -= h;
-            double a, b;
-            if (!sample(mk(dp[0], dp[1], dp[2]), a)) return false;
-            if (!sample(mk(dm[0], dm[1], dm[2]), b)) return false;
-            gv[i] = (a - b) / (2.0 * h);
-        }
-        g = mk(gv[0], gv[1], gv[2]);
+        double a, b;
+        if (!sample(mk(p.x + h, p.y, p.z), a) || !sample(mk(p.x - h, p.y, p.z), b)) return false;
+        const double gx = (a - b) / (2.0 * h);
+        if (!sample(mk(p.x, p.y + h, p.z), a) || !sample(mk(p.x, p.y - h, p.z), b)) return false;
+        const double gy = (a - b) / (2.0 * h);
+        if (!sample(mk(p.x, p.y, p.z + h), a) || !sample(mk(p.x, p.y, p.z - h), b)) return false;
+        const double gz = (a - b) / (2.0 * h);
+        g = mk(gx, gy, gz);
         return true;
     }
 };

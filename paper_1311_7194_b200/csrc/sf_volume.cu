@@ -275,6 +275,8 @@ static VolParams make_params(const sf_grid_config& c, const sf_aux_quant& a, uin
     for (int b = 0; b < 16; ++b)
         if ((1 << b) == P.M) P.mshift = b;
     P.occ_fine_words = (P.table_size + 31) / 32;
+    const uint64_t nc = static_cast<uint64_t>(P.Nc);
+    P.occ_coarse_words = (nc * nc * nc + 31) / 32;
     return P;
 }
 
@@ -309,13 +311,17 @@ static void volume_init_device(Volume& v) {
     SF_CUDA(cudaMalloc(&v.d_payload, std::max<uint64_t>(pool_voxels, 1) * sizeof(uint16_t)));
     SF_CUDA(cudaMalloc(&v.d_free_list, std::max<uint32_t>(P.capacity, 1) * sizeof(int32_t)));
     SF_CUDA(cudaMalloc(&v.d_slot_key, std::max<uint32_t>(P.capacity, 1) * sizeof(int32_t)));
-    const uint64_t nc = static_cast<uint64_t>(P.Nc);
-    const uint64_t occ_words = P.occ_fine_words + (nc * nc * nc + 31) / 32;
+    const uint64_t occ_words = P.occ_fine_words + P.occ_coarse_words + 6;  // + bounding box
     SF_CUDA(cudaMalloc(&v.d_occ, occ_words * sizeof(uint32_t)));
     SF_CUDA(cudaMalloc(&v.d_vc, sizeof(VolCounters)));
     SF_CUDA(cudaMalloc(&v.d_aux, sizeof(AuxTables)));
     SF_CUDA(cudaMemset(v.d_table, 0xFF, P.table_size * sizeof(int32_t)));
     SF_CUDA(cudaMemset(v.d_occ, 0, occ_words * sizeof(uint32_t)));
+    {
+        const int empty_bb[6] = {INT32_MAX, INT32_MAX, INT32_MAX, -1, -1, -1};
+        SF_CUDA(cudaMemcpy(v.d_occ + P.occ_fine_words + P.occ_coarse_words, empty_bb, sizeof(empty_bb),
+                           cudaMemcpyHostToDevice));
+    }
     int blocks;
     grid_for(pool_voxels, blocks);
     k_fill_u16<<<blocks, 256>>>(v.d_payload, pool_voxels, kChiPayload);
