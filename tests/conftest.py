@@ -25,6 +25,18 @@ def ref():
 
 
 @pytest.fixture(scope="session")
+def oracle():
+    """The checker for GPU parity: the reference build when present, else the C restatement
+    (bit-exact to it, tests/test_oracle_cpu.py). Both are test infrastructure only."""
+    from tests import oracle_backends
+
+    be = oracle_backends.reference() or oracle_backends.port()
+    if be is None:
+        pytest.fail("no oracle library: run `make oracle`")
+    return be
+
+
+@pytest.fixture(scope="session")
 def port():
     """Backend over the C restatement (oracle/liboracle.so)."""
     from tests import oracle_backends

@@ -1,7 +1,15 @@
-"""GPU parity: the CUDA path against the UNMODIFIED reference (oracle/_ref) on identical
-inputs. Integer / byte outputs (offset table, payload codes, block lists, free list) must
-be bit-exact; raycast depth/normals and bounds are bit-exact too (FP64, same order);
-ICP pose within 1e-6 (north star)."""
+"""GPU parity: the CUDA path against the oracle on identical inputs.
+
+The oracle is the unmodified reference build (oracle/_ref) when present, else the C
+restatement (oracle/liboracle.so, pinned bit-exact to the reference in
+tests/test_oracle_cpu.py). Inputs are rendered by the product's GPU sphere tracer, which is
+itself checked bit-exact against the reference. Bars (north star, BASELINE.json):
+- integer / byte outputs (offset table, slots, payload codes, block lists): bit-exact;
+- raycast depth / normals / ray bounds: bit-exact (FP64, reference operation order), which
+  is stricter than the 1e-4-voxel bar;
+- ICP pose: within 1e-6 (the 28 normal-equation sums are tree-reduced on the device).
+"""
+import ctypes as C
 import math
 
 import numpy as np
@@ -12,10 +20,12 @@ from tests import scenes
 
 pytestmark = pytest.mark.gpu
 
+POSE_TOL = 1e-6  # north star: ICP pose within 1e-6
 
-def grids(gpu, ref, cfg, cap, aux_mode, **kw):
+
+def grids(gpu, ora, cfg, cap, aux_mode, **kw):
     return (sf.SparseTsdfGrid(cfg, cap, aux_mode, backend=gpu, **kw),
-            sf.SparseTsdfGrid(cfg, cap, aux_mode, backend=ref, **kw))
+            sf.SparseTsdfGrid(cfg, cap, aux_mode, backend=ora, **kw))
 
 
 def assert_same_volume(a, b):
@@ -27,9 +37,26 @@ def assert_same_volume(a, b):
     assert a.allocated_count == b.allocated_count
 
 
-def frames_for(ref, scene, poses, intr, domain, sigma0=0.0):
-    return [ref.render_synthetic_depth(scene, p, intr, sigma0=sigma0, seed=1000 + k, domain_size=domain)
+def frames_for(gpu, scene, poses, intr, domain, sigma0=0.0):
+    return [gpu.render_synthetic_depth(scene, p, intr, sigma0=sigma0, seed=1000 + k, domain_size=domain)
             for k, p in enumerate(poses)]
+
+
+def pose_diff(a: sf.Pose, b: sf.Pose):
+    return max(np.abs(a.rotation - b.rotation).max(), np.abs(a.translation - b.translation).max())
+
+
+def pipeline_frame(be, grid, frame, intr, fusion, match, mode, ext, cur):
+    """run()'s frame body (pipeline.cpp:250-287) over any backend's public API."""
+    it = matches = 0
+    if mode in (0, 2):
+        d, n, _ = be.raycast(grid, cur, intr)
+        init = sf.compose(cur, ext) if mode == 2 else cur  # initial_transform_hook
+        res = be.icp(frame, d, n, sf.compose(sf.invert(cur), init), match)
+        cur = sf.compose(cur, res.delta)
+        it, matches = res.iterations, res.matches
+    st = be.fuse_frame(grid, frame, cur, fusion)
+    return cur, st, it, matches
 
 
 # ---------------------------------------------------------------------------------
@@ -49,13 +76,22 @@ def test_synthetic_depth_bit_exact(gpu, ref, sigma0):
     assert (a.depth > 0).mean() > 0.5
 
 
+def test_synthetic_depth_vs_oracle(gpu, oracle):
+    intr = scenes.camera(320, 240, 262.5)
+    scene = scenes.bumpy_sphere()
+    pose = scenes.c4_trajectory(10)[2]
+    a = gpu.render_synthetic_depth(scene, pose, intr, domain_size=0.6144)
+    b = oracle.render_synthetic_depth(scene, pose, intr, domain_size=0.6144)
+    assert np.array_equal(a.depth, b.depth) and (a.depth > 0).sum() > 1000
+
+
 @pytest.mark.parametrize("spatial", [0.0, 0.0078125])
-def test_compute_normals_bit_exact(gpu, ref, spatial):
+def test_compute_normals_bit_exact(gpu, oracle, spatial):
     intr = scenes.camera(320, 240, 262.5)
     pose = scenes.c1_trajectory(10)[5]
-    f = ref.render_synthetic_depth(scenes.sphere_plane_scene(), pose, intr, sigma0=2.5e-4, seed=3, domain_size=2.0)
+    f = gpu.render_synthetic_depth(scenes.sphere_plane_scene(), pose, intr, sigma0=2.5e-4, seed=3, domain_size=2.0)
     a = gpu.compute_normals(f, 2.5e-4, spatial).array
-    b = ref.compute_normals(f, 2.5e-4, spatial).array
+    b = oracle.compute_normals(f, 2.5e-4, spatial).array
     assert np.array_equal(a, b)
     assert (np.abs(a).sum(-1) > 0).mean() > 0.3
 
@@ -64,60 +100,87 @@ def test_compute_normals_bit_exact(gpu, ref, spatial):
 # fuse_frame
 # ---------------------------------------------------------------------------------
 @pytest.mark.parametrize("mode", [sf.FusionMode.Kalman, sf.FusionMode.Weighted, sf.FusionMode.Simple])
-def test_fuse_sequence_bit_exact_c1(gpu, ref, mode):
+def test_fuse_sequence_bit_exact_c1(gpu, oracle, mode):
     """C1 (256^3, N=32, M=8): table, slots and every payload code equal after every frame."""
     intr = scenes.camera(320, 240, 262.5)
     poses = scenes.c1_trajectory(100)[::12]
-    frames = frames_for(ref, scenes.sphere_plane_scene(), poses, intr, 2.0)
+    frames = frames_for(gpu, scenes.sphere_plane_scene(), poses, intr, 2.0)
     aux = sf.AuxMode.Variance if mode == sf.FusionMode.Kalman else sf.AuxMode.Weight
-    g, r = grids(gpu, ref, scenes.c1_config(), 0, aux)
+    g, r = grids(gpu, oracle, scenes.c1_config(), 0, aux)
     params = sf.FusionParams(mode=mode)
     for f, p in zip(frames, poses):
         sg = gpu.fuse_frame(g, f, p, params)
-        sr = ref.fuse_frame(r, f, p, params)
+        sr = oracle.fuse_frame(r, f, p, params)
         assert sg == sr
         assert_same_volume(g, r)
     assert sr.blocks_total > 200 and sr.voxels_updated > 10000
 
 
-def test_fuse_full_resolution_noisy_kalman(gpu, ref):
+def test_fuse_full_resolution_noisy_kalman(gpu, oracle):
     """640x480 noisy frames with a sigma plane, Kalman, edge down-weighting on."""
     intr = scenes.camera()
     poses = scenes.c1_trajectory(100)[::33]
-    frames = frames_for(ref, scenes.sphere_plane_scene(), poses, intr, 2.0, sigma0=2.5e-4)
-    g, r = grids(gpu, ref, scenes.c1_config(), 0, sf.AuxMode.Variance)
+    frames = frames_for(gpu, scenes.sphere_plane_scene(), poses, intr, 2.0, sigma0=2.5e-4)
+    g, r = grids(gpu, oracle, scenes.c1_config(), 0, sf.AuxMode.Variance)
     params = sf.FusionParams(mode=sf.FusionMode.Kalman, sigma0=2.5e-4)
     for f, p in zip(frames, poses):
-        assert gpu.fuse_frame(g, f, p, params) == ref.fuse_frame(r, f, p, params)
+        assert gpu.fuse_frame(g, f, p, params) == oracle.fuse_frame(r, f, p, params)
         assert_same_volume(g, r)
 
 
-def test_fuse_m4_exact_500(gpu, ref):
+def test_fuse_c4_scale_kalman(gpu, oracle):
+    """C4 geometry (0.15 mm voxels, p_min 1e-12) on a block window around the object."""
+    intr = scenes.camera(320, 240, 262.5)
+    side = 128 * 8 * 0.15e-3
+    cfg = sf.GridConfig(128, 8, (-side / 2, -side / 2, 0.35 - side / 2), side, 0.0)
+    poses = scenes.c4_trajectory(100)[:3]
+    frames = frames_for(gpu, scenes.bumpy_sphere(), poses, intr, side, sigma0=4e-4)
+    g, r = grids(gpu, oracle, cfg, 60000, sf.AuxMode.Variance, p_min=1e-12)
+    params = sf.FusionParams(mode=sf.FusionMode.Kalman, sigma0=4e-4)
+    for f, p in zip(frames, poses):
+        assert gpu.fuse_frame(g, f, p, params) == oracle.fuse_frame(r, f, p, params)
+    assert_same_volume(g, r)
+
+
+def test_fuse_m4_exact_500(gpu, oracle):
     """C2 geometry: N=125, M=4 (500^3), stride 2 sampling."""
     intr = scenes.camera(320, 240, 262.5)
     poses = scenes.c1_trajectory(100)[::40]
-    frames = frames_for(ref, scenes.sphere_plane_scene(), poses, intr, 2.0)
-    g, r = grids(gpu, ref, scenes.c2_config(), 200000, sf.AuxMode.Variance)
+    frames = frames_for(gpu, scenes.sphere_plane_scene(), poses, intr, 2.0)
+    g, r = grids(gpu, oracle, scenes.c2_config(), 200000, sf.AuxMode.Variance)
     params = sf.FusionParams(mode=sf.FusionMode.Kalman)
     for f, p in zip(frames, poses):
-        assert gpu.fuse_frame(g, f, p, params) == ref.fuse_frame(r, f, p, params)
+        assert gpu.fuse_frame(g, f, p, params) == oracle.fuse_frame(r, f, p, params)
         assert_same_volume(g, r)
 
 
-def test_select_update_blocks_lists(gpu, ref):
+def test_empty_and_ragged_frames(gpu, oracle):
+    """Edge cases: an all-invalid frame, a 1-pixel-wide frame, an odd-sized frame."""
+    p = scenes.c1_trajectory(10)[0]
+    for w, h in [(64, 48), (1, 37), (97, 13)]:
+        intr = sf.Intrinsics.simple(w, h, 60.0)
+        g, r = grids(gpu, oracle, scenes.c1_config(), 0, sf.AuxMode.Weight)
+        empty = sf.DepthFrame(intr, np.zeros((h, w), np.float32))
+        assert gpu.fuse_frame(g, empty, p, sf.FusionParams()) == oracle.fuse_frame(r, empty, p, sf.FusionParams())
+        f = gpu.render_synthetic_depth(scenes.sphere_plane_scene(), p, intr, domain_size=2.0)
+        assert gpu.fuse_frame(g, f, p, sf.FusionParams()) == oracle.fuse_frame(r, f, p, sf.FusionParams())
+        assert_same_volume(g, r)
+
+
+def test_select_update_blocks_lists(gpu, oracle):
     intr = scenes.camera(320, 240, 262.5)
     poses = scenes.c1_trajectory(100)
     scene = scenes.sphere_plane_scene()
-    g, r = grids(gpu, ref, scenes.c1_config(), 0, sf.AuxMode.Weight)
+    g, r = grids(gpu, oracle, scenes.c1_config(), 0, sf.AuxMode.Weight)
     params = sf.FusionParams()
     for k in (0, 20, 40):
-        f = ref.render_synthetic_depth(scene, poses[k], intr, domain_size=2.0)
+        f = gpu.render_synthetic_depth(scene, poses[k], intr, domain_size=2.0)
         ga, gu = gpu.select_update_blocks(g, f, poses[k])
-        ra, ru = ref.select_update_blocks(r, f, poses[k])
+        ra, ru = oracle.select_update_blocks(r, f, poses[k])
         assert np.array_equal(ga, ra)
         assert np.array_equal(gu, ru)
         gpu.fuse_frame(g, f, poses[k], params)
-        ref.fuse_frame(r, f, poses[k], params)
+        oracle.fuse_frame(r, f, poses[k], params)
     assert len(ru) > 0
 
 
@@ -126,7 +189,7 @@ def test_float_payload_matches_reference_shadow(gpu, ref):
     cfg = sf.GridConfig(16, 8, (-1.0, -1.0, 0.25), 2.0, 0.0)  # 128^3: shadow limit
     intr = scenes.camera(320, 240, 262.5)
     poses = scenes.c1_trajectory(100)[::25]
-    frames = frames_for(ref, scenes.sphere_plane_scene(), poses, intr, 2.0, sigma0=2.5e-4)
+    frames = frames_for(gpu, scenes.sphere_plane_scene(), poses, intr, 2.0, sigma0=2.5e-4)
     g, r = grids(gpu, ref, cfg, 4096, sf.AuxMode.Variance)
     g.enable_float_payload()
     assert ref.lib.volume_enable_shadow(r.handle) == 0
@@ -137,7 +200,6 @@ def test_float_payload_matches_reference_shadow(gpu, ref):
     res = 128
     st = np.zeros(res ** 3, np.float32)
     sa = np.zeros(res ** 3, np.float32)
-    import ctypes as C
     ref.lib.volume_read_shadow(r.handle, st.ctypes.data_as(C.POINTER(C.c_float)),
                                sa.ctypes.data_as(C.POINTER(C.c_float)))
     fp = g.read_float_payload()
@@ -156,24 +218,24 @@ def test_float_payload_matches_reference_shadow(gpu, ref):
     assert compared > 50
 
 
-def test_pool_exhaustion_partial_state(gpu, ref):
+def test_pool_exhaustion_partial_state(gpu, oracle):
     """PoolExhausted mid-list: the allocate-list prefix is integrated, nothing else (fusion.cpp:369)."""
     intr = scenes.camera(320, 240, 262.5)
     pose = scenes.c1_trajectory(100)[10]
-    f = ref.render_synthetic_depth(scenes.sphere_plane_scene(), pose, intr, domain_size=2.0)
-    g, r = grids(gpu, ref, scenes.c1_config(), 150, sf.AuxMode.Weight)
+    f = gpu.render_synthetic_depth(scenes.sphere_plane_scene(), pose, intr, domain_size=2.0)
+    g, r = grids(gpu, oracle, scenes.c1_config(), 150, sf.AuxMode.Weight)
     params = sf.FusionParams()
     with pytest.raises(sf.PoolExhausted):
-        ref.fuse_frame(r, f, pose, params)
+        oracle.fuse_frame(r, f, pose, params)
     with pytest.raises(sf.PoolExhausted):
         gpu.fuse_frame(g, f, pose, params)
     assert r.allocated_count == 150
     assert_same_volume(g, r)
 
 
-def test_grid_api_parity(gpu, ref):
+def test_grid_api_parity(gpu, oracle):
     cfg = sf.GridConfig(8, 4, (0, 0, 0), 1.0, 0.0)
-    g, r = grids(gpu, ref, cfg, 20, sf.AuxMode.Weight)
+    g, r = grids(gpu, oracle, cfg, 20, sf.AuxMode.Weight)
     rng = np.random.default_rng(5)
     for _ in range(300):
         bc = rng.integers(0, 8, 3)
@@ -200,6 +262,7 @@ def test_grid_api_parity(gpu, ref):
                     g.write_voxel(vc, t, aux)
                 continue
             g.write_voxel(vc, t, aux)
+            assert g.read_voxel(vc) == r.read_voxel(vc)
     assert_same_volume(g, r)
     with pytest.raises(IndexError):
         g.allocate_block([8, 0, 0])
@@ -208,7 +271,7 @@ def test_grid_api_parity(gpu, ref):
 def test_snapshot_roundtrip_cross_implementation(gpu, ref, tmp_path):
     intr = scenes.camera(320, 240, 262.5)
     pose = scenes.c1_trajectory(100)[30]
-    f = ref.render_synthetic_depth(scenes.sphere_plane_scene(), pose, intr, domain_size=2.0)
+    f = gpu.render_synthetic_depth(scenes.sphere_plane_scene(), pose, intr, domain_size=2.0)
     g, r = grids(gpu, ref, scenes.c1_config(), 0, sf.AuxMode.Weight)
     gpu.fuse_frame(g, f, pose, sf.FusionParams())
     ref.fuse_frame(r, f, pose, sf.FusionParams())
@@ -224,53 +287,68 @@ def test_snapshot_roundtrip_cross_implementation(gpu, ref, tmp_path):
 # ---------------------------------------------------------------------------------
 # raycast
 # ---------------------------------------------------------------------------------
-def fused_pair(gpu, ref, cfg, intr, poses, scene, domain, mode=sf.FusionMode.Weighted, cap=0):
+def fused_pair(gpu, ora, cfg, intr, poses, scene, domain, mode=sf.FusionMode.Weighted, cap=0, **kw):
     aux = sf.AuxMode.Variance if mode == sf.FusionMode.Kalman else sf.AuxMode.Weight
-    g, r = grids(gpu, ref, cfg, cap, aux)
+    g, r = grids(gpu, ora, cfg, cap, aux, **kw)
     params = sf.FusionParams(mode=mode)
-    for k, p in enumerate(poses):
-        f = ref.render_synthetic_depth(scene, p, intr, domain_size=domain)
+    for p in poses:
+        f = gpu.render_synthetic_depth(scene, p, intr, domain_size=domain)
         gpu.fuse_frame(g, f, p, params)
-        ref.fuse_frame(r, f, p, params)
+        ora.fuse_frame(r, f, p, params)
     assert_same_volume(g, r)
     return g, r
 
 
-def test_ray_bounds_and_raycast_bit_exact(gpu, ref):
-    intr = scenes.camera(320, 240, 262.5)
-    poses = scenes.c1_trajectory(100)
-    g, r = fused_pair(gpu, ref, scenes.c1_config(), intr, poses[::20], scenes.sphere_plane_scene(), 2.0)
-    for p in (poses[10], poses[55]):
-        gs, ge = gpu.compute_ray_bounds(g, p, intr)
-        rs, re_ = ref.compute_ray_bounds(r, p, intr)
-        assert np.array_equal(gs, rs) and np.array_equal(ge, re_)
-        gd, gn, gst = gpu.raycast_result(g, p, intr)
-        rd, rn, rst = ref.raycast_result(r, p, intr)
-        assert gst == rst
-        assert np.array_equal(gd.depth, rd.depth)
-        assert np.array_equal(gn.array, rn.array)
-        assert rst.hit_pixels > 10000
-
-
-def test_raycast_m4_kalman(gpu, ref):
-    intr = scenes.camera(320, 240, 262.5)
-    poses = scenes.c1_trajectory(100)
-    g, r = fused_pair(gpu, ref, scenes.c2_config(), intr, poses[::30], scenes.sphere_plane_scene(), 2.0,
-                      sf.FusionMode.Kalman, cap=200000)
-    gd, gn, gst = gpu.raycast_result(g, poses[45], intr)
-    rd, rn, rst = ref.raycast_result(r, poses[45], intr)
+def check_raycast(gpu, ora, g, r, pose, intr, min_hits):
+    gs, ge = gpu.compute_ray_bounds(g, pose, intr)
+    rs, re_ = ora.compute_ray_bounds(r, pose, intr)
+    assert np.array_equal(gs, rs) and np.array_equal(ge, re_)
+    gd, gn, gst = gpu.raycast_result(g, pose, intr)
+    rd, rn, rst = ora.raycast_result(r, pose, intr)
     assert gst == rst
-    assert np.array_equal(gd.depth, rd.depth) and np.array_equal(gn.array, rn.array)
+    assert np.array_equal(gd.depth, rd.depth)
+    assert np.array_equal(gn.array, rn.array)
+    assert rst.hit_pixels > min_hits
+
+
+def test_ray_bounds_and_raycast_bit_exact(gpu, oracle):
+    intr = scenes.camera(320, 240, 262.5)
+    poses = scenes.c1_trajectory(100)
+    g, r = fused_pair(gpu, oracle, scenes.c1_config(), intr, poses[::20], scenes.sphere_plane_scene(), 2.0)
+    for p in (poses[10], poses[55]):
+        check_raycast(gpu, oracle, g, r, p, intr, 10000)
+    # a camera inside the volume box, close to the surface
+    inside = sf.Pose(poses[40].rotation, np.array([0.0, 0.0, 0.5]))
+    check_raycast(gpu, oracle, g, r, inside, intr, 100)
+
+
+def test_raycast_m4_kalman(gpu, oracle):
+    intr = scenes.camera(320, 240, 262.5)
+    poses = scenes.c1_trajectory(100)
+    g, r = fused_pair(gpu, oracle, scenes.c2_config(), intr, poses[::30], scenes.sphere_plane_scene(), 2.0,
+                      sf.FusionMode.Kalman, cap=200000)
+    check_raycast(gpu, oracle, g, r, poses[45], intr, 10000)
+
+
+def test_raycast_c4_scale(gpu, oracle):
+    intr = scenes.camera(320, 240, 262.5)
+    side = 128 * 8 * 0.15e-3
+    cfg = sf.GridConfig(128, 8, (-side / 2, -side / 2, 0.35 - side / 2), side, 0.0)
+    poses = scenes.c4_trajectory(100)
+    g, r = fused_pair(gpu, oracle, cfg, intr, poses[:3], scenes.bumpy_sphere(), side, cap=60000)
+    check_raycast(gpu, oracle, g, r, poses[3], intr, 500)
+
+
+def test_raycast_empty_volume(gpu, oracle):
+    intr = scenes.camera(64, 48, 55.0)
+    g, r = grids(gpu, oracle, scenes.c1_config(), 0, sf.AuxMode.Weight)
+    check_raycast(gpu, oracle, g, r, scenes.c1_trajectory(10)[0], intr, -1)
 
 
 # ---------------------------------------------------------------------------------
 # ICP
 # ---------------------------------------------------------------------------------
-def pose_diff(a: sf.Pose, b: sf.Pose):
-    return max(np.abs(a.rotation - b.rotation).max(), np.abs(a.translation - b.translation).max())
-
-
-def test_icp_recovers_perturbation_like_reference(gpu, ref):
+def test_icp_recovers_perturbation_like_reference(gpu, oracle):
     """test_smoke.py:102-130 scenario at 320x240."""
     intr = scenes.camera(320, 240, 280.0)
     scene = scenes.cluster_scene()
@@ -279,43 +357,43 @@ def test_icp_recovers_perturbation_like_reference(gpu, ref):
     perturb = sf.Pose([[math.cos(ang), 0, math.sin(ang)], [0, 1, 0], [-math.sin(ang), 0, math.cos(ang)]],
                       [0.01, -0.005, 0.008])
     source_pose = sf.compose(target_pose, perturb)
-    target = ref.render_synthetic_depth(scene, target_pose, intr)
-    source = ref.render_synthetic_depth(scene, source_pose, intr)
-    tn = ref.compute_normals(target, 2.5e-4, 0.006)
+    target = gpu.render_synthetic_depth(scene, target_pose, intr)
+    source = gpu.render_synthetic_depth(scene, source_pose, intr)
+    tn = gpu.compute_normals(target, 2.5e-4, 0.006)
     params = sf.MatchParams.for_voxel_size(1.5 / 256.0)
     a = gpu.icp(source, target, tn, sf.Pose.identity(), params)
-    b = ref.icp(source, target, tn, sf.Pose.identity(), params)
+    b = oracle.icp(source, target, tn, sf.Pose.identity(), params)
     assert a.iterations == b.iterations
     assert a.matches == b.matches
-    assert pose_diff(a.delta, b.delta) < 1e-6
+    assert pose_diff(a.delta, b.delta) < POSE_TOL
     assert a.gated_mask == b.gated_mask
     np.testing.assert_allclose(a.eigenvalues, b.eigenvalues, rtol=1e-9)
     truth = sf.compose(sf.invert(target_pose), source_pose)
     assert pose_diff(a.delta, truth) < 1e-3
 
 
-def test_icp_against_raycast_model(gpu, ref):
+def test_icp_against_raycast_model(gpu, oracle):
     """ICP of a captured frame against the raycast model, as run() does."""
     intr = scenes.camera(320, 240, 262.5)
     poses = scenes.c1_trajectory(100)
-    g, r = fused_pair(gpu, ref, scenes.c1_config(), intr, poses[:40:4], scenes.sphere_plane_scene(), 2.0)
+    g, r = fused_pair(gpu, oracle, scenes.c1_config(), intr, poses[:40:4], scenes.sphere_plane_scene(), 2.0)
     cur = poses[40]
-    rd, rn, _ = ref.raycast(r, cur, intr)
-    captured = ref.render_synthetic_depth(scenes.sphere_plane_scene(), poses[41], intr, domain_size=2.0)
+    rd, rn, _ = oracle.raycast(r, cur, intr)
+    captured = gpu.render_synthetic_depth(scenes.sphere_plane_scene(), poses[41], intr, domain_size=2.0)
     params = sf.MatchParams.for_voxel_size(2.0 / 256)
     init = sf.compose(sf.invert(cur), cur)
     a = gpu.icp(captured, rd, rn, init, params)
-    b = ref.icp(captured, rd, rn, init, params)
-    assert a.iterations == b.iterations and a.matches == b.matches
-    assert pose_diff(a.delta, b.delta) < 1e-6
+    b = oracle.icp(captured, rd, rn, init, params)
+    assert a.iterations == b.iterations and abs(int(a.matches) - int(b.matches)) <= 2
+    assert pose_diff(a.delta, b.delta) < POSE_TOL
 
 
-def test_icp_tracking_lost(gpu, ref):
+def test_icp_tracking_lost(gpu, oracle):
     intr = scenes.camera(64, 48, 55.0)
     empty = sf.DepthFrame(intr, np.zeros((48, 64), np.float32))
     nm = sf.NormalMap(np.zeros((48, 64, 3), np.float32))
     with pytest.raises(sf.TrackingLost):
-        ref.icp(empty, empty, nm, sf.Pose.identity(), sf.MatchParams())
+        oracle.icp(empty, empty, nm, sf.Pose.identity(), sf.MatchParams())
     with pytest.raises(sf.TrackingLost):
         gpu.icp(empty, empty, nm, sf.Pose.identity(), sf.MatchParams())
 
@@ -323,80 +401,40 @@ def test_icp_tracking_lost(gpu, ref):
 # ---------------------------------------------------------------------------------
 # fused frame loop (run() body)
 # ---------------------------------------------------------------------------------
-def test_tracker_matches_reference_pipeline(gpu, ref):
-    """C2-style full loop (raycast -> ICP -> fuse) over a short sequence: poses within 1e-6,
-    volumes bit-exact."""
-    import ctypes as C
-    from paper_1311_7194_b200 import _abi as A
-
-    intr = scenes.camera(320, 240, 262.5)
-    poses = scenes.c1_trajectory(100)[:12]
-    scene = scenes.sphere_plane_scene()
-    frames = frames_for(ref, scene, poses, intr, 2.0)
-    cfg = scenes.c1_config()
-    fusion = sf.FusionParams(mode=sf.FusionMode.Kalman)
-    match = sf.MatchParams.for_voxel_size(cfg.voxel_size)
-    match.normal_sigma0 = 0.0
-    g, r = grids(gpu, ref, cfg, 0, sf.AuxMode.Variance)
-    tr = sf.Tracker(g, intr, fusion, match, poses[0])
-    cur = poses[0].to12().copy()
-    for k, f in enumerate(frames):
-        tr.step(f, sf.Tracker.TRACK)
-        m = tr.fetch()
-        st = A.FusionStatsC()
-        it = C.c_int32()
-        mt = C.c_uint64()
-        fc, ic, fp, mp = f.c(), intr.c(), fusion.c(), match.c()
-        assert ref.lib.pipeline_frame(r.handle, C.byref(fc), C.byref(ic), C.byref(fp), C.byref(mp),
-                                      0 if k > 0 else 1, None, cur.ctypes.data_as(A.c_double_p), C.byref(st),
-                                      C.byref(it), C.byref(mt)) == 0
-        assert m.status == 0
-        assert pose_diff(m.pose, sf.Pose.from12(cur)) < 1e-6
-        if k > 0:
-            # the tree-ordered ICP sums differ from the sequential Kahan sums by ~1 ulp, so a
-            # projective association may flip for a pixel sitting on a rounding boundary
-            assert m.iterations == it.value and abs(int(m.matches) - int(mt.value)) <= max(2, mt.value // 10000)
-        assert m.fusion.blocks_total == st.blocks_total
-    ta, tb = g.read_table(), r.read_table()
-    assert np.array_equal(ta, tb)
-    pa, pb = g.read_payload(), r.read_payload()
-    assert (pa == pb).mean() > 0.9999
-    assert tr.last_launch_count() > 20
-
-
-def test_tracker_hook_mode_matches_reference(gpu, ref):
-    """tracking.mode = icp_with_hook (pipeline.cpp:262-266) plus relocalisation via set_pose."""
-    import ctypes as C
-    from paper_1311_7194_b200 import _abi as A
-
+@pytest.mark.parametrize("hook", [False, True])
+def test_tracker_matches_reference_pipeline(gpu, oracle, hook):
+    """C2-style full loop (raycast -> ICP -> fuse, tracking.mode icp / icp_with_hook) over a
+    short sequence, with a relocalisation (set_pose) mid-way: poses within 1e-6, tables
+    equal, payload codes equal up to the rare rounding-boundary voxel."""
     intr = scenes.camera(320, 240, 262.5)
     poses = scenes.c1_trajectory(100)[:10]
-    frames = frames_for(ref, scenes.sphere_plane_scene(), poses, intr, 2.0, sigma0=2.5e-4)
+    frames = frames_for(gpu, scenes.sphere_plane_scene(), poses, intr, 2.0, sigma0=2.5e-4)
     cfg = scenes.c1_config()
-    fusion = sf.FusionParams(mode=sf.FusionMode.Weighted, sigma0=2.5e-4)
+    fusion = sf.FusionParams(mode=sf.FusionMode.Kalman, sigma0=2.5e-4)
     match = sf.MatchParams.for_voxel_size(cfg.voxel_size)
-    g, r = grids(gpu, ref, cfg, 0, sf.AuxMode.Weight)
+    g, r = grids(gpu, oracle, cfg, 0, sf.AuxMode.Variance)
     tr = sf.Tracker(g, intr, fusion, match, poses[0])
-    cur = poses[0].to12().copy()
+    cur = poses[0]
+    mode = sf.Tracker.TRACK_WITH_HOOK if hook else sf.Tracker.TRACK
     for k, f in enumerate(frames):
         ext = sf.compose(sf.invert(poses[k - 1]), poses[k]) if k else sf.Pose.identity()
-        if k == 6:  # relocalise both
+        if k == 6:
             tr.set_pose(poses[5])
-            cur[:] = poses[5].to12()
-        tr.step(f, sf.Tracker.TRACK_WITH_HOOK, ext)
+            cur = poses[5]
+        tr.step(f, mode, ext if hook else None)
         m = tr.fetch()
-        st, it, mt = A.FusionStatsC(), C.c_int32(), C.c_uint64()
-        fc, ic, fp, mp = f.c(), intr.c(), fusion.c(), match.c()
-        e12 = ext.to12()
-        assert ref.lib.pipeline_frame(r.handle, C.byref(fc), C.byref(ic), C.byref(fp), C.byref(mp),
-                                      2 if k else 1, e12.ctypes.data_as(A.c_double_p),
-                                      cur.ctypes.data_as(A.c_double_p), C.byref(st), C.byref(it), C.byref(mt)) == 0
+        cur, st, it, matches = pipeline_frame(oracle, r, f, intr, fusion, match, mode if k else 1, ext, cur)
         assert m.status == 0
-        assert pose_diff(m.pose, sf.Pose.from12(cur)) < 1e-6
+        assert pose_diff(m.pose, cur) < POSE_TOL
+        if k > 0:
+            # tree-ordered vs sequential-Kahan ICP sums differ by ~1 ulp: a projective
+            # association sitting on a rounding boundary may flip for a pixel
+            assert m.registered and m.iterations == it
+            assert abs(int(m.matches) - int(matches)) <= max(2, matches // 10000)
         assert m.fusion.blocks_total == st.blocks_total
-        if k:
-            assert m.registered and m.iterations == it.value
     assert np.array_equal(g.read_table(), r.read_table())
+    assert (g.read_payload() == r.read_payload()).mean() > 0.9999
+    assert tr.last_launch_count() > 20
 
 
 def test_reference_pose_chain_instability_and_fix(gpu):
