@@ -19,7 +19,7 @@ OBJS    := $(addprefix $(OBJ_DIR)/,$(addsuffix .o,$(SRCS)))
 HDRS    := $(wildcard $(SRC_DIR)/*.h $(SRC_DIR)/*.cuh) include/sf_gpu.h
 LIB     := $(OUT_DIR)/libsf_gpu.so
 
-.PHONY: all lib oracle clean
+.PHONY: all lib oracle clean cpptests
 all: lib
 lib: $(LIB)
 
@@ -37,3 +37,11 @@ oracle:
 
 clean:
 	rm -rf build $(LIB)
+
+# C++ conformance cases over include/sparsefusion_gpu.hpp (run on a GPU by tests/test_gpu_cpp_api.py)
+CPPTEST := tests/cpp/_build/test_gpu_api
+cpptests: $(CPPTEST)
+$(CPPTEST): tests/cpp/test_gpu_api.cpp include/sparsefusion_gpu.hpp include/sf_gpu.h $(LIB)
+	@mkdir -p tests/cpp/_build
+	g++ -std=c++17 -O2 -ffp-contract=off -Iinclude -Ioracle/shim $< -L$(OUT_DIR) -lsf_gpu \
+	    -Wl,-rpath,'$$ORIGIN/../../../$(OUT_DIR)' -o $@
