@@ -165,7 +165,8 @@ __global__ void k_edge(const float* __restrict__ depth, int w, int h, double sig
 __global__ void k_pixel_meas(const float* __restrict__ depth, const float* __restrict__ sigma, int w, int h,
                              Intr intr, FuseParams fp, const float* __restrict__ normals,
                              const uint8_t* __restrict__ edge, double* __restrict__ pix_var,
-                             double* __restrict__ pix_w, uint8_t* __restrict__ pix_ok, const int* dead) {
+                             double* __restrict__ pix_w, uint8_t* __restrict__ pix_ok, float* __restrict__ pix_dm,
+                             const int* dead) {
     if (dead && *dead) return;
     const int u = blockIdx.x * blockDim.x + threadIdx.x;
     const int v = blockIdx.y * blockDim.y + threadIdx.y;
@@ -205,6 +206,7 @@ __global__ void k_pixel_meas(const float* __restrict__ depth, const float* __res
     pix_var[idx] = var;
     pix_w[idx] = wk;
     pix_ok[idx] = ok;
+    pix_dm[idx] = ok ? depth[idx] : 0.0f;
 }
 
 // ---------------------------------------------------------------------------------
@@ -394,6 +396,241 @@ __device__ __forceinline__ uint8_t aux_encode_dev(const VolParams& P, const doub
         else hi = mid - 1;
     }
     return static_cast<uint8_t>(lo);
+}
+
+// ---------------------------------------------------------------------------------
+// Fast integrate (M = 4 or 8): same results bit for bit, fewer FP64 divisions.
+//
+// Only rounding DECISIONS of the reference reach the stored state: the pixel picked by
+// lround(u), lround(v) (fusion.cpp:92-93), the chi cut |T| > delta, the tsdf code
+// lround(clamp(T)/delta*127) and the aux code. The fast path evaluates the quotients with a
+// Newton-refined reciprocal (error < 4 ulp) and accepts a decision only when it is certain
+// under a margin many orders of magnitude above that error; otherwise (probability ~1e-9
+// per voxel) the voxel is recomputed with the reference's exact IEEE divisions. FP64,
+// explicit fma only inside the reciprocal refinement.
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ bool approx_rcp(double z, double& r) {
+    if (!(fabs(z) > 1e-30 && fabs(z) < 1e30)) return false;
+    double x = (double)__frcp_rn((float)z);  // ~24 bits
+    x = fma(x, fma(-z, x, 1.0), x);          // ~48 bits
+    x = fma(x, fma(-z, x, 1.0), x);          // ~full precision
+    r = x;
+    return true;
+}
+// lround decision certain when the interval [a - e, a + e] holds no rounding boundary.
+__device__ __forceinline__ bool certain_lround(double a, int& out) {
+    const double e = 1e-9 + 1e-12 * fabs(a);
+    if (!(fabs(a) < 1e9)) return false;
+    const int lo = ref_lround_int(a - e), hi = ref_lround_int(a + e);
+    out = lo;
+    return lo == hi;
+}
+// Variance-mode aux code from an approximate value: certain unless within 1e-12 relative of
+// a threshold (each threshold is an exact reference encode boundary).
+__device__ __forceinline__ bool certain_aux_var(const double* s_thr, double a, double a_err, int& out) {
+    int lo = 0, hi = 255;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (a >= s_thr[mid]) lo = mid;
+        else hi = mid - 1;
+    }
+    out = lo;
+    const double m = 1e-12 * fabs(a) + 100.0 * a_err + 1e-300;
+    if (lo > 0 && !(a - m >= s_thr[lo])) return false;
+    if (lo < 255 && !(a + m < s_thr[lo + 1])) return false;
+    return true;
+}
+
+// Filter rules (fusion.cpp:237-272); `approx` replaces the one division by a reciprocal.
+template <int MODE>
+__device__ __forceinline__ bool filter_rule(bool has_prior, double prior_t, double prior_a, double tsdf_k, double pk,
+                                            double wk, const FuseParams& fp, bool approx, double& new_t,
+                                            double& new_a, double& a_err) {
+    a_err = 0.0;  // absolute error bound of new_a on the approx path
+    if (MODE == 0) {
+        new_t = has_prior ? (1.0 - wk) * prior_t + wk * tsdf_k : tsdf_k;
+        new_a = wk;
+    } else if (MODE == 1) {
+        if (!has_prior) {
+            new_t = tsdf_k;
+            new_a = wk;
+        } else {
+            const double num = prior_a * prior_t + wk * tsdf_k, den = prior_a + wk;
+            double r;
+            if (approx) {
+                if (!approx_rcp(den, r)) return false;
+                new_t = num * r;
+            } else {
+                new_t = num / den;
+            }
+            new_a = dmin(prior_a + wk, fp.w_max);
+        }
+    } else {
+        if (!has_prior) {
+            new_t = tsdf_k;
+            new_a = pk;
+        } else {
+            const double predicted = prior_a + fp.q;
+            const double den = predicted + pk;
+            double gain, r;
+            if (approx) {
+                if (!approx_rcp(den, r)) return false;
+                gain = predicted * r;
+            } else {
+                gain = predicted / den;
+            }
+            new_t = prior_t + gain * (tsdf_k - prior_t);
+            new_a = (1.0 - gain) * predicted;
+            // 1 - gain cancels when gain ~ 1: |gain' - gain| <= 4 ulp(gain) propagates as an
+            // absolute error ~4.5e-16 * predicted, independent of new_a's magnitude.
+            if (approx) a_err = 1e-15 * predicted;
+        }
+    }
+    return true;
+}
+
+// Payload code of a filter result. approx: decisions must be certain (else return false).
+__device__ __forceinline__ bool encode_cell(const VolParams& P, const double* s_thr, double new_t, double new_a,
+                                            double a_err, bool approx, double inv_delta, double inv_wmax,
+                                            uint16_t& out) {
+    const double delta = P.delta;
+    if (!approx) {
+        if (fabs(new_t) > delta) {
+            out = kChiPayload;
+        } else {
+            const int8_t code = quantize_tsdf(new_t, delta);
+            const uint8_t ac = aux_encode_dev(P, s_thr, new_a);
+            out = static_cast<uint16_t>(static_cast<uint8_t>(code)) | static_cast<uint16_t>(ac << 8);
+        }
+        return true;
+    }
+    const double at = fabs(new_t);
+    const double tol = 1e-12 * delta;
+    if (!(fabs(at - delta) > tol)) return false;  // chi cut too close to call
+    if (at > delta) {
+        out = kChiPayload;
+        return true;
+    }
+    int code, ac;
+    if (!certain_lround(dclamp(new_t, -delta, delta) * inv_delta * (double)kTsdfCodeRange, code)) return false;
+    if (P.aux_mode == 0) {
+        if (!certain_lround(dclamp(new_a, 0.0, P.aux_w_max) * inv_wmax * 255.0, ac)) return false;
+    } else {
+        if (!certain_aux_var(s_thr, new_a, a_err, ac)) return false;
+    }
+    out = static_cast<uint16_t>(static_cast<uint8_t>(static_cast<int8_t>(code))) |
+          static_cast<uint16_t>(static_cast<uint8_t>(ac) << 8);
+    return true;
+}
+
+template <int MODE, int MS>
+__global__ void __launch_bounds__(256)
+    k_integrate_fast(VolParams P, const FrameConsts* __restrict__ fc, FuseParams fp, const int2* __restrict__ work,
+                     const FrameCounters* __restrict__ ctr, const AuxTables* __restrict__ aux,
+                     const float* __restrict__ pix_dm, const double* __restrict__ pix_var,
+                     const double* __restrict__ pix_w, uint16_t* __restrict__ payload,
+                     unsigned long long* __restrict__ voxels_updated) {
+    constexpr int M = 1 << MS, M3 = M * M * M;
+    constexpr int VPT = (M3 + 255) / 256;  // voxels per thread
+    __shared__ double s_tdec[256], s_adec[256], s_thr[256];
+    if (ctr->skip) return;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        s_tdec[i] = aux->tsdf_decode[i];
+        s_adec[i] = aux->aux_decode[i];
+        s_thr[i] = aux->aux_thresh[i];
+    }
+    __syncthreads();
+    const Pose inv = fc->inv;
+    const Intr intr = fc->intr;
+    const double delta = P.delta;
+    const double inv_delta = 1.0 / delta, inv_wmax = 1.0 / P.aux_w_max;
+    const int w = intr.w, h = intr.h;
+    const unsigned n_work = ctr->limit + ctr->n_update;
+    const int N = P.N;
+    unsigned long long updated = 0;
+    for (unsigned item = blockIdx.x; item < n_work; item += gridDim.x) {
+        const int2 wk = work[item];
+        const uint32_t slot = static_cast<uint32_t>(wk.x) & 0x7fffffffu;
+        const bool fresh = (static_cast<uint32_t>(wk.x) >> 31) != 0;
+        const int key = wk.y;
+        const int bx = key % N, by = (key / N) % N, bz = key / (N * N);
+        // Phase A: addresses, projections and all loads of this thread's voxels issued
+        // before any dependent arithmetic (memory-level parallelism).
+        size_t pidx[VPT], pix[VPT];
+        double zc[VPT];
+        uint16_t cellv[VPT];
+        float dmv[VPT];
+        bool inb[VPT];
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+            const int l = threadIdx.x + j * 256;
+            inb[j] = false;
+            pix[j] = 0;
+            zc[j] = 0.0;
+            pidx[j] = (size_t)slot * M3 + l;
+            cellv[j] = kChiPayload;
+            dmv[j] = 0.0f;
+            if (M3 < 256 * VPT && l >= M3) continue;
+            if (!fresh) cellv[j] = payload[pidx[j]];
+            const int lx = l & (M - 1), ly = (l >> MS) & (M - 1), lz = l >> (2 * MS);
+            // estimate_measurement (fusion.cpp:81-99)
+            const d3 xc = apply(inv, voxel_center(P, (bx << MS) + lx, (by << MS) + ly, (bz << MS) + lz));
+            zc[j] = xc.z;
+            if (xc.z > 0.0) {
+                const double nx = intr.fx * xc.x, ny = intr.fy * xc.y;
+                int u, v;
+                double r;
+                bool ok = approx_rcp(xc.z, r) && certain_lround(nx * r + intr.cx, u) && certain_lround(ny * r + intr.cy, v);
+                if (!ok) {  // exact reference projection
+                    u = ref_lround_int(nx / xc.z + intr.cx);
+                    v = ref_lround_int(ny / xc.z + intr.cy);
+                }
+                if (u >= 0 && v >= 0 && u < w && v < h) {
+                    pix[j] = (size_t)v * w + u;
+                    inb[j] = true;
+                    dmv[j] = pix_dm[pix[j]];  // depth where the pixel passes every per-pixel test, else 0
+                }
+            }
+        }
+        // Phase B: band test (fusion.cpp:145), filter, quantize, store.
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+            const int l = threadIdx.x + j * 256;
+            if (M3 < 256 * VPT && l >= M3) continue;
+            double tsdf_k = 0.0;
+            bool meas = false;
+            if (inb[j] && dmv[j] > 0.0f) {
+                tsdf_k = (double)dmv[j] - zc[j];
+                meas = !(fabs(tsdf_k) > delta);
+            }
+            if (!meas) {
+                if (fresh) payload[pidx[j]] = kChiPayload;
+                continue;
+            }
+            bool has_prior = false;
+            double prior_t = 0.0, prior_a = 0.0;
+            const uint16_t cell = cellv[j];
+            const int8_t code = static_cast<int8_t>(cell & 0xFF);
+            if (code != kChiCode) {
+                has_prior = true;
+                prior_t = s_tdec[(int)code + 128];
+                prior_a = s_adec[cell >> 8];
+            }
+            const double pk = MODE == 2 ? pix_var[pix[j]] : 0.0;
+            const double wk_ = MODE == 2 ? 0.0 : pix_w[pix[j]];
+            double new_t, new_a, a_err;
+            uint16_t out;
+            if (!(filter_rule<MODE>(has_prior, prior_t, prior_a, tsdf_k, pk, wk_, fp, true, new_t, new_a, a_err) &&
+                  encode_cell(P, s_thr, new_t, new_a, a_err, true, inv_delta, inv_wmax, out))) {
+                filter_rule<MODE>(has_prior, prior_t, prior_a, tsdf_k, pk, wk_, fp, false, new_t, new_a, a_err);
+                encode_cell(P, s_thr, new_t, new_a, 0.0, false, inv_delta, inv_wmax, out);
+            }
+            payload[pidx[j]] = out;
+            ++updated;
+        }
+    }
+    for (int off = 16; off > 0; off >>= 1) updated += __shfl_down_sync(0xffffffffu, updated, off);
+    if ((threadIdx.x & 31) == 0 && updated) atomicAdd(voxels_updated, updated);
 }
 
 template <int MODE, bool FLOATP>
@@ -609,7 +846,7 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
             n += 2;
         }
         k_pixel_meas<<<grd2, blk2, 0, s>>>(depth, sigma, w, h, intr, fp, fb.normals, fb.edge, fb.pix_var, fb.pix_w,
-                                            fb.pix_ok, dead);
+                                            fb.pix_ok, fb.pix_dm, dead);
         SF_LAUNCH_CHECK();
         n += 1;
     }
@@ -652,7 +889,21 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
                                                                v.d_fpayload, vu)
         const bool fpl = v.d_fpayload != nullptr;
         if (events && events->before_integrate) record_event(events->before_integrate, s);
-        if (fp.mode == 0) {
+        const bool fast = !fpl && (P.mshift == 3 || P.mshift == 2);
+#define SF_INTEGRATE_FAST(MODE, MS)                                                                            \
+    k_integrate_fast<MODE, MS><<<kPersistentCtas, 256, 0, s>>>(P, fb.fc, fp, fb.work, fb.ctr, v.d_aux, fb.pix_dm,   \
+                                                               fb.pix_var, fb.pix_w, v.d_payload, vu)
+        if (fast) {
+            if (P.mshift == 3) {
+                if (fp.mode == 0) SF_INTEGRATE_FAST(0, 3);
+                else if (fp.mode == 1) SF_INTEGRATE_FAST(1, 3);
+                else SF_INTEGRATE_FAST(2, 3);
+            } else {
+                if (fp.mode == 0) SF_INTEGRATE_FAST(0, 2);
+                else if (fp.mode == 1) SF_INTEGRATE_FAST(1, 2);
+                else SF_INTEGRATE_FAST(2, 2);
+            }
+        } else if (fp.mode == 0) {
             if (fpl) SF_INTEGRATE(0, true);
             else SF_INTEGRATE(0, false);
         } else if (fp.mode == 1) {
@@ -663,6 +914,7 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
             else SF_INTEGRATE(2, false);
         }
 #undef SF_INTEGRATE
+#undef SF_INTEGRATE_FAST
         SF_LAUNCH_CHECK();
         if (events && events->after_integrate) record_event(events->after_integrate, s);
         k_fuse_finalize<<<1, 1, 0, s>>>(fb.ctr, v.d_vc);

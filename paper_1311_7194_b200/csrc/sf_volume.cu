@@ -104,7 +104,7 @@ void FrameBuffers::release() {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
-    void* ptrs[] = {depth, sigma, normals, edge, pix_var, pix_w, pix_ok, keys, keys_sorted, keys_unique,
+    void* ptrs[] = {depth, sigma, normals, edge, pix_var, pix_w, pix_ok, pix_dm, keys, keys_sorted, keys_unique,
                     flags, ranks, cub_temp, work, ctr, fc, pose};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -113,6 +113,7 @@ void FrameBuffers::release() {
     depth = sigma = normals = nullptr;
     edge = pix_ok = nullptr;
     pix_var = pix_w = nullptr;
+    pix_dm = nullptr;
     keys = keys_sorted = keys_unique = flags = ranks = nullptr;
     cub_temp = nullptr;
     work = nullptr;
@@ -143,6 +144,7 @@ void ensure_frame_buffers(Volume& v, FrameBuffers& fb, int w, int h) {
     SF_CUDA(cudaMalloc(&fb.pix_var, n * sizeof(double)));
     SF_CUDA(cudaMalloc(&fb.pix_w, n * sizeof(double)));
     SF_CUDA(cudaMalloc(&fb.pix_ok, n));
+    SF_CUDA(cudaMalloc(&fb.pix_dm, n * sizeof(float)));
     SF_CUDA(cudaMalloc(&fb.keys, fb.key_cap * sizeof(uint32_t)));
     SF_CUDA(cudaMalloc(&fb.keys_sorted, fb.key_cap * sizeof(uint32_t)));
     SF_CUDA(cudaMalloc(&fb.keys_unique, fb.key_cap * sizeof(uint32_t)));
