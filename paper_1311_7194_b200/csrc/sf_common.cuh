@@ -139,6 +139,43 @@ SF_HD int ref_to_int(double x) {
 }
 SF_HD int ref_floor_int(double x) { return ref_to_int(floor(x)); }
 
+// ---- conversion-free exact helpers (device hot loops) --------------------------------
+// FP64 <-> integer conversions and floor/round run on the SM's low-rate XU pipe; these
+// equivalents use the FP64 add pipe and integer ALU only (magic number 1.5 * 2^52).
+constexpr double kMagic52 = 6755399441055744.0;
+// (double)n, exact for |n| < 2^51
+__device__ __forceinline__ double i2d_exact(long long n) {
+    return __longlong_as_double(__double_as_longlong(kMagic52) + n) - kMagic52;
+}
+// floor(x) as (double, int), exact for |x| < 2^30 (caller checks the range)
+__device__ __forceinline__ double floor_exact(double x, int& xi) {
+    const double t = x + kMagic52;  // round to nearest integer (ties to even)
+    double n = t - kMagic52;
+    int ni = static_cast<int>(static_cast<unsigned int>(__double_as_longlong(t)));
+    if (n > x) {
+        n -= 1.0;
+        ni -= 1;
+    }
+    xi = ni;
+    return n;
+}
+// static_cast<int>(std::floor(x)) (ref_floor_int) via floor_exact when |x| < 2^30.
+__device__ __forceinline__ int ref_floor_int_fast(double x) {
+    if (!(fabs(x) < 1073741824.0)) return ref_floor_int(x);
+    int xi;
+    floor_exact(x, xi);
+    return xi;
+}
+// std::lround(a) when it is certain under the margin e (a not within e of k + 1/2).
+__device__ __forceinline__ bool certain_lround_fast(double a, double e, int& out) {
+    if (!(fabs(a) < 1e9)) return false;
+    const double t = a + kMagic52;
+    const double n = t - kMagic52;  // nearest integer
+    const double d = a - n;          // exact, |d| <= 1/2
+    out = static_cast<int>(static_cast<unsigned int>(__double_as_longlong(t)));
+    return fabs(d) < 0.5 - e;
+}
+
 // Quantizers (grid.cpp:20-27): lround(clamp(d,-delta,delta) / delta * 127).
 SF_HD int8_t quantize_tsdf(double d, double delta) {
     const double clamped = dclamp(d, -delta, delta);
@@ -159,6 +196,7 @@ struct VolParams {
     int Nc;                   // coarse occupancy lattice: ceil(N / 16) super-blocks per axis
     uint64_t occ_fine_words;    // uint32 words of the fine (per-block) bitmap; coarse bits follow
     uint64_t occ_coarse_words;  // uint32 words of the coarse bitmap; 6 ints of bounding box follow
+    double inv_voxel;           // RN(1 / voxel): Markstein-corrected division by voxel (sf_render.cu)
 };
 
 constexpr int kCoarseShift = 4;  // super-block = 16^3 blocks
@@ -188,6 +226,11 @@ __device__ __forceinline__ void occ_set(const VolParams& P, uint32_t* occ, uint6
 SF_HD d3 voxel_center(const VolParams& P, int x, int y, int z) {
     return d3{P.ox + ((double)x + 0.5) * P.voxel, P.oy + ((double)y + 0.5) * P.voxel,
               P.oz + ((double)z + 0.5) * P.voxel};
+}
+// the same values without int->double conversions (exact for |coordinate| < 2^51)
+__device__ __forceinline__ d3 voxel_center_fast(const VolParams& P, int x, int y, int z) {
+    return d3{P.ox + (i2d_exact(x) + 0.5) * P.voxel, P.oy + (i2d_exact(y) + 0.5) * P.voxel,
+              P.oz + (i2d_exact(z) + 0.5) * P.voxel};
 }
 // block_min_corner (grid.cpp:275-277): origin + bc * block_side
 SF_HD d3 block_min_corner(const VolParams& P, int x, int y, int z) {

@@ -165,7 +165,7 @@ __global__ void k_edge(const float* __restrict__ depth, int w, int h, double sig
 __global__ void k_pixel_meas(const float* __restrict__ depth, const float* __restrict__ sigma, int w, int h,
                              Intr intr, FuseParams fp, const float* __restrict__ normals,
                              const uint8_t* __restrict__ edge, double* __restrict__ pix_var,
-                             double* __restrict__ pix_w, uint8_t* __restrict__ pix_ok, float* __restrict__ pix_dm,
+                             double* __restrict__ pix_w, uint8_t* __restrict__ pix_ok, double* __restrict__ pix_dm,
                              const int* dead) {
     if (dead && *dead) return;
     const int u = blockIdx.x * blockDim.x + threadIdx.x;
@@ -206,7 +206,7 @@ __global__ void k_pixel_meas(const float* __restrict__ depth, const float* __res
     pix_var[idx] = var;
     pix_w[idx] = wk;
     pix_ok[idx] = ok;
-    pix_dm[idx] = ok ? depth[idx] : 0.0f;
+    pix_dm[idx] = ok ? (double)depth[idx] : 0.0;
 }
 
 // ---------------------------------------------------------------------------------
@@ -411,19 +411,18 @@ __device__ __forceinline__ uint8_t aux_encode_dev(const VolParams& P, const doub
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ bool approx_rcp(double z, double& r) {
     if (!(fabs(z) > 1e-30 && fabs(z) < 1e30)) return false;
-    double x = (double)__frcp_rn((float)z);  // ~24 bits
-    x = fma(x, fma(-z, x, 1.0), x);          // ~48 bits
-    x = fma(x, fma(-z, x, 1.0), x);          // ~full precision
+    double x;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(x) : "d"(z));  // MUFU.RCP64H, ~20 bits
+    x = fma(x, fma(-z, x, 1.0), x);                          // ~40 bits
+    x = fma(x, fma(-z, x, 1.0), x);                          // ~full precision
+    x = fma(x, fma(-z, x, 1.0), x);
     r = x;
     return true;
 }
 // lround decision certain when the interval [a - e, a + e] holds no rounding boundary.
+// Conversion-free (certain_lround_fast): the XU pipe was this kernel's limiter.
 __device__ __forceinline__ bool certain_lround(double a, int& out) {
-    const double e = 1e-9 + 1e-12 * fabs(a);
-    if (!(fabs(a) < 1e9)) return false;
-    const int lo = ref_lround_int(a - e), hi = ref_lround_int(a + e);
-    out = lo;
-    return lo == hi;
+    return certain_lround_fast(a, 1e-9 + 1e-12 * fabs(a), out);
 }
 // Variance-mode aux code from an approximate value: certain unless within 1e-12 relative of
 // a threshold (each threshold is an exact reference encode boundary).
@@ -527,7 +526,7 @@ template <int MODE, int MS>
 __global__ void __launch_bounds__(256)
     k_integrate_fast(VolParams P, const FrameConsts* __restrict__ fc, FuseParams fp, const int2* __restrict__ work,
                      const FrameCounters* __restrict__ ctr, const AuxTables* __restrict__ aux,
-                     const float* __restrict__ pix_dm, const double* __restrict__ pix_var,
+                     const double* __restrict__ pix_dm, const double* __restrict__ pix_var,
                      const double* __restrict__ pix_w, uint16_t* __restrict__ payload,
                      unsigned long long* __restrict__ voxels_updated) {
     constexpr int M = 1 << MS, M3 = M * M * M;
@@ -559,7 +558,7 @@ __global__ void __launch_bounds__(256)
         size_t pidx[VPT], pix[VPT];
         double zc[VPT];
         uint16_t cellv[VPT];
-        float dmv[VPT];
+        double dmv[VPT];
         bool inb[VPT];
 #pragma unroll
         for (int j = 0; j < VPT; ++j) {
@@ -569,12 +568,12 @@ __global__ void __launch_bounds__(256)
             zc[j] = 0.0;
             pidx[j] = (size_t)slot * M3 + l;
             cellv[j] = kChiPayload;
-            dmv[j] = 0.0f;
+            dmv[j] = 0.0;
             if (M3 < 256 * VPT && l >= M3) continue;
             if (!fresh) cellv[j] = payload[pidx[j]];
             const int lx = l & (M - 1), ly = (l >> MS) & (M - 1), lz = l >> (2 * MS);
             // estimate_measurement (fusion.cpp:81-99)
-            const d3 xc = apply(inv, voxel_center(P, (bx << MS) + lx, (by << MS) + ly, (bz << MS) + lz));
+            const d3 xc = apply(inv, voxel_center_fast(P, (bx << MS) + lx, (by << MS) + ly, (bz << MS) + lz));
             zc[j] = xc.z;
             if (xc.z > 0.0) {
                 const double nx = intr.fx * xc.x, ny = intr.fy * xc.y;
@@ -599,8 +598,8 @@ __global__ void __launch_bounds__(256)
             if (M3 < 256 * VPT && l >= M3) continue;
             double tsdf_k = 0.0;
             bool meas = false;
-            if (inb[j] && dmv[j] > 0.0f) {
-                tsdf_k = (double)dmv[j] - zc[j];
+            if (inb[j] && dmv[j] > 0.0) {
+                tsdf_k = dmv[j] - zc[j];
                 meas = !(fabs(tsdf_k) > delta);
             }
             if (!meas) {

@@ -96,7 +96,7 @@ struct FrameBuffers {
     double* pix_var = nullptr; // w*h per-pixel p_k
     double* pix_w = nullptr;   // w*h per-pixel w_k
     uint8_t* pix_ok = nullptr; // w*h valid && quality >= 0.2
-    float* pix_dm = nullptr;   // w*h depth where pix_ok, else 0 (one gather per voxel)
+    double* pix_dm = nullptr;  // w*h depth where pix_ok, else 0 (one gather per voxel)
     uint32_t key_cap = 0;
     uint32_t* keys = nullptr;
     uint32_t* keys_sorted = nullptr;

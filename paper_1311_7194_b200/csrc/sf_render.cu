@@ -190,20 +190,61 @@ struct Sampler {
         return true;
     }
 
+    // a / voxel correctly rounded: q = RN(a * RN(1/voxel)) is within 1 ulp, and one
+    // fma-residual correction gives RN(a / voxel) (Markstein's theorem), FP64 pipe only.
+    __device__ __forceinline__ double div_voxel(double a) const {
+        const double q = a * P.inv_voxel;
+        const double r = fma(-q, P.voxel, a);
+        return fma(r, P.inv_voxel, q);
+    }
+
     __device__ bool sample(d3 p, double& out) const {
-        const double gx = (p.x - P.ox) / P.voxel - 0.5;
-        const double gy = (p.y - P.oy) / P.voxel - 0.5;
-        const double gz = (p.z - P.oz) / P.voxel - 0.5;
-        const int bx = ref_floor_int(gx), by = ref_floor_int(gy), bz = ref_floor_int(gz);
+        const double gx = div_voxel(p.x - P.ox) - 0.5;
+        const double gy = div_voxel(p.y - P.oy) - 0.5;
+        const double gz = div_voxel(p.z - P.oz) - 0.5;
+        // |g| >= 2^30 (or NaN) lies outside [0, res - 1) whatever floor gives
+        constexpr double kLim = 1073741824.0;
+        if (!(fabs(gx) < kLim && fabs(gy) < kLim && fabs(gz) < kLim)) return false;
+        int bx, by, bz;
+        const double flx = floor_exact(gx, bx), fly = floor_exact(gy, by), flz = floor_exact(gz, bz);
         const int res = P.res;
         if (bx < 0 || by < 0 || bz < 0 || bx + 1 >= res || by + 1 >= res || bz + 1 >= res) return false;
         // The base corner's block EMPTY => voxel_code fails => nullopt (render.cpp:14-15,39):
         // decided from the 1-bit occupancy map without touching the 4-byte table.
         if (!occupied(occ, table_index(P, blk(bx), blk(by), blk(bz)))) return false;
-        const double fx = gx - (double)bx, fy = gy - (double)by, fz = gz - (double)bz;
+        const double fx = gx - flx, fy = gy - fly, fz = gz - flz;
         double c[8];
-        for (int i = 0; i < 8; ++i)
-            if (!code(bx + (i & 1), by + ((i >> 1) & 1), bz + ((i >> 2) & 1), c[i])) return false;
+        if (P.mshift >= 0) {
+            // All 8 table reads issued together, then all 8 payload reads (no dependent
+            // branch between loads); any EMPTY block or chi corner => nullopt.
+            const int ms = P.mshift, mm = P.M - 1, N = P.N;
+            const int bxs[2] = {bx >> ms, (bx + 1) >> ms}, lxs[2] = {bx & mm, (bx + 1) & mm};
+            const int bys[2] = {by >> ms, (by + 1) >> ms}, lys[2] = {by & mm, (by + 1) & mm};
+            const int bzs[2] = {bz >> ms, (bz + 1) >> ms}, lzs[2] = {bz & mm, (bz + 1) & mm};
+            int32_t s[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                s[i] = __ldg(&table[((size_t)bzs[i >> 2] * N + bys[(i >> 1) & 1]) * N + bxs[i & 1]]);
+            bool ok = true;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) ok = ok && s[i] != kEmpty;
+            if (!ok) return false;
+            uint16_t pl[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                pl[i] = __ldg(&payload[(size_t)s[i] * P.M3 + (((lzs[i >> 2] << ms) + lys[(i >> 1) & 1]) << ms) +
+                                       lxs[i & 1]]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int8_t cc = static_cast<int8_t>(pl[i] & 0xFF);
+                ok = ok && cc != kChiCode;
+                c[i] = tdec[(int)cc + 128];
+            }
+            if (!ok) return false;
+        } else {
+            for (int i = 0; i < 8; ++i)
+                if (!code(bx + (i & 1), by + ((i >> 1) & 1), bz + ((i >> 2) & 1), c[i])) return false;
+        }
         const double x0 = c[0] + (c[1] - c[0]) * fx;
         const double x1 = c[2] + (c[3] - c[2]) * fx;
         const double x2 = c[4] + (c[5] - c[4]) * fx;
@@ -228,20 +269,36 @@ struct Sampler {
     }
 };
 
+// One ray per group of G lanes (G = 8: four rays per warp). Stage 1 evaluates G consecutive
+// points of the reference's sequential t lattice at once (lane k walks the same additions
+// t += step, so every t is bit-identical), then finds the first sign change in lattice
+// order with ballots/shuffles: "previous sample" is the last VALID sample before it, as in
+// render.cpp:185-207, carried across groups. Samples past the bracket are discarded
+// (sampling is pure), so results and the stage-1 step count equal the reference's.
+// Stage 2 runs redundantly in all G lanes (same addresses: broadcast loads); the six
+// gradient samples run one per lane.
+template <int G>
 __global__ void __launch_bounds__(256)
     k_raycast(VolParams P, const FrameConsts* __restrict__ fc, const int32_t* __restrict__ table,
               const uint16_t* __restrict__ payload, const uint32_t* __restrict__ occ, const AuxTables* __restrict__ aux,
               const float* __restrict__ t_start, const float* __restrict__ t_end, float* __restrict__ depth_out,
               float* __restrict__ normals_out, RayCounters* stats, int w, int h, const int* dead) {
+    static_assert(G >= 8 && G <= 32 && (G & (G - 1)) == 0, "group of 8..32 lanes");
+    constexpr int kTileX = 8, kTileY = 256 / G / kTileX;
     __shared__ double s_tdec[256];
     if (dead && *dead) return;
-    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-    for (int i = tid; i < 256; i += blockDim.x * blockDim.y) s_tdec[i] = aux->tsdf_decode[i];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_tdec[i] = aux->tsdf_decode[i];
     __syncthreads();
-    const int u = blockIdx.x * blockDim.x + threadIdx.x;
-    const int v = blockIdx.y * blockDim.y + threadIdx.y;
+    const int lane = threadIdx.x & 31;
+    const int g = lane & (G - 1);
+    const int gbase = lane & ~(G - 1);
+    const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << gbase;
+    const int ray = threadIdx.x / G;
+    const int u = blockIdx.x * kTileX + ray % kTileX;
+    const int v = blockIdx.y * kTileY + ray / kTileX;
     unsigned long long steps = 0, hits = 0, with_bounds = 0;
-    if (u < w && v < h) {
+    auto group_bits = [&](bool pred) { return (__ballot_sync(gmask, pred) & gmask) >> gbase; };
+    if (u < w && v < h) {  // uniform within the group
         const size_t idx = (size_t)v * w + u;
         float out_d = 0.0f, nx = 0.f, ny = 0.f, nz = 0.f;
         const float fs = t_start[idx], fe = t_end[idx];
@@ -255,29 +312,57 @@ __global__ void __launch_bounds__(256)
             const double fine_tol = 0.01 * vox;
             const d3 dir_cam = normalized(unproject(intr, u, v, 1.0));
             const d3 dir = mv(pose.R, dir_cam);
-            const double t0 = fs, t1 = fe;
-            double prev_t = 0.0, prev_val = 0.0;
-            bool have_prev = false, bracketed = false;
+            const double t1 = fe;
+            bool carry = false, bracketed = false;
+            double carry_t = 0.0, carry_val = 0.0;
             double hit_a = 0.0, hit_b = 0.0, val_a = 0.0, val_b = 0.0;
-            for (double t = t0;; t += coarse_step) {
-                const bool final_sample = t >= t1;
-                if (final_sample) t = t1;
-                ++steps;
-                double val;
-                if (S.sample(add(pose.t, scale(t, dir)), val)) {
-                    if (have_prev && prev_val > 0.0 && val < 0.0) {
-                        hit_a = prev_t;
-                        val_a = prev_val;
-                        hit_b = t;
-                        val_b = val;
-                        bracketed = true;
+            double t_base = fs;
+            for (;;) {
+                double t = t_base;
+                bool has = true, fin = false;
+                for (int k = 0; k < g; ++k) {
+                    if (t >= t1) {
+                        has = false;
                         break;
                     }
-                    have_prev = true;
-                    prev_t = t;
-                    prev_val = val;
+                    t += coarse_step;
                 }
-                if (final_sample) break;
+                if (has && t >= t1) {
+                    fin = true;
+                    t = t1;
+                }
+                double val = 0.0;
+                const bool valid = has && S.sample(add(pose.t, scale(t, dir)), val);
+                const unsigned vm = group_bits(valid), fm = group_bits(fin), hm = group_bits(has);
+                const unsigned below = vm & ((1u << g) - 1u);
+                const int pl = below ? 31 - __clz(below) : 0;
+                double pv = __shfl_sync(gmask, val, pl, G), pt = __shfl_sync(gmask, t, pl, G);
+                bool hp = below != 0;
+                if (!hp) {
+                    hp = carry;
+                    pv = carry_val;
+                    pt = carry_t;
+                }
+                const unsigned hit = group_bits(valid && hp && pv > 0.0 && val < 0.0);
+                if (hit) {
+                    const int hl = __ffs(hit) - 1;
+                    hit_a = __shfl_sync(gmask, pt, hl, G);
+                    val_a = __shfl_sync(gmask, pv, hl, G);
+                    hit_b = __shfl_sync(gmask, t, hl, G);
+                    val_b = __shfl_sync(gmask, val, hl, G);
+                    steps += hl + 1;
+                    bracketed = true;
+                    break;
+                }
+                steps += __popc(hm);
+                if (fm || hm != (G == 32 ? 0xffffffffu : (1u << G) - 1u)) break;
+                if (vm) {
+                    const int ll = 31 - __clz(vm);
+                    carry = true;
+                    carry_t = __shfl_sync(gmask, t, ll, G);
+                    carry_val = __shfl_sync(gmask, val, ll, G);
+                }
+                t_base = __shfl_sync(gmask, t, G - 1, G) + coarse_step;
             }
             if (bracketed) {
                 double root = hit_b;
@@ -308,29 +393,48 @@ __global__ void __launch_bounds__(256)
                 if (!(dd < intr.near_plane || dd > intr.far_plane)) {
                     out_d = (float)dd;
                     hits = 1;
-                    d3 g;
-                    if (S.gradient(add(pose.t, scale(root, dir)), vox, g) && sqnorm(g) > 0.0) {
-                        // world_to_cam * grad.normalized()  (render.cpp:242-245)
-                        const d3 n_cam = mv(mt(pose.R), normalized(g));
-                        nx = (float)n_cam.x;
-                        ny = (float)n_cam.y;
-                        nz = (float)n_cam.z;
+                    // sample_tsdf_gradient (render.cpp:50-63): lane a < 6 takes p +- h e_(a/2)
+                    const d3 p = add(pose.t, scale(root, dir));
+                    const double hh = (g & 1) ? -vox : vox;
+                    d3 q = p;
+                    if (g < 2) q = mk(p.x + hh, p.y, p.z);
+                    else if (g < 4) q = mk(p.x, p.y + hh, p.z);
+                    else q = mk(p.x, p.y, p.z + hh);
+                    double sv = 0.0;
+                    const bool sok = g < 6 && S.sample(q, sv);
+                    const unsigned okm = group_bits(sok);
+                    double s6[6];
+#pragma unroll
+                    for (int a = 0; a < 6; ++a) s6[a] = __shfl_sync(gmask, sv, a, G);
+                    if (okm == 0x3fu) {
+                        const d3 gr = mk((s6[0] - s6[1]) / (2.0 * vox), (s6[2] - s6[3]) / (2.0 * vox),
+                                         (s6[4] - s6[5]) / (2.0 * vox));
+                        if (sqnorm(gr) > 0.0) {
+                            // world_to_cam * grad.normalized()  (render.cpp:242-245)
+                            const d3 n_cam = mv(mt(pose.R), normalized(gr));
+                            nx = (float)n_cam.x;
+                            ny = (float)n_cam.y;
+                            nz = (float)n_cam.z;
+                        }
                     }
                 }
             }
         }
-        depth_out[idx] = out_d;
-        normals_out[3 * idx] = nx;
-        normals_out[3 * idx + 1] = ny;
-        normals_out[3 * idx + 2] = nz;
+        if (g == 0) {
+            depth_out[idx] = out_d;
+            normals_out[3 * idx] = nx;
+            normals_out[3 * idx + 1] = ny;
+            normals_out[3 * idx + 2] = nz;
+        }
     }
+    if (g != 0) steps = hits = with_bounds = 0;  // per-ray values are replicated in the group
     // RaycastStats: warp reduction, one atomic per warp and counter.
     for (int off = 16; off > 0; off >>= 1) {
         steps += __shfl_down_sync(0xffffffffu, steps, off);
         hits += __shfl_down_sync(0xffffffffu, hits, off);
         with_bounds += __shfl_down_sync(0xffffffffu, with_bounds, off);
     }
-    if ((tid & 31) == 0 && stats) {
+    if (lane == 0 && stats) {
         if (steps) atomicAdd(&stats->sample_steps, steps);
         if (hits) atomicAdd(&stats->hit_pixels, hits);
         if (with_bounds) atomicAdd(&stats->rays_with_bounds, with_bounds);
@@ -351,8 +455,9 @@ void launch_ray_bounds(Volume& v, const FrameConsts* d_fc, const Intr& intr, flo
 void launch_raycast(Volume& v, const FrameConsts* d_fc, const Intr& intr, const float* t_start, const float* t_end,
                     float* depth, float* normals, RayCounters* d_stats, cudaStream_t s, uint64_t* launches,
                     const int* dead_flag) {
-    const dim3 blk(32, 4), grd((intr.w + 31) / 32, (intr.h + 3) / 4);
-    k_raycast<<<grd, blk, 0, s>>>(v.P, d_fc, v.d_table, v.d_payload, v.d_occ, v.d_aux, t_start, t_end, depth, normals,
+    constexpr int G = 8;  // lanes per ray; 256-thread CTA = 8x4 pixel tile
+    const dim3 blk(256), grd((intr.w + 7) / 8, (intr.h + 3) / 4);
+    k_raycast<G><<<grd, blk, 0, s>>>(v.P, d_fc, v.d_table, v.d_payload, v.d_occ, v.d_aux, t_start, t_end, depth, normals,
                                   d_stats, intr.w, intr.h, dead_flag);
     SF_LAUNCH_CHECK();
     if (launches) *launches += 1;

@@ -144,7 +144,7 @@ void ensure_frame_buffers(Volume& v, FrameBuffers& fb, int w, int h) {
     SF_CUDA(cudaMalloc(&fb.pix_var, n * sizeof(double)));
     SF_CUDA(cudaMalloc(&fb.pix_w, n * sizeof(double)));
     SF_CUDA(cudaMalloc(&fb.pix_ok, n));
-    SF_CUDA(cudaMalloc(&fb.pix_dm, n * sizeof(float)));
+    SF_CUDA(cudaMalloc(&fb.pix_dm, n * sizeof(double)));
     SF_CUDA(cudaMalloc(&fb.keys, fb.key_cap * sizeof(uint32_t)));
     SF_CUDA(cudaMalloc(&fb.keys_sorted, fb.key_cap * sizeof(uint32_t)));
     SF_CUDA(cudaMalloc(&fb.keys_unique, fb.key_cap * sizeof(uint32_t)));
@@ -264,6 +264,7 @@ static VolParams make_params(const sf_grid_config& c, const sf_aux_quant& a, uin
     P.oz = c.box_origin[2];
     P.box_side = c.box_side;
     P.voxel = c.box_side / P.res;                      // GridConfig::voxel_size (grid.hpp:36)
+    P.inv_voxel = 1.0 / P.voxel;
     P.block_side = P.voxel * P.M;                      // SparseTsdfGrid::block_side (grid.hpp:149)
     P.delta = c.truncation > 0.0 ? c.truncation : 4.0 * P.voxel;  // grid.hpp:37
     P.aux_mode = a.mode;
