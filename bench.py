@@ -270,7 +270,7 @@ def run_ours(args, world, rank, local):
         dist.barrier()
     step_ms = [ev0[i].elapsed_time(ev1[i]) for i in range(steps)]
     total_ms = sum(step_ms)
-    launches_per_step = tracker.last_launch_count()
+    launches_total = sum(mm.kernel_launches for mm in metrics)
     statuses = [mm.status for mm in metrics]
     if any(statuses):
         raise RuntimeError(f"tracking failed during the timed region: {statuses}")
@@ -352,7 +352,7 @@ def run_ours(args, world, rank, local):
                      "ms_per_launch_mean": sum(integ_ms) / steps},
         "e2e": {"value": world * steps / (e2e_ms * 1e-3), "unit": "frames/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
-        "gpu_launches": launches_per_step * steps,
+        "gpu_launches": launches_total,
         "clocks": clocks.summary(),
     }
     if rank == 0 and not args.no_cpu_baseline:

@@ -267,6 +267,7 @@ typedef struct {
     sf_raycast_stats raycast;
     uint64_t blocks_processed; /* allocate-list prefix + update list integrated this frame */
     uint64_t voxels_visited;   /* blocks_processed * M^3 */
+    uint64_t kernel_launches;  /* device kernels this frame ran (graph: top level + 2 per ICP iteration) */
 } sf_frame_metrics;
 
 int sf_tracker_create(sf_volume_t vol, const sf_tracker_config* config, const double initial_pose[12],
@@ -289,8 +290,9 @@ int sf_tracker_fetch(sf_tracker_t tr, sf_frame_metrics* out, void* stream);
 int sf_tracker_stage_times(sf_tracker_t tr, float ms[5]);
 /* Device pointer to the tracker's pose (12 doubles). */
 int sf_tracker_device_pose(sf_tracker_t tr, const double** device_pose);
-/* Number of this library's kernels launched by the last sf_tracker_step (excl. graphs
- * replay bookkeeping): the bench's gpu_launches figure. */
+/* Number of this library's kernels the last sf_tracker_step launched at issue time. With
+ * graphs the ICP iterations run as a device-side loop whose kernels are counted only after
+ * the fact: sf_frame_metrics.kernel_launches (after fetch) is the complete per-frame count. */
 int sf_tracker_last_launch_count(sf_tracker_t tr, uint64_t* count);
 /* Bytes one step moves across PCIe when the frame is a host frame (depth [+ sigma]) and
  * bytes sf_tracker_fetch reads back. */

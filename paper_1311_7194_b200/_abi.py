@@ -155,6 +155,7 @@ class FrameMetricsC(C.Structure):
         ("raycast", RaycastStatsC),
         ("blocks_processed", C.c_uint64),
         ("voxels_visited", C.c_uint64),
+        ("kernel_launches", C.c_uint64),
     ]
 
 

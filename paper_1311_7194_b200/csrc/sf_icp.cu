@@ -9,10 +9,12 @@
 //   k_icp_assemble  per match: shrunk row (c_hat, n), d; 21 + 6 + 1 compensated sums
 //                   (double-double TwoSum accumulators), warp shuffle -> CTA partials
 //                   (registration.cpp:76-123). The last CTA merges the partials in a fixed
-//                   order and runs Jacobi 6x6, gated solve, unshrink, apply_motion and the
-//                   convergence test (registration.cpp:125-220) — one thread, registers only.
-// A converged / failed state makes the remaining iterations' kernels exit at once, so the
-// whole ICP (max_iterations x 2 launches) is a fixed launch sequence: CUDA-graph friendly.
+//                   order; one warp runs the Jacobi 6x6 (rows across lanes, bit-identical to
+//                   the sequential sweep), one thread the gated solve, unshrink, apply_motion
+//                   and the convergence test (registration.cpp:125-220).
+// Under CUDA-graph capture (tracker) the iterations are a conditional WHILE node: the body
+// repeats until converged / lost / max_iterations, decided on the device. Issued eagerly,
+// a converged / failed state makes the remaining iterations' kernels exit at once.
 // Partials are merged in a fixed order, so results are deterministic run to run.
 //
 // Parity: the association and every per-match quantity are FP64 in the reference order.
@@ -20,6 +22,7 @@
 // Kahan); both are within ~1 ulp of the exact sum, pose parity is asserted at 1e-6.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 
 #include "sf_icp.cuh"
@@ -27,12 +30,14 @@
 
 namespace sf {
 
-__global__ void k_icp_init(IcpState* st, const double* __restrict__ initial12, const int* dead) {
+__global__ void k_icp_init(IcpState* st, const double* __restrict__ initial12, const int* dead, int max_iterations,
+                           int use_cond, cudaGraphConditionalHandle cond) {
     IcpState z;
     memset(&z, 0, sizeof(z));
     z.delta = pose_from12(initial12);
     z.done = (dead && *dead) ? 1 : 0;
     *st = z;
+    if (use_cond) cudaGraphSetConditional(cond, (!z.done && max_iterations > 0) ? 1u : 0u);
 }
 
 // Returns true in every thread of the CTA that finished last (all partials visible).
@@ -190,22 +195,17 @@ __global__ void __launch_bounds__(kIcpThreads)
         part_count[blockIdx.x] = s_c[0];
     }
     if (last_cta(counter)) {
+        if (threadIdx.x == 0) st->bodies += 1;
         bbox_finalize(st, part_bbox, part_count, gridDim.x, prm);
         if (threadIdx.x == 0) *counter = 0;
     }
 }
 
 // solve_gated + apply_motion + convergence (registration.cpp:175-212), one thread.
-__device__ __noinline__ void solve_finalize(IcpState* st, const double* s_sum, const IcpParamsDev& prm, int iter) {
-    double A[36];
-    int k = 0;
-#pragma unroll
-    for (int i = 0; i < 6; ++i)
-#pragma unroll
-        for (int j = i; j < 6; ++j, ++k) {
-            A[i * 6 + j] = s_sum[k];
-            A[j * 6 + i] = s_sum[k];
-        }
+// The eigendecomposition of the normal matrix is done before, by one warp (e).
+__device__ __noinline__ void solve_finalize(IcpState* st, const double* s_sum, const Eig6& e,
+                                            const IcpParamsDev& prm) {
+    const int iter = st->iterations;  // iterations completed before this one
     double b[6];
 #pragma unroll
     for (int i = 0; i < 6; ++i) b[i] = s_sum[21 + i];
@@ -214,8 +214,6 @@ __device__ __noinline__ void solve_finalize(IcpState* st, const double* s_sum, c
     const double n_pairs = static_cast<double>(cnt);
     st->pair_count = cnt;
     st->residual_rms = sqrt(dmax(0.0, res_sq) / n_pairs);
-    Eig6 e;
-    eigendecompose_sym6(A, e);
     double x[6] = {0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 6; ++i) {
@@ -249,13 +247,17 @@ __device__ __noinline__ void solve_finalize(IcpState* st, const double* s_sum, c
     if (st->shrunk_norm < prm.eps) st->done = 1;
 }
 
-constexpr int kMergeLanes = 8;  // threads per sum in the final merge (224 of 256 threads busy)
+constexpr int kMergeLanes = kIcpThreads / kSums;  // threads per sum in the final merge (252 of 256 busy)
 
 // assemble (registration.cpp:93-123) on the shrunk matches (registration.cpp:65-72).
 __global__ void __launch_bounds__(kIcpThreads)
     k_icp_assemble(IcpState* st, const MatchRec* __restrict__ rec, const uint8_t* __restrict__ flag, int n,
-                   DD* __restrict__ part, unsigned int* counter, IcpParamsDev prm, int iter) {
-    if (st->done) return;
+                   DD* __restrict__ part, unsigned int* counter, IcpParamsDev prm, int use_cond,
+                   cudaGraphConditionalHandle cond) {
+    if (st->done) {  // converged / lost (possibly in this iteration's match pass): end the loop
+        if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0u);
+        return;
+    }
     const d3 c = st->center, inv = st->inv_scale, scl = st->scale;
     DD acc[kSums];
 #pragma unroll
@@ -300,24 +302,35 @@ __global__ void __launch_bounds__(kIcpThreads)
         part[blockIdx.x * kSums + threadIdx.x] = a;
     }
     if (!last_cta(counter)) return;
-    // Fixed-order merge of all CTA partials: sum k, lane j takes partials j, j+8, ...
-    __shared__ DD s_m[kSums][kMergeLanes];
+    // Fixed-order merge of all CTA partials: sum k, lane j takes partials j, j+L, ... The
+    // loads go straight to L2 (ld.cg, after last_cta's fence) in batches of kBatch so their
+    // latencies overlap; the merge order is fixed, so the result is deterministic.
+    constexpr int L = kMergeLanes, kBatch = 8;
+    __shared__ DD s_m[kSums][L];
     __shared__ double s_sum[kSums];
     const int nparts = gridDim.x;
-    if (threadIdx.x < kSums * kMergeLanes) {
-        const int k = threadIdx.x / kMergeLanes, j = threadIdx.x % kMergeLanes;
-        const volatile DD* vp = part;
+    if (threadIdx.x < kSums * L) {
+        const int k = threadIdx.x % kSums, j = threadIdx.x / kSums;
+        const double2* vp = reinterpret_cast<const double2*>(part);
         DD a{0.0, 0.0};
         bool first = true;
-        for (int p = j; p < nparts; p += kMergeLanes) {
-            DD b;
-            b.hi = vp[p * kSums + k].hi;
-            b.lo = vp[p * kSums + k].lo;
-            if (first) {
-                a = b;
-                first = false;
-            } else {
-                dd_merge(a, b);
+        for (int p0 = j; p0 < nparts; p0 += kBatch * L) {
+            double2 b[kBatch];
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) {
+                const int p = p0 + u * L;
+                b[u] = p < nparts ? __ldcg(&vp[p * kSums + k]) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) {
+                if (p0 + u * L >= nparts) break;
+                const DD x{b[u].x, b[u].y};
+                if (first) {
+                    a = x;
+                    first = false;
+                } else {
+                    dd_merge(a, x);
+                }
             }
         }
         s_m[k][j] = a;
@@ -329,9 +342,21 @@ __global__ void __launch_bounds__(kIcpThreads)
         s_sum[threadIdx.x] = a.hi + a.lo;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        solve_finalize(st, s_sum, prm, iter);
-        *counter = 0;
+    if (threadIdx.x < 32) {
+        __shared__ double s_A[36];
+        __shared__ Eig6 s_eig;
+        for (int i = threadIdx.x; i < 36; i += 32) {
+            const int r = i / 6, c = i % 6, lo = r < c ? r : c, hi = r < c ? c : r;
+            s_A[i] = s_sum[lo * 6 - lo * (lo - 1) / 2 + (hi - lo)];  // packed upper triangle, row-major
+        }
+        __syncwarp();
+        eigendecompose_sym6_warp(s_A, &s_eig);
+        __syncwarp();
+        if (threadIdx.x == 0) {
+            solve_finalize(st, s_sum, s_eig, prm);
+            *counter = 0;
+            if (use_cond) cudaGraphSetConditional(cond, (!st->done && st->iterations < prm.max_iterations) ? 1u : 0u);
+        }
     }
 }
 
@@ -346,23 +371,73 @@ IcpParamsDev make_icp_params(const sf_match_params& p) {
     return d;
 }
 
-// Launch the whole ICP: init + max_iterations x (match, assemble).
+// Launch the whole ICP: init + the iterations (match, assemble).
+// Under stream capture the iterations become a conditional WHILE node of the graph being
+// captured: the body {match, assemble} repeats while the assemble's last CTA keeps the
+// condition set (not converged, not lost, fewer than max_iterations), so a frame launches
+// 1 + 2 x iterations kernels. Issued eagerly, it is the fixed sequence of max_iterations
+// (match, assemble) pairs whose kernels exit at once after convergence.
+// *device_loop (optional) reports which form was used; the loop form adds only the init
+// launch to *launches (the caller adds 2 x IcpState::bodies after the fact).
 void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* tgt, const float* tgt_n,
                 const Intr& si, const Intr& ti, const double* d_initial, const IcpParamsDev& prm, cudaStream_t s,
-                uint64_t* launches, const int* dead) {
+                uint64_t* launches, const int* dead, bool* device_loop) {
     const int n = si.w * si.h;
-    k_icp_init<<<1, 1, 0, s>>>(wk.st, d_initial, dead);
-    SF_LAUNCH_CHECK();
-    uint64_t cnt = 1;
-    for (int it = 0; it < prm.max_iterations; ++it) {
-        k_icp_match<<<kIcpCtas, kIcpThreads, 0, s>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st, wk.rec, wk.flag,
-                                                     wk.part_bbox, wk.part_count, wk.counters);
-        k_icp_assemble<<<kIcpCtas, kIcpThreads, 0, s>>>(wk.st, wk.rec, wk.flag, n, wk.part, wk.counters + 1, prm,
-                                                        it);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    SF_CUDA(cudaStreamIsCapturing(s, &cs));
+    // SF_ICP_DEVICE_LOOP=0 keeps the fixed launch sequence under capture too (Nsight Compute
+    // does not profile kernels inside conditional graph nodes).
+    static const bool loop_enabled = [] {
+        const char* e = std::getenv("SF_ICP_DEVICE_LOOP");
+        return !(e && e[0] == '0');
+    }();
+    const bool loop = loop_enabled && cs == cudaStreamCaptureStatusActive && prm.max_iterations > 0;
+    if (device_loop) *device_loop = loop;
+    if (!loop) {
+        k_icp_init<<<1, 1, 0, s>>>(wk.st, d_initial, dead, prm.max_iterations, 0, 0);
         SF_LAUNCH_CHECK();
-        cnt += 2;
+        uint64_t cnt = 1;
+        for (int it = 0; it < prm.max_iterations; ++it) {
+            k_icp_match<<<kIcpCtas, kIcpThreads, 0, s>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st, wk.rec, wk.flag,
+                                                         wk.part_bbox, wk.part_count, wk.counters);
+            k_icp_assemble<<<kIcpCtas, kIcpThreads, 0, s>>>(wk.st, wk.rec, wk.flag, n, wk.part, wk.counters + 1, prm,
+                                                            0, 0);
+            SF_LAUNCH_CHECK();
+            cnt += 2;
+        }
+        if (launches) *launches += cnt;
+        return;
     }
-    if (launches) *launches += cnt;
+    cudaGraph_t g = nullptr;
+    SF_CUDA(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, nullptr, nullptr));
+    cudaGraphConditionalHandle cond;
+    SF_CUDA(cudaGraphConditionalHandleCreate(&cond, g, 0, 0));
+    k_icp_init<<<1, 1, 0, s>>>(wk.st, d_initial, dead, prm.max_iterations, 1, cond);
+    SF_LAUNCH_CHECK();
+    if (launches) *launches += 1;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    SF_CUDA(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &ndeps));
+    cudaGraphNodeParams cp = {cudaGraphNodeTypeConditional};
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    SF_CUDA(cudaGraphAddNode(&node, g, deps, ndeps, &cp));
+    SF_CUDA(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    if (!wk.body_stream) SF_CUDA(cudaStreamCreateWithFlags(&wk.body_stream, cudaStreamNonBlocking));
+    cudaStream_t bs = wk.body_stream;
+    SF_CUDA(cudaStreamBeginCaptureToGraph(bs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    k_icp_match<<<kIcpCtas, kIcpThreads, 0, bs>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st, wk.rec, wk.flag,
+                                                  wk.part_bbox, wk.part_count, wk.counters);
+    k_icp_assemble<<<kIcpCtas, kIcpThreads, 0, bs>>>(wk.st, wk.rec, wk.flag, n, wk.part, wk.counters + 1, prm, 1,
+                                                     cond);
+    const cudaError_t le = cudaGetLastError();
+    cudaGraph_t captured = nullptr;
+    const cudaError_t ee = cudaStreamEndCapture(bs, &captured);
+    SF_CUDA(le);
+    SF_CUDA(ee);
 }
 
 void fill_icp_result(const IcpState& st, sf_icp_result* out) {

@@ -32,7 +32,7 @@ struct IcpState {
     int done;       // converged or failed: later iterations are no-ops
     int lost;       // TrackingLost raised
     int iterations;
-    int pad;
+    int bodies;     // iterations whose match pass ran (device-side loop: kernel launches = 2 x bodies)
     unsigned long long matches;       // matches of the last completed iteration
     unsigned long long lost_count;    // match count that triggered TrackingLost
     d3 center, scale, inv_scale;      // shrink of the current iteration
@@ -105,13 +105,17 @@ struct IcpWork {
         initial = nullptr;
         w = h = 0;
     }
-    ~IcpWork() { release(); }
+    cudaStream_t body_stream = nullptr;  // captures the body of the device-side iteration loop
+    ~IcpWork() {
+        release();
+        if (body_stream) cudaStreamDestroy(body_stream);
+    }
 };
 
 IcpParamsDev make_icp_params(const sf_match_params& p);
 void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* tgt, const float* tgt_n,
                 const Intr& si, const Intr& ti, const double* d_initial, const IcpParamsDev& prm, cudaStream_t s,
-                uint64_t* launches, const int* dead);
+                uint64_t* launches, const int* dead, bool* device_loop = nullptr);
 void fill_icp_result(const IcpState& st, sf_icp_result* out);
 
 }  // namespace sf

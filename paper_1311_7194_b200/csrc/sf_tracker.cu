@@ -107,6 +107,9 @@ struct sf_tracker {
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // stage timing (graph nodes)
     cudaGraphExec_t graph[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};  // [mode][sigma]
     uint64_t graph_kernels[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+    bool graph_icp_loop[3][2] = {{false, false}, {false, false}, {false, false}};
+    bool issue_icp_loop = false;  // set by issue(): ICP iterations run as a device-side loop
+    bool last_icp_loop = false;
     // pinned fetch staging
     struct Fetch {
         double cur[12];
@@ -139,6 +142,7 @@ struct sf_tracker {
         const FuseParams& p = has_sigma ? fp_sigma : fp;
         const float* sig = has_sigma ? d_cap_sigma : nullptr;
         record_event(ev[0], s);
+        issue_icp_loop = false;
         if (mode == 0 || mode == 3) {
             k_tracker_begin_track<<<1, 1, 0, s>>>(d_cur, mode == 3 ? d_gt : nullptr, d_init_delta, d_rstats, d_td);
             SF_LAUNCH_CHECK();
@@ -150,7 +154,7 @@ struct sf_tracker {
             launch_compute_normals(d_cap, cam.w, cam.h, cam, cfg.match.normal_sigma0, cfg.match.normal_spatial_scale,
                                    icp.src_normals, s, &n, dead);
             launch_icp(icp, d_cap, icp.src_normals, d_model_depth, d_model_normals, cam, cam, d_init_delta, icp_prm, s,
-                       &n, dead);
+                       &n, dead, &issue_icp_loop);
             k_tracker_after_icp<<<1, 1, 0, s>>>(d_cur, fb.pose, icp.st, d_td, cfg.orthonormalize);
             SF_LAUNCH_CHECK();
             ++n;
@@ -173,20 +177,6 @@ struct sf_tracker {
         return n;
     }
 };
-
-static uint64_t count_kernel_nodes(cudaGraph_t g) {
-    size_t num = 0;
-    SF_CUDA(cudaGraphGetNodes(g, nullptr, &num));
-    std::vector<cudaGraphNode_t> nodes(num);
-    SF_CUDA(cudaGraphGetNodes(g, nodes.data(), &num));
-    uint64_t k = 0;
-    for (auto nd : nodes) {
-        cudaGraphNodeType t;
-        SF_CUDA(cudaGraphNodeGetType(nd, &t));
-        if (t == cudaGraphNodeTypeKernel) ++k;
-    }
-    return k;
-}
 
 extern "C" {
 
@@ -264,24 +254,30 @@ int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, con
             cudaGraphExec_t& ge = tr->graph[gmode][sidx];
             if (!ge) {
                 cudaGraph_t g;
+                uint64_t issued = 0;
                 if (!tr->capture_stream) SF_CUDA(cudaStreamCreateWithFlags(&tr->capture_stream, cudaStreamNonBlocking));
                 cudaStream_t cs = tr->capture_stream;
                 SF_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
                 try {
-                    tr->issue(eff, has_sigma, cs);
+                    issued = tr->issue(eff, has_sigma, cs);
                 } catch (...) {
                     cudaStreamEndCapture(cs, &g);
                     throw;
                 }
                 SF_CUDA(cudaStreamEndCapture(cs, &g));
                 SF_CUDA(cudaGraphInstantiate(&ge, g, 0));
-                tr->graph_kernels[gmode][sidx] = count_kernel_nodes(g);
+                // kernels issued into the top-level graph (the ICP loop body is counted per
+                // iteration at fetch time)
+                tr->graph_kernels[gmode][sidx] = issued;
+                tr->graph_icp_loop[gmode][sidx] = tr->issue_icp_loop;
                 SF_CUDA(cudaGraphDestroy(g));
             }
             SF_CUDA(cudaGraphLaunch(ge, s));
             tr->last_launches = tr->graph_kernels[gmode][sidx];
+            tr->last_icp_loop = tr->graph_icp_loop[gmode][sidx];
         } else {
             tr->last_launches = tr->issue(eff, has_sigma, s);
+            tr->last_icp_loop = tr->issue_icp_loop;
         }
         tr->last_mode = eff;
         ++tr->frames;
@@ -335,6 +331,8 @@ int sf_tracker_fetch(sf_tracker_t tr, sf_frame_metrics* out, void* stream) {
         out->blocks_processed = static_cast<uint64_t>(h->ctr.limit) + h->ctr.n_update;
         if (h->ctr.skip) out->blocks_processed = 0;
         out->voxels_visited = out->blocks_processed * m * m * m;
+        out->kernel_launches = tr->last_launches;
+        if (tr->last_icp_loop) out->kernel_launches += 2ull * static_cast<uint64_t>(h->icp.bodies);
         return SF_OK;
     });
 }
