@@ -197,6 +197,8 @@ struct VolParams {
     uint64_t occ_fine_words;    // uint32 words of the fine (per-block) bitmap; coarse bits follow
     uint64_t occ_coarse_words;  // uint32 words of the coarse bitmap; 6 ints of bounding box follow
     double inv_voxel;           // RN(1 / voxel): Markstein-corrected division by voxel (sf_render.cu)
+    double aux_lg_pmin, aux_lg_scale;
+    int nshift;  // log2(N) when N is a power of two, else -1  // variance codes: log2(p_min), 255 / log2(p_max / p_min) (code guess)
 };
 
 constexpr int kCoarseShift = 4;  // super-block = 16^3 blocks

@@ -383,19 +383,33 @@ __global__ void k_visible(VolParams P, const FrameConsts* __restrict__ fc, Frame
 // ---------------------------------------------------------------------------------
 // per-voxel integration
 // ---------------------------------------------------------------------------------
+// log2(v) to ~0.01 for positive normal v, from the exponent and a quadratic in the
+// mantissa (integer + FP64 pipe only).
+__device__ __forceinline__ double approx_log2(double v) {
+    const long long b = __double_as_longlong(v);
+    const int e = static_cast<int>((b >> 52) & 0x7ff) - 1023;
+    const double m = __longlong_as_double((b & 0x000fffffffffffffLL) | 0x3ff0000000000000LL) - 1.0;
+    return i2d_exact(e) + m * (1.3465 - 0.3465 * m);
+}
+// Variance-mode aux code #{k in 1..255 : value >= thresh[k]} (thresholds ascending, each an
+// exact reference encode boundary): guess from the log-scale formula of grid.cpp:42-45,
+// then walk to the exact answer (almost always zero or one step).
+__device__ __forceinline__ int aux_var_code(const VolParams& P, const double* s_thr, double value) {
+    if (value != value) return 0;  // NaN: every comparison fails
+    const double vc = dclamp(value, P.aux_p_min, P.aux_p_max);
+    const double gs = dclamp((approx_log2(vc) - P.aux_lg_pmin) * P.aux_lg_scale, 0.0, 255.0);
+    int g = static_cast<int>(static_cast<unsigned int>(__double_as_longlong(gs + kMagic52)));
+    while (g < 255 && value >= s_thr[g + 1]) ++g;
+    while (g > 0 && !(value >= s_thr[g])) --g;
+    return g;
+}
+
 __device__ __forceinline__ uint8_t aux_encode_dev(const VolParams& P, const double* s_thr, double value) {
     if (P.aux_mode == 0) {
         const double clamped = dclamp(value, 0.0, P.aux_w_max);
         return static_cast<uint8_t>(static_cast<long long>(llround(clamped / P.aux_w_max * 255.0)));
     }
-    // #{k in 1..255 : value >= thresh[k]} by binary search (thresholds ascending).
-    int lo = 0, hi = 255;  // answer in [lo, hi]
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (value >= s_thr[mid]) lo = mid;
-        else hi = mid - 1;
-    }
-    return static_cast<uint8_t>(lo);
+    return static_cast<uint8_t>(aux_var_code(P, s_thr, value));
 }
 
 // ---------------------------------------------------------------------------------
@@ -426,13 +440,9 @@ __device__ __forceinline__ bool certain_lround(double a, int& out) {
 }
 // Variance-mode aux code from an approximate value: certain unless within 1e-12 relative of
 // a threshold (each threshold is an exact reference encode boundary).
-__device__ __forceinline__ bool certain_aux_var(const double* s_thr, double a, double a_err, int& out) {
-    int lo = 0, hi = 255;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (a >= s_thr[mid]) lo = mid;
-        else hi = mid - 1;
-    }
+__device__ __forceinline__ bool certain_aux_var(const VolParams& P, const double* s_thr, double a, double a_err,
+                                                int& out) {
+    const int lo = aux_var_code(P, s_thr, a);
     out = lo;
     const double m = 1e-12 * fabs(a) + 100.0 * a_err + 1e-300;
     if (lo > 0 && !(a - m >= s_thr[lo])) return false;
@@ -515,7 +525,7 @@ __device__ __forceinline__ bool encode_cell(const VolParams& P, const double* s_
     if (P.aux_mode == 0) {
         if (!certain_lround(dclamp(new_a, 0.0, P.aux_w_max) * inv_wmax * 255.0, ac)) return false;
     } else {
-        if (!certain_aux_var(s_thr, new_a, a_err, ac)) return false;
+        if (!certain_aux_var(P, s_thr, new_a, a_err, ac)) return false;
     }
     out = static_cast<uint16_t>(static_cast<uint8_t>(static_cast<int8_t>(code))) |
           static_cast<uint16_t>(static_cast<uint8_t>(ac) << 8);
@@ -552,7 +562,16 @@ __global__ void __launch_bounds__(256)
         const uint32_t slot = static_cast<uint32_t>(wk.x) & 0x7fffffffu;
         const bool fresh = (static_cast<uint32_t>(wk.x) >> 31) != 0;
         const int key = wk.y;
-        const int bx = key % N, by = (key / N) % N, bz = key / (N * N);
+        int bx, by, bz;
+        if (P.nshift >= 0) {
+            bx = key & (N - 1);
+            by = (key >> P.nshift) & (N - 1);
+            bz = key >> (2 * P.nshift);
+        } else {
+            bx = key % N;
+            by = (key / N) % N;
+            bz = key / (N * N);
+        }
         // Phase A: addresses, projections and all loads of this thread's voxels issued
         // before any dependent arithmetic (memory-level parallelism).
         size_t pidx[VPT], pix[VPT];

@@ -145,7 +145,8 @@ void ensure_frame_buffers(Volume& v, FrameBuffers& fb, int w, int h);
 // tracker. All are asynchronous on `stream`; `dead_flag` (device int, may be NULL) turns
 // the launched kernels into no-ops when set (tracker after TrackingLost / PoolExhausted).
 struct RayCounters {
-    unsigned long long sample_steps, hit_pixels, rays_with_bounds, pad;
+    unsigned long long sample_steps, hit_pixels, rays_with_bounds;
+    unsigned long long listed;  // length of the active-ray list written by the ray-bounds pass
 };
 void launch_consts(const VolParams& P, const Intr& intr, const double* d_pose, FrameConsts* d_fc, cudaStream_t s,
                    uint64_t* launches);
@@ -156,11 +157,16 @@ struct FuseEvents {
 void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* depth, const float* sigma,
                  const FuseParams& fp, cudaStream_t s, bool export_lists_only, uint64_t* launches,
                  const int* dead_flag, const FuseEvents* events = nullptr);
+// With ray_list (+ list_ctr, depth, normals) the pass also appends every pixel with
+// non-empty bounds to ray_list (length in list_ctr->listed, which must start at 0) and
+// writes the empty raycast result (0 depth / normal) for the others.
 void launch_ray_bounds(Volume& v, const FrameConsts* d_fc, const Intr& intr, float* t_start, float* t_end,
-                       cudaStream_t s, uint64_t* launches, const int* dead_flag);
+                       cudaStream_t s, uint64_t* launches, const int* dead_flag, int* ray_list = nullptr,
+                       RayCounters* list_ctr = nullptr, float* depth = nullptr, float* normals = nullptr);
+// Marches the rays of ray_list (from launch_ray_bounds; length in d_stats->listed).
 void launch_raycast(Volume& v, const FrameConsts* d_fc, const Intr& intr, const float* t_start, const float* t_end,
                     float* depth, float* normals, RayCounters* d_stats, cudaStream_t s, uint64_t* launches,
-                    const int* dead_flag);
+                    const int* dead_flag, const int* ray_list);
 void launch_compute_normals(const float* depth, int w, int h, const Intr& intr, double sigma0,
                             double spatial_scale, float* normals, cudaStream_t s, uint64_t* launches,
                             const int* dead_flag);

@@ -19,9 +19,116 @@ __device__ __forceinline__ bool occupied(const uint32_t* __restrict__ occ, uint6
     return (__ldg(&occ[ti >> 5]) >> (ti & 31)) & 1u;
 }
 
-__global__ void k_ray_bounds(VolParams P, const FrameConsts* __restrict__ fc, const uint32_t* __restrict__ occ,
+// ---- exact skipping along one DDA axis -----------------------------------------------
+// An axis of the DDA is the sequence s_0 = tm, s_{k+1} = RN(s_k + td), tm, td > 0. Inside
+// one binade [2^e, 2^(e+1)) every sum is a multiple of the same ulp u, so
+// s_{k+1} = s_k + rint(td / u) * u as long as the result stays in the binade: the sequence is
+// an arithmetic progression in integer mantissa units, and one real addition carries it
+// into the next binade. (When td / u is a half-integer the sum is a rounding tie; RNE makes
+// the first result even and every later increment the even neighbour, again constant.)
+// seq_below counts the terms < X in O(binades) and returns the exact bits the sequential
+// additions would produce for the first term >= X and the last term < X.
+// floor(a / b) for 0 <= a < 2^53, 0 < b < 2^53: FP64 estimate, then exact integer correction
+// (a 64-bit integer division is a long software sequence on the GPU).
+__device__ __forceinline__ long long floor_div_53(long long a, long long b) {
+    const double bd = static_cast<double>(b);
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(bd));
+    r = fma(r, fma(-bd, r, 1.0), r);
+    r = fma(r, fma(-bd, r, 1.0), r);
+    long long j = static_cast<long long>(static_cast<double>(a) * r);
+    while (j > 0 && j * b > a) --j;
+    while ((j + 1) * b <= a) ++j;
+    return j;
+}
+
+struct SeqPos {
+    long long k;  // number of terms < X
+    double at;    // s_k (first term >= X)
+    double prev;  // s_{k-1}, or -inf when k == 0
+};
+__device__ __forceinline__ bool seq_below(double t, double d, double X, long long kmax, SeqPos& out) {
+    constexpr long long kMantMask = (1LL << 52) - 1;
+    long long K = 0;
+    double prev = -INFINITY;
+    for (int guard = 0; guard < 48; ++guard) {
+        if (!(t < X)) {
+            out = SeqPos{K, t, prev};
+            return true;
+        }
+        if (K > kmax) return false;
+        const long long tb = __double_as_longlong(t);
+        const int e = static_cast<int>((tb >> 52) & 0x7ff);
+        if (e < 64 || e > 1900) return false;
+        const double q = d * __longlong_as_double(static_cast<long long>(1075 - e + 1023) << 52);  // td / ulp(t)
+        if (!(q < 1125899906842624.0)) {  // td >= 2^50 ulps: one plain step
+            prev = t;
+            t = t + d;
+            ++K;
+            continue;
+        }
+        const double qt = q + kMagic52, qr = qt - kMagic52;
+        long long k = (__double_as_longlong(qt) & kMantMask) - (1LL << 51);  // rint(q)
+        const long long m = (tb & kMantMask) | (1LL << 52);
+        if (fabs(q - qr) == 0.5) {  // tie
+            if (m & 1) {            // odd start: one real step makes it even
+                prev = t;
+                t = t + d;
+                ++K;
+                continue;
+            }
+            const long long k0 = static_cast<long long>(floor(q));
+            k = k0 + (k0 & 1);
+        }
+        if (k <= 0) return false;  // the sequence does not move
+        constexpr long long kLim = (1LL << 53) - 1;  // largest mantissa integer of the binade
+        const long long xb = __double_as_longlong(X);
+        if (static_cast<int>((xb >> 52) & 0x7ff) == e) {
+            const long long mx = (xb & kMantMask) | (1LL << 52);
+            const long long cnt = floor_div_53(mx - m + k - 1, k);  // #{j >= 0 : m + j k < mx}
+            if (m + cnt * k <= kLim) {  // the first term >= X is still in this binade
+                out = SeqPos{K + cnt, __longlong_as_double(tb + cnt * k), __longlong_as_double(tb + (cnt - 1) * k)};
+                return out.k <= kmax;
+            }
+        }
+        const long long room = floor_div_53(kLim - m, k);  // in-binade steps j: m + j k <= kLim
+        prev = __longlong_as_double(tb + room * k);  // every in-binade term is < X
+        t = prev + d;                                // the real addition into the next binade
+        K += room + 1;
+    }
+    return false;
+}
+
+// DDA state of render.cpp:103-144.
+struct Dda {
+    int cx, cy, cz, sx, sy, sz;
+    double tmx, tmy, tmz, tdx, tdy, tdz;
+    double t_in;
+};
+// Take every step with tm < T at once (the sequential loop takes them in tm order, ties
+// x before y before z; the state after all steps below T does not depend on that order).
+// Only valid when no cell visited before T can be occupied (the caller guarantees it).
+// Returns false (state untouched) when a sequence is out of the fast path's domain.
+__device__ __forceinline__ bool dda_jump(Dda& s, double T) {
+    SeqPos px{0, s.tmx, -INFINITY}, py{0, s.tmy, -INFINITY}, pz{0, s.tmz, -INFINITY};
+    constexpr long long kMax = 1 << 24;
+    if (s.sx != 0 && !seq_below(s.tmx, s.tdx, T, kMax, px)) return false;
+    if (s.sy != 0 && !seq_below(s.tmy, s.tdy, T, kMax, py)) return false;
+    if (s.sz != 0 && !seq_below(s.tmz, s.tdz, T, kMax, pz)) return false;
+    s.cx += s.sx * static_cast<int>(px.k);
+    s.cy += s.sy * static_cast<int>(py.k);
+    s.cz += s.sz * static_cast<int>(pz.k);
+    s.tmx = px.at;
+    s.tmy = py.at;
+    s.tmz = pz.at;
+    s.t_in = dmax(s.t_in, dmax(px.prev, dmax(py.prev, pz.prev)));  // time of the last step taken
+    return true;
+}
+
+__global__ void __launch_bounds__(256, 3) k_ray_bounds(VolParams P, const FrameConsts* __restrict__ fc, const uint32_t* __restrict__ occ,
                              const VolCounters* __restrict__ vc, float* __restrict__ t_start,
-                             float* __restrict__ t_end, int w, int h, const int* dead) {
+                             float* __restrict__ t_end, int w, int h, const int* dead, int* __restrict__ ray_list,
+                             RayCounters* list_ctr, float* __restrict__ depth_out, float* __restrict__ normals_out) {
     // Coarse occupancy (1 bit per 16^3 blocks) staged in shared memory: the DDA only reads
     // the fine bitmap (L2) inside super-blocks that ever held a block. Exact: a clear coarse
     // bit implies every block of the super-block is EMPTY.
@@ -75,6 +182,7 @@ __global__ void k_ray_bounds(VolParams P, const FrameConsts* __restrict__ fc, co
         // meets no allocated block, so its DDA would find nothing.
         const int* bb = occ_bbox(P, occ);
         const int bx0 = bb[0], by0 = bb[1], bz0 = bb[2], bx1 = bb[3], by1 = bb[4], bz1 = bb[5];
+        double t_grown = -INFINITY;  // entry time into the occupied box grown by one block
         if (lo <= hi && bx0 <= bx1) {
             double rlo = lo, rhi = hi;
             const int bl[3] = {bx0, by0, bz0}, bh[3] = {bx1, by1, bz1};
@@ -96,6 +204,7 @@ __global__ void k_ray_bounds(VolParams P, const FrameConsts* __restrict__ fc, co
                 rhi = dmin(rhi, t1);
             }
             if (!(rlo <= rhi)) lo = 1.0, hi = 0.0;
+            t_grown = rlo;
         }
         if (lo <= hi && bx0 <= bx1) {
             // Scalar (register-resident) Amanatides-Woo state; same operations as render.cpp:103-144.
@@ -119,42 +228,67 @@ __global__ void k_ray_bounds(VolParams P, const FrameConsts* __restrict__ fc, co
                     td = INFINITY;
                 }
             };
-            int sx, sy, sz;
-            double tmx, tmy, tmz, tdx, tdy, tdz;
-            init_axis(dir[0], box_lo[0], cx, ex, sx, tmx, tdx);
-            init_axis(dir[1], box_lo[1], cy, ey, sy, tmy, tdy);
-            init_axis(dir[2], box_lo[2], cz, ez, sz, tmz, tdz);
+            Dda s;
+            s.cx = cx;
+            s.cy = cy;
+            s.cz = cz;
+            init_axis(dir[0], box_lo[0], cx, ex, s.sx, s.tmx, s.tdx);
+            init_axis(dir[1], box_lo[1], cy, ey, s.sy, s.tmy, s.tdy);
+            init_axis(dir[2], box_lo[2], cz, ez, s.sz, s.tmz, s.tdz);
+            s.t_in = lo;
             double first = INFINITY, last = -INFINITY;
-            double t_in = lo;
-            while (t_in <= hi) {
+            const double td_min = dmin(s.tdx, dmin(s.tdy, s.tdz));
+            // Skip the run-up to the occupied box: every cell entered before the ray reaches
+            // the box grown by one block lies outside the occupied box.
+            if (t_grown > lo + 4.0 * td_min) dda_jump(s, t_grown);
+            const double sb_side = side * (1 << kCoarseShift);
+            while (s.t_in <= hi) {
                 // Past the occupied box in the direction of travel: no later cell can be
                 // allocated (cells move monotonically per axis), so first/last are final.
-                if ((sx >= 0 && cx > bx1) || (sx <= 0 && cx < bx0) || (sy >= 0 && cy > by1) || (sy <= 0 && cy < by0) ||
-                    (sz >= 0 && cz > bz1) || (sz <= 0 && cz < bz0))
+                if ((s.sx >= 0 && s.cx > bx1) || (s.sx <= 0 && s.cx < bx0) || (s.sy >= 0 && s.cy > by1) ||
+                    (s.sy <= 0 && s.cy < by0) || (s.sz >= 0 && s.cz > bz1) || (s.sz <= 0 && s.cz < bz0))
                     break;
-                const int axis = tmx <= tmy ? (tmx <= tmz ? 0 : 2) : (tmy <= tmz ? 1 : 2);
-                const double tm = axis == 0 ? tmx : (axis == 1 ? tmy : tmz);
+                const int axis = s.tmx <= s.tmy ? (s.tmx <= s.tmz ? 0 : 2) : (s.tmy <= s.tmz ? 1 : 2);
+                const double tm = axis == 0 ? s.tmx : (axis == 1 ? s.tmy : s.tmz);
                 const double t_out = dmin(tm, hi);
-                if (cx >= bx0 && cx <= bx1 && cy >= by0 && cy <= by1 && cz >= bz0 && cz <= bz1) {
-                    const int cc = ((cz >> kCoarseShift) * P.Nc + (cy >> kCoarseShift)) * P.Nc + (cx >> kCoarseShift);
-                    if (((s_coarse[cc >> 5] >> (cc & 31)) & 1u) && occupied(occ, table_index(P, cx, cy, cz))) {
-                        first = dmin(first, t_in);
-                        last = dmax(last, t_out);
+                const int cc =
+                    ((s.cz >> kCoarseShift) * P.Nc + (s.cy >> kCoarseShift)) * P.Nc + (s.cx >> kCoarseShift);
+                if (!((s_coarse[cc >> 5] >> (cc & 31)) & 1u)) {
+                    // Super-block never held a block: jump to a quarter cell before the ray
+                    // leaves it (the cells visited up to then are inside it, hence empty).
+                    const int sbx = s.cx >> kCoarseShift, sby = s.cy >> kCoarseShift, sbz = s.cz >> kCoarseShift;
+                    const double ox_ = box_lo[0] + sbx * sb_side, oy_ = box_lo[1] + sby * sb_side,
+                                 oz_ = box_lo[2] + sbz * sb_side;
+                    double t_exit = INFINITY;
+                    if (s.sx > 0) t_exit = dmin(t_exit, (ox_ + sb_side - org[0]) / dir[0]);
+                    if (s.sx < 0) t_exit = dmin(t_exit, (ox_ - org[0]) / dir[0]);
+                    if (s.sy > 0) t_exit = dmin(t_exit, (oy_ + sb_side - org[1]) / dir[1]);
+                    if (s.sy < 0) t_exit = dmin(t_exit, (oy_ - org[1]) / dir[1]);
+                    if (s.sz > 0) t_exit = dmin(t_exit, (oz_ + sb_side - org[2]) / dir[2]);
+                    if (s.sz < 0) t_exit = dmin(t_exit, (oz_ - org[2]) / dir[2]);
+                    const double T = dmin(t_exit, hi) - 0.25 * td_min;
+                    if (T > tm + 3.0 * td_min && dda_jump(s, T)) {
+                        if (s.cx < 0 || s.cx >= n || s.cy < 0 || s.cy >= n || s.cz < 0 || s.cz >= n) break;
+                        continue;
                     }
+                } else if (s.cx >= bx0 && s.cx <= bx1 && s.cy >= by0 && s.cy <= by1 && s.cz >= bz0 && s.cz <= bz1 &&
+                           occupied(occ, table_index(P, s.cx, s.cy, s.cz))) {
+                    first = dmin(first, s.t_in);
+                    last = dmax(last, t_out);
                 }
-                t_in = tm;
+                s.t_in = tm;
                 if (axis == 0) {
-                    cx += sx;
-                    if (cx < 0 || cx >= n) break;
-                    tmx += tdx;
+                    s.cx += s.sx;
+                    if (s.cx < 0 || s.cx >= n) break;
+                    s.tmx += s.tdx;
                 } else if (axis == 1) {
-                    cy += sy;
-                    if (cy < 0 || cy >= n) break;
-                    tmy += tdy;
+                    s.cy += s.sy;
+                    if (s.cy < 0 || s.cy >= n) break;
+                    s.tmy += s.tdy;
                 } else {
-                    cz += sz;
-                    if (cz < 0 || cz >= n) break;
-                    tmz += tdz;
+                    s.cz += s.sz;
+                    if (s.cz < 0 || s.cz >= n) break;
+                    s.tmz += s.tdz;
                 }
             }
             if (first <= last) {
@@ -165,6 +299,27 @@ __global__ void k_ray_bounds(VolParams P, const FrameConsts* __restrict__ fc, co
     }
     t_start[idx] = ts;
     t_end[idx] = te;
+    if (ray_list) {
+        // Active-ray list for the march (warp-aggregated append); inactive pixels get the
+        // empty raycast result here.
+        const bool act = ts <= te;
+        if (!act) {
+            depth_out[idx] = 0.0f;
+            normals_out[3 * idx] = 0.0f;
+            normals_out[3 * idx + 1] = 0.0f;
+            normals_out[3 * idx + 2] = 0.0f;
+        }
+        const unsigned am = __activemask();
+        const unsigned bal = __ballot_sync(am, act);
+        const int lane = (threadIdx.y * blockDim.x + threadIdx.x) & 31;
+        unsigned long long base = 0;
+        if (bal) {
+            const int leader = __ffs(bal) - 1;
+            if (lane == leader) base = atomicAdd(&list_ctr->listed, static_cast<unsigned long long>(__popc(bal)));
+            base = __shfl_sync(am, base, leader);
+        }
+        if (act) ray_list[base + __popc(bal & ((1u << lane) - 1u))] = static_cast<int>(idx);
+    }
 }
 
 // voxel_code + sample_tsdf (render.cpp:12-48). Returns false for nullopt.
@@ -218,22 +373,39 @@ struct Sampler {
             // All 8 table reads issued together, then all 8 payload reads (no dependent
             // branch between loads); any EMPTY block or chi corner => nullopt.
             const int ms = P.mshift, mm = P.M - 1, N = P.N;
-            const int bxs[2] = {bx >> ms, (bx + 1) >> ms}, lxs[2] = {bx & mm, (bx + 1) & mm};
-            const int bys[2] = {by >> ms, (by + 1) >> ms}, lys[2] = {by & mm, (by + 1) & mm};
-            const int bzs[2] = {bz >> ms, (bz + 1) >> ms}, lzs[2] = {bz & mm, (bz + 1) & mm};
-            int32_t s[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-                s[i] = __ldg(&table[((size_t)bzs[i >> 2] * N + bys[(i >> 1) & 1]) * N + bxs[i & 1]]);
-            bool ok = true;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) ok = ok && s[i] != kEmpty;
-            if (!ok) return false;
+            const int lx = bx & mm, ly = by & mm, lz = bz & mm;
             uint16_t pl[8];
+            bool ok = true;
+            if (lx != mm && ly != mm && lz != mm) {
+                // all eight corners in the base block (7/8)^3 of the time: one table read
+                const int32_t slot = __ldg(&table[((size_t)(bz >> ms) * N + (by >> ms)) * N + (bx >> ms)]);
+                if (slot == kEmpty) return false;
+                const uint16_t* b = payload + (size_t)slot * P.M3 + (((lz << ms) + ly) << ms) + lx;
+                const int M = P.M, MM = M * M;
+                pl[0] = __ldg(b);
+                pl[1] = __ldg(b + 1);
+                pl[2] = __ldg(b + M);
+                pl[3] = __ldg(b + M + 1);
+                pl[4] = __ldg(b + MM);
+                pl[5] = __ldg(b + MM + 1);
+                pl[6] = __ldg(b + MM + M);
+                pl[7] = __ldg(b + MM + M + 1);
+            } else {
+                const int bxs[2] = {bx >> ms, (bx + 1) >> ms}, lxs[2] = {lx, (bx + 1) & mm};
+                const int bys[2] = {by >> ms, (by + 1) >> ms}, lys[2] = {ly, (by + 1) & mm};
+                const int bzs[2] = {bz >> ms, (bz + 1) >> ms}, lzs[2] = {lz, (bz + 1) & mm};
+                int32_t s[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-                pl[i] = __ldg(&payload[(size_t)s[i] * P.M3 + (((lzs[i >> 2] << ms) + lys[(i >> 1) & 1]) << ms) +
-                                       lxs[i & 1]]);
+                for (int i = 0; i < 8; ++i)
+                    s[i] = __ldg(&table[((size_t)bzs[i >> 2] * N + bys[(i >> 1) & 1]) * N + bxs[i & 1]]);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) ok = ok && s[i] != kEmpty;
+                if (!ok) return false;
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    pl[i] = __ldg(&payload[(size_t)s[i] * P.M3 + (((lzs[i >> 2] << ms) + lys[(i >> 1) & 1]) << ms) +
+                                           lxs[i & 1]]);
+            }
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const int8_t cc = static_cast<int8_t>(pl[i] & 0xFF);
@@ -278,13 +450,15 @@ struct Sampler {
 // Stage 2 runs redundantly in all G lanes (same addresses: broadcast loads); the six
 // gradient samples run one per lane.
 template <int G>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
     k_raycast(VolParams P, const FrameConsts* __restrict__ fc, const int32_t* __restrict__ table,
               const uint16_t* __restrict__ payload, const uint32_t* __restrict__ occ, const AuxTables* __restrict__ aux,
               const float* __restrict__ t_start, const float* __restrict__ t_end, float* __restrict__ depth_out,
-              float* __restrict__ normals_out, RayCounters* stats, int w, int h, const int* dead) {
+              float* __restrict__ normals_out, RayCounters* stats, int w, int h, const int* dead,
+              const int* __restrict__ ray_list) {
     static_assert(G >= 8 && G <= 32 && (G & (G - 1)) == 0, "group of 8..32 lanes");
-    constexpr int kTileX = 8, kTileY = 256 / G / kTileX;
+    (void)h;
+    constexpr int kRaysPerCta = 256 / G;
     __shared__ double s_tdec[256];
     if (dead && *dead) return;
     for (int i = threadIdx.x; i < 256; i += blockDim.x) s_tdec[i] = aux->tsdf_decode[i];
@@ -293,17 +467,17 @@ __global__ void __launch_bounds__(256)
     const int g = lane & (G - 1);
     const int gbase = lane & ~(G - 1);
     const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << gbase;
-    const int ray = threadIdx.x / G;
-    const int u = blockIdx.x * kTileX + ray % kTileX;
-    const int v = blockIdx.y * kTileY + ray / kTileX;
     unsigned long long steps = 0, hits = 0, with_bounds = 0;
     auto group_bits = [&](bool pred) { return (__ballot_sync(gmask, pred) & gmask) >> gbase; };
-    if (u < w && v < h) {  // uniform within the group
-        const size_t idx = (size_t)v * w + u;
+    const unsigned long long n_rays = stats->listed;
+    for (unsigned long long r = (unsigned long long)blockIdx.x * kRaysPerCta + threadIdx.x / G; r < n_rays;
+         r += (unsigned long long)gridDim.x * kRaysPerCta) {  // uniform within the group
+        const int idx = ray_list[r];
+        const int u = idx % w, v = idx / w;
         float out_d = 0.0f, nx = 0.f, ny = 0.f, nz = 0.f;
         const float fs = t_start[idx], fe = t_end[idx];
         if (fs <= fe) {  // !bounds.empty(u, v)
-            with_bounds = 1;
+            with_bounds += 1;
             const Sampler S{P, table, payload, occ, s_tdec};
             const Intr& intr = fc->intr;
             const Pose& pose = fc->pose;
@@ -392,7 +566,7 @@ __global__ void __launch_bounds__(256)
                 const double dd = root * dir_cam.z;
                 if (!(dd < intr.near_plane || dd > intr.far_plane)) {
                     out_d = (float)dd;
-                    hits = 1;
+                    hits += 1;
                     // sample_tsdf_gradient (render.cpp:50-63): lane a < 6 takes p +- h e_(a/2)
                     const d3 p = add(pose.t, scale(root, dir));
                     const double hh = (g & 1) ? -vox : vox;
@@ -442,23 +616,25 @@ __global__ void __launch_bounds__(256)
 }
 
 void launch_ray_bounds(Volume& v, const FrameConsts* d_fc, const Intr& intr, float* t_start, float* t_end,
-                       cudaStream_t s, uint64_t* launches, const int* dead_flag) {
+                       cudaStream_t s, uint64_t* launches, const int* dead_flag, int* ray_list,
+                       RayCounters* list_ctr, float* depth, float* normals) {
     const dim3 blk(32, 8), grd((intr.w + 31) / 32, (intr.h + 7) / 8);
     const uint64_t nc = v.P.Nc;
     const size_t smem = ((nc * nc * nc + 31) / 32) * sizeof(uint32_t);
     if (smem > 48 * 1024) SF_CUDA(cudaFuncSetAttribute(k_ray_bounds, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_ray_bounds<<<grd, blk, smem, s>>>(v.P, d_fc, v.d_occ, v.d_vc, t_start, t_end, intr.w, intr.h, dead_flag);
+    k_ray_bounds<<<grd, blk, smem, s>>>(v.P, d_fc, v.d_occ, v.d_vc, t_start, t_end, intr.w, intr.h, dead_flag,
+                                        ray_list, list_ctr, depth, normals);
     SF_LAUNCH_CHECK();
     if (launches) *launches += 1;
 }
 
 void launch_raycast(Volume& v, const FrameConsts* d_fc, const Intr& intr, const float* t_start, const float* t_end,
                     float* depth, float* normals, RayCounters* d_stats, cudaStream_t s, uint64_t* launches,
-                    const int* dead_flag) {
-    constexpr int G = 8;  // lanes per ray; 256-thread CTA = 8x4 pixel tile
-    const dim3 blk(256), grd((intr.w + 7) / 8, (intr.h + 3) / 4);
+                    const int* dead_flag, const int* ray_list) {
+    constexpr int G = 8;  // lanes per ray: 32 rays per 256-thread CTA, persistent over the list
+    const dim3 blk(256), grd(148 * 3);
     k_raycast<G><<<grd, blk, 0, s>>>(v.P, d_fc, v.d_table, v.d_payload, v.d_occ, v.d_aux, t_start, t_end, depth, normals,
-                                  d_stats, intr.w, intr.h, dead_flag);
+                                     d_stats, intr.w, intr.h, dead_flag, ray_list);
     SF_LAUNCH_CHECK();
     if (launches) *launches += 1;
 }
@@ -467,6 +643,7 @@ void launch_raycast(Volume& v, const FrameConsts* d_fc, const Intr& intr, const 
 struct RayScratch {
     int w = 0, h = 0;
     float *ts = nullptr, *te = nullptr, *depth = nullptr, *normals = nullptr;
+    int* list = nullptr;
     FrameConsts* fc = nullptr;
     double* pose = nullptr;
     RayCounters* stats = nullptr;
@@ -481,14 +658,16 @@ struct RayScratch {
         SF_CUDA(cudaMalloc(&fc, sizeof(FrameConsts)));
         SF_CUDA(cudaMalloc(&pose, 12 * sizeof(double)));
         SF_CUDA(cudaMalloc(&stats, sizeof(RayCounters)));
+        SF_CUDA(cudaMalloc(&list, n * sizeof(int)));
         w = W;
         h = H;
     }
     void release() {
-        void* p[] = {ts, te, depth, normals, fc, pose, stats};
+        void* p[] = {ts, te, depth, normals, fc, pose, stats, list};
         for (void* q : p)
             if (q) cudaFree(q);
         ts = te = depth = normals = nullptr;
+        list = nullptr;
         fc = nullptr;
         pose = nullptr;
         stats = nullptr;
@@ -550,10 +729,10 @@ int sf_raycast(sf_volume_t v, const double pose[12], const sf_intrinsics* intr, 
         SF_CUDA(cudaMemcpyAsync(rs.pose, pose, 12 * sizeof(double), cudaMemcpyHostToDevice, s));
         SF_CUDA(cudaMemsetAsync(rs.stats, 0, sizeof(RayCounters), s));
         launch_consts(v->P, I, rs.pose, rs.fc, s, nullptr);
-        launch_ray_bounds(*v, rs.fc, I, rs.ts, rs.te, s, nullptr, nullptr);
         float* d = out_on_device ? depth : rs.depth;
         float* nm = out_on_device ? normals_xyz : rs.normals;
-        launch_raycast(*v, rs.fc, I, rs.ts, rs.te, d, nm, rs.stats, s, nullptr, nullptr);
+        launch_ray_bounds(*v, rs.fc, I, rs.ts, rs.te, s, nullptr, nullptr, rs.list, rs.stats, d, nm);
+        launch_raycast(*v, rs.fc, I, rs.ts, rs.te, d, nm, rs.stats, s, nullptr, nullptr, rs.list);
         const size_t n = static_cast<size_t>(intr->width) * intr->height;
         if (!out_on_device) {
             SF_CUDA(cudaMemcpyAsync(depth, rs.depth, n * sizeof(float), cudaMemcpyDeviceToHost, s));

@@ -271,12 +271,17 @@ static VolParams make_params(const sf_grid_config& c, const sf_aux_quant& a, uin
     P.aux_w_max = a.w_max;
     P.aux_p_min = a.p_min;
     P.aux_p_max = a.p_max;
+    P.aux_lg_pmin = a.mode == 1 ? std::log2(a.p_min) : 0.0;
+    P.aux_lg_scale = a.mode == 1 ? 255.0 / std::log2(a.p_max / a.p_min) : 0.0;
     P.table_size = static_cast<uint64_t>(P.N) * P.N * P.N;
     P.capacity = capacity;
     P.Nc = (P.N + (1 << kCoarseShift) - 1) >> kCoarseShift;
     P.mshift = -1;
     for (int b = 0; b < 16; ++b)
         if ((1 << b) == P.M) P.mshift = b;
+    P.nshift = -1;
+    for (int b = 0; b < 16; ++b)
+        if ((1 << b) == P.N) P.nshift = b;
     P.occ_fine_words = (P.table_size + 31) / 32;
     const uint64_t nc = static_cast<uint64_t>(P.Nc);
     P.occ_coarse_words = (nc * nc * nc + 31) / 32;
