@@ -1,25 +1,24 @@
 // sf_icp.cu — projective point-to-plane ICP on the device (registration.cpp:17-224).
 //
-// Every iteration is two launches with device-side control (no host round trip):
-//   k_icp_match     per source pixel: projective association + distance / normal
-//                   rejection (registration.cpp:17-50); match record to HBM/L2; per-CTA
-//                   bbox (min/max of p and q) and count. The last CTA to finish merges the
-//                   partials -> shrink centre / scale (registration.cpp:52-74), or
-//                   TrackingLost below 10 matches (registration.cpp:202-204).
-//   k_icp_assemble  per match: shrunk row (c_hat, n), d; 21 + 6 + 1 compensated sums
-//                   (double-double TwoSum accumulators), warp shuffle -> CTA partials
-//                   (registration.cpp:76-123). The last CTA merges the partials in a fixed
-//                   order; one warp runs the Jacobi 6x6 (rows across lanes, bit-identical to
-//                   the sequential sweep), one thread the gated solve, unshrink, apply_motion
-//                   and the convergence test (registration.cpp:125-220).
+// Every iteration is ONE launch with device-side control (no host round trip):
+//   k_icp_step  per source pixel: projective association + distance / normal rejection
+//               (registration.cpp:17-50), then the 21 + 6 + 1 normal-equation sums in
+//               unshrunk form (double-double TwoSum accumulators) and the shrink bounding box
+//               (registration.cpp:52-123); CTA partials in a fixed order. The last CTA merges
+//               them, raises TrackingLost below 10 matches (registration.cpp:202-204), forms
+//               the shrink (centre / scale) and applies it to the sums as a linear map; one
+//               warp runs the Jacobi 6x6 (rows across lanes, bit-identical to the sequential
+//               sweep), one thread the gated solve, unshrink, apply_motion and the
+//               convergence test (registration.cpp:125-220).
 // Under CUDA-graph capture (tracker) the iterations are a conditional WHILE node: the body
 // repeats until converged / lost / max_iterations, decided on the device. Issued eagerly,
 // a converged / failed state makes the remaining iterations' kernels exit at once.
 // Partials are merged in a fixed order, so results are deterministic run to run.
 //
-// Parity: the association and every per-match quantity are FP64 in the reference order.
-// The only deviation is the summation order of the 28 sums (tree instead of sequential
-// Kahan); both are within ~1 ulp of the exact sum, pose parity is asserted at 1e-6.
+// Parity: the association is FP64 in the reference order (the same matches). The normal
+// equations differ from the reference's by rounding only: tree instead of sequential Kahan
+// summation, and shrink applied to the sums instead of to each match (~1e-15 relative);
+// pose parity is asserted at 1e-6.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -49,156 +48,6 @@ __device__ __forceinline__ bool last_cta(unsigned int* counter) {
     __syncthreads();
     if (s_last) __threadfence();
     return s_last;
-}
-
-// shrink's centre / scale (registration.cpp:54-64) from the bbox partials (min/max and
-// integer counts are exact in any order).
-__device__ void bbox_finalize(IcpState* st, const double* __restrict__ part_bbox,
-                              const unsigned long long* __restrict__ part_count, int nparts, const IcpParamsDev& prm) {
-    double b[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
-    unsigned long long cnt = 0;
-    for (int p = threadIdx.x; p < nparts; p += blockDim.x) {
-        const volatile double* pb = part_bbox + p * 6;
-        for (int a = 0; a < 3; ++a) {
-            b[a] = dmin(b[a], pb[a]);
-            b[3 + a] = dmax(b[3 + a], pb[3 + a]);
-        }
-        cnt += ((const volatile unsigned long long*)part_count)[p];
-    }
-    for (int off = 16; off > 0; off >>= 1) {
-        for (int a = 0; a < 3; ++a) {
-            b[a] = dmin(b[a], __shfl_down_sync(0xffffffffu, b[a], off));
-            b[3 + a] = dmax(b[3 + a], __shfl_down_sync(0xffffffffu, b[3 + a], off));
-        }
-        cnt += __shfl_down_sync(0xffffffffu, cnt, off);
-    }
-    __shared__ double s_b[kIcpThreads / 32][6];
-    __shared__ unsigned long long s_c[kIcpThreads / 32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (lane == 0) {
-        for (int a = 0; a < 6; ++a) s_b[wid][a] = b[a];
-        s_c[wid] = cnt;
-    }
-    __syncthreads();
-    if (threadIdx.x != 0) return;
-    for (int k = 1; k < (int)(blockDim.x / 32); ++k) {
-        for (int a = 0; a < 3; ++a) {
-            s_b[0][a] = dmin(s_b[0][a], s_b[k][a]);
-            s_b[0][3 + a] = dmax(s_b[0][3 + a], s_b[k][3 + a]);
-        }
-        s_c[0] += s_c[k];
-    }
-    cnt = s_c[0];
-    if (cnt < 10) {
-        st->lost = 1;
-        st->lost_count = cnt;
-        st->done = 1;
-        return;
-    }
-    st->matches = cnt;
-    st->cur_count = cnt;
-    const d3 l = mk(s_b[0][0], s_b[0][1], s_b[0][2]), hh = mk(s_b[0][3], s_b[0][4], s_b[0][5]);
-    const d3 c = scale(0.5, add(l, hh));
-    const d3 ext = sub(hh, l);
-    const d3 s = mk(dmax(ext.x, prm.floor), dmax(ext.y, prm.floor), dmax(ext.z, prm.floor));  // cwiseMax(floor)
-    st->center = c;
-    st->scale = s;
-    st->inv_scale = mk(1.0 / s.x, 1.0 / s.y, 1.0 / s.z);
-}
-
-// match_points (registration.cpp:17-50) + bbox partials of shrink (registration.cpp:54-59)
-__global__ void __launch_bounds__(kIcpThreads)
-    k_icp_match(const float* __restrict__ src, const float* __restrict__ src_n, const float* __restrict__ tgt,
-                const float* __restrict__ tgt_n, Intr si, Intr ti, IcpParamsDev prm, IcpState* st,
-                MatchRec* __restrict__ rec, uint8_t* __restrict__ flag, double* __restrict__ part_bbox,
-                unsigned long long* __restrict__ part_count, unsigned int* counter) {
-    if (st->done) return;
-    const Pose delta = st->delta;
-    const int w = si.w, h = si.h;
-    const int n = w * h;
-    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-    unsigned long long cnt = 0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int u = i % w, v = i / w;
-        uint8_t ok = 0;
-        const float sd = src[i];
-        const float snx = src_n[3 * i], sny = src_n[3 * i + 1], snz = src_n[3 * i + 2];
-        if (sd > 0.0f && (snx * snx + sny * sny) + snz * snz > 0.0f) {
-            const d3 p = apply(delta, unproject(si, u, v, sd));
-            double pu, pv;
-            if (project(ti, p, pu, pv)) {
-                const int tu = ref_lround_int(pu), tv = ref_lround_int(pv);
-                if (tu >= 0 && tv >= 0 && tu < ti.w && tv < ti.h) {
-                    const int j = tv * ti.w + tu;
-                    const float td = tgt[j];
-                    const float tnx = tgt_n[3 * j], tny = tgt_n[3 * j + 1], tnz = tgt_n[3 * j + 2];
-                    if (td > 0.0f && (tnx * tnx + tny * tny) + tnz * tnz > 0.0f) {
-                        const d3 q = unproject(ti, tu, tv, td);
-                        if (!(sqnorm(sub(p, q)) > prm.max_dist_sq)) {
-                            const d3 nn = mk(tnx, tny, tnz);
-                            const d3 ns = mv(delta.R, mk(snx, sny, snz));
-                            if (!(dot(ns, nn) < prm.cos_max)) {
-                                ok = 1;
-                                MatchRec r;
-                                r.p[0] = p.x;
-                                r.p[1] = p.y;
-                                r.p[2] = p.z;
-                                r.q[0] = q.x;
-                                r.q[1] = q.y;
-                                r.q[2] = q.z;
-                                r.n[0] = nn.x;
-                                r.n[1] = nn.y;
-                                r.n[2] = nn.z;
-                                rec[i] = r;
-                                const double pp[3] = {p.x, p.y, p.z}, qq[3] = {q.x, q.y, q.z};
-                                for (int a = 0; a < 3; ++a) {
-                                    lo[a] = dmin(dmin(lo[a], pp[a]), qq[a]);
-                                    hi[a] = dmax(dmax(hi[a], pp[a]), qq[a]);
-                                }
-                                ++cnt;
-                            }
-                        }
-                    }
-                }
-            }
-        }
-        flag[i] = ok;
-    }
-    // CTA reduction (min/max are exact: order-free)
-    for (int off = 16; off > 0; off >>= 1) {
-        for (int a = 0; a < 3; ++a) {
-            lo[a] = dmin(lo[a], __shfl_down_sync(0xffffffffu, lo[a], off));
-            hi[a] = dmax(hi[a], __shfl_down_sync(0xffffffffu, hi[a], off));
-        }
-        cnt += __shfl_down_sync(0xffffffffu, cnt, off);
-    }
-    __shared__ double s_b[kIcpThreads / 32][6];
-    __shared__ unsigned long long s_c[kIcpThreads / 32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (lane == 0) {
-        for (int a = 0; a < 3; ++a) {
-            s_b[wid][a] = lo[a];
-            s_b[wid][3 + a] = hi[a];
-        }
-        s_c[wid] = cnt;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int k = 1; k < kIcpThreads / 32; ++k) {
-            for (int a = 0; a < 3; ++a) {
-                s_b[0][a] = dmin(s_b[0][a], s_b[k][a]);
-                s_b[0][3 + a] = dmax(s_b[0][3 + a], s_b[k][3 + a]);
-            }
-            s_c[0] += s_c[k];
-        }
-        for (int a = 0; a < 6; ++a) part_bbox[blockIdx.x * 6 + a] = s_b[0][a];
-        part_count[blockIdx.x] = s_c[0];
-    }
-    if (last_cta(counter)) {
-        if (threadIdx.x == 0) st->bodies += 1;
-        bbox_finalize(st, part_bbox, part_count, gridDim.x, prm);
-        if (threadIdx.x == 0) *counter = 0;
-    }
 }
 
 // solve_gated + apply_motion + convergence (registration.cpp:175-212), one thread.
@@ -242,75 +91,211 @@ __device__ __noinline__ void solve_finalize(IcpState* st, const double* s_sum, c
     const d3 t = sub(mk(x[3], x[4], x[5]), cross(r, c));
     st->motion_r = r;
     st->motion_t = t;
-    st->delta = apply_motion(st->delta, r, t);
+    st->delta = apply_motion_fast(st->delta, r, t);
     st->iterations = iter + 1;
     if (st->shrunk_norm < prm.eps) st->done = 1;
 }
 
+constexpr int kStepCtas = 148;  // one CTA per SM (double-double accumulators); fixed => deterministic
+constexpr int kStepSmem = kSums * kIcpThreads * static_cast<int>(sizeof(DD));  // CTA-reduction transpose
 constexpr int kMergeLanes = kIcpThreads / kSums;  // threads per sum in the final merge (252 of 256 busy)
 
-// assemble (registration.cpp:93-123) on the shrunk matches (registration.cpp:65-72).
-__global__ void __launch_bounds__(kIcpThreads)
-    k_icp_assemble(IcpState* st, const MatchRec* __restrict__ rec, const uint8_t* __restrict__ flag, int n,
-                   DD* __restrict__ part, unsigned int* counter, IcpParamsDev prm, int use_cond,
-                   cudaGraphConditionalHandle cond) {
-    if (st->done) {  // converged / lost (possibly in this iteration's match pass): end the loop
+// match_points association for source pixel i (registration.cpp:17-50).
+__device__ __forceinline__ bool associate(int i, const float* __restrict__ src, const float* __restrict__ src_n,
+                                          const float* __restrict__ tgt, const float* __restrict__ tgt_n,
+                                          const Intr& si, const Intr& ti, const IcpParamsDev& prm, const Pose& delta,
+                                          d3& p, d3& q, d3& nn) {
+    const int u = i % si.w, v = i / si.w;
+    const float sd = src[i];
+    const float snx = src_n[3 * i], sny = src_n[3 * i + 1], snz = src_n[3 * i + 2];
+    if (!(sd > 0.0f && (snx * snx + sny * sny) + snz * snz > 0.0f)) return false;
+    p = apply(delta, unproject(si, u, v, sd));
+    double pu, pv;
+    if (!project(ti, p, pu, pv)) return false;
+    const int tu = ref_lround_int(pu), tv = ref_lround_int(pv);
+    if (!(tu >= 0 && tv >= 0 && tu < ti.w && tv < ti.h)) return false;
+    const int j = tv * ti.w + tu;
+    const float td = tgt[j];
+    const float tnx = tgt_n[3 * j], tny = tgt_n[3 * j + 1], tnz = tgt_n[3 * j + 2];
+    if (!(td > 0.0f && (tnx * tnx + tny * tny) + tnz * tnz > 0.0f)) return false;
+    q = unproject(ti, tu, tv, td);
+    if (sqnorm(sub(p, q)) > prm.max_dist_sq) return false;
+    nn = mk(tnx, tny, tnz);
+    const d3 ns = mv(delta.R, mk(snx, sny, snz));
+    return !(dot(ns, nn) < prm.cos_max);
+}
+
+__host__ __device__ constexpr int packed_index(int i, int j) {  // upper triangle of 6x6, row-major, i <= j
+    return i * 6 - i * (i - 1) / 2 + (j - i);
+}
+
+// One ICP iteration (registration.cpp:17-123 + 175-212) in one launch.
+//
+// The reference shrinks the matches (centre c, scale s from their bounding box) before it
+// assembles A = sum row row^T, b = -sum row d with row = (s^-1 (p - c) x n, n) and
+// d = (s (p^ - q^)) . n. Both are linear in the unshrunk sums: row = L (p x n, n) with
+// L = [[S^-1, -S^-1 [c]x], [0, I]] and d = (p - q) . n, so A = L S6 L^T, b = -L t6 where
+// S6 = sum r r^T, t6 = sum r d over r = (p x n, n). Every CTA therefore accumulates the 28
+// unshrunk sums (double-double) together with the bounding box in the same pass as the
+// association, and the last CTA to finish merges the partials in a fixed order, forms c, s,
+// applies L (~1e-15 relative: the same result as shrinking first, up to rounding), runs the
+// warp-parallel Jacobi and the gated solve. No match records go through HBM.
+__global__ void __launch_bounds__(kIcpThreads, 1)
+    k_icp_step(const float* __restrict__ src, const float* __restrict__ src_n, const float* __restrict__ tgt,
+               const float* __restrict__ tgt_n, Intr si, Intr ti, IcpParamsDev prm, IcpState* st,
+               double* __restrict__ part_bbox, unsigned long long* __restrict__ part_count, DD* __restrict__ part,
+               unsigned int* counter, int use_cond, cudaGraphConditionalHandle cond) {
+    extern __shared__ DD s_red[];  // [kSums][kIcpThreads]
+    if (st->done) {  // converged / lost: end the device-side loop
         if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0u);
         return;
     }
-    const d3 c = st->center, inv = st->inv_scale, scl = st->scale;
+    const Pose delta = st->delta;
+    const int n = si.w * si.h;
+    const int tid = threadIdx.x;
     DD acc[kSums];
 #pragma unroll
     for (int k = 0; k < kSums; ++k) acc[k] = DD{0.0, 0.0};
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        if (!flag[i]) continue;
-        const MatchRec r = rec[i];
-        const d3 p = mk(r.p[0], r.p[1], r.p[2]), q = mk(r.q[0], r.q[1], r.q[2]), nn = mk(r.n[0], r.n[1], r.n[2]);
-        const d3 p_hat = cmul(inv, sub(p, c));
-        const d3 q_hat = cmul(inv, sub(q, c));
-        const d3 c_hat = cmul(inv, sub(cross(p, nn), cross(c, nn)));
-        const double row[6] = {c_hat.x, c_hat.y, c_hat.z, nn.x, nn.y, nn.z};
-        const double d = dot(cmul(scl, sub(p_hat, q_hat)), nn);
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    unsigned long long cnt = 0;
+    for (int i = blockIdx.x * blockDim.x + tid; i < n; i += gridDim.x * blockDim.x) {
+        d3 p, q, nn;
+        if (!associate(i, src, src_n, tgt, tgt_n, si, ti, prm, delta, p, q, nn)) continue;
+        const d3 pxn = cross(p, nn);
+        const double r[6] = {pxn.x, pxn.y, pxn.z, nn.x, nn.y, nn.z};
+        const double d = dot(sub(p, q), nn);
         int k = 0;
 #pragma unroll
         for (int a = 0; a < 6; ++a)
 #pragma unroll
-            for (int b = a; b < 6; ++b, ++k) dd_add(acc[k], row[a] * row[b]);
+            for (int b = a; b < 6; ++b, ++k) dd_add(acc[k], r[a] * r[b]);
 #pragma unroll
-        for (int a = 0; a < 6; ++a) dd_add(acc[21 + a], -row[a] * d);
+        for (int a = 0; a < 6; ++a) dd_add(acc[21 + a], r[a] * d);
         dd_add(acc[27], d * d);
+        const double pp[3] = {p.x, p.y, p.z}, qq[3] = {q.x, q.y, q.z};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {  // shrink's bounding box (registration.cpp:54-59)
+            lo[a] = dmin(dmin(lo[a], pp[a]), qq[a]);
+            hi[a] = dmax(dmax(hi[a], pp[a]), qq[a]);
+        }
+        ++cnt;
     }
-    // warp tree
+    // ---- CTA reduction: box and count by shuffles (exact in any order); the 28 sums by a
+    // shared-memory transpose in a fixed order (thread order within 32-thread segments).
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
 #pragma unroll
-        for (int k = 0; k < kSums; ++k) {
-            DD o;
-            o.hi = __shfl_down_sync(0xffffffffu, acc[k].hi, off);
-            o.lo = __shfl_down_sync(0xffffffffu, acc[k].lo, off);
-            dd_merge(acc[k], o);
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = dmin(lo[a], __shfl_down_sync(0xffffffffu, lo[a], off));
+            hi[a] = dmax(hi[a], __shfl_down_sync(0xffffffffu, hi[a], off));
         }
+        cnt += __shfl_down_sync(0xffffffffu, cnt, off);
     }
-    __shared__ DD s_acc[kIcpThreads / 32][kSums];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (lane == 0)
-        for (int k = 0; k < kSums; ++k) s_acc[wid][k] = acc[k];
+    __shared__ double s_b[kIcpThreads / 32][6];
+    __shared__ unsigned long long s_c[kIcpThreads / 32];
+    const int lane = tid & 31, wid = tid >> 5;
+    if (lane == 0) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            s_b[wid][a] = lo[a];
+            s_b[wid][3 + a] = hi[a];
+        }
+        s_c[wid] = cnt;
+    }
+#pragma unroll
+    for (int k = 0; k < kSums; ++k) s_red[k * kIcpThreads + tid] = acc[k];
     __syncthreads();
-    if (threadIdx.x < kSums) {
-        DD a = s_acc[0][threadIdx.x];
-        for (int w = 1; w < kIcpThreads / 32; ++w) dd_merge(a, s_acc[w][threadIdx.x]);
-        part[blockIdx.x * kSums + threadIdx.x] = a;
+    constexpr int kSeg = kIcpThreads / 32;  // 8 segments of 32 threads per sum
+    DD seg{0.0, 0.0};
+    if (tid < kSums * kSeg) {
+        const DD* row = s_red + (tid / kSeg) * kIcpThreads + (tid % kSeg) * 32;
+        seg = row[0];
+        for (int t = 1; t < 32; ++t) dd_merge(seg, row[t]);
+    }
+    __syncthreads();
+    if (tid < kSums * kSeg) s_red[(tid / kSeg) * kIcpThreads + (tid % kSeg)] = seg;
+    if (tid == 0) {
+        for (int w = 1; w < kIcpThreads / 32; ++w) {
+            for (int a = 0; a < 3; ++a) {
+                s_b[0][a] = dmin(s_b[0][a], s_b[w][a]);
+                s_b[0][3 + a] = dmax(s_b[0][3 + a], s_b[w][3 + a]);
+            }
+            s_c[0] += s_c[w];
+        }
+        for (int a = 0; a < 6; ++a) part_bbox[blockIdx.x * 6 + a] = s_b[0][a];
+        part_count[blockIdx.x] = s_c[0];
+    }
+    __syncthreads();
+    if (tid < kSums) {
+        DD a = s_red[tid * kIcpThreads];
+        for (int j = 1; j < kSeg; ++j) dd_merge(a, s_red[tid * kIcpThreads + j]);
+        part[blockIdx.x * kSums + tid] = a;
     }
     if (!last_cta(counter)) return;
-    // Fixed-order merge of all CTA partials: sum k, lane j takes partials j, j+L, ... The
-    // loads go straight to L2 (ld.cg, after last_cta's fence) in batches of kBatch so their
-    // latencies overlap; the merge order is fixed, so the result is deterministic.
+
+    // ---- last CTA: merge the partials (fixed order) --------------------------------------
+    const int nparts = gridDim.x;
+    __shared__ int s_lost;
+    {
+        double b[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        unsigned long long c = 0;
+        for (int p = tid; p < nparts; p += blockDim.x) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                b[a] = dmin(b[a], __ldcg(&part_bbox[p * 6 + a]));
+                b[3 + a] = dmax(b[3 + a], __ldcg(&part_bbox[p * 6 + 3 + a]));
+            }
+            c += __ldcg(&part_count[p]);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                b[a] = dmin(b[a], __shfl_down_sync(0xffffffffu, b[a], off));
+                b[3 + a] = dmax(b[3 + a], __shfl_down_sync(0xffffffffu, b[3 + a], off));
+            }
+            c += __shfl_down_sync(0xffffffffu, c, off);
+        }
+        __syncthreads();  // s_b / s_c reuse
+        if (lane == 0) {
+            for (int a = 0; a < 6; ++a) s_b[wid][a] = b[a];
+            s_c[wid] = c;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int w = 1; w < kIcpThreads / 32; ++w) {
+                for (int a = 0; a < 3; ++a) {
+                    s_b[0][a] = dmin(s_b[0][a], s_b[w][a]);
+                    s_b[0][3 + a] = dmax(s_b[0][3 + a], s_b[w][3 + a]);
+                }
+                s_c[0] += s_c[w];
+            }
+            const unsigned long long total = s_c[0];
+            st->bodies += 1;
+            s_lost = total < 10 ? 1 : 0;
+            if (total < 10) {  // TrackingLost (registration.cpp:202-204)
+                st->lost = 1;
+                st->lost_count = total;
+                st->done = 1;
+            } else {
+                st->matches = total;
+                st->cur_count = total;
+                // shrink centre / scale (registration.cpp:54-64)
+                const d3 l = mk(s_b[0][0], s_b[0][1], s_b[0][2]), hh = mk(s_b[0][3], s_b[0][4], s_b[0][5]);
+                const d3 cc = scale(0.5, add(l, hh));
+                const d3 ext = sub(hh, l);
+                const d3 sc = mk(dmax(ext.x, prm.floor), dmax(ext.y, prm.floor), dmax(ext.z, prm.floor));
+                st->center = cc;
+                st->scale = sc;
+                st->inv_scale = mk(1.0 / sc.x, 1.0 / sc.y, 1.0 / sc.z);
+            }
+        }
+    }
     constexpr int L = kMergeLanes, kBatch = 8;
     __shared__ DD s_m[kSums][L];
-    __shared__ double s_sum[kSums];
-    const int nparts = gridDim.x;
-    if (threadIdx.x < kSums * L) {
-        const int k = threadIdx.x % kSums, j = threadIdx.x / kSums;
+    __shared__ double s_sum[kSums], s_fin[kSums];
+    if (tid < kSums * L) {
+        const int k = tid % kSums, j = tid / kSums;
         const double2* vp = reinterpret_cast<const double2*>(part);
         DD a{0.0, 0.0};
         bool first = true;
@@ -336,27 +321,87 @@ __global__ void __launch_bounds__(kIcpThreads)
         s_m[k][j] = a;
     }
     __syncthreads();
-    if (threadIdx.x < kSums) {
-        DD a = s_m[threadIdx.x][0];
-        for (int j = 1; j < kMergeLanes; ++j) dd_merge(a, s_m[threadIdx.x][j]);
-        s_sum[threadIdx.x] = a.hi + a.lo;
+    if (s_lost) {
+        if (tid == 0) {
+            *counter = 0;
+            if (use_cond) cudaGraphSetConditional(cond, 0u);
+        }
+        return;
+    }
+    if (tid < kSums) {
+        DD a = s_m[tid][0];
+        for (int j = 1; j < L; ++j) dd_merge(a, s_m[tid][j]);
+        s_sum[tid] = a.hi + a.lo;
     }
     __syncthreads();
-    if (threadIdx.x < 32) {
-        __shared__ double s_A[36];
-        __shared__ Eig6 s_eig;
-        for (int i = threadIdx.x; i < 36; i += 32) {
-            const int r = i / 6, c = i % 6, lo = r < c ? r : c, hi = r < c ? c : r;
-            s_A[i] = s_sum[lo * 6 - lo * (lo - 1) / 2 + (hi - lo)];  // packed upper triangle, row-major
+    if (tid >= 32) return;
+    // ---- shrink as a linear map on the sums: A = L S6 L^T, b = -L t6, with
+    // L = [[D, -D C], [0, I]], D = diag(1/s), C = [c]x (one thread, fully unrolled: the 36
+    // entries are independent, so the latency overlaps).
+    if (lane == 0) {
+        const d3 c = st->center, inv = st->inv_scale;
+        const double C[3][3] = {{0.0, -c.z, c.y}, {c.z, 0.0, -c.x}, {-c.y, c.x, 0.0}};
+        const double D[3] = {inv.x, inv.y, inv.z};
+        double S[6][6];
+#pragma unroll
+        for (int i = 0; i < 6; ++i)
+#pragma unroll
+            for (int j = i; j < 6; ++j) S[i][j] = S[j][i] = s_sum[packed_index(i, j)];
+        // G = S L^T restricted to what is needed: G[k][j] = sum_l S[k][l] L[j][l]
+        double G[6][6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {  // L[j] = (D_j e_j, -D_j C[j])
+                double t = S[k][j];
+#pragma unroll
+                for (int l = 0; l < 3; ++l) t -= S[k][3 + l] * C[j][l];
+                G[k][j] = D[j] * t;
+            }
+#pragma unroll
+            for (int j = 3; j < 6; ++j) G[k][j] = S[k][j];
         }
-        __syncwarp();
-        eigendecompose_sym6_warp(s_A, &s_eig);
-        __syncwarp();
-        if (threadIdx.x == 0) {
-            solve_finalize(st, s_sum, s_eig, prm);
-            *counter = 0;
-            if (use_cond) cudaGraphSetConditional(cond, (!st->done && st->iterations < prm.max_iterations) ? 1u : 0u);
+#pragma unroll
+        for (int i = 0; i < 6; ++i)
+#pragma unroll
+            for (int j = i; j < 6; ++j) {
+                double a;
+                if (i < 3) {
+                    a = G[i][j];
+#pragma unroll
+                    for (int l = 0; l < 3; ++l) a -= C[i][l] * G[3 + l][j];
+                    a *= D[i];
+                } else {
+                    a = G[i][j];
+                }
+                s_fin[packed_index(i, j)] = a;
+            }
+        const double* T = s_sum + 21;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            double t = T[i];
+#pragma unroll
+            for (int l = 0; l < 3; ++l) t -= C[i][l] * T[3 + l];
+            s_fin[21 + i] = -(D[i] * t);
         }
+#pragma unroll
+        for (int i = 3; i < 6; ++i) s_fin[21 + i] = -T[i];
+        s_fin[27] = s_sum[27];
+    }
+    __syncwarp();
+    __shared__ double s_A[36];
+    __shared__ Eig6 s_eig;
+    for (int i = lane; i < 36; i += 32) {
+        const int r = i / 6, cc = i % 6;
+        s_A[i] = s_fin[r <= cc ? packed_index(r, cc) : packed_index(cc, r)];
+    }
+    __syncwarp();
+    eigendecompose_sym6_warp_rr(s_A, &s_eig);
+    __syncwarp();
+    if (lane == 0) {
+        solve_finalize(st, s_fin, s_eig, prm);
+        *counter = 0;
+        if (use_cond) cudaGraphSetConditional(cond, (!st->done && st->iterations < prm.max_iterations) ? 1u : 0u);
     }
 }
 
@@ -382,7 +427,7 @@ IcpParamsDev make_icp_params(const sf_match_params& p) {
 void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* tgt, const float* tgt_n,
                 const Intr& si, const Intr& ti, const double* d_initial, const IcpParamsDev& prm, cudaStream_t s,
                 uint64_t* launches, const int* dead, bool* device_loop) {
-    const int n = si.w * si.h;
+    SF_CUDA(cudaFuncSetAttribute(k_icp_step, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem));
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     SF_CUDA(cudaStreamIsCapturing(s, &cs));
     // SF_ICP_DEVICE_LOOP=0 keeps the fixed launch sequence under capture too (Nsight Compute
@@ -398,12 +443,10 @@ void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* 
         SF_LAUNCH_CHECK();
         uint64_t cnt = 1;
         for (int it = 0; it < prm.max_iterations; ++it) {
-            k_icp_match<<<kIcpCtas, kIcpThreads, 0, s>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st, wk.rec, wk.flag,
-                                                         wk.part_bbox, wk.part_count, wk.counters);
-            k_icp_assemble<<<kIcpCtas, kIcpThreads, 0, s>>>(wk.st, wk.rec, wk.flag, n, wk.part, wk.counters + 1, prm,
-                                                            0, 0);
+            k_icp_step<<<kStepCtas, kIcpThreads, kStepSmem, s>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st,
+                                                                 wk.part_bbox, wk.part_count, wk.part, wk.counters, 0, 0);
             SF_LAUNCH_CHECK();
-            cnt += 2;
+            cnt += 1;
         }
         if (launches) *launches += cnt;
         return;
@@ -429,10 +472,8 @@ void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* 
     if (!wk.body_stream) SF_CUDA(cudaStreamCreateWithFlags(&wk.body_stream, cudaStreamNonBlocking));
     cudaStream_t bs = wk.body_stream;
     SF_CUDA(cudaStreamBeginCaptureToGraph(bs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    k_icp_match<<<kIcpCtas, kIcpThreads, 0, bs>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st, wk.rec, wk.flag,
-                                                  wk.part_bbox, wk.part_count, wk.counters);
-    k_icp_assemble<<<kIcpCtas, kIcpThreads, 0, bs>>>(wk.st, wk.rec, wk.flag, n, wk.part, wk.counters + 1, prm, 1,
-                                                     cond);
+    k_icp_step<<<kStepCtas, kIcpThreads, kStepSmem, bs>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st, wk.part_bbox,
+                                                          wk.part_count, wk.part, wk.counters, 1, cond);
     const cudaError_t le = cudaGetLastError();
     cudaGraph_t captured = nullptr;
     const cudaError_t ee = cudaStreamEndCapture(bs, &captured);

@@ -32,7 +32,7 @@ struct IcpState {
     int done;       // converged or failed: later iterations are no-ops
     int lost;       // TrackingLost raised
     int iterations;
-    int bodies;     // iterations whose match pass ran (device-side loop: kernel launches = 2 x bodies)
+    int bodies;     // iterations whose step kernel ran (device-side loop: one launch each)
     unsigned long long matches;       // matches of the last completed iteration
     unsigned long long lost_count;    // match count that triggered TrackingLost
     d3 center, scale, inv_scale;      // shrink of the current iteration
@@ -51,15 +51,9 @@ struct IcpParamsDev {
     int max_iterations;
 };
 
-struct MatchRec {
-    double p[3], q[3], n[3];
-};
-
 // Scratch for one ICP (owned by the caller: stand-alone API or tracker).
 struct IcpWork {
     int w = 0, h = 0;
-    MatchRec* rec = nullptr;
-    uint8_t* flag = nullptr;
     double* part_bbox = nullptr;
     unsigned long long* part_count = nullptr;
     DD* part = nullptr;
@@ -69,13 +63,11 @@ struct IcpWork {
     double* initial = nullptr;
     unsigned int* counters = nullptr;  // "last CTA" tickets of the two fused reductions
     void ensure(int W, int H) {
-        if (W == w && H == h && rec) return;
+        if (W == w && H == h && st) return;
         release();
         const size_t n = static_cast<size_t>(W) * H;
         SF_CUDA(cudaMalloc(&counters, 4 * sizeof(unsigned int)));
         SF_CUDA(cudaMemset(counters, 0, 4 * sizeof(unsigned int)));
-        SF_CUDA(cudaMalloc(&rec, n * sizeof(MatchRec)));
-        SF_CUDA(cudaMalloc(&flag, n));
         SF_CUDA(cudaMalloc(&part_bbox, kIcpCtas * 6 * sizeof(double)));
         SF_CUDA(cudaMalloc(&part_count, kIcpCtas * sizeof(unsigned long long)));
         SF_CUDA(cudaMalloc(&part, kIcpCtas * kSums * sizeof(DD)));
@@ -90,13 +82,11 @@ struct IcpWork {
         h = H;
     }
     void release() {
-        void* p[] = {rec, flag, part_bbox, part_count, part, st, src_normals, src, tgt, tgt_n, src_n_in, initial,
+        void* p[] = {part_bbox, part_count, part, st, src_normals, src, tgt, tgt_n, src_n_in, initial,
                      counters};
         for (void* q : p)
             if (q) cudaFree(q);
         counters = nullptr;
-        rec = nullptr;
-        flag = nullptr;
         part_bbox = nullptr;
         part_count = nullptr;
         part = nullptr;

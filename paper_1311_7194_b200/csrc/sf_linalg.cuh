@@ -429,4 +429,163 @@ SF_HD Pose apply_motion(const Pose& pose, d3 r, d3 t) {
     return compose(corr, pose);
 }
 
+// apply_motion with the polar factor in closed form. The small-angle matrix is I + [w]x
+// (w = r); (I + W)^T (I + W) = I - W^2 has eigenvalue 1 along w and 1 + |w|^2 across it, so
+// its nearest rotation U V^T = (I + W) (I - W^2)^(-1/2) = k (I + W) + m w w^T with
+// k = 1 / sqrt(1 + |w|^2), m = 1 / (sqrt(1 + |w|^2) (1 + sqrt(1 + |w|^2))) (W w = 0).
+// Equal to the SVD route up to rounding (the polar factor of a non-singular matrix is
+// unique); one sqrt and two divisions instead of Jacobi SVD sweeps.
+SF_HD Pose apply_motion_fast(const Pose& pose, d3 r, d3 t) {
+    const double a = r.x, b = r.y, g = r.z;
+    const double x = (a * a + b * b) + g * g;
+    const double sq = sqrt(1.0 + x);
+    const double k = 1.0 / sq, m = 1.0 / (sq * (1.0 + sq));
+    Pose corr;
+    corr.R.m[0] = k + m * a * a;
+    corr.R.m[1] = -k * g + m * a * b;
+    corr.R.m[2] = k * b + m * a * g;
+    corr.R.m[3] = k * g + m * b * a;
+    corr.R.m[4] = k + m * b * b;
+    corr.R.m[5] = -k * a + m * b * g;
+    corr.R.m[6] = -k * b + m * g * a;
+    corr.R.m[7] = k * a + m * g * b;
+    corr.R.m[8] = k + m * g * g;
+    corr.t = t;
+    return compose(corr, pose);
+}
+
+#ifdef __CUDACC__
+// Jacobi eigendecomposition of a symmetric 6x6 by one warp with the parallel (round-robin)
+// ordering: each sweep is 5 rounds of 3 disjoint rotations, applied together (disjoint plane
+// rotations commute), so a sweep has 5 dependent rotation steps instead of 15. Same
+// rotation formula, thresholds and stopping rule as registration.cpp:125-165; the ordering
+// changes rounding only (the device ICP is tolerance-checked). Lane i < 6
+// owns row i of m and of v. Output as eigendecompose_sym6 (ascending, stable order).
+__device__ __forceinline__ void eigendecompose_sym6_warp_rr(const double* a, Eig6* out) {
+    constexpr unsigned kFull = 0xffffffffu;
+    // partner of lane i in round r (perfect matchings of K6)
+    constexpr int kPartner[5][6] = {{1, 0, 3, 2, 5, 4}, {2, 4, 0, 5, 1, 3}, {3, 5, 4, 0, 2, 1},
+                                    {4, 3, 5, 1, 0, 2}, {5, 2, 1, 4, 3, 0}};
+    const int lane = threadIdx.x & 31;
+    const int r = lane < 6 ? lane : 0;
+    double m[6], v[6];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+        m[j] = 0.5 * (a[r * 6 + j] + a[j * 6 + r]);
+        v[j] = r == j ? 1.0 : 0.0;
+    }
+    double sq = 0.0;
+#pragma unroll
+    for (int c = 0; c < 6; ++c)
+#pragma unroll
+        for (int rr = 0; rr < 6; ++rr) {
+            const double x = 0.5 * (a[rr * 6 + c] + a[c * 6 + rr]);
+            sq = (c == 0 && rr == 0) ? x * x : sq + x * x;
+        }
+    const double nrm = sqrt(sq);
+    const double tol = 1e-12 * ((1.0 < nrm) ? nrm : 1.0);
+    for (int sweep = 0; sweep < 64; ++sweep) {
+        double off = 0.0;  // sum of squares above the diagonal, same value in every lane
+#pragma unroll
+        for (int p = 0; p < 6; ++p)
+#pragma unroll
+            for (int q = p + 1; q < 6; ++q) {
+                const double mpq = __shfl_sync(kFull, m[q], p);
+                off += mpq * mpq;
+            }
+        if (sqrt(off) <= tol) break;
+#pragma unroll
+        for (int rd = 0; rd < 5; ++rd) {
+            // my pair (p, q), p < q; lanes >= 6 mirror lane 0
+            int j = 0;
+#pragma unroll
+            for (int i = 0; i < 6; ++i)
+                if (r == i) j = kPartner[rd][i];
+            const int p = r < j ? r : j, q = r < j ? j : r;
+            double mrow_j[6];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) mrow_j[k] = __shfl_sync(kFull, m[k], j);
+            // app, aqq, apq from my row and the partner's row
+            double mine_rr = 0.0, mine_rj = 0.0, part_jj = 0.0;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                if (k == r) mine_rr = m[k];
+                if (k == j) mine_rj = m[k];
+                if (k == j) part_jj = mrow_j[k];
+            }
+            const double app = r == p ? mine_rr : part_jj, aqq = r == p ? part_jj : mine_rr;
+            double apq = mine_rj;  // row p, column q: owned by lane p
+            {
+                double part_jr = 0.0;
+#pragma unroll
+                for (int k = 0; k < 6; ++k)
+                    if (k == r) part_jr = mrow_j[k];
+                if (r != p) apq = part_jr;
+            }
+            double c = 1.0, s = 0.0;
+            if (!(fabs(apq) <= tol / 30.0)) {
+                const double theta = (aqq - app) / (2.0 * apq);
+                const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                c = 1.0 / sqrt(t * t + 1.0);
+                s = t * c;
+            }
+            // rows: rot^T * m for my row (p: c*row_p - s*row_q; q: s*row_p + c*row_q)
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                const double mp = r == p ? m[k] : mrow_j[k], mq = r == p ? mrow_j[k] : m[k];
+                m[k] = r == p ? c * mp + (-s) * mq : s * mp + c * mq;
+            }
+            // columns: (rot^T m) * rot and v * rot; every lane needs all three pairs' (c, s)
+#pragma unroll
+            for (int pp = 0; pp < 6; ++pp) {
+                const int qq = kPartner[rd][pp];
+                if (qq < pp) continue;
+                const double cp = __shfl_sync(kFull, c, pp), sp = __shfl_sync(kFull, s, pp);
+                const double xp = m[pp], xq = m[qq];
+                m[pp] = xp * cp + xq * (-sp);
+                m[qq] = xp * sp + xq * cp;
+                const double vp = v[pp], vq = v[qq];
+                v[pp] = vp * cp + vq * (-sp);
+                v[qq] = vp * sp + vq * cp;
+            }
+        }
+    }
+    double d[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) d[k] = __shfl_sync(kFull, m[k], k);
+    int order[6] = {0, 1, 2, 3, 4, 5};
+    for (int i = 1; i < 6; ++i) {
+        const int val = order[i];
+        double dv = 0.0;
+#pragma unroll
+        for (int k = 0; k < 6; ++k)
+            if (k == val) dv = d[k];
+        int j = i;
+        while (j > 0) {
+            double dp = 0.0;
+            const int o = order[j - 1];
+#pragma unroll
+            for (int k = 0; k < 6; ++k)
+                if (k == o) dp = d[k];
+            if (!(dv < dp)) break;
+            order[j] = o;
+            --j;
+        }
+        order[j] = val;
+    }
+    if (lane < 6) {
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            const int o = order[i];
+#pragma unroll
+            for (int k = 0; k < 6; ++k)
+                if (k == o) {
+                    if (lane == 0) out->values[i] = d[k];
+                    out->vectors[i * 6 + lane] = v[k];
+                }
+        }
+    }
+}
+#endif
+
 }  // namespace sf

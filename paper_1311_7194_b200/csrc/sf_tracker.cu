@@ -336,7 +336,7 @@ int sf_tracker_fetch(sf_tracker_t tr, sf_frame_metrics* out, void* stream) {
         if (h->ctr.skip) out->blocks_processed = 0;
         out->voxels_visited = out->blocks_processed * m * m * m;
         out->kernel_launches = tr->last_launches;
-        if (tr->last_icp_loop) out->kernel_launches += 2ull * static_cast<uint64_t>(h->icp.bodies);
+        if (tr->last_icp_loop) out->kernel_launches += static_cast<uint64_t>(h->icp.bodies);
         return SF_OK;
     });
 }
