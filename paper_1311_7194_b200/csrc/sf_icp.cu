@@ -29,14 +29,18 @@
 
 namespace sf {
 
+// COND: the launch sits in a graph with the device-side iteration loop and drives its
+// condition. (Separate instantiations: kernels that call the device graph API are not
+// profiled by Nsight Compute, so the eager / fixed-sequence form must not contain the call.)
+template <bool COND>
 __global__ void k_icp_init(IcpState* st, const double* __restrict__ initial12, const int* dead, int max_iterations,
-                           int use_cond, cudaGraphConditionalHandle cond) {
+                           cudaGraphConditionalHandle cond) {
     IcpState z;
     memset(&z, 0, sizeof(z));
     z.delta = pose_from12(initial12);
     z.done = (dead && *dead) ? 1 : 0;
     *st = z;
-    if (use_cond) cudaGraphSetConditional(cond, (!z.done && max_iterations > 0) ? 1u : 0u);
+    if constexpr (COND) cudaGraphSetConditional(cond, (!z.done && max_iterations > 0) ? 1u : 0u);
 }
 
 // Returns true in every thread of the CTA that finished last (all partials visible).
@@ -140,14 +144,17 @@ __host__ __device__ constexpr int packed_index(int i, int j) {  // upper triangl
 // association, and the last CTA to finish merges the partials in a fixed order, forms c, s,
 // applies L (~1e-15 relative: the same result as shrinking first, up to rounding), runs the
 // warp-parallel Jacobi and the gated solve. No match records go through HBM.
+template <bool COND>
 __global__ void __launch_bounds__(kIcpThreads, 1)
     k_icp_step(const float* __restrict__ src, const float* __restrict__ src_n, const float* __restrict__ tgt,
                const float* __restrict__ tgt_n, Intr si, Intr ti, IcpParamsDev prm, IcpState* st,
                double* __restrict__ part_bbox, unsigned long long* __restrict__ part_count, DD* __restrict__ part,
-               unsigned int* counter, int use_cond, cudaGraphConditionalHandle cond) {
+               unsigned int* counter, cudaGraphConditionalHandle cond) {
     extern __shared__ DD s_red[];  // [kSums][kIcpThreads]
     if (st->done) {  // converged / lost: end the device-side loop
-        if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0u);
+        if constexpr (COND) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0u);
+        }
         return;
     }
     const Pose delta = st->delta;
@@ -324,7 +331,7 @@ __global__ void __launch_bounds__(kIcpThreads, 1)
     if (s_lost) {
         if (tid == 0) {
             *counter = 0;
-            if (use_cond) cudaGraphSetConditional(cond, 0u);
+            if constexpr (COND) cudaGraphSetConditional(cond, 0u);
         }
         return;
     }
@@ -401,7 +408,8 @@ __global__ void __launch_bounds__(kIcpThreads, 1)
     if (lane == 0) {
         solve_finalize(st, s_fin, s_eig, prm);
         *counter = 0;
-        if (use_cond) cudaGraphSetConditional(cond, (!st->done && st->iterations < prm.max_iterations) ? 1u : 0u);
+        if constexpr (COND)
+            cudaGraphSetConditional(cond, (!st->done && st->iterations < prm.max_iterations) ? 1u : 0u);
     }
 }
 
@@ -427,7 +435,8 @@ IcpParamsDev make_icp_params(const sf_match_params& p) {
 void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* tgt, const float* tgt_n,
                 const Intr& si, const Intr& ti, const double* d_initial, const IcpParamsDev& prm, cudaStream_t s,
                 uint64_t* launches, const int* dead, bool* device_loop) {
-    SF_CUDA(cudaFuncSetAttribute(k_icp_step, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem));
+    SF_CUDA(cudaFuncSetAttribute(k_icp_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem));
+    SF_CUDA(cudaFuncSetAttribute(k_icp_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem));
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     SF_CUDA(cudaStreamIsCapturing(s, &cs));
     // SF_ICP_DEVICE_LOOP=0 keeps the fixed launch sequence under capture too (Nsight Compute
@@ -439,12 +448,13 @@ void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* 
     const bool loop = loop_enabled && cs == cudaStreamCaptureStatusActive && prm.max_iterations > 0;
     if (device_loop) *device_loop = loop;
     if (!loop) {
-        k_icp_init<<<1, 1, 0, s>>>(wk.st, d_initial, dead, prm.max_iterations, 0, 0);
+        k_icp_init<false><<<1, 1, 0, s>>>(wk.st, d_initial, dead, prm.max_iterations, 0);
         SF_LAUNCH_CHECK();
         uint64_t cnt = 1;
         for (int it = 0; it < prm.max_iterations; ++it) {
-            k_icp_step<<<kStepCtas, kIcpThreads, kStepSmem, s>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st,
-                                                                 wk.part_bbox, wk.part_count, wk.part, wk.counters, 0, 0);
+            k_icp_step<false><<<kStepCtas, kIcpThreads, kStepSmem, s>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st,
+                                                                        wk.part_bbox, wk.part_count, wk.part,
+                                                                        wk.counters, 0);
             SF_LAUNCH_CHECK();
             cnt += 1;
         }
@@ -455,7 +465,7 @@ void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* 
     SF_CUDA(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, nullptr, nullptr));
     cudaGraphConditionalHandle cond;
     SF_CUDA(cudaGraphConditionalHandleCreate(&cond, g, 0, 0));
-    k_icp_init<<<1, 1, 0, s>>>(wk.st, d_initial, dead, prm.max_iterations, 1, cond);
+    k_icp_init<true><<<1, 1, 0, s>>>(wk.st, d_initial, dead, prm.max_iterations, cond);
     SF_LAUNCH_CHECK();
     if (launches) *launches += 1;
     const cudaGraphNode_t* deps = nullptr;
@@ -472,8 +482,9 @@ void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* 
     if (!wk.body_stream) SF_CUDA(cudaStreamCreateWithFlags(&wk.body_stream, cudaStreamNonBlocking));
     cudaStream_t bs = wk.body_stream;
     SF_CUDA(cudaStreamBeginCaptureToGraph(bs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    k_icp_step<<<kStepCtas, kIcpThreads, kStepSmem, bs>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st, wk.part_bbox,
-                                                          wk.part_count, wk.part, wk.counters, 1, cond);
+    k_icp_step<true><<<kStepCtas, kIcpThreads, kStepSmem, bs>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st,
+                                                                wk.part_bbox, wk.part_count, wk.part, wk.counters,
+                                                                cond);
     const cudaError_t le = cudaGetLastError();
     cudaGraph_t captured = nullptr;
     const cudaError_t ee = cudaStreamEndCapture(bs, &captured);

@@ -461,3 +461,28 @@ def test_reference_pose_chain_instability_and_fix(gpu):
         orth[fix] = errs
     assert orth[False][25] > 1e4 * max(orth[False][3], 1e-16)  # exponential growth
     assert max(orth[True]) < 1e-14
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["fuse_kalman", "fuse_weighted_raycast", "icp"])
+def test_golden_cases_gpu(gpu, name):
+    """The CUDA path against the frozen reference outputs (tests/golden/golden.json, generated
+    from the unmodified reference build): fusion, ray bounds, raycast and normals bit-exact;
+    ICP pose within POSE_TOL (tree-ordered sums)."""
+    import json
+    import os
+
+    from tests import golden_cases
+
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden.json")) as f:
+        want = json.load(f)["cases"][name]
+    got = json.loads(json.dumps(golden_cases.CASES[name](gpu)))
+    if name != "icp":
+        assert got == want
+        return
+    d_got = np.array([float.fromhex(v) for v in got["delta"]])
+    d_want = np.array([float.fromhex(v) for v in want["delta"]])
+    assert np.abs(d_got - d_want).max() < POSE_TOL
+    assert got["iterations"] == want["iterations"]
+    assert abs(got["matches"] - want["matches"]) <= max(8, want["matches"] // 2000)
+    assert got["gated"] == want["gated"]
