@@ -6,12 +6,15 @@
 //   k_edge             depth-edge mask                                              (fusion.cpp:40-62)
 //   k_pixel_meas       5x5 near-edge dilation + every per-pixel factor of the
 //                      measurement (sigma, p_k, w_k, grazing reject)                (fusion.cpp:63-70, 148-171)
-//   k_block_keys       surface samples -> block keys (FP64)                         (fusion.cpp:190-206)
-//   CUB radix sort + unique                 == std::set<BlockLess> order          (fusion.cpp:177-183,193)
-//   k_alloc_flags / CUB scan / k_alloc_assign / k_alloc_finalize
-//                      ordered slot assignment == sequential free-list pops;
-//                      PoolExhausted prefix semantics                              (fusion.cpp:294-299,369; grid.cpp:87-100)
-//   k_visible          SAT frustum test + 9 probes over allocated blocks            (grid.cpp:174-269; fusion.cpp:211-233)
+//   k_block_keys_set   surface samples -> block keys (FP64), deduplicated in an N^3-bit set (fusion.cpp:190-206)
+//   k_alloc_classify   new keys (EMPTY in the table)
+//   k_alloc_rank       ordered slot assignment: rank among the new keys == position in
+//                      std::set<BlockLess> order == sequential free-list pops;
+//                      PoolExhausted key / prefix semantics                        (fusion.cpp:294-299,369; grid.cpp:87-100)
+//   k_worklist         processed allocate set + SAT frustum test and 9 probes over the
+//                      other allocated blocks                                      (grid.cpp:174-269; fusion.cpp:211-233)
+//   (select_update_blocks exports the ordered lists: k_block_keys, CUB radix sort +
+//    unique == std::set order (fusion.cpp:177-183,193), k_visible)
 //   k_integrate        per voxel: project, band test, filter, quantize              (fusion.cpp:81-173, 237-272, 300-364)
 //   k_fuse_finalize    FusionStats                                                  (fusion.cpp:372-375)
 #include <cub/cub.cuh>
@@ -26,6 +29,7 @@ namespace sf {
 
 constexpr int kThreads = 256;
 constexpr int kPersistentCtas = 148 * 8;
+constexpr int kSmallCtas = 148;  // passes over the <= 57.6 k allocate-list keys
 
 // ---------------------------------------------------------------------------------
 // frame setup (one thread)
@@ -253,56 +257,132 @@ __global__ void k_list_len(FrameCounters* ctr, const uint32_t* __restrict__ uniq
     ctr->limit = len;
 }
 
-__global__ void k_alloc_flags(const FrameCounters* ctr, const uint32_t* __restrict__ uniq,
-                              const int32_t* __restrict__ table, uint32_t* __restrict__ flags, uint32_t cap) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= cap) return;
-    uint32_t f = 0;
-    if (i < ctr->n_list && !ctr->skip) f = table[uniq[i]] == kEmpty ? 1u : 0u;
-    flags[i] = f;
+// ---------------------------------------------------------------------------------
+// Fuse-path allocation without a global sort.
+//
+// Only two things depend on the ORDER of the reference's std::set allocate list: which slot
+// a new block receives (the r-th new key in (z,y,x) order takes the r-th pop of the free
+// list) and, on PoolExhausted, which prefix of the list is processed (keys below the first
+// unallocatable one). Integration itself is per block and order-free. So the keys are
+// deduplicated through an N^3-bit set (atomicOr), the new ones are ranked among themselves
+// by counting (rank = #{new keys < k}: exact, deterministic, O(n_new^2 / threads) and
+// n_new is small after the first frame), and the work list is built in any order.
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t warp_append(bool pred, uint32_t* counter) {
+    const unsigned am = __activemask();
+    const unsigned bal = __ballot_sync(am, pred);
+    const int lane = threadIdx.x & 31;
+    uint32_t base = 0;
+    if (bal) {
+        const int leader = __ffs(bal) - 1;
+        if (lane == leader) base = atomicAdd(counter, static_cast<uint32_t>(__popc(bal)));
+        base = __shfl_sync(am, base, leader);
+    }
+    return base + __popc(bal & ((1u << lane) - 1u));
 }
 
-// Ordered allocation: the r-th new key (in (z,y,x) order) receives the r-th pop of the
-// free-list stack, exactly as process_block's lazy allocate_block calls would.
-__global__ void k_alloc_assign(VolParams P, FrameCounters* ctr, const uint32_t* __restrict__ uniq,
-                               const uint32_t* __restrict__ ranks, int32_t* __restrict__ table,
-                               const int32_t* __restrict__ free_list, int32_t* __restrict__ slot_key,
-                               uint32_t* __restrict__ occ, const VolCounters* __restrict__ vc,
-                               int2* __restrict__ work, unsigned long long* high_water) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= ctr->n_list || ctr->skip) return;
-    const uint32_t key = uniq[i];
-    int32_t slot = table[key];
-    uint32_t fresh = 0;
-    if (slot == kEmpty) {
-        const unsigned long long r = ranks[i];
-        const unsigned long long top = vc->free_top;
-        if (r < top) {
-            slot = free_list[top - 1 - r];
-            table[key] = slot;
-            slot_key[slot] = static_cast<int32_t>(key);
-            occ_set(P, occ, key);
-            atomicMax(high_water, (unsigned long long)slot + 1ull);
-            fresh = 1;
-        } else {
-            if (r == top) ctr->limit = i;  // first unallocatable block: PoolExhausted here
-            slot = -1;
+// block_of_point keys of the surface samples (fusion.cpp:187-209), deduplicated in the key set.
+__global__ void k_block_keys_set(VolParams P, const FrameConsts* __restrict__ fc, const float* __restrict__ depth,
+                                 int w, int h, int stride, int su, int sv, uint32_t* __restrict__ keybits,
+                                 uint32_t* __restrict__ uniq, FrameCounters* ctr) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= su * sv || ctr->skip) return;
+    const int u = (i % su) * stride;
+    const int v = (i / su) * stride;
+    const bool valid = px_valid(depth, w, h, u, v);
+    d3 dir = mk(0, 0, 0);
+    double t_hit = 0.0;
+    if (valid) {
+        const Intr& intr = fc->intr;
+        const d3 dir_cam = normalized(unproject(intr, u, v, 1.0));
+        dir = mv(fc->pose.R, dir_cam);
+        t_hit = (double)depth[(size_t)v * w + u] / dir_cam.z;
+    }
+    const double offs[3] = {-fc->delta, 0.0, fc->delta};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        bool fresh = false;
+        uint32_t key = 0;
+        if (valid) {
+            const d3 x = add(fc->pose.t, scale(t_hit + offs[k], dir));
+            const int bx = ref_floor_int((x.x - P.ox) / P.block_side);
+            const int by = ref_floor_int((x.y - P.oy) / P.block_side);
+            const int bz = ref_floor_int((x.z - P.oz) / P.block_side);
+            if (bx >= 0 && by >= 0 && bz >= 0 && bx < P.N && by < P.N && bz < P.N) {
+                key = static_cast<uint32_t>(table_index(P, bx, by, bz));
+                const uint32_t bit = 1u << (key & 31);
+                fresh = !(atomicOr(&keybits[key >> 5], bit) & bit);
+            }
+        }
+        const uint32_t j = warp_append(fresh, &ctr->n_unique);
+        if (fresh) uniq[j] = key;
+    }
+}
+
+// New keys (EMPTY table entry) of the allocate set.
+__global__ void k_alloc_classify(FrameCounters* ctr, const uint32_t* __restrict__ uniq,
+                                 const int32_t* __restrict__ table, uint32_t* __restrict__ isnew,
+                                 uint32_t* __restrict__ new_keys) {
+    if (ctr->skip) return;
+    const uint32_t n = ctr->n_unique;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t key = uniq[i];
+        const bool fresh = table[key] == kEmpty;
+        isnew[i] = fresh ? 1u : 0u;
+        const uint32_t j = warp_append(fresh, &ctr->n_new);
+        if (fresh) new_keys[j] = key;
+    }
+}
+
+// Ordered slots for the new keys: rank = #{new keys < key}; the rank-th pop of the free
+// list, as the reference's lazy allocate_block calls in list order would (grid.cpp:87-100).
+// The last CTA settles the counters: PoolExhausted when n_new exceeds the free list.
+constexpr int kRankTile = 2048;
+__global__ void __launch_bounds__(256)
+    k_alloc_rank(VolParams P, FrameCounters* ctr, const uint32_t* __restrict__ new_keys, int32_t* __restrict__ table,
+                 const int32_t* __restrict__ free_list, int32_t* __restrict__ slot_key, uint32_t* __restrict__ occ,
+                 VolCounters* vc) {
+    __shared__ uint32_t s_keys[kRankTile];
+    __shared__ bool s_last;
+    if (ctr->skip) return;
+    const uint32_t n = ctr->n_new;
+    const unsigned long long top = vc->free_top;
+    for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+        const uint32_t i = base + threadIdx.x;
+        const uint32_t key = i < n ? new_keys[i] : 0xffffffffu;
+        uint32_t rank = 0;
+        for (uint32_t t0 = 0; t0 < n; t0 += kRankTile) {
+            const uint32_t m = min(n - t0, (uint32_t)kRankTile);
+            __syncthreads();
+            for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) s_keys[j] = new_keys[t0 + j];
+            __syncthreads();
+            for (uint32_t j = 0; j < m; ++j) rank += s_keys[j] < key ? 1u : 0u;
+        }
+        if (i < n) {
+            if (rank < top) {
+                const int32_t slot = free_list[top - 1 - rank];
+                table[key] = slot;
+                slot_key[slot] = static_cast<int32_t>(key);
+                occ_set(P, occ, key);
+                atomicMax(&vc->high_water, (unsigned long long)slot + 1ull);
+            } else if (rank == top) {
+                ctr->exhaust_key = key;  // PoolExhausted at this key (fusion.cpp:369)
+            }
         }
     }
-    work[i] = make_int2(static_cast<int32_t>(static_cast<uint32_t>(slot) | (fresh << 31)), static_cast<int32_t>(key));
-}
-
-__global__ void k_alloc_finalize(FrameCounters* ctr, const uint32_t* __restrict__ flags,
-                                 const uint32_t* __restrict__ ranks, VolCounters* vc) {
-    if (ctr->skip) return;
-    const uint32_t n = ctr->n_list;
-    const unsigned long long n_new = n ? (unsigned long long)ranks[n - 1] + flags[n - 1] : 0ull;
-    const unsigned long long top = vc->free_top;
-    const unsigned long long got = n_new < top ? n_new : top;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&ctr->tickets, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    __threadfence();
+    const unsigned long long got = n < top ? n : top;
     vc->free_top = top - got;
     vc->allocated_count += got;
-    ctr->n_new = static_cast<uint32_t>(n_new);
-    ctr->exhausted = n_new > top ? 1u : 0u;
+    ctr->exhausted = n > top ? 1u : 0u;
+    if (n <= top) ctr->exhaust_key = 0xffffffffu;
+    ctr->n_list = ctr->n_unique;
+    ctr->upd_base = ctr->n_unique;
 }
 
 // ---------------------------------------------------------------------------------
@@ -378,6 +458,80 @@ __global__ void k_visible(VolParams P, const FrameConsts* __restrict__ fc, Frame
         if (export_only) export_keys[j] = static_cast<uint32_t>(key);
         else work[base + j] = make_int2(static_cast<int32_t>(s), key);
     }
+}
+
+// Fuse-path work list: the processed part of the allocate set (everything, or the keys
+// below the PoolExhausted key), then — unless exhausted — the visible allocated blocks
+// outside the allocate set (membership from the key set), at [upd_base, ...).
+__global__ void k_worklist(VolParams P, const FrameConsts* __restrict__ fc, FrameCounters* ctr,
+                           const VolCounters* __restrict__ vc, const int32_t* __restrict__ slot_key,
+                           const int32_t* __restrict__ table, const uint32_t* __restrict__ uniq,
+                           const uint32_t* __restrict__ isnew, const uint32_t* __restrict__ keybits,
+                           const float* __restrict__ depth, int w, int h, int2* __restrict__ work) {
+    if (ctr->skip) return;
+    const uint32_t n = ctr->n_unique, ex_key = ctr->exhaust_key;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t key = uniq[i];
+        const bool take = key < ex_key;
+        const uint32_t j = warp_append(take, &ctr->limit);
+        if (take) {
+            const uint32_t slot = static_cast<uint32_t>(table[key]);
+            work[j] = make_int2(static_cast<int32_t>(slot | (isnew[i] << 31)), static_cast<int32_t>(key));
+        }
+    }
+    if (ctr->exhausted) return;  // PoolExhausted: the update list is never reached
+    const unsigned long long hw = vc->high_water;
+    const uint32_t base = ctr->upd_base;
+    const Intr& intr = fc->intr;
+    for (unsigned long long s = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; s < hw; s += stride) {
+        const int32_t key = slot_key[s];
+        bool vis = false;
+        if (key >= 0 && !((keybits[key >> 5] >> (key & 31)) & 1u)) {
+            int bx, by, bz;
+            if (P.nshift >= 0) {
+                bx = key & (P.N - 1);
+                by = (key >> P.nshift) & (P.N - 1);
+                bz = key >> (2 * P.nshift);
+            } else {
+                bx = key % P.N;
+                by = (key / P.N) % P.N;
+                bz = key / (P.N * P.N);
+            }
+            const d3 lo = block_min_corner(P, bx, by, bz);
+            const double side = P.block_side;
+            const d3 hi = add(lo, mk(side, side, side));
+            if (frustum_intersects_block(P, fc, lo, hi)) {
+                for (int k = 0; k < 9 && !vis; ++k) {
+                    const d3 probe = k == 8 ? add(lo, mk(0.5 * side, 0.5 * side, 0.5 * side))
+                                            : add(lo, mk(k & 1 ? side : 0.0, k & 2 ? side : 0.0, k & 4 ? side : 0.0));
+                    const d3 xc = apply(fc->inv, probe);
+                    double pu, pv;
+                    if (!project(intr, xc, pu, pv)) continue;
+                    const int u = ref_lround_int(pu);
+                    const int v = ref_lround_int(pv);
+                    if (!(u >= 0 && v >= 0 && u < w && v < h)) continue;
+                    const float d = depth[(size_t)v * w + u];
+                    if (!(d > 0.0f) || xc.z <= d + fc->delta) vis = true;
+                }
+            }
+        }
+        const uint32_t j = warp_append(vis, &ctr->n_update);
+        if (vis) work[base + j] = make_int2(static_cast<int32_t>(s), key);
+    }
+}
+
+// Work item i: the allocate part [0, limit), then the update part [upd_base, upd_base + n_update).
+__device__ __forceinline__ int2 work_at(const int2* __restrict__ work, uint32_t limit, uint32_t upd_base, uint32_t i) {
+    return i < limit ? work[i] : work[upd_base + (i - limit)];
+}
+// The key set must be empty for the next frame: clear the words of this frame's keys (the
+// work-list pass, its only reader, has finished).
+__device__ __forceinline__ void clear_keybits(const FrameCounters* ctr, const uint32_t* __restrict__ uniq,
+                                              uint32_t* __restrict__ keybits) {
+    const uint32_t n = ctr->n_unique;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        keybits[uniq[i] >> 5] = 0u;
 }
 
 // ---------------------------------------------------------------------------------
@@ -538,7 +692,8 @@ __global__ void __launch_bounds__(256)
                      const FrameCounters* __restrict__ ctr, const AuxTables* __restrict__ aux,
                      const double* __restrict__ pix_dm, const double* __restrict__ pix_var,
                      const double* __restrict__ pix_w, uint16_t* __restrict__ payload,
-                     unsigned long long* __restrict__ voxels_updated) {
+                     unsigned long long* __restrict__ voxels_updated, const uint32_t* __restrict__ uniq,
+                     uint32_t* __restrict__ keybits) {
     constexpr int M = 1 << MS, M3 = M * M * M;
     constexpr int VPT = (M3 + 255) / 256;  // voxels per thread
     __shared__ double s_tdec[256], s_adec[256], s_thr[256];
@@ -554,11 +709,13 @@ __global__ void __launch_bounds__(256)
     const double delta = P.delta;
     const double inv_delta = 1.0 / delta, inv_wmax = 1.0 / P.aux_w_max;
     const int w = intr.w, h = intr.h;
-    const unsigned n_work = ctr->limit + ctr->n_update;
+    clear_keybits(ctr, uniq, keybits);
+    const uint32_t limit = ctr->limit, upd_base = ctr->upd_base;
+    const unsigned n_work = limit + ctr->n_update;
     const int N = P.N;
     unsigned long long updated = 0;
     for (unsigned item = blockIdx.x; item < n_work; item += gridDim.x) {
-        const int2 wk = work[item];
+        const int2 wk = work_at(work, limit, upd_base, item);
         const uint32_t slot = static_cast<uint32_t>(wk.x) & 0x7fffffffu;
         const bool fresh = (static_cast<uint32_t>(wk.x) >> 31) != 0;
         const int key = wk.y;
@@ -657,7 +814,8 @@ __global__ void __launch_bounds__(kThreads)
                 const FrameCounters* __restrict__ ctr, const AuxTables* __restrict__ aux,
                 const float* __restrict__ depth, const double* __restrict__ pix_var, const double* __restrict__ pix_w,
                 const uint8_t* __restrict__ pix_ok, uint16_t* __restrict__ payload, float2* __restrict__ fpayload,
-                unsigned long long* __restrict__ voxels_updated) {
+                unsigned long long* __restrict__ voxels_updated, const uint32_t* __restrict__ uniq,
+                uint32_t* __restrict__ keybits) {
     __shared__ double s_tdec[256], s_adec[256], s_thr[256];
     if (ctr->skip) return;
     for (int i = threadIdx.x; i < 256; i += blockDim.x) {
@@ -670,7 +828,9 @@ __global__ void __launch_bounds__(kThreads)
     const Intr intr = fc->intr;
     const double delta = P.delta;
     const int w = intr.w, h = intr.h;
-    const unsigned long long n_work = (unsigned long long)ctr->limit + ctr->n_update;
+    clear_keybits(ctr, uniq, keybits);
+    const uint32_t limit = ctr->limit, upd_base = ctr->upd_base;
+    const unsigned long long n_work = (unsigned long long)limit + ctr->n_update;
     const unsigned long long total = n_work * (unsigned long long)P.M3;
     const int M = P.M, MM = P.M * P.M, N = P.N;
     unsigned long long updated = 0;
@@ -678,7 +838,7 @@ __global__ void __launch_bounds__(kThreads)
          g += (unsigned long long)gridDim.x * blockDim.x) {
         const unsigned long long item = g / (unsigned)P.M3;
         const int l = static_cast<int>(g - item * (unsigned)P.M3);
-        const int2 wk = work[item];
+        const int2 wk = work_at(work, limit, upd_base, static_cast<uint32_t>(item));
         const uint32_t slot = static_cast<uint32_t>(wk.x) & 0x7fffffffu;
         const bool fresh = (static_cast<uint32_t>(wk.x) >> 31) != 0;
         const int key = wk.y;
@@ -868,49 +1028,54 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
         SF_LAUNCH_CHECK();
         n += 1;
     }
-    // Keys -> sorted unique allocate list.
     const int su = (w + fb.stride - 1) / fb.stride, sv = (h + fb.stride - 1) / fb.stride;
-    const uint32_t sentinel = sentinel_of(P);
-    k_block_keys<<<(su * sv + kThreads - 1) / kThreads, kThreads, 0, s>>>(P, fb.fc, depth, w, h, fb.stride, su, sv,
-                                                                          fb.keys, sentinel, &fb.ctr->skip);
-    SF_LAUNCH_CHECK();
-    size_t tb = fb.cub_temp_bytes;
-    SF_CUDA(cub::DeviceRadixSort::SortKeys(fb.cub_temp, tb, fb.keys, fb.keys_sorted, (int)fb.key_cap, 0, end_bit_of(P), s));
-    tb = fb.cub_temp_bytes;
-    SF_CUDA(cub::DeviceSelect::Unique(fb.cub_temp, tb, fb.keys_sorted, fb.keys_unique, &fb.ctr->n_unique,
-                                      (int)fb.key_cap, s));
-    k_list_len<<<1, 1, 0, s>>>(fb.ctr, fb.keys_unique, sentinel);
-    SF_LAUNCH_CHECK();
-    n += 2 + 4;  // keys + list_len + (sort, unique: >= 4 CUB kernels)
-    const int kb = (fb.key_cap + kThreads - 1) / kThreads;
-    if (!export_only) {
-        k_alloc_flags<<<kb, kThreads, 0, s>>>(fb.ctr, fb.keys_unique, v.d_table, fb.flags, fb.key_cap);
+    if (export_only) {
+        // select_update_blocks: the ordered lists themselves are the output -> sorted
+        // unique allocate list (CUB), update list by the same visibility test.
+        const uint32_t sentinel = sentinel_of(P);
+        k_block_keys<<<(su * sv + kThreads - 1) / kThreads, kThreads, 0, s>>>(P, fb.fc, depth, w, h, fb.stride, su,
+                                                                              sv, fb.keys, sentinel, &fb.ctr->skip);
         SF_LAUNCH_CHECK();
+        size_t tb = fb.cub_temp_bytes;
+        SF_CUDA(cub::DeviceRadixSort::SortKeys(fb.cub_temp, tb, fb.keys, fb.keys_sorted, (int)fb.key_cap, 0,
+                                               end_bit_of(P), s));
         tb = fb.cub_temp_bytes;
-        SF_CUDA(cub::DeviceScan::ExclusiveSum(fb.cub_temp, tb, fb.flags, fb.ranks, (int)fb.key_cap, s));
-        k_alloc_assign<<<kb, kThreads, 0, s>>>(P, fb.ctr, fb.keys_unique, fb.ranks, v.d_table, v.d_free_list,
-                                               v.d_slot_key, v.d_occ, v.d_vc, fb.work, &v.d_vc->high_water);
+        SF_CUDA(cub::DeviceSelect::Unique(fb.cub_temp, tb, fb.keys_sorted, fb.keys_unique, &fb.ctr->n_unique,
+                                          (int)fb.key_cap, s));
+        k_list_len<<<1, 1, 0, s>>>(fb.ctr, fb.keys_unique, sentinel);
         SF_LAUNCH_CHECK();
-        k_alloc_finalize<<<1, 1, 0, s>>>(fb.ctr, fb.flags, fb.ranks, v.d_vc);
+        k_visible<<<kPersistentCtas, kThreads, 0, s>>>(P, fb.fc, fb.ctr, v.d_vc, v.d_slot_key, fb.keys_unique, depth,
+                                                       w, h, fb.work, fb.keys /* reused as export buffer */, 1);
         SF_LAUNCH_CHECK();
-        n += 5;
+        n += 3 + 4;  // keys + list_len + visible + (sort, unique: >= 4 CUB kernels)
+    } else {
+        // fuse_frame: unordered key set + ranked new keys + work list (no global sort)
+        k_block_keys_set<<<(su * sv + kThreads - 1) / kThreads, kThreads, 0, s>>>(
+            P, fb.fc, depth, w, h, fb.stride, su, sv, v.d_keybits, fb.keys_unique, fb.ctr);
+        SF_LAUNCH_CHECK();
+        k_alloc_classify<<<kSmallCtas, kThreads, 0, s>>>(fb.ctr, fb.keys_unique, v.d_table, fb.flags, fb.ranks);
+        SF_LAUNCH_CHECK();
+        k_alloc_rank<<<kSmallCtas, kThreads, 0, s>>>(P, fb.ctr, fb.ranks, v.d_table, v.d_free_list, v.d_slot_key,
+                                                     v.d_occ, v.d_vc);
+        SF_LAUNCH_CHECK();
+        k_worklist<<<kPersistentCtas, kThreads, 0, s>>>(P, fb.fc, fb.ctr, v.d_vc, v.d_slot_key, v.d_table,
+                                                        fb.keys_unique, fb.flags, v.d_keybits, depth, w, h, fb.work);
+        SF_LAUNCH_CHECK();
+        n += 4;
     }
-    k_visible<<<kPersistentCtas, kThreads, 0, s>>>(P, fb.fc, fb.ctr, v.d_vc, v.d_slot_key, fb.keys_unique, depth, w, h,
-                                                   fb.work, fb.keys /* reused as export buffer */, export_only ? 1 : 0);
-    SF_LAUNCH_CHECK();
-    n += 1;
     if (!export_only) {
         unsigned long long* vu = &fb.ctr->voxels_updated;
 #define SF_INTEGRATE(MODE, FP)                                                                                    \
     k_integrate<MODE, FP><<<kPersistentCtas, kThreads, 0, s>>>(P, fb.fc, fp, fb.work, fb.ctr, v.d_aux, depth,       \
                                                                fb.pix_var, fb.pix_w, fb.pix_ok, v.d_payload,        \
-                                                               v.d_fpayload, vu)
+                                                               v.d_fpayload, vu, fb.keys_unique, v.d_keybits)
         const bool fpl = v.d_fpayload != nullptr;
         if (events && events->before_integrate) record_event(events->before_integrate, s);
         const bool fast = !fpl && (P.mshift == 3 || P.mshift == 2);
 #define SF_INTEGRATE_FAST(MODE, MS)                                                                            \
     k_integrate_fast<MODE, MS><<<kPersistentCtas, 256, 0, s>>>(P, fb.fc, fp, fb.work, fb.ctr, v.d_aux, fb.pix_dm,   \
-                                                               fb.pix_var, fb.pix_w, v.d_payload, vu)
+                                                               fb.pix_var, fb.pix_w, v.d_payload, vu,               \
+                                                               fb.keys_unique, v.d_keybits)
         if (fast) {
             if (P.mshift == 3) {
                 if (fp.mode == 0) SF_INTEGRATE_FAST(0, 3);

@@ -70,7 +70,9 @@ struct FrameCounters {
     uint32_t n_update;   // update-list length
     uint32_t exhausted;  // PoolExhausted raised this frame
     uint32_t skip;       // whole fuse skipped (tracker dead / tracking lost)
-    uint32_t pad;
+    uint32_t exhaust_key;  // smallest allocate-list key that found no free slot (PoolExhausted), else ~0
+    uint32_t upd_base;     // work-list index where the update list starts
+    uint32_t tickets;      // last-CTA ticket of the allocation pass
     unsigned long long voxels_updated;
     unsigned long long alloc_before;
     unsigned long long alloc_now;
@@ -130,6 +132,7 @@ struct sf_volume {
     int32_t* d_free_list = nullptr;  // capacity (stack, bottom..top)
     int32_t* d_slot_key = nullptr;   // capacity: table index of the block in each slot, -1 free
     uint32_t* d_occ = nullptr;       // occupancy bitmap, N^3 bits
+    uint32_t* d_keybits = nullptr;   // the frame's allocate-list keys, N^3 bits (zero between frames)
     sf::VolCounters* d_vc = nullptr;
     sf::AuxTables* d_aux = nullptr;
     sf::AuxTables h_aux{};

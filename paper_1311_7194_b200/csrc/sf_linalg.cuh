@@ -501,7 +501,7 @@ __device__ __forceinline__ void eigendecompose_sym6_warp_rr(const double* a, Eig
 #pragma unroll
             for (int i = 0; i < 6; ++i)
                 if (r == i) j = kPartner[rd][i];
-            const int p = r < j ? r : j, q = r < j ? j : r;
+            const int p = r < j ? r : j;
             double mrow_j[6];
 #pragma unroll
             for (int k = 0; k < 6; ++k) mrow_j[k] = __shfl_sync(kFull, m[k], j);

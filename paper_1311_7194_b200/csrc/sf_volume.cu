@@ -321,6 +321,8 @@ static void volume_init_device(Volume& v) {
     SF_CUDA(cudaMalloc(&v.d_slot_key, std::max<uint32_t>(P.capacity, 1) * sizeof(int32_t)));
     const uint64_t occ_words = P.occ_fine_words + P.occ_coarse_words + 6;  // + bounding box
     SF_CUDA(cudaMalloc(&v.d_occ, occ_words * sizeof(uint32_t)));
+    SF_CUDA(cudaMalloc(&v.d_keybits, P.occ_fine_words * sizeof(uint32_t)));
+    SF_CUDA(cudaMemset(v.d_keybits, 0, P.occ_fine_words * sizeof(uint32_t)));
     SF_CUDA(cudaMalloc(&v.d_vc, sizeof(VolCounters)));
     SF_CUDA(cudaMalloc(&v.d_aux, sizeof(AuxTables)));
     SF_CUDA(cudaMemset(v.d_table, 0xFF, P.table_size * sizeof(int32_t)));
@@ -348,7 +350,8 @@ static void volume_init_device(Volume& v) {
 static void volume_free_device(Volume& v) {
     cudaSetDevice(v.device);
     v.fb.release();
-    void* ptrs[] = {v.d_table, v.d_payload, v.d_fpayload, v.d_free_list, v.d_slot_key, v.d_occ, v.d_vc, v.d_aux};
+    void* ptrs[] = {v.d_table, v.d_payload, v.d_fpayload, v.d_free_list, v.d_slot_key, v.d_occ, v.d_keybits,
+                    v.d_vc,    v.d_aux};
     for (void* p : ptrs)
         if (p) cudaFree(p);
 }

@@ -434,7 +434,8 @@ def test_tracker_matches_reference_pipeline(gpu, oracle, hook):
         assert m.fusion.blocks_total == st.blocks_total
     assert np.array_equal(g.read_table(), r.read_table())
     assert (g.read_payload() == r.read_payload()).mean() > 0.9999
-    assert tr.last_launch_count() > 20
+    assert tr.last_launch_count() > 10
+    assert tr.fetch().kernel_launches > tr.last_launch_count()  # + the device-side ICP iterations
 
 
 def test_reference_pose_chain_instability_and_fix(gpu):
