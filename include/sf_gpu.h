@@ -268,6 +268,7 @@ typedef struct {
     uint64_t blocks_processed; /* allocate-list prefix + update list integrated this frame */
     uint64_t voxels_visited;   /* blocks_processed * M^3 */
     uint64_t kernel_launches;  /* device kernels this frame ran (graph: top level + 2 per ICP iteration) */
+    uint64_t exact_voxels;     /* voxels the integrate kernel settled on its FP64 fallback (uncertain FP32 decision) */
 } sf_frame_metrics;
 
 int sf_tracker_create(sf_volume_t vol, const sf_tracker_config* config, const double initial_pose[12],

@@ -156,6 +156,7 @@ class FrameMetricsC(C.Structure):
         ("blocks_processed", C.c_uint64),
         ("voxels_visited", C.c_uint64),
         ("kernel_launches", C.c_uint64),
+        ("exact_voxels", C.c_uint64),
     ]
 
 

@@ -675,6 +675,7 @@ class FrameMetrics:
     blocks_processed: int = 0
     voxels_visited: int = 0
     kernel_launches: int = 0  # this library's kernels the frame ran (incl. device-side ICP loop)
+    exact_voxels: int = 0  # integrate voxels settled on the FP64 fallback (uncertain FP32 decision)
 
 
 class Tracker:
@@ -725,7 +726,7 @@ class Tracker:
                             m.matches, m.residual_rms, list(m.lambda_over_n), [bool(x) for x in m.gated_mask],
                             FusionStats(f.voxels_updated, f.blocks_allocated_now, f.blocks_total, f.memory_bytes),
                             RaycastStats(r.sample_steps, r.hit_pixels, r.rays_with_bounds),
-                            m.blocks_processed, m.voxels_visited, m.kernel_launches)
+                            m.blocks_processed, m.voxels_visited, m.kernel_launches, m.exact_voxels)
 
     def stage_times(self):
         """Device-timed stages of the last step (ms): raycast, icp, fuse prologue, integrate, total."""

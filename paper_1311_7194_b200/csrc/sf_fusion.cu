@@ -170,7 +170,7 @@ __global__ void k_pixel_meas(const float* __restrict__ depth, const float* __res
                              Intr intr, FuseParams fp, const float* __restrict__ normals,
                              const uint8_t* __restrict__ edge, double* __restrict__ pix_var,
                              double* __restrict__ pix_w, uint8_t* __restrict__ pix_ok, double* __restrict__ pix_dm,
-                             const int* dead) {
+                             float2* __restrict__ pix_f, const int* dead) {
     if (dead && *dead) return;
     const int u = blockIdx.x * blockDim.x + threadIdx.x;
     const int v = blockIdx.y * blockDim.y + threadIdx.y;
@@ -211,6 +211,7 @@ __global__ void k_pixel_meas(const float* __restrict__ depth, const float* __res
     pix_w[idx] = wk;
     pix_ok[idx] = ok;
     pix_dm[idx] = ok ? (double)depth[idx] : 0.0;
+    pix_f[idx] = make_float2(ok ? depth[idx] : 0.0f, static_cast<float>(fp.mode == 2 ? var : wk));
 }
 
 // ---------------------------------------------------------------------------------
@@ -567,15 +568,9 @@ __device__ __forceinline__ uint8_t aux_encode_dev(const VolParams& P, const doub
 }
 
 // ---------------------------------------------------------------------------------
-// Fast integrate (M = 4 or 8): same results bit for bit, fewer FP64 divisions.
-//
-// Only rounding DECISIONS of the reference reach the stored state: the pixel picked by
-// lround(u), lround(v) (fusion.cpp:92-93), the chi cut |T| > delta, the tsdf code
-// lround(clamp(T)/delta*127) and the aux code. The fast path evaluates the quotients with a
-// Newton-refined reciprocal (error < 4 ulp) and accepts a decision only when it is certain
-// under a margin many orders of magnitude above that error; otherwise (probability ~1e-9
-// per voxel) the voxel is recomputed with the reference's exact IEEE divisions. FP64,
-// explicit fma only inside the reciprocal refinement.
+// FP64 filter rules and payload encoding (fusion.cpp:237-272, 353-361), shared by the
+// generic kernel and the exact fallback of the row kernel. The `approx` variants replace the
+// one division by a Newton-refined reciprocal and certify the resulting decisions.
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ bool approx_rcp(double z, double& r) {
     if (!(fabs(z) > 1e-30 && fabs(z) < 1e30)) return false;
@@ -686,126 +681,401 @@ __device__ __forceinline__ bool encode_cell(const VolParams& P, const double* s_
     return true;
 }
 
+// ---------------------------------------------------------------------------------
+// Row-compacted integrate (M = 4 or 8): the roofline kernel. Bit-exact by certification.
+//
+// Only rounding DECISIONS of the reference reach the stored state: z > 0, the pixel
+// lround(u), lround(v) (fusion.cpp:92-93), the band cut |T| > delta (fusion.cpp:145), the
+// chi cut |T'| > delta and the tsdf / aux codes (fusion.cpp:353-361). Everything in between
+// is evaluated in FP32 with a rigorous error bound, and a decision is accepted only when the
+// value is farther than that bound from the decision boundary; otherwise the voxel is
+// recomputed by the reference's FP64 path (`exact_voxel`, probability ~1e-3 per voxel).
+//
+// Phase 1 (one thread per x-row of M voxels): one vector load of the row's payload (16 B at
+// M = 8), the row origin in camera space in FP64 (x_c = R^T(voxel_center - t), the
+// reference's order), then per voxel x_c = origin + lx * voxel * R^T e_x in FP32, projection
+// with a hardware reciprocal, certified pixel rounding, one float2 gather {depth, p_k} and the
+// band test on T = (d - z_hi) - (z_lo + lx dz) (double-float row origin: error ~1e-9 m).
+// Voxels in the band are compacted into a shared-memory queue (uncertain ones at its top).
+// Phase 2: the CTA drains the queue densely (no divergence between in-band and free-space
+// voxels): Kalman / weighted / simple update in FP32, certified quantisation, 2 B store.
+// Error bounds and margins: DESIGN.md §3.2.
+// ---------------------------------------------------------------------------------
+constexpr float kMagic23 = 12582912.0f;  // 1.5 * 2^23
+// std::lround(a) when certain under margin e; requires |a| < 2^22 (callers clamp).
+__device__ __forceinline__ bool certain_lround_f(float a, float e, int& out) {
+    const float t = __fadd_rn(a, kMagic23);
+    const float n = __fsub_rn(t, kMagic23);
+    const float d = __fsub_rn(a, n);  // exact: |a - n| <= 1/2, both multiples of ulp(a)
+    out = __float_as_int(t) - __float_as_int(kMagic23);
+    return fabsf(d) < 0.5f - e;
+}
+__device__ __forceinline__ float rcp_approx_f(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));  // MUFU.RCP, <= 1 ulp
+    return r;
+}
+// log2(v) to ~0.01 for positive normal v (exponent + quadratic in the mantissa).
+__device__ __forceinline__ float approx_log2_f(float v) {
+    const int b = __float_as_int(v);
+    const float m = __int_as_float((b & 0x007fffff) | 0x3f800000) - 1.0f;
+    return static_cast<float>((b >> 23) - 127) + m * (1.3465f - 0.3465f * m);
+}
+
+// Per-frame constants of the row kernel, computed once per CTA into shared memory.
+struct RowShared {
+    double R[9], t[3];  // world -> camera (invert(pose)): x_c = R x + t, the reference's order
+    double ox, oy, oz, voxel;
+    float Dxf, Dyf, Dzf;      // x_c step per voxel along x: voxel * R e_x
+    float fxf, fyf, cxf, cyf;
+    float Fmax, Wpix, Mvox;   // max(fx, fy), max(w, h) + 2, M * voxel
+    float thr_in, thr_out;    // band test: |T| certainly inside / outside delta
+    float k127, ecode;        // 127 / delta; tsdf-code margin (code units)
+    float q, w_max, k255w, lg_pmin, lg_scale;
+    float thr_lo, thr_hi;     // clamp range of the variance code guess
+};
+
+// Phase-2 update of one in-band voxel in FP32; false when a decision is not certain.
+template <int MODE>
+__device__ __forceinline__ bool approx_update(uint32_t cell, float tk, float pf, const RowShared& rc,
+                                              const float* s_tdec, const float* s_adec, const float* s_thr,
+                                              uint32_t& out) {
+    const int code = static_cast<int>(static_cast<int8_t>(cell & 0xFF));
+    const bool has_prior = code != kChiCode;
+    const float pt = s_tdec[code + 128], pa = s_adec[cell >> 8];
+    float nt, na, pred = 0.0f;
+    // filters (fusion.cpp:237-272)
+    if (MODE == 0) {
+        nt = has_prior ? (1.0f - pf) * pt + pf * tk : tk;
+        na = pf;
+    } else if (MODE == 1) {
+        nt = has_prior ? (pa * pt + pf * tk) * rcp_approx_f(pa + pf) : tk;
+        na = has_prior ? fminf(pa + pf, rc.w_max) : pf;
+    } else {
+        pred = has_prior ? pa + rc.q : 0.0f;
+        const float gain = pred * rcp_approx_f(pred + pf);
+        nt = has_prior ? pt + gain * (tk - pt) : tk;
+        na = has_prior ? pf * gain : pf;  // pf * gain == (1 - gain) * predicted, without the cancellation
+    }
+    // chi cut and tsdf code (grid.cpp:20-23; |nt| <= delta so the clamp is the identity)
+    const float a = nt * rc.k127;
+    const float aa = fabsf(a);
+    if (!(fabsf(aa - 127.0f) > rc.ecode)) return false;
+    if (aa > 127.0f) {
+        out = kChiPayload;
+        return true;
+    }
+    int tc;
+    if (!certain_lround_f(a, rc.ecode, tc)) return false;
+    int ac;
+    if (MODE == 2) {
+        // #{k : na >= thresh[k]} (thresholds = exact reference encode boundaries). Margin:
+        // FP32 evaluation (<= 2e-6 relative) + the reference's own cancellation in
+        // (1 - gain) * predicted (<= 1e-15 * predicted) + float thresholds (2^-24).
+        const float m = 3e-6f * na + 1e-15f * pred;
+        // The log-scale guess is within 0.1 code of the encode formula, so the code is one of
+        // round(guess) - 1 .. + 1: two comparisons settle it (s_thr is shifted by one with
+        // -inf / +inf sentinels so every index below is in range).
+        const float vc = fminf(fmaxf(na, rc.thr_lo), rc.thr_hi);
+        const float gs = fminf(fmaxf((approx_log2_f(vc) - rc.lg_pmin) * rc.lg_scale, 0.0f), 255.0f);
+        const int gr = __float_as_int(__fadd_rn(gs, kMagic23)) - __float_as_int(kMagic23);
+        const float t_m1 = s_thr[gr], t_0 = s_thr[gr + 1], t_p1 = s_thr[gr + 2], t_p2 = s_thr[gr + 3];
+        // thresholds of codes gr-1 .. gr+2 (s_thr[k + 1] = thresh[k])
+        if (!(na >= t_m1) || !(na < t_p2)) return false;  // guess off by more than one: exact path
+        const bool ge0 = na >= t_0, ge1 = na >= t_p1;
+        const int g = gr - 1 + static_cast<int>(ge0) + static_cast<int>(ge1);
+        const float lo = ge1 ? t_p1 : ge0 ? t_0 : t_m1;   // thresh[g]
+        const float hi = ge1 ? t_p2 : ge0 ? t_p1 : t_0;   // thresh[g + 1]
+        if (!(na - m >= lo) && g > 0) return false;
+        if (!(na + m < hi) && g < 255) return false;
+        ac = g;
+    } else {
+        if (!certain_lround_f(fminf(fmaxf(na, 0.0f), rc.w_max) * rc.k255w, 1e-3f, ac)) return false;
+    }
+    out = static_cast<uint32_t>(static_cast<uint8_t>(tc)) | (static_cast<uint32_t>(ac) << 8);
+    return true;
+}
+
+// The reference's FP64 path for one voxel (fusion.cpp:81-173, 237-364): the payload code,
+// or -1 when there is no measurement.
+template <int MODE>
+__device__ __noinline__ int exact_voxel(const VolParams& P, const FrameConsts* __restrict__ fc, const FuseParams& fp,
+                                        const AuxTables* __restrict__ aux, int key, int l, uint32_t cell,
+                                        const double* __restrict__ pix_dm, const double* __restrict__ pix_var,
+                                        const double* __restrict__ pix_w) {
+    const int N = P.N, M = P.M;
+    const int bx = key % N, by = (key / N) % N, bz = key / (N * N);
+    const int lx = l % M, ly = (l / M) % M, lz = l / (M * M);
+    const d3 xc = apply(fc->inv, voxel_center(P, bx * M + lx, by * M + ly, bz * M + lz));
+    double pu, pv;
+    if (!project(fc->intr, xc, pu, pv)) return -1;
+    const int u = ref_lround_int(pu), v = ref_lround_int(pv);
+    if (!(u >= 0 && v >= 0 && u < fc->intr.w && v < fc->intr.h)) return -1;
+    const size_t pix = (size_t)v * fc->intr.w + u;
+    const double dm = pix_dm[pix];  // depth where the pixel passes every per-pixel test, else 0
+    if (!(dm > 0.0)) return -1;
+    const double tsdf_k = dm - xc.z;
+    if (fabs(tsdf_k) > P.delta) return -1;
+    const int8_t code = static_cast<int8_t>(cell & 0xFF);
+    const bool has_prior = code != kChiCode;
+    const double prior_t = has_prior ? aux->tsdf_decode[(int)code + 128] : 0.0;
+    const double prior_a = has_prior ? aux->aux_decode[cell >> 8] : 0.0;
+    double new_t, new_a, a_err;
+    filter_rule<MODE>(has_prior, prior_t, prior_a, tsdf_k, MODE == 2 ? pix_var[pix] : 0.0,
+                      MODE == 2 ? 0.0 : pix_w[pix], fp, false, new_t, new_a, a_err);
+    uint16_t out;
+    encode_cell(P, aux->aux_thresh, new_t, new_a, 0.0, false, 1.0 / P.delta, 1.0 / P.aux_w_max, out);
+    return out;
+}
+
+constexpr int kRowThreads = 256;
+constexpr int kRowCtasPerSm = 3;
+constexpr uint32_t kGrabUnits = 4;  // 32-row units a warp takes per atomic (before the tail)
+
+template <int MS>
+struct RowVec;
+template <>
+struct RowVec<3> {
+    using T = uint4;
+    __device__ static uint32_t cell(const uint4& r, int lx) {
+        const uint32_t w = lx < 2 ? r.x : lx < 4 ? r.y : lx < 6 ? r.z : r.w;
+        return (lx & 1) ? (w >> 16) : (w & 0xFFFF);
+    }
+    __device__ static uint4 chi() { return make_uint4(0x00800080u, 0x00800080u, 0x00800080u, 0x00800080u); }
+};
+template <>
+struct RowVec<2> {
+    using T = uint2;
+    __device__ static uint32_t cell(const uint2& r, int lx) {
+        const uint32_t w = lx < 2 ? r.x : r.y;
+        return (lx & 1) ? (w >> 16) : (w & 0xFFFF);
+    }
+    __device__ static uint2 chi() { return make_uint2(0x00800080u, 0x00800080u); }
+};
+
+// Per-warp ring of queued voxels: >= 31 left over + 32 rows x M new entries, a power of two.
+template <int MS>
+struct RowRing {
+    static constexpr int kEntries = MS == 3 ? 512 : 256;
+    static constexpr size_t kBytes = (kRowThreads / 32) * kEntries * sizeof(uint4);
+};
+
 template <int MODE, int MS>
-__global__ void __launch_bounds__(256)
-    k_integrate_fast(VolParams P, const FrameConsts* __restrict__ fc, FuseParams fp, const int2* __restrict__ work,
-                     const FrameCounters* __restrict__ ctr, const AuxTables* __restrict__ aux,
-                     const double* __restrict__ pix_dm, const double* __restrict__ pix_var,
-                     const double* __restrict__ pix_w, uint16_t* __restrict__ payload,
-                     unsigned long long* __restrict__ voxels_updated, const uint32_t* __restrict__ uniq,
-                     uint32_t* __restrict__ keybits) {
-    constexpr int M = 1 << MS, M3 = M * M * M;
-    constexpr int VPT = (M3 + 255) / 256;  // voxels per thread
-    __shared__ double s_tdec[256], s_adec[256], s_thr[256];
+__global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
+    k_integrate_rows(VolParams P, const FrameConsts* __restrict__ fc, FuseParams fp, const int2* __restrict__ work,
+                     FrameCounters* __restrict__ ctr, const AuxTables* __restrict__ aux,
+                     const float2* __restrict__ pix_f, const double* __restrict__ pix_dm,
+                     const double* __restrict__ pix_var, const double* __restrict__ pix_w,
+                     const int32_t* __restrict__ slot_key, uint16_t* __restrict__ payload,
+                     const uint32_t* __restrict__ uniq, uint32_t* __restrict__ keybits) {
+    constexpr int M = 1 << MS, M3 = M * M * M, RPB = M * M;
+    constexpr int kRing = RowRing<MS>::kEntries;
+    using RV = RowVec<MS>;
+    __shared__ float s_tdec[256], s_adec[256], s_thr[260];  // s_thr[k + 1] = thresh[k]; +-inf sentinels
+    extern __shared__ uint4 s_ring[];  // per warp kRing entries: {slot, l | cell << 9 | exact << 31, T, p}
+    __shared__ RowShared sh;
+    __shared__ VolParams sP;  // by reference into the (noinline) exact path without a stack copy
+    __shared__ FuseParams sFp;
     if (ctr->skip) return;
     for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-        s_tdec[i] = aux->tsdf_decode[i];
-        s_adec[i] = aux->aux_decode[i];
-        s_thr[i] = aux->aux_thresh[i];
+        s_tdec[i] = aux->tsdf_decode_f[i];
+        s_adec[i] = aux->aux_decode_f[i];
+        s_thr[i + 1] = aux->aux_thresh_f[i];
     }
-    __syncthreads();
-    const Pose inv = fc->inv;
-    const Intr intr = fc->intr;
-    const double delta = P.delta;
-    const double inv_delta = 1.0 / delta, inv_wmax = 1.0 / P.aux_w_max;
-    const int w = intr.w, h = intr.h;
+    if (threadIdx.x == 0) {
+        s_thr[0] = -INFINITY;
+        s_thr[257] = s_thr[258] = s_thr[259] = INFINITY;
+        sP = P;
+        sFp = fp;
+        const Pose inv = fc->inv;
+        const Intr intr = fc->intr;
+        for (int i = 0; i < 9; ++i) sh.R[i] = inv.R.m[i];
+        sh.t[0] = inv.t.x;
+        sh.t[1] = inv.t.y;
+        sh.t[2] = inv.t.z;
+        sh.ox = P.ox;
+        sh.oy = P.oy;
+        sh.oz = P.oz;
+        sh.voxel = P.voxel;
+        sh.Dxf = static_cast<float>(P.voxel * inv.R.m[0]);
+        sh.Dyf = static_cast<float>(P.voxel * inv.R.m[3]);
+        sh.Dzf = static_cast<float>(P.voxel * inv.R.m[6]);
+        sh.fxf = static_cast<float>(intr.fx);
+        sh.fyf = static_cast<float>(intr.fy);
+        sh.cxf = static_cast<float>(intr.cx);
+        sh.cyf = static_cast<float>(intr.cy);
+        sh.Fmax = static_cast<float>(dmax(intr.fx, intr.fy));
+        sh.Wpix = static_cast<float>(intr.w > intr.h ? intr.w : intr.h) + 2.0f;
+        sh.Mvox = static_cast<float>(M * P.voxel);
+        // T error bound (m) for rows with z < 16 m: double-float row origin, lx * dz, and the
+        // (Sterbenz-exact in the band) subtraction d - z_hi
+        const double delta = P.delta;
+        const double eT = 0x1p-21 * (delta + 2.0 * M * P.voxel) + 0x1p-41;
+        sh.thr_out = static_cast<float>((delta + eT) * 1.000001);
+        sh.thr_in = static_cast<float>((delta - eT) * 0.999999);
+        sh.k127 = static_cast<float>(kTsdfCodeRange / delta);
+        sh.ecode = static_cast<float>(1e-3 + 4.0 * eT * (kTsdfCodeRange / delta));
+        sh.q = static_cast<float>(fp.q);
+        sh.w_max = static_cast<float>(P.aux_w_max);
+        sh.k255w = static_cast<float>(255.0 / P.aux_w_max);
+        sh.lg_pmin = static_cast<float>(P.aux_lg_pmin);
+        sh.lg_scale = static_cast<float>(P.aux_lg_scale);
+        sh.thr_lo = static_cast<float>(P.aux_p_min * 0.5);
+        sh.thr_hi = static_cast<float>(P.aux_p_max * 2.0);
+    }
     clear_keybits(ctr, uniq, keybits);
+    __syncthreads();
     const uint32_t limit = ctr->limit, upd_base = ctr->upd_base;
-    const unsigned n_work = limit + ctr->n_update;
-    const int N = P.N;
-    unsigned long long updated = 0;
-    for (unsigned item = blockIdx.x; item < n_work; item += gridDim.x) {
-        const int2 wk = work_at(work, limit, upd_base, item);
-        const uint32_t slot = static_cast<uint32_t>(wk.x) & 0x7fffffffu;
-        const bool fresh = (static_cast<uint32_t>(wk.x) >> 31) != 0;
-        const int key = wk.y;
-        int bx, by, bz;
-        if (P.nshift >= 0) {
-            bx = key & (N - 1);
-            by = (key >> P.nshift) & (N - 1);
-            bz = key >> (2 * P.nshift);
-        } else {
-            bx = key % N;
-            by = (key / N) % N;
-            bz = key / (N * N);
-        }
-        // Phase A: addresses, projections and all loads of this thread's voxels issued
-        // before any dependent arithmetic (memory-level parallelism).
-        size_t pidx[VPT], pix[VPT];
-        double zc[VPT];
-        uint16_t cellv[VPT];
-        double dmv[VPT];
-        bool inb[VPT];
-#pragma unroll
-        for (int j = 0; j < VPT; ++j) {
-            const int l = threadIdx.x + j * 256;
-            inb[j] = false;
-            pix[j] = 0;
-            zc[j] = 0.0;
-            pidx[j] = (size_t)slot * M3 + l;
-            cellv[j] = kChiPayload;
-            dmv[j] = 0.0;
-            if (M3 < 256 * VPT && l >= M3) continue;
-            if (!fresh) cellv[j] = payload[pidx[j]];
-            const int lx = l & (M - 1), ly = (l >> MS) & (M - 1), lz = l >> (2 * MS);
-            // estimate_measurement (fusion.cpp:81-99)
-            const d3 xc = apply(inv, voxel_center_fast(P, (bx << MS) + lx, (by << MS) + ly, (bz << MS) + lz));
-            zc[j] = xc.z;
-            if (xc.z > 0.0) {
-                const double nx = intr.fx * xc.x, ny = intr.fy * xc.y;
-                int u, v;
-                double r;
-                bool ok = approx_rcp(xc.z, r) && certain_lround(nx * r + intr.cx, u) && certain_lround(ny * r + intr.cy, v);
-                if (!ok) {  // exact reference projection
-                    u = ref_lround_int(nx / xc.z + intr.cx);
-                    v = ref_lround_int(ny / xc.z + intr.cy);
-                }
-                if (u >= 0 && v >= 0 && u < w && v < h) {
-                    pix[j] = (size_t)v * w + u;
-                    inb[j] = true;
-                    dmv[j] = pix_dm[pix[j]];  // depth where the pixel passes every per-pixel test, else 0
-                }
+    const unsigned long long n_rows = ((unsigned long long)limit + ctr->n_update) * RPB;
+    const int w = fc->intr.w, h = fc->intr.h, N = P.N;
+    const int lane = threadIdx.x & 31;
+    uint4* ring = s_ring + (threadIdx.x >> 5) * kRing;
+    uint32_t head = 0, tail = 0;  // warp-uniform ring cursors (monotone; index & (kRing - 1))
+    uint32_t updated = 0, exact = 0;
+    // Phase 2 on ring entries [head, head + n): lanes take one entry each.
+    auto drain = [&](uint32_t n) {
+        if (lane < n) {
+            const uint4 e = ring[(head + lane) & (kRing - 1)];
+            const uint32_t l = e.y & 0x1FF, cell = (e.y >> 9) & 0xFFFF;
+            uint32_t out;
+            int code = 0;
+            if ((e.y >> 31) ||
+                !approx_update<MODE>(cell, __uint_as_float(e.z), __uint_as_float(e.w), sh, s_tdec, s_adec, s_thr, out)) {
+                ++exact;
+                code = exact_voxel<MODE>(sP, fc, sFp, aux, slot_key[e.x], static_cast<int>(l), cell, pix_dm, pix_var,
+                                         pix_w);
+                out = static_cast<uint32_t>(code);
+            }
+            if (code >= 0) {
+                payload[(size_t)e.x * M3 + l] = static_cast<uint16_t>(out);
+                ++updated;
             }
         }
-        // Phase B: band test (fusion.cpp:145), filter, quantize, store.
+        head += n;
+    };
+    // Guided dynamic scheduling in units of 32 rows: kGrabUnits per atomic while plenty of work
+    // remains, single units for the tail (the last grabs decide when the kernel ends).
+    const uint32_t n_units = static_cast<uint32_t>((n_rows + 31) / 32);
+    const uint32_t tail_units = gridDim.x * (kRowThreads / 32) * 2 * kGrabUnits;
+    uint32_t seen = 0;
+    for (;;) {
+        const uint32_t step = seen + tail_units < n_units ? kGrabUnits : 1u;
+        uint32_t grab = 0;
+        if (lane == 0) grab = atomicAdd(&ctr->row_chunks, step);
+        grab = __shfl_sync(0xffffffffu, grab, 0);
+        seen = grab + step;
+        if (grab >= n_units) break;
+        const uint32_t units = min(step, n_units - grab);
+        const unsigned long long grab_row = (unsigned long long)grab * 32;
+        for (uint32_t sub = 0; sub < units; ++sub) {
+            // ---------------- phase 1: one x-row per lane ----------------
+            const unsigned long long row = grab_row + sub * 32 + lane;
+            uint32_t amask = 0, emask = 0, slot = 0, rbase = 0;
+            float tk[M], pf[M];
+            typename RV::T cells = RV::chi();
+            if (row < n_rows) {
+                const uint32_t item = static_cast<uint32_t>(row >> (2 * MS));
+                const int r = static_cast<int>(row & (RPB - 1));
+                const int2 wk = work_at(work, limit, upd_base, item);
+                slot = static_cast<uint32_t>(wk.x) & 0x7fffffffu;
+                const bool fresh = (static_cast<uint32_t>(wk.x) >> 31) != 0;
+                const int key = wk.y;
+                int bx, by, bz;
+                if (P.nshift >= 0) {
+                    bx = key & (N - 1);
+                    by = (key >> P.nshift) & (N - 1);
+                    bz = key >> (2 * P.nshift);
+                } else {
+                    bx = key % N;
+                    by = (key / N) % N;
+                    bz = key / (N * N);
+                }
+                rbase = static_cast<uint32_t>(r * M);
+                typename RV::T* prow = reinterpret_cast<typename RV::T*>(payload + (size_t)slot * M3 + rbase);
+                if (fresh) *prow = RV::chi();  // newly allocated block: chi-initialised (grid.cpp:87-100)
+                else cells = *prow;
+                const int ly = r & (M - 1), lz = r >> MS;
+                // row origin x_c = R (voxel_center) + t in FP64 (voxel_center, grid.cpp:271-273)
+                const double vx = sh.ox + (i2d_exact(bx << MS) + 0.5) * sh.voxel;
+                const double vy = sh.oy + (i2d_exact((by << MS) + ly) + 0.5) * sh.voxel;
+                const double vz = sh.oz + (i2d_exact((bz << MS) + lz) + 0.5) * sh.voxel;
+                const double Ax = ((sh.R[0] * vx + sh.R[1] * vy) + sh.R[2] * vz) + sh.t[0];
+                const double Ay = ((sh.R[3] * vx + sh.R[4] * vy) + sh.R[5] * vz) + sh.t[1];
+                const double Az = ((sh.R[6] * vx + sh.R[7] * vy) + sh.R[8] * vz) + sh.t[2];
+                const float Axf = static_cast<float>(Ax), Ayf = static_cast<float>(Ay);
+                const float Azh = static_cast<float>(Az);
+                const float Azl = static_cast<float>(Az - static_cast<double>(Azh));
+                const float Dxf = sh.Dxf, Dyf = sh.Dyf, Dzf = sh.Dzf;
+                const float zend = fmaf(static_cast<float>(M - 1), Dzf, Azh);
+                const float zlo = fminf(Azh, zend) - 1e-6f, zhi = fmaxf(Azh, zend) + 1e-6f;
+                const float rzlo = rcp_approx_f(zlo);
+                const float X = fmaxf(fabsf(Axf), fabsf(Ayf)) + sh.Mvox, Z = fabsf(Azh) + sh.Mvox;
+                const float Xq = sh.Fmax * X * rzlo;  // >= |u - cx|, |v - cy| over the row
+                if (zlo > 1e-3f && zhi < 16.0f && Xq < 2097152.0f) {
+                    // pixel-rounding margin of the row; |u|, |v| < 2^22 guaranteed
+                    const float eu = 1.6f * (0x1p-23f * Xq * (2.5f + Z * rzlo) + 0x1p-24f * sh.Wpix);
+                    const float half = 0.5f - eu;
+                    const float fxf = sh.fxf, fyf = sh.fyf, cxf = sh.cxf, cyf = sh.cyf;
+                    const float thr_in = sh.thr_in, thr_out = sh.thr_out;
 #pragma unroll
-        for (int j = 0; j < VPT; ++j) {
-            const int l = threadIdx.x + j * 256;
-            if (M3 < 256 * VPT && l >= M3) continue;
-            double tsdf_k = 0.0;
-            bool meas = false;
-            if (inb[j] && dmv[j] > 0.0) {
-                tsdf_k = dmv[j] - zc[j];
-                meas = !(fabs(tsdf_k) > delta);
+                    for (int lx = 0; lx < M; ++lx) {
+                        // explicit fma: one rounding per coordinate (the bounds above assume <= 2)
+                        const float xf = lx == 0 ? Axf : fmaf(static_cast<float>(lx), Dxf, Axf);
+                        const float yf = lx == 0 ? Ayf : fmaf(static_cast<float>(lx), Dyf, Ayf);
+                        const float zf = lx == 0 ? Azh : fmaf(static_cast<float>(lx), Dzf, Azh);
+                        const float rz = rcp_approx_f(zf);
+                        const float uf = fmaf(fxf, xf * rz, cxf), vf = fmaf(fyf, yf * rz, cyf);
+                        const float tu = __fadd_rn(uf, kMagic23), tv = __fadd_rn(vf, kMagic23);
+                        const bool cert = fabsf(__fsub_rn(uf, __fsub_rn(tu, kMagic23))) < half &&
+                                          fabsf(__fsub_rn(vf, __fsub_rn(tv, kMagic23))) < half;
+                        const uint32_t u = static_cast<uint32_t>(__float_as_int(tu) - __float_as_int(kMagic23));
+                        const uint32_t v = static_cast<uint32_t>(__float_as_int(tv) - __float_as_int(kMagic23));
+                        const bool inimg = cert && u < (uint32_t)w && v < (uint32_t)h;
+                        const float2 px = pix_f[inimg ? v * (uint32_t)w + u : 0u];
+                        const float t = (px.x - Azh) - (lx == 0 ? Azl : fmaf(static_cast<float>(lx), Dzf, Azl));
+                        const float at = fabsf(t);
+                        const bool meas = inimg && px.x > 0.0f;
+                        const bool in = meas && at < thr_in;
+                        const bool unc = !cert || (meas && !(at < thr_in) && !(at > thr_out));
+                        amask |= static_cast<uint32_t>(in) << lx;
+                        emask |= static_cast<uint32_t>(unc) << lx;
+                        tk[lx] = t;
+                        pf[lx] = px.y;
+                    }
+                } else if (!(zhi < -1e-3f)) {
+                    emask = (1u << M) - 1u;  // row near / across the camera plane, or very far: exact path
+                }
             }
-            if (!meas) {
-                if (fresh) payload[pidx[j]] = kChiPayload;
-                continue;
+            // ---------------- warp compaction into the ring ----------------
+            const uint32_t qmask = amask | emask;
+            const uint32_t cnt = static_cast<uint32_t>(__popc(qmask));
+            uint32_t incl = cnt;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += y;
             }
-            bool has_prior = false;
-            double prior_t = 0.0, prior_a = 0.0;
-            const uint16_t cell = cellv[j];
-            const int8_t code = static_cast<int8_t>(cell & 0xFF);
-            if (code != kChiCode) {
-                has_prior = true;
-                prior_t = s_tdec[(int)code + 128];
-                prior_a = s_adec[cell >> 8];
+            uint32_t pos = tail + incl - cnt;
+#pragma unroll
+            for (int lx = 0; lx < M; ++lx) {
+                const uint32_t meta = (rbase + lx) | (RV::cell(cells, lx) << 9) | ((emask >> lx) << 31);
+                if (qmask & (1u << lx))
+                    ring[pos++ & (kRing - 1)] = make_uint4(slot, meta, __float_as_uint(tk[lx]), __float_as_uint(pf[lx]));
             }
-            const double pk = MODE == 2 ? pix_var[pix[j]] : 0.0;
-            const double wk_ = MODE == 2 ? 0.0 : pix_w[pix[j]];
-            double new_t, new_a, a_err;
-            uint16_t out;
-            if (!(filter_rule<MODE>(has_prior, prior_t, prior_a, tsdf_k, pk, wk_, fp, true, new_t, new_a, a_err) &&
-                  encode_cell(P, s_thr, new_t, new_a, a_err, true, inv_delta, inv_wmax, out))) {
-                filter_rule<MODE>(has_prior, prior_t, prior_a, tsdf_k, pk, wk_, fp, false, new_t, new_a, a_err);
-                encode_cell(P, s_thr, new_t, new_a, 0.0, false, inv_delta, inv_wmax, out);
-            }
-            payload[pidx[j]] = out;
-            ++updated;
+            tail += __shfl_sync(0xffffffffu, incl, 31);
+            __syncwarp();  // ring entries and the fresh rows' chi stores before the drain
+            // ---------------- phase 2: drain full rounds ----------------
+            while (tail - head >= 32) drain(32);
+            __syncwarp();  // drained slots may be refilled by the next compaction
         }
     }
-    for (int off = 16; off > 0; off >>= 1) updated += __shfl_down_sync(0xffffffffu, updated, off);
-    if ((threadIdx.x & 31) == 0 && updated) atomicAdd(voxels_updated, updated);
+    drain(tail - head);
+    for (int off = 16; off > 0; off >>= 1) {
+        updated += __shfl_down_sync(0xffffffffu, updated, off);
+        exact += __shfl_down_sync(0xffffffffu, exact, off);
+    }
+    if (lane == 0 && updated) atomicAdd(&ctr->voxels_updated, (unsigned long long)updated);
+    if (lane == 0 && exact) atomicAdd(&ctr->exact_voxels, (unsigned long long)exact);
 }
 
 template <int MODE, bool FLOATP>
@@ -1001,6 +1271,20 @@ FuseParams resolve_fuse_params(const Volume& v, const sf_fusion_params& p, bool 
     return f;
 }
 
+template <int MODE, int MS>
+static void launch_integrate_rows(Volume& v, FrameBuffers& fb, const FuseParams& fp, cudaStream_t s) {
+    static_assert(RowRing<MS>::kBytes <= 200 * 1024, "ring exceeds shared memory");
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+        SF_CUDA(cudaFuncSetAttribute(k_integrate_rows<MODE, MS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)RowRing<MS>::kBytes));
+        configured = true;
+    }
+    k_integrate_rows<MODE, MS><<<148 * kRowCtasPerSm, kRowThreads, RowRing<MS>::kBytes, s>>>(
+        v.P, fb.fc, fp, fb.work, fb.ctr, v.d_aux, fb.pix_f, fb.pix_dm, fb.pix_var, fb.pix_w, v.d_slot_key,
+        v.d_payload, fb.keys_unique, v.d_keybits);
+}
+
 void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* depth, const float* sigma,
                  const FuseParams& fp, cudaStream_t s, bool export_only, uint64_t* launches, const int* dead_flag,
                  const FuseEvents* events) {
@@ -1024,7 +1308,7 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
             n += 2;
         }
         k_pixel_meas<<<grd2, blk2, 0, s>>>(depth, sigma, w, h, intr, fp, fb.normals, fb.edge, fb.pix_var, fb.pix_w,
-                                            fb.pix_ok, fb.pix_dm, dead);
+                                            fb.pix_ok, fb.pix_dm, fb.pix_f, dead);
         SF_LAUNCH_CHECK();
         n += 1;
     }
@@ -1071,20 +1355,17 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
                                                                v.d_fpayload, vu, fb.keys_unique, v.d_keybits)
         const bool fpl = v.d_fpayload != nullptr;
         if (events && events->before_integrate) record_event(events->before_integrate, s);
-        const bool fast = !fpl && (P.mshift == 3 || P.mshift == 2);
-#define SF_INTEGRATE_FAST(MODE, MS)                                                                            \
-    k_integrate_fast<MODE, MS><<<kPersistentCtas, 256, 0, s>>>(P, fb.fc, fp, fb.work, fb.ctr, v.d_aux, fb.pix_dm,   \
-                                                               fb.pix_var, fb.pix_w, v.d_payload, vu,               \
-                                                               fb.keys_unique, v.d_keybits)
+        const bool fast = !fpl && (P.mshift == 3 || P.mshift == 2) && v.h_aux.fp32_ok;
+#define SF_INTEGRATE_ROWS(MODE, MS) launch_integrate_rows<MODE, MS>(v, fb, fp, s)
         if (fast) {
             if (P.mshift == 3) {
-                if (fp.mode == 0) SF_INTEGRATE_FAST(0, 3);
-                else if (fp.mode == 1) SF_INTEGRATE_FAST(1, 3);
-                else SF_INTEGRATE_FAST(2, 3);
+                if (fp.mode == 0) SF_INTEGRATE_ROWS(0, 3);
+                else if (fp.mode == 1) SF_INTEGRATE_ROWS(1, 3);
+                else SF_INTEGRATE_ROWS(2, 3);
             } else {
-                if (fp.mode == 0) SF_INTEGRATE_FAST(0, 2);
-                else if (fp.mode == 1) SF_INTEGRATE_FAST(1, 2);
-                else SF_INTEGRATE_FAST(2, 2);
+                if (fp.mode == 0) SF_INTEGRATE_ROWS(0, 2);
+                else if (fp.mode == 1) SF_INTEGRATE_ROWS(1, 2);
+                else SF_INTEGRATE_ROWS(2, 2);
             }
         } else if (fp.mode == 0) {
             if (fpl) SF_INTEGRATE(0, true);
@@ -1097,7 +1378,7 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
             else SF_INTEGRATE(2, false);
         }
 #undef SF_INTEGRATE
-#undef SF_INTEGRATE_FAST
+#undef SF_INTEGRATE_ROWS
         SF_LAUNCH_CHECK();
         if (events && events->after_integrate) record_event(events->after_integrate, s);
         k_fuse_finalize<<<1, 1, 0, s>>>(fb.ctr, v.d_vc);

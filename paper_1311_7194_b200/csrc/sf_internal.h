@@ -76,6 +76,9 @@ struct FrameCounters {
     unsigned long long voxels_updated;
     unsigned long long alloc_before;
     unsigned long long alloc_now;
+    unsigned long long exact_voxels;  // integrate: voxels decided on the FP64 fallback path
+    uint32_t row_chunks;              // integrate: next row chunk (dynamic scheduling)
+    uint32_t pad_;
 };
 
 // Device-side aux codec tables (host-computed with the reference's libm).
@@ -83,6 +86,10 @@ struct AuxTables {
     double tsdf_decode[256];  // dequantize_tsdf(code)        (grid.cpp:25-27), index code+128
     double aux_decode[256];   // AuxQuantization::decode(code) (grid.cpp:48-51)
     double aux_thresh[256];   // variance mode: thresh[k] = min v with encode(v) >= k, k = 1..255
+    // FP32 copies (round to nearest) for the certified single-precision integrate path;
+    // their rounding error is part of that path's decision margins (sf_fusion.cu).
+    float tsdf_decode_f[256], aux_decode_f[256], aux_thresh_f[256];
+    int fp32_ok;  // all codec values representable as normal floats (else the FP64 kernel runs)
 };
 void build_aux_tables(const VolParams& P, AuxTables* t);
 uint8_t host_aux_encode(const VolParams& P, double value);  // reference encode (grid.cpp:38-46)
@@ -99,6 +106,7 @@ struct FrameBuffers {
     double* pix_w = nullptr;   // w*h per-pixel w_k
     uint8_t* pix_ok = nullptr; // w*h valid && quality >= 0.2
     double* pix_dm = nullptr;  // w*h depth where pix_ok, else 0 (one gather per voxel)
+    float2* pix_f = nullptr;   // w*h {depth where pix_ok else 0, (float) p_k or w_k}: FP32 integrate
     uint32_t key_cap = 0;
     uint32_t* keys = nullptr;
     uint32_t* keys_sorted = nullptr;

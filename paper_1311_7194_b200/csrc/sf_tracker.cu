@@ -335,6 +335,7 @@ int sf_tracker_fetch(sf_tracker_t tr, sf_frame_metrics* out, void* stream) {
         out->blocks_processed = static_cast<uint64_t>(h->ctr.limit) + h->ctr.n_update;
         if (h->ctr.skip) out->blocks_processed = 0;
         out->voxels_visited = out->blocks_processed * m * m * m;
+        out->exact_voxels = h->ctr.exact_voxels;
         out->kernel_launches = tr->last_launches;
         if (tr->last_icp_loop) out->kernel_launches += static_cast<uint64_t>(h->icp.bodies);
         return SF_OK;

@@ -74,12 +74,27 @@ static double bitsd(uint64_t b) {
 // Variance-mode encode is a monotone step function of the value (log is monotone), so
 // encode(v) == #{k : v >= thresh[k]}. Each threshold is located by bisection over the
 // ordered bit patterns of positive doubles, with the reference's own libm log: exact.
+static void build_aux_thresholds(const VolParams& P, AuxTables* t);
 void build_aux_tables(const VolParams& P, AuxTables* t) {
     for (int c = -128; c < 128; ++c) t->tsdf_decode[c + 128] = dequantize_tsdf(static_cast<int8_t>(c), P.delta);
     for (int c = 0; c < 256; ++c) t->aux_decode[c] = host_aux_decode(P, static_cast<uint8_t>(c));
     t->aux_thresh[0] = -INFINITY;
     for (int k = 1; k < 256; ++k) t->aux_thresh[k] = INFINITY;
-    if (P.aux_mode != 1) return;
+    if (P.aux_mode == 1) build_aux_thresholds(P, t);
+    // FP32 copies; the single-precision path runs only when every value is a normal float
+    // (or 0 / inf) far from the float range limits.
+    auto fits = [](double x) { return x == 0.0 || std::isinf(x) || (std::fabs(x) > 1e-30 && std::fabs(x) < 1e30); };
+    t->fp32_ok = fits(P.delta) && P.delta > 0.0 ? 1 : 0;
+    for (int c = 0; c < 256; ++c) {
+        t->tsdf_decode_f[c] = static_cast<float>(t->tsdf_decode[c]);
+        t->aux_decode_f[c] = static_cast<float>(t->aux_decode[c]);
+        t->aux_thresh_f[c] = static_cast<float>(t->aux_thresh[c]);
+        if (!fits(t->tsdf_decode[c]) || !fits(t->aux_decode[c]) || !fits(t->aux_thresh[c])) t->fp32_ok = 0;
+    }
+    if (P.aux_mode == 0 && !fits(P.aux_w_max)) t->fp32_ok = 0;
+}
+
+static void build_aux_thresholds(const VolParams& P, AuxTables* t) {
     const double lo0 = P.aux_p_min, hi0 = P.aux_p_max;
     if (!(lo0 > 0.0) || !(hi0 > lo0)) return;
     for (int k = 1; k < 256; ++k) {
@@ -104,7 +119,7 @@ void FrameBuffers::release() {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
-    void* ptrs[] = {depth, sigma, normals, edge, pix_var, pix_w, pix_ok, pix_dm, keys, keys_sorted, keys_unique,
+    void* ptrs[] = {depth, sigma, normals, edge, pix_var, pix_w, pix_ok, pix_dm, pix_f, keys, keys_sorted, keys_unique,
                     flags, ranks, cub_temp, work, ctr, fc, pose};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -114,6 +129,7 @@ void FrameBuffers::release() {
     edge = pix_ok = nullptr;
     pix_var = pix_w = nullptr;
     pix_dm = nullptr;
+    pix_f = nullptr;
     keys = keys_sorted = keys_unique = flags = ranks = nullptr;
     cub_temp = nullptr;
     work = nullptr;
@@ -145,6 +161,7 @@ void ensure_frame_buffers(Volume& v, FrameBuffers& fb, int w, int h) {
     SF_CUDA(cudaMalloc(&fb.pix_w, n * sizeof(double)));
     SF_CUDA(cudaMalloc(&fb.pix_ok, n));
     SF_CUDA(cudaMalloc(&fb.pix_dm, n * sizeof(double)));
+    SF_CUDA(cudaMalloc(&fb.pix_f, n * sizeof(float2)));
     SF_CUDA(cudaMalloc(&fb.keys, fb.key_cap * sizeof(uint32_t)));
     SF_CUDA(cudaMalloc(&fb.keys_sorted, fb.key_cap * sizeof(uint32_t)));
     SF_CUDA(cudaMalloc(&fb.keys_unique, fb.key_cap * sizeof(uint32_t)));
