@@ -161,6 +161,35 @@ int sf_volume_create(const sf_grid_config* config, uint64_t pool_capacity, const
 int sf_volume_destroy(sf_volume_t vol);
 int sf_volume_get_info(sf_volume_t vol, sf_volume_info* out);
 
+/* ---- spatial sharding across GPUs --------------------
+ * No reference counterpart: the reference volume is one process. A sharded volume
+ * allocates only the blocks its rank owns: owner(block) = hash of its (2^brick_shift)^3-block
+ * brick % world (sf_shard_owner). Call on an empty volume. Integrating the same frame on
+ * every rank's volume yields, over the union of ranks, exactly the single volume's blocks
+ * and payloads. */
+int sf_volume_set_shard(sf_volume_t vol, int32_t rank, int32_t world, int32_t brick_shift);
+int32_t sf_shard_owner(int32_t bx, int32_t by, int32_t bz, int32_t brick_shift, int32_t world);
+/* Composite of per-rank raycasts (device pointers, asynchronous on `stream`):
+ * key[i] = float_bits(depth) << 32 | (normal missing) << 31 | rank for hit pixels, INT64_MAX
+ * otherwise; after an all-reduce MIN of `key` over ranks, sf_composite_select zeroes the
+ * depth / normals of pixels this rank did not win, so an all-reduce SUM of their bit
+ * patterns (int32) assembles the nearest-depth composite on every rank. */
+/* Halo exchange after an integrate on a sharded volume (device pointers; synchronises):
+ * pack writes (table index, M^3 payload codes) records of the blocks the last sf_integrate
+ * processed that touch (26-neighbourhood) a brick of another rank; *count = records (error
+ * SF_OUT_OF_RANGE if > cap). apply mirrors, read-only, the records that touch a brick of this
+ * rank (allocating them on first sight; *applied = mirrored). With every rank's records applied
+ * on every rank, each trilinear sample the reference raycast takes is evaluable on the rank
+ * owning its base voxel, so the composite is exact. */
+int sf_shard_pack_halo(sf_volume_t vol, int32_t* keys, uint16_t* payloads, uint64_t cap, uint32_t* count,
+                       void* stream);
+int sf_shard_apply_halo(sf_volume_t vol, const int32_t* keys, const uint16_t* payloads, uint64_t n,
+                        uint32_t* applied, void* stream);
+int sf_composite_key(const float* depth, const float* normals_xyz, uint64_t n, int32_t rank, int64_t* key,
+                     void* stream);
+int sf_composite_select(const int64_t* key, uint64_t n, int32_t rank, float* depth, float* normals_xyz,
+                        void* stream);
+
 /* SparseTsdfGrid::allocate_block / free_block / block_slot (grid.cpp:82-119). */
 int sf_volume_allocate_block(sf_volume_t vol, const int32_t bc[3], int32_t* slot_out);
 int sf_volume_free_block(sf_volume_t vol, const int32_t bc[3]);
@@ -218,6 +247,12 @@ int sf_ray_bounds(sf_volume_t vol, const double pose[12], const sf_intrinsics* i
 int sf_raycast(sf_volume_t vol, const double pose[12], const sf_intrinsics* intr,
                float* depth, float* normals_xyz, int32_t out_on_device,
                sf_raycast_stats* stats, void* stream);
+/* raycast(grid, pose, intrinsics, bounds) with caller-supplied bounds (render.hpp:61-63):
+ * the sharded path marches every rank's volume from the all-reduced (global) bounds.
+ * `on_device` applies to the bounds and the outputs alike. */
+int sf_raycast_with_bounds(sf_volume_t vol, const double pose[12], const sf_intrinsics* intr,
+                           const float* t_start, const float* t_end, float* depth, float* normals_xyz,
+                           int32_t on_device, sf_raycast_stats* stats, void* stream);
 
 /* compute_normals(frame, opts) (camera.hpp:90, camera.cpp:44-76). */
 int sf_compute_normals(const sf_frame* frame, double sigma0, double spatial_scale,

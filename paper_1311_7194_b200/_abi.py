@@ -221,6 +221,14 @@ PRODUCT_ONLY = {
     "tracker_stage_times": (C.c_int, [vp, P(C.c_float)]),
     "tracker_io_bytes": (C.c_int, [vp, i32, u64p, u64p]),
     "debug_aux_tables": (C.c_int, [P(AuxQuantC), C.c_double, c_double_p, c_double_p, c_double_p]),
+    # spatial sharding
+    "volume_set_shard": (C.c_int, [vp, i32, i32, i32]),
+    "shard_owner": (C.c_int32, [i32, i32, i32, i32, i32]),
+    "raycast_with_bounds": (C.c_int, [vp, c_double_p, P(IntrinsicsC), vp, vp, vp, vp, i32, P(RaycastStatsC), vp]),
+    "composite_key": (C.c_int, [vp, vp, u64, i32, vp, vp]),
+    "composite_select": (C.c_int, [vp, u64, i32, vp, vp, vp]),
+    "shard_pack_halo": (C.c_int, [vp, vp, vp, u64, P(C.c_uint32), vp]),
+    "shard_apply_halo": (C.c_int, [vp, vp, vp, u64, P(C.c_uint32), vp]),
 }
 
 REF_ONLY = {

@@ -199,7 +199,24 @@ struct VolParams {
     double inv_voxel;           // RN(1 / voxel): Markstein-corrected division by voxel (sf_render.cu)
     double aux_lg_pmin, aux_lg_scale;
     int nshift;  // log2(N) when N is a power of two, else -1  // variance codes: log2(p_min), 255 / log2(p_max / p_min) (code guess)
+    // Spatial sharding: this volume allocates only the blocks it owns,
+    // owner = hash of the (2^shard_shift)^3-block brick % shard_world. world 1 = owns all.
+    int shard_rank, shard_world, shard_shift;
 };
+
+// Owner rank of block (bx, by, bz) under brick sharding (identical on host and device).
+SF_HD int shard_owner(int bx, int by, int bz, int shift, int world) {
+    const uint32_t x = static_cast<uint32_t>(bx) >> shift, y = static_cast<uint32_t>(by) >> shift,
+                   z = static_cast<uint32_t>(bz) >> shift;
+    uint32_t hsh = x * 0x9E3779B1u ^ y * 0x85EBCA77u ^ z * 0xC2B2AE3Du;
+    hsh ^= hsh >> 15;
+    hsh *= 0x2C1B3C6Du;
+    hsh ^= hsh >> 12;
+    return static_cast<int>(hsh % static_cast<uint32_t>(world));
+}
+SF_HD bool shard_owns(const VolParams& P, int bx, int by, int bz) {
+    return P.shard_world <= 1 || shard_owner(bx, by, bz, P.shard_shift, P.shard_world) == P.shard_rank;
+}
 
 constexpr int kCoarseShift = 4;  // super-block = 16^3 blocks
 

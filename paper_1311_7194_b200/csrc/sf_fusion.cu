@@ -88,7 +88,7 @@ __global__ void k_frame_consts(VolParams P, Intr intr, const double* __restrict_
 __global__ void k_fuse_begin(FrameCounters* ctr, const VolCounters* vc, const int* dead) {
     FrameCounters z;
     memset(&z, 0, sizeof(z));
-    z.alloc_before = vc->allocated_count;
+    z.alloc_before = vc->allocated_count - vc->halo_count;  // owned blocks only
     z.skip = dead ? static_cast<uint32_t>(*dead != 0) : 0u;
     *ctr = z;
 }
@@ -239,7 +239,7 @@ __global__ void k_block_keys(VolParams P, const FrameConsts* __restrict__ fc, co
             const int bx = ref_floor_int((x.x - P.ox) / P.block_side);
             const int by = ref_floor_int((x.y - P.oy) / P.block_side);
             const int bz = ref_floor_int((x.z - P.oz) / P.block_side);
-            const bool in = bx >= 0 && by >= 0 && bz >= 0 && bx < P.N && by < P.N && bz < P.N;
+            const bool in = bx >= 0 && by >= 0 && bz >= 0 && bx < P.N && by < P.N && bz < P.N && shard_owns(P, bx, by, bz);
             out[k] = in ? static_cast<uint32_t>(table_index(P, bx, by, bz)) : sentinel;
         }
         k0 = out[0];
@@ -309,7 +309,7 @@ __global__ void k_block_keys_set(VolParams P, const FrameConsts* __restrict__ fc
             const int bx = ref_floor_int((x.x - P.ox) / P.block_side);
             const int by = ref_floor_int((x.y - P.oy) / P.block_side);
             const int bz = ref_floor_int((x.z - P.oz) / P.block_side);
-            if (bx >= 0 && by >= 0 && bz >= 0 && bx < P.N && by < P.N && bz < P.N) {
+            if (bx >= 0 && by >= 0 && bz >= 0 && bx < P.N && by < P.N && bz < P.N && shard_owns(P, bx, by, bz)) {
                 key = static_cast<uint32_t>(table_index(P, bx, by, bz));
                 const uint32_t bit = 1u << (key & 31);
                 fresh = !(atomicOr(&keybits[key >> 5], bit) & bit);
@@ -437,6 +437,7 @@ __global__ void k_visible(VolParams P, const FrameConsts* __restrict__ fc, Frame
         if (key < 0) continue;
         if (in_sorted(uniq, n_list, static_cast<uint32_t>(key))) continue;  // in the allocate set
         const int bx = key % P.N, by = (key / P.N) % P.N, bz = key / (P.N * P.N);
+        if (!shard_owns(P, bx, by, bz)) continue;  // mirrored halo block of another rank
         const d3 lo = block_min_corner(P, bx, by, bz);
         const double side = P.block_side;
         const d3 hi = add(lo, mk(side, side, side));
@@ -502,7 +503,8 @@ __global__ void k_worklist(VolParams P, const FrameConsts* __restrict__ fc, Fram
             const d3 lo = block_min_corner(P, bx, by, bz);
             const double side = P.block_side;
             const d3 hi = add(lo, mk(side, side, side));
-            if (frustum_intersects_block(P, fc, lo, hi)) {
+            // a sharded volume integrates only its own blocks (mirrored halo blocks are read-only)
+            if (shard_owns(P, bx, by, bz) && frustum_intersects_block(P, fc, lo, hi)) {
                 for (int k = 0; k < 9 && !vis; ++k) {
                     const d3 probe = k == 8 ? add(lo, mk(0.5 * side, 0.5 * side, 0.5 * side))
                                             : add(lo, mk(k & 1 ? side : 0.0, k & 2 ? side : 0.0, k & 4 ? side : 0.0));
@@ -1203,7 +1205,7 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 __global__ void k_fuse_finalize(FrameCounters* ctr, const VolCounters* vc) {
-    ctr->alloc_now = vc->allocated_count;
+    ctr->alloc_now = vc->allocated_count - vc->halo_count;
 }
 
 // ---------------------------------------------------------------------------------

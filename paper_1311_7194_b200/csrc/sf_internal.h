@@ -58,7 +58,7 @@ struct VolCounters {
     unsigned long long allocated_count;
     unsigned long long free_top;    // size of the free-list stack
     unsigned long long high_water;  // 1 + highest slot ever handed out
-    unsigned long long pad;
+    unsigned long long halo_count;  // sharded volume: mirrored blocks of other ranks
 };
 
 // Per-frame device counters (zeroed by the frame-setup kernel).

@@ -628,6 +628,59 @@ void launch_ray_bounds(Volume& v, const FrameConsts* d_fc, const Intr& intr, flo
     if (launches) *launches += 1;
 }
 
+// Active-ray list from caller-supplied bounds (raycast(..., bounds), render.hpp:61-63);
+// pixels with empty bounds get the empty raycast result.
+__global__ void k_list_from_bounds(const float* __restrict__ t_start, const float* __restrict__ t_end, int n,
+                                   int* __restrict__ ray_list, RayCounters* list_ctr, float* __restrict__ depth_out,
+                                   float* __restrict__ normals_out) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool act = idx < n && t_start[idx] <= t_end[idx];
+    if (idx < n && !act) {
+        depth_out[idx] = 0.0f;
+        normals_out[3 * idx] = 0.0f;
+        normals_out[3 * idx + 1] = 0.0f;
+        normals_out[3 * idx + 2] = 0.0f;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, act);
+    const int lane = threadIdx.x & 31;
+    unsigned long long base = 0;
+    if (bal) {
+        const int leader = __ffs(bal) - 1;
+        if (lane == leader) base = atomicAdd(&list_ctr->listed, static_cast<unsigned long long>(__popc(bal)));
+        base = __shfl_sync(0xffffffffu, base, leader);
+    }
+    if (act) ray_list[base + __popc(bal & ((1u << lane) - 1u))] = idx;
+}
+
+// Composite of per-rank raycasts (sf_gpu.h): nearest depth wins, a rank with a normal wins
+// ties against one without, then the lower rank.
+__global__ void k_composite_key(const float* __restrict__ depth, const float* __restrict__ normals, uint64_t n,
+                                int rank, long long* __restrict__ key) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float d = depth[i];
+    long long k = 0x7fffffffffffffffLL;
+    if (d > 0.0f) {
+        const bool no_normal = normals[3 * i] == 0.0f && normals[3 * i + 1] == 0.0f && normals[3 * i + 2] == 0.0f;
+        k = (static_cast<long long>(__float_as_uint(d)) << 32) | (static_cast<long long>(no_normal) << 31) |
+            static_cast<long long>(rank);
+    }
+    key[i] = k;
+}
+__global__ void k_composite_select(const long long* __restrict__ key, uint64_t n, int rank, float* __restrict__ depth,
+                                   float* __restrict__ normals) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const long long k = key[i];
+    const bool win = k != 0x7fffffffffffffffLL && static_cast<int>(k & 0x7fffffff) == rank;
+    if (!win) {
+        depth[i] = 0.0f;
+        normals[3 * i] = 0.0f;
+        normals[3 * i + 1] = 0.0f;
+        normals[3 * i + 2] = 0.0f;
+    }
+}
+
 void launch_raycast(Volume& v, const FrameConsts* d_fc, const Intr& intr, const float* t_start, const float* t_end,
                     float* depth, float* normals, RayCounters* d_stats, cudaStream_t s, uint64_t* launches,
                     const int* dead_flag, const int* ray_list) {
@@ -746,6 +799,76 @@ int sf_raycast(sf_volume_t v, const double pose[12], const sf_intrinsics* intr, 
             stats->hit_pixels = c.hit_pixels;
             stats->rays_with_bounds = c.rays_with_bounds;
         }
+        return SF_OK;
+    });
+}
+
+int sf_raycast_with_bounds(sf_volume_t v, const double pose[12], const sf_intrinsics* intr, const float* t_start,
+                           const float* t_end, float* depth, float* normals_xyz, int32_t on_device,
+                           sf_raycast_stats* stats, void* stream) {
+    return guarded([&]() -> int {
+        if (!v || !pose || !intr || !t_start || !t_end || !depth || !normals_xyz)
+            throw Error(SF_INVALID_ARGUMENT, "sf_raycast_with_bounds: null argument");
+        SF_CUDA(cudaSetDevice(v->device));
+        validate_intr(*intr);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        RayScratch& rs = ray_scratch();
+        rs.ensure(intr->width, intr->height);
+        const Intr I = to_intr(*intr);
+        const size_t n = static_cast<size_t>(intr->width) * intr->height;
+        SF_CUDA(cudaMemcpyAsync(rs.pose, pose, 12 * sizeof(double), cudaMemcpyHostToDevice, s));
+        SF_CUDA(cudaMemsetAsync(rs.stats, 0, sizeof(RayCounters), s));
+        launch_consts(v->P, I, rs.pose, rs.fc, s, nullptr);
+        const float* ts = t_start;
+        const float* te = t_end;
+        if (!on_device) {
+            SF_CUDA(cudaMemcpyAsync(rs.ts, t_start, n * sizeof(float), cudaMemcpyHostToDevice, s));
+            SF_CUDA(cudaMemcpyAsync(rs.te, t_end, n * sizeof(float), cudaMemcpyHostToDevice, s));
+            ts = rs.ts;
+            te = rs.te;
+        }
+        float* d = on_device ? depth : rs.depth;
+        float* nm = on_device ? normals_xyz : rs.normals;
+        k_list_from_bounds<<<(int)((n + 255) / 256), 256, 0, s>>>(ts, te, (int)n, rs.list, rs.stats, d, nm);
+        SF_LAUNCH_CHECK();
+        launch_raycast(*v, rs.fc, I, ts, te, d, nm, rs.stats, s, nullptr, nullptr, rs.list);
+        if (!on_device) {
+            SF_CUDA(cudaMemcpyAsync(depth, rs.depth, n * sizeof(float), cudaMemcpyDeviceToHost, s));
+            SF_CUDA(cudaMemcpyAsync(normals_xyz, rs.normals, 3 * n * sizeof(float), cudaMemcpyDeviceToHost, s));
+        }
+        RayCounters c{};
+        SF_CUDA(cudaMemcpyAsync(&c, rs.stats, sizeof(c), cudaMemcpyDeviceToHost, s));
+        SF_CUDA(cudaStreamSynchronize(s));
+        if (stats) {
+            stats->sample_steps = c.sample_steps;
+            stats->hit_pixels = c.hit_pixels;
+            stats->rays_with_bounds = c.rays_with_bounds;
+        }
+        return SF_OK;
+    });
+}
+
+int sf_composite_key(const float* depth, const float* normals_xyz, uint64_t n, int32_t rank, int64_t* key,
+                     void* stream) {
+    return guarded([&]() -> int {
+        if (!depth || !normals_xyz || !key || rank < 0) throw Error(SF_INVALID_ARGUMENT, "sf_composite_key: bad argument");
+        if (n == 0) return SF_OK;
+        k_composite_key<<<(unsigned)((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+            depth, normals_xyz, n, rank, reinterpret_cast<long long*>(key));
+        SF_LAUNCH_CHECK();
+        return SF_OK;
+    });
+}
+
+int sf_composite_select(const int64_t* key, uint64_t n, int32_t rank, float* depth, float* normals_xyz,
+                        void* stream) {
+    return guarded([&]() -> int {
+        if (!depth || !normals_xyz || !key || rank < 0)
+            throw Error(SF_INVALID_ARGUMENT, "sf_composite_select: bad argument");
+        if (n == 0) return SF_OK;
+        k_composite_select<<<(unsigned)((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+            reinterpret_cast<const long long*>(key), n, rank, depth, normals_xyz);
+        SF_LAUNCH_CHECK();
         return SF_OK;
     });
 }

@@ -302,6 +302,9 @@ static VolParams make_params(const sf_grid_config& c, const sf_aux_quant& a, uin
     P.occ_fine_words = (P.table_size + 31) / 32;
     const uint64_t nc = static_cast<uint64_t>(P.Nc);
     P.occ_coarse_words = (nc * nc * nc + 31) / 32;
+    P.shard_rank = 0;
+    P.shard_world = 1;
+    P.shard_shift = 3;
     return P;
 }
 
@@ -417,6 +420,25 @@ int sf_volume_destroy(sf_volume_t vol) {
     volume_free_device(*vol);
     delete vol;
     return SF_OK;
+}
+
+int sf_volume_set_shard(sf_volume_t v, int32_t rank, int32_t world, int32_t brick_shift) {
+    return guarded([&]() -> int {
+        if (!v) throw Error(SF_INVALID_ARGUMENT, "sf_volume_set_shard: null volume");
+        if (world < 1 || rank < 0 || rank >= world || brick_shift < 0 || brick_shift > 16)
+            throw Error(SF_INVALID_ARGUMENT, "sf_volume_set_shard: need 0 <= rank < world, 0 <= brick_shift <= 16");
+        if (v->host_allocated() != 0)
+            throw Error(SF_LOGIC_ERROR, "sf_volume_set_shard: the volume already holds blocks");
+        v->P.shard_rank = rank;
+        v->P.shard_world = world;
+        v->P.shard_shift = brick_shift;
+        return SF_OK;
+    });
+}
+
+int32_t sf_shard_owner(int32_t bx, int32_t by, int32_t bz, int32_t brick_shift, int32_t world) {
+    if (world < 1 || brick_shift < 0 || brick_shift > 16) return -1;
+    return shard_owner(bx, by, bz, brick_shift, world);
 }
 
 int sf_volume_get_info(sf_volume_t v, sf_volume_info* out) {

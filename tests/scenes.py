@@ -56,3 +56,28 @@ def cluster_scene():
     s.add_sphere([0.05, 0.30, 1.10], 0.16)
     s.add_sphere([-0.12, -0.28, 1.05], 0.13)
     return s
+
+
+def c5_scene(center=(0.0, 0.0, 0.0), spacing=0.3, r=0.08, bump=0.024):
+    """C5: a 3x3 grid of C4 bumpy spheres in the x-z plane around `center`, so the blocks of a
+    sharded pool land on every owner."""
+    s = sf.AnalyticScene()
+    o = r / math.sqrt(3.0)
+    for i in (-1, 0, 1):
+        for j in (-1, 0, 1):
+            c = (center[0] + i * spacing, center[1], center[2] + j * spacing)
+            s.add_sphere(list(c), r)
+            for b in range(8):
+                s.add_sphere([c[0] + (o if b & 1 else -o), c[1] + (o if b & 2 else -o),
+                              c[2] + (o if b & 4 else -o)], bump)
+    return s
+
+
+def c5_config(blocks_per_axis=1024, voxel=0.15e-3):
+    """C5: 8192^3 sparse at 0.15 mm (N = 1024, M = 8), box centred on the object grid."""
+    side = blocks_per_axis * 8 * voxel
+    return sf.GridConfig(blocks_per_axis, 8, (-side / 2, -side / 2, -side / 2), side, 0.0)
+
+
+def c5_trajectory(frames=100, radius=0.9):
+    return sf.orbit_trajectory([0.0, 0.0, 0.0], radius, frames, (0.0, 1.0, 0.0), 0.0, 2.0 * math.pi)

@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     text = open(os.path.join(ROOT, "include", "sf_gpu.h")).read()
-    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(sf_[a-z0-9_]+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^(?:int|int32_t|const char\*)\s+(sf_[a-z0-9_]+)\s*\(", text, re.M)))
 
 
 def test_library_exports_every_declared_symbol():

@@ -1,0 +1,119 @@
+"""Sharded block pool emulated as R ranks on one GPU (LocalComm): the same
+phases and reductions the NCCL path runs, checked against the single volume / the oracle."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1311_7194_b200 as sfp
+from paper_1311_7194_b200 import api as sf
+from paper_1311_7194_b200 import shard
+from tests import scenes
+
+pytestmark = pytest.mark.gpu
+
+
+def _frames(be, scene, poses, intr, domain, sigma0=0.0):
+    return [be.render_synthetic_depth(scene, p, intr, sigma0=sigma0, seed=7 + k, domain_size=domain)
+            for k, p in enumerate(poses)]
+
+
+def _small_c5(world):
+    # C5 geometry at 4x the voxel (N = 256): same object grid, fast enough for a test
+    cfg = scenes.c5_config(blocks_per_axis=256, voxel=0.6e-3)
+    shards = [shard.ShardVolume(cfg, 200_000 // world + 20_000, sf.AuxMode.Variance, r, world, p_min=1e-12)
+              for r in range(world)]
+    return cfg, shards
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_integrate_union_equals_oracle(gpu, oracle, world):
+    """Block set and payloads over the union of shards == the reference's single grid, bit-exact."""
+    intr = scenes.camera(160, 120, 131.25)
+    cfg = scenes.c1_config()
+    poses = scenes.c1_trajectory(100)[:6]
+    frames = _frames(gpu, scenes.sphere_plane_scene(), poses, intr, 2.0, sigma0=2.5e-4)
+    fusion = sf.FusionParams(mode=sf.FusionMode.Kalman)
+    shards = [shard.ShardVolume(cfg, 0, sf.AuxMode.Variance, r, world) for r in range(world)]
+    ref = sf.SparseTsdfGrid(cfg, 0, sf.AuxMode.Variance, backend=oracle)
+    for f, p in zip(frames, poses):
+        st = [s.fuse(f, p, fusion) for s in shards]
+        rs = oracle.fuse_frame(ref, f, p, fusion)
+        assert sum(x.voxels_updated for x in st) == rs.voxels_updated
+        assert sum(x.blocks_total for x in st) == rs.blocks_total
+    u = shard.union_blocks([s.grid for s in shards], shards)
+    assert u == shard.union_blocks([ref])
+    owners = {shard.shard_owner((ti % 32, (ti // 32) % 32, ti // 1024), world) for ti in u}
+    assert len(owners) == world  # every rank holds blocks
+    for r, s in enumerate(shards):  # and only its own
+        t = s.grid.read_table()
+        for ti in np.nonzero(t >= 0)[0][:200].tolist():
+            assert shard.shard_owner((ti % 32, (ti // 32) % 32, ti // 1024), world) == r
+
+
+def test_sharded_bounds_and_composite_c5(gpu):
+    """Union of shards == single volume; global bounds and the nearest-depth composite
+    (with mirrored halo blocks) equal the single volume's ray bounds and raycast bit for bit."""
+    world = 3
+    cfg, shards = _small_c5(world)
+    single = sf.SparseTsdfGrid(cfg, 220_000, sf.AuxMode.Variance, p_min=1e-12)
+    intr = scenes.camera(320, 240, 262.5)
+    poses = scenes.c5_trajectory(100, radius=0.9)[:4]
+    frames = _frames(gpu, scenes.c5_scene(), poses, intr, cfg.box_side, sigma0=4e-4)
+    fusion = sf.FusionParams(mode=sf.FusionMode.Kalman)
+    for f, p in zip(frames, poses):
+        for s in shards:
+            s.fuse(f, p, fusion)
+        shard.exchange_halo(shards, shard.LocalComm(world))
+        sfp.fuse_frame(single, f, p, fusion)
+    assert shard.union_blocks([s.grid for s in shards], shards) == shard.union_blocks([single])
+    comm = shard.LocalComm(world)
+    pose = poses[-1]
+    depth, normals, stats, ts, te = shard.sharded_raycast(shards, comm, pose, intr)
+    ts0, te0 = sfp.compute_ray_bounds(single, pose, intr)
+    assert np.array_equal(ts[0].cpu().numpy().view(np.uint32), ts0.view(np.uint32))
+    assert np.array_equal(te[0].cpu().numpy().view(np.uint32), te0.view(np.uint32))
+    for r in range(1, world):  # replicated on every rank
+        assert torch.equal(depth[r], depth[0]) and torch.equal(normals[r], normals[0])
+    d1, n1, st1 = sfp.raycast_result(single, pose, intr)
+    dc = depth[0].cpu().numpy()
+    nc = normals[0].cpu().numpy()
+    hit = d1.depth > 0
+    same = (dc.view(np.uint32) == d1.depth.view(np.uint32))
+    frac_same = same[hit].mean()
+    frac_miss = ((dc == 0) & hit).mean() / max(hit.mean(), 1e-9)
+    both = hit & (dc > 0)
+    err = np.abs(dc - d1.depth)[both].max() if both.any() else 0.0
+    print(f"composite: {hit.sum()} hit px, identical depth {frac_same:.4f}, missing {frac_miss:.4f}, "
+          f"max |dz| where both hit {err:.3e} m (voxel {cfg.voxel_size:.1e})")
+    assert hit.sum() > 1000
+    # with the halo exchange the composite is the single-volume raycast, bit for bit
+    assert np.array_equal(dc.view(np.uint32), d1.depth.view(np.uint32))
+    assert np.array_equal(nc.view(np.uint32), n1.array.view(np.uint32))
+
+
+def test_sharded_tracker_follows_single(gpu):
+    """run() over 3 shards (icp_with_hook) reproduces the single-volume tracker exactly."""
+    world = 3
+    cfg, shards = _small_c5(world)
+    intr = scenes.camera(320, 240, 262.5)
+    traj = scenes.c5_trajectory(100, radius=0.9)[:6]
+    frames = _frames(gpu, scenes.c5_scene(), traj, intr, cfg.box_side, sigma0=4e-4)
+    fusion = sf.FusionParams(mode=sf.FusionMode.Kalman)
+    match = sf.MatchParams.for_voxel_size(cfg.voxel_size)
+    tr = shard.ShardedTracker(shards, shard.LocalComm(world), intr, fusion, match, traj[0])
+    single = sf.SparseTsdfGrid(cfg, 220_000, sf.AuxMode.Variance, p_min=1e-12)
+    str_ = sf.Tracker(single, intr, fusion, match, traj[0])
+    for k, f in enumerate(frames):
+        ext = sf.compose(sf.invert(traj[k - 1]), traj[k]) if k else None
+        m = tr.step(f, external=ext)
+        if k == 0:
+            str_.step(f, sf.Tracker.TRACK)
+        else:
+            str_.step(f, sf.Tracker.TRACK_WITH_HOOK, ext)
+        ms = str_.fetch()
+        dp = max(np.abs(m.pose.rotation - ms.pose.rotation).max(), np.abs(m.pose.translation - ms.pose.translation).max())
+        print(f"frame {k}: registered={m.registered} it={m.iterations} matches={m.matches} vs {ms.matches} "
+              f"pose diff {dp:.2e}, blocks {m.blocks_total} vs {ms.fusion.blocks_total}")
+        assert dp == 0.0 and m.matches == ms.matches and m.blocks_total == ms.fusion.blocks_total
