@@ -168,6 +168,8 @@ class ShardVolume:
 
 def exchange_halo(shards: List[ShardVolume], comm):
     """After an integrate on every local rank: mirror the blocks bordering each rank's bricks."""
+    if comm.world <= 1:
+        return
     recs = [s.pack_halo() for s in shards]
     for s, incoming in zip(shards, comm.exchange(recs)):
         for keys, pays, count in incoming:
