@@ -96,8 +96,110 @@ __device__ __noinline__ void solve_finalize(IcpState* st, const double* s_sum, c
     st->motion_r = r;
     st->motion_t = t;
     st->delta = apply_motion_fast(st->delta, r, t);
+    st->eig_pending = 0;  // eigenpairs computed by this path
     st->iterations = iter + 1;
     if (st->shrunk_norm < prm.eps) st->done = 1;
+}
+
+// Fast path of solve_gated (registration.cpp:175-193). When every eigenvalue of A passes the
+// gate lambda_i / N > theta, the gated solution sum_i v_i (v_i . b) / lambda_i is A^-1 b. A
+// Cholesky factorisation of A - c I succeeding certifies lambda_min(A) > c - |E| (backward
+// stability, |E| <= 7 eps |A|_F); c = theta N (1 + 1e-9) + 64 eps |A|_F leaves room for the
+// reference's own eigenvalue rounding, so the reference gates every direction in too. Then
+// x = A^-1 b by a second Cholesky (same solution up to rounding). Returns false (Jacobi path)
+// otherwise. One thread.
+__device__ __noinline__ bool fast_gated_solve(const double* s_fin, double n_pairs, double theta, double* x) {
+    double A[6][6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+        for (int j = i; j < 6; ++j) A[i][j] = A[j][i] = s_fin[i * 6 - i * (i - 1) / 2 + (j - i)];
+    double fro = 0.0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+        for (int j = 0; j < 6; ++j) fro += A[i][j] * A[i][j];
+    fro = sqrt(fro);
+    const double shift = theta * n_pairs * (1.0 + 1e-9) + 64.0 * 2.220446049250313e-16 * fro;
+    double L[6][6];
+    for (int pass = 0; pass < 2; ++pass) {
+        const double sh = pass == 0 ? shift : 0.0;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+            double s = A[j][j] - sh;
+#pragma unroll
+            for (int k = 0; k < j; ++k) s -= L[j][k] * L[j][k];
+            if (!(s > 0.0)) return false;
+            const double d = sqrt(s), inv = 1.0 / d;
+            L[j][j] = d;
+#pragma unroll
+            for (int i = j + 1; i < 6; ++i) {
+                double t = A[i][j];
+#pragma unroll
+                for (int k = 0; k < j; ++k) t -= L[i][k] * L[j][k];
+                L[i][j] = t * inv;
+            }
+        }
+    }
+    double y[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {  // L y = b
+        double t = s_fin[21 + i];
+#pragma unroll
+        for (int k = 0; k < i; ++k) t -= L[i][k] * y[k];
+        y[i] = t / L[i][i];
+    }
+#pragma unroll
+    for (int i = 5; i >= 0; --i) {  // L^T x = y
+        double t = y[i];
+#pragma unroll
+        for (int k = i + 1; k < 6; ++k) t -= L[k][i] * x[k];
+        x[i] = t / L[i][i];
+    }
+    return true;
+}
+
+// Gated solution x (fast path) -> the rest of solve_gated + apply_motion + convergence.
+__device__ __noinline__ void finalize_motion(IcpState* st, const double* s_fin, const double* x, const IcpParamsDev& prm) {
+    const int iter = st->iterations;
+    const unsigned long long cnt = st->cur_count;
+    st->pair_count = cnt;
+    st->residual_rms = sqrt(dmax(0.0, s_fin[27]) / static_cast<double>(cnt));
+    for (int i = 0; i < 6; ++i) st->gated[i] = 1;
+    for (int i = 0; i < 21; ++i) st->A_last[i] = s_fin[i];
+    st->eig_pending = 1;
+    double xn = x[0] * x[0];
+#pragma unroll
+    for (int r = 1; r < 6; ++r) xn = xn + x[r] * x[r];
+    st->shrunk_norm = sqrt(xn);
+    const d3 s = st->scale, c = st->center;
+    const d3 r = mk((1.0 / s.x) * x[0], (1.0 / s.y) * x[1], (1.0 / s.z) * x[2]);
+    const d3 t = sub(mk(x[3], x[4], x[5]), cross(r, c));
+    st->motion_r = r;
+    st->motion_t = t;
+    st->delta = apply_motion_fast(st->delta, r, t);
+    st->iterations = iter + 1;
+    if (st->shrunk_norm < prm.eps) st->done = 1;
+}
+
+// Deferred eigendecomposition of the last iteration's normal matrix (GatedSolution
+// eigenvalues / eigenvectors for IcpResult and the frame metrics). One warp.
+__global__ void k_icp_report(IcpState* st) {
+    if (!st->eig_pending) return;
+    __shared__ double s_A[36];
+    __shared__ Eig6 s_eig;
+    const int lane = threadIdx.x & 31;
+    for (int i = lane; i < 36; i += 32) {
+        const int r = i / 6, c = i % 6;
+        const int a = r <= c ? r : c, b = r <= c ? c : r;
+        s_A[i] = st->A_last[a * 6 - a * (a - 1) / 2 + (b - a)];
+    }
+    __syncwarp();
+    eigendecompose_sym6_warp_rr(s_A, &s_eig);
+    __syncwarp();
+    if (lane < 6) st->eigenvalues[lane] = s_eig.values[lane];
+    for (int i = lane; i < 36; i += 32) st->eigenvectors[i] = s_eig.vectors[i];
+    if (lane == 0) st->eig_pending = 0;
 }
 
 constexpr int kStepCtas = 148;  // one CTA per SM (double-double accumulators); fixed => deterministic
@@ -298,7 +400,7 @@ __global__ void __launch_bounds__(kIcpThreads, 1)
             }
         }
     }
-    constexpr int L = kMergeLanes, kBatch = 8;
+    constexpr int L = kMergeLanes, kBatch = (kStepCtas + kMergeLanes - 1) / kMergeLanes;  // one L2 round trip
     __shared__ DD s_m[kSums][L];
     __shared__ double s_sum[kSums], s_fin[kSums];
     if (tid < kSums * L) {
@@ -396,6 +498,19 @@ __global__ void __launch_bounds__(kIcpThreads, 1)
         s_fin[27] = s_sum[27];
     }
     __syncwarp();
+    __shared__ int s_fast;
+    if (lane == 0) {
+        double x[6];
+        s_fast = fast_gated_solve(s_fin, static_cast<double>(st->cur_count), prm.theta, x) ? 1 : 0;
+        if (s_fast) {
+            finalize_motion(st, s_fin, x, prm);
+            *counter = 0;
+            if constexpr (COND)
+                cudaGraphSetConditional(cond, (!st->done && st->iterations < prm.max_iterations) ? 1u : 0u);
+        }
+    }
+    __syncwarp();
+    if (s_fast) return;
     __shared__ double s_A[36];
     __shared__ Eig6 s_eig;
     for (int i = lane; i < 36; i += 32) {
@@ -492,6 +607,12 @@ void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* 
     SF_CUDA(ee);
 }
 
+void launch_icp_report(IcpWork& wk, cudaStream_t s, uint64_t* launches) {
+    k_icp_report<<<1, 32, 0, s>>>(wk.st);
+    SF_LAUNCH_CHECK();
+    if (launches) *launches += 1;
+}
+
 void fill_icp_result(const IcpState& st, sf_icp_result* out) {
     memset(out, 0, sizeof(*out));
     pose_to12(st.delta, out->delta);
@@ -556,6 +677,7 @@ extern "C" int sf_icp(const sf_frame* source, const float* source_normals, const
         SF_CUDA(cudaMemcpyAsync(wk.initial, initial, 12 * sizeof(double), cudaMemcpyHostToDevice, s));
         const IcpParamsDev prm = make_icp_params(*params);
         launch_icp(wk, d_src, d_sn, d_tgt, d_tn, SI, TI, wk.initial, prm, s, nullptr, nullptr);
+        launch_icp_report(wk, s, nullptr);
         IcpState hs;
         SF_CUDA(cudaMemcpyAsync(&hs, wk.st, sizeof(hs), cudaMemcpyDeviceToHost, s));
         SF_CUDA(cudaStreamSynchronize(s));

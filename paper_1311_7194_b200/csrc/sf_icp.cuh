@@ -44,6 +44,10 @@ struct IcpState {
     double residual_rms, shrunk_norm;
     unsigned long long pair_count;
     d3 motion_r, motion_t;
+    // Fast gated solve (every eigenvalue certified above the gate): the eigendecomposition of
+    // the last iteration's normal matrix is deferred to k_icp_report (off the critical path).
+    int eig_pending;
+    double A_last[21];  // packed upper triangle of the last iteration's (shrunk) normal matrix
 };
 
 struct IcpParamsDev {
@@ -107,5 +111,7 @@ void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* 
                 const Intr& si, const Intr& ti, const double* d_initial, const IcpParamsDev& prm, cudaStream_t s,
                 uint64_t* launches, const int* dead, bool* device_loop = nullptr);
 void fill_icp_result(const IcpState& st, sf_icp_result* out);
+// Eigenpairs of the last iteration when the fast gated solve deferred them (one warp).
+void launch_icp_report(IcpWork& wk, cudaStream_t s, uint64_t* launches);
 
 }  // namespace sf

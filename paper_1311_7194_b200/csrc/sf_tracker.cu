@@ -105,6 +105,8 @@ struct sf_tracker {
     bool last_registered = false;
     uint64_t last_launches = 0;
     cudaStream_t capture_stream = nullptr;  // graphs are captured here (the legacy stream cannot capture)
+    cudaStream_t side_stream = nullptr;     // graph branch: deferred ICP eigenpairs, parallel to the fuse
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // stage timing (graph nodes)
     cudaGraphExec_t graph[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};  // [mode][sigma]
     uint64_t graph_kernels[3][2] = {{0, 0}, {0, 0}, {0, 0}};
@@ -132,6 +134,9 @@ struct sf_tracker {
             if (q) cudaFree(q);
         if (h) cudaFreeHost(h);
         if (capture_stream) cudaStreamDestroy(capture_stream);
+        if (side_stream) cudaStreamDestroy(side_stream);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
         for (auto e : ev)
             if (e) cudaEventDestroy(e);
     }
@@ -144,6 +149,7 @@ struct sf_tracker {
         const float* sig = has_sigma ? d_cap_sigma : nullptr;
         record_event(ev[0], s);
         issue_icp_loop = false;
+        bool joined = true;
         if (mode == 0 || mode == 3) {
             k_tracker_begin_track<<<1, 1, 0, s>>>(d_cur, mode == 3 ? d_gt : nullptr, d_init_delta, d_rstats, d_td);
             SF_LAUNCH_CHECK();
@@ -161,6 +167,12 @@ struct sf_tracker {
             k_tracker_after_icp<<<1, 1, 0, s>>>(d_cur, fb.pose, icp.st, d_td, cfg.orthonormalize);
             SF_LAUNCH_CHECK();
             ++n;
+            // the deferred eigenpairs of the last ICP iteration run beside the fuse
+            SF_CUDA(cudaEventRecord(ev_fork, s));
+            SF_CUDA(cudaStreamWaitEvent(side_stream, ev_fork, 0));
+            launch_icp_report(icp, side_stream, &n);
+            SF_CUDA(cudaEventRecord(ev_join, side_stream));
+            joined = false;
             record_event(ev[2], s);
         } else {
             k_tracker_begin_gt<<<1, 1, 0, s>>>(d_gt, d_cur, fb.pose, d_rstats, d_td, mode == 1 ? 1 : 0);
@@ -173,6 +185,10 @@ struct sf_tracker {
         fe.before_integrate = ev[3];
         fe.after_integrate = ev[4];
         launch_fuse(*vol, fb, cam, d_cap, sig, p, s, false, &n, dead, &fe);
+        if (!joined) {
+            SF_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+            joined = true;
+        }
         k_tracker_finish<<<1, 1, 0, s>>>(fb.ctr, d_td);
         SF_LAUNCH_CHECK();
         ++n;
@@ -218,6 +234,9 @@ int sf_tracker_create(sf_volume_t vol, const sf_tracker_config* config, const do
         SF_CUDA(cudaMemcpy(t->d_cur, initial_pose, 12 * sizeof(double), cudaMemcpyHostToDevice));
         SF_CUDA(cudaMallocHost(&t->h, sizeof(sf_tracker::Fetch)));
         for (auto& e : t->ev) SF_CUDA(cudaEventCreate(&e));
+        SF_CUDA(cudaStreamCreateWithFlags(&t->side_stream, cudaStreamNonBlocking));
+        SF_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
+        SF_CUDA(cudaEventCreateWithFlags(&t->ev_join, cudaEventDisableTiming));
         std::memset(t->h, 0, sizeof(sf_tracker::Fetch));
         *out = t.release();
         return SF_OK;
