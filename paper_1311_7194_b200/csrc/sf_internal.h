@@ -157,7 +157,13 @@ void ensure_frame_buffers(Volume& v, FrameBuffers& fb, int w, int h);
 // the launched kernels into no-ops when set (tracker after TrackingLost / PoolExhausted).
 struct RayCounters {
     unsigned long long sample_steps, hit_pixels, rays_with_bounds;
-    unsigned long long listed;  // length of the active-ray list written by the ray-bounds pass
+    unsigned long long listed;    // length of the active-ray list written by the ray-bounds pass
+    unsigned long long brackets;  // rays the stage-1 march bracketed (refine-pass list length)
+};
+// A stage-1 bracket [a, b] with TSDF values (va > 0 > vb) of pixel idx (render.cpp:207-208).
+struct RayBracket {
+    double a, b, va, vb;
+    int idx, pad;
 };
 void launch_consts(const VolParams& P, const Intr& intr, const double* d_pose, FrameConsts* d_fc, cudaStream_t s,
                    uint64_t* launches);
@@ -177,7 +183,7 @@ void launch_ray_bounds(Volume& v, const FrameConsts* d_fc, const Intr& intr, flo
 // Marches the rays of ray_list (from launch_ray_bounds; length in d_stats->listed).
 void launch_raycast(Volume& v, const FrameConsts* d_fc, const Intr& intr, const float* t_start, const float* t_end,
                     float* depth, float* normals, RayCounters* d_stats, cudaStream_t s, uint64_t* launches,
-                    const int* dead_flag, const int* ray_list);
+                    const int* dead_flag, const int* ray_list, RayBracket* brackets);
 void launch_compute_normals(const float* depth, int w, int h, const Intr& intr, double sigma0,
                             double spatial_scale, float* normals, cudaStream_t s, uint64_t* launches,
                             const int* dead_flag);

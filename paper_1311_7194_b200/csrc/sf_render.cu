@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(256, 3)
               const uint16_t* __restrict__ payload, const uint32_t* __restrict__ occ, const AuxTables* __restrict__ aux,
               const float* __restrict__ t_start, const float* __restrict__ t_end, float* __restrict__ depth_out,
               float* __restrict__ normals_out, RayCounters* stats, int w, int h, const int* dead,
-              const int* __restrict__ ray_list) {
+              const int* __restrict__ ray_list, RayBracket* __restrict__ brackets) {
     static_assert(G >= 8 && G <= 32 && (G & (G - 1)) == 0, "group of 8..32 lanes");
     (void)h;
     constexpr int kRaysPerCta = 256 / G;
@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(256, 3)
     const int g = lane & (G - 1);
     const int gbase = lane & ~(G - 1);
     const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << gbase;
-    unsigned long long steps = 0, hits = 0, with_bounds = 0;
+    unsigned long long steps = 0, with_bounds = 0;
     auto group_bits = [&](bool pred) { return (__ballot_sync(gmask, pred) & gmask) >> gbase; };
     const unsigned long long n_rays = stats->listed;
     for (unsigned long long r = (unsigned long long)blockIdx.x * kRaysPerCta + threadIdx.x / G; r < n_rays;
@@ -475,6 +475,8 @@ __global__ void __launch_bounds__(256, 3)
         const int idx = ray_list[r];
         const int u = idx % w, v = idx / w;
         float out_d = 0.0f, nx = 0.f, ny = 0.f, nz = 0.f;
+        bool bracket_out = false;
+        RayBracket br{};
         const float fs = t_start[idx], fe = t_end[idx];
         if (fs <= fe) {  // !bounds.empty(u, v)
             with_bounds += 1;
@@ -538,81 +540,117 @@ __global__ void __launch_bounds__(256, 3)
                 }
                 t_base = __shfl_sync(gmask, t, G - 1, G) + coarse_step;
             }
-            if (bracketed) {
-                double root = hit_b;
-                for (int iter = 0; iter < 48 && hit_b - hit_a > fine_tol; ++iter) {
-                    double t_new = hit_b - val_b * (hit_b - hit_a) / (val_b - val_a);
-                    if (!(t_new > hit_a) || !(t_new < hit_b)) t_new = 0.5 * (hit_a + hit_b);
-                    double val;
-                    if (!S.sample(add(pose.t, scale(t_new, dir)), val)) {
-                        hit_a = t_new;
-                        val_a = dmax(val_a, 1e-12);
-                        continue;
-                    }
-                    if (val > 0.0) {
-                        hit_a = t_new;
-                        val_a = val;
-                    } else {
-                        hit_b = t_new;
-                        val_b = val;
-                    }
-                }
-                if (val_b != val_a) {
-                    const double interp = hit_b - val_b * (hit_b - hit_a) / (val_b - val_a);
-                    root = dclamp(interp, hit_a, hit_b);
-                } else {
-                    root = 0.5 * (hit_a + hit_b);
-                }
-                const double dd = root * dir_cam.z;
-                if (!(dd < intr.near_plane || dd > intr.far_plane)) {
-                    out_d = (float)dd;
-                    hits += 1;
-                    // sample_tsdf_gradient (render.cpp:50-63): lane a < 6 takes p +- h e_(a/2)
-                    const d3 p = add(pose.t, scale(root, dir));
-                    const double hh = (g & 1) ? -vox : vox;
-                    d3 q = p;
-                    if (g < 2) q = mk(p.x + hh, p.y, p.z);
-                    else if (g < 4) q = mk(p.x, p.y + hh, p.z);
-                    else q = mk(p.x, p.y, p.z + hh);
-                    double sv = 0.0;
-                    const bool sok = g < 6 && S.sample(q, sv);
-                    const unsigned okm = group_bits(sok);
-                    double s6[6];
-#pragma unroll
-                    for (int a = 0; a < 6; ++a) s6[a] = __shfl_sync(gmask, sv, a, G);
-                    if (okm == 0x3fu) {
-                        const d3 gr = mk((s6[0] - s6[1]) / (2.0 * vox), (s6[2] - s6[3]) / (2.0 * vox),
-                                         (s6[4] - s6[5]) / (2.0 * vox));
-                        if (sqnorm(gr) > 0.0) {
-                            // world_to_cam * grad.normalized()  (render.cpp:242-245)
-                            const d3 n_cam = mv(mt(pose.R), normalized(gr));
-                            nx = (float)n_cam.x;
-                            ny = (float)n_cam.y;
-                            nz = (float)n_cam.z;
-                        }
-                    }
-                }
+            if (bracketed && g == 0) {
+                bracket_out = true;
+                br = RayBracket{hit_a, hit_b, val_a, val_b, idx, 0};
             }
         }
-        if (g == 0) {
+        // Rays with a bracket go to the one-thread-per-ray refine pass (stage 2 + normal);
+        // the others get the empty result here.
+        const unsigned am = __activemask();
+        const unsigned bal = __ballot_sync(am, bracket_out);
+        unsigned long long base = 0;
+        if (bal) {
+            const int leader = __ffs(bal) - 1;
+            if (lane == leader) base = atomicAdd(&stats->brackets, static_cast<unsigned long long>(__popc(bal)));
+            base = __shfl_sync(am, base, leader);
+        }
+        if (bracket_out) {
+            brackets[base + __popc(bal & ((1u << lane) - 1u))] = br;
+        } else if (g == 0) {
             depth_out[idx] = out_d;
             normals_out[3 * idx] = nx;
             normals_out[3 * idx + 1] = ny;
             normals_out[3 * idx + 2] = nz;
         }
     }
-    if (g != 0) steps = hits = with_bounds = 0;  // per-ray values are replicated in the group
+    if (g != 0) steps = with_bounds = 0;  // per-ray values are replicated in the group
     // RaycastStats: warp reduction, one atomic per warp and counter.
     for (int off = 16; off > 0; off >>= 1) {
         steps += __shfl_down_sync(0xffffffffu, steps, off);
-        hits += __shfl_down_sync(0xffffffffu, hits, off);
         with_bounds += __shfl_down_sync(0xffffffffu, with_bounds, off);
     }
     if (lane == 0 && stats) {
         if (steps) atomicAdd(&stats->sample_steps, steps);
-        if (hits) atomicAdd(&stats->hit_pixels, hits);
         if (with_bounds) atomicAdd(&stats->rays_with_bounds, with_bounds);
     }
+}
+
+// Stage 2 (secant / bisection to 0.01 voxel, render.cpp:209-233) and the gradient normal
+// (render.cpp:236-246) for every bracketed ray: one thread per ray (the sequential secant
+// iterations have no parallelism within a ray; the six gradient samples are independent).
+__global__ void __launch_bounds__(256)
+    k_raycast_refine(VolParams P, const FrameConsts* __restrict__ fc, const int32_t* __restrict__ table,
+                     const uint16_t* __restrict__ payload, const uint32_t* __restrict__ occ,
+                     const AuxTables* __restrict__ aux, const RayBracket* __restrict__ brackets,
+                     float* __restrict__ depth_out, float* __restrict__ normals_out, RayCounters* stats, int w,
+                     const int* dead) {
+    __shared__ double s_tdec[256];
+    if (dead && *dead) return;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_tdec[i] = aux->tsdf_decode[i];
+    __syncthreads();
+    const Sampler S{P, table, payload, occ, s_tdec};
+    const Intr& intr = fc->intr;
+    const Pose& pose = fc->pose;
+    const double vox = P.voxel;
+    const double fine_tol = 0.01 * vox;
+    const unsigned long long n = stats->brackets;
+    unsigned long long hits = 0;
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const RayBracket b = brackets[i];
+        const int idx = b.idx;
+        const int u = idx % w, v = idx / w;
+        const d3 dir_cam = normalized(unproject(intr, u, v, 1.0));
+        const d3 dir = mv(pose.R, dir_cam);
+        double hit_a = b.a, hit_b = b.b, val_a = b.va, val_b = b.vb;
+        float out_d = 0.0f, nx = 0.f, ny = 0.f, nz = 0.f;
+        for (int iter = 0; iter < 48 && hit_b - hit_a > fine_tol; ++iter) {
+            double t_new = hit_b - val_b * (hit_b - hit_a) / (val_b - val_a);
+            if (!(t_new > hit_a) || !(t_new < hit_b)) t_new = 0.5 * (hit_a + hit_b);
+            double val;
+            if (!S.sample(add(pose.t, scale(t_new, dir)), val)) {
+                hit_a = t_new;
+                val_a = dmax(val_a, 1e-12);
+                continue;
+            }
+            if (val > 0.0) {
+                hit_a = t_new;
+                val_a = val;
+            } else {
+                hit_b = t_new;
+                val_b = val;
+            }
+        }
+        double root;
+        if (val_b != val_a) {
+            const double interp = hit_b - val_b * (hit_b - hit_a) / (val_b - val_a);
+            root = dclamp(interp, hit_a, hit_b);
+        } else {
+            root = 0.5 * (hit_a + hit_b);
+        }
+        const double dd = root * dir_cam.z;
+        if (!(dd < intr.near_plane || dd > intr.far_plane)) {
+            out_d = (float)dd;
+            hits += 1;
+            // sample_tsdf_gradient (render.cpp:50-63)
+            const d3 p = add(pose.t, scale(root, dir));
+            d3 gr;
+            if (S.gradient(p, vox, gr) && sqnorm(gr) > 0.0) {
+                // world_to_cam * grad.normalized()  (render.cpp:242-245)
+                const d3 n_cam = mv(mt(pose.R), normalized(gr));
+                nx = (float)n_cam.x;
+                ny = (float)n_cam.y;
+                nz = (float)n_cam.z;
+            }
+        }
+        depth_out[idx] = out_d;
+        normals_out[3 * idx] = nx;
+        normals_out[3 * idx + 1] = ny;
+        normals_out[3 * idx + 2] = nz;
+    }
+    for (int off = 16; off > 0; off >>= 1) hits += __shfl_down_sync(0xffffffffu, hits, off);
+    if ((threadIdx.x & 31) == 0 && hits) atomicAdd(&stats->hit_pixels, hits);
 }
 
 void launch_ray_bounds(Volume& v, const FrameConsts* d_fc, const Intr& intr, float* t_start, float* t_end,
@@ -683,13 +721,16 @@ __global__ void k_composite_select(const long long* __restrict__ key, uint64_t n
 
 void launch_raycast(Volume& v, const FrameConsts* d_fc, const Intr& intr, const float* t_start, const float* t_end,
                     float* depth, float* normals, RayCounters* d_stats, cudaStream_t s, uint64_t* launches,
-                    const int* dead_flag, const int* ray_list) {
+                    const int* dead_flag, const int* ray_list, RayBracket* brackets) {
     constexpr int G = 8;  // lanes per ray: 32 rays per 256-thread CTA, persistent over the list
     const dim3 blk(256), grd(148 * 3);
     k_raycast<G><<<grd, blk, 0, s>>>(v.P, d_fc, v.d_table, v.d_payload, v.d_occ, v.d_aux, t_start, t_end, depth, normals,
-                                     d_stats, intr.w, intr.h, dead_flag, ray_list);
+                                     d_stats, intr.w, intr.h, dead_flag, ray_list, brackets);
     SF_LAUNCH_CHECK();
-    if (launches) *launches += 1;
+    k_raycast_refine<<<148 * 4, 256, 0, s>>>(v.P, d_fc, v.d_table, v.d_payload, v.d_occ, v.d_aux, brackets, depth,
+                                             normals, d_stats, intr.w, dead_flag);
+    SF_LAUNCH_CHECK();
+    if (launches) *launches += 2;
 }
 
 // Scratch for the stand-alone raycast API.
@@ -697,6 +738,7 @@ struct RayScratch {
     int w = 0, h = 0;
     float *ts = nullptr, *te = nullptr, *depth = nullptr, *normals = nullptr;
     int* list = nullptr;
+    RayBracket* brackets = nullptr;
     FrameConsts* fc = nullptr;
     double* pose = nullptr;
     RayCounters* stats = nullptr;
@@ -712,15 +754,17 @@ struct RayScratch {
         SF_CUDA(cudaMalloc(&pose, 12 * sizeof(double)));
         SF_CUDA(cudaMalloc(&stats, sizeof(RayCounters)));
         SF_CUDA(cudaMalloc(&list, n * sizeof(int)));
+        SF_CUDA(cudaMalloc(&brackets, n * sizeof(RayBracket)));
         w = W;
         h = H;
     }
     void release() {
-        void* p[] = {ts, te, depth, normals, fc, pose, stats, list};
+        void* p[] = {ts, te, depth, normals, fc, pose, stats, list, brackets};
         for (void* q : p)
             if (q) cudaFree(q);
         ts = te = depth = normals = nullptr;
         list = nullptr;
+        brackets = nullptr;
         fc = nullptr;
         pose = nullptr;
         stats = nullptr;
@@ -785,7 +829,7 @@ int sf_raycast(sf_volume_t v, const double pose[12], const sf_intrinsics* intr, 
         float* d = out_on_device ? depth : rs.depth;
         float* nm = out_on_device ? normals_xyz : rs.normals;
         launch_ray_bounds(*v, rs.fc, I, rs.ts, rs.te, s, nullptr, nullptr, rs.list, rs.stats, d, nm);
-        launch_raycast(*v, rs.fc, I, rs.ts, rs.te, d, nm, rs.stats, s, nullptr, nullptr, rs.list);
+        launch_raycast(*v, rs.fc, I, rs.ts, rs.te, d, nm, rs.stats, s, nullptr, nullptr, rs.list, rs.brackets);
         const size_t n = static_cast<size_t>(intr->width) * intr->height;
         if (!out_on_device) {
             SF_CUDA(cudaMemcpyAsync(depth, rs.depth, n * sizeof(float), cudaMemcpyDeviceToHost, s));
@@ -831,7 +875,7 @@ int sf_raycast_with_bounds(sf_volume_t v, const double pose[12], const sf_intrin
         float* nm = on_device ? normals_xyz : rs.normals;
         k_list_from_bounds<<<(int)((n + 255) / 256), 256, 0, s>>>(ts, te, (int)n, rs.list, rs.stats, d, nm);
         SF_LAUNCH_CHECK();
-        launch_raycast(*v, rs.fc, I, ts, te, d, nm, rs.stats, s, nullptr, nullptr, rs.list);
+        launch_raycast(*v, rs.fc, I, ts, te, d, nm, rs.stats, s, nullptr, nullptr, rs.list, rs.brackets);
         if (!on_device) {
             SF_CUDA(cudaMemcpyAsync(depth, rs.depth, n * sizeof(float), cudaMemcpyDeviceToHost, s));
             SF_CUDA(cudaMemcpyAsync(normals_xyz, rs.normals, 3 * n * sizeof(float), cudaMemcpyDeviceToHost, s));

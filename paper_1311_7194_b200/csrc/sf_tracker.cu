@@ -98,6 +98,7 @@ struct sf_tracker {
     float *d_cap = nullptr, *d_cap_sigma = nullptr;
     RayCounters* d_rstats = nullptr;
     int* d_ray_list = nullptr;  // active rays of the model raycast
+    RayBracket* d_brackets = nullptr;  // stage-1 brackets (refine pass)
     TrackerDev* d_td = nullptr;
     // host-side
     int frames = 0;
@@ -129,7 +130,7 @@ struct sf_tracker {
             for (auto& g : row)
                 if (g) cudaGraphExecDestroy(g);
         void* p[] = {d_cur, d_init_delta, d_gt, d_rc_fc, d_ts, d_te, d_model_depth, d_model_normals, d_cap,
-                     d_cap_sigma, d_rstats, d_td, d_ray_list};
+                     d_cap_sigma, d_rstats, d_td, d_ray_list, d_brackets};
         for (void* q : p)
             if (q) cudaFree(q);
         if (h) cudaFreeHost(h);
@@ -158,7 +159,7 @@ struct sf_tracker {
             launch_ray_bounds(*vol, d_rc_fc, cam, d_ts, d_te, s, &n, dead, d_ray_list, d_rstats, d_model_depth,
                               d_model_normals);
             launch_raycast(*vol, d_rc_fc, cam, d_ts, d_te, d_model_depth, d_model_normals, d_rstats, s, &n, dead,
-                           d_ray_list);
+                           d_ray_list, d_brackets);
             record_event(ev[1], s);
             launch_compute_normals(d_cap, cam.w, cam.h, cam, cfg.match.normal_sigma0, cfg.match.normal_spatial_scale,
                                    icp.src_normals, s, &n, dead);
@@ -228,6 +229,7 @@ int sf_tracker_create(sf_volume_t vol, const sf_tracker_config* config, const do
         SF_CUDA(cudaMalloc(&t->d_cap_sigma, n * sizeof(float)));
         SF_CUDA(cudaMalloc(&t->d_rstats, sizeof(RayCounters)));
         SF_CUDA(cudaMalloc(&t->d_ray_list, n * sizeof(int)));
+        SF_CUDA(cudaMalloc(&t->d_brackets, n * sizeof(RayBracket)));
         SF_CUDA(cudaMalloc(&t->d_td, sizeof(TrackerDev)));
         SF_CUDA(cudaMemset(t->d_td, 0, sizeof(TrackerDev)));
         SF_CUDA(cudaMemset(t->d_rstats, 0, sizeof(RayCounters)));
