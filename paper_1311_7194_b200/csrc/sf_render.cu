@@ -141,8 +141,12 @@ __global__ void __launch_bounds__(256, 3) k_ray_bounds(VolParams P, const FrameC
         for (int i = tid; i < cwords; i += blockDim.x * blockDim.y) s_coarse[i] = __ldg(&occ[P.occ_fine_words + i]);
         __syncthreads();
     }
-    const int u = blockIdx.x * blockDim.x + threadIdx.x;
-    const int v = blockIdx.y * blockDim.y + threadIdx.y;
+    // Each warp takes an 8x4 pixel patch of the CTA's 32x8 tile (rather than a 32x1 row):
+    // neighbouring rays have similar DDA lengths, so fewer lanes idle in the step loop.
+    const int tl = threadIdx.y * blockDim.x + threadIdx.x;
+    const int wp = tl >> 5, ln = tl & 31;
+    const int u = blockIdx.x * blockDim.x + (wp & 3) * 8 + (ln & 7);
+    const int v = blockIdx.y * blockDim.y + (wp >> 2) * 4 + (ln >> 3);
     if (u >= w || v >= h) return;
     const size_t idx = (size_t)v * w + u;
     float ts = INFINITY, te = -INFINITY;
