@@ -431,6 +431,79 @@ struct Sampler {
         return true;
     }
 
+    // sample() for the refinement near a known surface: no occupancy early-out (the table is
+    // authoritative: same result), and the slot of the last single-block sample is cached, so
+    // successive samples in the same block cost one L1-resident payload read.
+    __device__ bool sample_near(d3 p, double& out, int64_t& ckey, int32_t& cslot) const {
+        if (P.mshift < 0) return sample(p, out);
+        const double gx = div_voxel(p.x - P.ox) - 0.5;
+        const double gy = div_voxel(p.y - P.oy) - 0.5;
+        const double gz = div_voxel(p.z - P.oz) - 0.5;
+        constexpr double kLim = 1073741824.0;
+        if (!(fabs(gx) < kLim && fabs(gy) < kLim && fabs(gz) < kLim)) return false;
+        int bx, by, bz;
+        const double flx = floor_exact(gx, bx), fly = floor_exact(gy, by), flz = floor_exact(gz, bz);
+        const int res = P.res;
+        if (bx < 0 || by < 0 || bz < 0 || bx + 1 >= res || by + 1 >= res || bz + 1 >= res) return false;
+        const double fx = gx - flx, fy = gy - fly, fz = gz - flz;
+        const int ms = P.mshift, mm = P.M - 1, N = P.N;
+        const int lx = bx & mm, ly = by & mm, lz = bz & mm;
+        uint16_t pl[8];
+        if (lx != mm && ly != mm && lz != mm) {
+            const int64_t key = ((int64_t)(bz >> ms) * N + (by >> ms)) * N + (bx >> ms);
+            if (key != ckey) {
+                cslot = __ldg(&table[key]);
+                ckey = key;
+            }
+            if (cslot == kEmpty) return false;
+            const uint16_t* b = payload + (size_t)cslot * P.M3 + (((lz << ms) + ly) << ms) + lx;
+            const int M = P.M, MM = M * M;
+            pl[0] = __ldg(b);
+            pl[1] = __ldg(b + 1);
+            pl[2] = __ldg(b + M);
+            pl[3] = __ldg(b + M + 1);
+            pl[4] = __ldg(b + MM);
+            pl[5] = __ldg(b + MM + 1);
+            pl[6] = __ldg(b + MM + M);
+            pl[7] = __ldg(b + MM + M + 1);
+        } else {
+            return sample(p, out);  // corners in several blocks (1 - (7/8)^3 of the samples)
+        }
+        double c[8];
+        bool ok = true;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int8_t cc = static_cast<int8_t>(pl[i] & 0xFF);
+            ok = ok && cc != kChiCode;
+            c[i] = tdec[(int)cc + 128];
+        }
+        if (!ok) return false;
+        const double x0 = c[0] + (c[1] - c[0]) * fx;
+        const double x1 = c[2] + (c[3] - c[2]) * fx;
+        const double x2 = c[4] + (c[5] - c[4]) * fx;
+        const double x3 = c[6] + (c[7] - c[6]) * fx;
+        const double y0 = x0 + (x1 - x0) * fy;
+        const double y1 = x2 + (x3 - x2) * fy;
+        out = y0 + (y1 - y0) * fz;
+        return true;
+    }
+
+    // sample_tsdf_gradient (render.cpp:50-63) with the near-surface sampler
+    __device__ bool gradient_near(d3 p, double h, d3& g, int64_t& ckey, int32_t& cslot) const {
+        double a, b;
+        if (!sample_near(mk(p.x + h, p.y, p.z), a, ckey, cslot) || !sample_near(mk(p.x - h, p.y, p.z), b, ckey, cslot))
+            return false;
+        const double gx = (a - b) / (2.0 * h);
+        if (!sample_near(mk(p.x, p.y + h, p.z), a, ckey, cslot) || !sample_near(mk(p.x, p.y - h, p.z), b, ckey, cslot))
+            return false;
+        const double gy = (a - b) / (2.0 * h);
+        if (!sample_near(mk(p.x, p.y, p.z + h), a, ckey, cslot) || !sample_near(mk(p.x, p.y, p.z - h), b, ckey, cslot))
+            return false;
+        const double gz = (a - b) / (2.0 * h);
+        g = mk(gx, gy, gz);
+        return true;
+    }
+
     // sample_tsdf_gradient (render.cpp:50-63)
     __device__ bool gradient(d3 p, double h, d3& g) const {
         double a, b;
@@ -609,11 +682,13 @@ __global__ void __launch_bounds__(256)
         const d3 dir = mv(pose.R, dir_cam);
         double hit_a = b.a, hit_b = b.b, val_a = b.va, val_b = b.vb;
         float out_d = 0.0f, nx = 0.f, ny = 0.f, nz = 0.f;
+        int64_t ckey = -1;
+        int32_t cslot = kEmpty;
         for (int iter = 0; iter < 48 && hit_b - hit_a > fine_tol; ++iter) {
             double t_new = hit_b - val_b * (hit_b - hit_a) / (val_b - val_a);
             if (!(t_new > hit_a) || !(t_new < hit_b)) t_new = 0.5 * (hit_a + hit_b);
             double val;
-            if (!S.sample(add(pose.t, scale(t_new, dir)), val)) {
+            if (!S.sample_near(add(pose.t, scale(t_new, dir)), val, ckey, cslot)) {
                 hit_a = t_new;
                 val_a = dmax(val_a, 1e-12);
                 continue;
@@ -640,7 +715,7 @@ __global__ void __launch_bounds__(256)
             // sample_tsdf_gradient (render.cpp:50-63)
             const d3 p = add(pose.t, scale(root, dir));
             d3 gr;
-            if (S.gradient(p, vox, gr) && sqnorm(gr) > 0.0) {
+            if (S.gradient_near(p, vox, gr, ckey, cslot) && sqnorm(gr) > 0.0) {
                 // world_to_cam * grad.normalized()  (render.cpp:242-245)
                 const d3 n_cam = mv(mt(pose.R), normalized(gr));
                 nx = (float)n_cam.x;
