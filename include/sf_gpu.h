@@ -161,6 +161,19 @@ int sf_volume_create(const sf_grid_config* config, uint64_t pool_capacity, const
 int sf_volume_destroy(sf_volume_t vol);
 int sf_volume_get_info(sf_volume_t vol, sf_volume_info* out);
 
+/* ---- marching cubes (marching_cubes.hpp:37-44, marching_cubes.cpp:74-196) -----------
+ * The reference's mesh exactly: same vertices (float, welded per batch by cube-edge id in
+ * first-reference order), normals and triangles. region_pose / region_intrinsics: optional
+ * FrustumRegion (both or neither); batch_memory_budget: MarchingCubesOptions (0 = 64 MiB).
+ * The mesh lives on the device until sf_mesh_read (triangles as 3 x uint32). */
+typedef struct sf_mesh* sf_mesh_t;
+int sf_marching_cubes(sf_volume_t vol, const double region_pose[12], const sf_intrinsics* region_intrinsics,
+                      uint64_t batch_memory_budget, sf_mesh_t* out, void* stream);
+int sf_mesh_counts(sf_mesh_t mesh, uint64_t* vertices, uint64_t* triangles);
+int sf_mesh_read(sf_mesh_t mesh, float* vertices_xyz, float* normals_xyz, uint32_t* triangles,
+                 int32_t out_on_device, void* stream);
+int sf_mesh_destroy(sf_mesh_t mesh);
+
 /* ---- spatial sharding across GPUs --------------------
  * No reference counterpart: the reference volume is one process. A sharded volume
  * allocates only the blocks its rank owns: owner(block) = hash of its (2^brick_shift)^3-block

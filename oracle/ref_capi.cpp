@@ -14,6 +14,7 @@
 #include "sparsefusion/camera.hpp"
 #include "sparsefusion/fusion.hpp"
 #include "sparsefusion/grid.hpp"
+#include "sparsefusion/marching_cubes.hpp"
 #include "sparsefusion/pose.hpp"
 #include "sparsefusion/registration.hpp"
 #include "sparsefusion/render.hpp"
@@ -23,6 +24,9 @@ using namespace sparsefusion;
 
 struct sfref_volume {
     std::unique_ptr<SparseTsdfGrid> grid;
+};
+struct sfref_mesh {
+    Mesh mesh;
 };
 
 namespace {
@@ -521,6 +525,42 @@ int sfref_pipeline_frame(sfref_volume* v, const sf_frame* captured, const sf_int
         }
         return SF_OK;
     });
+}
+
+int sfref_marching_cubes(sfref_volume* v, const double region_pose[12], const sf_intrinsics* region_intrinsics,
+                         uint64_t batch_memory_budget, sfref_mesh** out, void*) {
+    return guarded([&]() -> int {
+        MarchingCubesOptions o;
+        if (region_pose) o.region = FrustumRegion{to_pose(region_pose), to_intr(region_intrinsics)};
+        if (batch_memory_budget) o.batch_memory_budget = batch_memory_budget;
+        auto m = std::make_unique<sfref_mesh>();
+        m->mesh = marching_cubes(*v->grid, o);
+        *out = m.release();
+        return SF_OK;
+    });
+}
+
+int sfref_mesh_counts(sfref_mesh* m, uint64_t* vertices, uint64_t* triangles) {
+    if (vertices) *vertices = m->mesh.vertices.size();
+    if (triangles) *triangles = m->mesh.triangles.size();
+    return SF_OK;
+}
+
+int sfref_mesh_read(sfref_mesh* m, float* vertices_xyz, float* normals_xyz, uint32_t* triangles, int32_t, void*) {
+    for (size_t i = 0; i < m->mesh.vertices.size(); ++i)
+        for (int k = 0; k < 3; ++k) {
+            if (vertices_xyz) vertices_xyz[3 * i + k] = m->mesh.vertices[i][k];
+            if (normals_xyz) normals_xyz[3 * i + k] = m->mesh.normals[i][k];
+        }
+    for (size_t i = 0; i < m->mesh.triangles.size(); ++i)
+        for (int k = 0; k < 3; ++k)
+            if (triangles) triangles[3 * i + k] = m->mesh.triangles[i][k];
+    return SF_OK;
+}
+
+int sfref_mesh_destroy(sfref_mesh* m) {
+    delete m;
+    return SF_OK;
 }
 
 }  // extern "C"

@@ -54,6 +54,12 @@ def raycast(grid, pose, intrinsics):
     return grid.backend.raycast(grid, pose, intrinsics)
 
 
+def marching_cubes(grid, region=None, batch_memory_budget=0):
+    """marching_cubes (marching_cubes.hpp:37-44; module.cpp:291-293): (vertices, normals,
+    triangles) numpy arrays. region: optional (Pose, Intrinsics) FrustumRegion."""
+    return grid.backend.marching_cubes(grid, region, batch_memory_budget)
+
+
 def raycast_result(grid, pose, intrinsics, out_depth=None, out_normals=None, stream=None):
     """RaycastResult (render.hpp:51-55): (DepthFrame, NormalMap, RaycastStats)."""
     return grid.backend.raycast_result(grid, pose, intrinsics, out_depth, out_normals, stream)

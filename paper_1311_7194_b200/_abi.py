@@ -206,6 +206,15 @@ SIGNATURES = {
     ),
 }
 
+# marching cubes: the product and the reference build (the C restatement does not cover it;
+# its parity is checked against the reference itself)
+MESH = {
+    "marching_cubes": (C.c_int, [vp, c_double_p, P(IntrinsicsC), u64, P(vp), vp]),
+    "mesh_counts": (C.c_int, [vp, u64p, u64p]),
+    "mesh_read": (C.c_int, [vp, vp, vp, vp, i32, vp]),
+    "mesh_destroy": (C.c_int, [vp]),
+}
+
 PRODUCT_ONLY = {
     "version": (C.c_char_p, []),
     "volume_read_free_list": (C.c_int, [vp, i32p, u64p]),
@@ -252,7 +261,8 @@ REF_ONLY = {
 
 # sf_gpu.h declarations that the CPU suite checks are exported by libsf_gpu.so
 EXPORTED = sorted(
-    ["sf_" + k for k in SIGNATURES] + ["sf_" + k for k in PRODUCT_ONLY if k != "debug_aux_tables"]
+    ["sf_" + k for k in SIGNATURES] + ["sf_" + k for k in MESH]
+    + ["sf_" + k for k in PRODUCT_ONLY if k != "debug_aux_tables"]
 )
 
 
@@ -288,5 +298,5 @@ def product() -> Lib:
                 f"{LIB_PATH} is not built; run `make` (or __graft_entry__.build()) - "
                 "the sparse-TSDF path has no CPU fallback"
             )
-        _product = Lib(LIB_PATH, "sf", PRODUCT_ONLY)
+        _product = Lib(LIB_PATH, "sf", {**PRODUCT_ONLY, **MESH})
     return _product

@@ -484,6 +484,30 @@ class Backend:
             shrunk_motion_norm=r.shrunk_motion_norm, pair_count=r.pair_count,
             motion_r=np.array(list(r.motion_r)), motion_t=np.array(list(r.motion_t)))
 
+    # --- marching cubes (marching_cubes.hpp:37-44; module.cpp:291-293) ---
+    def marching_cubes(self, grid, region=None, batch_memory_budget: int = 0):
+        """(vertices (V,3) float32, normals (V,3) float32, triangles (T,3) uint32).
+        region: optional (Pose, Intrinsics) FrustumRegion."""
+        h = C.c_void_p()
+        if region is not None:
+            pose, intr = region
+            p12 = pose.to12()
+            ic = intr.c()
+            self.check(self.lib.marching_cubes(grid.handle, _dptr(p12), C.byref(ic), batch_memory_budget,
+                                               C.byref(h), None))
+        else:
+            self.check(self.lib.marching_cubes(grid.handle, None, None, batch_memory_budget, C.byref(h), None))
+        try:
+            nv, nt = C.c_uint64(), C.c_uint64()
+            self.check(self.lib.mesh_counts(h, C.byref(nv), C.byref(nt)))
+            v = np.zeros((nv.value, 3), dtype=np.float32)
+            n = np.zeros((nv.value, 3), dtype=np.float32)
+            t = np.zeros((nt.value, 3), dtype=np.uint32)
+            self.check(self.lib.mesh_read(h, v.ctypes.data, n.ctypes.data, t.ctypes.data, 0, None))
+        finally:
+            self.lib.mesh_destroy(h)
+        return v, n, t
+
     # --- synthetic input (scene.hpp:69-71) ---
     def render_synthetic_depth(self, scene: AnalyticScene, pose: Pose, intrinsics: Intrinsics, sigma0: float = 0.0,
                                seed: int = 0, max_steps: int = 256, tolerance_scale: float = 1e-5,

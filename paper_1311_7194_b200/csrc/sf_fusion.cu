@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "sf_internal.h"
+#include "sf_sample.cuh"
 
 namespace sf {
 
@@ -398,28 +399,6 @@ __device__ __forceinline__ bool in_sorted(const uint32_t* __restrict__ a, uint32
         else hi = mid;
     }
     return lo < n && a[lo] == key;
-}
-
-__device__ bool frustum_intersects_block(const VolParams& P, const FrameConsts* __restrict__ fc, d3 lo, d3 hi) {
-    // box axes: the box projection is exactly [lo_a, hi_a]
-    const double blo[3] = {lo.x, lo.y, lo.z}, bhi[3] = {hi.x, hi.y, hi.z};
-    for (int k = 0; k < 3; ++k) {
-        if (fc->sat_hi[k] < blo[k] || bhi[k] < fc->sat_lo[k]) return false;
-    }
-    for (int k = 3; k < kSatAxes; ++k) {
-        if (!fc->sat_valid[k]) continue;
-        const d3 a = fc->sat_axis[k];
-        double mn = INFINITY, mx = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const d3 p = mk(i & 1 ? hi.x : lo.x, i & 2 ? hi.y : lo.y, i & 4 ? hi.z : lo.z);
-            const double d = dot(a, p);
-            mn = dmin(mn, d);
-            mx = dmax(mx, d);
-        }
-        if (fc->sat_hi[k] < mn || mx < fc->sat_lo[k]) return false;
-    }
-    return true;
 }
 
 __global__ void k_visible(VolParams P, const FrameConsts* __restrict__ fc, FrameCounters* ctr,

@@ -12,12 +12,10 @@
 #include <vector>
 
 #include "sf_internal.h"
+#include "sf_sample.cuh"
 
 namespace sf {
 
-__device__ __forceinline__ bool occupied(const uint32_t* __restrict__ occ, uint64_t ti) {
-    return (__ldg(&occ[ti >> 5]) >> (ti & 31)) & 1u;
-}
 
 // ---- exact skipping along one DDA axis -----------------------------------------------
 // An axis of the DDA is the sequence s_0 = tm, s_{k+1} = RN(s_k + td), tm, td > 0. Inside
@@ -326,198 +324,6 @@ __global__ void __launch_bounds__(256, 3) k_ray_bounds(VolParams P, const FrameC
     }
 }
 
-// voxel_code + sample_tsdf (render.cpp:12-48). Returns false for nullopt.
-struct Sampler {
-    VolParams P;
-    const int32_t* __restrict__ table;
-    const uint16_t* __restrict__ payload;
-    const uint32_t* __restrict__ occ;
-    const double* tdec;  // shared-memory LUT, index code + 128
-
-    __device__ __forceinline__ int blk(int x) const { return P.mshift >= 0 ? (x >> P.mshift) : x / P.M; }
-
-    __device__ __forceinline__ bool code(int x, int y, int z, double& out) const {
-        const int M = P.M;
-        const int bx = blk(x), by = blk(y), bz = blk(z);
-        const int32_t slot = __ldg(&table[table_index(P, bx, by, bz)]);
-        if (slot == kEmpty) return false;
-        const int lx = x - bx * M, ly = y - by * M, lz = z - bz * M;
-        const uint16_t pl = __ldg(&payload[(size_t)slot * P.M3 + (lz * M + ly) * M + lx]);
-        const int8_t c = static_cast<int8_t>(pl & 0xFF);
-        if (c == kChiCode) return false;
-        out = tdec[(int)c + 128];
-        return true;
-    }
-
-    // a / voxel correctly rounded: q = RN(a * RN(1/voxel)) is within 1 ulp, and one
-    // fma-residual correction gives RN(a / voxel) (Markstein's theorem), FP64 pipe only.
-    __device__ __forceinline__ double div_voxel(double a) const {
-        const double q = a * P.inv_voxel;
-        const double r = fma(-q, P.voxel, a);
-        return fma(r, P.inv_voxel, q);
-    }
-
-    __device__ bool sample(d3 p, double& out) const {
-        const double gx = div_voxel(p.x - P.ox) - 0.5;
-        const double gy = div_voxel(p.y - P.oy) - 0.5;
-        const double gz = div_voxel(p.z - P.oz) - 0.5;
-        // |g| >= 2^30 (or NaN) lies outside [0, res - 1) whatever floor gives
-        constexpr double kLim = 1073741824.0;
-        if (!(fabs(gx) < kLim && fabs(gy) < kLim && fabs(gz) < kLim)) return false;
-        int bx, by, bz;
-        const double flx = floor_exact(gx, bx), fly = floor_exact(gy, by), flz = floor_exact(gz, bz);
-        const int res = P.res;
-        if (bx < 0 || by < 0 || bz < 0 || bx + 1 >= res || by + 1 >= res || bz + 1 >= res) return false;
-        // The base corner's block EMPTY => voxel_code fails => nullopt (render.cpp:14-15,39):
-        // decided from the 1-bit occupancy map without touching the 4-byte table.
-        if (!occupied(occ, table_index(P, blk(bx), blk(by), blk(bz)))) return false;
-        const double fx = gx - flx, fy = gy - fly, fz = gz - flz;
-        double c[8];
-        if (P.mshift >= 0) {
-            // All 8 table reads issued together, then all 8 payload reads (no dependent
-            // branch between loads); any EMPTY block or chi corner => nullopt.
-            const int ms = P.mshift, mm = P.M - 1, N = P.N;
-            const int lx = bx & mm, ly = by & mm, lz = bz & mm;
-            uint16_t pl[8];
-            bool ok = true;
-            if (lx != mm && ly != mm && lz != mm) {
-                // all eight corners in the base block (7/8)^3 of the time: one table read
-                const int32_t slot = __ldg(&table[((size_t)(bz >> ms) * N + (by >> ms)) * N + (bx >> ms)]);
-                if (slot == kEmpty) return false;
-                const uint16_t* b = payload + (size_t)slot * P.M3 + (((lz << ms) + ly) << ms) + lx;
-                const int M = P.M, MM = M * M;
-                pl[0] = __ldg(b);
-                pl[1] = __ldg(b + 1);
-                pl[2] = __ldg(b + M);
-                pl[3] = __ldg(b + M + 1);
-                pl[4] = __ldg(b + MM);
-                pl[5] = __ldg(b + MM + 1);
-                pl[6] = __ldg(b + MM + M);
-                pl[7] = __ldg(b + MM + M + 1);
-            } else {
-                const int bxs[2] = {bx >> ms, (bx + 1) >> ms}, lxs[2] = {lx, (bx + 1) & mm};
-                const int bys[2] = {by >> ms, (by + 1) >> ms}, lys[2] = {ly, (by + 1) & mm};
-                const int bzs[2] = {bz >> ms, (bz + 1) >> ms}, lzs[2] = {lz, (bz + 1) & mm};
-                int32_t s[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    s[i] = __ldg(&table[((size_t)bzs[i >> 2] * N + bys[(i >> 1) & 1]) * N + bxs[i & 1]]);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) ok = ok && s[i] != kEmpty;
-                if (!ok) return false;
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    pl[i] = __ldg(&payload[(size_t)s[i] * P.M3 + (((lzs[i >> 2] << ms) + lys[(i >> 1) & 1]) << ms) +
-                                           lxs[i & 1]]);
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int8_t cc = static_cast<int8_t>(pl[i] & 0xFF);
-                ok = ok && cc != kChiCode;
-                c[i] = tdec[(int)cc + 128];
-            }
-            if (!ok) return false;
-        } else {
-            for (int i = 0; i < 8; ++i)
-                if (!code(bx + (i & 1), by + ((i >> 1) & 1), bz + ((i >> 2) & 1), c[i])) return false;
-        }
-        const double x0 = c[0] + (c[1] - c[0]) * fx;
-        const double x1 = c[2] + (c[3] - c[2]) * fx;
-        const double x2 = c[4] + (c[5] - c[4]) * fx;
-        const double x3 = c[6] + (c[7] - c[6]) * fx;
-        const double y0 = x0 + (x1 - x0) * fy;
-        const double y1 = x2 + (x3 - x2) * fy;
-        out = y0 + (y1 - y0) * fz;
-        return true;
-    }
-
-    // sample() for the refinement near a known surface: no occupancy early-out (the table is
-    // authoritative: same result), and the slot of the last single-block sample is cached, so
-    // successive samples in the same block cost one L1-resident payload read.
-    __device__ bool sample_near(d3 p, double& out, int64_t& ckey, int32_t& cslot) const {
-        if (P.mshift < 0) return sample(p, out);
-        const double gx = div_voxel(p.x - P.ox) - 0.5;
-        const double gy = div_voxel(p.y - P.oy) - 0.5;
-        const double gz = div_voxel(p.z - P.oz) - 0.5;
-        constexpr double kLim = 1073741824.0;
-        if (!(fabs(gx) < kLim && fabs(gy) < kLim && fabs(gz) < kLim)) return false;
-        int bx, by, bz;
-        const double flx = floor_exact(gx, bx), fly = floor_exact(gy, by), flz = floor_exact(gz, bz);
-        const int res = P.res;
-        if (bx < 0 || by < 0 || bz < 0 || bx + 1 >= res || by + 1 >= res || bz + 1 >= res) return false;
-        const double fx = gx - flx, fy = gy - fly, fz = gz - flz;
-        const int ms = P.mshift, mm = P.M - 1, N = P.N;
-        const int lx = bx & mm, ly = by & mm, lz = bz & mm;
-        uint16_t pl[8];
-        if (lx != mm && ly != mm && lz != mm) {
-            const int64_t key = ((int64_t)(bz >> ms) * N + (by >> ms)) * N + (bx >> ms);
-            if (key != ckey) {
-                cslot = __ldg(&table[key]);
-                ckey = key;
-            }
-            if (cslot == kEmpty) return false;
-            const uint16_t* b = payload + (size_t)cslot * P.M3 + (((lz << ms) + ly) << ms) + lx;
-            const int M = P.M, MM = M * M;
-            pl[0] = __ldg(b);
-            pl[1] = __ldg(b + 1);
-            pl[2] = __ldg(b + M);
-            pl[3] = __ldg(b + M + 1);
-            pl[4] = __ldg(b + MM);
-            pl[5] = __ldg(b + MM + 1);
-            pl[6] = __ldg(b + MM + M);
-            pl[7] = __ldg(b + MM + M + 1);
-        } else {
-            return sample(p, out);  // corners in several blocks (1 - (7/8)^3 of the samples)
-        }
-        double c[8];
-        bool ok = true;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int8_t cc = static_cast<int8_t>(pl[i] & 0xFF);
-            ok = ok && cc != kChiCode;
-            c[i] = tdec[(int)cc + 128];
-        }
-        if (!ok) return false;
-        const double x0 = c[0] + (c[1] - c[0]) * fx;
-        const double x1 = c[2] + (c[3] - c[2]) * fx;
-        const double x2 = c[4] + (c[5] - c[4]) * fx;
-        const double x3 = c[6] + (c[7] - c[6]) * fx;
-        const double y0 = x0 + (x1 - x0) * fy;
-        const double y1 = x2 + (x3 - x2) * fy;
-        out = y0 + (y1 - y0) * fz;
-        return true;
-    }
-
-    // sample_tsdf_gradient (render.cpp:50-63) with the near-surface sampler
-    __device__ bool gradient_near(d3 p, double h, d3& g, int64_t& ckey, int32_t& cslot) const {
-        double a, b;
-        if (!sample_near(mk(p.x + h, p.y, p.z), a, ckey, cslot) || !sample_near(mk(p.x - h, p.y, p.z), b, ckey, cslot))
-            return false;
-        const double gx = (a - b) / (2.0 * h);
-        if (!sample_near(mk(p.x, p.y + h, p.z), a, ckey, cslot) || !sample_near(mk(p.x, p.y - h, p.z), b, ckey, cslot))
-            return false;
-        const double gy = (a - b) / (2.0 * h);
-        if (!sample_near(mk(p.x, p.y, p.z + h), a, ckey, cslot) || !sample_near(mk(p.x, p.y, p.z - h), b, ckey, cslot))
-            return false;
-        const double gz = (a - b) / (2.0 * h);
-        g = mk(gx, gy, gz);
-        return true;
-    }
-
-    // sample_tsdf_gradient (render.cpp:50-63)
-    __device__ bool gradient(d3 p, double h, d3& g) const {
-        double a, b;
-        if (!sample(mk(p.x + h, p.y, p.z), a) || !sample(mk(p.x - h, p.y, p.z), b)) return false;
-        const double gx = (a - b) / (2.0 * h);
-        if (!sample(mk(p.x, p.y + h, p.z), a) || !sample(mk(p.x, p.y - h, p.z), b)) return false;
-        const double gy = (a - b) / (2.0 * h);
-        if (!sample(mk(p.x, p.y, p.z + h), a) || !sample(mk(p.x, p.y, p.z - h), b)) return false;
-        const double gz = (a - b) / (2.0 * h);
-        g = mk(gx, gy, gz);
-        return true;
-    }
-};
-
 // One ray per group of G lanes (G = 8: four rays per warp). Stage 1 evaluates G consecutive
 // points of the reference's sequential t lattice at once (lane k walks the same additions
 // t += step, so every t is bit-identical), then finds the first sign change in lattice
@@ -560,9 +366,7 @@ __global__ void __launch_bounds__(256, 3)
             const Sampler S{P, table, payload, occ, s_tdec};
             const Intr& intr = fc->intr;
             const Pose& pose = fc->pose;
-            const double vox = P.voxel;
             const double coarse_step = 0.5 * P.delta;
-            const double fine_tol = 0.01 * vox;
             const d3 dir_cam = normalized(unproject(intr, u, v, 1.0));
             const d3 dir = mv(pose.R, dir_cam);
             const double t1 = fe;

@@ -29,7 +29,7 @@ def reference():
     if "ref" not in _cache:
         if not os.path.exists(REF_SO):
             _try_build("ref")
-        _cache["ref"] = Backend(A.Lib(REF_SO, "sfref", A.REF_ONLY), "reference") if os.path.exists(REF_SO) else None
+        _cache["ref"] = Backend(A.Lib(REF_SO, "sfref", {**A.REF_ONLY, **A.MESH}), "reference") if os.path.exists(REF_SO) else None
     return _cache["ref"]
 
 
