@@ -378,6 +378,12 @@ def run_ours(args, world, rank, local):
     e2e_s = time.perf_counter() - t0
     h2d, d2h = tr2.io_bytes(True)
 
+    # marching cubes of the reconstructed C4 volume (§8f; bit-identical to the reference mesh)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    mv, _, mt = sf.marching_cubes(grid)
+    mesh_ms = (time.perf_counter() - t0) * 1e3
+
     total_ms, e2e_ms, value, e2e_value = aggregate_ranks(total_ms, e2e_s * 1e3, steps, world, dev, dist)
     signature = list(metrics[-1].pose.to12()) + [float(metrics[-1].fusion.blocks_total), float(vox_updated)]
     consistent = replicas_consistent(signature, dev, dist, world)
@@ -418,6 +424,8 @@ def run_ours(args, world, rank, local):
         "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": launches_total,
+        "marching_cubes": {"ms": mesh_ms, "vertices": int(len(mv)), "triangles": int(len(mt)),
+                           "note": "whole C4 volume after the run, host wall time incl. device->host mesh copy"},
         "clocks": clocks.summary(),
     }
     if rank == 0 and not args.no_cpu_baseline:

@@ -285,6 +285,48 @@ inline RaycastResult raycast(const SparseTsdfGrid& grid, const Pose& pose, const
     return r;
 }
 
+// ---- marching cubes (marching_cubes.hpp:16-44) ----------------------------------------
+struct Mesh {
+    std::vector<std::array<float, 3>> vertices, normals;
+    std::vector<std::array<std::uint32_t, 3>> triangles;
+    bool empty() const { return triangles.empty(); }
+};
+struct FrustumRegion {
+    Pose pose;
+    Intrinsics intrinsics;
+};
+struct MarchingCubesOptions {
+    std::optional<FrustumRegion> region;
+    std::size_t batch_memory_budget = 64ull << 20;
+};
+inline Mesh marching_cubes(const SparseTsdfGrid& grid, const MarchingCubesOptions& options = {}) {
+    sf_mesh_t h = nullptr;
+    if (options.region) {
+        const auto p = options.region->pose.packed();
+        const sf_intrinsics ic = options.region->intrinsics.c();
+        check(sf_marching_cubes(grid.handle(), p.data(), &ic, options.batch_memory_budget, &h, nullptr));
+    } else {
+        check(sf_marching_cubes(grid.handle(), nullptr, nullptr, options.batch_memory_budget, &h, nullptr));
+    }
+    std::uint64_t nv = 0, nt = 0;
+    Mesh m;
+    const int st = sf_mesh_counts(h, &nv, &nt);
+    if (st == SF_OK) {
+        m.vertices.resize(nv);
+        m.normals.resize(nv);
+        m.triangles.resize(nt);
+        const int rd = sf_mesh_read(h, m.vertices.empty() ? nullptr : m.vertices[0].data(),
+                                    m.normals.empty() ? nullptr : m.normals[0].data(),
+                                    m.triangles.empty() ? nullptr : m.triangles[0].data(), 0, nullptr);
+        sf_mesh_destroy(h);
+        check(rd);
+    } else {
+        sf_mesh_destroy(h);
+        check(st);
+    }
+    return m;
+}
+
 inline NormalMap compute_normals(const DepthFrame& frame, double sigma0 = 2.5e-4, double spatial_scale = 0.0) {
     NormalMap m(frame.intrinsics.width, frame.intrinsics.height);
     const sf_frame f = frame.c();

@@ -176,3 +176,28 @@ TEST_CASE("tracker runs the fused-frame loop without losing track") {
     CHECK(err < 0.01);
     CHECK(m.fusion.blocks_total == grid.allocated_count());
 }
+
+TEST_CASE("marching cubes: one written cube straddling all eight blocks") {  // test_render.cpp:249-272
+    GridConfig cfg;
+    cfg.blocks_per_axis = 2;
+    cfg.voxels_per_block_axis = 4;
+    cfg.box_origin = {0.0, 0.0, 0.0};
+    cfg.box_side = 1.0;
+    SparseTsdfGrid grid(cfg, 8);
+    CHECK(marching_cubes(grid).empty());
+    const double delta = grid.delta();
+    for (int bz = 0; bz < 2; ++bz)
+        for (int by = 0; by < 2; ++by)
+            for (int bx = 0; bx < 2; ++bx) grid.allocate_block({bx, by, bz});
+    for (int dz = 0; dz < 2; ++dz)
+        for (int dy = 0; dy < 2; ++dy)
+            for (int dx = 0; dx < 2; ++dx) {
+                const bool inside = dx == 0 && dy == 0 && dz == 0;
+                grid.write_voxel({3 + dx, 3 + dy, 3 + dz}, inside ? -0.3 * delta : 0.3 * delta, 1.0);
+            }
+    const Mesh mesh = marching_cubes(grid);
+    CHECK(mesh.triangles.size() == 1);
+    CHECK(mesh.vertices.size() == 3);
+    for (const auto& n : mesh.normals)
+        CHECK(std::abs(std::sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]) - 1.0f) < 1e-5f);
+}
