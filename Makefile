@@ -14,7 +14,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -fmad=false -std=c++17 --expt-relaxed-constexpr
 SRC_DIR := paper_1311_7194_b200/csrc
 OUT_DIR := paper_1311_7194_b200/_native
 OBJ_DIR := build/obj
-SRCS    := sf_volume sf_fusion sf_render sf_icp sf_tracker sf_scene sf_shard sf_mesh
+SRCS    := sf_volume sf_fusion sf_render sf_icp sf_tracker sf_scene sf_shard sf_mesh sf_io
 OBJS    := $(addprefix $(OBJ_DIR)/,$(addsuffix .o,$(SRCS)))
 HDRS    := $(wildcard $(SRC_DIR)/*.h $(SRC_DIR)/*.cuh) include/sf_gpu.h
 LIB     := $(OUT_DIR)/libsf_gpu.so

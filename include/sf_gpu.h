@@ -161,6 +161,13 @@ int sf_volume_create(const sf_grid_config* config, uint64_t pool_capacity, const
 int sf_volume_destroy(sf_volume_t vol);
 int sf_volume_get_info(sf_volume_t vol, sf_volume_info* out);
 
+/* ---- DFRM depth frames (frame_io.hpp:15-16, frame_io.cpp:28-79) ------------------------
+ * write: the reference's byte layout; frame buffers may be host or device (frame->on_device).
+ * read: depth == NULL only fills *intrinsics (size query); out-of-range depths become 0. */
+int sf_dfrm_write(const char* path, const sf_frame* frame);
+int sf_dfrm_read(const char* path, sf_intrinsics* intrinsics, float* depth, float* sigma, int32_t* has_sigma,
+                 int32_t out_on_device);
+
 /* ---- marching cubes (marching_cubes.hpp:37-44, marching_cubes.cpp:74-196) -----------
  * The reference's mesh exactly: same vertices (float, welded per batch by cube-edge id in
  * first-reference order), normals and triangles. region_pose / region_intrinsics: optional

@@ -13,6 +13,7 @@
 #include "../include/sf_gpu.h"
 #include "sparsefusion/camera.hpp"
 #include "sparsefusion/fusion.hpp"
+#include "sparsefusion/frame_io.hpp"
 #include "sparsefusion/grid.hpp"
 #include "sparsefusion/marching_cubes.hpp"
 #include "sparsefusion/pose.hpp"
@@ -561,6 +562,33 @@ int sfref_mesh_read(sfref_mesh* m, float* vertices_xyz, float* normals_xyz, uint
 int sfref_mesh_destroy(sfref_mesh* m) {
     delete m;
     return SF_OK;
+}
+
+int sfref_dfrm_write(const char* path, const sf_frame* frame) {
+    return guarded([&]() -> int {
+        write_dfrm(to_frame(frame), path);
+        return SF_OK;
+    });
+}
+
+int sfref_dfrm_read(const char* path, sf_intrinsics* intrinsics, float* depth, float* sigma, int32_t* has_sigma,
+                    int32_t) {
+    return guarded([&]() -> int {
+        const DepthFrame f = read_dfrm(path);
+        intrinsics->width = f.intrinsics.width;
+        intrinsics->height = f.intrinsics.height;
+        intrinsics->fx = f.intrinsics.fx;
+        intrinsics->fy = f.intrinsics.fy;
+        intrinsics->cx = f.intrinsics.cx;
+        intrinsics->cy = f.intrinsics.cy;
+        intrinsics->near_plane = f.intrinsics.near_plane;
+        intrinsics->far_plane = f.intrinsics.far_plane;
+        if (!depth) return SF_OK;
+        std::memcpy(depth, f.depth.data(), f.depth.size() * sizeof(float));
+        if (has_sigma) *has_sigma = f.has_sigma() ? 1 : 0;
+        if (f.has_sigma() && sigma) std::memcpy(sigma, f.sigma.data(), f.sigma.size() * sizeof(float));
+        return SF_OK;
+    });
 }
 
 }  // extern "C"

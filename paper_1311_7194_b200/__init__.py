@@ -54,6 +54,16 @@ def raycast(grid, pose, intrinsics):
     return grid.backend.raycast(grid, pose, intrinsics)
 
 
+def write_dfrm(frame, path):
+    """write_dfrm (frame_io.hpp:15; module.cpp:304): the reference's DFRM byte layout."""
+    default_backend().write_dfrm(frame, path)
+
+
+def read_dfrm(path):
+    """read_dfrm (frame_io.hpp:16; module.cpp:305)."""
+    return default_backend().read_dfrm(path)
+
+
 def marching_cubes(grid, region=None, batch_memory_budget=0):
     """marching_cubes (marching_cubes.hpp:37-44; module.cpp:291-293): (vertices, normals,
     triangles) numpy arrays. region: optional (Pose, Intrinsics) FrustumRegion."""

@@ -213,6 +213,8 @@ MESH = {
     "mesh_counts": (C.c_int, [vp, u64p, u64p]),
     "mesh_read": (C.c_int, [vp, vp, vp, vp, i32, vp]),
     "mesh_destroy": (C.c_int, [vp]),
+    "dfrm_write": (C.c_int, [C.c_char_p, P(FrameC)]),
+    "dfrm_read": (C.c_int, [C.c_char_p, P(IntrinsicsC), vp, vp, P(C.c_int32), i32]),
 }
 
 PRODUCT_ONLY = {

@@ -484,6 +484,21 @@ class Backend:
             shrunk_motion_norm=r.shrunk_motion_norm, pair_count=r.pair_count,
             motion_r=np.array(list(r.motion_r)), motion_t=np.array(list(r.motion_t)))
 
+    # --- DFRM files (frame_io.hpp:15-16; module.cpp:304-305) ---
+    def write_dfrm(self, frame: DepthFrame, path: str):
+        fc = frame.c()
+        self.check(self.lib.dfrm_write(path.encode(), C.byref(fc)))
+
+    def read_dfrm(self, path: str) -> DepthFrame:
+        ic = A.IntrinsicsC()
+        self.check(self.lib.dfrm_read(path.encode(), C.byref(ic), None, None, None, 0))
+        intr = Intrinsics(ic.width, ic.height, ic.fx, ic.fy, ic.cx, ic.cy, ic.near_plane, ic.far_plane)
+        d = np.zeros((ic.height, ic.width), dtype=np.float32)
+        s = np.zeros_like(d)
+        hs = C.c_int32(0)
+        self.check(self.lib.dfrm_read(path.encode(), C.byref(ic), d.ctypes.data, s.ctypes.data, C.byref(hs), 0))
+        return DepthFrame(intr, d, s if hs.value else None)
+
     # --- marching cubes (marching_cubes.hpp:37-44; module.cpp:291-293) ---
     def marching_cubes(self, grid, region=None, batch_memory_budget: int = 0):
         """(vertices (V,3) float32, normals (V,3) float32, triangles (T,3) uint32).

@@ -140,3 +140,32 @@ def test_reference_wrapper_fuses_on_cpu(ref):
     assert st.blocks_total > 20 and st.voxels_updated > 1000
     assert st.memory_bytes == 2 * st.blocks_total * 512 + 4 * 32 ** 3
     assert ref.lib.volume_check_consistency(g.handle) == 0
+
+
+def test_dfrm_files_match_reference(tmp_path):
+    """DFRM write is byte-identical to the reference's write_dfrm; read applies its
+    out-of-range rule (frame_io.cpp:28-79). Host buffers only: no GPU needed."""
+    from tests import oracle_backends
+
+    ref = oracle_backends.reference()
+    if ref is None:
+        pytest.skip("reference build absent")
+    gpu = sf.default_backend()
+    intr = sf.Intrinsics.simple(40, 30, 35.0, 0.2, 3.0)
+    rng = np.random.default_rng(5)
+    depth = rng.uniform(0.0, 4.0, (30, 40)).astype(np.float32)
+    depth[::7, ::5] = 0.0
+    sigma = rng.uniform(0.0, 0.01, (30, 40)).astype(np.float32)
+    for sg in (None, sigma):
+        f = sf.DepthFrame(intr, depth, sg)
+        a, b = str(tmp_path / "a.dfrm"), str(tmp_path / "b.dfrm")
+        gpu.write_dfrm(f, a)
+        ref.write_dfrm(f, b)
+        assert open(a, "rb").read() == open(b, "rb").read()
+        ra, rb = gpu.read_dfrm(a), ref.read_dfrm(b)
+        assert np.array_equal(ra.depth.view(np.uint32), rb.depth.view(np.uint32))
+        assert (ra.sigma is None) == (sg is None) == (rb.sigma is None)
+        if sg is not None:
+            assert np.array_equal(ra.sigma, rb.sigma)
+        assert (ra.intrinsics.width, ra.intrinsics.height) == (40, 30)
+        assert np.all((ra.depth == 0) | ((ra.depth >= np.float32(0.2)) & (ra.depth <= np.float32(3.0))))
