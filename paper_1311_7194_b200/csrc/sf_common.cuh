@@ -279,6 +279,7 @@ struct FuseParams {
     double w_fixed, w_max, q, sigma0, min_variance;
     int downweight;
     int has_sigma;
+    int refine;  // refinement_steps (fusion.hpp:25): sub-pixel descent (generic kernel)
 };
 
 }  // namespace sf

@@ -171,14 +171,14 @@ __global__ void k_pixel_meas(const float* __restrict__ depth, const float* __res
                              Intr intr, FuseParams fp, const float* __restrict__ normals,
                              const uint8_t* __restrict__ edge, double* __restrict__ pix_var,
                              double* __restrict__ pix_w, uint8_t* __restrict__ pix_ok, double* __restrict__ pix_dm,
-                             float2* __restrict__ pix_f, const int* dead) {
+                             float2* __restrict__ pix_f, double* __restrict__ pix_q, const int* dead) {
     if (dead && *dead) return;
     const int u = blockIdx.x * blockDim.x + threadIdx.x;
     const int v = blockIdx.y * blockDim.y + threadIdx.y;
     if (u >= w || v >= h) return;
     const size_t idx = (size_t)v * w + u;
     uint8_t ok = 0;
-    double var = 0.0, wk = 0.0;
+    double var = 0.0, wk = 0.0, qual = 1.0;
     if (px_valid(depth, w, h, u, v)) {
         const double measured = depth[idx];
         const double sg = fp.has_sigma && sigma[idx] > 0.0f ? static_cast<double>(sigma[idx])
@@ -200,6 +200,7 @@ __global__ void k_pixel_meas(const float* __restrict__ depth, const float* __res
                     if (nu >= 0 && nv >= 0 && nu < w && nv < h && edge[(size_t)nv * w + nu]) near = true;
                 }
             if (near) quality *= 0.5;
+            qual = quality;
             if (quality < 0.2) {
                 ok = 0;
             } else {
@@ -209,6 +210,7 @@ __global__ void k_pixel_meas(const float* __restrict__ depth, const float* __res
         }
     }
     pix_var[idx] = var;
+    pix_q[idx] = qual;
     pix_w[idx] = wk;
     pix_ok[idx] = ok;
     pix_dm[idx] = ok ? (double)depth[idx] : 0.0;
@@ -1059,6 +1061,91 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
     if (lane == 0 && exact) atomicAdd(&ctr->exact_voxels, (unsigned long long)exact);
 }
 
+// ---- measurement refinement (fusion.cpp:99-143) ---------------------------------------
+// glibc's hypot (dbl-64, the non-FMA build of Borges' corrected algorithm used by the
+// reference's libm; checked against libm on 5e4 random pairs, tests/test_oracle_cpu.py):
+// not correctly rounded, so the exact operation sequence matters.
+__device__ __forceinline__ double glibc_hypot_kernel(double ax, double ay) {
+    double h = sqrt(ax * ax + ay * ay);
+    double t1, t2;
+    if (h <= 2.0 * ay) {
+        const double delta = h - ay;
+        t1 = ax * (2.0 * delta - ax);
+        t2 = (delta - 2.0 * (ax - ay)) * delta;
+    } else {
+        const double delta = h - ax;
+        t1 = 2.0 * delta * (ax - 2.0 * ay);
+        t2 = (4.0 * delta - ay) * ay + delta * delta;
+    }
+    h -= (t1 + t2) / (2.0 * h);
+    return h;
+}
+__device__ double glibc_hypot(double x, double y) {
+    if (!isfinite(x) || !isfinite(y)) {
+        if (isinf(x) || isinf(y)) return INFINITY;
+        return x + y;
+    }
+    x = fabs(x);
+    y = fabs(y);
+    double ax = x < y ? y : x, ay = x < y ? x : y;
+    constexpr double kScale = 0x1p-600, kLarge = 0x1p+511, kTiny = 0x1p-511, kEps = 0x1p-54;
+    if (ax > kLarge) {
+        if (ay <= ax * kEps) return ax + ay;
+        return glibc_hypot_kernel(ax * kScale, ay * kScale) / kScale;
+    }
+    if (ay < kTiny) {
+        if (ax >= ay / kEps) return ax + ay;
+        return glibc_hypot_kernel(ax / kScale, ay / kScale) * kScale;
+    }
+    if (ay <= ax * kEps) return ax + ay;
+    return glibc_hypot_kernel(ax, ay);
+}
+// bilinear depth (fusion.cpp:102-112)
+__device__ double depth_interp(const float* __restrict__ depth, int w, int h, double uu, double vv) {
+    const int u0 = ref_floor_int(uu), v0 = ref_floor_int(vv);
+    if (!(u0 >= 0 && v0 >= 0 && u0 < w && v0 < h) || !(u0 + 1 >= 0 && v0 + 1 >= 0 && u0 + 1 < w && v0 + 1 < h))
+        return 0.0;
+    const float d00 = depth[(size_t)v0 * w + u0], d10 = depth[(size_t)v0 * w + u0 + 1];
+    const float d01 = depth[(size_t)(v0 + 1) * w + u0], d11 = depth[(size_t)(v0 + 1) * w + u0 + 1];
+    if (d00 <= 0.0f || d10 <= 0.0f || d01 <= 0.0f || d11 <= 0.0f) return 0.0;
+    const double fu = uu - u0, fv = vv - v0;
+    return (d00 * (1.0 - fu) + d10 * fu) * (1.0 - fv) + (d01 * (1.0 - fu) + d11 * fu) * fv;
+}
+__device__ double refine_dist_sq(const float* __restrict__ depth, const Intr& I, double uu, double vv, d3 xc) {
+    const double d = depth_interp(depth, I.w, I.h, uu, vv);
+    if (d <= 0.0) return INFINITY;
+    return sqnorm(sub(unproject(I, uu, vv, d), xc));
+}
+// Sub-pixel descent (fusion.cpp:113-141). Returns true when it moved the measurement: then
+// (u, v), measured and tsdf_k are the refined ones.
+__device__ __noinline__ bool refine_measurement(const float* __restrict__ depth, const Intr& I, int steps, double pu,
+                                                double pv, d3 xc, int& u, int& v, double& measured, double& tsdf_k) {
+    double cu = pu, cv = pv;
+    double best = refine_dist_sq(depth, I, cu, cv, xc);
+    if (!isfinite(best)) return false;
+    const double hh = 0.5;  // gradient probe and step length, pixels
+    for (int step = 0; step < steps; ++step) {
+        const double gu = refine_dist_sq(depth, I, cu + hh, cv, xc) - refine_dist_sq(depth, I, cu - hh, cv, xc);
+        const double gv = refine_dist_sq(depth, I, cu, cv + hh, xc) - refine_dist_sq(depth, I, cu, cv - hh, xc);
+        const double norm = glibc_hypot(gu, gv);
+        if (!isfinite(norm) || norm == 0.0) break;
+        const double nu = cu - hh * gu / norm;
+        const double nv = cv - hh * gv / norm;
+        const double cand = refine_dist_sq(depth, I, nu, nv, xc);
+        if (!(cand < best)) break;
+        best = cand;
+        cu = nu;
+        cv = nv;
+    }
+    const double d_here = depth_interp(depth, I.w, I.h, cu, cv);
+    if (!(d_here > 0.0)) return false;
+    u = ref_lround_int(cu);
+    v = ref_lround_int(cv);
+    measured = d_here;
+    tsdf_k = (d_here >= xc.z ? 1.0 : -1.0) * sqrt(best);
+    return true;
+}
+
 template <int MODE, bool FLOATP>
 __global__ void __launch_bounds__(kThreads)
     k_integrate(VolParams P, const FrameConsts* __restrict__ fc, FuseParams fp, const int2* __restrict__ work,
@@ -1066,7 +1153,7 @@ __global__ void __launch_bounds__(kThreads)
                 const float* __restrict__ depth, const double* __restrict__ pix_var, const double* __restrict__ pix_w,
                 const uint8_t* __restrict__ pix_ok, uint16_t* __restrict__ payload, float2* __restrict__ fpayload,
                 unsigned long long* __restrict__ voxels_updated, const uint32_t* __restrict__ uniq,
-                uint32_t* __restrict__ keybits) {
+                uint32_t* __restrict__ keybits, const float* __restrict__ sigma, const double* __restrict__ pix_q) {
     __shared__ double s_tdec[256], s_adec[256], s_thr[256];
     if (ctr->skip) return;
     for (int i = threadIdx.x; i < 256; i += blockDim.x) {
@@ -1102,15 +1189,39 @@ __global__ void __launch_bounds__(kThreads)
         double tsdf_k = 0.0;
         size_t pix = 0;
         double pu, pv;
+        bool refined = false;
+        double r_var = 0.0, r_w = 0.0;
         if (project(intr, xc, pu, pv)) {
-            const int u = ref_lround_int(pu);
-            const int v = ref_lround_int(pv);
+            int u = ref_lround_int(pu);
+            int v = ref_lround_int(pv);
             if (u >= 0 && v >= 0 && u < w && v < h) {
                 pix = (size_t)v * w + u;
                 const float d = depth[pix];
                 if (d > 0.0f) {
-                    tsdf_k = (double)d - xc.z;
-                    meas = !(fabs(tsdf_k) > delta) && pix_ok[pix];
+                    double measured = d;
+                    tsdf_k = measured - xc.z;
+                    if (fp.refine > 0)
+                        refined = refine_measurement(depth, intr, fp.refine, pu, pv, xc, u, v, measured, tsdf_k);
+                    if (!refined) {
+                        meas = !(fabs(tsdf_k) > delta) && pix_ok[pix];
+                    } else if (!(fabs(tsdf_k) > delta)) {
+                        // measurement at the refined pixel with the interpolated depth (fusion.cpp:147-171)
+                        pix = (size_t)v * w + u;
+                        const double sg = fp.has_sigma && sigma[pix] > 0.0f ? static_cast<double>(sigma[pix])
+                                                                             : fp.sigma0 * measured * measured;
+                        r_var = dmax(sg * sg, fp.min_variance);
+                        r_w = fp.w_fixed;
+                        meas = true;
+                        if (fp.downweight) {
+                            const double q = pix_q[pix];
+                            if (q < 0.2) {
+                                meas = false;
+                            } else {
+                                r_w *= q;
+                                r_var /= q;
+                            }
+                        }
+                    }
                 }
             }
         }
@@ -1143,11 +1254,11 @@ __global__ void __launch_bounds__(kThreads)
         // filters (fusion.cpp:237-272)
         double new_t, new_a;
         if (MODE == 0) {  // simple
-            const double wk_ = pix_w[pix];
+            const double wk_ = refined ? r_w : pix_w[pix];
             new_t = has_prior ? (1.0 - wk_) * prior_t + wk_ * tsdf_k : tsdf_k;
             new_a = wk_;
         } else if (MODE == 1) {  // weighted
-            const double wk_ = pix_w[pix];
+            const double wk_ = refined ? r_w : pix_w[pix];
             if (!has_prior) {
                 new_t = tsdf_k;
                 new_a = wk_;
@@ -1156,7 +1267,7 @@ __global__ void __launch_bounds__(kThreads)
                 new_a = dmin(prior_a + wk_, fp.w_max);
             }
         } else {  // kalman
-            const double pk = pix_var[pix];
+            const double pk = refined ? r_var : pix_var[pix];
             if (!has_prior) {
                 new_t = tsdf_k;
                 new_a = pk;
@@ -1232,8 +1343,6 @@ FuseParams resolve_fuse_params(const Volume& v, const sf_fusion_params& p, bool 
     if (p.mode != 2 && v.aux.mode != 0)
         throw Error(SF_INVALID_ARGUMENT, "fusion: weight-mode grid required for this fusion mode");
     if (p.mode < 0 || p.mode > 2) throw Error(SF_INVALID_ARGUMENT, "fusion: unknown mode");
-    if (p.refinement_steps > 0)
-        throw Error(SF_UNSUPPORTED, "fusion: refinement_steps > 0 is not implemented on the device path");
     FuseParams f{};
     f.mode = p.mode;
     f.w_fixed = p.w_fixed;
@@ -1249,6 +1358,7 @@ FuseParams resolve_fuse_params(const Volume& v, const sf_fusion_params& p, bool 
     f.min_variance = p.min_variance;
     f.downweight = p.edge_downweight ? 1 : 0;
     f.has_sigma = has_sigma ? 1 : 0;
+    f.refine = p.refinement_steps;
     return f;
 }
 
@@ -1289,7 +1399,7 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
             n += 2;
         }
         k_pixel_meas<<<grd2, blk2, 0, s>>>(depth, sigma, w, h, intr, fp, fb.normals, fb.edge, fb.pix_var, fb.pix_w,
-                                            fb.pix_ok, fb.pix_dm, fb.pix_f, dead);
+                                            fb.pix_ok, fb.pix_dm, fb.pix_f, fb.pix_q, dead);
         SF_LAUNCH_CHECK();
         n += 1;
     }
@@ -1333,10 +1443,11 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
 #define SF_INTEGRATE(MODE, FP)                                                                                    \
     k_integrate<MODE, FP><<<kPersistentCtas, kThreads, 0, s>>>(P, fb.fc, fp, fb.work, fb.ctr, v.d_aux, depth,       \
                                                                fb.pix_var, fb.pix_w, fb.pix_ok, v.d_payload,        \
-                                                               v.d_fpayload, vu, fb.keys_unique, v.d_keybits)
+                                                               v.d_fpayload, vu, fb.keys_unique, v.d_keybits, sigma,     \
+                                                               fb.pix_q)
         const bool fpl = v.d_fpayload != nullptr;
         if (events && events->before_integrate) record_event(events->before_integrate, s);
-        const bool fast = !fpl && (P.mshift == 3 || P.mshift == 2) && v.h_aux.fp32_ok;
+        const bool fast = !fpl && (P.mshift == 3 || P.mshift == 2) && v.h_aux.fp32_ok && fp.refine == 0;
 #define SF_INTEGRATE_ROWS(MODE, MS) launch_integrate_rows<MODE, MS>(v, fb, fp, s)
         if (fast) {
             if (P.mshift == 3) {

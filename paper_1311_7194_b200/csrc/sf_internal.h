@@ -107,6 +107,7 @@ struct FrameBuffers {
     uint8_t* pix_ok = nullptr; // w*h valid && quality >= 0.2
     double* pix_dm = nullptr;  // w*h depth where pix_ok, else 0 (one gather per voxel)
     float2* pix_f = nullptr;   // w*h {depth where pix_ok else 0, (float) p_k or w_k}: FP32 integrate
+    double* pix_q = nullptr;   // w*h view quality incl. near-edge halving (refinement path)
     uint32_t key_cap = 0;
     uint32_t* keys = nullptr;
     uint32_t* keys_sorted = nullptr;

@@ -119,7 +119,7 @@ void FrameBuffers::release() {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
-    void* ptrs[] = {depth, sigma, normals, edge, pix_var, pix_w, pix_ok, pix_dm, pix_f, keys, keys_sorted, keys_unique,
+    void* ptrs[] = {depth, sigma, normals, edge, pix_var, pix_w, pix_ok, pix_dm, pix_f, pix_q, keys, keys_sorted, keys_unique,
                     flags, ranks, cub_temp, work, ctr, fc, pose};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -130,6 +130,7 @@ void FrameBuffers::release() {
     pix_var = pix_w = nullptr;
     pix_dm = nullptr;
     pix_f = nullptr;
+    pix_q = nullptr;
     keys = keys_sorted = keys_unique = flags = ranks = nullptr;
     cub_temp = nullptr;
     work = nullptr;
@@ -162,6 +163,7 @@ void ensure_frame_buffers(Volume& v, FrameBuffers& fb, int w, int h) {
     SF_CUDA(cudaMalloc(&fb.pix_ok, n));
     SF_CUDA(cudaMalloc(&fb.pix_dm, n * sizeof(double)));
     SF_CUDA(cudaMalloc(&fb.pix_f, n * sizeof(float2)));
+    SF_CUDA(cudaMalloc(&fb.pix_q, n * sizeof(double)));
     SF_CUDA(cudaMalloc(&fb.keys, fb.key_cap * sizeof(uint32_t)));
     SF_CUDA(cudaMalloc(&fb.keys_sorted, fb.key_cap * sizeof(uint32_t)));
     SF_CUDA(cudaMalloc(&fb.keys_unique, fb.key_cap * sizeof(uint32_t)));

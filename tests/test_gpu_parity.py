@@ -487,3 +487,22 @@ def test_golden_cases_gpu(gpu, name):
     assert got["iterations"] == want["iterations"]
     assert abs(got["matches"] - want["matches"]) <= max(8, want["matches"] // 2000)
     assert got["gated"] == want["gated"]
+
+
+@pytest.mark.parametrize("mode,steps", [(sf.FusionMode.Kalman, 2), (sf.FusionMode.Weighted, 4)])
+def test_fuse_refinement_bit_exact(gpu, ref, mode, steps):
+    """refinement_steps > 0 (fusion.cpp:99-143, bilinear depth + 0.5-px descent with libm's
+    hypot) on noisy frames with a sigma plane: tables and payload codes equal the reference's."""
+    intr = scenes.camera(160, 120, 131.25)
+    poses = scenes.c1_trajectory(100)[::15][:4]
+    frames = [gpu.render_synthetic_depth(scenes.sphere_plane_scene(), p, intr, sigma0=2.5e-4, seed=9 + k,
+                                         domain_size=2.0) for k, p in enumerate(poses)]
+    aux = sf.AuxMode.Variance if mode == sf.FusionMode.Kalman else sf.AuxMode.Weight
+    g, r = grids(gpu, ref, scenes.c1_config(), 0, aux)
+    params = sf.FusionParams(mode=mode, refinement_steps=steps)
+    for f, p in zip(frames, poses):
+        sg = gpu.fuse_frame(g, f, p, params)
+        sr = ref.fuse_frame(r, f, p, params)
+        assert sg == sr
+        assert_same_volume(g, r)
+    assert sr.voxels_updated > 1000

@@ -208,3 +208,41 @@ def test_invalid_arguments_mirror_reference(port, ref):
             be.fuse_frame(g, f, sf.Pose.identity(), sf.FusionParams(mode=sf.FusionMode.Kalman))
         with pytest.raises(ValueError):
             be.fuse_frame(g, f, sf.Pose.identity(), sf.FusionParams(w_fixed=1.5))
+
+
+def test_glibc_hypot_is_the_restated_kernel():
+    """The device refinement path (csrc/sf_fusion.cu glibc_hypot) restates the reference libm's
+    hypot: the non-FMA Borges kernel. Pin: identical to libm.hypot on random pairs across the
+    magnitudes of the refinement gradients (it is not correctly rounded, so the sequence matters)."""
+    import ctypes
+    import math
+    import random
+
+    libm = ctypes.CDLL("libm.so.6")
+    libm.hypot.restype = ctypes.c_double
+    libm.hypot.argtypes = [ctypes.c_double, ctypes.c_double]
+
+    def kernel(ax, ay):
+        h = math.sqrt(ax * ax + ay * ay)
+        if h <= 2.0 * ay:
+            d = h - ay
+            t1 = ax * (2.0 * d - ax)
+            t2 = (d - 2.0 * (ax - ay)) * d
+        else:
+            d = h - ax
+            t1 = 2.0 * d * (ax - 2.0 * ay)
+            t2 = (4.0 * d - ay) * ay + d * d
+        return h - (t1 + t2) / (2.0 * h)
+
+    def hyp(x, y):
+        x, y = abs(x), abs(y)
+        ax, ay = (y, x) if x < y else (x, y)
+        if ay <= ax * 2.0 ** -54:
+            return ax + ay
+        return kernel(ax, ay)
+
+    rng = random.Random(7)
+    for _ in range(20000):
+        a = rng.uniform(-1, 1) * 10 ** rng.uniform(-9, 1)
+        b = rng.uniform(-1, 1) * 10 ** rng.uniform(-9, 1)
+        assert hyp(a, b) == libm.hypot(a, b), (a, b)
