@@ -33,54 +33,60 @@ constexpr int kPersistentCtas = 148 * 8;
 constexpr int kSmallCtas = 148;  // passes over the <= 57.6 k allocate-list keys
 
 // ---------------------------------------------------------------------------------
-// frame setup (one thread)
+// frame setup (one warp: hull points, corner rays and SAT axes computed lane-parallel)
 // ---------------------------------------------------------------------------------
 __global__ void k_frame_consts(VolParams P, Intr intr, const double* __restrict__ pose12, FrameConsts* fc) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const Pose pose = pose_from12(pose12);
-    fc->pose = pose;
-    fc->inv = invert(pose);
-    fc->intr = intr;
-    fc->delta = P.delta;
-
-    // Frustum hull and separating axes, exactly as occupied_blocks_in_frustum builds them.
+    if (blockIdx.x != 0) return;
+    const int lane = threadIdx.x;
+    __shared__ d3 s_pts[8], s_rays[4];
+    __shared__ Pose s_pose;
+    if (lane == 0) {
+        const Pose pose = pose_from12(pose12);
+        s_pose = pose;
+        fc->pose = pose;
+        fc->inv = invert(pose);
+        fc->intr = intr;
+        fc->delta = P.delta;
+    }
+    __syncwarp();
+    const Pose pose = s_pose;
+    // Frustum hull and separating axes, exactly as occupied_blocks_in_frustum builds them
+    // (grid.cpp:228-262): hull points near/far x v x u, corner rays, 26 candidate axes.
     const double us[2] = {-0.5, intr.w - 0.5};
     const double vs[2] = {-0.5, intr.h - 0.5};
-    d3 pts[8];
-    int np = 0;
-    const double zs[2] = {intr.near_plane, intr.far_plane};
-    for (int iz = 0; iz < 2; ++iz)
-        for (int iv = 0; iv < 2; ++iv)
-            for (int iu = 0; iu < 2; ++iu) pts[np++] = apply(pose, unproject(intr, us[iu], vs[iv], zs[iz]));
-    const d3 optical = col(pose.R, 2);
-    auto corner_ray = [&](double u, double v) { return normalized(mv(pose.R, unproject(intr, u, v, 1.0))); };
-    const d3 r00 = corner_ray(us[0], vs[0]);
-    const d3 r10 = corner_ray(us[1], vs[0]);
-    const d3 r01 = corner_ray(us[0], vs[1]);
-    const d3 r11 = corner_ray(us[1], vs[1]);
-    d3 axes[kSatAxes];
-    int na = 0;
-    const d3 box_axes[3] = {mk(1, 0, 0), mk(0, 1, 0), mk(0, 0, 1)};
-    for (int i = 0; i < 3; ++i) axes[na++] = box_axes[i];
-    axes[na++] = optical;
-    axes[na++] = cross(r00, r10);  // top
-    axes[na++] = cross(r11, r01);  // bottom
-    axes[na++] = cross(r01, r00);  // left
-    axes[na++] = cross(r10, r11);  // right
-    const d3 edges[6] = {r00, r10, r01, r11, col(pose.R, 0), col(pose.R, 1)};
-    for (int e = 0; e < 6; ++e)
-        for (int a = 0; a < 3; ++a) axes[na++] = cross(edges[e], box_axes[a]);
-    for (int k = 0; k < kSatAxes; ++k) {
-        fc->sat_axis[k] = axes[k];
-        fc->sat_valid[k] = !(sqnorm(axes[k]) < 1e-18);
+    if (lane < 8) {
+        const double zs[2] = {intr.near_plane, intr.far_plane};
+        s_pts[lane] = apply(pose, unproject(intr, us[lane & 1], vs[(lane >> 1) & 1], zs[lane >> 2]));
+    } else if (lane < 12) {
+        const int r = lane - 8;  // r00, r10, r01, r11
+        s_rays[r] = normalized(mv(pose.R, unproject(intr, us[r & 1], vs[r >> 1], 1.0)));
+    }
+    __syncwarp();
+    if (lane < kSatAxes) {
+        const d3 r00 = s_rays[0], r10 = s_rays[1], r01 = s_rays[2], r11 = s_rays[3];
+        const d3 box_axes[3] = {mk(1, 0, 0), mk(0, 1, 0), mk(0, 0, 1)};
+        d3 ax;
+        if (lane < 3) ax = box_axes[lane];
+        else if (lane == 3) ax = col(pose.R, 2);  // optical axis
+        else if (lane == 4) ax = cross(r00, r10);  // top
+        else if (lane == 5) ax = cross(r11, r01);  // bottom
+        else if (lane == 6) ax = cross(r01, r00);  // left
+        else if (lane == 7) ax = cross(r10, r11);  // right
+        else {
+            const int e = (lane - 8) / 3, b = (lane - 8) % 3;
+            const d3 edges[6] = {r00, r10, r01, r11, col(pose.R, 0), col(pose.R, 1)};
+            ax = cross(edges[e], box_axes[b]);
+        }
+        fc->sat_axis[lane] = ax;
+        fc->sat_valid[lane] = !(sqnorm(ax) < 1e-18);
         double lo = INFINITY, hi = -INFINITY;
         for (int i = 0; i < 8; ++i) {
-            const double d = dot(axes[k], pts[i]);
+            const double d = dot(ax, s_pts[i]);
             lo = dmin(lo, d);
             hi = dmax(hi, d);
         }
-        fc->sat_lo[k] = lo;
-        fc->sat_hi[k] = hi;
+        fc->sat_lo[lane] = lo;
+        fc->sat_hi[lane] = hi;
     }
 }
 

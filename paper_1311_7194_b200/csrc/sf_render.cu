@@ -610,7 +610,8 @@ void launch_raycast(Volume& v, const FrameConsts* d_fc, const Intr& intr, const 
     k_raycast<G><<<grd, blk, 0, s>>>(v.P, d_fc, v.d_table, v.d_payload, v.d_occ, v.d_aux, t_start, t_end, depth, normals,
                                      d_stats, intr.w, intr.h, dead_flag, ray_list, brackets);
     SF_LAUNCH_CHECK();
-    k_raycast_refine<<<148 * 4, 256, 0, s>>>(v.P, d_fc, v.d_table, v.d_payload, v.d_occ, v.d_aux, brackets, depth,
+    // one warp per CTA: the ~30 k bracketed rays spread over all SMs (latency-bound, few warps)
+    k_raycast_refine<<<148 * 16, 32, 0, s>>>(v.P, d_fc, v.d_table, v.d_payload, v.d_occ, v.d_aux, brackets, depth,
                                              normals, d_stats, intr.w, dead_flag);
     SF_LAUNCH_CHECK();
     if (launches) *launches += 2;
