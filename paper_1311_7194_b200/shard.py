@@ -99,6 +99,9 @@ class DistComm:
         mx = max(counts)
         if mx == 0:
             return [[]]
+        if keys.shape[0] < mx:  # another rank packed more records than this rank's buffer holds
+            keys = torch.cat([keys, keys.new_zeros(mx - keys.shape[0])])
+            pays = torch.cat([pays, pays.new_zeros((mx - pays.shape[0],) + tuple(pays.shape[1:]))])
         k_send = keys[:mx].contiguous()
         p_send = pays[:mx].contiguous().view(torch.int32)  # NCCL / gloo have no 16-bit integer type
         k_all = [torch.empty_like(k_send) for _ in range(self.world)]

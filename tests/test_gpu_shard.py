@@ -117,3 +117,27 @@ def test_sharded_tracker_follows_single(gpu):
         print(f"frame {k}: registered={m.registered} it={m.iterations} matches={m.matches} vs {ms.matches} "
               f"pose diff {dp:.2e}, blocks {m.blocks_total} vs {ms.fusion.blocks_total}")
         assert dp == 0.0 and m.matches == ms.matches and m.blocks_total == ms.fusion.blocks_total
+
+
+@pytest.mark.slow
+def test_sharded_c5_full_scale(gpu):
+    """BASELINE C5 itself (8192^3 at 0.15 mm, N = 1024): two emulated shards track 8 frames
+    exactly like one volume (pose, matches, blocks; icp_with_hook)."""
+    cfg = scenes.c5_config()
+    intr = scenes.camera()
+    traj = scenes.c5_trajectory(100, radius=0.9)[:8]
+    frames = _frames(gpu, scenes.c5_scene(), traj, intr, cfg.box_side, sigma0=4e-4)
+    fusion = sf.FusionParams(mode=sf.FusionMode.Kalman, sigma0=4e-4)
+    match = sf.MatchParams.for_voxel_size(cfg.voxel_size)
+    match.max_distance = 4e-3
+    match.normal_sigma0 = 4e-4
+    runs = []
+    for world in (1, 2):
+        shards = [shard.ShardVolume(cfg, 600_000, sf.AuxMode.Variance, r, world, p_min=1e-12) for r in range(world)]
+        tr = shard.ShardedTracker(shards, shard.LocalComm(world), intr, fusion, match, traj[0])
+        ms = [tr.step(f, external=sf.compose(sf.invert(traj[k - 1]), traj[k]) if k else None)
+              for k, f in enumerate(frames)]
+        runs.append([(m.pose.to12().tobytes(), m.matches, m.blocks_total, m.voxels_updated) for m in ms])
+        del tr, shards
+    assert runs[0] == runs[1]
+    assert runs[0][-1][2] > 10000

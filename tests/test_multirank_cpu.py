@@ -78,9 +78,10 @@ def _shard_worker(rank, world, port, q):
     comm.all_reduce([mine.view(torch.int32)], "sum")
     # halo exchange: variable record counts per rank
     m3 = 8
-    count = 2 + rank
-    keys = torch.arange(10, dtype=torch.int32) + 100 * rank
-    pays = (torch.arange(10 * m3, dtype=torch.int16).reshape(10, m3) + 1000 * rank).contiguous()
+    count = 2 + 7 * rank  # rank 1 sends more records than rank 0's buffer holds
+    cap = 4 if rank == 0 else 10
+    keys = torch.arange(cap, dtype=torch.int32) + 100 * rank
+    pays = (torch.arange(cap * m3, dtype=torch.int16).reshape(cap, m3) + 1000 * rank).contiguous()
     got = comm.exchange([(keys, pays, count)])[0]
     recs = [(k[:c].tolist(), p[:c].tolist(), c) for k, p, c in got]
     q.put((rank, ts.tolist(), te.tolist(), mine.tolist(), recs))
@@ -104,5 +105,5 @@ def test_sharded_collectives_gloo():
         other = 1 - rank
         assert len(recs) == 1
         k, p, c = recs[0]
-        assert c == 2 + other and k == [100 * other + i for i in range(c)]
+        assert c == 2 + 7 * other and k == [100 * other + i for i in range(c)]
         assert p[0][0] == 1000 * other and len(p) == c
