@@ -9,6 +9,7 @@
 // All arithmetic is FP64 in the reference's order (no contraction), so depth, normals and
 // the stage-1 sample count are bit-identical to the CPU path.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "sf_internal.h"
@@ -126,7 +127,8 @@ __device__ __forceinline__ bool dda_jump(Dda& s, double T) {
 __global__ void __launch_bounds__(256, 3) k_ray_bounds(VolParams P, const FrameConsts* __restrict__ fc, const uint32_t* __restrict__ occ,
                              const VolCounters* __restrict__ vc, float* __restrict__ t_start,
                              float* __restrict__ t_end, int w, int h, const int* dead, int* __restrict__ ray_list,
-                             RayCounters* list_ctr, float* __restrict__ depth_out, float* __restrict__ normals_out) {
+                             RayCounters* list_ctr, float* __restrict__ depth_out, float* __restrict__ normals_out,
+                             double jump_cells) {
     // Coarse occupancy (1 bit per 16^3 blocks) staged in shared memory: the DDA only reads
     // the fine bitmap (L2) inside super-blocks that ever held a block. Exact: a clear coarse
     // bit implies every block of the super-block is EMPTY.
@@ -244,6 +246,7 @@ __global__ void __launch_bounds__(256, 3) k_ray_bounds(VolParams P, const FrameC
             // the box grown by one block lies outside the occupied box.
             if (t_grown > lo + 4.0 * td_min) dda_jump(s, t_grown);
             const double sb_side = side * (1 << kCoarseShift);
+            int declined_cc = -1;  // coarse cell whose skip was judged too short to jump
             while (s.t_in <= hi) {
                 // Past the occupied box in the direction of travel: no later cell can be
                 // allocated (cells move monotonically per axis), so first/last are final.
@@ -255,7 +258,7 @@ __global__ void __launch_bounds__(256, 3) k_ray_bounds(VolParams P, const FrameC
                 const double t_out = dmin(tm, hi);
                 const int cc =
                     ((s.cz >> kCoarseShift) * P.Nc + (s.cy >> kCoarseShift)) * P.Nc + (s.cx >> kCoarseShift);
-                if (!((s_coarse[cc >> 5] >> (cc & 31)) & 1u)) {
+                if (!((s_coarse[cc >> 5] >> (cc & 31)) & 1u) && cc != declined_cc) {
                     // Super-block never held a block: jump to a quarter cell before the ray
                     // leaves it (the cells visited up to then are inside it, hence empty).
                     const int sbx = s.cx >> kCoarseShift, sby = s.cy >> kCoarseShift, sbz = s.cz >> kCoarseShift;
@@ -269,10 +272,14 @@ __global__ void __launch_bounds__(256, 3) k_ray_bounds(VolParams P, const FrameC
                     if (s.sz > 0) t_exit = dmin(t_exit, (oz_ + sb_side - org[2]) / dir[2]);
                     if (s.sz < 0) t_exit = dmin(t_exit, (oz_ - org[2]) / dir[2]);
                     const double T = dmin(t_exit, hi) - 0.25 * td_min;
-                    if (T > tm + 3.0 * td_min && dda_jump(s, T)) {
+                    // a jump costs a few hundred instructions: worth it past ~16 plain steps
+                    if (T > tm + jump_cells * td_min && dda_jump(s, T)) {
                         if (s.cx < 0 || s.cx >= n || s.cy < 0 || s.cy >= n || s.cz < 0 || s.cz >= n) break;
                         continue;
                     }
+                    declined_cc = cc;  // short crossing: plain steps through it (no occupancy reads)
+                } else if (cc == declined_cc) {
+                    // inside a super-block that never held a block: the cell is empty
                 } else if (s.cx >= bx0 && s.cx <= bx1 && s.cy >= by0 && s.cy <= by1 && s.cz >= bz0 && s.cz <= bz1 &&
                            occupied(occ, table_index(P, s.cx, s.cy, s.cz))) {
                     first = dmin(first, s.t_in);
@@ -536,6 +543,16 @@ __global__ void __launch_bounds__(256)
     if ((threadIdx.x & 31) == 0 && hits) atomicAdd(&stats->hit_pixels, hits);
 }
 
+// Minimum number of DDA cells an exact skip must save (a jump costs a few hundred
+// instructions; shorter crossings of empty super-blocks are stepped without occupancy reads).
+static double ray_jump_cells() {
+    static const double j = [] {
+        const char* e = std::getenv("SF_RAY_JUMP_CELLS");
+        return e ? std::atof(e) : 16.0;
+    }();
+    return j;
+}
+
 void launch_ray_bounds(Volume& v, const FrameConsts* d_fc, const Intr& intr, float* t_start, float* t_end,
                        cudaStream_t s, uint64_t* launches, const int* dead_flag, int* ray_list,
                        RayCounters* list_ctr, float* depth, float* normals) {
@@ -544,7 +561,7 @@ void launch_ray_bounds(Volume& v, const FrameConsts* d_fc, const Intr& intr, flo
     const size_t smem = ((nc * nc * nc + 31) / 32) * sizeof(uint32_t);
     if (smem > 48 * 1024) SF_CUDA(cudaFuncSetAttribute(k_ray_bounds, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_ray_bounds<<<grd, blk, smem, s>>>(v.P, d_fc, v.d_occ, v.d_vc, t_start, t_end, intr.w, intr.h, dead_flag,
-                                        ray_list, list_ctr, depth, normals);
+                                        ray_list, list_ctr, depth, normals, ray_jump_cells());
     SF_LAUNCH_CHECK();
     if (launches) *launches += 1;
 }
