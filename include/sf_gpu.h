@@ -339,6 +339,10 @@ int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, con
 int sf_tracker_set_pose(sf_tracker_t tr, const double pose[12], void* stream);
 /* Synchronises `stream` and copies the metrics of the last step. */
 int sf_tracker_fetch(sf_tracker_t tr, sf_frame_metrics* out, void* stream);
+/* Streaming: metrics of frame `frame` (one of the last two steps) without waiting for later
+ * steps. With host frames, step k's host->device copy overlaps step k-1's compute, so a
+ * caller that issues step k+1 before fetching step k pipelines input transfer and compute. */
+int sf_tracker_fetch_frame(sf_tracker_t tr, int32_t frame, sf_frame_metrics* out);
 /* Device-timed stages of the last step, in ms (CUDA events recorded inside the step /
  * graph): [0] raycast (bounds + march), [1] ICP (source normals + all iterations),
  * [2] fuse prologue (frame prep, keys, sort/unique, allocation, visibility),

@@ -226,6 +226,7 @@ PRODUCT_ONLY = {
     "tracker_destroy": (C.c_int, [vp]),
     "tracker_step": (C.c_int, [vp, P(FrameC), i32, c_double_p, vp]),
     "tracker_fetch": (C.c_int, [vp, P(FrameMetricsC), vp]),
+    "tracker_fetch_frame": (C.c_int, [vp, i32, P(FrameMetricsC)]),
     "tracker_set_pose": (C.c_int, [vp, c_double_p, vp]),
     "tracker_device_pose": (C.c_int, [vp, P(c_double_p)]),
     "tracker_last_launch_count": (C.c_int, [vp, u64p]),

@@ -756,9 +756,8 @@ class Tracker:
         p12 = pose.to12()
         self.grid.backend.check(self._lib.tracker_set_pose(self.handle, _dptr(p12), stream))
 
-    def fetch(self, stream=None) -> FrameMetrics:
-        m = A.FrameMetricsC()
-        self.grid.backend.check(self._lib.tracker_fetch(self.handle, C.byref(m), stream))
+    @staticmethod
+    def _metrics(m) -> "FrameMetrics":
         f = m.fusion
         r = m.raycast
         return FrameMetrics(m.frame, bool(m.registered), m.status, Pose.from12(list(m.pose)), m.iterations,
@@ -766,6 +765,18 @@ class Tracker:
                             FusionStats(f.voxels_updated, f.blocks_allocated_now, f.blocks_total, f.memory_bytes),
                             RaycastStats(r.sample_steps, r.hit_pixels, r.rays_with_bounds),
                             m.blocks_processed, m.voxels_visited, m.kernel_launches, m.exact_voxels)
+
+    def fetch(self, stream=None) -> FrameMetrics:
+        m = A.FrameMetricsC()
+        self.grid.backend.check(self._lib.tracker_fetch(self.handle, C.byref(m), stream))
+        return self._metrics(m)
+
+    def fetch_frame(self, frame: int) -> FrameMetrics:
+        """Metrics of one of the last two steps, without waiting for later ones (streaming:
+        issue step k+1, then fetch step k)."""
+        m = A.FrameMetricsC()
+        self.grid.backend.check(self._lib.tracker_fetch_frame(self.handle, frame, C.byref(m)))
+        return self._metrics(m)
 
     def stage_times(self):
         """Device-timed stages of the last step (ms): raycast, icp, fuse prologue, integrate, total."""

@@ -108,13 +108,20 @@ struct sf_tracker {
     cudaStream_t capture_stream = nullptr;  // graphs are captured here (the legacy stream cannot capture)
     cudaStream_t side_stream = nullptr;     // graph branch: deferred ICP eigenpairs, parallel to the fuse
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // Streaming host frames: the H2D copy of frame k runs on copy_stream into stage[k % 2]
+    // while frame k-1 computes; each frame's metrics are snapshotted into snap[k % 2].
+    cudaStream_t copy_stream = nullptr;
+    float* d_stage[2] = {nullptr, nullptr};
+    float* d_stage_sigma[2] = {nullptr, nullptr};
+    cudaEvent_t ev_staged[2] = {nullptr, nullptr}, ev_stage_free[2] = {nullptr, nullptr};
+    cudaEvent_t ev_snap[2] = {nullptr, nullptr};
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // stage timing (graph nodes)
     cudaGraphExec_t graph[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};  // [mode][sigma]
     uint64_t graph_kernels[3][2] = {{0, 0}, {0, 0}, {0, 0}};
     bool graph_icp_loop[3][2] = {{false, false}, {false, false}, {false, false}};
     bool issue_icp_loop = false;  // set by issue(): ICP iterations run as a device-side loop
     bool last_icp_loop = false;
-    // pinned fetch staging
+    // pinned fetch staging (also the per-frame snapshot layout)
     struct Fetch {
         double cur[12];
         double fuse_pose[12];
@@ -123,6 +130,23 @@ struct sf_tracker {
         RayCounters rs;
         IcpState icp;
     }* h = nullptr;
+    Fetch* snap = nullptr;  // pinned [2]: per-frame metric snapshots (streaming)
+    struct SnapMeta {
+        int frame, mode;
+        uint64_t launches;
+        bool icp_loop;
+    } snap_meta[2] = {};
+
+    // device buffers -> pinned host f (asynchronous on s)
+    void copy_metrics(Fetch* f, cudaStream_t s) {
+        SF_CUDA(cudaMemcpyAsync(f->cur, d_cur, sizeof(f->cur), cudaMemcpyDeviceToHost, s));
+        SF_CUDA(cudaMemcpyAsync(f->fuse_pose, fb.pose, sizeof(f->fuse_pose), cudaMemcpyDeviceToHost, s));
+        SF_CUDA(cudaMemcpyAsync(&f->td, d_td, sizeof(TrackerDev), cudaMemcpyDeviceToHost, s));
+        SF_CUDA(cudaMemcpyAsync(&f->ctr, fb.ctr, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
+        SF_CUDA(cudaMemcpyAsync(&f->rs, d_rstats, sizeof(RayCounters), cudaMemcpyDeviceToHost, s));
+        SF_CUDA(cudaMemcpyAsync(&f->icp, icp.st, sizeof(IcpState), cudaMemcpyDeviceToHost, s));
+    }
+    void decode(const Fetch* f, int frame, int mode, uint64_t launches, bool icp_loop, sf_frame_metrics* out) const;
 
     ~sf_tracker() {
         cudaSetDevice(vol ? vol->device : 0);
@@ -138,6 +162,15 @@ struct sf_tracker {
         if (side_stream) cudaStreamDestroy(side_stream);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
+        for (int i = 0; i < 2; ++i) {
+            if (d_stage[i]) cudaFree(d_stage[i]);
+            if (d_stage_sigma[i]) cudaFree(d_stage_sigma[i]);
+            if (ev_staged[i]) cudaEventDestroy(ev_staged[i]);
+            if (ev_stage_free[i]) cudaEventDestroy(ev_stage_free[i]);
+            if (ev_snap[i]) cudaEventDestroy(ev_snap[i]);
+        }
+        if (snap) cudaFreeHost(snap);
         for (auto e : ev)
             if (e) cudaEventDestroy(e);
     }
@@ -237,6 +270,16 @@ int sf_tracker_create(sf_volume_t vol, const sf_tracker_config* config, const do
         SF_CUDA(cudaMallocHost(&t->h, sizeof(sf_tracker::Fetch)));
         for (auto& e : t->ev) SF_CUDA(cudaEventCreate(&e));
         SF_CUDA(cudaStreamCreateWithFlags(&t->side_stream, cudaStreamNonBlocking));
+        SF_CUDA(cudaStreamCreateWithFlags(&t->copy_stream, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            SF_CUDA(cudaMalloc(&t->d_stage[i], n * sizeof(float)));
+            SF_CUDA(cudaMalloc(&t->d_stage_sigma[i], n * sizeof(float)));
+            SF_CUDA(cudaEventCreateWithFlags(&t->ev_staged[i], cudaEventDisableTiming));
+            SF_CUDA(cudaEventCreateWithFlags(&t->ev_stage_free[i], cudaEventDisableTiming));
+            SF_CUDA(cudaEventCreateWithFlags(&t->ev_snap[i], cudaEventDisableTiming));
+        }
+        SF_CUDA(cudaMallocHost(&t->snap, 2 * sizeof(sf_tracker::Fetch)));
+        std::memset(t->snap, 0, 2 * sizeof(sf_tracker::Fetch));
         SF_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
         SF_CUDA(cudaEventCreateWithFlags(&t->ev_join, cudaEventDisableTiming));
         std::memset(t->h, 0, sizeof(sf_tracker::Fetch));
@@ -261,10 +304,29 @@ int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, con
         SF_CUDA(cudaSetDevice(tr->vol->device));
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         const size_t n = static_cast<size_t>(tr->cam.w) * tr->cam.h;
-        const cudaMemcpyKind kind = captured->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-        SF_CUDA(cudaMemcpyAsync(tr->d_cap, captured->depth, n * sizeof(float), kind, s));
         const bool has_sigma = captured->sigma != nullptr;
-        if (has_sigma) SF_CUDA(cudaMemcpyAsync(tr->d_cap_sigma, captured->sigma, n * sizeof(float), kind, s));
+        const int slot = tr->frames & 1;
+        if (captured->on_device) {
+            SF_CUDA(cudaMemcpyAsync(tr->d_cap, captured->depth, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+            if (has_sigma)
+                SF_CUDA(cudaMemcpyAsync(tr->d_cap_sigma, captured->sigma, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        } else {
+            // Host frame: the H2D copy runs on the copy stream into a staging buffer, so it
+            // overlaps the previous frame's compute; the frame then starts with a D2D copy.
+            SF_CUDA(cudaStreamWaitEvent(tr->copy_stream, tr->ev_stage_free[slot], 0));
+            SF_CUDA(cudaMemcpyAsync(tr->d_stage[slot], captured->depth, n * sizeof(float), cudaMemcpyHostToDevice,
+                                    tr->copy_stream));
+            if (has_sigma)
+                SF_CUDA(cudaMemcpyAsync(tr->d_stage_sigma[slot], captured->sigma, n * sizeof(float),
+                                        cudaMemcpyHostToDevice, tr->copy_stream));
+            SF_CUDA(cudaEventRecord(tr->ev_staged[slot], tr->copy_stream));
+            SF_CUDA(cudaStreamWaitEvent(s, tr->ev_staged[slot], 0));
+            SF_CUDA(cudaMemcpyAsync(tr->d_cap, tr->d_stage[slot], n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+            if (has_sigma)
+                SF_CUDA(cudaMemcpyAsync(tr->d_cap_sigma, tr->d_stage_sigma[slot], n * sizeof(float),
+                                        cudaMemcpyDeviceToDevice, s));
+            SF_CUDA(cudaEventRecord(tr->ev_stage_free[slot], s));
+        }
         // First frame: fuse at the current (initial) pose without registration (pipeline.cpp:250-252).
         // internal modes: 0 track, 1 ground truth, 2 fuse at current (first frame), 3 track with
         // an external initial delta (tracking.mode = icp_with_hook, pipeline.cpp:262-266)
@@ -305,6 +367,11 @@ int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, con
             tr->last_icp_loop = tr->issue_icp_loop;
         }
         tr->last_mode = eff;
+        // metric snapshot of this frame (read by sf_tracker_fetch_frame without waiting for
+        // frames issued later)
+        tr->copy_metrics(&tr->snap[slot], s);
+        SF_CUDA(cudaEventRecord(tr->ev_snap[slot], s));
+        tr->snap_meta[slot] = {tr->frames, eff, tr->last_launches, tr->last_icp_loop};
         ++tr->frames;
         return SF_OK;
     });
@@ -319,46 +386,59 @@ int sf_tracker_set_pose(sf_tracker_t tr, const double pose[12], void* stream) {
     });
 }
 
+void sf_tracker::decode(const Fetch* f, int frame, int mode, uint64_t launches, bool icp_loop,
+                        sf_frame_metrics* out) const {
+    std::memset(out, 0, sizeof(*out));
+    out->frame = frame;
+    out->status = f->td.status;
+    out->registered = (mode == 0 || mode == 3) ? f->td.registered : 0;
+    std::memcpy(out->pose, f->fuse_pose, sizeof(out->pose));
+    if (out->registered) {
+        out->iterations = f->icp.iterations;
+        out->matches = f->icp.matches;
+        out->residual_rms = f->icp.residual_rms;
+        for (int i = 0; i < 6; ++i) {
+            out->lambda_over_n[i] = f->icp.eigenvalues[i] / static_cast<double>(f->icp.pair_count);
+            out->gated_mask[i] = f->icp.gated[i];
+        }
+    }
+    const uint64_t nn = vol->P.N, m = vol->P.M;
+    out->fusion.voxels_updated = f->ctr.voxels_updated;
+    out->fusion.blocks_allocated_now = f->ctr.alloc_now - f->ctr.alloc_before;
+    out->fusion.blocks_total = f->ctr.alloc_now;
+    out->fusion.memory_bytes = 2ull * f->ctr.alloc_now * m * m * m + 4ull * nn * nn * nn;
+    out->raycast.sample_steps = f->rs.sample_steps;
+    out->raycast.hit_pixels = f->rs.hit_pixels;
+    out->raycast.rays_with_bounds = f->rs.rays_with_bounds;
+    out->blocks_processed = static_cast<uint64_t>(f->ctr.limit) + f->ctr.n_update;
+    if (f->ctr.skip) out->blocks_processed = 0;
+    out->voxels_visited = out->blocks_processed * m * m * m;
+    out->exact_voxels = f->ctr.exact_voxels;
+    out->kernel_launches = launches;
+    if (icp_loop) out->kernel_launches += static_cast<uint64_t>(f->icp.bodies);
+}
+
 int sf_tracker_fetch(sf_tracker_t tr, sf_frame_metrics* out, void* stream) {
     return guarded([&]() -> int {
         SF_CUDA(cudaSetDevice(tr->vol->device));
         cudaStream_t s = static_cast<cudaStream_t>(stream);
-        auto* h = tr->h;
-        SF_CUDA(cudaMemcpyAsync(h->cur, tr->d_cur, sizeof(h->cur), cudaMemcpyDeviceToHost, s));
-        SF_CUDA(cudaMemcpyAsync(h->fuse_pose, tr->fb.pose, sizeof(h->fuse_pose), cudaMemcpyDeviceToHost, s));
-        SF_CUDA(cudaMemcpyAsync(&h->td, tr->d_td, sizeof(TrackerDev), cudaMemcpyDeviceToHost, s));
-        SF_CUDA(cudaMemcpyAsync(&h->ctr, tr->fb.ctr, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
-        SF_CUDA(cudaMemcpyAsync(&h->rs, tr->d_rstats, sizeof(RayCounters), cudaMemcpyDeviceToHost, s));
-        SF_CUDA(cudaMemcpyAsync(&h->icp, tr->icp.st, sizeof(IcpState), cudaMemcpyDeviceToHost, s));
+        tr->copy_metrics(tr->h, s);
         SF_CUDA(cudaStreamSynchronize(s));
-        std::memset(out, 0, sizeof(*out));
-        out->frame = tr->frames - 1;
-        out->status = h->td.status;
-        out->registered = (tr->last_mode == 0 || tr->last_mode == 3) ? h->td.registered : 0;
-        std::memcpy(out->pose, h->fuse_pose, sizeof(out->pose));
-        if (out->registered) {
-            out->iterations = h->icp.iterations;
-            out->matches = h->icp.matches;
-            out->residual_rms = h->icp.residual_rms;
-            for (int i = 0; i < 6; ++i) {
-                out->lambda_over_n[i] = h->icp.eigenvalues[i] / static_cast<double>(h->icp.pair_count);
-                out->gated_mask[i] = h->icp.gated[i];
-            }
-        }
-        const uint64_t nn = tr->vol->P.N, m = tr->vol->P.M;
-        out->fusion.voxels_updated = h->ctr.voxels_updated;
-        out->fusion.blocks_allocated_now = h->ctr.alloc_now - h->ctr.alloc_before;
-        out->fusion.blocks_total = h->ctr.alloc_now;
-        out->fusion.memory_bytes = 2ull * h->ctr.alloc_now * m * m * m + 4ull * nn * nn * nn;
-        out->raycast.sample_steps = h->rs.sample_steps;
-        out->raycast.hit_pixels = h->rs.hit_pixels;
-        out->raycast.rays_with_bounds = h->rs.rays_with_bounds;
-        out->blocks_processed = static_cast<uint64_t>(h->ctr.limit) + h->ctr.n_update;
-        if (h->ctr.skip) out->blocks_processed = 0;
-        out->voxels_visited = out->blocks_processed * m * m * m;
-        out->exact_voxels = h->ctr.exact_voxels;
-        out->kernel_launches = tr->last_launches;
-        if (tr->last_icp_loop) out->kernel_launches += static_cast<uint64_t>(h->icp.bodies);
+        tr->decode(tr->h, tr->frames - 1, tr->last_mode, tr->last_launches, tr->last_icp_loop, out);
+        return SF_OK;
+    });
+}
+
+int sf_tracker_fetch_frame(sf_tracker_t tr, int32_t frame, sf_frame_metrics* out) {
+    return guarded([&]() -> int {
+        if (!tr || !out) throw Error(SF_INVALID_ARGUMENT, "sf_tracker_fetch_frame: null argument");
+        if (frame < 0 || frame >= tr->frames || frame < tr->frames - 2)
+            throw Error(SF_OUT_OF_RANGE, "sf_tracker_fetch_frame: only the last two frames are kept");
+        SF_CUDA(cudaSetDevice(tr->vol->device));
+        const int slot = frame & 1;
+        const auto& mt = tr->snap_meta[slot];
+        SF_CUDA(cudaEventSynchronize(tr->ev_snap[slot]));
+        tr->decode(&tr->snap[slot], mt.frame, mt.mode, mt.launches, mt.icp_loop, out);
         return SF_OK;
     });
 }

@@ -506,3 +506,31 @@ def test_fuse_refinement_bit_exact(gpu, ref, mode, steps):
         assert sg == sr
         assert_same_volume(g, r)
     assert sr.voxels_updated > 1000
+
+
+def test_tracker_streaming_fetch_matches_synchronous(gpu):
+    """Host frames streamed (step k+1 issued before fetching step k; H2D overlaps compute)
+    give the same per-frame metrics as step/fetch in lockstep."""
+    intr = scenes.camera(320, 240, 262.5)
+    cfg = scenes.c1_config()
+    poses = scenes.c1_trajectory(100)[:8]
+    frames = [gpu.render_synthetic_depth(scenes.sphere_plane_scene(), p, intr, sigma0=2.5e-4, seed=21 + k,
+                                         domain_size=2.0) for k, p in enumerate(poses)]
+    fusion = sf.FusionParams(mode=sf.FusionMode.Kalman)
+    match = sf.MatchParams.for_voxel_size(cfg.voxel_size)
+    runs = []
+    for streaming in (False, True):
+        grid = sf.SparseTsdfGrid(cfg, 0, sf.AuxMode.Variance)
+        tr = sf.Tracker(grid, intr, fusion, match, poses[0])
+        out = []
+        for k, f in enumerate(frames):
+            tr.step(f, sf.Tracker.TRACK)
+            if not streaming:
+                out.append(tr.fetch())
+            elif k > 0:
+                out.append(tr.fetch_frame(k - 1))
+        if streaming:
+            out.append(tr.fetch_frame(len(frames) - 1))
+        runs.append([(m.frame, m.pose.to12().tobytes(), m.matches, m.fusion.voxels_updated, m.fusion.blocks_total,
+                      m.raycast.hit_pixels) for m in out])
+    assert runs[0] == runs[1]
