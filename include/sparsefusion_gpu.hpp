@@ -403,6 +403,12 @@ public:
         if (m.status == SF_POOL_EXHAUSTED) throw PoolExhausted("grid: payload pool exhausted");
         return m;
     }
+    // streaming: metrics of one of the last two steps, without waiting for later steps
+    sf_frame_metrics fetch_frame(int frame) {
+        sf_frame_metrics m{};
+        check(sf_tracker_fetch_frame(h_, frame, &m));
+        return m;
+    }
 
 private:
     sf_tracker_t h_ = nullptr;
