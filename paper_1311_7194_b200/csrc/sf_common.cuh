@@ -271,6 +271,9 @@ struct FrameConsts {
     d3 sat_axis[kSatAxes];
     double sat_lo[kSatAxes], sat_hi[kSatAxes];
     int sat_valid[kSatAxes];
+    // Inward unit normals (camera frame) of the four side faces of the frustum pyramid: a
+    // conservative "block strictly inside" test that skips the SAT for most blocks.
+    d3 side_n[4];
 };
 
 // Fusion parameters (fusion.hpp:18-31) resolved on the host.

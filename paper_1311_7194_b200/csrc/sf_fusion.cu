@@ -60,6 +60,15 @@ __global__ void k_frame_consts(VolParams P, Intr intr, const double* __restrict_
     } else if (lane < 12) {
         const int r = lane - 8;  // r00, r10, r01, r11
         s_rays[r] = normalized(mv(pose.R, unproject(intr, us[r & 1], vs[r >> 1], 1.0)));
+    } else if (lane < 16) {
+        // side face through the camera centre and two image corners, in the camera frame,
+        // oriented so the optical axis is inside
+        const int f = lane - 12;  // top (v = -0.5), bottom, left (u = -0.5), right
+        const d3 a = f < 2 ? unproject(intr, us[0], vs[f], 1.0) : unproject(intr, us[f - 2], vs[0], 1.0);
+        const d3 b = f < 2 ? unproject(intr, us[1], vs[f], 1.0) : unproject(intr, us[f - 2], vs[1], 1.0);
+        d3 nrm = normalized(cross(a, b));
+        if (nrm.z < 0.0) nrm = neg(nrm);
+        fc->side_n[f] = nrm;
     }
     __syncwarp();
     if (lane < kSatAxes) {
@@ -409,6 +418,19 @@ __device__ __forceinline__ bool in_sorted(const uint32_t* __restrict__ a, uint32
     return lo < n && a[lo] == key;
 }
 
+// Conservative: the block's bounding sphere lies strictly inside the frustum (margins far
+// above rounding), hence the exact SAT (grid.cpp:228-269) would report an intersection.
+__device__ __forceinline__ bool block_surely_inside(const VolParams& P, const FrameConsts* __restrict__ fc, d3 lo) {
+    const double hs = 0.5 * P.block_side;
+    const d3 c = apply(fc->inv, add(lo, mk(hs, hs, hs)));
+    const double r = hs * 1.7320508075688772 * (1.0 + 1e-9) + 1e-12;
+    if (!(c.z - r > fc->intr.near_plane * (1.0 + 1e-9) && c.z + r < fc->intr.far_plane * (1.0 - 1e-9))) return false;
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+        if (!(dot(fc->side_n[f], c) > r)) return false;
+    return true;
+}
+
 __global__ void k_visible(VolParams P, const FrameConsts* __restrict__ fc, FrameCounters* ctr,
                           const VolCounters* __restrict__ vc, const int32_t* __restrict__ slot_key,
                           const uint32_t* __restrict__ uniq, const float* __restrict__ depth, int w, int h,
@@ -428,7 +450,7 @@ __global__ void k_visible(VolParams P, const FrameConsts* __restrict__ fc, Frame
         const d3 lo = block_min_corner(P, bx, by, bz);
         const double side = P.block_side;
         const d3 hi = add(lo, mk(side, side, side));
-        if (!frustum_intersects_block(P, fc, lo, hi)) continue;
+        if (!block_surely_inside(P, fc, lo) && !frustum_intersects_block(P, fc, lo, hi)) continue;
         bool visible = false;
         for (int i = 0; i < 9 && !visible; ++i) {
             const d3 probe = i == 8 ? add(lo, mk(0.5 * side, 0.5 * side, 0.5 * side))
@@ -491,7 +513,7 @@ __global__ void k_worklist(VolParams P, const FrameConsts* __restrict__ fc, Fram
             const double side = P.block_side;
             const d3 hi = add(lo, mk(side, side, side));
             // a sharded volume integrates only its own blocks (mirrored halo blocks are read-only)
-            if (shard_owns(P, bx, by, bz) && frustum_intersects_block(P, fc, lo, hi)) {
+            if (shard_owns(P, bx, by, bz) && (block_surely_inside(P, fc, lo) || frustum_intersects_block(P, fc, lo, hi))) {
                 for (int k = 0; k < 9 && !vis; ++k) {
                     const d3 probe = k == 8 ? add(lo, mk(0.5 * side, 0.5 * side, 0.5 * side))
                                             : add(lo, mk(k & 1 ? side : 0.0, k & 2 ? side : 0.0, k & 4 ? side : 0.0));
