@@ -466,7 +466,7 @@ def run_sharded(args, world, rank, local):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
-    if world > 1:
+    if world > 1 or args.sharded_nccl:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
@@ -541,7 +541,7 @@ def run_sharded(args, world, rank, local):
             "workload": "C5: 8192^3 sparse @ 0.15 mm (N=1024, M=8) block pool sharded by 8^3-block brick "
                         f"across {nshards} ranks, halo exchange + global ray bounds + nearest-depth composite "
                         "(NCCL), ICP on the composite, 640x480, Kalman, icp_with_hook",
-            "shards": nshards, "emulated_on_one_gpu": world == 1, "frames": nframes,
+            "shards": nshards, "emulated_on_one_gpu": isinstance(comm, shard.LocalComm), "frames": nframes,
             "pool_per_rank": pool, "l2": "flushed (400 MB write) between timed steps",
             "parallelism": f"block-pool shards x{nshards}", "relocalise_every": c["reseed"],
         },
@@ -605,12 +605,14 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--local-shards", type=int, default=0,
                     help="run the sharded C5 loop as this many emulated ranks on one GPU")
+    ap.add_argument("--sharded-nccl", action="store_true",
+                    help="run the sharded C5 loop over NCCL even with one rank (torchrun, for testing)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world, rank, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, world, rank, local)
-    elif world > 1 or args.local_shards > 0:
+    elif world > 1 or args.local_shards > 0 or args.sharded_nccl:
         run_sharded(args, world, rank, local)
     else:
         run_ours(args, world, rank, local)
