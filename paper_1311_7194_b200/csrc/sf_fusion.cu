@@ -1404,9 +1404,31 @@ static void launch_integrate_rows(Volume& v, FrameBuffers& fb, const FuseParams&
         v.d_payload, fb.keys_unique, v.d_keybits);
 }
 
+// Frame prep of fuse_frame (depends only on the frame): normals with the fusion options
+// (sigma0, spatial_scale = 0.25 * delta; fusion.cpp:33-36), edge mask, per-pixel measurement
+// factors (fusion.cpp:40-72, 148-171).
+void launch_fuse_prep(Volume& v, FrameBuffers& fb, const Intr& intr, const float* depth, const float* sigma,
+                      const FuseParams& fp, cudaStream_t s, uint64_t* launches, const int* dead) {
+    const int w = fb.w, h = fb.h;
+    const dim3 blk2(32, 8), grd2((w + 31) / 32, (h + 7) / 8);
+    uint64_t n = 0;
+    if (fp.downweight) {
+        k_normals<<<grd2, blk2, 0, s>>>(depth, w, h, intr, fp.sigma0, 0.25 * v.P.delta, fb.normals, dead);
+        SF_LAUNCH_CHECK();
+        k_edge<<<grd2, blk2, 0, s>>>(depth, w, h, fp.sigma0, fb.edge, dead);
+        SF_LAUNCH_CHECK();
+        n += 2;
+    }
+    k_pixel_meas<<<grd2, blk2, 0, s>>>(depth, sigma, w, h, intr, fp, fb.normals, fb.edge, fb.pix_var, fb.pix_w,
+                                        fb.pix_ok, fb.pix_dm, fb.pix_f, fb.pix_q, dead);
+    SF_LAUNCH_CHECK();
+    n += 1;
+    if (launches) *launches += n;
+}
+
 void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* depth, const float* sigma,
                  const FuseParams& fp, cudaStream_t s, bool export_only, uint64_t* launches, const int* dead_flag,
-                 const FuseEvents* events) {
+                 const FuseEvents* events, bool prep_done) {
     const int w = fb.w, h = fb.h;
     const VolParams& P = v.P;
     uint64_t n = 0;
@@ -1416,21 +1438,7 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
     n += 1;
     const dim3 blk2(32, 8), grd2((w + 31) / 32, (h + 7) / 8);
     const int* dead = reinterpret_cast<const int*>(&fb.ctr->skip);
-    if (!export_only) {
-        // Frame prep: normals with the fusion options (sigma0, spatial_scale = 0.25 * delta;
-        // fusion.cpp:33-36), edge mask, per-pixel measurement factors.
-        if (fp.downweight) {
-            k_normals<<<grd2, blk2, 0, s>>>(depth, w, h, intr, fp.sigma0, 0.25 * P.delta, fb.normals, dead);
-            SF_LAUNCH_CHECK();
-            k_edge<<<grd2, blk2, 0, s>>>(depth, w, h, fp.sigma0, fb.edge, dead);
-            SF_LAUNCH_CHECK();
-            n += 2;
-        }
-        k_pixel_meas<<<grd2, blk2, 0, s>>>(depth, sigma, w, h, intr, fp, fb.normals, fb.edge, fb.pix_var, fb.pix_w,
-                                            fb.pix_ok, fb.pix_dm, fb.pix_f, fb.pix_q, dead);
-        SF_LAUNCH_CHECK();
-        n += 1;
-    }
+    if (!export_only && !prep_done) launch_fuse_prep(v, fb, intr, depth, sigma, fp, s, &n, dead);
     const int su = (w + fb.stride - 1) / fb.stride, sv = (h + fb.stride - 1) / fb.stride;
     if (export_only) {
         // select_update_blocks: the ordered lists themselves are the output -> sorted

@@ -172,9 +172,12 @@ void launch_consts(const VolParams& P, const Intr& intr, const double* d_pose, F
 struct FuseEvents {
     cudaEvent_t before_integrate = nullptr, after_integrate = nullptr;
 };
+// prep_done: launch_fuse_prep already ran for this frame (e.g. on a parallel graph branch).
 void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* depth, const float* sigma,
                  const FuseParams& fp, cudaStream_t s, bool export_lists_only, uint64_t* launches,
-                 const int* dead_flag, const FuseEvents* events = nullptr);
+                 const int* dead_flag, const FuseEvents* events = nullptr, bool prep_done = false);
+void launch_fuse_prep(Volume& v, FrameBuffers& fb, const Intr& intr, const float* depth, const float* sigma,
+                      const FuseParams& fp, cudaStream_t s, uint64_t* launches, const int* dead);
 // With ray_list (+ list_ctr, depth, normals) the pass also appends every pixel with
 // non-empty bounds to ray_list (length in list_ctr->listed, which must start at 0) and
 // writes the empty raycast result (0 depth / normal) for the others.

@@ -107,7 +107,7 @@ struct sf_tracker {
     uint64_t last_launches = 0;
     cudaStream_t capture_stream = nullptr;  // graphs are captured here (the legacy stream cannot capture)
     cudaStream_t side_stream = nullptr;     // graph branch: deferred ICP eigenpairs, parallel to the fuse
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_prep_fork = nullptr, ev_prep_join = nullptr;
     // Streaming host frames: the H2D copy of frame k runs on copy_stream into stage[k % 2]
     // while frame k-1 computes; each frame's metrics are snapshotted into snap[k % 2].
     cudaStream_t copy_stream = nullptr;
@@ -162,6 +162,8 @@ struct sf_tracker {
         if (side_stream) cudaStreamDestroy(side_stream);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
+        if (ev_prep_fork) cudaEventDestroy(ev_prep_fork);
+        if (ev_prep_join) cudaEventDestroy(ev_prep_join);
         if (copy_stream) cudaStreamDestroy(copy_stream);
         for (int i = 0; i < 2; ++i) {
             if (d_stage[i]) cudaFree(d_stage[i]);
@@ -184,7 +186,17 @@ struct sf_tracker {
         record_event(ev[0], s);
         issue_icp_loop = false;
         bool joined = true;
+        bool prep_done = false;
         if (mode == 0 || mode == 3) {
+            // Branch: everything that depends only on the captured frame (ICP source normals,
+            // the fusion's normals / edge mask / per-pixel factors) runs beside the raycast.
+            SF_CUDA(cudaEventRecord(ev_prep_fork, s));
+            SF_CUDA(cudaStreamWaitEvent(side_stream, ev_prep_fork, 0));
+            launch_compute_normals(d_cap, cam.w, cam.h, cam, cfg.match.normal_sigma0, cfg.match.normal_spatial_scale,
+                                   icp.src_normals, side_stream, &n, dead);
+            launch_fuse_prep(*vol, fb, cam, d_cap, sig, p, side_stream, &n, dead);
+            SF_CUDA(cudaEventRecord(ev_prep_join, side_stream));
+            prep_done = true;
             k_tracker_begin_track<<<1, 1, 0, s>>>(d_cur, mode == 3 ? d_gt : nullptr, d_init_delta, d_rstats, d_td);
             SF_LAUNCH_CHECK();
             ++n;
@@ -194,8 +206,7 @@ struct sf_tracker {
             launch_raycast(*vol, d_rc_fc, cam, d_ts, d_te, d_model_depth, d_model_normals, d_rstats, s, &n, dead,
                            d_ray_list, d_brackets);
             record_event(ev[1], s);
-            launch_compute_normals(d_cap, cam.w, cam.h, cam, cfg.match.normal_sigma0, cfg.match.normal_spatial_scale,
-                                   icp.src_normals, s, &n, dead);
+            SF_CUDA(cudaStreamWaitEvent(s, ev_prep_join, 0));
             launch_icp(icp, d_cap, icp.src_normals, d_model_depth, d_model_normals, cam, cam, d_init_delta, icp_prm, s,
                        &n, dead, &issue_icp_loop);
             k_tracker_after_icp<<<1, 1, 0, s>>>(d_cur, fb.pose, icp.st, d_td, cfg.orthonormalize);
@@ -218,7 +229,7 @@ struct sf_tracker {
         FuseEvents fe;
         fe.before_integrate = ev[3];
         fe.after_integrate = ev[4];
-        launch_fuse(*vol, fb, cam, d_cap, sig, p, s, false, &n, dead, &fe);
+        launch_fuse(*vol, fb, cam, d_cap, sig, p, s, false, &n, dead, &fe, prep_done);
         if (!joined) {
             SF_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
             joined = true;
@@ -282,6 +293,8 @@ int sf_tracker_create(sf_volume_t vol, const sf_tracker_config* config, const do
         std::memset(t->snap, 0, 2 * sizeof(sf_tracker::Fetch));
         SF_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
         SF_CUDA(cudaEventCreateWithFlags(&t->ev_join, cudaEventDisableTiming));
+        SF_CUDA(cudaEventCreateWithFlags(&t->ev_prep_fork, cudaEventDisableTiming));
+        SF_CUDA(cudaEventCreateWithFlags(&t->ev_prep_join, cudaEventDisableTiming));
         std::memset(t->h, 0, sizeof(sf_tracker::Fetch));
         *out = t.release();
         return SF_OK;
