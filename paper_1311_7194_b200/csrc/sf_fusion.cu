@@ -37,77 +37,12 @@ constexpr int kSmallCtas = 148;  // passes over the <= 57.6 k allocate-list keys
 // ---------------------------------------------------------------------------------
 __global__ void k_frame_consts(VolParams P, Intr intr, const double* __restrict__ pose12, FrameConsts* fc) {
     if (blockIdx.x != 0) return;
-    const int lane = threadIdx.x;
-    __shared__ d3 s_pts[8], s_rays[4];
-    __shared__ Pose s_pose;
-    if (lane == 0) {
-        const Pose pose = pose_from12(pose12);
-        s_pose = pose;
-        fc->pose = pose;
-        fc->inv = invert(pose);
-        fc->intr = intr;
-        fc->delta = P.delta;
-    }
-    __syncwarp();
-    const Pose pose = s_pose;
-    // Frustum hull and separating axes, exactly as occupied_blocks_in_frustum builds them
-    // (grid.cpp:228-262): hull points near/far x v x u, corner rays, 26 candidate axes.
-    const double us[2] = {-0.5, intr.w - 0.5};
-    const double vs[2] = {-0.5, intr.h - 0.5};
-    if (lane < 8) {
-        const double zs[2] = {intr.near_plane, intr.far_plane};
-        s_pts[lane] = apply(pose, unproject(intr, us[lane & 1], vs[(lane >> 1) & 1], zs[lane >> 2]));
-    } else if (lane < 12) {
-        const int r = lane - 8;  // r00, r10, r01, r11
-        s_rays[r] = normalized(mv(pose.R, unproject(intr, us[r & 1], vs[r >> 1], 1.0)));
-    } else if (lane < 16) {
-        // side face through the camera centre and two image corners, in the camera frame,
-        // oriented so the optical axis is inside
-        const int f = lane - 12;  // top (v = -0.5), bottom, left (u = -0.5), right
-        const d3 a = f < 2 ? unproject(intr, us[0], vs[f], 1.0) : unproject(intr, us[f - 2], vs[0], 1.0);
-        const d3 b = f < 2 ? unproject(intr, us[1], vs[f], 1.0) : unproject(intr, us[f - 2], vs[1], 1.0);
-        d3 nrm = normalized(cross(a, b));
-        if (nrm.z < 0.0) nrm = neg(nrm);
-        fc->side_n[f] = nrm;
-    }
-    __syncwarp();
-    if (lane < kSatAxes) {
-        const d3 r00 = s_rays[0], r10 = s_rays[1], r01 = s_rays[2], r11 = s_rays[3];
-        const d3 box_axes[3] = {mk(1, 0, 0), mk(0, 1, 0), mk(0, 0, 1)};
-        d3 ax;
-        if (lane < 3) ax = box_axes[lane];
-        else if (lane == 3) ax = col(pose.R, 2);  // optical axis
-        else if (lane == 4) ax = cross(r00, r10);  // top
-        else if (lane == 5) ax = cross(r11, r01);  // bottom
-        else if (lane == 6) ax = cross(r01, r00);  // left
-        else if (lane == 7) ax = cross(r10, r11);  // right
-        else {
-            const int e = (lane - 8) / 3, b = (lane - 8) % 3;
-            const d3 edges[6] = {r00, r10, r01, r11, col(pose.R, 0), col(pose.R, 1)};
-            ax = cross(edges[e], box_axes[b]);
-        }
-        fc->sat_axis[lane] = ax;
-        fc->sat_valid[lane] = !(sqnorm(ax) < 1e-18);
-        double lo = INFINITY, hi = -INFINITY;
-        for (int i = 0; i < 8; ++i) {
-            const double d = dot(ax, s_pts[i]);
-            lo = dmin(lo, d);
-            hi = dmax(hi, d);
-        }
-        fc->sat_lo[lane] = lo;
-        fc->sat_hi[lane] = hi;
-    }
+    frame_consts_warp(P, intr, pose12, fc);
 }
 
 // Zero the per-frame counters; a set dead flag (tracker: tracking lost / pool exhausted
 // earlier) turns every later kernel of the frame into a no-op.
-__global__ void k_fuse_begin(FrameCounters* ctr, const VolCounters* vc, const int* dead) {
-    FrameCounters z;
-    memset(&z, 0, sizeof(z));
-    z.alloc_before = vc->allocated_count - vc->halo_count;  // owned blocks only
-    z.skip = dead ? static_cast<uint32_t>(*dead != 0) : 0u;
-    *ctr = z;
-}
+__global__ void k_fuse_begin(FrameCounters* ctr, const VolCounters* vc, const int* dead) { fuse_begin_body(ctr, vc, dead); }
 
 // ---------------------------------------------------------------------------------
 // frame preparation
@@ -1322,9 +1257,7 @@ __global__ void __launch_bounds__(kThreads)
     if ((threadIdx.x & 31) == 0 && updated) atomicAdd(voxels_updated, updated);
 }
 
-__global__ void k_fuse_finalize(FrameCounters* ctr, const VolCounters* vc) {
-    ctr->alloc_now = vc->allocated_count - vc->halo_count;
-}
+__global__ void k_fuse_finalize(FrameCounters* ctr, const VolCounters* vc) { fuse_finalize_body(ctr, vc); }
 
 // ---------------------------------------------------------------------------------
 // host launchers
@@ -1428,14 +1361,16 @@ void launch_fuse_prep(Volume& v, FrameBuffers& fb, const Intr& intr, const float
 
 void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* depth, const float* sigma,
                  const FuseParams& fp, cudaStream_t s, bool export_only, uint64_t* launches, const int* dead_flag,
-                 const FuseEvents* events, bool prep_done) {
+                 const FuseEvents* events, bool prep_done, bool caller_brackets) {
     const int w = fb.w, h = fb.h;
     const VolParams& P = v.P;
     uint64_t n = 0;
-    launch_consts(P, intr, fb.pose, fb.fc, s, &n);
-    k_fuse_begin<<<1, 1, 0, s>>>(fb.ctr, v.d_vc, dead_flag);
-    SF_LAUNCH_CHECK();
-    n += 1;
+    if (!caller_brackets) {  // else the caller ran frame_consts_warp + fuse_begin_body in its own kernel
+        launch_consts(P, intr, fb.pose, fb.fc, s, &n);
+        k_fuse_begin<<<1, 1, 0, s>>>(fb.ctr, v.d_vc, dead_flag);
+        SF_LAUNCH_CHECK();
+        n += 1;
+    }
     const dim3 blk2(32, 8), grd2((w + 31) / 32, (h + 7) / 8);
     const int* dead = reinterpret_cast<const int*>(&fb.ctr->skip);
     if (!export_only && !prep_done) launch_fuse_prep(v, fb, intr, depth, sigma, fp, s, &n, dead);
@@ -1509,9 +1444,12 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
 #undef SF_INTEGRATE_ROWS
         SF_LAUNCH_CHECK();
         if (events && events->after_integrate) record_event(events->after_integrate, s);
-        k_fuse_finalize<<<1, 1, 0, s>>>(fb.ctr, v.d_vc);
-        SF_LAUNCH_CHECK();
-        n += 2;
+        n += 1;
+        if (!caller_brackets) {
+            k_fuse_finalize<<<1, 1, 0, s>>>(fb.ctr, v.d_vc);
+            SF_LAUNCH_CHECK();
+            n += 1;
+        }
     }
     if (launches) *launches += n;
 }

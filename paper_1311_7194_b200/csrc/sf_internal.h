@@ -175,7 +175,10 @@ struct FuseEvents {
 // prep_done: launch_fuse_prep already ran for this frame (e.g. on a parallel graph branch).
 void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* depth, const float* sigma,
                  const FuseParams& fp, cudaStream_t s, bool export_lists_only, uint64_t* launches,
-                 const int* dead_flag, const FuseEvents* events = nullptr, bool prep_done = false);
+                 const int* dead_flag, const FuseEvents* events = nullptr, bool prep_done = false,
+                 bool caller_brackets = false);
+// caller_brackets: the caller ran frame_consts_warp + fuse_begin_body (sf_sample.cuh) before
+// and runs fuse_finalize_body after (tracker kernels that merge them with their own work).
 void launch_fuse_prep(Volume& v, FrameBuffers& fb, const Intr& intr, const float* depth, const float* sigma,
                       const FuseParams& fp, cudaStream_t s, uint64_t* launches, const int* dead);
 // With ray_list (+ list_ctr, depth, normals) the pass also appends every pixel with

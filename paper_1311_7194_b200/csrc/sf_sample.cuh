@@ -226,4 +226,81 @@ __device__ inline bool frustum_intersects_block(const VolParams& P, const FrameC
     return true;
 }
 
+// ---- per-frame setup shared by the fusion and tracker kernels -------------------------
+// frame constants: one warp (hull points, corner rays and SAT axes lane-parallel)
+__device__ inline void frame_consts_warp(const VolParams& P, const Intr& intr, const double* __restrict__ pose12,
+                                  FrameConsts* fc) {
+    const int lane = threadIdx.x & 31;
+    __shared__ d3 s_pts[8], s_rays[4];
+    __shared__ Pose s_pose;
+    if (lane == 0) {
+        const Pose pose = pose_from12(pose12);
+        s_pose = pose;
+        fc->pose = pose;
+        fc->inv = invert(pose);
+        fc->intr = intr;
+        fc->delta = P.delta;
+    }
+    __syncwarp();
+    const Pose pose = s_pose;
+    // Frustum hull and separating axes, exactly as occupied_blocks_in_frustum builds them
+    // (grid.cpp:228-262): hull points near/far x v x u, corner rays, 26 candidate axes.
+    const double us[2] = {-0.5, intr.w - 0.5};
+    const double vs[2] = {-0.5, intr.h - 0.5};
+    if (lane < 8) {
+        const double zs[2] = {intr.near_plane, intr.far_plane};
+        s_pts[lane] = apply(pose, unproject(intr, us[lane & 1], vs[(lane >> 1) & 1], zs[lane >> 2]));
+    } else if (lane < 12) {
+        const int r = lane - 8;  // r00, r10, r01, r11
+        s_rays[r] = normalized(mv(pose.R, unproject(intr, us[r & 1], vs[r >> 1], 1.0)));
+    } else if (lane < 16) {
+        // side face through the camera centre and two image corners, in the camera frame,
+        // oriented so the optical axis is inside
+        const int f = lane - 12;  // top (v = -0.5), bottom, left (u = -0.5), right
+        const d3 a = f < 2 ? unproject(intr, us[0], vs[f], 1.0) : unproject(intr, us[f - 2], vs[0], 1.0);
+        const d3 b = f < 2 ? unproject(intr, us[1], vs[f], 1.0) : unproject(intr, us[f - 2], vs[1], 1.0);
+        d3 nrm = normalized(cross(a, b));
+        if (nrm.z < 0.0) nrm = neg(nrm);
+        fc->side_n[f] = nrm;
+    }
+    __syncwarp();
+    if (lane < kSatAxes) {
+        const d3 r00 = s_rays[0], r10 = s_rays[1], r01 = s_rays[2], r11 = s_rays[3];
+        const d3 box_axes[3] = {mk(1, 0, 0), mk(0, 1, 0), mk(0, 0, 1)};
+        d3 ax;
+        if (lane < 3) ax = box_axes[lane];
+        else if (lane == 3) ax = col(pose.R, 2);  // optical axis
+        else if (lane == 4) ax = cross(r00, r10);  // top
+        else if (lane == 5) ax = cross(r11, r01);  // bottom
+        else if (lane == 6) ax = cross(r01, r00);  // left
+        else if (lane == 7) ax = cross(r10, r11);  // right
+        else {
+            const int e = (lane - 8) / 3, b = (lane - 8) % 3;
+            const d3 edges[6] = {r00, r10, r01, r11, col(pose.R, 0), col(pose.R, 1)};
+            ax = cross(edges[e], box_axes[b]);
+        }
+        fc->sat_axis[lane] = ax;
+        fc->sat_valid[lane] = !(sqnorm(ax) < 1e-18);
+        double lo = INFINITY, hi = -INFINITY;
+        for (int i = 0; i < 8; ++i) {
+            const double d = dot(ax, s_pts[i]);
+            lo = dmin(lo, d);
+            hi = dmax(hi, d);
+        }
+        fc->sat_lo[lane] = lo;
+        fc->sat_hi[lane] = hi;
+    }
+}
+
+// Zero the per-frame counters; a set dead flag turns the frame's later kernels into no-ops.
+__device__ inline void fuse_begin_body(FrameCounters* ctr, const VolCounters* vc, const int* dead) {
+    FrameCounters z;
+    memset(&z, 0, sizeof(z));
+    z.alloc_before = vc->allocated_count - vc->halo_count;  // owned blocks only
+    z.skip = dead ? static_cast<uint32_t>(*dead != 0) : 0u;
+    *ctr = z;
+}
+__device__ inline void fuse_finalize_body(FrameCounters* ctr, const VolCounters* vc) {
+    ctr->alloc_now = vc->allocated_count - vc->halo_count;
+}
 }  // namespace sf

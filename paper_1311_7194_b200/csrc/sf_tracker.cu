@@ -18,6 +18,7 @@
 
 #include "sf_icp.cuh"
 #include "sf_linalg.cuh"
+#include "sf_sample.cuh"
 
 namespace sf {
 
@@ -55,6 +56,52 @@ __global__ void k_tracker_after_icp(double* __restrict__ cur, double* __restrict
     pose_to12(est, cur);
     pose_to12(est, fuse_pose);
     td->registered = 1;
+}
+
+// One warp: begin_track (lane 0) and the raycast's frame constants at the current pose.
+__global__ void k_tracker_begin_track_consts(VolParams P, Intr cam, const double* __restrict__ cur,
+                                             const double* __restrict__ external, double* __restrict__ init_delta,
+                                             RayCounters* rstats, const TrackerDev* td, FrameConsts* fc) {
+    if (threadIdx.x == 0 && !td->dead) {
+        const Pose c = pose_from12(cur);
+        const Pose init = external ? compose(c, pose_from12(external)) : c;
+        pose_to12(compose(invert(c), init), init_delta);
+        RayCounters z{0, 0, 0, 0};
+        *rstats = z;
+    }
+    frame_consts_warp(P, cam, cur, fc);
+}
+
+// One warp: the pose update after ICP (lane 0, as k_tracker_after_icp), then the fusion's
+// frame constants at that pose and its counter reset (launch_fuse's first two kernels).
+__global__ void k_tracker_after_icp_fuse_begin(double* __restrict__ cur, double* __restrict__ fuse_pose,
+                                               const IcpState* st, TrackerDev* td, int orthonormalize, VolParams P,
+                                               Intr cam, FrameConsts* fc, FrameCounters* ctr, const VolCounters* vc) {
+    if (threadIdx.x == 0 && !td->dead) {
+        if (st->lost) {
+            td->dead = 1;
+            td->status = SF_TRACKING_LOST;
+        } else {
+            Pose est = compose(pose_from12(cur), st->delta);  // pipeline.cpp:282
+            if (orthonormalize) est.R = nearest_rotation(est.R);
+            pose_to12(est, cur);
+            pose_to12(est, fuse_pose);
+            td->registered = 1;
+        }
+    }
+    __syncwarp();
+    frame_consts_warp(P, cam, fuse_pose, fc);
+    if (threadIdx.x == 0) fuse_begin_body(ctr, vc, &td->dead);
+}
+
+// fuse_finalize + tracker finish
+__global__ void k_tracker_fuse_finish(FrameCounters* ctr, const VolCounters* vc, TrackerDev* td) {
+    fuse_finalize_body(ctr, vc);
+    if (td->dead) return;
+    if (ctr->exhausted) {
+        td->dead = 1;
+        td->status = SF_POOL_EXHAUSTED;
+    }
 }
 
 __global__ void k_tracker_begin_gt(const double* __restrict__ gt, double* __restrict__ cur,
@@ -186,7 +233,7 @@ struct sf_tracker {
         record_event(ev[0], s);
         issue_icp_loop = false;
         bool joined = true;
-        bool prep_done = false;
+        bool prep_done = false, merged = false;
         if (mode == 0 || mode == 3) {
             // Branch: everything that depends only on the captured frame (ICP source normals,
             // the fusion's normals / edge mask / per-pixel factors) runs beside the raycast.
@@ -197,10 +244,10 @@ struct sf_tracker {
             launch_fuse_prep(*vol, fb, cam, d_cap, sig, p, side_stream, &n, dead);
             SF_CUDA(cudaEventRecord(ev_prep_join, side_stream));
             prep_done = true;
-            k_tracker_begin_track<<<1, 1, 0, s>>>(d_cur, mode == 3 ? d_gt : nullptr, d_init_delta, d_rstats, d_td);
+            k_tracker_begin_track_consts<<<1, 32, 0, s>>>(vol->P, cam, d_cur, mode == 3 ? d_gt : nullptr,
+                                                          d_init_delta, d_rstats, d_td, d_rc_fc);
             SF_LAUNCH_CHECK();
             ++n;
-            launch_consts(vol->P, cam, d_cur, d_rc_fc, s, &n);
             launch_ray_bounds(*vol, d_rc_fc, cam, d_ts, d_te, s, &n, dead, d_ray_list, d_rstats, d_model_depth,
                               d_model_normals);
             launch_raycast(*vol, d_rc_fc, cam, d_ts, d_te, d_model_depth, d_model_normals, d_rstats, s, &n, dead,
@@ -209,9 +256,11 @@ struct sf_tracker {
             SF_CUDA(cudaStreamWaitEvent(s, ev_prep_join, 0));
             launch_icp(icp, d_cap, icp.src_normals, d_model_depth, d_model_normals, cam, cam, d_init_delta, icp_prm, s,
                        &n, dead, &issue_icp_loop);
-            k_tracker_after_icp<<<1, 1, 0, s>>>(d_cur, fb.pose, icp.st, d_td, cfg.orthonormalize);
+            k_tracker_after_icp_fuse_begin<<<1, 32, 0, s>>>(d_cur, fb.pose, icp.st, d_td, cfg.orthonormalize, vol->P,
+                                                            cam, fb.fc, fb.ctr, vol->d_vc);
             SF_LAUNCH_CHECK();
             ++n;
+            merged = true;
             // the deferred eigenpairs of the last ICP iteration run beside the fuse
             SF_CUDA(cudaEventRecord(ev_fork, s));
             SF_CUDA(cudaStreamWaitEvent(side_stream, ev_fork, 0));
@@ -229,12 +278,13 @@ struct sf_tracker {
         FuseEvents fe;
         fe.before_integrate = ev[3];
         fe.after_integrate = ev[4];
-        launch_fuse(*vol, fb, cam, d_cap, sig, p, s, false, &n, dead, &fe, prep_done);
+        launch_fuse(*vol, fb, cam, d_cap, sig, p, s, false, &n, dead, &fe, prep_done, merged);
         if (!joined) {
             SF_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
             joined = true;
         }
-        k_tracker_finish<<<1, 1, 0, s>>>(fb.ctr, d_td);
+        if (merged) k_tracker_fuse_finish<<<1, 1, 0, s>>>(fb.ctr, vol->d_vc, d_td);
+        else k_tracker_finish<<<1, 1, 0, s>>>(fb.ctr, d_td);
         SF_LAUNCH_CHECK();
         ++n;
         record_event(ev[5], s);
@@ -472,8 +522,8 @@ int sf_tracker_device_pose(sf_tracker_t tr, const double** device_pose) {
 int sf_tracker_io_bytes(sf_tracker_t tr, int32_t has_sigma, uint64_t* h2d, uint64_t* d2h) {
     const uint64_t n = static_cast<uint64_t>(tr->cam.w) * tr->cam.h;
     *h2d = n * sizeof(float) * (has_sigma ? 2 : 1);
-    const sf_tracker::Fetch* f = nullptr;
-    *d2h = sizeof(f->cur) + sizeof(f->fuse_pose) + sizeof(f->td) + sizeof(f->ctr) + sizeof(f->rs) + sizeof(f->icp);
+    using F = sf_tracker::Fetch;  // the per-frame metric snapshot read back by fetch
+    *d2h = sizeof(F::cur) + sizeof(F::fuse_pose) + sizeof(F::td) + sizeof(F::ctr) + sizeof(F::rs) + sizeof(F::icp);
     return SF_OK;
 }
 
