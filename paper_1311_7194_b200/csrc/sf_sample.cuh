@@ -130,36 +130,31 @@ struct Sampler {
         const int res = P.res;
         if (bx < 0 || by < 0 || bz < 0 || bx + 1 >= res || by + 1 >= res || bz + 1 >= res) return false;
         const double fx = gx - flx, fy = gy - fly, fz = gz - flz;
+        // One branch-free path for every corner layout (the 1-, 2-, 4- and 8-block cases would
+        // diverge within a warp): per corner its block's slot — the cached one when the block
+        // matches, else a table read — then the payload code. Any EMPTY block or chi corner
+        // gives nullopt (render.cpp:14-15, 39), as in sample().
         const int ms = P.mshift, mm = P.M - 1, N = P.N;
-        const int lx = bx & mm, ly = by & mm, lz = bz & mm;
-        uint16_t pl[8];
-        if (lx != mm && ly != mm && lz != mm) {
-            const int64_t key = ((int64_t)(bz >> ms) * N + (by >> ms)) * N + (bx >> ms);
-            if (key != ckey) {
-                cslot = __ldg(&table[key]);
-                ckey = key;
-            }
-            if (cslot == kEmpty) return false;
-            const uint16_t* b = payload + (size_t)cslot * P.M3 + (((lz << ms) + ly) << ms) + lx;
-            const int M = P.M, MM = M * M;
-            pl[0] = __ldg(b);
-            pl[1] = __ldg(b + 1);
-            pl[2] = __ldg(b + M);
-            pl[3] = __ldg(b + M + 1);
-            pl[4] = __ldg(b + MM);
-            pl[5] = __ldg(b + MM + 1);
-            pl[6] = __ldg(b + MM + M);
-            pl[7] = __ldg(b + MM + M + 1);
-        } else {
-            return sample(p, out);  // corners in several blocks (1 - (7/8)^3 of the samples)
-        }
-        double c[8];
+        const int xs[2] = {bx, bx + 1}, ys[2] = {by, by + 1}, zs[2] = {bz, bz + 1};
         bool ok = true;
+        double c[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const int8_t cc = static_cast<int8_t>(pl[i] & 0xFF);
+            const int x = xs[i & 1], y = ys[(i >> 1) & 1], z = zs[i >> 2];
+            const int64_t key = ((int64_t)(z >> ms) * N + (y >> ms)) * N + (x >> ms);
+            int32_t sl = cslot;
+            if (key != ckey) sl = __ldg(&table[key]);
+            ok = ok && sl != kEmpty;
+            uint16_t pl = kChiPayload;
+            if (sl != kEmpty)
+                pl = __ldg(&payload[(size_t)sl * P.M3 + ((((z & mm) << ms) + (y & mm)) << ms) + (x & mm)]);
+            const int8_t cc = static_cast<int8_t>(pl & 0xFF);
             ok = ok && cc != kChiCode;
             c[i] = tdec[(int)cc + 128];
+            if (i == 0 && key != ckey) {  // cache the base corner's block
+                ckey = key;
+                cslot = sl;
+            }
         }
         if (!ok) return false;
         const double x0 = c[0] + (c[1] - c[0]) * fx;
