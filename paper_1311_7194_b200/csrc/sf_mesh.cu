@@ -325,8 +325,10 @@ __global__ void k_mc_vertices(VolParams P, const int32_t* __restrict__ table, co
         const d3 p = add(pa, scale(t, sub(pb, pa)));
         float nx = 0.f, ny = 0.f, nz = 0.f;
         d3 g;
-        bool ok = S.gradient(p, vox, g);
-        if (!ok) ok = S.gradient(p, 0.5 * vox, g);
+        int64_t ckey = -1;  // block-slot cache of the near-surface sampler (same values as sample())
+        int32_t cslot = kEmpty;
+        bool ok = S.gradient_near(p, vox, g, ckey, cslot);
+        if (!ok) ok = S.gradient_near(p, 0.5 * vox, g, ckey, cslot);
         if (ok && sqnorm(g) > 0.0) {
             const d3 n = normalized(g);
             nx = (float)n.x;
