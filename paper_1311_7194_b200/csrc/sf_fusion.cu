@@ -915,10 +915,14 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
         const unsigned long long grab_row = (unsigned long long)grab * 32;
         for (uint32_t sub = 0; sub < units; ++sub) {
             // ---------------- phase 1: one x-row per lane ----------------
+            // Row set-up (divergent), then a converged loop over the row's M voxels in which
+            // every lane evaluates its voxel and in-band / uncertain voxels are appended to the
+            // warp's ring right away (one ballot per voxel position: nothing held in registers).
             const unsigned long long row = grab_row + sub * 32 + lane;
-            uint32_t amask = 0, emask = 0, slot = 0, rbase = 0;
-            float tk[M], pf[M];
+            uint32_t slot = 0, rbase = 0;
             typename RV::T cells = RV::chi();
+            bool fast = false, exact_row = false;
+            float Axf = 0.f, Ayf = 0.f, Azh = 1.f, Azl = 0.f, half = -1.f;
             if (row < n_rows) {
                 const uint32_t item = static_cast<uint32_t>(row >> (2 * MS));
                 const int r = static_cast<int>(row & (RPB - 1));
@@ -948,67 +952,54 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
                 const double Ax = ((sh.R[0] * vx + sh.R[1] * vy) + sh.R[2] * vz) + sh.t[0];
                 const double Ay = ((sh.R[3] * vx + sh.R[4] * vy) + sh.R[5] * vz) + sh.t[1];
                 const double Az = ((sh.R[6] * vx + sh.R[7] * vy) + sh.R[8] * vz) + sh.t[2];
-                const float Axf = static_cast<float>(Ax), Ayf = static_cast<float>(Ay);
-                const float Azh = static_cast<float>(Az);
-                const float Azl = static_cast<float>(Az - static_cast<double>(Azh));
-                const float Dxf = sh.Dxf, Dyf = sh.Dyf, Dzf = sh.Dzf;
-                const float zend = fmaf(static_cast<float>(M - 1), Dzf, Azh);
+                Axf = static_cast<float>(Ax);
+                Ayf = static_cast<float>(Ay);
+                Azh = static_cast<float>(Az);
+                Azl = static_cast<float>(Az - static_cast<double>(Azh));
+                const float zend = fmaf(static_cast<float>(M - 1), sh.Dzf, Azh);
                 const float zlo = fminf(Azh, zend) - 1e-6f, zhi = fmaxf(Azh, zend) + 1e-6f;
                 const float rzlo = rcp_approx_f(zlo);
                 const float X = fmaxf(fabsf(Axf), fabsf(Ayf)) + sh.Mvox, Z = fabsf(Azh) + sh.Mvox;
                 const float Xq = sh.Fmax * X * rzlo;  // >= |u - cx|, |v - cy| over the row
-                if (zlo > 1e-3f && zhi < 16.0f && Xq < 2097152.0f) {
-                    // pixel-rounding margin of the row; |u|, |v| < 2^22 guaranteed
-                    const float eu = 1.6f * (0x1p-23f * Xq * (2.5f + Z * rzlo) + 0x1p-24f * sh.Wpix);
-                    const float half = 0.5f - eu;
-                    const float fxf = sh.fxf, fyf = sh.fyf, cxf = sh.cxf, cyf = sh.cyf;
-                    const float thr_in = sh.thr_in, thr_out = sh.thr_out;
-#pragma unroll
-                    for (int lx = 0; lx < M; ++lx) {
-                        // explicit fma: one rounding per coordinate (the bounds above assume <= 2)
-                        const float xf = lx == 0 ? Axf : fmaf(static_cast<float>(lx), Dxf, Axf);
-                        const float yf = lx == 0 ? Ayf : fmaf(static_cast<float>(lx), Dyf, Ayf);
-                        const float zf = lx == 0 ? Azh : fmaf(static_cast<float>(lx), Dzf, Azh);
-                        const float rz = rcp_approx_f(zf);
-                        const float uf = fmaf(fxf, xf * rz, cxf), vf = fmaf(fyf, yf * rz, cyf);
-                        const float tu = __fadd_rn(uf, kMagic23), tv = __fadd_rn(vf, kMagic23);
-                        const bool cert = fabsf(__fsub_rn(uf, __fsub_rn(tu, kMagic23))) < half &&
-                                          fabsf(__fsub_rn(vf, __fsub_rn(tv, kMagic23))) < half;
-                        const uint32_t u = static_cast<uint32_t>(__float_as_int(tu) - __float_as_int(kMagic23));
-                        const uint32_t v = static_cast<uint32_t>(__float_as_int(tv) - __float_as_int(kMagic23));
-                        const bool inimg = cert && u < (uint32_t)w && v < (uint32_t)h;
-                        const float2 px = pix_f[inimg ? v * (uint32_t)w + u : 0u];
-                        const float t = (px.x - Azh) - (lx == 0 ? Azl : fmaf(static_cast<float>(lx), Dzf, Azl));
-                        const float at = fabsf(t);
-                        const bool meas = inimg && px.x > 0.0f;
-                        const bool in = meas && at < thr_in;
-                        const bool unc = !cert || (meas && !(at < thr_in) && !(at > thr_out));
-                        amask |= static_cast<uint32_t>(in) << lx;
-                        emask |= static_cast<uint32_t>(unc) << lx;
-                        tk[lx] = t;
-                        pf[lx] = px.y;
-                    }
-                } else if (!(zhi < -1e-3f)) {
-                    emask = (1u << M) - 1u;  // row near / across the camera plane, or very far: exact path
-                }
+                fast = zlo > 1e-3f && zhi < 16.0f && Xq < 2097152.0f;
+                // pixel-rounding margin of the row; |u|, |v| < 2^22 guaranteed
+                if (fast) half = 0.5f - 1.6f * (0x1p-23f * Xq * (2.5f + Z * rzlo) + 0x1p-24f * sh.Wpix);
+                // row near / across the camera plane, or very far: exact path for all its voxels
+                else exact_row = !(zhi < -1e-3f);
             }
-            // ---------------- warp compaction into the ring ----------------
-            const uint32_t qmask = amask | emask;
-            const uint32_t cnt = static_cast<uint32_t>(__popc(qmask));
-            uint32_t incl = cnt;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
-                if (lane >= off) incl += y;
-            }
-            uint32_t pos = tail + incl - cnt;
+            const float Dxf = sh.Dxf, Dyf = sh.Dyf, Dzf = sh.Dzf;
+            const float fxf = sh.fxf, fyf = sh.fyf, cxf = sh.cxf, cyf = sh.cyf;
+            const float thr_in = sh.thr_in, thr_out = sh.thr_out;
+            const unsigned lt_mask = (1u << lane) - 1u;
 #pragma unroll
             for (int lx = 0; lx < M; ++lx) {
-                const uint32_t meta = (rbase + lx) | (RV::cell(cells, lx) << 9) | ((emask >> lx) << 31);
-                if (qmask & (1u << lx))
-                    ring[pos++ & (kRing - 1)] = make_uint4(slot, meta, __float_as_uint(tk[lx]), __float_as_uint(pf[lx]));
+                // explicit fma: one rounding per coordinate (the bounds above assume <= 2)
+                const float xf = lx == 0 ? Axf : fmaf(static_cast<float>(lx), Dxf, Axf);
+                const float yf = lx == 0 ? Ayf : fmaf(static_cast<float>(lx), Dyf, Ayf);
+                const float zf = lx == 0 ? Azh : fmaf(static_cast<float>(lx), Dzf, Azh);
+                const float rz = rcp_approx_f(zf);
+                const float uf = fmaf(fxf, xf * rz, cxf), vf = fmaf(fyf, yf * rz, cyf);
+                const float tu = __fadd_rn(uf, kMagic23), tv = __fadd_rn(vf, kMagic23);
+                const bool cert = fabsf(__fsub_rn(uf, __fsub_rn(tu, kMagic23))) < half &&
+                                  fabsf(__fsub_rn(vf, __fsub_rn(tv, kMagic23))) < half;
+                const uint32_t u = static_cast<uint32_t>(__float_as_int(tu) - __float_as_int(kMagic23));
+                const uint32_t v = static_cast<uint32_t>(__float_as_int(tv) - __float_as_int(kMagic23));
+                const bool inimg = fast && cert && u < (uint32_t)w && v < (uint32_t)h;
+                const float2 px = pix_f[inimg ? v * (uint32_t)w + u : 0u];
+                const float t = (px.x - Azh) - (lx == 0 ? Azl : fmaf(static_cast<float>(lx), Dzf, Azl));
+                const float at = fabsf(t);
+                const bool meas = inimg && px.x > 0.0f;
+                const bool in = meas && at < thr_in;
+                const bool unc = exact_row || (fast && (!cert || (meas && !(at < thr_in) && !(at > thr_out))));
+                const bool q = in || unc;
+                const unsigned bal = __ballot_sync(0xffffffffu, q);
+                if (q) {
+                    const uint32_t meta = (rbase + lx) | (RV::cell(cells, lx) << 9) | (unc ? 0x80000000u : 0u);
+                    ring[(tail + __popc(bal & lt_mask)) & (kRing - 1)] =
+                        make_uint4(slot, meta, __float_as_uint(t), __float_as_uint(px.y));
+                }
+                tail += __popc(bal);
             }
-            tail += __shfl_sync(0xffffffffu, incl, 31);
             __syncwarp();  // ring entries and the fresh rows' chi stores before the drain
             // ---------------- phase 2: drain full rounds ----------------
             while (tail - head >= 32) drain(32);
