@@ -81,3 +81,42 @@ def c5_config(blocks_per_axis=1024, voxel=0.15e-3):
 
 def c5_trajectory(frames=100, radius=0.9):
     return sf.orbit_trajectory([0.0, 0.0, 0.0], radius, frames, (0.0, 1.0, 0.0), 0.0, 2.0 * math.pi)
+
+
+def c3_scene():
+    """C3: a 2.8 m room (six inward walls at +-1.4 m) with box furniture and a sphere
+    (SURVEY.md §8d C3)."""
+    s = sf.AnalyticScene()
+    for a in range(3):
+        for sgn in (1.0, -1.0):
+            n = [0.0, 0.0, 0.0]
+            n[a] = sgn
+            s.add_plane(n, -1.4)
+    s.add_box([0.6, 1.0, 0.5], [0.3, 0.2, 0.3])
+    s.add_box([-0.5, 1.1, 0.7], [0.25, 0.3, 0.2])
+    s.add_sphere([-0.7, 0.3, -0.6], 0.25)
+    return s
+
+
+def c3_config():
+    """C3: 3000^3 sparse at 1 mm (N = 375, M = 8), box (-1.5, -1.5, -1.5) + 3 m."""
+    return sf.GridConfig(375, 8, (-1.5, -1.5, -1.5), 3.0, 0.0)
+
+
+def c3_trajectory(frames=100, radius=0.3):
+    """Outward-looking pan: 360 degrees about +y from a circle of `radius`."""
+    out = []
+    for k in range(frames):
+        a = 2.0 * math.pi * k / frames
+        c, s_ = math.cos(a), math.sin(a)
+        t = [radius * c, 0.0, radius * s_]
+        fwd = [c, 0.0, s_]
+        up = [0.0, 1.0, 0.0]
+        right = [fwd[1] * up[2] - fwd[2] * up[1], fwd[2] * up[0] - fwd[0] * up[2], fwd[0] * up[1] - fwd[1] * up[0]]
+        nr = math.sqrt(sum(x * x for x in right))
+        right = [x / nr for x in right]
+        down = [fwd[1] * right[2] - fwd[2] * right[1], fwd[2] * right[0] - fwd[0] * right[2],
+                fwd[0] * right[1] - fwd[1] * right[0]]
+        R = [[right[i], down[i], fwd[i]] for i in range(3)]
+        out.append(sf.Pose(R, t))
+    return out

@@ -534,3 +534,28 @@ def test_tracker_streaming_fetch_matches_synchronous(gpu):
         runs.append([(m.frame, m.pose.to12().tobytes(), m.matches, m.fusion.voxels_updated, m.fusion.blocks_total,
                       m.raycast.hit_pixels) for m in out])
     assert runs[0] == runs[1]
+
+
+def test_c3_room_fuse_and_raycast(gpu, oracle):
+    """C3 (3 m room, 3000^3 at 1 mm: N = 375, not a power of two): Kalman fusion with a sigma
+    plane, tables / payload codes / ray bounds / raycast equal the oracle's."""
+    intr = scenes.camera(160, 120, 131.25)
+    cfg = scenes.c3_config()
+    poses = scenes.c3_trajectory(100)[::9][:3]
+    frames = frames_for(gpu, scenes.c3_scene(), poses, intr, 3.0, sigma0=2.5e-4)
+    g, r = grids(gpu, oracle, cfg, 400_000, sf.AuxMode.Variance)
+    params = sf.FusionParams(mode=sf.FusionMode.Kalman)
+    for f, p in zip(frames, poses):
+        assert gpu.fuse_frame(g, f, p, params) == oracle.fuse_frame(r, f, p, params)
+    assert_same_volume(g, r)
+    assert r.allocated_count > 5000
+    pose = poses[-1]
+    tg, eg = gpu.compute_ray_bounds(g, pose, intr)
+    tr, er = oracle.compute_ray_bounds(r, pose, intr)
+    assert np.array_equal(tg.view(np.uint32), tr.view(np.uint32)) and np.array_equal(eg.view(np.uint32), er.view(np.uint32))
+    dg, ng, sg = gpu.raycast_result(g, pose, intr)
+    dr, nr, sr = oracle.raycast_result(r, pose, intr)
+    assert np.array_equal(dg.depth.view(np.uint32), dr.depth.view(np.uint32))
+    assert np.array_equal(ng.array.view(np.uint32), nr.array.view(np.uint32))
+    assert (sg.sample_steps, sg.hit_pixels, sg.rays_with_bounds) == (sr.sample_steps, sr.hit_pixels, sr.rays_with_bounds)
+    assert sg.hit_pixels > 500
