@@ -21,6 +21,7 @@ the whole job (strong scaling). `--local-shards R` runs the same sharded loop as
 ranks on one GPU (in-process reductions instead of NCCL) for testing.
 """
 import argparse
+import contextlib
 import json
 import math
 import os
@@ -293,40 +294,54 @@ def run_ours(args, world, rank, local):
     sp = stream.cuda_stream
     flush = torch.empty(400 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
-    grid = sf.SparseTsdfGrid(grid_cfg, c["pool"], sf.AuxMode.Variance, p_min=c["p_min"], device=local)
-    tracker = sf.Tracker(grid, intr, fusion, match, poses[0])
     hooks = hook_deltas(sf, poses)
     HOOK = sf.Tracker.TRACK_WITH_HOOK
-    tracker.step(dframes[0], HOOK, hooks[0], stream=sp)  # frame 0: fused at the first pose
-    for k in range(1, 1 + args.warmup):
-        if reseed_due(c, k):
-            tracker.set_pose(poses[k - 1], stream=sp)
-        tracker.step(dframes[k], HOOK, hooks[k], stream=sp)
-    m = tracker.fetch(stream=sp)
-    if m.status != 0:
-        raise RuntimeError(f"warm-up failed with status {m.status}")
-    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
-    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
-    stage, metrics = [], []
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
-        for i in range(steps):
-            k = 1 + args.warmup + i
-            if not os.environ.get("SF_BENCH_NO_FLUSH"):
-                flush.fill_(i & 0xFF)  # evict L2 (126 MB) between timed steps
+
+    def device_run(stage_level, use_graphs=True, clocks=None):
+        """Fresh volume; warm-up frames, then `steps` device-timed fused frames (CUDA events on
+        the launching stream, L2 flushed before every step). `stage_level` sets the tracker's
+        in-graph stage events (2 all, 1 integrate kernel only, 0 none)."""
+        grid = sf.SparseTsdfGrid(grid_cfg, c["pool"], sf.AuxMode.Variance, p_min=c["p_min"], device=local)
+        tracker = sf.Tracker(grid, intr, fusion, match, poses[0], use_graphs=use_graphs)
+        tracker.set_stage_timing(stage_level)
+        tracker.step(dframes[0], HOOK, hooks[0], stream=sp)  # frame 0: fused at the first pose
+        for k in range(1, 1 + args.warmup):
             if reseed_due(c, k):
                 tracker.set_pose(poses[k - 1], stream=sp)
-            ev0[i].record(stream)
             tracker.step(dframes[k], HOOK, hooks[k], stream=sp)
-            ev1[i].record(stream)
-            metrics.append(tracker.fetch(stream=sp))  # synchronises (outside the events)
-            stage.append(tracker.stage_times())
+        m = tracker.fetch(stream=sp)
+        if m.status != 0:
+            raise RuntimeError(f"warm-up failed with status {m.status}")
+        ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        stage, metrics = [], []
+        if dist:
+            dist.barrier()
         torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    step_ms = [ev0[i].elapsed_time(ev1[i]) for i in range(steps)]
+        with (clocks if clocks is not None else contextlib.nullcontext()):
+            for i in range(steps):
+                k = 1 + args.warmup + i
+                if not os.environ.get("SF_BENCH_NO_FLUSH"):
+                    flush.fill_(i & 0xFF)  # evict L2 (126 MB) between timed steps
+                if reseed_due(c, k):
+                    tracker.set_pose(poses[k - 1], stream=sp)
+                ev0[i].record(stream)
+                tracker.step(dframes[k], HOOK, hooks[k], stream=sp)
+                ev1[i].record(stream)
+                metrics.append(tracker.fetch(stream=sp))  # synchronises (outside the events)
+                stage.append(tracker.stage_times())
+            torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        return grid, [ev0[i].elapsed_time(ev1[i]) for i in range(steps)], metrics, stage
+
+    # Throughput run: no stage events inside the frame graph (each event node costs a few us).
+    clocks = ClockSampler(local)
+    grid, step_ms, metrics, _ = device_run(0, clocks=clocks)
+    # Breakdown run (fresh volume, same frames): the stage events, incl. the integrate kernel's
+    # pair that the roofline divides by.
+    _, step_ms_b, metrics_b, stage = device_run(int(os.environ.get("SF_BENCH_STAGE_LEVEL", "2")),
+                                                use_graphs=os.environ.get("SF_BENCH_STAGE_GRAPHS", "1") == "1")
     total_ms = sum(step_ms)
     launches_total = sum(mm.kernel_launches for mm in metrics)
     statuses = [mm.status for mm in metrics]
@@ -345,7 +360,7 @@ def run_ours(args, world, rank, local):
     integ_ms = [s[3] for s in stage]
     # per processed block: M^3 payload cells read + written (2 B each) + its 8 B work item;
     # per launch: the 8 B/pixel {depth, p_k} table the voxels gather from
-    integ_bytes = [b * (m3 * 4 + 8) + px * 8 for b in blocks]
+    integ_bytes = [mm.blocks_processed * (m3 * 4 + 8) + px * 8 for mm in metrics_b]
     achieved = sum(integ_bytes) / (sum(integ_ms) * 1e-3) / 1e9
     peak, peak_kind = hbm_peak()
     traffic = None  # DRAM bytes per launch of the roofline kernel from the committed ncu capture
@@ -358,6 +373,7 @@ def run_ours(args, world, rank, local):
     # e2e: fresh volume, pinned HOST frames, H2D inside the step + metrics read-back
     grid2 = sf.SparseTsdfGrid(grid_cfg, c["pool"], sf.AuxMode.Variance, p_min=c["p_min"], device=local)
     tr2 = sf.Tracker(grid2, intr, fusion, match, poses[0])
+    tr2.set_stage_timing(0)
     pinned = []
     for f in frames:
         d = torch.from_numpy(f.depth).pin_memory()
@@ -422,6 +438,11 @@ def run_ours(args, world, rank, local):
         "voxel_updates_per_s": world * vox_updated / (total_ms * 1e-3),
         "stage_ms_mean": dict(zip(["raycast", "icp", "fuse_prologue", "integrate", "total"],
                                   [sum(s[j] for s in stage) / steps for j in range(5)])),
+        "stage_run": {"ms_per_step": sum(step_ms_b) / steps,
+                      "note": "stage_ms_mean and the roofline kernel time come from a second device-timed run "
+                              "(fresh volume, same frames) with CUDA events inside the frame graph; the "
+                              "throughput run has none (each graph event node adds a few us per step)",
+                      "same_result": bool(np.array_equal(metrics_b[-1].pose.to12(), metrics[-1].pose.to12()))},
         "blocks_processed_mean": sum(blocks) / steps,
         "integrate_exact_fallback_frac": sum(mm.exact_voxels for mm in metrics) / max(1, sum(blocks) * m3),
         "icp_iterations_mean": sum(mm.iterations for mm in metrics) / steps,
@@ -429,7 +450,8 @@ def run_ours(args, world, rank, local):
         "roofline": {"bound": "hbm", "kernel": "k_integrate_rows<Kalman>", "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "bytes_per_launch_mean": sum(integ_bytes) / steps,
-                     "ms_per_launch_mean": sum(integ_ms) / steps},
+                     "ms_per_launch_mean": sum(integ_ms) / steps,
+                     "kernel_span_ms_mean": sum(mm.integrate_ns for mm in metrics) / steps * 1e-6},
         "replicas_consistent": consistent,
         "e2e_same_result": bool(np.array_equal(e2e_metrics[-1].pose.to12(), metrics[-1].pose.to12())),
         "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,

@@ -324,6 +324,7 @@ typedef struct {
     uint64_t voxels_visited;   /* blocks_processed * M^3 */
     uint64_t kernel_launches;  /* device kernels this frame ran (graph: top level + 2 per ICP iteration) */
     uint64_t exact_voxels;     /* voxels the integrate kernel settled on its FP64 fallback (uncertain FP32 decision) */
+    uint64_t integrate_ns;     /* integrate kernel span on the device clock: first CTA start to last CTA end (%globaltimer) */
 } sf_frame_metrics;
 
 int sf_tracker_create(sf_volume_t vol, const sf_tracker_config* config, const double initial_pose[12],
@@ -346,8 +347,13 @@ int sf_tracker_fetch_frame(sf_tracker_t tr, int32_t frame, sf_frame_metrics* out
 /* Device-timed stages of the last step, in ms (CUDA events recorded inside the step /
  * graph): [0] raycast (bounds + march), [1] ICP (source normals + all iterations),
  * [2] fuse prologue (frame prep, keys, sort/unique, allocation, visibility),
- * [3] the per-voxel integrate kernel, [4] whole step. Call after sf_tracker_fetch. */
+ * [3] the per-voxel integrate kernel, [4] whole step. Call after sf_tracker_fetch. A stage
+ * whose events are not recorded (sf_tracker_set_stage_timing) reads -1. */
 int sf_tracker_stage_times(sf_tracker_t tr, float ms[5]);
+/* Stage-timing events inside the step: 2 = all stages (default), 1 = the integrate kernel's
+ * pair only, 0 = none. Each event is a node of the frame graph and costs a few microseconds
+ * of the step, so throughput runs switch them off. Rebuilds the cached graphs. */
+int sf_tracker_set_stage_timing(sf_tracker_t tr, int32_t level);
 /* Device pointer to the tracker's pose (12 doubles). */
 int sf_tracker_device_pose(sf_tracker_t tr, const double** device_pose);
 /* Number of this library's kernels the last sf_tracker_step launched at issue time. With

@@ -409,6 +409,13 @@ public:
         check(sf_tracker_fetch_frame(h_, frame, &m));
         return m;
     }
+    // stage-timing events inside the frame graph: 2 all (default), 1 integrate only, 0 none
+    void set_stage_timing(int level) { check(sf_tracker_set_stage_timing(h_, level)); }
+    std::array<float, 5> stage_times() {
+        std::array<float, 5> ms{};
+        check(sf_tracker_stage_times(h_, ms.data()));
+        return ms;
+    }
 
 private:
     sf_tracker_t h_ = nullptr;

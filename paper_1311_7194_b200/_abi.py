@@ -157,6 +157,7 @@ class FrameMetricsC(C.Structure):
         ("voxels_visited", C.c_uint64),
         ("kernel_launches", C.c_uint64),
         ("exact_voxels", C.c_uint64),
+        ("integrate_ns", C.c_uint64),
     ]
 
 
@@ -231,6 +232,7 @@ PRODUCT_ONLY = {
     "tracker_device_pose": (C.c_int, [vp, P(c_double_p)]),
     "tracker_last_launch_count": (C.c_int, [vp, u64p]),
     "tracker_stage_times": (C.c_int, [vp, P(C.c_float)]),
+    "tracker_set_stage_timing": (C.c_int, [vp, C.c_int32]),
     "tracker_io_bytes": (C.c_int, [vp, i32, u64p, u64p]),
     "debug_aux_tables": (C.c_int, [P(AuxQuantC), C.c_double, c_double_p, c_double_p, c_double_p]),
     # spatial sharding

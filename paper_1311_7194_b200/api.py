@@ -715,6 +715,7 @@ class FrameMetrics:
     voxels_visited: int = 0
     kernel_launches: int = 0  # this library's kernels the frame ran (incl. device-side ICP loop)
     exact_voxels: int = 0  # integrate voxels settled on the FP64 fallback (uncertain FP32 decision)
+    integrate_ns: int = 0  # integrate kernel span on the device clock (first CTA start .. last CTA end)
 
 
 class Tracker:
@@ -764,7 +765,8 @@ class Tracker:
                             m.matches, m.residual_rms, list(m.lambda_over_n), [bool(x) for x in m.gated_mask],
                             FusionStats(f.voxels_updated, f.blocks_allocated_now, f.blocks_total, f.memory_bytes),
                             RaycastStats(r.sample_steps, r.hit_pixels, r.rays_with_bounds),
-                            m.blocks_processed, m.voxels_visited, m.kernel_launches, m.exact_voxels)
+                            m.blocks_processed, m.voxels_visited, m.kernel_launches, m.exact_voxels,
+                            m.integrate_ns)
 
     def fetch(self, stream=None) -> FrameMetrics:
         m = A.FrameMetricsC()
@@ -783,6 +785,10 @@ class Tracker:
         ms = (C.c_float * 5)()
         self.grid.backend.check(self._lib.tracker_stage_times(self.handle, ms))
         return list(ms)
+
+    def set_stage_timing(self, level: int):
+        """Stage-timing events inside the step: 2 all (default), 1 integrate kernel only, 0 none."""
+        self.grid.backend.check(self._lib.tracker_set_stage_timing(self.handle, int(level)))
 
     def io_bytes(self, has_sigma: bool):
         """(h2d, d2h) bytes of one host-frame step + fetch."""

@@ -19,6 +19,13 @@
 
 namespace sf {
 
+// Device clock (ns); used for in-kernel span measurements.
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 constexpr int32_t kEmpty = -1;          // SparseTsdfGrid::kEmpty (grid.hpp:98)
 constexpr int8_t kChiCode = -128;       // grid.hpp:19
 constexpr int kTsdfCodeRange = 127;     // grid.hpp:21

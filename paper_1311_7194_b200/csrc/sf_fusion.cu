@@ -823,6 +823,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
     __shared__ VolParams sP;  // by reference into the (noinline) exact path without a stack copy
     __shared__ FuseParams sFp;
     if (ctr->skip) return;
+    if (threadIdx.x == 0) atomicMin(&ctr->t_begin, globaltimer_ns());
     for (int i = threadIdx.x; i < 256; i += blockDim.x) {
         s_tdec[i] = aux->tsdf_decode_f[i];
         s_adec[i] = aux->aux_decode_f[i];
@@ -1013,6 +1014,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
     }
     if (lane == 0 && updated) atomicAdd(&ctr->voxels_updated, (unsigned long long)updated);
     if (lane == 0 && exact) atomicAdd(&ctr->exact_voxels, (unsigned long long)exact);
+    if (lane == 0) atomicMax(&ctr->t_end, globaltimer_ns());
 }
 
 // ---- measurement refinement (fusion.cpp:99-143) ---------------------------------------

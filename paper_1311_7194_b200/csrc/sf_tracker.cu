@@ -163,6 +163,10 @@ struct sf_tracker {
     cudaEvent_t ev_staged[2] = {nullptr, nullptr}, ev_stage_free[2] = {nullptr, nullptr};
     cudaEvent_t ev_snap[2] = {nullptr, nullptr};
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // stage timing (graph nodes)
+    int stage_events = 2;  // 2: all stage events, 1: integrate pair only, 0: none
+    void mark(int i, cudaStream_t s) {
+        if (stage_events == 2 || (stage_events == 1 && (i == 3 || i == 4))) record_event(ev[i], s);
+    }
     cudaGraphExec_t graph[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};  // [mode][sigma]
     uint64_t graph_kernels[3][2] = {{0, 0}, {0, 0}, {0, 0}};
     bool graph_icp_loop[3][2] = {{false, false}, {false, false}, {false, false}};
@@ -230,7 +234,7 @@ struct sf_tracker {
         const int* dead = &d_td->dead;
         const FuseParams& p = has_sigma ? fp_sigma : fp;
         const float* sig = has_sigma ? d_cap_sigma : nullptr;
-        record_event(ev[0], s);
+        mark(0, s);
         issue_icp_loop = false;
         bool joined = true;
         bool prep_done = false, merged = false;
@@ -252,7 +256,7 @@ struct sf_tracker {
                               d_model_normals);
             launch_raycast(*vol, d_rc_fc, cam, d_ts, d_te, d_model_depth, d_model_normals, d_rstats, s, &n, dead,
                            d_ray_list, d_brackets);
-            record_event(ev[1], s);
+            mark(1, s);
             SF_CUDA(cudaStreamWaitEvent(s, ev_prep_join, 0));
             launch_icp(icp, d_cap, icp.src_normals, d_model_depth, d_model_normals, cam, cam, d_init_delta, icp_prm, s,
                        &n, dead, &issue_icp_loop);
@@ -267,17 +271,17 @@ struct sf_tracker {
             launch_icp_report(icp, side_stream, &n);
             SF_CUDA(cudaEventRecord(ev_join, side_stream));
             joined = false;
-            record_event(ev[2], s);
+            mark(2, s);
         } else {
             k_tracker_begin_gt<<<1, 1, 0, s>>>(d_gt, d_cur, fb.pose, d_rstats, d_td, mode == 1 ? 1 : 0);
             SF_LAUNCH_CHECK();
             ++n;
-            record_event(ev[1], s);
-            record_event(ev[2], s);
+            mark(1, s);
+            mark(2, s);
         }
         FuseEvents fe;
-        fe.before_integrate = ev[3];
-        fe.after_integrate = ev[4];
+        fe.before_integrate = stage_events ? ev[3] : nullptr;
+        fe.after_integrate = stage_events ? ev[4] : nullptr;
         launch_fuse(*vol, fb, cam, d_cap, sig, p, s, false, &n, dead, &fe, prep_done, merged);
         if (!joined) {
             SF_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
@@ -287,7 +291,7 @@ struct sf_tracker {
         else k_tracker_finish<<<1, 1, 0, s>>>(fb.ctr, d_td);
         SF_LAUNCH_CHECK();
         ++n;
-        record_event(ev[5], s);
+        mark(5, s);
         return n;
     }
 };
@@ -477,6 +481,7 @@ void sf_tracker::decode(const Fetch* f, int frame, int mode, uint64_t launches, 
     if (f->ctr.skip) out->blocks_processed = 0;
     out->voxels_visited = out->blocks_processed * m * m * m;
     out->exact_voxels = f->ctr.exact_voxels;
+    out->integrate_ns = f->ctr.t_end > f->ctr.t_begin ? f->ctr.t_end - f->ctr.t_begin : 0;
     out->kernel_launches = launches;
     if (icp_loop) out->kernel_launches += static_cast<uint64_t>(f->icp.bodies);
 }
@@ -509,7 +514,27 @@ int sf_tracker_fetch_frame(sf_tracker_t tr, int32_t frame, sf_frame_metrics* out
 int sf_tracker_stage_times(sf_tracker_t tr, float ms[5]) {
     return guarded([&]() -> int {
         const int pairs[5][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {0, 5}};
-        for (int i = 0; i < 5; ++i) SF_CUDA(cudaEventElapsedTime(&ms[i], tr->ev[pairs[i][0]], tr->ev[pairs[i][1]]));
+        for (int i = 0; i < 5; ++i) {
+            const bool have = tr->stage_events == 2 || (tr->stage_events == 1 && i == 3);
+            ms[i] = -1.0f;  // stage not recorded
+            if (have) SF_CUDA(cudaEventElapsedTime(&ms[i], tr->ev[pairs[i][0]], tr->ev[pairs[i][1]]));
+        }
+        return SF_OK;
+    });
+}
+
+int sf_tracker_set_stage_timing(sf_tracker_t tr, int32_t level) {
+    return guarded([&]() -> int {
+        if (!tr || level < 0 || level > 2) throw Error(SF_INVALID_ARGUMENT, "sf_tracker_set_stage_timing: bad level");
+        if (level == tr->stage_events) return SF_OK;
+        SF_CUDA(cudaSetDevice(tr->vol->device));
+        SF_CUDA(cudaDeviceSynchronize());
+        for (auto& row : tr->graph)
+            for (auto& g : row) {
+                if (g) SF_CUDA(cudaGraphExecDestroy(g));
+                g = nullptr;
+            }
+        tr->stage_events = level;
         return SF_OK;
     });
 }

@@ -510,7 +510,8 @@ def test_fuse_refinement_bit_exact(gpu, ref, mode, steps):
 
 def test_tracker_streaming_fetch_matches_synchronous(gpu):
     """Host frames streamed (step k+1 issued before fetching step k; H2D overlaps compute)
-    give the same per-frame metrics as step/fetch in lockstep."""
+    give the same per-frame metrics as step/fetch in lockstep, with or without the stage-timing
+    events in the frame graph."""
     intr = scenes.camera(320, 240, 262.5)
     cfg = scenes.c1_config()
     poses = scenes.c1_trajectory(100)[:8]
@@ -519,9 +520,10 @@ def test_tracker_streaming_fetch_matches_synchronous(gpu):
     fusion = sf.FusionParams(mode=sf.FusionMode.Kalman)
     match = sf.MatchParams.for_voxel_size(cfg.voxel_size)
     runs = []
-    for streaming in (False, True):
+    for streaming, level in ((False, 2), (True, 2), (False, 0)):
         grid = sf.SparseTsdfGrid(cfg, 0, sf.AuxMode.Variance)
         tr = sf.Tracker(grid, intr, fusion, match, poses[0])
+        tr.set_stage_timing(level)  # stage events are graph nodes only: same results
         out = []
         for k, f in enumerate(frames):
             tr.step(f, sf.Tracker.TRACK)
@@ -531,9 +533,12 @@ def test_tracker_streaming_fetch_matches_synchronous(gpu):
                 out.append(tr.fetch_frame(k - 1))
         if streaming:
             out.append(tr.fetch_frame(len(frames) - 1))
+        st = tr.stage_times()
+        assert (min(st) > 0) if level == 2 else (st == [-1.0] * 5)
+        assert all(m.integrate_ns > 0 for m in out[1:])  # device-clock span of the integrate kernel
         runs.append([(m.frame, m.pose.to12().tobytes(), m.matches, m.fusion.voxels_updated, m.fusion.blocks_total,
                       m.raycast.hit_pixels) for m in out])
-    assert runs[0] == runs[1]
+    assert runs[0] == runs[1] == runs[2]
 
 
 def test_c3_room_fuse_and_raycast(gpu, oracle):
