@@ -6,13 +6,13 @@
 //   k_edge             depth-edge mask                                              (fusion.cpp:40-62)
 //   k_pixel_meas       5x5 near-edge dilation + every per-pixel factor of the
 //                      measurement (sigma, p_k, w_k, grazing reject)                (fusion.cpp:63-70, 148-171)
-//   k_block_keys_set   surface samples -> block keys (FP64), deduplicated in an N^3-bit set (fusion.cpp:190-206)
-//   k_alloc_classify   new keys (EMPTY in the table)
-//   k_alloc_rank       ordered slot assignment: rank among the new keys == position in
-//                      std::set<BlockLess> order == sequential free-list pops;
-//                      PoolExhausted key / prefix semantics                        (fusion.cpp:294-299,369; grid.cpp:87-100)
-//   k_worklist         processed allocate set + SAT frustum test and 9 probes over the
-//                      other allocated blocks                                      (grid.cpp:174-269; fusion.cpp:211-233)
+//   k_block_keys_set   surface samples -> block keys (FP64), deduplicated in an N^3-bit set,
+//                      new keys (EMPTY in the table) split off                     (fusion.cpp:190-206)
+//   k_alloc_visible    ordered slot assignment (rank among the new keys == position in
+//                      std::set<BlockLess> order == sequential free-list pops; PoolExhausted
+//                      key / prefix semantics; fusion.cpp:294-299,369; grid.cpp:87-100)
+//                      beside the SAT frustum test + 9 probes over the other allocated
+//                      blocks (grid.cpp:174-269; fusion.cpp:211-233)
 //   (select_update_blocks exports the ordered lists: k_block_keys, CUB radix sort +
 //    unique == std::set order (fusion.cpp:177-183,193), k_visible)
 //   k_integrate        per voxel: project, band test, filter, quantize              (fusion.cpp:81-173, 237-272, 300-364)
@@ -236,9 +236,14 @@ __device__ __forceinline__ uint32_t warp_append(bool pred, uint32_t* counter) {
 }
 
 // block_of_point keys of the surface samples (fusion.cpp:187-209), deduplicated in the key set.
+// The first inserter of a key also classifies it: an existing block's work item is written
+// at once (item j = its position in the unordered allocate set); a new key (EMPTY table
+// entry) is appended to the new-key list with j, and gets its slot in k_alloc_visible.
 __global__ void k_block_keys_set(VolParams P, const FrameConsts* __restrict__ fc, const float* __restrict__ depth,
                                  int w, int h, int stride, int su, int sv, uint32_t* __restrict__ keybits,
-                                 uint32_t* __restrict__ uniq, FrameCounters* ctr) {
+                                 uint32_t* __restrict__ uniq, FrameCounters* ctr, const int32_t* __restrict__ table,
+                                 uint32_t* __restrict__ new_keys, uint32_t* __restrict__ new_idx,
+                                 int2* __restrict__ work) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= su * sv || ctr->skip) return;
     const int u = (i % su) * stride;
@@ -253,90 +258,211 @@ __global__ void k_block_keys_set(VolParams P, const FrameConsts* __restrict__ fc
         t_hit = (double)depth[(size_t)v * w + u] / dir_cam.z;
     }
     const double offs[3] = {-fc->delta, 0.0, fc->delta};
+    uint32_t keys[3];
+    bool fresh[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        bool fresh = false;
-        uint32_t key = 0;
+        fresh[k] = false;
+        keys[k] = 0;
         if (valid) {
             const d3 x = add(fc->pose.t, scale(t_hit + offs[k], dir));
             const int bx = ref_floor_int((x.x - P.ox) / P.block_side);
             const int by = ref_floor_int((x.y - P.oy) / P.block_side);
             const int bz = ref_floor_int((x.z - P.oz) / P.block_side);
-            if (bx >= 0 && by >= 0 && bz >= 0 && bx < P.N && by < P.N && bz < P.N && shard_owns(P, bx, by, bz)) {
-                key = static_cast<uint32_t>(table_index(P, bx, by, bz));
-                const uint32_t bit = 1u << (key & 31);
-                fresh = !(atomicOr(&keybits[key >> 5], bit) & bit);
-            }
+            if (bx >= 0 && by >= 0 && bz >= 0 && bx < P.N && by < P.N && bz < P.N && shard_owns(P, bx, by, bz))
+                keys[k] = static_cast<uint32_t>(table_index(P, bx, by, bz));
+            else keys[k] = 0xffffffffu;
+        } else keys[k] = 0xffffffffu;
+    }
+    // the three insertions are independent (one round trip to L2 for all of them)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        if (keys[k] != 0xffffffffu) {
+            const uint32_t bit = 1u << (keys[k] & 31);
+            fresh[k] = !(atomicOr(&keybits[keys[k] >> 5], bit) & bit);
         }
-        const uint32_t j = warp_append(fresh, &ctr->n_unique);
-        if (fresh) uniq[j] = key;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const uint32_t key = keys[k];
+        const int32_t slot = fresh[k] ? table[key] : kEmpty;
+        const uint32_t j = warp_append(fresh[k], &ctr->n_unique);
+        if (fresh[k]) uniq[j] = key;
+        const bool isnew = fresh[k] && slot == kEmpty;
+        const uint32_t q = warp_append(isnew, &ctr->n_new);
+        if (isnew) {
+            new_keys[q] = key;
+            new_idx[q] = j;
+            work[j] = make_int2(static_cast<int32_t>(0x80000000u), static_cast<int32_t>(key));
+        } else if (fresh[k]) {
+            work[j] = make_int2(slot, static_cast<int32_t>(key));
+        }
     }
 }
 
-// New keys (EMPTY table entry) of the allocate set.
-__global__ void k_alloc_classify(FrameCounters* ctr, const uint32_t* __restrict__ uniq,
-                                 const int32_t* __restrict__ table, uint32_t* __restrict__ isnew,
-                                 uint32_t* __restrict__ new_keys) {
-    if (ctr->skip) return;
-    const uint32_t n = ctr->n_unique;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t key = uniq[i];
-        const bool fresh = table[key] == kEmpty;
-        isnew[i] = fresh ? 1u : 0u;
-        const uint32_t j = warp_append(fresh, &ctr->n_new);
-        if (fresh) new_keys[j] = key;
-    }
+// Conservative: the block's bounding sphere lies strictly inside the frustum (margins far
+// above rounding), hence the exact SAT (grid.cpp:228-269) would report an intersection.
+__device__ __forceinline__ bool block_surely_inside(const VolParams& P, const FrameConsts* __restrict__ fc, d3 lo) {
+    const double hs = 0.5 * P.block_side;
+    const d3 c = apply(fc->inv, add(lo, mk(hs, hs, hs)));
+    const double r = hs * 1.7320508075688772 * (1.0 + 1e-9) + 1e-12;
+    if (!(c.z - r > fc->intr.near_plane * (1.0 + 1e-9) && c.z + r < fc->intr.far_plane * (1.0 - 1e-9))) return false;
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+        if (!(dot(fc->side_n[f], c) > r)) return false;
+    return true;
 }
 
-// Ordered slots for the new keys: rank = #{new keys < key}; the rank-th pop of the free
-// list, as the reference's lazy allocate_block calls in list order would (grid.cpp:87-100).
-// The last CTA settles the counters: PoolExhausted when n_new exceeds the free list.
-constexpr int kRankTile = 2048;
+// Visible allocated blocks outside the allocate set (membership from the key set): exact
+// frustum SAT + 9 probes (grid.cpp:174-269; fusion.cpp:211-233).
+__device__ __forceinline__ bool block_visible(const VolParams& P, const FrameConsts* __restrict__ fc, int32_t key,
+                                              const float* __restrict__ depth, int w, int h) {
+    int bx, by, bz;
+    if (P.nshift >= 0) {
+        bx = key & (P.N - 1);
+        by = (key >> P.nshift) & (P.N - 1);
+        bz = key >> (2 * P.nshift);
+    } else {
+        bx = key % P.N;
+        by = (key / P.N) % P.N;
+        bz = key / (P.N * P.N);
+    }
+    const d3 lo = block_min_corner(P, bx, by, bz);
+    const double side = P.block_side;
+    const d3 hi = add(lo, mk(side, side, side));
+    // a sharded volume integrates only its own blocks (mirrored halo blocks are read-only)
+    if (!shard_owns(P, bx, by, bz) || !(block_surely_inside(P, fc, lo) || frustum_intersects_block(P, fc, lo, hi)))
+        return false;
+    const Intr& intr = fc->intr;
+    for (int k = 0; k < 9; ++k) {
+        const d3 probe = k == 8 ? add(lo, mk(0.5 * side, 0.5 * side, 0.5 * side))
+                                : add(lo, mk(k & 1 ? side : 0.0, k & 2 ? side : 0.0, k & 4 ? side : 0.0));
+        const d3 xc = apply(fc->inv, probe);
+        double pu, pv;
+        if (!project(intr, xc, pu, pv)) continue;
+        const int u = ref_lround_int(pu);
+        const int v = ref_lround_int(pv);
+        if (!(u >= 0 && v >= 0 && u < w && v < h)) continue;
+        const float d = depth[(size_t)v * w + u];
+        if (!(d > 0.0f) || xc.z <= d + fc->delta) return true;
+    }
+    return false;
+}
+
+// One launch, two roles, then a last-CTA epilogue:
+//  - CTAs [0, kRankCtas): ordered slots for the new keys. rank = #{new keys < key} (one warp
+//    per kRankKeys keys, lanes over the list) is the key's position among the new keys in
+//    std::set<BlockLess> order, so its slot is the rank-th pop of the free list — what the
+//    reference's lazy allocate_block calls in list order produce (fusion.cpp:294-299;
+//    grid.cpp:87-100); rank == free_top is the PoolExhausted key (fusion.cpp:369).
+//  - the other CTAs: the update list over the blocks allocated before this frame (slots
+//    below the frame's starting high-water mark). It does not depend on the allocation:
+//    slots (re)used this frame hold keys of the allocate set, which the key set excludes.
+//  - last CTA: counters; on PoolExhausted the processed allocate prefix (keys below the
+//    exhaustion key) is compacted to the front of the work list and the update list dropped.
+constexpr int kRankCtas = 148;
+constexpr int kRankKeys = 4;
 __global__ void __launch_bounds__(256)
-    k_alloc_rank(VolParams P, FrameCounters* ctr, const uint32_t* __restrict__ new_keys, int32_t* __restrict__ table,
-                 const int32_t* __restrict__ free_list, int32_t* __restrict__ slot_key, uint32_t* __restrict__ occ,
-                 VolCounters* vc) {
-    __shared__ uint32_t s_keys[kRankTile];
+    k_alloc_visible(VolParams P, const FrameConsts* __restrict__ fc, FrameCounters* ctr, VolCounters* vc,
+                    const uint32_t* __restrict__ new_keys, const uint32_t* __restrict__ new_idx,
+                    int32_t* __restrict__ table, const int32_t* __restrict__ free_list, int32_t* __restrict__ slot_key,
+                    uint32_t* __restrict__ occ, const uint32_t* __restrict__ uniq, const uint32_t* __restrict__ keybits,
+                    const float* __restrict__ depth, int w, int h, int2* __restrict__ work) {
     __shared__ bool s_last;
+    __shared__ uint32_t s_wsum[8];
     if (ctr->skip) return;
-    const uint32_t n = ctr->n_new;
+    const uint32_t n = ctr->n_new, n_unique = ctr->n_unique;
     const unsigned long long top = vc->free_top;
-    for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
-        const uint32_t i = base + threadIdx.x;
-        const uint32_t key = i < n ? new_keys[i] : 0xffffffffu;
-        uint32_t rank = 0;
-        for (uint32_t t0 = 0; t0 < n; t0 += kRankTile) {
-            const uint32_t m = min(n - t0, (uint32_t)kRankTile);
-            __syncthreads();
-            for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) s_keys[j] = new_keys[t0 + j];
-            __syncthreads();
-            for (uint32_t j = 0; j < m; ++j) rank += s_keys[j] < key ? 1u : 0u;
-        }
-        if (i < n) {
-            if (rank < top) {
-                const int32_t slot = free_list[top - 1 - rank];
-                table[key] = slot;
-                slot_key[slot] = static_cast<int32_t>(key);
-                occ_set(P, occ, key);
-                atomicMax(&vc->high_water, (unsigned long long)slot + 1ull);
-            } else if (rank == top) {
-                ctr->exhaust_key = key;  // PoolExhausted at this key (fusion.cpp:369)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (blockIdx.x < kRankCtas) {
+        const uint32_t nw = kRankCtas * (blockDim.x >> 5);
+        for (uint32_t g = blockIdx.x * (blockDim.x >> 5) + warp; g * kRankKeys < n; g += nw) {
+            uint32_t kq[kRankKeys], rank[kRankKeys];
+#pragma unroll
+            for (int t = 0; t < kRankKeys; ++t) {
+                const uint32_t q = g * kRankKeys + t;
+                kq[t] = q < n ? new_keys[q] : 0u;
+                rank[t] = 0;
             }
+            for (uint32_t j = lane; j < n; j += 32) {
+                const uint32_t x = new_keys[j];
+#pragma unroll
+                for (int t = 0; t < kRankKeys; ++t) rank[t] += x < kq[t] ? 1u : 0u;
+            }
+#pragma unroll
+            for (int t = 0; t < kRankKeys; ++t) {
+                const uint32_t r = __reduce_add_sync(0xffffffffu, rank[t]);
+                const uint32_t q = g * kRankKeys + t;
+                if (lane == t && q < n) {
+                    const uint32_t key = kq[t];
+                    if (r < top) {
+                        const int32_t slot = free_list[top - 1 - r];
+                        table[key] = slot;
+                        slot_key[slot] = static_cast<int32_t>(key);
+                        occ_set(P, occ, key);
+                        atomicMax(&vc->high_water, (unsigned long long)slot + 1ull);
+                        work[new_idx[q]] = make_int2(static_cast<int32_t>(static_cast<uint32_t>(slot) | 0x80000000u),
+                                                     static_cast<int32_t>(key));
+                    } else if (r == top) {
+                        ctr->exhaust_key = key;  // PoolExhausted at this key (fusion.cpp:369)
+                    }
+                }
+            }
+        }
+    } else {
+        const unsigned long long hw = ctr->hw_before;
+        const uint32_t stride = (gridDim.x - kRankCtas) * blockDim.x;
+        for (unsigned long long s = (blockIdx.x - kRankCtas) * (unsigned long long)blockDim.x + threadIdx.x; s < hw;
+             s += stride) {
+            const int32_t key = slot_key[s];
+            const bool vis = key >= 0 && !((keybits[key >> 5] >> (key & 31)) & 1u) &&
+                             block_visible(P, fc, key, depth, w, h);
+            const uint32_t j = warp_append(vis, &ctr->n_update);
+            if (vis) work[n_unique + j] = make_int2(static_cast<int32_t>(s), key);
         }
     }
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) s_last = atomicAdd(&ctr->tickets, 1u) == gridDim.x - 1;
     __syncthreads();
-    if (!s_last || threadIdx.x != 0) return;
+    if (!s_last) return;
     __threadfence();
-    const unsigned long long got = n < top ? n : top;
-    vc->free_top = top - got;
-    vc->allocated_count += got;
-    ctr->exhausted = n > top ? 1u : 0u;
-    if (n <= top) ctr->exhaust_key = 0xffffffffu;
-    ctr->n_list = ctr->n_unique;
-    ctr->upd_base = ctr->n_unique;
+    const bool exhausted = n > top;
+    if (threadIdx.x == 0) {
+        const unsigned long long got = n < top ? n : top;
+        vc->free_top = top - got;
+        vc->allocated_count += got;
+        ctr->exhausted = exhausted ? 1u : 0u;
+        if (!exhausted) ctr->exhaust_key = 0xffffffffu;
+        ctr->n_list = n_unique;
+        ctr->upd_base = n_unique;
+        if (!exhausted) ctr->limit = n_unique;
+        else ctr->n_update = 0;  // the update list is never reached
+    }
+    if (!exhausted) return;
+    // PoolExhausted: keep the items of keys below the exhaustion key (all of them have slots:
+    // a new key below it has a smaller rank), compacted in place in chunk order.
+    const uint32_t ex_key = *(volatile uint32_t*)&ctr->exhaust_key;
+    uint32_t pos = 0;
+    for (uint32_t base = 0; base < n_unique; base += blockDim.x) {
+        const uint32_t i = base + threadIdx.x;
+        int2 it = make_int2(0, 0);
+        bool take = false;
+        if (i < n_unique) {
+            it = work[i];
+            take = static_cast<uint32_t>(it.y) < ex_key;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, take);
+        if (lane == 0) s_wsum[warp] = __popc(bal);
+        __syncthreads();
+        uint32_t off = pos;
+        for (int k = 0; k < warp; ++k) off += s_wsum[k];
+        uint32_t tot = 0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) tot += s_wsum[k];
+        if (take) work[off + __popc(bal & ((1u << lane) - 1u))] = it;
+        pos += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) ctr->limit = pos;
 }
 
 // ---------------------------------------------------------------------------------
@@ -351,19 +477,6 @@ __device__ __forceinline__ bool in_sorted(const uint32_t* __restrict__ a, uint32
         else hi = mid;
     }
     return lo < n && a[lo] == key;
-}
-
-// Conservative: the block's bounding sphere lies strictly inside the frustum (margins far
-// above rounding), hence the exact SAT (grid.cpp:228-269) would report an intersection.
-__device__ __forceinline__ bool block_surely_inside(const VolParams& P, const FrameConsts* __restrict__ fc, d3 lo) {
-    const double hs = 0.5 * P.block_side;
-    const d3 c = apply(fc->inv, add(lo, mk(hs, hs, hs)));
-    const double r = hs * 1.7320508075688772 * (1.0 + 1e-9) + 1e-12;
-    if (!(c.z - r > fc->intr.near_plane * (1.0 + 1e-9) && c.z + r < fc->intr.far_plane * (1.0 - 1e-9))) return false;
-#pragma unroll
-    for (int f = 0; f < 4; ++f)
-        if (!(dot(fc->side_n[f], c) > r)) return false;
-    return true;
 }
 
 __global__ void k_visible(VolParams P, const FrameConsts* __restrict__ fc, FrameCounters* ctr,
@@ -403,68 +516,6 @@ __global__ void k_visible(VolParams P, const FrameConsts* __restrict__ fc, Frame
         const uint32_t j = atomicAdd(&ctr->n_update, 1u);
         if (export_only) export_keys[j] = static_cast<uint32_t>(key);
         else work[base + j] = make_int2(static_cast<int32_t>(s), key);
-    }
-}
-
-// Fuse-path work list: the processed part of the allocate set (everything, or the keys
-// below the PoolExhausted key), then — unless exhausted — the visible allocated blocks
-// outside the allocate set (membership from the key set), at [upd_base, ...).
-__global__ void k_worklist(VolParams P, const FrameConsts* __restrict__ fc, FrameCounters* ctr,
-                           const VolCounters* __restrict__ vc, const int32_t* __restrict__ slot_key,
-                           const int32_t* __restrict__ table, const uint32_t* __restrict__ uniq,
-                           const uint32_t* __restrict__ isnew, const uint32_t* __restrict__ keybits,
-                           const float* __restrict__ depth, int w, int h, int2* __restrict__ work) {
-    if (ctr->skip) return;
-    const uint32_t n = ctr->n_unique, ex_key = ctr->exhaust_key;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const uint32_t key = uniq[i];
-        const bool take = key < ex_key;
-        const uint32_t j = warp_append(take, &ctr->limit);
-        if (take) {
-            const uint32_t slot = static_cast<uint32_t>(table[key]);
-            work[j] = make_int2(static_cast<int32_t>(slot | (isnew[i] << 31)), static_cast<int32_t>(key));
-        }
-    }
-    if (ctr->exhausted) return;  // PoolExhausted: the update list is never reached
-    const unsigned long long hw = vc->high_water;
-    const uint32_t base = ctr->upd_base;
-    const Intr& intr = fc->intr;
-    for (unsigned long long s = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; s < hw; s += stride) {
-        const int32_t key = slot_key[s];
-        bool vis = false;
-        if (key >= 0 && !((keybits[key >> 5] >> (key & 31)) & 1u)) {
-            int bx, by, bz;
-            if (P.nshift >= 0) {
-                bx = key & (P.N - 1);
-                by = (key >> P.nshift) & (P.N - 1);
-                bz = key >> (2 * P.nshift);
-            } else {
-                bx = key % P.N;
-                by = (key / P.N) % P.N;
-                bz = key / (P.N * P.N);
-            }
-            const d3 lo = block_min_corner(P, bx, by, bz);
-            const double side = P.block_side;
-            const d3 hi = add(lo, mk(side, side, side));
-            // a sharded volume integrates only its own blocks (mirrored halo blocks are read-only)
-            if (shard_owns(P, bx, by, bz) && (block_surely_inside(P, fc, lo) || frustum_intersects_block(P, fc, lo, hi))) {
-                for (int k = 0; k < 9 && !vis; ++k) {
-                    const d3 probe = k == 8 ? add(lo, mk(0.5 * side, 0.5 * side, 0.5 * side))
-                                            : add(lo, mk(k & 1 ? side : 0.0, k & 2 ? side : 0.0, k & 4 ? side : 0.0));
-                    const d3 xc = apply(fc->inv, probe);
-                    double pu, pv;
-                    if (!project(intr, xc, pu, pv)) continue;
-                    const int u = ref_lround_int(pu);
-                    const int v = ref_lround_int(pv);
-                    if (!(u >= 0 && v >= 0 && u < w && v < h)) continue;
-                    const float d = depth[(size_t)v * w + u];
-                    if (!(d > 0.0f) || xc.z <= d + fc->delta) vis = true;
-                }
-            }
-        }
-        const uint32_t j = warp_append(vis, &ctr->n_update);
-        if (vis) work[base + j] = make_int2(static_cast<int32_t>(s), key);
     }
 }
 
@@ -1390,17 +1441,14 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
     } else {
         // fuse_frame: unordered key set + ranked new keys + work list (no global sort)
         k_block_keys_set<<<(su * sv + kThreads - 1) / kThreads, kThreads, 0, s>>>(
-            P, fb.fc, depth, w, h, fb.stride, su, sv, v.d_keybits, fb.keys_unique, fb.ctr);
+            P, fb.fc, depth, w, h, fb.stride, su, sv, v.d_keybits, fb.keys_unique, fb.ctr, v.d_table, fb.ranks,
+            fb.flags, fb.work);
         SF_LAUNCH_CHECK();
-        k_alloc_classify<<<kSmallCtas, kThreads, 0, s>>>(fb.ctr, fb.keys_unique, v.d_table, fb.flags, fb.ranks);
+        k_alloc_visible<<<kPersistentCtas, kThreads, 0, s>>>(P, fb.fc, fb.ctr, v.d_vc, fb.ranks, fb.flags, v.d_table,
+                                                            v.d_free_list, v.d_slot_key, v.d_occ, fb.keys_unique,
+                                                            v.d_keybits, depth, w, h, fb.work);
         SF_LAUNCH_CHECK();
-        k_alloc_rank<<<kSmallCtas, kThreads, 0, s>>>(P, fb.ctr, fb.ranks, v.d_table, v.d_free_list, v.d_slot_key,
-                                                     v.d_occ, v.d_vc);
-        SF_LAUNCH_CHECK();
-        k_worklist<<<kPersistentCtas, kThreads, 0, s>>>(P, fb.fc, fb.ctr, v.d_vc, v.d_slot_key, v.d_table,
-                                                        fb.keys_unique, fb.flags, v.d_keybits, depth, w, h, fb.work);
-        SF_LAUNCH_CHECK();
-        n += 4;
+        n += 2;
     }
     if (!export_only) {
         unsigned long long* vu = &fb.ctr->voxels_updated;

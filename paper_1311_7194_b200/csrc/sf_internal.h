@@ -79,6 +79,7 @@ struct FrameCounters {
     unsigned long long exact_voxels;  // integrate: voxels decided on the FP64 fallback path
     uint32_t row_chunks;              // integrate: next row chunk (dynamic scheduling)
     uint32_t pad_;
+    unsigned long long hw_before;     // slot high-water mark when the frame started
     unsigned long long t_begin;       // integrate: first CTA start (%globaltimer, ns)
     unsigned long long t_end;         // integrate: last CTA end
 };

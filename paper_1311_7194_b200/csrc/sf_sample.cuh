@@ -294,6 +294,7 @@ __device__ inline void fuse_begin_body(FrameCounters* ctr, const VolCounters* vc
     z.alloc_before = vc->allocated_count - vc->halo_count;  // owned blocks only
     z.skip = dead ? static_cast<uint32_t>(*dead != 0) : 0u;
     z.t_begin = ~0ull;
+    z.hw_before = vc->high_water;
     *ctr = z;
 }
 __device__ inline void fuse_finalize_body(FrameCounters* ctr, const VolCounters* vc) {
