@@ -146,6 +146,7 @@ struct sf_volume {
     uint32_t* d_occ = nullptr;       // occupancy bitmap, N^3 bits
     uint32_t* d_keybits = nullptr;   // the frame's allocate-list keys, N^3 bits (zero between frames)
     sf::VolCounters* d_vc = nullptr;
+    uint32_t* d_sched = nullptr;     // self-resetting work counters of persistent kernels (zero between launches)
     sf::AuxTables* d_aux = nullptr;
     sf::AuxTables h_aux{};
     sf::FrameBuffers fb;  // scratch for the stand-alone API calls

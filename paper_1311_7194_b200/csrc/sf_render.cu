@@ -9,6 +9,7 @@
 // All arithmetic is FP64 in the reference's order (no contraction), so depth, normals and
 // the stage-1 sample count are bit-identical to the CPU path.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -124,11 +125,11 @@ __device__ __forceinline__ bool dda_jump(Dda& s, double T) {
     return true;
 }
 
-__global__ void __launch_bounds__(256, 3) k_ray_bounds(VolParams P, const FrameConsts* __restrict__ fc, const uint32_t* __restrict__ occ,
+__global__ void __launch_bounds__(256, 2) k_ray_bounds(VolParams P, const FrameConsts* __restrict__ fc, const uint32_t* __restrict__ occ,
                              const VolCounters* __restrict__ vc, float* __restrict__ t_start,
                              float* __restrict__ t_end, int w, int h, const int* dead, int* __restrict__ ray_list,
                              RayCounters* list_ctr, float* __restrict__ depth_out, float* __restrict__ normals_out,
-                             double jump_cells) {
+                             double jump_cells, uint32_t* __restrict__ sched, unsigned long long* __restrict__ dbg) {
     // Coarse occupancy (1 bit per 16^3 blocks) staged in shared memory: the DDA only reads
     // the fine bitmap (L2) inside super-blocks that ever held a block. Exact: a clear coarse
     // bit implies every block of the super-block is EMPTY.
@@ -141,193 +142,250 @@ __global__ void __launch_bounds__(256, 3) k_ray_bounds(VolParams P, const FrameC
         for (int i = tid; i < cwords; i += blockDim.x * blockDim.y) s_coarse[i] = __ldg(&occ[P.occ_fine_words + i]);
         __syncthreads();
     }
-    // Each warp takes an 8x4 pixel patch of the CTA's 32x8 tile (rather than a 32x1 row):
-    // neighbouring rays have similar DDA lengths, so fewer lanes idle in the step loop.
+    // Persistent CTAs; each warp takes 8x4-pixel patches from a counter (neighbouring rays have
+    // similar DDA lengths, so fewer lanes idle in the step loop; dynamic patches balance the
+    // SMs: ray cost varies by orders of magnitude across the image).
     const int tl = threadIdx.y * blockDim.x + threadIdx.x;
-    const int wp = tl >> 5, ln = tl & 31;
-    const int u = blockIdx.x * blockDim.x + (wp & 3) * 8 + (ln & 7);
-    const int v = blockIdx.y * blockDim.y + (wp >> 2) * 4 + (ln >> 3);
-    if (u >= w || v >= h) return;
-    const size_t idx = (size_t)v * w + u;
-    float ts = INFINITY, te = -INFINITY;
-    if (vc->allocated_count != 0) {
-        const Intr& intr = fc->intr;
-        const Pose& pose = fc->pose;
-        const int n = P.N;
-        const double side = P.block_side;
-        const double box_lo[3] = {P.ox, P.oy, P.oz};
-        const double box_hi[3] = {P.ox + P.box_side, P.oy + P.box_side, P.oz + P.box_side};
-        const double org[3] = {pose.t.x, pose.t.y, pose.t.z};
-        const d3 dir_cam = normalized(unproject(intr, u, v, 1.0));
-        const d3 dv3 = mv(pose.R, dir_cam);
-        const double dir[3] = {dv3.x, dv3.y, dv3.z};
-        double lo = intr.near_plane / dir_cam.z;
-        double hi = intr.far_plane / dir_cam.z;
-        for (int a = 0; a < 3; ++a) {
-            if (fabs(dir[a]) < 1e-15) {
-                if (org[a] < box_lo[a] || org[a] > box_hi[a]) {
-                    lo = 1.0;
-                    hi = 0.0;
-                    break;
-                }
-                continue;
-            }
-            double t0 = (box_lo[a] - org[a]) / dir[a];
-            double t1 = (box_hi[a] - org[a]) / dir[a];
-            if (t0 > t1) {
-                const double tmp = t0;
-                t0 = t1;
-                t1 = tmp;
-            }
-            lo = dmax(lo, t0);
-            hi = dmin(hi, t1);
-        }
-        // Conservative reject: a ray missing the occupied bounding box (grown by one block)
-        // meets no allocated block, so its DDA would find nothing.
-        const int* bb = occ_bbox(P, occ);
-        const int bx0 = bb[0], by0 = bb[1], bz0 = bb[2], bx1 = bb[3], by1 = bb[4], bz1 = bb[5];
-        double t_grown = -INFINITY;  // entry time into the occupied box grown by one block
-        if (lo <= hi && bx0 <= bx1) {
-            double rlo = lo, rhi = hi;
-            const int bl[3] = {bx0, by0, bz0}, bh[3] = {bx1, by1, bz1};
-#pragma unroll
+    const int ln = tl & 31;
+    const int pw = (w + 7) >> 3, n_patches = pw * ((h + 3) >> 2);
+    for (;;) {
+        int patch = 0;
+        if (ln == 0) patch = static_cast<int>(atomicAdd(&sched[0], 1u));
+        patch = __shfl_sync(0xffffffffu, patch, 0);
+        if (patch >= n_patches) break;
+        const int u = (patch % pw) * 8 + (ln & 7);
+        const int v = (patch / pw) * 4 + (ln >> 3);
+        if (u >= w || v >= h) continue;
+        const size_t idx = (size_t)v * w + u;
+        float ts = INFINITY, te = -INFINITY;
+        unsigned long long dbg_t0 = dbg ? globaltimer_ns() : 0ull;
+        unsigned dbg_steps = 0;
+        if (vc->allocated_count != 0) {
+            const Intr& intr = fc->intr;
+            const Pose& pose = fc->pose;
+            const int n = P.N;
+            const double side = P.block_side;
+            const double box_lo[3] = {P.ox, P.oy, P.oz};
+            const double box_hi[3] = {P.ox + P.box_side, P.oy + P.box_side, P.oz + P.box_side};
+            const double org[3] = {pose.t.x, pose.t.y, pose.t.z};
+            const d3 dir_cam = normalized(unproject(intr, u, v, 1.0));
+            const d3 dv3 = mv(pose.R, dir_cam);
+            const double dir[3] = {dv3.x, dv3.y, dv3.z};
+            double lo = intr.near_plane / dir_cam.z;
+            double hi = intr.far_plane / dir_cam.z;
             for (int a = 0; a < 3; ++a) {
-                const double wlo = box_lo[a] + (double)(bl[a] - 1) * side;
-                const double whi = box_lo[a] + (double)(bh[a] + 2) * side;
-                if (fabs(dir[a]) < 1e-300) {
-                    if (org[a] < wlo || org[a] > whi) rhi = -INFINITY;
+                if (fabs(dir[a]) < 1e-15) {
+                    if (org[a] < box_lo[a] || org[a] > box_hi[a]) {
+                        lo = 1.0;
+                        hi = 0.0;
+                        break;
+                    }
                     continue;
                 }
-                double t0 = (wlo - org[a]) / dir[a], t1 = (whi - org[a]) / dir[a];
+                double t0 = (box_lo[a] - org[a]) / dir[a];
+                double t1 = (box_hi[a] - org[a]) / dir[a];
                 if (t0 > t1) {
                     const double tmp = t0;
                     t0 = t1;
                     t1 = tmp;
                 }
-                rlo = dmax(rlo, t0);
-                rhi = dmin(rhi, t1);
+                lo = dmax(lo, t0);
+                hi = dmin(hi, t1);
             }
-            if (!(rlo <= rhi)) lo = 1.0, hi = 0.0;
-            t_grown = rlo;
-        }
-        if (lo <= hi && bx0 <= bx1) {
-            // Scalar (register-resident) Amanatides-Woo state; same operations as render.cpp:103-144.
-            const double ex = org[0] + lo * dir[0], ey = org[1] + lo * dir[1], ez = org[2] + lo * dir[2];
-            auto clampc = [n](int c) { return c < 0 ? 0 : (n - 1 < c ? n - 1 : c); };  // std::clamp(c, 0, n-1)
-            int cx = clampc(ref_floor_int((ex - box_lo[0]) / side));
-            int cy = clampc(ref_floor_int((ey - box_lo[1]) / side));
-            int cz = clampc(ref_floor_int((ez - box_lo[2]) / side));
-            auto init_axis = [&](double d, double blo, int c, double e, int& st, double& tm, double& td) {
-                if (d > 1e-15) {
-                    st = 1;
-                    tm = lo + (blo + (double)(c + 1) * side - e) / d;
-                    td = side / d;
-                } else if (d < -1e-15) {
-                    st = -1;
-                    tm = lo + (blo + (double)c * side - e) / d;
-                    td = -side / d;
-                } else {
-                    st = 0;
-                    tm = INFINITY;
-                    td = INFINITY;
-                }
-            };
-            Dda s;
-            s.cx = cx;
-            s.cy = cy;
-            s.cz = cz;
-            init_axis(dir[0], box_lo[0], cx, ex, s.sx, s.tmx, s.tdx);
-            init_axis(dir[1], box_lo[1], cy, ey, s.sy, s.tmy, s.tdy);
-            init_axis(dir[2], box_lo[2], cz, ez, s.sz, s.tmz, s.tdz);
-            s.t_in = lo;
-            double first = INFINITY, last = -INFINITY;
-            const double td_min = dmin(s.tdx, dmin(s.tdy, s.tdz));
-            // Skip the run-up to the occupied box: every cell entered before the ray reaches
-            // the box grown by one block lies outside the occupied box.
-            if (t_grown > lo + 4.0 * td_min) dda_jump(s, t_grown);
-            const double sb_side = side * (1 << kCoarseShift);
-            int declined_cc = -1;  // coarse cell whose skip was judged too short to jump
-            while (s.t_in <= hi) {
-                // Past the occupied box in the direction of travel: no later cell can be
-                // allocated (cells move monotonically per axis), so first/last are final.
-                if ((s.sx >= 0 && s.cx > bx1) || (s.sx <= 0 && s.cx < bx0) || (s.sy >= 0 && s.cy > by1) ||
-                    (s.sy <= 0 && s.cy < by0) || (s.sz >= 0 && s.cz > bz1) || (s.sz <= 0 && s.cz < bz0))
-                    break;
-                const int axis = s.tmx <= s.tmy ? (s.tmx <= s.tmz ? 0 : 2) : (s.tmy <= s.tmz ? 1 : 2);
-                const double tm = axis == 0 ? s.tmx : (axis == 1 ? s.tmy : s.tmz);
-                const double t_out = dmin(tm, hi);
-                const int cc =
-                    ((s.cz >> kCoarseShift) * P.Nc + (s.cy >> kCoarseShift)) * P.Nc + (s.cx >> kCoarseShift);
-                if (!((s_coarse[cc >> 5] >> (cc & 31)) & 1u) && cc != declined_cc) {
-                    // Super-block never held a block: jump to a quarter cell before the ray
-                    // leaves it (the cells visited up to then are inside it, hence empty).
-                    const int sbx = s.cx >> kCoarseShift, sby = s.cy >> kCoarseShift, sbz = s.cz >> kCoarseShift;
-                    const double ox_ = box_lo[0] + sbx * sb_side, oy_ = box_lo[1] + sby * sb_side,
-                                 oz_ = box_lo[2] + sbz * sb_side;
-                    double t_exit = INFINITY;
-                    if (s.sx > 0) t_exit = dmin(t_exit, (ox_ + sb_side - org[0]) / dir[0]);
-                    if (s.sx < 0) t_exit = dmin(t_exit, (ox_ - org[0]) / dir[0]);
-                    if (s.sy > 0) t_exit = dmin(t_exit, (oy_ + sb_side - org[1]) / dir[1]);
-                    if (s.sy < 0) t_exit = dmin(t_exit, (oy_ - org[1]) / dir[1]);
-                    if (s.sz > 0) t_exit = dmin(t_exit, (oz_ + sb_side - org[2]) / dir[2]);
-                    if (s.sz < 0) t_exit = dmin(t_exit, (oz_ - org[2]) / dir[2]);
-                    const double T = dmin(t_exit, hi) - 0.25 * td_min;
-                    // a jump costs a few hundred instructions: worth it past ~16 plain steps
-                    if (T > tm + jump_cells * td_min && dda_jump(s, T)) {
-                        if (s.cx < 0 || s.cx >= n || s.cy < 0 || s.cy >= n || s.cz < 0 || s.cz >= n) break;
+            // Conservative reject: a ray missing the occupied bounding box (grown by one block)
+            // meets no allocated block, so its DDA would find nothing.
+            const int* bb = occ_bbox(P, occ);
+            const int bx0 = bb[0], by0 = bb[1], bz0 = bb[2], bx1 = bb[3], by1 = bb[4], bz1 = bb[5];
+            double t_grown = -INFINITY;  // entry time into the occupied box grown by one block
+            if (lo <= hi && bx0 <= bx1) {
+                double rlo = lo, rhi = hi;
+                const int bl[3] = {bx0, by0, bz0}, bh[3] = {bx1, by1, bz1};
+    #pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const double wlo = box_lo[a] + (double)(bl[a] - 1) * side;
+                    const double whi = box_lo[a] + (double)(bh[a] + 2) * side;
+                    if (fabs(dir[a]) < 1e-300) {
+                        if (org[a] < wlo || org[a] > whi) rhi = -INFINITY;
                         continue;
                     }
-                    declined_cc = cc;  // short crossing: plain steps through it (no occupancy reads)
-                } else if (cc == declined_cc) {
-                    // inside a super-block that never held a block: the cell is empty
-                } else if (s.cx >= bx0 && s.cx <= bx1 && s.cy >= by0 && s.cy <= by1 && s.cz >= bz0 && s.cz <= bz1 &&
-                           occupied(occ, table_index(P, s.cx, s.cy, s.cz))) {
-                    first = dmin(first, s.t_in);
-                    last = dmax(last, t_out);
+                    double t0 = (wlo - org[a]) / dir[a], t1 = (whi - org[a]) / dir[a];
+                    if (t0 > t1) {
+                        const double tmp = t0;
+                        t0 = t1;
+                        t1 = tmp;
+                    }
+                    rlo = dmax(rlo, t0);
+                    rhi = dmin(rhi, t1);
                 }
-                s.t_in = tm;
-                if (axis == 0) {
-                    s.cx += s.sx;
-                    if (s.cx < 0 || s.cx >= n) break;
-                    s.tmx += s.tdx;
-                } else if (axis == 1) {
-                    s.cy += s.sy;
-                    if (s.cy < 0 || s.cy >= n) break;
-                    s.tmy += s.tdy;
-                } else {
-                    s.cz += s.sz;
-                    if (s.cz < 0 || s.cz >= n) break;
-                    s.tmz += s.tdz;
+                if (!(rlo <= rhi)) lo = 1.0, hi = 0.0;
+                t_grown = rlo;
+            }
+            if (lo <= hi && bx0 <= bx1) {
+                // Scalar (register-resident) Amanatides-Woo state; same operations as render.cpp:103-144.
+                const double ex = org[0] + lo * dir[0], ey = org[1] + lo * dir[1], ez = org[2] + lo * dir[2];
+                auto clampc = [n](int c) { return c < 0 ? 0 : (n - 1 < c ? n - 1 : c); };  // std::clamp(c, 0, n-1)
+                int cx = clampc(ref_floor_int((ex - box_lo[0]) / side));
+                int cy = clampc(ref_floor_int((ey - box_lo[1]) / side));
+                int cz = clampc(ref_floor_int((ez - box_lo[2]) / side));
+                auto init_axis = [&](double d, double blo, int c, double e, int& st, double& tm, double& td) {
+                    if (d > 1e-15) {
+                        st = 1;
+                        tm = lo + (blo + (double)(c + 1) * side - e) / d;
+                        td = side / d;
+                    } else if (d < -1e-15) {
+                        st = -1;
+                        tm = lo + (blo + (double)c * side - e) / d;
+                        td = -side / d;
+                    } else {
+                        st = 0;
+                        tm = INFINITY;
+                        td = INFINITY;
+                    }
+                };
+                Dda s;
+                s.cx = cx;
+                s.cy = cy;
+                s.cz = cz;
+                init_axis(dir[0], box_lo[0], cx, ex, s.sx, s.tmx, s.tdx);
+                init_axis(dir[1], box_lo[1], cy, ey, s.sy, s.tmy, s.tdy);
+                init_axis(dir[2], box_lo[2], cz, ez, s.sz, s.tmz, s.tdz);
+                s.t_in = lo;
+                double first = INFINITY, last = -INFINITY;
+                const double td_min = dmin(s.tdx, dmin(s.tdy, s.tdz));
+                // Skip the run-up to the occupied box: every cell entered before the ray reaches
+                // the box grown by one block lies outside the occupied box.
+                if (t_grown > lo + 4.0 * td_min) { dda_jump(s, t_grown); dbg_steps += 1u << 16; }
+                const double sb_side = side * (1 << kCoarseShift);
+                int declined_cc = -1;  // coarse cell whose skip was judged too short to jump
+                // Loop state derived from the cells (recomputed after a jump, stepped otherwise):
+                //  r* = steps left on an axis before the ray leaves the occupied box in its direction
+                //       of travel (no later cell can be allocated: cells move monotonically per axis,
+                //       so first/last are final there); the original loop tests all three per step,
+                //       only the stepped axis can change;
+                //  in-box test r* <= w*; table index and coarse cell kept incrementally.
+                const int wx = bx1 - bx0, wy = by1 - by0, wz = bz1 - bz0;
+                const int kx = s.sx, ky = s.sy * n, kz = s.sz * n * n;  // N^3 < 2^31 (N <= 1024)
+                const double inv_dir[3] = {1.0 / dir[0], 1.0 / dir[1], 1.0 / dir[2]};
+                int rx, ry, rz, cc, key;
+                uint32_t cbit;
+                auto derive = [&]() {
+                    rx = s.sx > 0 ? bx1 - s.cx : s.cx - bx0;
+                    ry = s.sy > 0 ? by1 - s.cy : s.cy - by0;
+                    rz = s.sz > 0 ? bz1 - s.cz : s.cz - bz0;
+                    key = (s.cz * n + s.cy) * n + s.cx;
+                    cc = ((s.cz >> kCoarseShift) * P.Nc + (s.cy >> kCoarseShift)) * P.Nc + (s.cx >> kCoarseShift);
+                    cbit = (s_coarse[cc >> 5] >> (cc & 31)) & 1u;
+                };
+                // an axis that does not move must lie inside the box, else no cell ever is
+                // (sx == 0: r = c - b0 must be in [0, w])
+                auto outside = [&]() {
+                    return rx < 0 || ry < 0 || rz < 0 || (s.sx == 0 && rx > wx) || (s.sy == 0 && ry > wy) ||
+                           (s.sz == 0 && rz > wz);
+                };
+                bool live = s.cx >= 0 && s.cx < n && s.cy >= 0 && s.cy < n && s.cz >= 0 && s.cz < n;
+                if (live) {
+                    derive();
+                    live = !outside();
+                }
+                while (live && s.t_in <= hi) {
+                    ++dbg_steps;
+                    const int axis = s.tmx <= s.tmy ? (s.tmx <= s.tmz ? 0 : 2) : (s.tmy <= s.tmz ? 1 : 2);
+                    const double tm = axis == 0 ? s.tmx : (axis == 1 ? s.tmy : s.tmz);
+                    if (!cbit && cc != declined_cc) {
+                        // Super-block never held a block: jump to a quarter cell before the ray
+                        // leaves it (the cells visited up to then are inside it, hence empty).
+                        const int sbx = s.cx >> kCoarseShift, sby = s.cy >> kCoarseShift, sbz = s.cz >> kCoarseShift;
+                        const double ox_ = box_lo[0] + sbx * sb_side, oy_ = box_lo[1] + sby * sb_side,
+                                     oz_ = box_lo[2] + sbz * sb_side;
+                        // exit time through the reciprocal: the quarter-cell margin of T below
+                        // absorbs its rounding (a few ulps of t)
+                        double t_exit = INFINITY;
+                        if (s.sx != 0) t_exit = dmin(t_exit, ((s.sx > 0 ? ox_ + sb_side : ox_) - org[0]) * inv_dir[0]);
+                        if (s.sy != 0) t_exit = dmin(t_exit, ((s.sy > 0 ? oy_ + sb_side : oy_) - org[1]) * inv_dir[1]);
+                        if (s.sz != 0) t_exit = dmin(t_exit, ((s.sz > 0 ? oz_ + sb_side : oz_) - org[2]) * inv_dir[2]);
+                        const double T = dmin(t_exit, hi) - 0.25 * td_min;
+                        // a jump costs a few hundred instructions: worth it past ~16 plain steps
+                        if (T > tm + jump_cells * td_min && (dbg_steps += 1u << 16, dda_jump(s, T))) {
+                            if (s.cx < 0 || s.cx >= n || s.cy < 0 || s.cy >= n || s.cz < 0 || s.cz >= n) break;
+                            derive();
+                            if (outside()) break;
+                            continue;
+                        }
+                        declined_cc = cc;  // short crossing: plain steps through it (no occupancy reads)
+                    } else if (cc != declined_cc && rx <= wx && ry <= wy && rz <= wz && occupied(occ, static_cast<uint32_t>(key))) {
+                        // t_in and t_out never decrease along the ray
+                        if (first == INFINITY) first = s.t_in;
+                        last = dmin(tm, hi);
+                    }
+                    s.t_in = tm;
+                    int cold;
+                    if (axis == 0) {
+                        cold = s.cx;
+                        s.cx += s.sx;
+                        if (--rx < 0) break;
+                        s.tmx += s.tdx;
+                        key += kx;
+                        cold ^= s.cx;
+                    } else if (axis == 1) {
+                        cold = s.cy;
+                        s.cy += s.sy;
+                        if (--ry < 0) break;
+                        s.tmy += s.tdy;
+                        key += ky;
+                        cold ^= s.cy;
+                    } else {
+                        cold = s.cz;
+                        s.cz += s.sz;
+                        if (--rz < 0) break;
+                        s.tmz += s.tdz;
+                        key += kz;
+                        cold ^= s.cz;
+                    }
+                    if (cold >> kCoarseShift) {  // crossed into another super-block
+                        cc = ((s.cz >> kCoarseShift) * P.Nc + (s.cy >> kCoarseShift)) * P.Nc + (s.cx >> kCoarseShift);
+                        cbit = (s_coarse[cc >> 5] >> (cc & 31)) & 1u;
+                    }
+                }
+                if (first <= last) {
+                    ts = (float)dmax(first, lo);
+                    te = (float)dmin(last, hi);
                 }
             }
-            if (first <= last) {
-                ts = (float)dmax(first, lo);
-                te = (float)dmin(last, hi);
+        }
+        t_start[idx] = ts;
+        t_end[idx] = te;
+        if (dbg) {
+            dbg[3 * idx] = dbg_t0;
+            dbg[3 * idx + 1] = globaltimer_ns();
+            dbg[3 * idx + 2] = dbg_steps | ((unsigned long long)(blockIdx.x) << 32);
+        }
+        if (ray_list) {
+            // Active-ray list for the march (warp-aggregated append); inactive pixels get the
+            // empty raycast result here.
+            const bool act = ts <= te;
+            if (!act) {
+                depth_out[idx] = 0.0f;
+                normals_out[3 * idx] = 0.0f;
+                normals_out[3 * idx + 1] = 0.0f;
+                normals_out[3 * idx + 2] = 0.0f;
             }
+            const unsigned am = __activemask();
+            const unsigned bal = __ballot_sync(am, act);
+            const int lane = (threadIdx.y * blockDim.x + threadIdx.x) & 31;
+            unsigned long long base = 0;
+            if (bal) {
+                const int leader = __ffs(bal) - 1;
+                if (lane == leader) base = atomicAdd(&list_ctr->listed, static_cast<unsigned long long>(__popc(bal)));
+                base = __shfl_sync(am, base, leader);
+            }
+            if (act) ray_list[base + __popc(bal & ((1u << lane) - 1u))] = static_cast<int>(idx);
         }
     }
-    t_start[idx] = ts;
-    t_end[idx] = te;
-    if (ray_list) {
-        // Active-ray list for the march (warp-aggregated append); inactive pixels get the
-        // empty raycast result here.
-        const bool act = ts <= te;
-        if (!act) {
-            depth_out[idx] = 0.0f;
-            normals_out[3 * idx] = 0.0f;
-            normals_out[3 * idx + 1] = 0.0f;
-            normals_out[3 * idx + 2] = 0.0f;
-        }
-        const unsigned am = __activemask();
-        const unsigned bal = __ballot_sync(am, act);
-        const int lane = (threadIdx.y * blockDim.x + threadIdx.x) & 31;
-        unsigned long long base = 0;
-        if (bal) {
-            const int leader = __ffs(bal) - 1;
-            if (lane == leader) base = atomicAdd(&list_ctr->listed, static_cast<unsigned long long>(__popc(bal)));
-            base = __shfl_sync(am, base, leader);
-        }
-        if (act) ray_list[base + __popc(bal & ((1u << lane) - 1u))] = static_cast<int>(idx);
+    // last CTA out resets the counters for the next launch
+    __syncthreads();
+    if (tl == 0 && atomicAdd(&sched[1], 1u) == gridDim.x - 1) {
+        sched[0] = 0;
+        sched[1] = 0;
     }
 }
 
@@ -553,16 +611,37 @@ static double ray_jump_cells() {
     return j;
 }
 
+// Debug (SF_RB_DEBUG=<path>): per-ray start/end device times and DDA step counts of every
+// ray-bounds launch appended to <path> (synchronises the stream; never in a captured graph).
+static unsigned long long* rb_debug_buffer(size_t n) {
+    static unsigned long long* buf = nullptr;
+    if (!std::getenv("SF_RB_DEBUG")) return nullptr;
+    if (!buf) SF_CUDA(cudaMalloc(&buf, 3 * n * sizeof(unsigned long long)));
+    return buf;
+}
+static void rb_debug_dump(unsigned long long* buf, size_t n, cudaStream_t s) {
+    if (!buf) return;
+    std::vector<unsigned long long> h(3 * n);
+    SF_CUDA(cudaMemcpyAsync(h.data(), buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    SF_CUDA(cudaStreamSynchronize(s));
+    if (FILE* f = std::fopen(std::getenv("SF_RB_DEBUG"), "ab")) {
+        std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+        std::fclose(f);
+    }
+}
+
 void launch_ray_bounds(Volume& v, const FrameConsts* d_fc, const Intr& intr, float* t_start, float* t_end,
                        cudaStream_t s, uint64_t* launches, const int* dead_flag, int* ray_list,
                        RayCounters* list_ctr, float* depth, float* normals) {
-    const dim3 blk(32, 8), grd((intr.w + 31) / 32, (intr.h + 7) / 8);
+    unsigned long long* rb_dbg = rb_debug_buffer((size_t)intr.w * intr.h);
+    const dim3 blk(32, 8), grd(148 * 2);
     const uint64_t nc = v.P.Nc;
     const size_t smem = ((nc * nc * nc + 31) / 32) * sizeof(uint32_t);
     if (smem > 48 * 1024) SF_CUDA(cudaFuncSetAttribute(k_ray_bounds, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_ray_bounds<<<grd, blk, smem, s>>>(v.P, d_fc, v.d_occ, v.d_vc, t_start, t_end, intr.w, intr.h, dead_flag,
-                                        ray_list, list_ctr, depth, normals, ray_jump_cells());
+                                        ray_list, list_ctr, depth, normals, ray_jump_cells(), v.d_sched, rb_dbg);
     SF_LAUNCH_CHECK();
+    rb_debug_dump(rb_dbg, (size_t)intr.w * intr.h, s);
     if (launches) *launches += 1;
 }
 

@@ -293,6 +293,8 @@ static VolParams make_params(const sf_grid_config& c, const sf_aux_quant& a, uin
     P.aux_lg_pmin = a.mode == 1 ? std::log2(a.p_min) : 0.0;
     P.aux_lg_scale = a.mode == 1 ? 255.0 / std::log2(a.p_max / a.p_min) : 0.0;
     P.table_size = static_cast<uint64_t>(P.N) * P.N * P.N;
+    // table indices travel as int32 (slot -> key map, work items, ray DDA)
+    if (P.table_size > 0x7fffffffull) throw Error(SF_INVALID_ARGUMENT, "grid: more than 2^31 blocks (N^3)");
     P.capacity = capacity;
     P.Nc = (P.N + (1 << kCoarseShift) - 1) >> kCoarseShift;
     P.mshift = -1;
@@ -346,6 +348,8 @@ static void volume_init_device(Volume& v) {
     SF_CUDA(cudaMalloc(&v.d_keybits, P.occ_fine_words * sizeof(uint32_t)));
     SF_CUDA(cudaMemset(v.d_keybits, 0, P.occ_fine_words * sizeof(uint32_t)));
     SF_CUDA(cudaMalloc(&v.d_vc, sizeof(VolCounters)));
+    SF_CUDA(cudaMalloc(&v.d_sched, 8 * sizeof(uint32_t)));
+    SF_CUDA(cudaMemset(v.d_sched, 0, 8 * sizeof(uint32_t)));
     SF_CUDA(cudaMalloc(&v.d_aux, sizeof(AuxTables)));
     SF_CUDA(cudaMemset(v.d_table, 0xFF, P.table_size * sizeof(int32_t)));
     SF_CUDA(cudaMemset(v.d_occ, 0, occ_words * sizeof(uint32_t)));
@@ -373,7 +377,7 @@ static void volume_free_device(Volume& v) {
     cudaSetDevice(v.device);
     v.fb.release();
     void* ptrs[] = {v.d_table, v.d_payload, v.d_fpayload, v.d_free_list, v.d_slot_key, v.d_occ, v.d_keybits,
-                    v.d_vc,    v.d_aux};
+                    v.d_vc,    v.d_aux,      v.d_sched};
     for (void* p : ptrs)
         if (p) cudaFree(p);
 }
