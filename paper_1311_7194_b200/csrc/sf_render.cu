@@ -287,7 +287,9 @@ __global__ void __launch_bounds__(256, 2) k_ray_bounds(VolParams P, const FrameC
                     derive();
                     live = !outside();
                 }
-                while (live && s.t_in <= hi) {
+                uint32_t pend_word = 0, pend_bit = 0;  // occupancy probe of the previous step
+            double pend_tin = 0.0, pend_tout = 0.0;
+            while (live && s.t_in <= hi) {
                     ++dbg_steps;
                     const int axis = s.tmx <= s.tmy ? (s.tmx <= s.tmz ? 0 : 2) : (s.tmy <= s.tmz ? 1 : 2);
                     const double tm = axis == 0 ? s.tmx : (axis == 1 ? s.tmy : s.tmz);
@@ -312,39 +314,47 @@ __global__ void __launch_bounds__(256, 2) k_ray_bounds(VolParams P, const FrameC
                             continue;
                         }
                         declined_cc = cc;  // short crossing: plain steps through it (no occupancy reads)
-                    } else if (cc != declined_cc && rx <= wx && ry <= wy && rz <= wz && occupied(occ, static_cast<uint32_t>(key))) {
-                        // t_in and t_out never decrease along the ray
-                        if (first == INFINITY) first = s.t_in;
-                        last = dmin(tm, hi);
+                    }
+                    // Occupancy of the cell (only inside a super-block that ever held a block;
+                    // cbit set implies cc != declined_cc). The word is consumed one step later,
+                    // so its load overlaps the next DDA step instead of stalling this one.
+                    {
+                        const bool probe = cbit && rx <= wx && ry <= wy && rz <= wz;
+                        const uint32_t word = probe ? __ldg(&occ[static_cast<uint32_t>(key) >> 5]) : 0u;
+                        if ((pend_word >> pend_bit) & 1u) {  // t_in and t_out never decrease along the ray
+                            if (first == INFINITY) first = pend_tin;
+                            last = pend_tout;
+                        }
+                        pend_word = word;
+                        pend_bit = static_cast<uint32_t>(key) & 31u;
+                        pend_tin = s.t_in;
+                        pend_tout = dmin(tm, hi);
                     }
                     s.t_in = tm;
-                    int cold;
-                    if (axis == 0) {
-                        cold = s.cx;
-                        s.cx += s.sx;
-                        if (--rx < 0) break;
-                        s.tmx += s.tdx;
-                        key += kx;
-                        cold ^= s.cx;
-                    } else if (axis == 1) {
-                        cold = s.cy;
-                        s.cy += s.sy;
-                        if (--ry < 0) break;
-                        s.tmy += s.tdy;
-                        key += ky;
-                        cold ^= s.cy;
-                    } else {
-                        cold = s.cz;
-                        s.cz += s.sz;
-                        if (--rz < 0) break;
-                        s.tmz += s.tdz;
-                        key += kz;
-                        cold ^= s.cz;
-                    }
-                    if (cold >> kCoarseShift) {  // crossed into another super-block
+                    // step the axis with the smallest tm (branch-free: the lanes of a warp step
+                    // different axes)
+                    const bool a0 = axis == 0, a1 = axis == 1, a2 = axis == 2;
+                    const int cxo = s.cx, cyo = s.cy, czo = s.cz;
+                    s.cx += a0 ? s.sx : 0;
+                    s.cy += a1 ? s.sy : 0;
+                    s.cz += a2 ? s.sz : 0;
+                    rx -= a0 ? 1 : 0;
+                    ry -= a1 ? 1 : 0;
+                    rz -= a2 ? 1 : 0;
+                    if ((rx | ry | rz) < 0) break;
+                    const double tn = tm + (a0 ? s.tdx : (a1 ? s.tdy : s.tdz));
+                    s.tmx = a0 ? tn : s.tmx;
+                    s.tmy = a1 ? tn : s.tmy;
+                    s.tmz = a2 ? tn : s.tmz;
+                    key += a0 ? kx : (a1 ? ky : kz);
+                    if (((cxo ^ s.cx) | (cyo ^ s.cy) | (czo ^ s.cz)) >> kCoarseShift) {  // crossed into another super-block
                         cc = ((s.cz >> kCoarseShift) * P.Nc + (s.cy >> kCoarseShift)) * P.Nc + (s.cx >> kCoarseShift);
                         cbit = (s_coarse[cc >> 5] >> (cc & 31)) & 1u;
                     }
+                }
+                if ((pend_word >> pend_bit) & 1u) {
+                    if (first == INFINITY) first = pend_tin;
+                    last = pend_tout;
                 }
                 if (first <= last) {
                     ts = (float)dmax(first, lo);
