@@ -30,7 +30,6 @@ namespace sf {
 
 constexpr int kThreads = 256;
 constexpr int kPersistentCtas = 148 * 8;
-constexpr int kSmallCtas = 148;  // passes over the <= 57.6 k allocate-list keys
 
 // ---------------------------------------------------------------------------------
 // frame setup (one warp: hull points, corner rays and SAT axes computed lane-parallel)
@@ -1415,7 +1414,6 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
         SF_LAUNCH_CHECK();
         n += 1;
     }
-    const dim3 blk2(32, 8), grd2((w + 31) / 32, (h + 7) / 8);
     const int* dead = reinterpret_cast<const int*>(&fb.ctr->skip);
     if (!export_only && !prep_done) launch_fuse_prep(v, fb, intr, depth, sigma, fp, s, &n, dead);
     const int su = (w + fb.stride - 1) / fb.stride, sv = (h + fb.stride - 1) / fb.stride;

@@ -147,6 +147,8 @@ struct sf_volume {
     uint32_t* d_keybits = nullptr;   // the frame's allocate-list keys, N^3 bits (zero between frames)
     sf::VolCounters* d_vc = nullptr;
     uint32_t* d_sched = nullptr;     // self-resetting work counters of persistent kernels (zero between launches)
+    uint32_t* d_patch_order = nullptr;  // ray-bounds patch order for an order_w x order_h image
+    int order_w = -1, order_h = -1;
     sf::AuxTables* d_aux = nullptr;
     sf::AuxTables h_aux{};
     sf::FrameBuffers fb;  // scratch for the stand-alone API calls
@@ -156,6 +158,7 @@ struct sf_volume {
 namespace sf {
 using Volume = ::sf_volume;
 void ensure_frame_buffers(Volume& v, FrameBuffers& fb, int w, int h);
+void ensure_patch_order(Volume& v, int w, int h);
 
 // Launchers shared between the stand-alone API (sf_integrate, sf_raycast, sf_icp) and the
 // tracker. All are asynchronous on `stream`; `dead_flag` (device int, may be NULL) turns

@@ -125,275 +125,290 @@ __device__ __forceinline__ bool dda_jump(Dda& s, double T) {
     return true;
 }
 
+// Ray bounds of pixel (u, v) (render.cpp:65-153): writes t_start / t_end; true when the ray
+// has bounds (!bounds.empty(u, v)).
+__device__ __forceinline__ bool bounds_pixel(const VolParams& P, const FrameConsts* __restrict__ fc,
+                                             const uint32_t* __restrict__ occ, const VolCounters* __restrict__ vc,
+                                             const uint32_t* __restrict__ s_coarse, float* __restrict__ t_start,
+                                             float* __restrict__ t_end, int w, double jump_cells,
+                                             unsigned long long* __restrict__ dbg, int u, int v) {
+    const size_t idx = (size_t)v * w + u;
+    float ts = INFINITY, te = -INFINITY;
+    unsigned long long dbg_t0 = dbg ? globaltimer_ns() : 0ull;
+    unsigned dbg_steps = 0;
+    if (vc->allocated_count != 0) {
+        const Intr& intr = fc->intr;
+        const Pose& pose = fc->pose;
+        const int n = P.N;
+        const double side = P.block_side;
+        const double box_lo[3] = {P.ox, P.oy, P.oz};
+        const double box_hi[3] = {P.ox + P.box_side, P.oy + P.box_side, P.oz + P.box_side};
+        const double org[3] = {pose.t.x, pose.t.y, pose.t.z};
+        const d3 dir_cam = normalized(unproject(intr, u, v, 1.0));
+        const d3 dv3 = mv(pose.R, dir_cam);
+        const double dir[3] = {dv3.x, dv3.y, dv3.z};
+        double lo = intr.near_plane / dir_cam.z;
+        double hi = intr.far_plane / dir_cam.z;
+        for (int a = 0; a < 3; ++a) {
+            if (fabs(dir[a]) < 1e-15) {
+                if (org[a] < box_lo[a] || org[a] > box_hi[a]) {
+                    lo = 1.0;
+                    hi = 0.0;
+                    break;
+                }
+                continue;
+            }
+            double t0 = (box_lo[a] - org[a]) / dir[a];
+            double t1 = (box_hi[a] - org[a]) / dir[a];
+            if (t0 > t1) {
+                const double tmp = t0;
+                t0 = t1;
+                t1 = tmp;
+            }
+            lo = dmax(lo, t0);
+            hi = dmin(hi, t1);
+        }
+        // Conservative reject: a ray missing the occupied bounding box (grown by one block)
+        // meets no allocated block, so its DDA would find nothing.
+        const int* bb = occ_bbox(P, occ);
+        const int bx0 = bb[0], by0 = bb[1], bz0 = bb[2], bx1 = bb[3], by1 = bb[4], bz1 = bb[5];
+        double t_grown = -INFINITY;  // entry time into the occupied box grown by one block
+        if (lo <= hi && bx0 <= bx1) {
+            double rlo = lo, rhi = hi;
+            const int bl[3] = {bx0, by0, bz0}, bh[3] = {bx1, by1, bz1};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const double wlo = box_lo[a] + (double)(bl[a] - 1) * side;
+                const double whi = box_lo[a] + (double)(bh[a] + 2) * side;
+                if (fabs(dir[a]) < 1e-300) {
+                    if (org[a] < wlo || org[a] > whi) rhi = -INFINITY;
+                    continue;
+                }
+                double t0 = (wlo - org[a]) / dir[a], t1 = (whi - org[a]) / dir[a];
+                if (t0 > t1) {
+                    const double tmp = t0;
+                    t0 = t1;
+                    t1 = tmp;
+                }
+                rlo = dmax(rlo, t0);
+                rhi = dmin(rhi, t1);
+            }
+            if (!(rlo <= rhi)) lo = 1.0, hi = 0.0;
+            t_grown = rlo;
+        }
+        if (lo <= hi && bx0 <= bx1) {
+            // Scalar (register-resident) Amanatides-Woo state; same operations as render.cpp:103-144.
+            const double ex = org[0] + lo * dir[0], ey = org[1] + lo * dir[1], ez = org[2] + lo * dir[2];
+            auto clampc = [n](int c) { return c < 0 ? 0 : (n - 1 < c ? n - 1 : c); };  // std::clamp(c, 0, n-1)
+            int cx = clampc(ref_floor_int((ex - box_lo[0]) / side));
+            int cy = clampc(ref_floor_int((ey - box_lo[1]) / side));
+            int cz = clampc(ref_floor_int((ez - box_lo[2]) / side));
+            auto init_axis = [&](double d, double blo, int c, double e, int& st, double& tm, double& td) {
+                if (d > 1e-15) {
+                    st = 1;
+                    tm = lo + (blo + (double)(c + 1) * side - e) / d;
+                    td = side / d;
+                } else if (d < -1e-15) {
+                    st = -1;
+                    tm = lo + (blo + (double)c * side - e) / d;
+                    td = -side / d;
+                } else {
+                    st = 0;
+                    tm = INFINITY;
+                    td = INFINITY;
+                }
+            };
+            Dda s;
+            s.cx = cx;
+            s.cy = cy;
+            s.cz = cz;
+            init_axis(dir[0], box_lo[0], cx, ex, s.sx, s.tmx, s.tdx);
+            init_axis(dir[1], box_lo[1], cy, ey, s.sy, s.tmy, s.tdy);
+            init_axis(dir[2], box_lo[2], cz, ez, s.sz, s.tmz, s.tdz);
+            s.t_in = lo;
+            double first = INFINITY, last = -INFINITY;
+            const double td_min = dmin(s.tdx, dmin(s.tdy, s.tdz));
+            // Skip the run-up to the occupied box: every cell entered before the ray reaches
+            // the box grown by one block lies outside the occupied box.
+            if (t_grown > lo + 4.0 * td_min) { dda_jump(s, t_grown); dbg_steps += 1u << 16; }
+            const double sb_side = side * (1 << kCoarseShift);
+            int declined_cc = -1;  // coarse cell whose skip was judged too short to jump
+            // Loop state derived from the cells (recomputed after a jump, stepped otherwise):
+            //  r* = steps left on an axis before the ray leaves the occupied box in its direction
+            //       of travel (no later cell can be allocated: cells move monotonically per axis,
+            //       so first/last are final there); the original loop tests all three per step,
+            //       only the stepped axis can change;
+            //  in-box test r* <= w*; table index and coarse cell kept incrementally.
+            const int wx = bx1 - bx0, wy = by1 - by0, wz = bz1 - bz0;
+            const int kx = s.sx, ky = s.sy * n, kz = s.sz * n * n;  // N^3 < 2^31 (N <= 1024)
+            const double inv_dir[3] = {1.0 / dir[0], 1.0 / dir[1], 1.0 / dir[2]};
+            int rx, ry, rz, cc, key;
+            uint32_t cbit;
+            auto derive = [&]() {
+                rx = s.sx > 0 ? bx1 - s.cx : s.cx - bx0;
+                ry = s.sy > 0 ? by1 - s.cy : s.cy - by0;
+                rz = s.sz > 0 ? bz1 - s.cz : s.cz - bz0;
+                key = (s.cz * n + s.cy) * n + s.cx;
+                cc = ((s.cz >> kCoarseShift) * P.Nc + (s.cy >> kCoarseShift)) * P.Nc + (s.cx >> kCoarseShift);
+                cbit = (s_coarse[cc >> 5] >> (cc & 31)) & 1u;
+            };
+            // an axis that does not move must lie inside the box, else no cell ever is
+            // (sx == 0: r = c - b0 must be in [0, w])
+            auto outside = [&]() {
+                return rx < 0 || ry < 0 || rz < 0 || (s.sx == 0 && rx > wx) || (s.sy == 0 && ry > wy) ||
+                       (s.sz == 0 && rz > wz);
+            };
+            bool live = s.cx >= 0 && s.cx < n && s.cy >= 0 && s.cy < n && s.cz >= 0 && s.cz < n;
+            if (live) {
+                derive();
+                live = !outside();
+            }
+            uint32_t pend_word = 0, pend_bit = 0;  // occupancy probe of the previous step
+        double pend_tin = 0.0, pend_tout = 0.0;
+        while (live && s.t_in <= hi) {
+                ++dbg_steps;
+                const int axis = s.tmx <= s.tmy ? (s.tmx <= s.tmz ? 0 : 2) : (s.tmy <= s.tmz ? 1 : 2);
+                const double tm = axis == 0 ? s.tmx : (axis == 1 ? s.tmy : s.tmz);
+                if (!cbit && cc != declined_cc) {
+                    // Super-block never held a block: jump to a quarter cell before the ray
+                    // leaves it (the cells visited up to then are inside it, hence empty).
+                    const int sbx = s.cx >> kCoarseShift, sby = s.cy >> kCoarseShift, sbz = s.cz >> kCoarseShift;
+                    const double ox_ = box_lo[0] + sbx * sb_side, oy_ = box_lo[1] + sby * sb_side,
+                                 oz_ = box_lo[2] + sbz * sb_side;
+                    // exit time through the reciprocal: the quarter-cell margin of T below
+                    // absorbs its rounding (a few ulps of t)
+                    double t_exit = INFINITY;
+                    if (s.sx != 0) t_exit = dmin(t_exit, ((s.sx > 0 ? ox_ + sb_side : ox_) - org[0]) * inv_dir[0]);
+                    if (s.sy != 0) t_exit = dmin(t_exit, ((s.sy > 0 ? oy_ + sb_side : oy_) - org[1]) * inv_dir[1]);
+                    if (s.sz != 0) t_exit = dmin(t_exit, ((s.sz > 0 ? oz_ + sb_side : oz_) - org[2]) * inv_dir[2]);
+                    const double T = dmin(t_exit, hi) - 0.25 * td_min;
+                    // a jump costs a few hundred instructions: worth it past ~16 plain steps
+                    if (T > tm + jump_cells * td_min && (dbg_steps += 1u << 16, dda_jump(s, T))) {
+                        if (s.cx < 0 || s.cx >= n || s.cy < 0 || s.cy >= n || s.cz < 0 || s.cz >= n) break;
+                        derive();
+                        if (outside()) break;
+                        continue;
+                    }
+                    declined_cc = cc;  // short crossing: plain steps through it (no occupancy reads)
+                }
+                // Occupancy of the cell (only inside a super-block that ever held a block;
+                // cbit set implies cc != declined_cc). The word is consumed one step later,
+                // so its load overlaps the next DDA step instead of stalling this one.
+                {
+                    const bool probe = cbit && rx <= wx && ry <= wy && rz <= wz;
+                    const uint32_t word = probe ? __ldg(&occ[static_cast<uint32_t>(key) >> 5]) : 0u;
+                    if ((pend_word >> pend_bit) & 1u) {  // t_in and t_out never decrease along the ray
+                        if (first == INFINITY) first = pend_tin;
+                        last = pend_tout;
+                    }
+                    pend_word = word;
+                    pend_bit = static_cast<uint32_t>(key) & 31u;
+                    pend_tin = s.t_in;
+                    pend_tout = dmin(tm, hi);
+                }
+                s.t_in = tm;
+                // step the axis with the smallest tm (branch-free: the lanes of a warp step
+                // different axes)
+                const bool a0 = axis == 0, a1 = axis == 1, a2 = axis == 2;
+                const int cxo = s.cx, cyo = s.cy, czo = s.cz;
+                s.cx += a0 ? s.sx : 0;
+                s.cy += a1 ? s.sy : 0;
+                s.cz += a2 ? s.sz : 0;
+                rx -= a0 ? 1 : 0;
+                ry -= a1 ? 1 : 0;
+                rz -= a2 ? 1 : 0;
+                if ((rx | ry | rz) < 0) break;
+                const double tn = tm + (a0 ? s.tdx : (a1 ? s.tdy : s.tdz));
+                s.tmx = a0 ? tn : s.tmx;
+                s.tmy = a1 ? tn : s.tmy;
+                s.tmz = a2 ? tn : s.tmz;
+                key += a0 ? kx : (a1 ? ky : kz);
+                if (((cxo ^ s.cx) | (cyo ^ s.cy) | (czo ^ s.cz)) >> kCoarseShift) {  // crossed into another super-block
+                    cc = ((s.cz >> kCoarseShift) * P.Nc + (s.cy >> kCoarseShift)) * P.Nc + (s.cx >> kCoarseShift);
+                    cbit = (s_coarse[cc >> 5] >> (cc & 31)) & 1u;
+                }
+            }
+            if ((pend_word >> pend_bit) & 1u) {
+                if (first == INFINITY) first = pend_tin;
+                last = pend_tout;
+            }
+            if (first <= last) {
+                ts = (float)dmax(first, lo);
+                te = (float)dmin(last, hi);
+            }
+        }
+    }
+    t_start[idx] = ts;
+    t_end[idx] = te;
+    if (dbg) {
+        dbg[3 * idx] = dbg_t0;
+        dbg[3 * idx + 1] = globaltimer_ns();
+        dbg[3 * idx + 2] = dbg_steps | ((unsigned long long)(blockIdx.x) << 32);
+    }
+    return ts <= te;
+}
+
+__device__ __forceinline__ void write_empty(float* __restrict__ depth_out, float* __restrict__ normals_out, size_t idx) {
+    depth_out[idx] = 0.0f;
+    normals_out[3 * idx] = 0.0f;
+    normals_out[3 * idx + 1] = 0.0f;
+    normals_out[3 * idx + 2] = 0.0f;
+}
+
+// Coarse occupancy (1 bit per 16^3 blocks) staged in shared memory: the DDA only reads the
+// fine bitmap (L2) inside super-blocks that ever held a block. Exact: a clear coarse bit
+// implies every block of the super-block is EMPTY.
+__device__ __forceinline__ void stage_coarse(const VolParams& P, const uint32_t* __restrict__ occ, uint32_t* s_coarse) {
+    const uint64_t nc = P.Nc;
+    const int cwords = static_cast<int>((nc * nc * nc + 31) / 32);
+    for (int i = threadIdx.x; i < cwords; i += blockDim.x) s_coarse[i] = __ldg(&occ[P.occ_fine_words + i]);
+}
+
 __global__ void __launch_bounds__(256, 2) k_ray_bounds(VolParams P, const FrameConsts* __restrict__ fc, const uint32_t* __restrict__ occ,
                              const VolCounters* __restrict__ vc, float* __restrict__ t_start,
                              float* __restrict__ t_end, int w, int h, const int* dead, int* __restrict__ ray_list,
                              RayCounters* list_ctr, float* __restrict__ depth_out, float* __restrict__ normals_out,
-                             double jump_cells, uint32_t* __restrict__ sched, unsigned long long* __restrict__ dbg) {
-    // Coarse occupancy (1 bit per 16^3 blocks) staged in shared memory: the DDA only reads
-    // the fine bitmap (L2) inside super-blocks that ever held a block. Exact: a clear coarse
-    // bit implies every block of the super-block is EMPTY.
+                             double jump_cells, uint32_t* __restrict__ sched, const uint32_t* __restrict__ order,
+                             unsigned long long* __restrict__ dbg) {
     extern __shared__ uint32_t s_coarse[];
     if (dead && *dead) return;
-    {
-        const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-        const uint64_t nc = P.Nc;
-        const int cwords = static_cast<int>((nc * nc * nc + 31) / 32);
-        for (int i = tid; i < cwords; i += blockDim.x * blockDim.y) s_coarse[i] = __ldg(&occ[P.occ_fine_words + i]);
-        __syncthreads();
-    }
+    stage_coarse(P, occ, s_coarse);
+    __syncthreads();
     // Persistent CTAs; each warp takes 8x4-pixel patches from a counter (neighbouring rays have
     // similar DDA lengths, so fewer lanes idle in the step loop; dynamic patches balance the
-    // SMs: ray cost varies by orders of magnitude across the image).
-    const int tl = threadIdx.y * blockDim.x + threadIdx.x;
-    const int ln = tl & 31;
+    // SMs: ray cost varies by orders of magnitude across the image). Patches are handed out
+    // centre first (`order`): the long rays usually sit in the middle of the image.
+    const int ln = threadIdx.x & 31;
     const int pw = (w + 7) >> 3, n_patches = pw * ((h + 3) >> 2);
     for (;;) {
         int patch = 0;
         if (ln == 0) patch = static_cast<int>(atomicAdd(&sched[0], 1u));
         patch = __shfl_sync(0xffffffffu, patch, 0);
         if (patch >= n_patches) break;
+        patch = static_cast<int>(__ldg(&order[patch]));
         const int u = (patch % pw) * 8 + (ln & 7);
         const int v = (patch / pw) * 4 + (ln >> 3);
         if (u >= w || v >= h) continue;
-        const size_t idx = (size_t)v * w + u;
-        float ts = INFINITY, te = -INFINITY;
-        unsigned long long dbg_t0 = dbg ? globaltimer_ns() : 0ull;
-        unsigned dbg_steps = 0;
-        if (vc->allocated_count != 0) {
-            const Intr& intr = fc->intr;
-            const Pose& pose = fc->pose;
-            const int n = P.N;
-            const double side = P.block_side;
-            const double box_lo[3] = {P.ox, P.oy, P.oz};
-            const double box_hi[3] = {P.ox + P.box_side, P.oy + P.box_side, P.oz + P.box_side};
-            const double org[3] = {pose.t.x, pose.t.y, pose.t.z};
-            const d3 dir_cam = normalized(unproject(intr, u, v, 1.0));
-            const d3 dv3 = mv(pose.R, dir_cam);
-            const double dir[3] = {dv3.x, dv3.y, dv3.z};
-            double lo = intr.near_plane / dir_cam.z;
-            double hi = intr.far_plane / dir_cam.z;
-            for (int a = 0; a < 3; ++a) {
-                if (fabs(dir[a]) < 1e-15) {
-                    if (org[a] < box_lo[a] || org[a] > box_hi[a]) {
-                        lo = 1.0;
-                        hi = 0.0;
-                        break;
-                    }
-                    continue;
-                }
-                double t0 = (box_lo[a] - org[a]) / dir[a];
-                double t1 = (box_hi[a] - org[a]) / dir[a];
-                if (t0 > t1) {
-                    const double tmp = t0;
-                    t0 = t1;
-                    t1 = tmp;
-                }
-                lo = dmax(lo, t0);
-                hi = dmin(hi, t1);
-            }
-            // Conservative reject: a ray missing the occupied bounding box (grown by one block)
-            // meets no allocated block, so its DDA would find nothing.
-            const int* bb = occ_bbox(P, occ);
-            const int bx0 = bb[0], by0 = bb[1], bz0 = bb[2], bx1 = bb[3], by1 = bb[4], bz1 = bb[5];
-            double t_grown = -INFINITY;  // entry time into the occupied box grown by one block
-            if (lo <= hi && bx0 <= bx1) {
-                double rlo = lo, rhi = hi;
-                const int bl[3] = {bx0, by0, bz0}, bh[3] = {bx1, by1, bz1};
-    #pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    const double wlo = box_lo[a] + (double)(bl[a] - 1) * side;
-                    const double whi = box_lo[a] + (double)(bh[a] + 2) * side;
-                    if (fabs(dir[a]) < 1e-300) {
-                        if (org[a] < wlo || org[a] > whi) rhi = -INFINITY;
-                        continue;
-                    }
-                    double t0 = (wlo - org[a]) / dir[a], t1 = (whi - org[a]) / dir[a];
-                    if (t0 > t1) {
-                        const double tmp = t0;
-                        t0 = t1;
-                        t1 = tmp;
-                    }
-                    rlo = dmax(rlo, t0);
-                    rhi = dmin(rhi, t1);
-                }
-                if (!(rlo <= rhi)) lo = 1.0, hi = 0.0;
-                t_grown = rlo;
-            }
-            if (lo <= hi && bx0 <= bx1) {
-                // Scalar (register-resident) Amanatides-Woo state; same operations as render.cpp:103-144.
-                const double ex = org[0] + lo * dir[0], ey = org[1] + lo * dir[1], ez = org[2] + lo * dir[2];
-                auto clampc = [n](int c) { return c < 0 ? 0 : (n - 1 < c ? n - 1 : c); };  // std::clamp(c, 0, n-1)
-                int cx = clampc(ref_floor_int((ex - box_lo[0]) / side));
-                int cy = clampc(ref_floor_int((ey - box_lo[1]) / side));
-                int cz = clampc(ref_floor_int((ez - box_lo[2]) / side));
-                auto init_axis = [&](double d, double blo, int c, double e, int& st, double& tm, double& td) {
-                    if (d > 1e-15) {
-                        st = 1;
-                        tm = lo + (blo + (double)(c + 1) * side - e) / d;
-                        td = side / d;
-                    } else if (d < -1e-15) {
-                        st = -1;
-                        tm = lo + (blo + (double)c * side - e) / d;
-                        td = -side / d;
-                    } else {
-                        st = 0;
-                        tm = INFINITY;
-                        td = INFINITY;
-                    }
-                };
-                Dda s;
-                s.cx = cx;
-                s.cy = cy;
-                s.cz = cz;
-                init_axis(dir[0], box_lo[0], cx, ex, s.sx, s.tmx, s.tdx);
-                init_axis(dir[1], box_lo[1], cy, ey, s.sy, s.tmy, s.tdy);
-                init_axis(dir[2], box_lo[2], cz, ez, s.sz, s.tmz, s.tdz);
-                s.t_in = lo;
-                double first = INFINITY, last = -INFINITY;
-                const double td_min = dmin(s.tdx, dmin(s.tdy, s.tdz));
-                // Skip the run-up to the occupied box: every cell entered before the ray reaches
-                // the box grown by one block lies outside the occupied box.
-                if (t_grown > lo + 4.0 * td_min) { dda_jump(s, t_grown); dbg_steps += 1u << 16; }
-                const double sb_side = side * (1 << kCoarseShift);
-                int declined_cc = -1;  // coarse cell whose skip was judged too short to jump
-                // Loop state derived from the cells (recomputed after a jump, stepped otherwise):
-                //  r* = steps left on an axis before the ray leaves the occupied box in its direction
-                //       of travel (no later cell can be allocated: cells move monotonically per axis,
-                //       so first/last are final there); the original loop tests all three per step,
-                //       only the stepped axis can change;
-                //  in-box test r* <= w*; table index and coarse cell kept incrementally.
-                const int wx = bx1 - bx0, wy = by1 - by0, wz = bz1 - bz0;
-                const int kx = s.sx, ky = s.sy * n, kz = s.sz * n * n;  // N^3 < 2^31 (N <= 1024)
-                const double inv_dir[3] = {1.0 / dir[0], 1.0 / dir[1], 1.0 / dir[2]};
-                int rx, ry, rz, cc, key;
-                uint32_t cbit;
-                auto derive = [&]() {
-                    rx = s.sx > 0 ? bx1 - s.cx : s.cx - bx0;
-                    ry = s.sy > 0 ? by1 - s.cy : s.cy - by0;
-                    rz = s.sz > 0 ? bz1 - s.cz : s.cz - bz0;
-                    key = (s.cz * n + s.cy) * n + s.cx;
-                    cc = ((s.cz >> kCoarseShift) * P.Nc + (s.cy >> kCoarseShift)) * P.Nc + (s.cx >> kCoarseShift);
-                    cbit = (s_coarse[cc >> 5] >> (cc & 31)) & 1u;
-                };
-                // an axis that does not move must lie inside the box, else no cell ever is
-                // (sx == 0: r = c - b0 must be in [0, w])
-                auto outside = [&]() {
-                    return rx < 0 || ry < 0 || rz < 0 || (s.sx == 0 && rx > wx) || (s.sy == 0 && ry > wy) ||
-                           (s.sz == 0 && rz > wz);
-                };
-                bool live = s.cx >= 0 && s.cx < n && s.cy >= 0 && s.cy < n && s.cz >= 0 && s.cz < n;
-                if (live) {
-                    derive();
-                    live = !outside();
-                }
-                uint32_t pend_word = 0, pend_bit = 0;  // occupancy probe of the previous step
-            double pend_tin = 0.0, pend_tout = 0.0;
-            while (live && s.t_in <= hi) {
-                    ++dbg_steps;
-                    const int axis = s.tmx <= s.tmy ? (s.tmx <= s.tmz ? 0 : 2) : (s.tmy <= s.tmz ? 1 : 2);
-                    const double tm = axis == 0 ? s.tmx : (axis == 1 ? s.tmy : s.tmz);
-                    if (!cbit && cc != declined_cc) {
-                        // Super-block never held a block: jump to a quarter cell before the ray
-                        // leaves it (the cells visited up to then are inside it, hence empty).
-                        const int sbx = s.cx >> kCoarseShift, sby = s.cy >> kCoarseShift, sbz = s.cz >> kCoarseShift;
-                        const double ox_ = box_lo[0] + sbx * sb_side, oy_ = box_lo[1] + sby * sb_side,
-                                     oz_ = box_lo[2] + sbz * sb_side;
-                        // exit time through the reciprocal: the quarter-cell margin of T below
-                        // absorbs its rounding (a few ulps of t)
-                        double t_exit = INFINITY;
-                        if (s.sx != 0) t_exit = dmin(t_exit, ((s.sx > 0 ? ox_ + sb_side : ox_) - org[0]) * inv_dir[0]);
-                        if (s.sy != 0) t_exit = dmin(t_exit, ((s.sy > 0 ? oy_ + sb_side : oy_) - org[1]) * inv_dir[1]);
-                        if (s.sz != 0) t_exit = dmin(t_exit, ((s.sz > 0 ? oz_ + sb_side : oz_) - org[2]) * inv_dir[2]);
-                        const double T = dmin(t_exit, hi) - 0.25 * td_min;
-                        // a jump costs a few hundred instructions: worth it past ~16 plain steps
-                        if (T > tm + jump_cells * td_min && (dbg_steps += 1u << 16, dda_jump(s, T))) {
-                            if (s.cx < 0 || s.cx >= n || s.cy < 0 || s.cy >= n || s.cz < 0 || s.cz >= n) break;
-                            derive();
-                            if (outside()) break;
-                            continue;
-                        }
-                        declined_cc = cc;  // short crossing: plain steps through it (no occupancy reads)
-                    }
-                    // Occupancy of the cell (only inside a super-block that ever held a block;
-                    // cbit set implies cc != declined_cc). The word is consumed one step later,
-                    // so its load overlaps the next DDA step instead of stalling this one.
-                    {
-                        const bool probe = cbit && rx <= wx && ry <= wy && rz <= wz;
-                        const uint32_t word = probe ? __ldg(&occ[static_cast<uint32_t>(key) >> 5]) : 0u;
-                        if ((pend_word >> pend_bit) & 1u) {  // t_in and t_out never decrease along the ray
-                            if (first == INFINITY) first = pend_tin;
-                            last = pend_tout;
-                        }
-                        pend_word = word;
-                        pend_bit = static_cast<uint32_t>(key) & 31u;
-                        pend_tin = s.t_in;
-                        pend_tout = dmin(tm, hi);
-                    }
-                    s.t_in = tm;
-                    // step the axis with the smallest tm (branch-free: the lanes of a warp step
-                    // different axes)
-                    const bool a0 = axis == 0, a1 = axis == 1, a2 = axis == 2;
-                    const int cxo = s.cx, cyo = s.cy, czo = s.cz;
-                    s.cx += a0 ? s.sx : 0;
-                    s.cy += a1 ? s.sy : 0;
-                    s.cz += a2 ? s.sz : 0;
-                    rx -= a0 ? 1 : 0;
-                    ry -= a1 ? 1 : 0;
-                    rz -= a2 ? 1 : 0;
-                    if ((rx | ry | rz) < 0) break;
-                    const double tn = tm + (a0 ? s.tdx : (a1 ? s.tdy : s.tdz));
-                    s.tmx = a0 ? tn : s.tmx;
-                    s.tmy = a1 ? tn : s.tmy;
-                    s.tmz = a2 ? tn : s.tmz;
-                    key += a0 ? kx : (a1 ? ky : kz);
-                    if (((cxo ^ s.cx) | (cyo ^ s.cy) | (czo ^ s.cz)) >> kCoarseShift) {  // crossed into another super-block
-                        cc = ((s.cz >> kCoarseShift) * P.Nc + (s.cy >> kCoarseShift)) * P.Nc + (s.cx >> kCoarseShift);
-                        cbit = (s_coarse[cc >> 5] >> (cc & 31)) & 1u;
-                    }
-                }
-                if ((pend_word >> pend_bit) & 1u) {
-                    if (first == INFINITY) first = pend_tin;
-                    last = pend_tout;
-                }
-                if (first <= last) {
-                    ts = (float)dmax(first, lo);
-                    te = (float)dmin(last, hi);
-                }
-            }
-        }
-        t_start[idx] = ts;
-        t_end[idx] = te;
-        if (dbg) {
-            dbg[3 * idx] = dbg_t0;
-            dbg[3 * idx + 1] = globaltimer_ns();
-            dbg[3 * idx + 2] = dbg_steps | ((unsigned long long)(blockIdx.x) << 32);
-        }
+        const bool act = bounds_pixel(P, fc, occ, vc, s_coarse, t_start, t_end, w, jump_cells, dbg, u, v);
         if (ray_list) {
             // Active-ray list for the march (warp-aggregated append); inactive pixels get the
             // empty raycast result here.
-            const bool act = ts <= te;
-            if (!act) {
-                depth_out[idx] = 0.0f;
-                normals_out[3 * idx] = 0.0f;
-                normals_out[3 * idx + 1] = 0.0f;
-                normals_out[3 * idx + 2] = 0.0f;
-            }
+            const int idx = v * w + u;
+            if (!act) write_empty(depth_out, normals_out, idx);
             const unsigned am = __activemask();
             const unsigned bal = __ballot_sync(am, act);
-            const int lane = (threadIdx.y * blockDim.x + threadIdx.x) & 31;
             unsigned long long base = 0;
             if (bal) {
                 const int leader = __ffs(bal) - 1;
-                if (lane == leader) base = atomicAdd(&list_ctr->listed, static_cast<unsigned long long>(__popc(bal)));
+                if (ln == leader) base = atomicAdd(&list_ctr->listed, static_cast<unsigned long long>(__popc(bal)));
                 base = __shfl_sync(am, base, leader);
             }
-            if (act) ray_list[base + __popc(bal & ((1u << lane) - 1u))] = static_cast<int>(idx);
+            if (act) ray_list[base + __popc(bal & ((1u << ln) - 1u))] = idx;
         }
     }
     // last CTA out resets the counters for the next launch
     __syncthreads();
-    if (tl == 0 && atomicAdd(&sched[1], 1u) == gridDim.x - 1) {
+    if (threadIdx.x == 0 && atomicAdd(&sched[1], 1u) == gridDim.x - 1) {
         sched[0] = 0;
         sched[1] = 0;
     }
@@ -407,6 +422,106 @@ __global__ void __launch_bounds__(256, 2) k_ray_bounds(VolParams P, const FrameC
 // (sampling is pure), so results and the stage-1 step count equal the reference's.
 // Stage 2 runs redundantly in all G lanes (same addresses: broadcast loads); the six
 // gradient samples run one per lane.
+// Stage 1 of the raycast for pixel idx (render.cpp:160-208) by a group of G lanes: returns
+// true with the bracket of the first + -> - crossing in group lane 0, else writes the empty
+// result.
+template <int G>
+__device__ __forceinline__ bool march_ray(const VolParams& P, const FrameConsts* __restrict__ fc,
+                                          const int32_t* __restrict__ table, const uint16_t* __restrict__ payload,
+                                          const uint32_t* __restrict__ occ, const double* s_tdec,
+                                          const float* __restrict__ t_start, const float* __restrict__ t_end,
+                                          float* __restrict__ depth_out, float* __restrict__ normals_out,
+                                          int w, int idx, RayBracket& out, unsigned long long& steps,
+                                          unsigned long long& with_bounds) {
+    const int lane = threadIdx.x & 31;
+    const int g = lane & (G - 1);
+    const int gbase = lane & ~(G - 1);
+    const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << gbase;
+    auto group_bits = [&](bool pred) { return (__ballot_sync(gmask, pred) & gmask) >> gbase; };
+    const int u = idx % w, v = idx / w;
+    float out_d = 0.0f, nx = 0.f, ny = 0.f, nz = 0.f;
+    bool bracket_out = false;
+    RayBracket br{};
+    const float fs = t_start[idx], fe = t_end[idx];
+    if (fs <= fe) {  // !bounds.empty(u, v)
+        with_bounds += 1;
+        const Sampler S{P, table, payload, occ, s_tdec};
+        const Intr& intr = fc->intr;
+        const Pose& pose = fc->pose;
+        const double coarse_step = 0.5 * P.delta;
+        const d3 dir_cam = normalized(unproject(intr, u, v, 1.0));
+        const d3 dir = mv(pose.R, dir_cam);
+        const double t1 = fe;
+        bool carry = false, bracketed = false;
+        double carry_t = 0.0, carry_val = 0.0;
+        double hit_a = 0.0, hit_b = 0.0, val_a = 0.0, val_b = 0.0;
+        double t_base = fs;
+        for (;;) {
+            double t = t_base;
+            bool has = true, fin = false;
+            for (int k = 0; k < g; ++k) {
+                if (t >= t1) {
+                    has = false;
+                    break;
+                }
+                t += coarse_step;
+            }
+            if (has && t >= t1) {
+                fin = true;
+                t = t1;
+            }
+            double val = 0.0;
+            const bool valid = has && S.sample(add(pose.t, scale(t, dir)), val);
+            const unsigned vm = group_bits(valid), fm = group_bits(fin), hm = group_bits(has);
+            const unsigned below = vm & ((1u << g) - 1u);
+            const int pl = below ? 31 - __clz(below) : 0;
+            double pv = __shfl_sync(gmask, val, pl, G), pt = __shfl_sync(gmask, t, pl, G);
+            bool hp = below != 0;
+            if (!hp) {
+                hp = carry;
+                pv = carry_val;
+                pt = carry_t;
+            }
+            const unsigned hit = group_bits(valid && hp && pv > 0.0 && val < 0.0);
+            if (hit) {
+                const int hl = __ffs(hit) - 1;
+                hit_a = __shfl_sync(gmask, pt, hl, G);
+                val_a = __shfl_sync(gmask, pv, hl, G);
+                hit_b = __shfl_sync(gmask, t, hl, G);
+                val_b = __shfl_sync(gmask, val, hl, G);
+                steps += hl + 1;
+                bracketed = true;
+                break;
+            }
+            steps += __popc(hm);
+            if (fm || hm != (G == 32 ? 0xffffffffu : (1u << G) - 1u)) break;
+            if (vm) {
+                const int ll = 31 - __clz(vm);
+                carry = true;
+                carry_t = __shfl_sync(gmask, t, ll, G);
+                carry_val = __shfl_sync(gmask, val, ll, G);
+            }
+            t_base = __shfl_sync(gmask, t, G - 1, G) + coarse_step;
+        }
+        if (bracketed && g == 0) {
+            bracket_out = true;
+            br = RayBracket{hit_a, hit_b, val_a, val_b, idx, 0};
+        }
+    }
+    // Rays with a bracket go to the refine (stage 2 + normal, returned to the caller in
+    // group lane 0); the others get the empty result here.
+    if (bracket_out) {
+        out = br;
+        return true;
+    } else if (g == 0) {
+        depth_out[idx] = out_d;
+        normals_out[3 * idx] = nx;
+        normals_out[3 * idx + 1] = ny;
+        normals_out[3 * idx + 2] = nz;
+    }
+    return false;
+}
+
 template <int G>
 __global__ void __launch_bounds__(256, 3)
     k_raycast(VolParams P, const FrameConsts* __restrict__ fc, const int32_t* __restrict__ table,
@@ -423,86 +538,15 @@ __global__ void __launch_bounds__(256, 3)
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int g = lane & (G - 1);
-    const int gbase = lane & ~(G - 1);
-    const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << gbase;
     unsigned long long steps = 0, with_bounds = 0;
-    auto group_bits = [&](bool pred) { return (__ballot_sync(gmask, pred) & gmask) >> gbase; };
     const unsigned long long n_rays = stats->listed;
     for (unsigned long long r = (unsigned long long)blockIdx.x * kRaysPerCta + threadIdx.x / G; r < n_rays;
          r += (unsigned long long)gridDim.x * kRaysPerCta) {  // uniform within the group
         const int idx = ray_list[r];
-        const int u = idx % w, v = idx / w;
-        float out_d = 0.0f, nx = 0.f, ny = 0.f, nz = 0.f;
-        bool bracket_out = false;
-        RayBracket br{};
-        const float fs = t_start[idx], fe = t_end[idx];
-        if (fs <= fe) {  // !bounds.empty(u, v)
-            with_bounds += 1;
-            const Sampler S{P, table, payload, occ, s_tdec};
-            const Intr& intr = fc->intr;
-            const Pose& pose = fc->pose;
-            const double coarse_step = 0.5 * P.delta;
-            const d3 dir_cam = normalized(unproject(intr, u, v, 1.0));
-            const d3 dir = mv(pose.R, dir_cam);
-            const double t1 = fe;
-            bool carry = false, bracketed = false;
-            double carry_t = 0.0, carry_val = 0.0;
-            double hit_a = 0.0, hit_b = 0.0, val_a = 0.0, val_b = 0.0;
-            double t_base = fs;
-            for (;;) {
-                double t = t_base;
-                bool has = true, fin = false;
-                for (int k = 0; k < g; ++k) {
-                    if (t >= t1) {
-                        has = false;
-                        break;
-                    }
-                    t += coarse_step;
-                }
-                if (has && t >= t1) {
-                    fin = true;
-                    t = t1;
-                }
-                double val = 0.0;
-                const bool valid = has && S.sample(add(pose.t, scale(t, dir)), val);
-                const unsigned vm = group_bits(valid), fm = group_bits(fin), hm = group_bits(has);
-                const unsigned below = vm & ((1u << g) - 1u);
-                const int pl = below ? 31 - __clz(below) : 0;
-                double pv = __shfl_sync(gmask, val, pl, G), pt = __shfl_sync(gmask, t, pl, G);
-                bool hp = below != 0;
-                if (!hp) {
-                    hp = carry;
-                    pv = carry_val;
-                    pt = carry_t;
-                }
-                const unsigned hit = group_bits(valid && hp && pv > 0.0 && val < 0.0);
-                if (hit) {
-                    const int hl = __ffs(hit) - 1;
-                    hit_a = __shfl_sync(gmask, pt, hl, G);
-                    val_a = __shfl_sync(gmask, pv, hl, G);
-                    hit_b = __shfl_sync(gmask, t, hl, G);
-                    val_b = __shfl_sync(gmask, val, hl, G);
-                    steps += hl + 1;
-                    bracketed = true;
-                    break;
-                }
-                steps += __popc(hm);
-                if (fm || hm != (G == 32 ? 0xffffffffu : (1u << G) - 1u)) break;
-                if (vm) {
-                    const int ll = 31 - __clz(vm);
-                    carry = true;
-                    carry_t = __shfl_sync(gmask, t, ll, G);
-                    carry_val = __shfl_sync(gmask, val, ll, G);
-                }
-                t_base = __shfl_sync(gmask, t, G - 1, G) + coarse_step;
-            }
-            if (bracketed && g == 0) {
-                bracket_out = true;
-                br = RayBracket{hit_a, hit_b, val_a, val_b, idx, 0};
-            }
-        }
-        // Rays with a bracket go to the one-thread-per-ray refine pass (stage 2 + normal);
-        // the others get the empty result here.
+        RayBracket br;
+        const bool bracket_out = march_ray<G>(P, fc, table, payload, occ, s_tdec, t_start, t_end, depth_out,
+                                              normals_out, w, idx, br, steps, with_bounds);
+        // bracketed rays go to the one-thread-per-ray refine pass
         const unsigned am = __activemask();
         const unsigned bal = __ballot_sync(am, bracket_out);
         unsigned long long base = 0;
@@ -511,14 +555,7 @@ __global__ void __launch_bounds__(256, 3)
             if (lane == leader) base = atomicAdd(&stats->brackets, static_cast<unsigned long long>(__popc(bal)));
             base = __shfl_sync(am, base, leader);
         }
-        if (bracket_out) {
-            brackets[base + __popc(bal & ((1u << lane) - 1u))] = br;
-        } else if (g == 0) {
-            depth_out[idx] = out_d;
-            normals_out[3 * idx] = nx;
-            normals_out[3 * idx + 1] = ny;
-            normals_out[3 * idx + 2] = nz;
-        }
+        if (bracket_out) brackets[base + __popc(bal & ((1u << lane) - 1u))] = br;
     }
     if (g != 0) steps = with_bounds = 0;  // per-ray values are replicated in the group
     // RaycastStats: warp reduction, one atomic per warp and counter.
@@ -530,6 +567,69 @@ __global__ void __launch_bounds__(256, 3)
         if (steps) atomicAdd(&stats->sample_steps, steps);
         if (with_bounds) atomicAdd(&stats->rays_with_bounds, with_bounds);
     }
+}
+
+// Stage 2 + gradient normal of one bracketed ray (render.cpp:209-246); returns 1 for a hit.
+__device__ __forceinline__ unsigned refine_ray(const Sampler& S, const VolParams& P, const FrameConsts* __restrict__ fc,
+                                               const RayBracket& b, float* __restrict__ depth_out,
+                                               float* __restrict__ normals_out, int w) {
+    const Intr& intr = fc->intr;
+    const Pose& pose = fc->pose;
+    const double vox = P.voxel;
+    const double fine_tol = 0.01 * vox;
+    unsigned hits = 0;
+    const int idx = b.idx;
+    const int u = idx % w, v = idx / w;
+    const d3 dir_cam = normalized(unproject(intr, u, v, 1.0));
+    const d3 dir = mv(pose.R, dir_cam);
+    double hit_a = b.a, hit_b = b.b, val_a = b.va, val_b = b.vb;
+    float out_d = 0.0f, nx = 0.f, ny = 0.f, nz = 0.f;
+    int64_t ckey = -1;
+    int32_t cslot = kEmpty;
+    for (int iter = 0; iter < 48 && hit_b - hit_a > fine_tol; ++iter) {
+        double t_new = hit_b - val_b * (hit_b - hit_a) / (val_b - val_a);
+        if (!(t_new > hit_a) || !(t_new < hit_b)) t_new = 0.5 * (hit_a + hit_b);
+        double val;
+        if (!S.sample_near(add(pose.t, scale(t_new, dir)), val, ckey, cslot)) {
+            hit_a = t_new;
+            val_a = dmax(val_a, 1e-12);
+            continue;
+        }
+        if (val > 0.0) {
+            hit_a = t_new;
+            val_a = val;
+        } else {
+            hit_b = t_new;
+            val_b = val;
+        }
+    }
+    double root;
+    if (val_b != val_a) {
+        const double interp = hit_b - val_b * (hit_b - hit_a) / (val_b - val_a);
+        root = dclamp(interp, hit_a, hit_b);
+    } else {
+        root = 0.5 * (hit_a + hit_b);
+    }
+    const double dd = root * dir_cam.z;
+    if (!(dd < intr.near_plane || dd > intr.far_plane)) {
+        out_d = (float)dd;
+        hits += 1;
+        // sample_tsdf_gradient (render.cpp:50-63)
+        const d3 p = add(pose.t, scale(root, dir));
+        d3 gr;
+        if (S.gradient_near(p, vox, gr, ckey, cslot) && sqnorm(gr) > 0.0) {
+            // world_to_cam * grad.normalized()  (render.cpp:242-245)
+            const d3 n_cam = mv(mt(pose.R), normalized(gr));
+            nx = (float)n_cam.x;
+            ny = (float)n_cam.y;
+            nz = (float)n_cam.z;
+        }
+    }
+    depth_out[idx] = out_d;
+    normals_out[3 * idx] = nx;
+    normals_out[3 * idx + 1] = ny;
+    normals_out[3 * idx + 2] = nz;
+    return hits;
 }
 
 // Stage 2 (secant / bisection to 0.01 voxel, render.cpp:209-233) and the gradient normal
@@ -546,66 +646,12 @@ __global__ void __launch_bounds__(256)
     for (int i = threadIdx.x; i < 256; i += blockDim.x) s_tdec[i] = aux->tsdf_decode[i];
     __syncthreads();
     const Sampler S{P, table, payload, occ, s_tdec};
-    const Intr& intr = fc->intr;
-    const Pose& pose = fc->pose;
-    const double vox = P.voxel;
-    const double fine_tol = 0.01 * vox;
     const unsigned long long n = stats->brackets;
     unsigned long long hits = 0;
     for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
          i += (unsigned long long)gridDim.x * blockDim.x) {
         const RayBracket b = brackets[i];
-        const int idx = b.idx;
-        const int u = idx % w, v = idx / w;
-        const d3 dir_cam = normalized(unproject(intr, u, v, 1.0));
-        const d3 dir = mv(pose.R, dir_cam);
-        double hit_a = b.a, hit_b = b.b, val_a = b.va, val_b = b.vb;
-        float out_d = 0.0f, nx = 0.f, ny = 0.f, nz = 0.f;
-        int64_t ckey = -1;
-        int32_t cslot = kEmpty;
-        for (int iter = 0; iter < 48 && hit_b - hit_a > fine_tol; ++iter) {
-            double t_new = hit_b - val_b * (hit_b - hit_a) / (val_b - val_a);
-            if (!(t_new > hit_a) || !(t_new < hit_b)) t_new = 0.5 * (hit_a + hit_b);
-            double val;
-            if (!S.sample_near(add(pose.t, scale(t_new, dir)), val, ckey, cslot)) {
-                hit_a = t_new;
-                val_a = dmax(val_a, 1e-12);
-                continue;
-            }
-            if (val > 0.0) {
-                hit_a = t_new;
-                val_a = val;
-            } else {
-                hit_b = t_new;
-                val_b = val;
-            }
-        }
-        double root;
-        if (val_b != val_a) {
-            const double interp = hit_b - val_b * (hit_b - hit_a) / (val_b - val_a);
-            root = dclamp(interp, hit_a, hit_b);
-        } else {
-            root = 0.5 * (hit_a + hit_b);
-        }
-        const double dd = root * dir_cam.z;
-        if (!(dd < intr.near_plane || dd > intr.far_plane)) {
-            out_d = (float)dd;
-            hits += 1;
-            // sample_tsdf_gradient (render.cpp:50-63)
-            const d3 p = add(pose.t, scale(root, dir));
-            d3 gr;
-            if (S.gradient_near(p, vox, gr, ckey, cslot) && sqnorm(gr) > 0.0) {
-                // world_to_cam * grad.normalized()  (render.cpp:242-245)
-                const d3 n_cam = mv(mt(pose.R), normalized(gr));
-                nx = (float)n_cam.x;
-                ny = (float)n_cam.y;
-                nz = (float)n_cam.z;
-            }
-        }
-        depth_out[idx] = out_d;
-        normals_out[3 * idx] = nx;
-        normals_out[3 * idx + 1] = ny;
-        normals_out[3 * idx + 2] = nz;
+        hits += refine_ray(S, P, fc, b, depth_out, normals_out, w);
     }
     for (int off = 16; off > 0; off >>= 1) hits += __shfl_down_sync(0xffffffffu, hits, off);
     if ((threadIdx.x & 31) == 0 && hits) atomicAdd(&stats->hit_pixels, hits);
@@ -640,16 +686,40 @@ static void rb_debug_dump(unsigned long long* buf, size_t n, cudaStream_t s) {
     }
 }
 
+// Patch order of k_ray_bounds: 8x4 patches sorted by the distance of their centre to the
+// image centre (built once per image size, outside graph capture: ensure_frame_buffers).
+void ensure_patch_order(Volume& v, int w, int h) {
+    if (w == v.order_w && h == v.order_h) return;
+    const int pw = (w + 7) >> 3, ph = (h + 3) >> 2;
+    std::vector<uint32_t> idx(static_cast<size_t>(pw) * ph);
+    std::vector<double> dist(idx.size());
+    for (int y = 0; y < ph; ++y)
+        for (int x = 0; x < pw; ++x) {
+            const double dx = (x * 8 + 4) - 0.5 * w, dy = (y * 4 + 2) - 0.5 * h;
+            idx[static_cast<size_t>(y) * pw + x] = static_cast<uint32_t>(y * pw + x);
+            dist[static_cast<size_t>(y) * pw + x] = dx * dx + dy * dy;
+        }
+    std::stable_sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t b) { return dist[a] < dist[b]; });
+    if (v.d_patch_order) SF_CUDA(cudaFree(v.d_patch_order));
+    v.d_patch_order = nullptr;
+    SF_CUDA(cudaMalloc(&v.d_patch_order, idx.size() * sizeof(uint32_t)));
+    SF_CUDA(cudaMemcpy(v.d_patch_order, idx.data(), idx.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    v.order_w = w;
+    v.order_h = h;
+}
+
 void launch_ray_bounds(Volume& v, const FrameConsts* d_fc, const Intr& intr, float* t_start, float* t_end,
                        cudaStream_t s, uint64_t* launches, const int* dead_flag, int* ray_list,
                        RayCounters* list_ctr, float* depth, float* normals) {
     unsigned long long* rb_dbg = rb_debug_buffer((size_t)intr.w * intr.h);
-    const dim3 blk(32, 8), grd(148 * 2);
+    ensure_patch_order(v, intr.w, intr.h);
+    const dim3 blk(256), grd(148 * 2);
     const uint64_t nc = v.P.Nc;
     const size_t smem = ((nc * nc * nc + 31) / 32) * sizeof(uint32_t);
     if (smem > 48 * 1024) SF_CUDA(cudaFuncSetAttribute(k_ray_bounds, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_ray_bounds<<<grd, blk, smem, s>>>(v.P, d_fc, v.d_occ, v.d_vc, t_start, t_end, intr.w, intr.h, dead_flag,
-                                        ray_list, list_ctr, depth, normals, ray_jump_cells(), v.d_sched, rb_dbg);
+                                        ray_list, list_ctr, depth, normals, ray_jump_cells(), v.d_sched,
+                                        v.d_patch_order, rb_dbg);
     SF_LAUNCH_CHECK();
     rb_debug_dump(rb_dbg, (size_t)intr.w * intr.h, s);
     if (launches) *launches += 1;

@@ -12,6 +12,7 @@
 // Ground-truth step (and the first frame): fuse at the given pose.
 // TrackingLost / PoolExhausted set a device "dead" flag: the rest of the frame and every
 // later step become no-ops, mirroring run()'s break (pipeline.cpp:289-299).
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -328,6 +329,7 @@ int sf_tracker_create(sf_volume_t vol, const sf_tracker_config* config, const do
         SF_CUDA(cudaMalloc(&t->d_rstats, sizeof(RayCounters)));
         SF_CUDA(cudaMalloc(&t->d_ray_list, n * sizeof(int)));
         SF_CUDA(cudaMalloc(&t->d_brackets, n * sizeof(RayBracket)));
+
         SF_CUDA(cudaMalloc(&t->d_td, sizeof(TrackerDev)));
         SF_CUDA(cudaMemset(t->d_td, 0, sizeof(TrackerDev)));
         SF_CUDA(cudaMemset(t->d_rstats, 0, sizeof(RayCounters)));

@@ -144,6 +144,7 @@ void FrameBuffers::release() {
 size_t cub_temp_bytes_needed(uint32_t key_cap);  // sf_fusion.cu
 
 void ensure_frame_buffers(Volume& v, FrameBuffers& fb, int w, int h) {
+    ensure_patch_order(v, w, h);  // the tracker captures ray bounds into a graph
     if (fb.w == w && fb.h == h && fb.ctr) return;
     fb.release();
     fb.device = v.device;
@@ -377,7 +378,7 @@ static void volume_free_device(Volume& v) {
     cudaSetDevice(v.device);
     v.fb.release();
     void* ptrs[] = {v.d_table, v.d_payload, v.d_fpayload, v.d_free_list, v.d_slot_key, v.d_occ, v.d_keybits,
-                    v.d_vc,    v.d_aux,      v.d_sched};
+                    v.d_vc,    v.d_aux,      v.d_sched, v.d_patch_order};
     for (void* p : ptrs)
         if (p) cudaFree(p);
 }
