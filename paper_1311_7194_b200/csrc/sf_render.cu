@@ -572,7 +572,8 @@ __global__ void __launch_bounds__(256, 3)
 // Stage 2 + gradient normal of one bracketed ray (render.cpp:209-246); returns 1 for a hit.
 __device__ __forceinline__ unsigned refine_ray(const Sampler& S, const VolParams& P, const FrameConsts* __restrict__ fc,
                                                const RayBracket& b, float* __restrict__ depth_out,
-                                               float* __restrict__ normals_out, int w) {
+                                               float* __restrict__ normals_out, int w, int* iters = nullptr,
+                                               unsigned long long* t_mid = nullptr) {
     const Intr& intr = fc->intr;
     const Pose& pose = fc->pose;
     const double vox = P.voxel;
@@ -586,7 +587,8 @@ __device__ __forceinline__ unsigned refine_ray(const Sampler& S, const VolParams
     float out_d = 0.0f, nx = 0.f, ny = 0.f, nz = 0.f;
     int64_t ckey = -1;
     int32_t cslot = kEmpty;
-    for (int iter = 0; iter < 48 && hit_b - hit_a > fine_tol; ++iter) {
+    int iter = 0;
+    for (; iter < 48 && hit_b - hit_a > fine_tol; ++iter) {
         double t_new = hit_b - val_b * (hit_b - hit_a) / (val_b - val_a);
         if (!(t_new > hit_a) || !(t_new < hit_b)) t_new = 0.5 * (hit_a + hit_b);
         double val;
@@ -603,6 +605,8 @@ __device__ __forceinline__ unsigned refine_ray(const Sampler& S, const VolParams
             val_b = val;
         }
     }
+    if (iters) *iters = iter;
+    if (t_mid) *t_mid = globaltimer_ns();
     double root;
     if (val_b != val_a) {
         const double interp = hit_b - val_b * (hit_b - hit_a) / (val_b - val_a);
@@ -640,7 +644,7 @@ __global__ void __launch_bounds__(256)
                      const uint16_t* __restrict__ payload, const uint32_t* __restrict__ occ,
                      const AuxTables* __restrict__ aux, const RayBracket* __restrict__ brackets,
                      float* __restrict__ depth_out, float* __restrict__ normals_out, RayCounters* stats, int w,
-                     const int* dead) {
+                     const int* dead, unsigned long long* __restrict__ dbg) {
     __shared__ double s_tdec[256];
     if (dead && *dead) return;
     for (int i = threadIdx.x; i < 256; i += blockDim.x) s_tdec[i] = aux->tsdf_decode[i];
@@ -651,7 +655,18 @@ __global__ void __launch_bounds__(256)
     for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
          i += (unsigned long long)gridDim.x * blockDim.x) {
         const RayBracket b = brackets[i];
-        hits += refine_ray(S, P, fc, b, depth_out, normals_out, w);
+        if (dbg) {  // SF_RF_DEBUG: per-ray {start, end of the secant loop, end, iterations | idx}
+            const unsigned long long t0 = globaltimer_ns();
+            int it = 0;
+            unsigned long long tm = 0;
+            hits += refine_ray(S, P, fc, b, depth_out, normals_out, w, &it, &tm);
+            dbg[4 * i] = t0;
+            dbg[4 * i + 1] = tm;
+            dbg[4 * i + 2] = globaltimer_ns();
+            dbg[4 * i + 3] = static_cast<unsigned long long>(it) | (static_cast<unsigned long long>(b.idx) << 32);
+        } else {
+            hits += refine_ray(S, P, fc, b, depth_out, normals_out, w);
+        }
     }
     for (int off = 16; off > 0; off >>= 1) hits += __shfl_down_sync(0xffffffffu, hits, off);
     if ((threadIdx.x & 31) == 0 && hits) atomicAdd(&stats->hit_pixels, hits);
@@ -787,9 +802,24 @@ void launch_raycast(Volume& v, const FrameConsts* d_fc, const Intr& intr, const 
                                      d_stats, intr.w, intr.h, dead_flag, ray_list, brackets);
     SF_LAUNCH_CHECK();
     // one warp per CTA: the ~30 k bracketed rays spread over all SMs (latency-bound, few warps)
+    static unsigned long long* rf_dbg = nullptr;  // SF_RF_DEBUG=<path>: per-ray refine timing (graph-less runs)
+    const char* rf_path = std::getenv("SF_RF_DEBUG");
+    if (rf_path && !rf_dbg) SF_CUDA(cudaMalloc(&rf_dbg, 4ull * intr.w * intr.h * sizeof(unsigned long long)));
     k_raycast_refine<<<148 * 16, 32, 0, s>>>(v.P, d_fc, v.d_table, v.d_payload, v.d_occ, v.d_aux, brackets, depth,
-                                             normals, d_stats, intr.w, dead_flag);
+                                             normals, d_stats, intr.w, dead_flag, rf_path ? rf_dbg : nullptr);
     SF_LAUNCH_CHECK();
+    if (rf_path) {
+        unsigned long long nb = 0;
+        SF_CUDA(cudaMemcpyAsync(&nb, &d_stats->brackets, sizeof(nb), cudaMemcpyDeviceToHost, s));
+        SF_CUDA(cudaStreamSynchronize(s));
+        std::vector<unsigned long long> hb(4 * nb + 1);
+        hb[0] = nb;
+        if (nb) SF_CUDA(cudaMemcpy(hb.data() + 1, rf_dbg, 4 * nb * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        if (FILE* f = std::fopen(rf_path, "ab")) {
+            std::fwrite(hb.data(), sizeof(unsigned long long), hb.size(), f);
+            std::fclose(f);
+        }
+    }
     if (launches) *launches += 2;
 }
 

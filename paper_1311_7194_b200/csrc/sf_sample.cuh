@@ -131,30 +131,37 @@ struct Sampler {
         if (bx < 0 || by < 0 || bz < 0 || bx + 1 >= res || by + 1 >= res || bz + 1 >= res) return false;
         const double fx = gx - flx, fy = gy - fly, fz = gz - flz;
         // One branch-free path for every corner layout (the 1-, 2-, 4- and 8-block cases would
-        // diverge within a warp): per corner its block's slot — the cached one when the block
-        // matches, else a table read — then the payload code. Any EMPTY block or chi corner
-        // gives nullopt (render.cpp:14-15, 39), as in sample().
+        // diverge within a warp). The base corner's block slot comes from the cache or one
+        // table read; a corner whose +1 step crosses into the next block along some axis reads
+        // that block's slot — those reads do not depend on the base one, so every table read
+        // and then every payload read of the sample is in flight at once. Any EMPTY block or
+        // chi corner gives nullopt (render.cpp:14-15, 39), as in sample(). Table indices fit
+        // int32 (N^3 < 2^31, checked at volume creation).
         const int ms = P.mshift, mm = P.M - 1, N = P.N;
-        const int xs[2] = {bx, bx + 1}, ys[2] = {by, by + 1}, zs[2] = {bz, bz + 1};
+        const int lx = bx & mm, ly = by & mm, lz = bz & mm;
+        const bool cx = lx == mm, cy = ly == mm, cz = lz == mm;
+        const int kb = ((bz >> ms) * N + (by >> ms)) * N + (bx >> ms);
+        const int32_t sb = kb == ckey ? cslot : __ldg(&table[kb]);
+        const int NN = N * N;
         bool ok = true;
         double c[8];
+        uint16_t pl[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const int x = xs[i & 1], y = ys[(i >> 1) & 1], z = zs[i >> 2];
-            const int64_t key = ((int64_t)(z >> ms) * N + (y >> ms)) * N + (x >> ms);
-            int32_t sl = cslot;
-            if (key != ckey) sl = __ldg(&table[key]);
+            const bool ox = (i & 1) && cx, oy = ((i >> 1) & 1) && cy, oz = (i >> 2) && cz;
+            const int32_t sl = (ox || oy || oz) ? __ldg(&table[kb + (ox ? 1 : 0) + (oy ? N : 0) + (oz ? NN : 0)]) : sb;
+            const int vx = ox ? 0 : lx + (i & 1), vy = oy ? 0 : ly + ((i >> 1) & 1), vz = oz ? 0 : lz + (i >> 2);
             ok = ok && sl != kEmpty;
-            uint16_t pl = kChiPayload;
-            if (sl != kEmpty)
-                pl = __ldg(&payload[(size_t)sl * P.M3 + ((((z & mm) << ms) + (y & mm)) << ms) + (x & mm)]);
-            const int8_t cc = static_cast<int8_t>(pl & 0xFF);
+            pl[i] = sl != kEmpty ? __ldg(&payload[((size_t)sl << (3 * ms)) + (((vz << ms) + vy) << ms) + vx])
+                                 : static_cast<uint16_t>(kChiPayload);
+        }
+        ckey = kb;  // cache the base corner's block
+        cslot = sb;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int8_t cc = static_cast<int8_t>(pl[i] & 0xFF);
             ok = ok && cc != kChiCode;
             c[i] = tdec[(int)cc + 128];
-            if (i == 0 && key != ckey) {  // cache the base corner's block
-                ckey = key;
-                cslot = sl;
-            }
         }
         if (!ok) return false;
         const double x0 = c[0] + (c[1] - c[0]) * fx;
