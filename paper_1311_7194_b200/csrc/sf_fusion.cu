@@ -243,6 +243,7 @@ __global__ void k_block_keys_set(VolParams P, const FrameConsts* __restrict__ fc
                                  uint32_t* __restrict__ uniq, FrameCounters* ctr, const int32_t* __restrict__ table,
                                  uint32_t* __restrict__ new_keys, uint32_t* __restrict__ new_idx,
                                  int2* __restrict__ work) {
+    pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= su * sv || ctr->skip) return;
     const int u = (i % su) * stride;
@@ -366,6 +367,7 @@ __global__ void __launch_bounds__(256)
                     int32_t* __restrict__ table, const int32_t* __restrict__ free_list, int32_t* __restrict__ slot_key,
                     uint32_t* __restrict__ occ, const uint32_t* __restrict__ uniq, const uint32_t* __restrict__ keybits,
                     const float* __restrict__ depth, int w, int h, int2* __restrict__ work) {
+    pdl_wait();
     __shared__ bool s_last;
     __shared__ uint32_t s_wsum[8];
     if (ctr->skip) return;
@@ -864,6 +866,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
                      const double* __restrict__ pix_var, const double* __restrict__ pix_w,
                      const int32_t* __restrict__ slot_key, uint16_t* __restrict__ payload,
                      const uint32_t* __restrict__ uniq, uint32_t* __restrict__ keybits) {
+    pdl_wait();
     constexpr int M = 1 << MS, M3 = M * M * M, RPB = M * M;
     constexpr int kRing = RowRing<MS>::kEntries;
     using RV = RowVec<MS>;
@@ -1375,7 +1378,7 @@ static void launch_integrate_rows(Volume& v, FrameBuffers& fb, const FuseParams&
                                      (int)RowRing<MS>::kBytes));
         configured = true;
     }
-    k_integrate_rows<MODE, MS><<<148 * kRowCtasPerSm, kRowThreads, RowRing<MS>::kBytes, s>>>(
+    launch_pdl(k_integrate_rows<MODE, MS>, dim3(148 * kRowCtasPerSm), dim3(kRowThreads), RowRing<MS>::kBytes, s, 
         v.P, fb.fc, fp, fb.work, fb.ctr, v.d_aux, fb.pix_f, fb.pix_dm, fb.pix_var, fb.pix_w, v.d_slot_key,
         v.d_payload, fb.keys_unique, v.d_keybits);
 }
@@ -1438,11 +1441,11 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
         n += 3 + 4;  // keys + list_len + visible + (sort, unique: >= 4 CUB kernels)
     } else {
         // fuse_frame: unordered key set + ranked new keys + work list (no global sort)
-        k_block_keys_set<<<(su * sv + kThreads - 1) / kThreads, kThreads, 0, s>>>(
+        launch_pdl(k_block_keys_set, dim3((su * sv + kThreads - 1) / kThreads), dim3(kThreads), 0, s, 
             P, fb.fc, depth, w, h, fb.stride, su, sv, v.d_keybits, fb.keys_unique, fb.ctr, v.d_table, fb.ranks,
             fb.flags, fb.work);
         SF_LAUNCH_CHECK();
-        k_alloc_visible<<<kPersistentCtas, kThreads, 0, s>>>(P, fb.fc, fb.ctr, v.d_vc, fb.ranks, fb.flags, v.d_table,
+        launch_pdl(k_alloc_visible, dim3(kPersistentCtas), dim3(kThreads), 0, s, P, fb.fc, fb.ctr, v.d_vc, fb.ranks, fb.flags, v.d_table,
                                                             v.d_free_list, v.d_slot_key, v.d_occ, fb.keys_unique,
                                                             v.d_keybits, depth, w, h, fb.work);
         SF_LAUNCH_CHECK();

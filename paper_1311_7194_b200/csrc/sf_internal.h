@@ -28,6 +28,28 @@ void set_last_error(const std::string& msg);
     } while (0)
 #define SF_LAUNCH_CHECK() SF_CUDA(cudaGetLastError())
 
+// Programmatic dependent launch (SF_PDL=0 disables): the launch of a kernel is prepared
+// while its stream predecessor runs; the kernel calls pdl_wait() (a no-op for a normal
+// launch) before anything else, which returns once the predecessor has completed and its
+// writes are visible. No kernel triggers early (griddepcontrol.launch_dependents): CTAs of
+// a waiting dependent would take SM slots from the predecessor's tail (measured slower).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    SF_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
 // Timing event usable both eagerly and under stream capture (as an event-record node).
 inline void record_event(cudaEvent_t ev, cudaStream_t s) {
     cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;

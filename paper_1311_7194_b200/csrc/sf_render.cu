@@ -370,6 +370,7 @@ __global__ void __launch_bounds__(256, 2) k_ray_bounds(VolParams P, const FrameC
                              RayCounters* list_ctr, float* __restrict__ depth_out, float* __restrict__ normals_out,
                              double jump_cells, uint32_t* __restrict__ sched, const uint32_t* __restrict__ order,
                              unsigned long long* __restrict__ dbg) {
+    pdl_wait();
     extern __shared__ uint32_t s_coarse[];
     if (dead && *dead) return;
     stage_coarse(P, occ, s_coarse);
@@ -529,6 +530,7 @@ __global__ void __launch_bounds__(256, 3)
               const float* __restrict__ t_start, const float* __restrict__ t_end, float* __restrict__ depth_out,
               float* __restrict__ normals_out, RayCounters* stats, int w, int h, const int* dead,
               const int* __restrict__ ray_list, RayBracket* __restrict__ brackets) {
+    pdl_wait();
     static_assert(G >= 8 && G <= 32 && (G & (G - 1)) == 0, "group of 8..32 lanes");
     (void)h;
     constexpr int kRaysPerCta = 256 / G;
@@ -645,6 +647,7 @@ __global__ void __launch_bounds__(256)
                      const AuxTables* __restrict__ aux, const RayBracket* __restrict__ brackets,
                      float* __restrict__ depth_out, float* __restrict__ normals_out, RayCounters* stats, int w,
                      const int* dead, unsigned long long* __restrict__ dbg) {
+    pdl_wait();
     __shared__ double s_tdec[256];
     if (dead && *dead) return;
     for (int i = threadIdx.x; i < 256; i += blockDim.x) s_tdec[i] = aux->tsdf_decode[i];
@@ -732,7 +735,7 @@ void launch_ray_bounds(Volume& v, const FrameConsts* d_fc, const Intr& intr, flo
     const uint64_t nc = v.P.Nc;
     const size_t smem = ((nc * nc * nc + 31) / 32) * sizeof(uint32_t);
     if (smem > 48 * 1024) SF_CUDA(cudaFuncSetAttribute(k_ray_bounds, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_ray_bounds<<<grd, blk, smem, s>>>(v.P, d_fc, v.d_occ, v.d_vc, t_start, t_end, intr.w, intr.h, dead_flag,
+    launch_pdl(k_ray_bounds, grd, blk, smem, s, v.P, d_fc, v.d_occ, v.d_vc, t_start, t_end, intr.w, intr.h, dead_flag,
                                         ray_list, list_ctr, depth, normals, ray_jump_cells(), v.d_sched,
                                         v.d_patch_order, rb_dbg);
     SF_LAUNCH_CHECK();
@@ -798,14 +801,14 @@ void launch_raycast(Volume& v, const FrameConsts* d_fc, const Intr& intr, const 
                     const int* dead_flag, const int* ray_list, RayBracket* brackets) {
     constexpr int G = 8;  // lanes per ray: 32 rays per 256-thread CTA, persistent over the list
     const dim3 blk(256), grd(148 * 3);
-    k_raycast<G><<<grd, blk, 0, s>>>(v.P, d_fc, v.d_table, v.d_payload, v.d_occ, v.d_aux, t_start, t_end, depth, normals,
+    launch_pdl(k_raycast<G>, grd, blk, 0, s, v.P, d_fc, v.d_table, v.d_payload, v.d_occ, v.d_aux, t_start, t_end, depth, normals,
                                      d_stats, intr.w, intr.h, dead_flag, ray_list, brackets);
     SF_LAUNCH_CHECK();
     // one warp per CTA: the ~30 k bracketed rays spread over all SMs (latency-bound, few warps)
     static unsigned long long* rf_dbg = nullptr;  // SF_RF_DEBUG=<path>: per-ray refine timing (graph-less runs)
     const char* rf_path = std::getenv("SF_RF_DEBUG");
     if (rf_path && !rf_dbg) SF_CUDA(cudaMalloc(&rf_dbg, 4ull * intr.w * intr.h * sizeof(unsigned long long)));
-    k_raycast_refine<<<148 * 16, 32, 0, s>>>(v.P, d_fc, v.d_table, v.d_payload, v.d_occ, v.d_aux, brackets, depth,
+    launch_pdl(k_raycast_refine, dim3(148 * 16), dim3(32), 0, s, v.P, d_fc, v.d_table, v.d_payload, v.d_occ, v.d_aux, brackets, depth,
                                              normals, d_stats, intr.w, dead_flag, rf_path ? rf_dbg : nullptr);
     SF_LAUNCH_CHECK();
     if (rf_path) {

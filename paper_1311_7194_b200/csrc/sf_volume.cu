@@ -9,6 +9,7 @@
 //   d_occ        uint32[N^3/32]    occupancy bitmap for the ray-bounds DDA (L2 resident), followed
 //                                  by a coarse 1-bit-per-16^3-blocks bitmap (shared-memory resident)
 //   d_fpayload   float2[cap*M^3]   optional float payload (FloatShadowGrid semantics)
+#include <cstdlib>
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -142,6 +143,14 @@ void FrameBuffers::release() {
 }
 
 size_t cub_temp_bytes_needed(uint32_t key_cap);  // sf_fusion.cu
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SF_PDL");
+        return !e || std::atoi(e) != 0;
+    }();
+    return on;
+}
 
 void ensure_frame_buffers(Volume& v, FrameBuffers& fb, int w, int h) {
     ensure_patch_order(v, w, h);  // the tracker captures ray bounds into a graph
