@@ -446,6 +446,8 @@ def run_ours(args, world, rank, local):
         "blocks_processed_mean": sum(blocks) / steps,
         "integrate_exact_fallback_frac": sum(mm.exact_voxels for mm in metrics) / max(1, sum(blocks) * m3),
         "icp_iterations_mean": sum(mm.iterations for mm in metrics) / steps,
+        "icp_steps_mean": sum(mm.icp_steps for mm in metrics) / steps,
+        "icp_device_ms_mean": sum(mm.icp_ns for mm in metrics) / steps * 1e-6,
         "tracking_error_last_frame": pose_err,
         "roofline": {"bound": "hbm", "kernel": "k_integrate_rows<Kalman>", "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,

@@ -325,6 +325,9 @@ typedef struct {
     uint64_t kernel_launches;  /* device kernels this frame ran (graph: top level + 2 per ICP iteration) */
     uint64_t exact_voxels;     /* voxels the integrate kernel settled on its FP64 fallback (uncertain FP32 decision) */
     uint64_t integrate_ns;     /* integrate kernel span on the device clock: first CTA start to last CTA end (%globaltimer) */
+    uint64_t icp_ns;           /* ICP span on the device clock: first step start to the end of the last iteration's solve */
+    int32_t icp_steps;         /* ICP step launches this frame (device-side loop: one per iteration) */
+    int32_t pad_;
 } sf_frame_metrics;
 
 int sf_tracker_create(sf_volume_t vol, const sf_tracker_config* config, const double initial_pose[12],

@@ -158,6 +158,9 @@ class FrameMetricsC(C.Structure):
         ("kernel_launches", C.c_uint64),
         ("exact_voxels", C.c_uint64),
         ("integrate_ns", C.c_uint64),
+        ("icp_ns", C.c_uint64),
+        ("icp_steps", C.c_int32),
+        ("pad_", C.c_int32),
     ]
 
 

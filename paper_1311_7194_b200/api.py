@@ -716,6 +716,8 @@ class FrameMetrics:
     kernel_launches: int = 0  # this library's kernels the frame ran (incl. device-side ICP loop)
     exact_voxels: int = 0  # integrate voxels settled on the FP64 fallback (uncertain FP32 decision)
     integrate_ns: int = 0  # integrate kernel span on the device clock (first CTA start .. last CTA end)
+    icp_ns: int = 0  # ICP span on the device clock (first step start .. end of the last solve)
+    icp_steps: int = 0  # ICP step launches (device-side loop: one per iteration)
 
 
 class Tracker:
@@ -766,7 +768,7 @@ class Tracker:
                             FusionStats(f.voxels_updated, f.blocks_allocated_now, f.blocks_total, f.memory_bytes),
                             RaycastStats(r.sample_steps, r.hit_pixels, r.rays_with_bounds),
                             m.blocks_processed, m.voxels_visited, m.kernel_launches, m.exact_voxels,
-                            m.integrate_ns)
+                            m.integrate_ns, m.icp_ns, m.icp_steps)
 
     def fetch(self, stream=None) -> FrameMetrics:
         m = A.FrameMetricsC()

@@ -35,12 +35,8 @@ namespace sf {
 template <bool COND>
 __global__ void k_icp_init(IcpState* st, const double* __restrict__ initial12, const int* dead, int max_iterations,
                            cudaGraphConditionalHandle cond) {
-    IcpState z;
-    memset(&z, 0, sizeof(z));
-    z.delta = pose_from12(initial12);
-    z.done = (dead && *dead) ? 1 : 0;
-    *st = z;
-    if constexpr (COND) cudaGraphSetConditional(cond, (!z.done && max_iterations > 0) ? 1u : 0u);
+    icp_state_init(st, initial12, dead && *dead);
+    if constexpr (COND) cudaGraphSetConditional(cond, (!st->done && max_iterations > 0) ? 1u : 0u);
 }
 
 // Returns true in every thread of the CTA that finished last (all partials visible).
@@ -253,6 +249,7 @@ __global__ void __launch_bounds__(kIcpThreads, 1)
                double* __restrict__ part_bbox, unsigned long long* __restrict__ part_count, DD* __restrict__ part,
                unsigned int* counter, cudaGraphConditionalHandle cond) {
     extern __shared__ DD s_red[];  // [kSums][kIcpThreads]
+    if (threadIdx.x == 0 && st->bodies == 0) atomicCAS(&st->t_step0, 0ull, globaltimer_ns());
     if (st->done) {  // converged / lost: end the device-side loop
         if constexpr (COND) {
             if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0u);
@@ -380,6 +377,7 @@ __global__ void __launch_bounds__(kIcpThreads, 1)
                 s_c[0] += s_c[w];
             }
             const unsigned long long total = s_c[0];
+            if (st->bodies == 0) st->t_assoc0 = globaltimer_ns();
             st->bodies += 1;
             s_lost = total < 10 ? 1 : 0;
             if (total < 10) {  // TrackingLost (registration.cpp:202-204)
@@ -505,6 +503,7 @@ __global__ void __launch_bounds__(kIcpThreads, 1)
         if (s_fast) {
             finalize_motion(st, s_fin, x, prm);
             *counter = 0;
+            st->t_end = globaltimer_ns();
             if constexpr (COND)
                 cudaGraphSetConditional(cond, (!st->done && st->iterations < prm.max_iterations) ? 1u : 0u);
         }
@@ -523,6 +522,7 @@ __global__ void __launch_bounds__(kIcpThreads, 1)
     if (lane == 0) {
         solve_finalize(st, s_fin, s_eig, prm);
         *counter = 0;
+        st->t_end = globaltimer_ns();
         if constexpr (COND)
             cudaGraphSetConditional(cond, (!st->done && st->iterations < prm.max_iterations) ? 1u : 0u);
     }
@@ -549,7 +549,7 @@ IcpParamsDev make_icp_params(const sf_match_params& p) {
 // launch to *launches (the caller adds 2 x IcpState::bodies after the fact).
 void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* tgt, const float* tgt_n,
                 const Intr& si, const Intr& ti, const double* d_initial, const IcpParamsDev& prm, cudaStream_t s,
-                uint64_t* launches, const int* dead, bool* device_loop) {
+                uint64_t* launches, const int* dead, bool* device_loop, bool state_ready) {
     SF_CUDA(cudaFuncSetAttribute(k_icp_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem));
     SF_CUDA(cudaFuncSetAttribute(k_icp_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem));
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -563,9 +563,12 @@ void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* 
     const bool loop = loop_enabled && cs == cudaStreamCaptureStatusActive && prm.max_iterations > 0;
     if (device_loop) *device_loop = loop;
     if (!loop) {
-        k_icp_init<false><<<1, 1, 0, s>>>(wk.st, d_initial, dead, prm.max_iterations, 0);
-        SF_LAUNCH_CHECK();
-        uint64_t cnt = 1;
+        uint64_t cnt = 0;
+        if (!state_ready) {
+            k_icp_init<false><<<1, 1, 0, s>>>(wk.st, d_initial, dead, prm.max_iterations, 0);
+            SF_LAUNCH_CHECK();
+            cnt = 1;
+        }
         for (int it = 0; it < prm.max_iterations; ++it) {
             k_icp_step<false><<<kStepCtas, kIcpThreads, kStepSmem, s>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st,
                                                                         wk.part_bbox, wk.part_count, wk.part,
@@ -580,9 +583,17 @@ void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* 
     SF_CUDA(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, nullptr, nullptr));
     cudaGraphConditionalHandle cond;
     SF_CUDA(cudaGraphConditionalHandleCreate(&cond, g, 0, 0));
-    k_icp_init<true><<<1, 1, 0, s>>>(wk.st, d_initial, dead, prm.max_iterations, cond);
+    if (state_ready) {
+        // first iteration as a plain node: it sets the condition for the loop of the others
+        // (the loop-entry latency of the conditional node is paid only by multi-iteration frames)
+        k_icp_step<true><<<kStepCtas, kIcpThreads, kStepSmem, s>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st,
+                                                                   wk.part_bbox, wk.part_count, wk.part, wk.counters,
+                                                                   cond);
+    } else {
+        k_icp_init<true><<<1, 1, 0, s>>>(wk.st, d_initial, dead, prm.max_iterations, cond);
+        if (launches) *launches += 1;
+    }
     SF_LAUNCH_CHECK();
-    if (launches) *launches += 1;
     const cudaGraphNode_t* deps = nullptr;
     size_t ndeps = 0;
     SF_CUDA(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &ndeps));

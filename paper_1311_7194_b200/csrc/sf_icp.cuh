@@ -48,6 +48,8 @@ struct IcpState {
     // the last iteration's normal matrix is deferred to k_icp_report (off the critical path).
     int eig_pending;
     double A_last[21];  // packed upper triangle of the last iteration's (shrunk) normal matrix
+    unsigned long long t_begin, t_end;  // device clock (ns): state init, end of the last solve
+    unsigned long long t_step0, t_assoc0;  // first step: first CTA start, association done (tail start)
 };
 
 struct IcpParamsDev {
@@ -107,9 +109,22 @@ struct IcpWork {
 };
 
 IcpParamsDev make_icp_params(const sf_match_params& p);
+// state_ready: the caller already initialised wk.st (icp_state_init in one of its kernels), so
+// the ICP starts with its first step; under capture the first step is a plain kernel node and
+// only later iterations run in the conditional WHILE node.
 void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* tgt, const float* tgt_n,
                 const Intr& si, const Intr& ti, const double* d_initial, const IcpParamsDev& prm, cudaStream_t s,
-                uint64_t* launches, const int* dead, bool* device_loop = nullptr);
+                uint64_t* launches, const int* dead, bool* device_loop = nullptr, bool state_ready = false);
+
+// IcpState for a new ICP from the initial delta (one thread).
+__device__ inline void icp_state_init(IcpState* st, const double* initial12, bool dead) {
+    IcpState z;
+    memset(&z, 0, sizeof(z));
+    z.delta = pose_from12(initial12);
+    z.done = dead ? 1 : 0;
+    z.t_begin = globaltimer_ns();
+    *st = z;
+}
 void fill_icp_result(const IcpState& st, sf_icp_result* out);
 // Eigenpairs of the last iteration when the fast gated solve deferred them (one warp).
 void launch_icp_report(IcpWork& wk, cudaStream_t s, uint64_t* launches);

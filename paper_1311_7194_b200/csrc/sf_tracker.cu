@@ -12,6 +12,7 @@
 // Ground-truth step (and the first frame): fuse at the given pose.
 // TrackingLost / PoolExhausted set a device "dead" flag: the rest of the frame and every
 // later step become no-ops, mirroring run()'s break (pipeline.cpp:289-299).
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -62,13 +63,17 @@ __global__ void k_tracker_after_icp(double* __restrict__ cur, double* __restrict
 // One warp: begin_track (lane 0) and the raycast's frame constants at the current pose.
 __global__ void k_tracker_begin_track_consts(VolParams P, Intr cam, const double* __restrict__ cur,
                                              const double* __restrict__ external, double* __restrict__ init_delta,
-                                             RayCounters* rstats, const TrackerDev* td, FrameConsts* fc) {
-    if (threadIdx.x == 0 && !td->dead) {
-        const Pose c = pose_from12(cur);
-        const Pose init = external ? compose(c, pose_from12(external)) : c;
-        pose_to12(compose(invert(c), init), init_delta);
-        RayCounters z{0, 0, 0, 0};
-        *rstats = z;
+                                             RayCounters* rstats, const TrackerDev* td, FrameConsts* fc,
+                                             IcpState* icp) {
+    if (threadIdx.x == 0) {
+        if (!td->dead) {
+            const Pose c = pose_from12(cur);
+            const Pose init = external ? compose(c, pose_from12(external)) : c;
+            pose_to12(compose(invert(c), init), init_delta);
+            RayCounters z{0, 0, 0, 0};
+            *rstats = z;
+        }
+        icp_state_init(icp, init_delta, td->dead != 0);  // the frame's ICP starts from init_delta
     }
     frame_consts_warp(P, cam, cur, fc);
 }
@@ -250,7 +255,7 @@ struct sf_tracker {
             SF_CUDA(cudaEventRecord(ev_prep_join, side_stream));
             prep_done = true;
             k_tracker_begin_track_consts<<<1, 32, 0, s>>>(vol->P, cam, d_cur, mode == 3 ? d_gt : nullptr,
-                                                          d_init_delta, d_rstats, d_td, d_rc_fc);
+                                                          d_init_delta, d_rstats, d_td, d_rc_fc, icp.st);
             SF_LAUNCH_CHECK();
             ++n;
             launch_ray_bounds(*vol, d_rc_fc, cam, d_ts, d_te, s, &n, dead, d_ray_list, d_rstats, d_model_depth,
@@ -260,7 +265,7 @@ struct sf_tracker {
             mark(1, s);
             SF_CUDA(cudaStreamWaitEvent(s, ev_prep_join, 0));
             launch_icp(icp, d_cap, icp.src_normals, d_model_depth, d_model_normals, cam, cam, d_init_delta, icp_prm, s,
-                       &n, dead, &issue_icp_loop);
+                       &n, dead, &issue_icp_loop, true);
             k_tracker_after_icp_fuse_begin<<<1, 32, 0, s>>>(d_cur, fb.pose, icp.st, d_td, cfg.orthonormalize, vol->P,
                                                             cam, fb.fc, fb.ctr, vol->d_vc);
             SF_LAUNCH_CHECK();
@@ -484,6 +489,8 @@ void sf_tracker::decode(const Fetch* f, int frame, int mode, uint64_t launches, 
     out->voxels_visited = out->blocks_processed * m * m * m;
     out->exact_voxels = f->ctr.exact_voxels;
     out->integrate_ns = f->ctr.t_end > f->ctr.t_begin ? f->ctr.t_end - f->ctr.t_begin : 0;
+    out->icp_ns = f->icp.t_step0 && f->icp.t_end > f->icp.t_step0 ? f->icp.t_end - f->icp.t_step0 : 0;
+    out->icp_steps = f->icp.bodies;
     out->kernel_launches = launches;
     if (icp_loop) out->kernel_launches += static_cast<uint64_t>(f->icp.bodies);
 }
