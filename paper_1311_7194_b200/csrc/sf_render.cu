@@ -125,18 +125,58 @@ __device__ __forceinline__ bool dda_jump(Dda& s, double T) {
     return true;
 }
 
+// Cheap conservative pre-test of pixel (u, v)'s ray: false only if the ray surely misses the
+// occupied box grown by one block between the near and far planes, in which case the exact
+// path below rejects it too (its slab clip and grown-box test are the same geometry, evaluated
+// exactly). Evaluated on the unnormalised ray x(s) = t + s R (du, dv, 1), whose camera depth
+// is s, with the box grown by a margin far above the rounding of either evaluation — no
+// square root and no division per ray (the exact path has a dozen). Most rays of a frame
+// miss the object.
+__device__ __forceinline__ bool may_meet_occupied(const VolParams& P, const FrameConsts* __restrict__ fc,
+                                                  const uint32_t* __restrict__ occ, int u, int v, double inv_fx,
+                                                  double inv_fy) {
+    const int* bb = occ_bbox(P, occ);
+    if (bb[0] > bb[3]) return false;  // nothing allocated: the exact path finds nothing either
+    const Intr& intr = fc->intr;
+    const Pose& pose = fc->pose;
+    const double du = (u - intr.cx) * inv_fx, dv = (v - intr.cy) * inv_fy;
+    const d3 wv = mv(pose.R, mk(du, dv, 1.0));
+    const double wd[3] = {wv.x, wv.y, wv.z}, org[3] = {pose.t.x, pose.t.y, pose.t.z};
+    const double box_lo[3] = {P.ox, P.oy, P.oz};
+    const double margin = 1e-7 * P.box_side + 1e-9;
+    double slo = intr.near_plane * (1.0 - 1e-9), shi = intr.far_plane * (1.0 + 1e-9);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double wlo = box_lo[a] + (double)(bb[a] - 1) * P.block_side - margin;
+        const double whi = box_lo[a] + (double)(bb[3 + a] + 2) * P.block_side + margin;
+        if (fabs(wd[a]) < 1e-12) {
+            if (org[a] < wlo || org[a] > whi) return false;
+            continue;
+        }
+        double r;  // ~1/wd[a] (two Newton steps on the hardware estimate: far below the margins)
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(wd[a]));
+        r = fma(r, fma(-wd[a], r, 1.0), r);
+        r = fma(r, fma(-wd[a], r, 1.0), r);
+        const double s0 = (wlo - org[a]) * r, s1 = (whi - org[a]) * r;
+        slo = dmax(slo, dmin(s0, s1));
+        shi = dmin(shi, dmax(s0, s1));
+    }
+    return slo <= shi * (1.0 + 1e-9) + 1e-12;
+}
+
 // Ray bounds of pixel (u, v) (render.cpp:65-153): writes t_start / t_end; true when the ray
 // has bounds (!bounds.empty(u, v)).
 __device__ __forceinline__ bool bounds_pixel(const VolParams& P, const FrameConsts* __restrict__ fc,
                                              const uint32_t* __restrict__ occ, const VolCounters* __restrict__ vc,
                                              const uint32_t* __restrict__ s_coarse, float* __restrict__ t_start,
                                              float* __restrict__ t_end, int w, double jump_cells,
-                                             unsigned long long* __restrict__ dbg, int u, int v) {
+                                             unsigned long long* __restrict__ dbg, int u, int v, double inv_fx,
+                                             double inv_fy) {
     const size_t idx = (size_t)v * w + u;
     float ts = INFINITY, te = -INFINITY;
     unsigned long long dbg_t0 = dbg ? globaltimer_ns() : 0ull;
     unsigned dbg_steps = 0;
-    if (vc->allocated_count != 0) {
+    if (vc->allocated_count != 0 && may_meet_occupied(P, fc, occ, u, v, inv_fx, inv_fy)) {
         const Intr& intr = fc->intr;
         const Pose& pose = fc->pose;
         const int n = P.N;
@@ -381,6 +421,7 @@ __global__ void __launch_bounds__(256, 2) k_ray_bounds(VolParams P, const FrameC
     // centre first (`order`): the long rays usually sit in the middle of the image.
     const int ln = threadIdx.x & 31;
     const int pw = (w + 7) >> 3, n_patches = pw * ((h + 3) >> 2);
+    const double inv_fx = 1.0 / fc->intr.fx, inv_fy = 1.0 / fc->intr.fy;
     for (;;) {
         int patch = 0;
         if (ln == 0) patch = static_cast<int>(atomicAdd(&sched[0], 1u));
@@ -390,7 +431,8 @@ __global__ void __launch_bounds__(256, 2) k_ray_bounds(VolParams P, const FrameC
         const int u = (patch % pw) * 8 + (ln & 7);
         const int v = (patch / pw) * 4 + (ln >> 3);
         if (u >= w || v >= h) continue;
-        const bool act = bounds_pixel(P, fc, occ, vc, s_coarse, t_start, t_end, w, jump_cells, dbg, u, v);
+        const bool act =
+            bounds_pixel(P, fc, occ, vc, s_coarse, t_start, t_end, w, jump_cells, dbg, u, v, inv_fx, inv_fy);
         if (ray_list) {
             // Active-ray list for the march (warp-aggregated append); inactive pixels get the
             // empty raycast result here.
