@@ -465,17 +465,16 @@ __global__ void __launch_bounds__(256, 2) k_ray_bounds(VolParams P, const FrameC
 // (sampling is pure), so results and the stage-1 step count equal the reference's.
 // Stage 2 runs redundantly in all G lanes (same addresses: broadcast loads); the six
 // gradient samples run one per lane.
-// Stage 1 of the raycast for pixel idx (render.cpp:160-208) by a group of G lanes: returns
-// true with the bracket of the first + -> - crossing in group lane 0, else writes the empty
-// result.
+// Stage 1 of the raycast for pixel idx (render.cpp:160-208) by a group of G lanes: appends the
+// bracket of the first + -> - crossing to the refine list, else writes the empty result.
 template <int G>
-__device__ __forceinline__ bool march_ray(const VolParams& P, const FrameConsts* __restrict__ fc,
+__device__ __forceinline__ void march_ray(const VolParams& P, const FrameConsts* __restrict__ fc,
                                           const int32_t* __restrict__ table, const uint16_t* __restrict__ payload,
                                           const uint32_t* __restrict__ occ, const double* s_tdec,
                                           const float* __restrict__ t_start, const float* __restrict__ t_end,
                                           float* __restrict__ depth_out, float* __restrict__ normals_out,
-                                          int w, int idx, RayBracket& out, unsigned long long& steps,
-                                          unsigned long long& with_bounds) {
+                                          RayCounters* stats, int w, RayBracket* __restrict__ brackets, int idx,
+                                          unsigned long long& steps, unsigned long long& with_bounds) {
     const int lane = threadIdx.x & 31;
     const int g = lane & (G - 1);
     const int gbase = lane & ~(G - 1);
@@ -551,18 +550,24 @@ __device__ __forceinline__ bool march_ray(const VolParams& P, const FrameConsts*
             br = RayBracket{hit_a, hit_b, val_a, val_b, idx, 0};
         }
     }
-    // Rays with a bracket go to the refine (stage 2 + normal, returned to the caller in
-    // group lane 0); the others get the empty result here.
+    // Rays with a bracket go to the one-thread-per-ray refine pass (stage 2 + normal); the
+    // others get the empty result here.
+    const unsigned am = __activemask();
+    const unsigned bal = __ballot_sync(am, bracket_out);
+    unsigned long long base = 0;
+    if (bal) {
+        const int leader = __ffs(bal) - 1;
+        if (lane == leader) base = atomicAdd(&stats->brackets, static_cast<unsigned long long>(__popc(bal)));
+        base = __shfl_sync(am, base, leader);
+    }
     if (bracket_out) {
-        out = br;
-        return true;
+        brackets[base + __popc(bal & ((1u << lane) - 1u))] = br;
     } else if (g == 0) {
         depth_out[idx] = out_d;
         normals_out[3 * idx] = nx;
         normals_out[3 * idx + 1] = ny;
         normals_out[3 * idx + 2] = nz;
     }
-    return false;
 }
 
 template <int G>
@@ -586,20 +591,8 @@ __global__ void __launch_bounds__(256, 3)
     const unsigned long long n_rays = stats->listed;
     for (unsigned long long r = (unsigned long long)blockIdx.x * kRaysPerCta + threadIdx.x / G; r < n_rays;
          r += (unsigned long long)gridDim.x * kRaysPerCta) {  // uniform within the group
-        const int idx = ray_list[r];
-        RayBracket br;
-        const bool bracket_out = march_ray<G>(P, fc, table, payload, occ, s_tdec, t_start, t_end, depth_out,
-                                              normals_out, w, idx, br, steps, with_bounds);
-        // bracketed rays go to the one-thread-per-ray refine pass
-        const unsigned am = __activemask();
-        const unsigned bal = __ballot_sync(am, bracket_out);
-        unsigned long long base = 0;
-        if (bal) {
-            const int leader = __ffs(bal) - 1;
-            if (lane == leader) base = atomicAdd(&stats->brackets, static_cast<unsigned long long>(__popc(bal)));
-            base = __shfl_sync(am, base, leader);
-        }
-        if (bracket_out) brackets[base + __popc(bal & ((1u << lane) - 1u))] = br;
+        march_ray<G>(P, fc, table, payload, occ, s_tdec, t_start, t_end, depth_out, normals_out, stats, w, brackets,
+                     ray_list[r], steps, with_bounds);
     }
     if (g != 0) steps = with_bounds = 0;  // per-ray values are replicated in the group
     // RaycastStats: warp reduction, one atomic per warp and counter.
