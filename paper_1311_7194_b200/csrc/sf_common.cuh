@@ -204,6 +204,7 @@ struct VolParams {
     uint64_t occ_fine_words;    // uint32 words of the fine (per-block) bitmap; coarse bits follow
     uint64_t occ_coarse_words;  // uint32 words of the coarse bitmap; 6 ints of bounding box follow
     double inv_voxel;           // RN(1 / voxel): Markstein-corrected division by voxel (sf_render.cu)
+    double inv_block_side;      // RN(1 / block_side): the same for block keys (sf_fusion.cu)
     double aux_lg_pmin, aux_lg_scale;
     int nshift;  // log2(N) when N is a power of two, else -1  // variance codes: log2(p_min), 255 / log2(p_max / p_min) (code guess)
     // Spatial sharding: this volume allocates only the blocks it owns,

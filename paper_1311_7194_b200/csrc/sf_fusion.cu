@@ -244,11 +244,13 @@ __global__ void k_block_keys_set(VolParams P, const FrameConsts* __restrict__ fc
                                  uint32_t* __restrict__ new_keys, uint32_t* __restrict__ new_idx,
                                  int2* __restrict__ work) {
     pdl_wait();
+    if (ctr->skip) return;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= su * sv || ctr->skip) return;
-    const int u = (i % su) * stride;
-    const int v = (i / su) * stride;
-    const bool valid = px_valid(depth, w, h, u, v);
+    const int lane = threadIdx.x & 31;
+    const bool in_range = i < su * sv;
+    const int u = in_range ? (i % su) * stride : 0;
+    const int v = in_range ? (i / su) * stride : 0;
+    const bool valid = in_range && px_valid(depth, w, h, u, v);
     d3 dir = mk(0, 0, 0);
     double t_hit = 0.0;
     if (valid) {
@@ -257,45 +259,73 @@ __global__ void k_block_keys_set(VolParams P, const FrameConsts* __restrict__ fc
         dir = mv(fc->pose.R, dir_cam);
         t_hit = (double)depth[(size_t)v * w + u] / dir_cam.z;
     }
+    // (x - origin) / block_side correctly rounded: RN(1/b) product + one fma-residual step
+    // (Markstein), as the reference's division (grid.cpp:283-287)
+    auto div_block = [&](double a) {
+        const double q = a * P.inv_block_side;
+        return fma(fma(-q, P.block_side, a), P.inv_block_side, q);
+    };
     const double offs[3] = {-fc->delta, 0.0, fc->delta};
     uint32_t keys[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        keys[k] = 0xffffffffu;
+        if (valid) {
+            const d3 x = add(fc->pose.t, scale(t_hit + offs[k], dir));
+            const int bx = ref_floor_int(div_block(x.x - P.ox));
+            const int by = ref_floor_int(div_block(x.y - P.oy));
+            const int bz = ref_floor_int(div_block(x.z - P.oz));
+            if (bx >= 0 && by >= 0 && bz >= 0 && bx < P.N && by < P.N && bz < P.N && shard_owns(P, bx, by, bz))
+                keys[k] = static_cast<uint32_t>(table_index(P, bx, by, bz));
+        }
+    }
+    // the three insertions, then the fresh keys' table reads, are independent of each other
     bool fresh[3];
+    int32_t slot[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         fresh[k] = false;
-        keys[k] = 0;
-        if (valid) {
-            const d3 x = add(fc->pose.t, scale(t_hit + offs[k], dir));
-            const int bx = ref_floor_int((x.x - P.ox) / P.block_side);
-            const int by = ref_floor_int((x.y - P.oy) / P.block_side);
-            const int bz = ref_floor_int((x.z - P.oz) / P.block_side);
-            if (bx >= 0 && by >= 0 && bz >= 0 && bx < P.N && by < P.N && bz < P.N && shard_owns(P, bx, by, bz))
-                keys[k] = static_cast<uint32_t>(table_index(P, bx, by, bz));
-            else keys[k] = 0xffffffffu;
-        } else keys[k] = 0xffffffffu;
-    }
-    // the three insertions are independent (one round trip to L2 for all of them)
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
         if (keys[k] != 0xffffffffu) {
             const uint32_t bit = 1u << (keys[k] & 31);
             fresh[k] = !(atomicOr(&keybits[keys[k] >> 5], bit) & bit);
         }
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) slot[k] = fresh[k] ? table[keys[k]] : kEmpty;
+    // one warp-wide reservation per list: inclusive scan of {fresh count, new count}
+    uint32_t nf = 0, nn = 0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
+        nf += fresh[k] ? 1u : 0u;
+        nn += (fresh[k] && slot[k] == kEmpty) ? 1u : 0u;
+    }
+    uint32_t sc = nf | (nn << 16);
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, sc, off);
+        if (lane >= off) sc += o;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, sc, 31);
+    uint32_t base_f = 0, base_n = 0;
+    if (lane == 0 && (tot & 0xffffu)) base_f = atomicAdd(&ctr->n_unique, tot & 0xffffu);
+    if (lane == 1 && (tot >> 16)) base_n = atomicAdd(&ctr->n_new, tot >> 16);
+    base_f = __shfl_sync(0xffffffffu, base_f, 0);
+    base_n = __shfl_sync(0xffffffffu, base_n, 1);
+    uint32_t j = base_f + (sc & 0xffffu) - nf, q = base_n + (sc >> 16) - nn;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (!fresh[k]) continue;
         const uint32_t key = keys[k];
-        const int32_t slot = fresh[k] ? table[key] : kEmpty;
-        const uint32_t j = warp_append(fresh[k], &ctr->n_unique);
-        if (fresh[k]) uniq[j] = key;
-        const bool isnew = fresh[k] && slot == kEmpty;
-        const uint32_t q = warp_append(isnew, &ctr->n_new);
-        if (isnew) {
+        uniq[j] = key;
+        if (slot[k] == kEmpty) {
             new_keys[q] = key;
             new_idx[q] = j;
             work[j] = make_int2(static_cast<int32_t>(0x80000000u), static_cast<int32_t>(key));
-        } else if (fresh[k]) {
-            work[j] = make_int2(slot, static_cast<int32_t>(key));
+            ++q;
+        } else {
+            work[j] = make_int2(slot[k], static_cast<int32_t>(key));
         }
+        ++j;
     }
 }
 

@@ -295,6 +295,7 @@ static VolParams make_params(const sf_grid_config& c, const sf_aux_quant& a, uin
     P.voxel = c.box_side / P.res;                      // GridConfig::voxel_size (grid.hpp:36)
     P.inv_voxel = 1.0 / P.voxel;
     P.block_side = P.voxel * P.M;                      // SparseTsdfGrid::block_side (grid.hpp:149)
+    P.inv_block_side = 1.0 / P.block_side;
     P.delta = c.truncation > 0.0 ? c.truncation : 4.0 * P.voxel;  // grid.hpp:37
     P.aux_mode = a.mode;
     P.aux_w_max = a.w_max;
