@@ -134,6 +134,42 @@ __global__ void k_tracker_finish(const FrameCounters* ctr, TrackerDev* td) {
 
 using namespace sf;
 
+// Everything a frame's metrics are decoded from (host side: pinned, mapped).
+struct TrackerFetch {
+    double cur[12];
+    double fuse_pose[12];
+    TrackerDev td;
+    FrameCounters ctr;
+    RayCounters rs;
+    IcpState icp;
+};
+
+template <typename T>
+__device__ __forceinline__ void copy_words(T* dst, const T* src, int tid, int nthreads) {
+    static_assert(sizeof(T) % 8 == 0, "8-byte words");
+    const unsigned long long* s = reinterpret_cast<const unsigned long long*>(src);
+    volatile unsigned long long* d = reinterpret_cast<volatile unsigned long long*>(dst);
+    for (int i = tid; i < static_cast<int>(sizeof(T) / 8); i += nthreads) d[i] = s[i];
+}
+
+// Frame metrics snapshot written straight to mapped pinned memory (one launch).
+__global__ void k_tracker_snapshot(TrackerFetch* dst, const double* __restrict__ cur,
+                                   const double* __restrict__ fuse_pose, const TrackerDev* __restrict__ td,
+                                   const FrameCounters* __restrict__ ctr, const RayCounters* __restrict__ rs,
+                                   const IcpState* __restrict__ icp) {
+    const int t = threadIdx.x, n = blockDim.x;
+    volatile double* dc = dst->cur;
+    volatile double* dp = dst->fuse_pose;
+    if (t < 12) {
+        dc[t] = cur[t];
+        dp[t] = fuse_pose[t];
+    }
+    copy_words(&dst->td, td, t, n);
+    copy_words(&dst->ctr, ctr, t, n);
+    copy_words(&dst->rs, rs, t, n);
+    copy_words(&dst->icp, icp, t, n);
+}
+
 struct sf_tracker {
     sf_volume* vol = nullptr;
     sf_tracker_config cfg{};
@@ -179,14 +215,8 @@ struct sf_tracker {
     bool issue_icp_loop = false;  // set by issue(): ICP iterations run as a device-side loop
     bool last_icp_loop = false;
     // pinned fetch staging (also the per-frame snapshot layout)
-    struct Fetch {
-        double cur[12];
-        double fuse_pose[12];
-        TrackerDev td;
-        FrameCounters ctr;
-        RayCounters rs;
-        IcpState icp;
-    }* h = nullptr;
+    using Fetch = TrackerFetch;
+    Fetch* h = nullptr;
     Fetch* snap = nullptr;  // pinned [2]: per-frame metric snapshots (streaming)
     struct SnapMeta {
         int frame, mode;
@@ -195,13 +225,13 @@ struct sf_tracker {
     } snap_meta[2] = {};
 
     // device buffers -> pinned host f (asynchronous on s)
+    // The frame's metrics into pinned host memory: one kernel storing through the mapped
+    // pointer (six separate device-to-host copies cost ~20 us of stream latency per step).
     void copy_metrics(Fetch* f, cudaStream_t s) {
-        SF_CUDA(cudaMemcpyAsync(f->cur, d_cur, sizeof(f->cur), cudaMemcpyDeviceToHost, s));
-        SF_CUDA(cudaMemcpyAsync(f->fuse_pose, fb.pose, sizeof(f->fuse_pose), cudaMemcpyDeviceToHost, s));
-        SF_CUDA(cudaMemcpyAsync(&f->td, d_td, sizeof(TrackerDev), cudaMemcpyDeviceToHost, s));
-        SF_CUDA(cudaMemcpyAsync(&f->ctr, fb.ctr, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
-        SF_CUDA(cudaMemcpyAsync(&f->rs, d_rstats, sizeof(RayCounters), cudaMemcpyDeviceToHost, s));
-        SF_CUDA(cudaMemcpyAsync(&f->icp, icp.st, sizeof(IcpState), cudaMemcpyDeviceToHost, s));
+        Fetch* df = nullptr;
+        SF_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&df), f, 0));
+        k_tracker_snapshot<<<1, 128, 0, s>>>(df, d_cur, fb.pose, d_td, fb.ctr, d_rstats, icp.st);
+        SF_LAUNCH_CHECK();
     }
     void decode(const Fetch* f, int frame, int mode, uint64_t launches, bool icp_loop, sf_frame_metrics* out) const;
 
@@ -444,6 +474,7 @@ int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, con
         // metric snapshot of this frame (read by sf_tracker_fetch_frame without waiting for
         // frames issued later)
         tr->copy_metrics(&tr->snap[slot], s);
+        tr->last_launches += 1;  // the snapshot kernel
         SF_CUDA(cudaEventRecord(tr->ev_snap[slot], s));
         tr->snap_meta[slot] = {tr->frames, eff, tr->last_launches, tr->last_icp_loop};
         ++tr->frames;
