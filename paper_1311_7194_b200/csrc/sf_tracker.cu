@@ -170,6 +170,38 @@ __global__ void k_tracker_snapshot(TrackerFetch* dst, const double* __restrict__
     copy_words(&dst->icp, icp, t, n);
 }
 
+// The captured frame (and its sigma plane) into the tracker's buffers: one launch for both.
+__global__ void k_copy_frame(float4* __restrict__ d0, const float4* __restrict__ s0, float4* __restrict__ d1,
+                             const float4* __restrict__ s1, size_t n4) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+        d0[i] = __ldg(&s0[i]);
+        if (d1) d1[i] = __ldg(&s1[i]);
+    }
+}
+// Returns true when it launched the kernel (false: plain copies for unaligned buffers).
+static bool launch_copy_frame(float* d0, const float* s0, float* d1, const float* s1, size_t n, cudaStream_t s) {
+    const bool vec = n % 4 == 0 && (reinterpret_cast<uintptr_t>(s0) & 15) == 0 &&
+                     (!d1 || (reinterpret_cast<uintptr_t>(s1) & 15) == 0);
+    if (!vec) {  // unaligned user buffers: plain copies
+        SF_CUDA(cudaMemcpyAsync(d0, s0, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        if (d1) SF_CUDA(cudaMemcpyAsync(d1, s1, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        return false;
+    }
+    k_copy_frame<<<148 * 2, 256, 0, s>>>(reinterpret_cast<float4*>(d0), reinterpret_cast<const float4*>(s0),
+                                         reinterpret_cast<float4*>(d1), reinterpret_cast<const float4*>(s1), n / 4);
+    SF_LAUNCH_CHECK();
+    return true;
+}
+
+// A host pose (12 doubles) into device memory through the kernel's parameters: no
+// host-to-device copy from pageable memory on the step's stream.
+struct Pose12 {
+    double v[12];
+};
+__global__ void k_set_pose12(double* __restrict__ dst, Pose12 p) {
+    if (threadIdx.x < 12) dst[threadIdx.x] = p.v[threadIdx.x];
+}
+
 struct sf_tracker {
     sf_volume* vol = nullptr;
     sf_tracker_config cfg{};
@@ -216,6 +248,7 @@ struct sf_tracker {
     bool last_icp_loop = false;
     // pinned fetch staging (also the per-frame snapshot layout)
     using Fetch = TrackerFetch;
+    uint64_t extra_launches = 0;  // kernels of the current step outside the frame graph
     Fetch* h = nullptr;
     Fetch* snap = nullptr;  // pinned [2]: per-frame metric snapshots (streaming)
     struct SnapMeta {
@@ -409,11 +442,11 @@ int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, con
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         const size_t n = static_cast<size_t>(tr->cam.w) * tr->cam.h;
         const bool has_sigma = captured->sigma != nullptr;
+        tr->extra_launches = 0;
         const int slot = tr->frames & 1;
         if (captured->on_device) {
-            SF_CUDA(cudaMemcpyAsync(tr->d_cap, captured->depth, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
-            if (has_sigma)
-                SF_CUDA(cudaMemcpyAsync(tr->d_cap_sigma, captured->sigma, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+            tr->extra_launches +=
+                launch_copy_frame(tr->d_cap, captured->depth, has_sigma ? tr->d_cap_sigma : nullptr, captured->sigma, n, s);
         } else {
             // Host frame: the H2D copy runs on the copy stream into a staging buffer, so it
             // overlaps the previous frame's compute; the frame then starts with a D2D copy.
@@ -425,10 +458,8 @@ int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, con
                                         cudaMemcpyHostToDevice, tr->copy_stream));
             SF_CUDA(cudaEventRecord(tr->ev_staged[slot], tr->copy_stream));
             SF_CUDA(cudaStreamWaitEvent(s, tr->ev_staged[slot], 0));
-            SF_CUDA(cudaMemcpyAsync(tr->d_cap, tr->d_stage[slot], n * sizeof(float), cudaMemcpyDeviceToDevice, s));
-            if (has_sigma)
-                SF_CUDA(cudaMemcpyAsync(tr->d_cap_sigma, tr->d_stage_sigma[slot], n * sizeof(float),
-                                        cudaMemcpyDeviceToDevice, s));
+            tr->extra_launches += launch_copy_frame(tr->d_cap, tr->d_stage[slot], has_sigma ? tr->d_cap_sigma : nullptr,
+                                                    tr->d_stage_sigma[slot], n, s);
             SF_CUDA(cudaEventRecord(tr->ev_stage_free[slot], s));
         }
         // First frame: fuse at the current (initial) pose without registration (pipeline.cpp:250-252).
@@ -436,8 +467,13 @@ int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, con
         // an external initial delta (tracking.mode = icp_with_hook, pipeline.cpp:262-266)
         int eff = mode == 2 ? 3 : mode;
         if (mode != 1 && tr->frames == 0) eff = 2;  // fuse at current, keep current
-        if (eff == 1 || eff == 3)
-            SF_CUDA(cudaMemcpyAsync(tr->d_gt, gt_pose, 12 * sizeof(double), cudaMemcpyHostToDevice, s));
+        if (eff == 1 || eff == 3) {
+            Pose12 g;
+            for (int i = 0; i < 12; ++i) g.v[i] = gt_pose[i];
+            k_set_pose12<<<1, 32, 0, s>>>(tr->d_gt, g);
+            SF_LAUNCH_CHECK();
+            tr->extra_launches += 1;
+        }
         if (eff == 2) SF_CUDA(cudaMemcpyAsync(tr->d_gt, tr->d_cur, 12 * sizeof(double), cudaMemcpyDeviceToDevice, s));
         const int gmode = eff == 0 ? 0 : eff == 1 ? 1 : 2;
         const int sidx = has_sigma ? 1 : 0;
@@ -474,7 +510,7 @@ int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, con
         // metric snapshot of this frame (read by sf_tracker_fetch_frame without waiting for
         // frames issued later)
         tr->copy_metrics(&tr->snap[slot], s);
-        tr->last_launches += 1;  // the snapshot kernel
+        tr->last_launches += 1 + tr->extra_launches;  // the snapshot kernel (+ the frame copy)
         SF_CUDA(cudaEventRecord(tr->ev_snap[slot], s));
         tr->snap_meta[slot] = {tr->frames, eff, tr->last_launches, tr->last_icp_loop};
         ++tr->frames;
@@ -485,8 +521,11 @@ int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, con
 int sf_tracker_set_pose(sf_tracker_t tr, const double pose[12], void* stream) {
     return guarded([&]() -> int {
         SF_CUDA(cudaSetDevice(tr->vol->device));
-        SF_CUDA(cudaMemcpyAsync(tr->d_cur, pose, 12 * sizeof(double), cudaMemcpyHostToDevice,
-                                static_cast<cudaStream_t>(stream)));
+        if (!tr || !pose) throw Error(SF_INVALID_ARGUMENT, "sf_tracker_set_pose: null argument");
+        Pose12 g;
+        for (int i = 0; i < 12; ++i) g.v[i] = pose[i];
+        k_set_pose12<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(tr->d_cur, g);
+        SF_LAUNCH_CHECK();
         return SF_OK;
     });
 }
