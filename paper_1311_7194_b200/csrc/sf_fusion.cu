@@ -1408,9 +1408,9 @@ static void launch_integrate_rows(Volume& v, FrameBuffers& fb, const FuseParams&
                                      (int)RowRing<MS>::kBytes));
         configured = true;
     }
-    launch_pdl(k_integrate_rows<MODE, MS>, dim3(148 * kRowCtasPerSm), dim3(kRowThreads), RowRing<MS>::kBytes, s, 
-        v.P, fb.fc, fp, fb.work, fb.ctr, v.d_aux, fb.pix_f, fb.pix_dm, fb.pix_var, fb.pix_w, v.d_slot_key,
-        v.d_payload, fb.keys_unique, v.d_keybits);
+    launch_pdl(k_integrate_rows<MODE, MS>, dim3(148 * kRowCtasPerSm), dim3(kRowThreads), RowRing<MS>::kBytes, s,
+               v.P, fb.fc, fp, fb.work, fb.ctr, v.d_aux, fb.pix_f, fb.pix_dm, fb.pix_var, fb.pix_w, v.d_slot_key,
+               v.d_payload, fb.keys_unique, v.d_keybits);
 }
 
 // Frame prep of fuse_frame (depends only on the frame): normals with the fusion options
@@ -1471,13 +1471,13 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
         n += 3 + 4;  // keys + list_len + visible + (sort, unique: >= 4 CUB kernels)
     } else {
         // fuse_frame: unordered key set + ranked new keys + work list (no global sort)
-        launch_pdl(k_block_keys_set, dim3((su * sv + kThreads - 1) / kThreads), dim3(kThreads), 0, s, 
-            P, fb.fc, depth, w, h, fb.stride, su, sv, v.d_keybits, fb.keys_unique, fb.ctr, v.d_table, fb.ranks,
-            fb.flags, fb.work);
+        launch_pdl(k_block_keys_set, dim3((su * sv + kThreads - 1) / kThreads), dim3(kThreads), 0, s, P, fb.fc, depth,
+                   w, h, fb.stride, su, sv, v.d_keybits, fb.keys_unique, fb.ctr, v.d_table, fb.ranks, fb.flags,
+                   fb.work);
         SF_LAUNCH_CHECK();
-        launch_pdl(k_alloc_visible, dim3(kPersistentCtas), dim3(kThreads), 0, s, P, fb.fc, fb.ctr, v.d_vc, fb.ranks, fb.flags, v.d_table,
-                                                            v.d_free_list, v.d_slot_key, v.d_occ, fb.keys_unique,
-                                                            v.d_keybits, depth, w, h, fb.work);
+        launch_pdl(k_alloc_visible, dim3(kPersistentCtas), dim3(kThreads), 0, s, P, fb.fc, fb.ctr, v.d_vc, fb.ranks,
+                   fb.flags, v.d_table, v.d_free_list, v.d_slot_key, v.d_occ, fb.keys_unique, v.d_keybits, depth, w,
+                   h, fb.work);
         SF_LAUNCH_CHECK();
         n += 2;
     }

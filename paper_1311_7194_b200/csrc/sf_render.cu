@@ -770,9 +770,8 @@ void launch_ray_bounds(Volume& v, const FrameConsts* d_fc, const Intr& intr, flo
     const uint64_t nc = v.P.Nc;
     const size_t smem = ((nc * nc * nc + 31) / 32) * sizeof(uint32_t);
     if (smem > 48 * 1024) SF_CUDA(cudaFuncSetAttribute(k_ray_bounds, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    launch_pdl(k_ray_bounds, grd, blk, smem, s, v.P, d_fc, v.d_occ, v.d_vc, t_start, t_end, intr.w, intr.h, dead_flag,
-                                        ray_list, list_ctr, depth, normals, ray_jump_cells(), v.d_sched,
-                                        v.d_patch_order, rb_dbg);
+    launch_pdl(k_ray_bounds, grd, blk, smem, s, v.P, d_fc, v.d_occ, v.d_vc, t_start, t_end, intr.w, intr.h,
+               dead_flag, ray_list, list_ctr, depth, normals, ray_jump_cells(), v.d_sched, v.d_patch_order, rb_dbg);
     SF_LAUNCH_CHECK();
     rb_debug_dump(rb_dbg, (size_t)intr.w * intr.h, s);
     if (launches) *launches += 1;
@@ -836,15 +835,15 @@ void launch_raycast(Volume& v, const FrameConsts* d_fc, const Intr& intr, const 
                     const int* dead_flag, const int* ray_list, RayBracket* brackets) {
     constexpr int G = 8;  // lanes per ray: 32 rays per 256-thread CTA, persistent over the list
     const dim3 blk(256), grd(148 * 3);
-    launch_pdl(k_raycast<G>, grd, blk, 0, s, v.P, d_fc, v.d_table, v.d_payload, v.d_occ, v.d_aux, t_start, t_end, depth, normals,
-                                     d_stats, intr.w, intr.h, dead_flag, ray_list, brackets);
+    launch_pdl(k_raycast<G>, grd, blk, 0, s, v.P, d_fc, v.d_table, v.d_payload, v.d_occ, v.d_aux, t_start, t_end,
+               depth, normals, d_stats, intr.w, intr.h, dead_flag, ray_list, brackets);
     SF_LAUNCH_CHECK();
     // one warp per CTA: the ~30 k bracketed rays spread over all SMs (latency-bound, few warps)
     static unsigned long long* rf_dbg = nullptr;  // SF_RF_DEBUG=<path>: per-ray refine timing (graph-less runs)
     const char* rf_path = std::getenv("SF_RF_DEBUG");
     if (rf_path && !rf_dbg) SF_CUDA(cudaMalloc(&rf_dbg, 4ull * intr.w * intr.h * sizeof(unsigned long long)));
-    launch_pdl(k_raycast_refine, dim3(148 * 16), dim3(32), 0, s, v.P, d_fc, v.d_table, v.d_payload, v.d_occ, v.d_aux, brackets, depth,
-                                             normals, d_stats, intr.w, dead_flag, rf_path ? rf_dbg : nullptr);
+    launch_pdl(k_raycast_refine, dim3(148 * 16), dim3(32), 0, s, v.P, d_fc, v.d_table, v.d_payload, v.d_occ,
+               v.d_aux, brackets, depth, normals, d_stats, intr.w, dead_flag, rf_path ? rf_dbg : nullptr);
     SF_LAUNCH_CHECK();
     if (rf_path) {
         unsigned long long nb = 0;
