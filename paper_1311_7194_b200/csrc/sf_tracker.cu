@@ -31,6 +31,64 @@ struct TrackerDev {
     int frame;
 };
 
+// Everything a frame's metrics are decoded from (host side: pinned, mapped).
+struct TrackerFetch {
+    double cur[12];
+    double fuse_pose[12];
+    TrackerDev td;
+    FrameCounters ctr;
+    RayCounters rs;
+    IcpState icp;
+};
+
+template <typename T>
+__device__ __forceinline__ void copy_words(T* dst, const T* src, int tid, int nthreads) {
+    static_assert(sizeof(T) % 8 == 0, "8-byte words");
+    const unsigned long long* s = reinterpret_cast<const unsigned long long*>(src);
+    volatile unsigned long long* d = reinterpret_cast<volatile unsigned long long*>(dst);
+    for (int i = tid; i < static_cast<int>(sizeof(T) / 8); i += nthreads) d[i] = s[i];
+}
+
+// Frame metrics snapshot written straight to mapped pinned memory (all threads of one CTA).
+__device__ inline void snapshot_body(TrackerFetch* dst, const double* __restrict__ cur,
+                                     const double* __restrict__ fuse_pose, const TrackerDev* td,
+                                     const FrameCounters* ctr, const RayCounters* __restrict__ rs,
+                                     const IcpState* __restrict__ icp) {
+    const int t = threadIdx.x, n = blockDim.x;
+    volatile double* dc = dst->cur;
+    volatile double* dp = dst->fuse_pose;
+    if (t < 12) {
+        dc[t] = cur[t];
+        dp[t] = fuse_pose[t];
+    }
+    copy_words(&dst->td, td, t, n);
+    copy_words(&dst->ctr, ctr, t, n);
+    copy_words(&dst->rs, rs, t, n);
+    copy_words(&dst->icp, icp, t, n);
+}
+__global__ void k_tracker_snapshot(TrackerFetch* dst, const double* __restrict__ cur,
+                                   const double* __restrict__ fuse_pose, const TrackerDev* __restrict__ td,
+                                   const FrameCounters* __restrict__ ctr, const RayCounters* __restrict__ rs,
+                                   const IcpState* __restrict__ icp) {
+    snapshot_body(dst, cur, fuse_pose, td, ctr, rs, icp);
+}
+
+// Where a step's last kernel leaves the frame's metrics: one of two mapped pinned snapshots
+// (by step parity, counted on the device in TrackerDev::frame) read by sf_tracker_fetch_frame.
+struct SnapTargets {
+    TrackerFetch* slot[2];
+    const double* cur;
+    const double* fuse_pose;
+    const RayCounters* rs;
+    const IcpState* icp;
+};
+__device__ inline void finish_snapshot(const SnapTargets& st, TrackerDev* td, const FrameCounters* ctr) {
+    __syncthreads();  // thread 0's final counter / status writes
+    snapshot_body(st.slot[td->frame & 1], st.cur, st.fuse_pose, td, ctr, st.rs, st.icp);
+    __syncthreads();
+    if (threadIdx.x == 0) td->frame += 1;
+}
+
 __global__ void k_tracker_begin_track(const double* __restrict__ cur, const double* __restrict__ external,
                                       double* __restrict__ init_delta, RayCounters* rstats, const TrackerDev* td) {
     if (td->dead) return;
@@ -101,13 +159,15 @@ __global__ void k_tracker_after_icp_fuse_begin(double* __restrict__ cur, double*
 }
 
 // fuse_finalize + tracker finish
-__global__ void k_tracker_fuse_finish(FrameCounters* ctr, const VolCounters* vc, TrackerDev* td) {
-    fuse_finalize_body(ctr, vc);
-    if (td->dead) return;
-    if (ctr->exhausted) {
-        td->dead = 1;
-        td->status = SF_POOL_EXHAUSTED;
+__global__ void k_tracker_fuse_finish(FrameCounters* ctr, const VolCounters* vc, TrackerDev* td, SnapTargets snap) {
+    if (threadIdx.x == 0) {
+        fuse_finalize_body(ctr, vc);
+        if (!td->dead && ctr->exhausted) {
+            td->dead = 1;
+            td->status = SF_POOL_EXHAUSTED;
+        }
     }
+    finish_snapshot(snap, td, ctr);
 }
 
 __global__ void k_tracker_begin_gt(const double* __restrict__ gt, double* __restrict__ cur,
@@ -122,53 +182,17 @@ __global__ void k_tracker_begin_gt(const double* __restrict__ gt, double* __rest
     td->registered = 0;
 }
 
-__global__ void k_tracker_finish(const FrameCounters* ctr, TrackerDev* td) {
-    if (td->dead) return;
-    if (ctr->exhausted) {
+__global__ void k_tracker_finish(const FrameCounters* ctr, TrackerDev* td, SnapTargets snap) {
+    if (threadIdx.x == 0 && !td->dead && ctr->exhausted) {
         td->dead = 1;
         td->status = SF_POOL_EXHAUSTED;
     }
+    finish_snapshot(snap, td, ctr);
 }
 
 }  // namespace sf
 
 using namespace sf;
-
-// Everything a frame's metrics are decoded from (host side: pinned, mapped).
-struct TrackerFetch {
-    double cur[12];
-    double fuse_pose[12];
-    TrackerDev td;
-    FrameCounters ctr;
-    RayCounters rs;
-    IcpState icp;
-};
-
-template <typename T>
-__device__ __forceinline__ void copy_words(T* dst, const T* src, int tid, int nthreads) {
-    static_assert(sizeof(T) % 8 == 0, "8-byte words");
-    const unsigned long long* s = reinterpret_cast<const unsigned long long*>(src);
-    volatile unsigned long long* d = reinterpret_cast<volatile unsigned long long*>(dst);
-    for (int i = tid; i < static_cast<int>(sizeof(T) / 8); i += nthreads) d[i] = s[i];
-}
-
-// Frame metrics snapshot written straight to mapped pinned memory (one launch).
-__global__ void k_tracker_snapshot(TrackerFetch* dst, const double* __restrict__ cur,
-                                   const double* __restrict__ fuse_pose, const TrackerDev* __restrict__ td,
-                                   const FrameCounters* __restrict__ ctr, const RayCounters* __restrict__ rs,
-                                   const IcpState* __restrict__ icp) {
-    const int t = threadIdx.x, n = blockDim.x;
-    volatile double* dc = dst->cur;
-    volatile double* dp = dst->fuse_pose;
-    if (t < 12) {
-        dc[t] = cur[t];
-        dp[t] = fuse_pose[t];
-    }
-    copy_words(&dst->td, td, t, n);
-    copy_words(&dst->ctr, ctr, t, n);
-    copy_words(&dst->rs, rs, t, n);
-    copy_words(&dst->icp, icp, t, n);
-}
 
 // The captured frame (and its sigma plane) into the tracker's buffers: one launch for both.
 __global__ void k_copy_frame(float4* __restrict__ d0, const float4* __restrict__ s0, float4* __restrict__ d1,
@@ -249,6 +273,7 @@ struct sf_tracker {
     // pinned fetch staging (also the per-frame snapshot layout)
     using Fetch = TrackerFetch;
     uint64_t extra_launches = 0;  // kernels of the current step outside the frame graph
+    TrackerFetch* snap_dev[2] = {nullptr, nullptr};  // device views of snap[0..1]
     Fetch* h = nullptr;
     Fetch* snap = nullptr;  // pinned [2]: per-frame metric snapshots (streaming)
     struct SnapMeta {
@@ -258,6 +283,16 @@ struct sf_tracker {
     } snap_meta[2] = {};
 
     // device buffers -> pinned host f (asynchronous on s)
+    SnapTargets snap_targets() const {
+        SnapTargets t;
+        t.slot[0] = snap_dev[0];
+        t.slot[1] = snap_dev[1];
+        t.cur = d_cur;
+        t.fuse_pose = fb.pose;
+        t.rs = d_rstats;
+        t.icp = icp.st;
+        return t;
+    }
     // The frame's metrics into pinned host memory: one kernel storing through the mapped
     // pointer (six separate device-to-host copies cost ~20 us of stream latency per step).
     void copy_metrics(Fetch* f, cudaStream_t s) {
@@ -356,8 +391,8 @@ struct sf_tracker {
             SF_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
             joined = true;
         }
-        if (merged) k_tracker_fuse_finish<<<1, 1, 0, s>>>(fb.ctr, vol->d_vc, d_td);
-        else k_tracker_finish<<<1, 1, 0, s>>>(fb.ctr, d_td);
+        if (merged) k_tracker_fuse_finish<<<1, 128, 0, s>>>(fb.ctr, vol->d_vc, d_td, snap_targets());
+        else k_tracker_finish<<<1, 128, 0, s>>>(fb.ctr, d_td, snap_targets());
         SF_LAUNCH_CHECK();
         ++n;
         mark(5, s);
@@ -415,6 +450,8 @@ int sf_tracker_create(sf_volume_t vol, const sf_tracker_config* config, const do
         }
         SF_CUDA(cudaMallocHost(&t->snap, 2 * sizeof(sf_tracker::Fetch)));
         std::memset(t->snap, 0, 2 * sizeof(sf_tracker::Fetch));
+        for (int i = 0; i < 2; ++i)
+            SF_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&t->snap_dev[i]), &t->snap[i], 0));
         SF_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
         SF_CUDA(cudaEventCreateWithFlags(&t->ev_join, cudaEventDisableTiming));
         SF_CUDA(cudaEventCreateWithFlags(&t->ev_prep_fork, cudaEventDisableTiming));
@@ -509,8 +546,8 @@ int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, con
         tr->last_mode = eff;
         // metric snapshot of this frame (read by sf_tracker_fetch_frame without waiting for
         // frames issued later)
-        tr->copy_metrics(&tr->snap[slot], s);
-        tr->last_launches += 1 + tr->extra_launches;  // the snapshot kernel (+ the frame copy)
+        // (the step's last kernel wrote this frame's metric snapshot into snap[slot])
+        tr->last_launches += tr->extra_launches;  // the frame copy / pose kernels
         SF_CUDA(cudaEventRecord(tr->ev_snap[slot], s));
         tr->snap_meta[slot] = {tr->frames, eff, tr->last_launches, tr->last_icp_loop};
         ++tr->frames;
