@@ -122,6 +122,14 @@ typedef struct {
     double shrink_floor;
     double normal_sigma0;
     double normal_spatial_scale;
+    /* Not in the reference struct: the order of the normal-equation sums.
+     * 0 (default): tree-reduced compensated sums in unshrunk form (one launch per iteration);
+     *    the pose equals the reference's to ~1e-15 per call.
+     * 1: the reference's order (registration.cpp:52-123): matches compacted in row-major order,
+     *    shrunk per match, 28 sequential Kahan sums, cyclic Jacobi, spectral gated solve and
+     *    the SVD apply_motion — bit-identical poses, so a tracked sequence stays bit-identical
+     *    to the reference frame after frame (slower: the Kahan chains are sequential). */
+    int32_t reduction;
 } sf_match_params;
 
 /* IcpResult + GatedSolution (registration.hpp:68-83). */
@@ -336,7 +344,13 @@ int sf_tracker_destroy(sf_tracker_t tr);
 /* mode 0: track (raycast + ICP, except for the tracker's first frame which is fused at the
  * current pose); mode 1: ground truth (fuse at gt_pose, no raycast/ICP); mode 2: track with
  * an external initial delta passed in gt_pose (tracking.mode = icp_with_hook: ICP starts
- * from compose(current, external), pipeline.cpp:262-267, registration.cpp:222-224). */
+ * from compose(current, external), pipeline.cpp:262-267, registration.cpp:222-224).
+ * Host frames (captured->on_device == 0) are copied asynchronously: the depth / sigma host
+ * buffers must stay valid and UNMODIFIED until this step has completed — i.e. until
+ * sf_tracker_fetch, sf_tracker_fetch_frame(k) of this step, or a synchronisation of `stream`.
+ * A capture loop that refills one pinned buffer must alternate two (or fetch first).
+ * The frame that raises TrackingLost / PoolExhausted reports what run()'s catch block pushes
+ * (pipeline.cpp:289-299); every later step is a no-op carrying the same status. */
 int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, const double gt_pose[12],
                     void* stream);
 /* Re-seed the tracker's current pose (relocalisation; asynchronous on `stream`). */

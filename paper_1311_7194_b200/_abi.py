@@ -99,6 +99,7 @@ class MatchParamsC(C.Structure):
         ("shrink_floor", C.c_double),
         ("normal_sigma0", C.c_double),
         ("normal_spatial_scale", C.c_double),
+        ("reduction", C.c_int32),
     ]
 
 

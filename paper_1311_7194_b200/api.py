@@ -275,6 +275,10 @@ class MatchParams:
     shrink_floor: float = 1e-6
     normal_sigma0: float = 2.5e-4
     normal_spatial_scale: float = 0.0
+    # not in the reference struct: 0 tree-ordered sums (fast, pose ~1e-15 of the reference per
+    # call); 1 the reference's sequential Kahan order (bit-identical poses, sf_gpu.h)
+    reduction: int = 0
+    TREE, REFERENCE_ORDER = 0, 1
 
     @staticmethod
     def for_voxel_size(voxel_size: float) -> "MatchParams":
@@ -284,7 +288,7 @@ class MatchParams:
     def c(self) -> A.MatchParamsC:
         return A.MatchParamsC(self.max_distance, self.max_normal_angle, self.max_iterations,
                               self.convergence_epsilon, self.eigen_threshold, self.shrink_floor,
-                              self.normal_sigma0, self.normal_spatial_scale)
+                              self.normal_sigma0, self.normal_spatial_scale, self.reduction)
 
 
 @dataclass

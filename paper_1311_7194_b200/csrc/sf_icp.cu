@@ -53,7 +53,7 @@ __device__ __forceinline__ bool last_cta(unsigned int* counter) {
 // solve_gated + apply_motion + convergence (registration.cpp:175-212), one thread.
 // The eigendecomposition of the normal matrix is done before, by one warp (e).
 __device__ __noinline__ void solve_finalize(IcpState* st, const double* s_sum, const Eig6& e,
-                                            const IcpParamsDev& prm) {
+                                            const IcpParamsDev& prm, bool exact_motion = false) {
     const int iter = st->iterations;  // iterations completed before this one
     double b[6];
 #pragma unroll
@@ -91,7 +91,9 @@ __device__ __noinline__ void solve_finalize(IcpState* st, const double* s_sum, c
     const d3 t = sub(mk(x[3], x[4], x[5]), cross(r, c));
     st->motion_r = r;
     st->motion_t = t;
-    st->delta = apply_motion_fast(st->delta, r, t);
+    // apply_motion (pose.cpp:31-43): the reference's SVD route, or its closed form (same polar
+    // factor up to rounding)
+    st->delta = exact_motion ? apply_motion(st->delta, r, t) : apply_motion_fast(st->delta, r, t);
     st->eig_pending = 0;  // eigenpairs computed by this path
     st->iterations = iter + 1;
     if (st->shrunk_norm < prm.eps) st->done = 1;
@@ -528,6 +530,251 @@ __global__ void __launch_bounds__(kIcpThreads, 1)
     }
 }
 
+// ---------------------------------------------------------------------------------
+// Reference-order reduction (sf_match_params.reduction == 1): bit-identical to the
+// reference's icp(). Per iteration three launches:
+//   k_icp_exact_match  association (the same `associate`), matches compacted in row-major
+//                      order: CTA b owns the contiguous pixel range [b * chunk, (b+1) * chunk)
+//                      and appends its matches in pixel order (ballot + CTA prefix); the
+//                      shrink's bounding box (min / max: exact in any order) and the counts;
+//                      the last CTA forms centre / scale (registration.cpp:52-64) or raises
+//                      TrackingLost (registration.cpp:202-204)
+//   k_icp_exact_terms  per match, the shrunk match and the 28 addends of assemble in the
+//                      reference's arithmetic (registration.cpp:65-70, 104-113), stored in
+//                      global match order
+//   k_icp_exact_solve  one warp: lane k runs the reference's Kahan accumulator k over the
+//                      addends in match order (registration.cpp:79-89, 107-113) — the same
+//                      sequence of floating-point operations, so the same sums — then the
+//                      cyclic Jacobi (eigendecompose_sym6_warp, same rotation order), the
+//                      spectral gated solve, unshrink and apply_motion with the SVD polar
+//                      factor (registration.cpp:125-212, pose.cpp:20-43).
+// The Kahan chains are sequential (4 dependent FP64 adds per match and sum), so an iteration
+// costs ~matches x the FP64 add latency; the tree path (default) is the fast one.
+// ---------------------------------------------------------------------------------
+constexpr int kExactCtas = kStepCtas;
+
+__host__ __device__ inline int exact_chunk(int n) {  // pixels per CTA range (multiple of 32)
+    return ((n + kExactCtas - 1) / kExactCtas + 31) & ~31;
+}
+
+template <bool COND>
+__global__ void __launch_bounds__(kIcpThreads, 1)
+    k_icp_exact_match(const float* __restrict__ src, const float* __restrict__ src_n, const float* __restrict__ tgt,
+                      const float* __restrict__ tgt_n, Intr si, Intr ti, IcpParamsDev prm, IcpState* st,
+                      MatchRec* __restrict__ rec, double* __restrict__ part_bbox,
+                      unsigned long long* __restrict__ part_count, unsigned int* counter,
+                      cudaGraphConditionalHandle cond) {
+    if (threadIdx.x == 0 && st->bodies == 0) atomicCAS(&st->t_step0, 0ull, globaltimer_ns());
+    if (st->done) {
+        if constexpr (COND) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0u);
+        }
+        return;
+    }
+    const Pose delta = st->delta;
+    const int n = si.w * si.h;
+    const int chunk = exact_chunk(n);
+    const int begin = blockIdx.x * chunk, end = min(n, begin + chunk);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    constexpr int kWarps = kIcpThreads / 32;
+    __shared__ unsigned int s_wcnt[kWarps];
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    unsigned int base = 0;  // matches this CTA appended so far
+    for (int r0 = begin; r0 < end; r0 += kIcpThreads) {
+        const int i = r0 + tid;
+        d3 p, q, nn;
+        const bool ok = i < end && associate(i, src, src_n, tgt, tgt_n, si, ti, prm, delta, p, q, nn);
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        if (lane == 0) s_wcnt[wid] = __popc(bal);
+        __syncthreads();
+        unsigned int off = base, tot = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const unsigned int c = s_wcnt[w];
+            off += w < wid ? c : 0u;
+            tot += c;
+        }
+        if (ok) {
+            MatchRec m;
+            m.p[0] = p.x, m.p[1] = p.y, m.p[2] = p.z;
+            m.q[0] = q.x, m.q[1] = q.y, m.q[2] = q.z;
+            m.n[0] = nn.x, m.n[1] = nn.y, m.n[2] = nn.z;
+            rec[begin + off + __popc(bal & ((1u << lane) - 1u))] = m;
+            const double pp[3] = {p.x, p.y, p.z}, qq[3] = {q.x, q.y, q.z};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {  // shrink's bounding box (registration.cpp:54-59)
+                lo[a] = dmin(dmin(lo[a], pp[a]), qq[a]);
+                hi[a] = dmax(dmax(hi[a], pp[a]), qq[a]);
+            }
+        }
+        base += tot;
+        __syncthreads();  // s_wcnt reuse
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = dmin(lo[a], __shfl_down_sync(0xffffffffu, lo[a], off));
+            hi[a] = dmax(hi[a], __shfl_down_sync(0xffffffffu, hi[a], off));
+        }
+    __shared__ double s_b[kWarps][6];
+    if (lane == 0)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            s_b[wid][a] = lo[a];
+            s_b[wid][3 + a] = hi[a];
+        }
+    __syncthreads();
+    if (tid == 0) {
+        for (int w = 1; w < kWarps; ++w)
+            for (int a = 0; a < 3; ++a) {
+                s_b[0][a] = dmin(s_b[0][a], s_b[w][a]);
+                s_b[0][3 + a] = dmax(s_b[0][3 + a], s_b[w][3 + a]);
+            }
+        for (int a = 0; a < 6; ++a) part_bbox[blockIdx.x * 6 + a] = s_b[0][a];
+        part_count[blockIdx.x] = base;
+    }
+    if (!last_cta(counter)) return;
+    if (tid == 0) {
+        double b[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        unsigned long long total = 0;
+        for (int c = 0; c < static_cast<int>(gridDim.x); ++c) {
+            for (int a = 0; a < 3; ++a) {
+                b[a] = dmin(b[a], __ldcg(&part_bbox[c * 6 + a]));
+                b[3 + a] = dmax(b[3 + a], __ldcg(&part_bbox[c * 6 + 3 + a]));
+            }
+            total += __ldcg(&part_count[c]);
+        }
+        if (st->bodies == 0) st->t_assoc0 = globaltimer_ns();
+        st->bodies += 1;
+        if (total < 10) {  // TrackingLost (registration.cpp:202-204)
+            st->lost = 1;
+            st->lost_count = total;
+            st->done = 1;
+            if constexpr (COND) cudaGraphSetConditional(cond, 0u);
+        } else {
+            st->matches = total;
+            st->cur_count = total;
+            // shrink centre / scale (registration.cpp:60-63)
+            const d3 l = mk(b[0], b[1], b[2]), hh = mk(b[3], b[4], b[5]);
+            const d3 ext = sub(hh, l);
+            const d3 sc = mk(dmax(ext.x, prm.floor), dmax(ext.y, prm.floor), dmax(ext.z, prm.floor));
+            st->center = scale(0.5, add(l, hh));
+            st->scale = sc;
+            st->inv_scale = mk(1.0 / sc.x, 1.0 / sc.y, 1.0 / sc.z);
+        }
+        *counter = 0;
+    }
+}
+
+// The 28 addends of assemble for every match, in global match order (CTA ranges in order).
+__global__ void __launch_bounds__(kIcpThreads)
+    k_icp_exact_terms(const IcpState* __restrict__ st, const MatchRec* __restrict__ rec,
+                      const unsigned long long* __restrict__ part_count, int n, double* __restrict__ terms) {
+    if (st->done) return;
+    const int b = blockIdx.x;
+    const unsigned long long cnt = part_count[b];
+    __shared__ unsigned long long s_off;
+    if (threadIdx.x < 32) {  // matches of the ranges before this one
+        unsigned long long o = 0;
+        for (int c = threadIdx.x; c < b; c += 32) o += part_count[c];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) o += __shfl_down_sync(0xffffffffu, o, off);
+        if (threadIdx.x == 0) s_off = o;
+    }
+    __syncthreads();
+    const d3 c = st->center, s = st->scale, inv = st->inv_scale;
+    const MatchRec* r = rec + static_cast<size_t>(b) * exact_chunk(n);
+    double* out = terms + s_off * kSums;
+    for (unsigned long long j = threadIdx.x; j < cnt; j += blockDim.x) {
+        const MatchRec m = r[j];
+        const d3 p = mk(m.p[0], m.p[1], m.p[2]), q = mk(m.q[0], m.q[1], m.q[2]), nn = mk(m.n[0], m.n[1], m.n[2]);
+        // ShrunkMatch (registration.cpp:65-69)
+        const d3 ph = cmul(inv, sub(p, c)), qh = cmul(inv, sub(q, c));
+        const d3 ch = cmul(inv, sub(cross(p, nn), cross(c, nn)));
+        // assemble's row and residual (registration.cpp:104-106)
+        const double row[6] = {ch.x, ch.y, ch.z, nn.x, nn.y, nn.z};
+        const double d = dot(cmul(s, sub(ph, qh)), nn);
+        double* t = out + j * kSums;
+        int k = 0;
+#pragma unroll
+        for (int a = 0; a < 6; ++a)
+#pragma unroll
+            for (int bb = a; bb < 6; ++bb, ++k) t[k] = row[a] * row[bb];
+#pragma unroll
+        for (int a = 0; a < 6; ++a) t[21 + a] = -row[a] * d;
+        t[27] = d * d;
+    }
+}
+
+// The reference's Compensated::add (registration.cpp:79-89).
+__device__ __forceinline__ void kahan_add(double& sum, double& carry, double value) {
+    const double y = value - carry;
+    const double t = sum + y;
+    carry = (t - sum) - y;
+    sum = t;
+}
+
+template <bool COND>
+__global__ void __launch_bounds__(32, 1)
+    k_icp_exact_solve(IcpState* st, const double* __restrict__ terms, IcpParamsDev prm,
+                      cudaGraphConditionalHandle cond) {
+    const int lane = threadIdx.x;
+    if (st->done) {  // lost in this iteration's match (or earlier)
+        if constexpr (COND) {
+            if (lane == 0) cudaGraphSetConditional(cond, 0u);
+        }
+        return;
+    }
+    const unsigned long long total = st->cur_count;
+    double sum = 0.0, carry = 0.0;
+    if (lane < kSums) {
+        constexpr int kAhead = 8;  // loads in flight ahead of the dependent chain
+        unsigned long long m = 0;
+        for (; m + kAhead <= total; m += kAhead) {
+            double x[kAhead];
+#pragma unroll
+            for (int u = 0; u < kAhead; ++u) x[u] = __ldcg(&terms[(m + u) * kSums + lane]);
+#pragma unroll
+            for (int u = 0; u < kAhead; ++u) kahan_add(sum, carry, x[u]);
+        }
+        for (; m < total; ++m) kahan_add(sum, carry, __ldcg(&terms[m * kSums + lane]));
+    }
+    __shared__ double s_sum[kSums];
+    __shared__ double s_A[36];
+    __shared__ Eig6 s_eig;
+    if (lane < kSums) s_sum[lane] = sum;
+    __syncwarp();
+    for (int i = lane; i < 36; i += 32) {  // eq.A from the upper-triangle sums (registration.cpp:115-120)
+        const int r = i / 6, cc = i % 6;
+        s_A[i] = s_sum[r <= cc ? packed_index(r, cc) : packed_index(cc, r)];
+    }
+    __syncwarp();
+    eigendecompose_sym6_warp(s_A, &s_eig);
+    __syncwarp();
+    if (lane == 0) {
+        solve_finalize(st, s_sum, s_eig, prm, true);
+        st->t_end = globaltimer_ns();
+        if constexpr (COND)
+            cudaGraphSetConditional(cond, (!st->done && st->iterations < prm.max_iterations) ? 1u : 0u);
+    }
+}
+
+// One reference-order iteration: the three launches (eager, or inside a capture).
+template <bool COND>
+static void issue_exact_iteration(IcpWork& wk, const float* src, const float* src_n, const float* tgt,
+                                  const float* tgt_n, const Intr& si, const Intr& ti, const IcpParamsDev& prm,
+                                  cudaStream_t s, cudaGraphConditionalHandle cond) {
+    const int n = si.w * si.h;
+    k_icp_exact_match<COND><<<kExactCtas, kIcpThreads, 0, s>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st, wk.rec,
+                                                                wk.part_bbox, wk.part_count, wk.counters + 1, cond);
+    SF_LAUNCH_CHECK();
+    k_icp_exact_terms<<<kExactCtas, kIcpThreads, 0, s>>>(wk.st, wk.rec, wk.part_count, n, wk.terms);
+    SF_LAUNCH_CHECK();
+    k_icp_exact_solve<COND><<<1, 32, 0, s>>>(wk.st, wk.terms, prm, cond);
+    SF_LAUNCH_CHECK();
+}
+
 IcpParamsDev make_icp_params(const sf_match_params& p) {
     IcpParamsDev d;
     d.cos_max = std::cos(p.max_normal_angle);          // registration.cpp:25
@@ -536,6 +783,7 @@ IcpParamsDev make_icp_params(const sf_match_params& p) {
     d.theta = p.eigen_threshold;
     d.floor = p.shrink_floor;
     d.max_iterations = p.max_iterations;
+    d.exact = p.reduction == 1 ? 1 : 0;
     return d;
 }
 
@@ -562,6 +810,7 @@ void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* 
     }();
     const bool loop = loop_enabled && cs == cudaStreamCaptureStatusActive && prm.max_iterations > 0;
     if (device_loop) *device_loop = loop;
+    if (prm.exact) wk.ensure_exact();
     if (!loop) {
         uint64_t cnt = 0;
         if (!state_ready) {
@@ -570,6 +819,11 @@ void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* 
             cnt = 1;
         }
         for (int it = 0; it < prm.max_iterations; ++it) {
+            if (prm.exact) {
+                issue_exact_iteration<false>(wk, src, src_n, tgt, tgt_n, si, ti, prm, s, 0);
+                cnt += 3;
+                continue;
+            }
             k_icp_step<false><<<kStepCtas, kIcpThreads, kStepSmem, s>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st,
                                                                         wk.part_bbox, wk.part_count, wk.part,
                                                                         wk.counters, 0);
@@ -586,9 +840,12 @@ void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* 
     if (state_ready) {
         // first iteration as a plain node: it sets the condition for the loop of the others
         // (the loop-entry latency of the conditional node is paid only by multi-iteration frames)
-        k_icp_step<true><<<kStepCtas, kIcpThreads, kStepSmem, s>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st,
-                                                                   wk.part_bbox, wk.part_count, wk.part, wk.counters,
-                                                                   cond);
+        if (prm.exact)
+            issue_exact_iteration<true>(wk, src, src_n, tgt, tgt_n, si, ti, prm, s, cond);
+        else
+            k_icp_step<true><<<kStepCtas, kIcpThreads, kStepSmem, s>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st,
+                                                                       wk.part_bbox, wk.part_count, wk.part,
+                                                                       wk.counters, cond);
     } else {
         k_icp_init<true><<<1, 1, 0, s>>>(wk.st, d_initial, dead, prm.max_iterations, cond);
         if (launches) *launches += 1;
@@ -608,9 +865,19 @@ void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* 
     if (!wk.body_stream) SF_CUDA(cudaStreamCreateWithFlags(&wk.body_stream, cudaStreamNonBlocking));
     cudaStream_t bs = wk.body_stream;
     SF_CUDA(cudaStreamBeginCaptureToGraph(bs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    k_icp_step<true><<<kStepCtas, kIcpThreads, kStepSmem, bs>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st,
-                                                                wk.part_bbox, wk.part_count, wk.part, wk.counters,
-                                                                cond);
+    if (prm.exact) {
+        try {
+            issue_exact_iteration<true>(wk, src, src_n, tgt, tgt_n, si, ti, prm, bs, cond);
+        } catch (...) {
+            cudaGraph_t g2 = nullptr;
+            cudaStreamEndCapture(bs, &g2);
+            throw;
+        }
+    } else {
+        k_icp_step<true><<<kStepCtas, kIcpThreads, kStepSmem, bs>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st,
+                                                                    wk.part_bbox, wk.part_count, wk.part,
+                                                                    wk.counters, cond);
+    }
     const cudaError_t le = cudaGetLastError();
     cudaGraph_t captured = nullptr;
     const cudaError_t ee = cudaStreamEndCapture(bs, &captured);

@@ -55,6 +55,12 @@ struct IcpState {
 struct IcpParamsDev {
     double max_dist_sq, cos_max, eps, theta, floor;
     int max_iterations;
+    int exact;  // sf_match_params.reduction == 1: the reference's summation order
+};
+
+// One correspondence of match_points (registration.hpp PointMatch), reference-order path.
+struct MatchRec {
+    double p[3], q[3], n[3];
 };
 
 // Scratch for one ICP (owned by the caller: stand-alone API or tracker).
@@ -68,6 +74,16 @@ struct IcpWork {
     float *src = nullptr, *tgt = nullptr, *tgt_n = nullptr, *src_n_in = nullptr;
     double* initial = nullptr;
     unsigned int* counters = nullptr;  // "last CTA" tickets of the two fused reductions
+    // reference-order reduction (allocated on first use): row-major-compacted matches per
+    // CTA range, and the 28 per-match terms in match order
+    MatchRec* rec = nullptr;
+    double* terms = nullptr;
+    void ensure_exact() {
+        if (rec) return;
+        const size_t n = static_cast<size_t>(w) * h;
+        SF_CUDA(cudaMalloc(&rec, n * sizeof(MatchRec)));
+        SF_CUDA(cudaMalloc(&terms, n * kSums * sizeof(double)));
+    }
     void ensure(int W, int H) {
         if (W == w && H == h && st) return;
         release();
@@ -89,9 +105,11 @@ struct IcpWork {
     }
     void release() {
         void* p[] = {part_bbox, part_count, part, st, src_normals, src, tgt, tgt_n, src_n_in, initial,
-                     counters};
+                     counters, rec, terms};
         for (void* q : p)
             if (q) cudaFree(q);
+        rec = nullptr;
+        terms = nullptr;
         counters = nullptr;
         part_bbox = nullptr;
         part_count = nullptr;

@@ -29,7 +29,16 @@ struct TrackerDev {
     int status;
     int registered;
     int frame;
+    int died_at;  // frame whose TrackingLost / PoolExhausted set `dead` (-1: none)
+    int pad_;
 };
+
+// run()'s catch blocks end the loop at the failing frame (pipeline.cpp:289-299).
+__device__ __forceinline__ void mark_dead(TrackerDev* td, int status) {
+    td->dead = 1;
+    td->status = status;
+    td->died_at = td->frame;
+}
 
 // Everything a frame's metrics are decoded from (host side: pinned, mapped).
 struct TrackerFetch {
@@ -90,7 +99,7 @@ __device__ inline void finish_snapshot(const SnapTargets& st, TrackerDev* td, co
 }
 
 __global__ void k_tracker_begin_track(const double* __restrict__ cur, const double* __restrict__ external,
-                                      double* __restrict__ init_delta, RayCounters* rstats, const TrackerDev* td) {
+                                      double* __restrict__ init_delta, RayCounters* rstats, TrackerDev* td) {
     if (td->dead) return;
     // initial_pose = initial_transform_hook(current, external) = external ? compose(current,
     // *external) : current (registration.cpp:222-224); initial_delta = compose(invert(current),
@@ -101,14 +110,14 @@ __global__ void k_tracker_begin_track(const double* __restrict__ cur, const doub
     pose_to12(d, init_delta);
     RayCounters z{0, 0, 0, 0};
     *rstats = z;
+    td->registered = 0;  // set again once ICP succeeds (pipeline.cpp:274)
 }
 
 __global__ void k_tracker_after_icp(double* __restrict__ cur, double* __restrict__ fuse_pose, const IcpState* st,
                                     TrackerDev* td, int orthonormalize) {
     if (td->dead) return;
     if (st->lost) {
-        td->dead = 1;
-        td->status = SF_TRACKING_LOST;
+        mark_dead(td, SF_TRACKING_LOST);
         return;
     }
     Pose est = compose(pose_from12(cur), st->delta);  // pipeline.cpp:282
@@ -121,7 +130,7 @@ __global__ void k_tracker_after_icp(double* __restrict__ cur, double* __restrict
 // One warp: begin_track (lane 0) and the raycast's frame constants at the current pose.
 __global__ void k_tracker_begin_track_consts(VolParams P, Intr cam, const double* __restrict__ cur,
                                              const double* __restrict__ external, double* __restrict__ init_delta,
-                                             RayCounters* rstats, const TrackerDev* td, FrameConsts* fc,
+                                             RayCounters* rstats, TrackerDev* td, FrameConsts* fc,
                                              IcpState* icp) {
     if (threadIdx.x == 0) {
         if (!td->dead) {
@@ -130,6 +139,7 @@ __global__ void k_tracker_begin_track_consts(VolParams P, Intr cam, const double
             pose_to12(compose(invert(c), init), init_delta);
             RayCounters z{0, 0, 0, 0};
             *rstats = z;
+            td->registered = 0;  // set again once ICP succeeds (pipeline.cpp:274)
         }
         icp_state_init(icp, init_delta, td->dead != 0);  // the frame's ICP starts from init_delta
     }
@@ -143,8 +153,7 @@ __global__ void k_tracker_after_icp_fuse_begin(double* __restrict__ cur, double*
                                                Intr cam, FrameConsts* fc, FrameCounters* ctr, const VolCounters* vc) {
     if (threadIdx.x == 0 && !td->dead) {
         if (st->lost) {
-            td->dead = 1;
-            td->status = SF_TRACKING_LOST;
+            mark_dead(td, SF_TRACKING_LOST);
         } else {
             Pose est = compose(pose_from12(cur), st->delta);  // pipeline.cpp:282
             if (orthonormalize) est.R = nearest_rotation(est.R);
@@ -162,10 +171,7 @@ __global__ void k_tracker_after_icp_fuse_begin(double* __restrict__ cur, double*
 __global__ void k_tracker_fuse_finish(FrameCounters* ctr, const VolCounters* vc, TrackerDev* td, SnapTargets snap) {
     if (threadIdx.x == 0) {
         fuse_finalize_body(ctr, vc);
-        if (!td->dead && ctr->exhausted) {
-            td->dead = 1;
-            td->status = SF_POOL_EXHAUSTED;
-        }
+        if (!td->dead && ctr->exhausted) mark_dead(td, SF_POOL_EXHAUSTED);
     }
     finish_snapshot(snap, td, ctr);
 }
@@ -183,10 +189,7 @@ __global__ void k_tracker_begin_gt(const double* __restrict__ gt, double* __rest
 }
 
 __global__ void k_tracker_finish(const FrameCounters* ctr, TrackerDev* td, SnapTargets snap) {
-    if (threadIdx.x == 0 && !td->dead && ctr->exhausted) {
-        td->dead = 1;
-        td->status = SF_POOL_EXHAUSTED;
-    }
+    if (threadIdx.x == 0 && !td->dead && ctr->exhausted) mark_dead(td, SF_POOL_EXHAUSTED);
     finish_snapshot(snap, td, ctr);
 }
 
@@ -418,6 +421,7 @@ int sf_tracker_create(sf_volume_t vol, const sf_tracker_config* config, const do
         if (w <= 0 || h <= 0) throw Error(SF_INVALID_ARGUMENT, "intrinsics: non-positive image size");
         ensure_frame_buffers(*vol, t->fb, w, h);
         t->icp.ensure(w, h);
+        if (t->icp_prm.exact) t->icp.ensure_exact();  // not allowed later, inside the graph capture
         const size_t n = static_cast<size_t>(w) * h;
         SF_CUDA(cudaMalloc(&t->d_cur, 12 * sizeof(double)));
         SF_CUDA(cudaMalloc(&t->d_init_delta, 12 * sizeof(double)));
@@ -434,7 +438,8 @@ int sf_tracker_create(sf_volume_t vol, const sf_tracker_config* config, const do
         SF_CUDA(cudaMalloc(&t->d_brackets, n * sizeof(RayBracket)));
 
         SF_CUDA(cudaMalloc(&t->d_td, sizeof(TrackerDev)));
-        SF_CUDA(cudaMemset(t->d_td, 0, sizeof(TrackerDev)));
+        const TrackerDev td0{0, 0, 0, 0, -1, 0};
+        SF_CUDA(cudaMemcpy(t->d_td, &td0, sizeof(TrackerDev), cudaMemcpyHostToDevice));
         SF_CUDA(cudaMemset(t->d_rstats, 0, sizeof(RayCounters)));
         SF_CUDA(cudaMemcpy(t->d_cur, initial_pose, 12 * sizeof(double), cudaMemcpyHostToDevice));
         SF_CUDA(cudaMallocHost(&t->h, sizeof(sf_tracker::Fetch)));
@@ -557,8 +562,8 @@ int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, con
 
 int sf_tracker_set_pose(sf_tracker_t tr, const double pose[12], void* stream) {
     return guarded([&]() -> int {
-        SF_CUDA(cudaSetDevice(tr->vol->device));
         if (!tr || !pose) throw Error(SF_INVALID_ARGUMENT, "sf_tracker_set_pose: null argument");
+        SF_CUDA(cudaSetDevice(tr->vol->device));
         Pose12 g;
         for (int i = 0; i < 12; ++i) g.v[i] = pose[i];
         k_set_pose12<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(tr->d_cur, g);
@@ -574,6 +579,16 @@ void sf_tracker::decode(const Fetch* f, int frame, int mode, uint64_t launches, 
     out->status = f->td.status;
     out->registered = (mode == 0 || mode == 3) ? f->td.registered : 0;
     std::memcpy(out->pose, f->fuse_pose, sizeof(out->pose));
+    // The frame that ended the run carries what run()'s catch block pushes (pipeline.cpp:289-299):
+    // TrackingLost -> not registered, default (identity) estimated pose, no fusion stats;
+    // PoolExhausted -> the registration, but default FusionStats (fuse_frame threw).
+    const bool died_here = f->td.dead && f->td.died_at == frame;
+    const bool lost_here = died_here && f->td.status == SF_TRACKING_LOST;
+    const bool exhausted_here = died_here && f->td.status == SF_POOL_EXHAUSTED;
+    if (lost_here) {
+        out->registered = 0;
+        for (int i = 0; i < 12; ++i) out->pose[i] = (i == 0 || i == 4 || i == 8) ? 1.0 : 0.0;
+    }
     if (out->registered) {
         out->iterations = f->icp.iterations;
         out->matches = f->icp.matches;
@@ -584,10 +599,12 @@ void sf_tracker::decode(const Fetch* f, int frame, int mode, uint64_t launches, 
         }
     }
     const uint64_t nn = vol->P.N, m = vol->P.M;
-    out->fusion.voxels_updated = f->ctr.voxels_updated;
-    out->fusion.blocks_allocated_now = f->ctr.alloc_now - f->ctr.alloc_before;
-    out->fusion.blocks_total = f->ctr.alloc_now;
-    out->fusion.memory_bytes = 2ull * f->ctr.alloc_now * m * m * m + 4ull * nn * nn * nn;
+    if (!lost_here && !exhausted_here) {
+        out->fusion.voxels_updated = f->ctr.voxels_updated;
+        out->fusion.blocks_allocated_now = f->ctr.alloc_now - f->ctr.alloc_before;
+        out->fusion.blocks_total = f->ctr.alloc_now;
+        out->fusion.memory_bytes = 2ull * f->ctr.alloc_now * m * m * m + 4ull * nn * nn * nn;
+    }
     out->raycast.sample_steps = f->rs.sample_steps;
     out->raycast.hit_pixels = f->rs.hit_pixels;
     out->raycast.rays_with_bounds = f->rs.rays_with_bounds;
@@ -599,11 +616,13 @@ void sf_tracker::decode(const Fetch* f, int frame, int mode, uint64_t launches, 
     out->icp_ns = f->icp.t_step0 && f->icp.t_end > f->icp.t_step0 ? f->icp.t_end - f->icp.t_step0 : 0;
     out->icp_steps = f->icp.bodies;
     out->kernel_launches = launches;
-    if (icp_loop) out->kernel_launches += static_cast<uint64_t>(f->icp.bodies);
+    // device-side ICP loop: one launch per iteration body (three in the reference-order mode)
+    if (icp_loop) out->kernel_launches += static_cast<uint64_t>(f->icp.bodies) * (icp_prm.exact ? 3u : 1u);
 }
 
 int sf_tracker_fetch(sf_tracker_t tr, sf_frame_metrics* out, void* stream) {
     return guarded([&]() -> int {
+        if (!tr || !out) throw Error(SF_INVALID_ARGUMENT, "sf_tracker_fetch: null argument");
         SF_CUDA(cudaSetDevice(tr->vol->device));
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         tr->copy_metrics(tr->h, s);
@@ -622,6 +641,10 @@ int sf_tracker_fetch_frame(sf_tracker_t tr, int32_t frame, sf_frame_metrics* out
         const int slot = frame & 1;
         const auto& mt = tr->snap_meta[slot];
         SF_CUDA(cudaEventSynchronize(tr->ev_snap[slot]));
+        // the device picked the snapshot slot by its own frame counter: it must be this frame's
+        if (mt.frame != frame || tr->snap[slot].td.frame != frame)
+            throw Error(SF_LOGIC_ERROR, "sf_tracker_fetch_frame: snapshot slot holds another frame "
+                                        "(a step failed after its launch)");
         tr->decode(&tr->snap[slot], mt.frame, mt.mode, mt.launches, mt.icp_loop, out);
         return SF_OK;
     });
@@ -629,6 +652,7 @@ int sf_tracker_fetch_frame(sf_tracker_t tr, int32_t frame, sf_frame_metrics* out
 
 int sf_tracker_stage_times(sf_tracker_t tr, float ms[5]) {
     return guarded([&]() -> int {
+        if (!tr || !ms) throw Error(SF_INVALID_ARGUMENT, "sf_tracker_stage_times: null argument");
         const int pairs[5][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {0, 5}};
         for (int i = 0; i < 5; ++i) {
             const bool have = tr->stage_events == 2 || (tr->stage_events == 1 && i == 3);
@@ -656,21 +680,30 @@ int sf_tracker_set_stage_timing(sf_tracker_t tr, int32_t level) {
 }
 
 int sf_tracker_device_pose(sf_tracker_t tr, const double** device_pose) {
-    *device_pose = tr->d_cur;
-    return SF_OK;
+    return guarded([&]() -> int {
+        if (!tr || !device_pose) throw Error(SF_INVALID_ARGUMENT, "sf_tracker_device_pose: null argument");
+        *device_pose = tr->d_cur;
+        return SF_OK;
+    });
 }
 
 int sf_tracker_io_bytes(sf_tracker_t tr, int32_t has_sigma, uint64_t* h2d, uint64_t* d2h) {
-    const uint64_t n = static_cast<uint64_t>(tr->cam.w) * tr->cam.h;
-    *h2d = n * sizeof(float) * (has_sigma ? 2 : 1);
-    using F = sf_tracker::Fetch;  // the per-frame metric snapshot read back by fetch
-    *d2h = sizeof(F::cur) + sizeof(F::fuse_pose) + sizeof(F::td) + sizeof(F::ctr) + sizeof(F::rs) + sizeof(F::icp);
-    return SF_OK;
+    return guarded([&]() -> int {
+        if (!tr || !h2d || !d2h) throw Error(SF_INVALID_ARGUMENT, "sf_tracker_io_bytes: null argument");
+        const uint64_t n = static_cast<uint64_t>(tr->cam.w) * tr->cam.h;
+        *h2d = n * sizeof(float) * (has_sigma ? 2 : 1);
+        using F = sf_tracker::Fetch;  // the per-frame metric snapshot read back by fetch
+        *d2h = sizeof(F::cur) + sizeof(F::fuse_pose) + sizeof(F::td) + sizeof(F::ctr) + sizeof(F::rs) + sizeof(F::icp);
+        return SF_OK;
+    });
 }
 
 int sf_tracker_last_launch_count(sf_tracker_t tr, uint64_t* count) {
-    *count = tr->last_launches;
-    return SF_OK;
+    return guarded([&]() -> int {
+        if (!tr || !count) throw Error(SF_INVALID_ARGUMENT, "sf_tracker_last_launch_count: null argument");
+        *count = tr->last_launches;
+        return SF_OK;
+    });
 }
 
 }  // extern "C"

@@ -388,6 +388,30 @@ def test_icp_against_raycast_model(gpu, oracle):
     assert pose_diff(a.delta, b.delta) < POSE_TOL
 
 
+def test_icp_reference_order_bit_identical(gpu, ref):
+    """MatchParams.reduction = REFERENCE_ORDER: the same delta pose, eigenpairs, gated mask,
+    residual and counts as the reference's icp(), bit for bit (sequential Kahan sums in match
+    order, cyclic Jacobi, spectral gated solve, SVD apply_motion)."""
+    intr = scenes.camera(320, 240, 262.5)
+    poses = scenes.c1_trajectory(100)[:12:3]
+    cfg = scenes.c1_config()
+    g, r = fused_pair(gpu, ref, cfg, intr, poses[:3], scenes.sphere_plane_scene(), 2.0)
+    src = gpu.render_synthetic_depth(scenes.sphere_plane_scene(), poses[3], intr, sigma0=2.5e-4, seed=9,
+                                     domain_size=2.0)
+    d, n, _ = ref.raycast(r, poses[2], intr)
+    match = sf.MatchParams.for_voxel_size(cfg.voxel_size)
+    match.reduction = sf.MatchParams.REFERENCE_ORDER
+    for init in (sf.Pose.identity(), sf.compose(sf.invert(poses[2]), poses[3])):
+        a = gpu.icp(src, d, n, init, match)
+        b = ref.icp(src, d, n, init, match)
+        assert a.iterations == b.iterations and a.matches == b.matches and a.iterations >= 2
+        assert np.array_equal(a.delta.to12(), b.delta.to12())
+        assert a.residual_rms == b.residual_rms and a.shrunk_motion_norm == b.shrunk_motion_norm
+        assert a.eigenvalues == b.eigenvalues and a.gated_mask == b.gated_mask
+        assert np.array_equal(a.eigenvectors, b.eigenvectors)
+        assert np.array_equal(a.motion_r, b.motion_r) and np.array_equal(a.motion_t, b.motion_t)
+
+
 def test_icp_tracking_lost(gpu, oracle):
     intr = scenes.camera(64, 48, 55.0)
     empty = sf.DepthFrame(intr, np.zeros((48, 64), np.float32))
@@ -436,6 +460,80 @@ def test_tracker_matches_reference_pipeline(gpu, oracle, hook):
     assert (g.read_payload() == r.read_payload()).mean() > 0.9999
     assert tr.last_launch_count() > 10
     assert tr.fetch().kernel_launches > tr.last_launch_count()  # + the device-side ICP iterations
+
+
+def reference_run(oracle, r, frames, intr, fusion, match, pose0):
+    """run()'s loop incl. its catch blocks (pipeline.cpp:233-301) over the oracle: the
+    FrameMetrics it pushes, as (status, registered, pose, fusion stats, iterations)."""
+    cur, out = pose0, []
+    for k, f in enumerate(frames):
+        fm = dict(status=0, registered=False, pose=sf.Pose.identity(), fusion=sf.FusionStats(0, 0, 0, 0), it=0)
+        try:
+            if k == 0:
+                fm["pose"] = cur
+            else:
+                d, n, _ = oracle.raycast(r, cur, intr)
+                res = oracle.icp(f, d, n, sf.compose(sf.invert(cur), cur), match)
+                fm.update(registered=True, it=res.iterations)
+                cur = sf.compose(cur, res.delta)
+                fm["pose"] = cur
+            fm["fusion"] = oracle.fuse_frame(r, f, fm["pose"], fusion)
+        except sf.TrackingLost:
+            fm["status"] = 5
+            out.append(fm)
+            break
+        except sf.PoolExhausted:
+            fm["status"] = 4
+            out.append(fm)
+            break
+        out.append(fm)
+    return out
+
+
+@pytest.mark.parametrize("failure", ["tracking_lost", "pool_exhausted"])
+def test_tracker_failure_frame_matches_reference_run(gpu, oracle, failure):
+    """The frame that raises TrackingLost / PoolExhausted reports what run()'s catch block
+    pushes (pipeline.cpp:289-299): TrackingLost -> not registered, identity pose, default
+    FusionStats; PoolExhausted -> the registration and pose, default FusionStats; the volume is
+    the reference's partial state; later steps are no-ops with the same status."""
+    intr = scenes.camera(160, 120, 131.25)
+    poses = scenes.c1_trajectory(100)[:5]
+    frames = [gpu.render_synthetic_depth(scenes.sphere_plane_scene(), p, intr, domain_size=2.0) for p in poses]
+    cfg = scenes.c1_config()
+    fusion = sf.FusionParams(mode=sf.FusionMode.Kalman)
+    match = sf.MatchParams.for_voxel_size(cfg.voxel_size)
+    cap = 0
+    if failure == "tracking_lost":
+        frames[3] = sf.DepthFrame(intr, np.zeros((120, 160), np.float32))  # < 10 matches
+    else:
+        # a pool that holds frames 0..k-1 and half of frame k's new blocks (k >= 2)
+        _, r0 = grids(gpu, oracle, cfg, 0, sf.AuxMode.Variance)
+        tot = [fm["fusion"].blocks_total for fm in reference_run(oracle, r0, frames, intr, fusion, match, poses[0])]
+        k = next(k for k in range(2, len(tot)) if tot[k] - tot[k - 1] >= 2)
+        cap = tot[k - 1] + (tot[k] - tot[k - 1]) // 2
+    g, r = grids(gpu, oracle, cfg, cap, sf.AuxMode.Variance)
+    ref = reference_run(oracle, r, frames, intr, fusion, match, poses[0])
+    assert ref[-1]["status"] == (5 if failure == "tracking_lost" else 4)
+    die = len(ref) - 1
+    assert die >= 2
+    tr = sf.Tracker(g, intr, fusion, match, poses[0])
+    for k, f in enumerate(frames):
+        tr.step(f, sf.Tracker.TRACK)
+        m = tr.fetch()
+        if k < die:
+            assert m.status == 0 and m.fusion == ref[k]["fusion"]
+            assert pose_diff(m.pose, ref[k]["pose"]) < POSE_TOL
+            continue
+        assert m.status == ref[die]["status"]
+        if k == die:
+            assert m.registered == ref[die]["registered"]
+            assert m.fusion == ref[die]["fusion"] == sf.FusionStats(0, 0, 0, 0)
+            assert pose_diff(m.pose, ref[die]["pose"]) < POSE_TOL
+            if not m.registered:
+                assert m.iterations == 0 and m.matches == 0
+            else:
+                assert m.iterations == ref[die]["it"]
+    assert_same_volume(g, r)
 
 
 def test_reference_pose_chain_instability_and_fix(gpu):
