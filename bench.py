@@ -491,6 +491,47 @@ def run_ours(args, world, rank, local):
             t = json.load(f)
         traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
 
+    def integrate_only(layout):
+        """Ground-truth poses (the integrate-only configuration of BASELINE configs[0], at C4):
+        per step one fuse_frame through the tracker (no raycast / ICP), the integrate kernel
+        timed by its in-graph event pair, L2 flushed between steps."""
+        g = sf.SparseTsdfGrid(grid_cfg, c["pool"], sf.AuxMode.Variance, p_min=c["p_min"], device=local)
+        g.set_payload_layout(layout)
+        tr = sf.Tracker(g, intr, fusion, match, poses[0])
+        tr.set_stage_timing(1)
+        GT = sf.Tracker.GROUND_TRUTH
+        for k in range(0, 1 + args.warmup):
+            tr.step(dframes[k], GT, poses[k], stream=sp)
+        tr.fetch(stream=sp)
+        kern_ms, ms_ = [], []
+        for i in range(steps):
+            k = 1 + args.warmup + i
+            flush.fill_(i & 0xFF)
+            tr.step(dframes[k], GT, poses[k], stream=sp)
+            ms_.append(tr.fetch(stream=sp))
+            kern_ms.append(tr.stage_times()[3])
+        if any(mm.status for mm in ms_):
+            raise RuntimeError(f"integrate-only run failed: {[mm.status for mm in ms_]}")
+        return g, ms_, kern_ms
+
+    def integrate_roofline(ms_, kern_ms, bytes_per_voxel, kernel):
+        b = [mm.blocks_processed * (m3 * bytes_per_voxel + 8) + px * 8 for mm in ms_]
+        ach = sum(b) / (sum(kern_ms) * 1e-3) / 1e9
+        return {"bound": "hbm", "kernel": kernel, "achieved": ach, "peak": peak, "peak_kind": peak_kind,
+                "unit": "GB/s", "frac": ach / peak, "bytes_per_launch_mean": sum(b) / steps,
+                "ms_per_launch_mean": sum(kern_ms) / steps,
+                "kernel_span_ms_mean": sum(mm.integrate_ns for mm in ms_) / steps * 1e-6,
+                "blocks_processed_mean": sum(mm.blocks_processed for mm in ms_) / steps,
+                "voxel_updates_per_s": sum(mm.fusion.voxels_updated for mm in ms_) / (sum(kern_ms) * 1e-3),
+                "exact_fallback_frac": sum(mm.exact_voxels for mm in ms_) /
+                max(1, sum(mm.blocks_processed for mm in ms_) * m3)}
+
+    # P2 layout (float2 {tsdf, variance} per voxel, north star (2)): 16 B per voxel read + written
+    g_f2, ms_f2, kern_f2 = integrate_only(sf.SparseTsdfGrid.FLOAT2)
+    g_p1, ms_p1, kern_p1 = integrate_only(sf.SparseTsdfGrid.CODES)
+    same_blocks = bool(np.array_equal(g_f2.read_table(), g_p1.read_table()))
+    del g_f2, g_p1
+
     # ICP stage (association is L2/HBM-bound: 32 B per pixel per iteration, SURVEY.md §8d):
     # source depth + normals (16 B) and the projected target depth + normals (16 B)
     icp_ms = [s[1] for s in stage]
@@ -573,6 +614,15 @@ def run_ours(args, world, rank, local):
                      "bytes_per_launch_mean": sum(integ_bytes) / steps,
                      "ms_per_launch_mean": sum(integ_ms) / steps,
                      "kernel_span_ms_mean": sum(mm.integrate_ns for mm in metrics) / steps * 1e-6},
+        "integrate_only": {
+            "workload": "C4 frames fused at their ground-truth poses (integrate-only, BASELINE configs[0] style); "
+                        "same frames, fresh volumes",
+            "float2_payload": integrate_roofline(ms_f2, kern_f2, 16, "k_integrate_rows<Kalman, M=8, float2>"),
+            "codes_payload": integrate_roofline(ms_p1, kern_p1, 4, "k_integrate_rows<Kalman, M=8, codes>"),
+            "same_block_tables": same_blocks,
+            "algorithmic_bytes": "per processed block M^3 x (read + write) of the payload (float2: 8 + 8 B, codes: "
+                                 "2 + 2 B per voxel) + its 8 B work item; per launch the 8 B/pixel {depth, p_k} table",
+        },
         "icp_roofline": {"bound": "hbm", "stage": "ICP (source normals + k_icp_step iterations)",
                          "achieved": icp_achieved, "peak": peak, "unit": "GB/s",
                          "frac": icp_achieved / peak if icp_achieved else None,

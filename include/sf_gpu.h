@@ -247,6 +247,24 @@ int sf_volume_load_snapshot(const char* path, uint64_t pool_capacity, int32_t de
  * sf_integrate alongside the quantized codes and used as the prior (fusion.cpp:313-318).
  * Unlike the reference shadow it is block-sparse, so any N is allowed. */
 int sf_volume_enable_float_payload(sf_volume_t vol);
+
+/* Payload layouts:
+ *   SF_PAYLOAD_CODES (default)        P1: the reference's 2-byte {int8 tsdf, uint8 aux} codes.
+ *   SF_PAYLOAD_CODES_FLOAT_SHADOW     P1 + the float shadow above (sf_volume_enable_float_payload).
+ *   SF_PAYLOAD_FLOAT2                 P2: float2 {tsdf, aux} per voxel ONLY, block-sparse, with
+ *                                     FloatShadowGrid semantics (chi = +inf / aux 0, the prior is
+ *                                     the float value, fusion.cpp:313-318, 357-361). Decisions
+ *                                     (pixel, band, chi cut) are the reference's; values are within
+ *                                     the north-star 1e-5. Set on an empty volume. The quantized
+ *                                     codes are not maintained: raycast, marching cubes, voxel and
+ *                                     payload-code access and snapshots return SF_UNSUPPORTED. */
+typedef enum {
+    SF_PAYLOAD_CODES = 0,
+    SF_PAYLOAD_CODES_FLOAT_SHADOW = 1,
+    SF_PAYLOAD_FLOAT2 = 2
+} sf_payload_layout;
+int sf_volume_set_payload_layout(sf_volume_t vol, int32_t layout);
+int sf_volume_get_payload_layout(sf_volume_t vol, int32_t* layout);
 int sf_volume_read_float_payload(sf_volume_t vol, uint64_t first_slot, uint64_t slot_count, float* host_tsdf_aux);
 
 /* ---- hot path ------------------------------------------------------------------------ */

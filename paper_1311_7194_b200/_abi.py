@@ -22,6 +22,10 @@ SF_CUDA_ERROR = 6
 SF_IO_ERROR = 7
 SF_UNSUPPORTED = 8
 
+SF_PAYLOAD_CODES = 0
+SF_PAYLOAD_CODES_FLOAT_SHADOW = 1
+SF_PAYLOAD_FLOAT2 = 2
+
 c_double_p = C.POINTER(C.c_double)
 c_float_p = C.POINTER(C.c_float)
 
@@ -227,6 +231,8 @@ PRODUCT_ONLY = {
     "volume_read_free_list": (C.c_int, [vp, i32p, u64p]),
     "volume_enable_float_payload": (C.c_int, [vp]),
     "volume_read_float_payload": (C.c_int, [vp, u64, u64, vp]),
+    "volume_set_payload_layout": (C.c_int, [vp, i32]),
+    "volume_get_payload_layout": (C.c_int, [vp, i32p]),
     "tracker_create": (C.c_int, [vp, P(TrackerConfigC), c_double_p, P(vp)]),
     "tracker_destroy": (C.c_int, [vp]),
     "tracker_step": (C.c_int, [vp, P(FrameC), i32, c_double_p, vp]),

@@ -692,6 +692,20 @@ class SparseTsdfGrid:
     def enable_float_payload(self):
         self.backend.check(self.backend.lib.volume_enable_float_payload(self.handle))
 
+    # payload layouts (sf_gpu.h sf_payload_layout)
+    CODES, CODES_FLOAT_SHADOW, FLOAT2 = A.SF_PAYLOAD_CODES, A.SF_PAYLOAD_CODES_FLOAT_SHADOW, A.SF_PAYLOAD_FLOAT2
+
+    def set_payload_layout(self, layout: int):
+        """FLOAT2: float {tsdf, aux} per voxel only (P2, set on an empty volume); CODES_FLOAT_SHADOW:
+        the reference's 2-byte codes plus a float shadow; CODES: codes only (default)."""
+        self.backend.check(self.backend.lib.volume_set_payload_layout(self.handle, int(layout)))
+
+    @property
+    def payload_layout(self) -> int:
+        out = C.c_int32()
+        self.backend.check(self.backend.lib.volume_get_payload_layout(self.handle, C.byref(out)))
+        return out.value
+
     def read_float_payload(self, first_slot: int = 0, count: Optional[int] = None) -> np.ndarray:
         if count is None:
             count = self.pool_capacity - first_slot

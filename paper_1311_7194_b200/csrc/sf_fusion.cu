@@ -761,6 +761,7 @@ struct RowShared {
     float k127, ecode;        // 127 / delta; tsdf-code margin (code units)
     float q, w_max, k255w, lg_pmin, lg_scale;
     float thr_lo, thr_hi;     // clamp range of the variance code guess
+    float delta_f, echi;      // float payload: chi cut |T'| > delta certain outside delta +- echi
 };
 
 // Phase-2 update of one in-band voxel in FP32; false when a decision is not certain.
@@ -856,6 +857,61 @@ __device__ __noinline__ int exact_voxel(const VolParams& P, const FrameConsts* _
     return out;
 }
 
+// Float payload (block-sparse FloatShadowGrid semantics, grid.hpp:77-88; fusion.cpp:313-318,
+// 350-362): phase-2 update of one in-band voxel in FP32 from its float prior. The stored value
+// only has to meet the value tolerance (1e-5), but the chi cut |T'| > delta is a decision:
+// false when it is not certain (then the FP64 path decides).
+template <int MODE>
+__device__ __forceinline__ bool approx_update_f2(float2 prior, float tk, float pf, const RowShared& rc, float2& out) {
+    const bool has_prior = prior.x < INFINITY;  // !FloatShadowGrid::is_chi
+    const float pt = prior.x, pa = prior.y;
+    float nt, na;
+    if (MODE == 0) {
+        nt = has_prior ? (1.0f - pf) * pt + pf * tk : tk;
+        na = pf;
+    } else if (MODE == 1) {
+        nt = has_prior ? (pa * pt + pf * tk) * rcp_approx_f(pa + pf) : tk;
+        na = has_prior ? fminf(pa + pf, rc.w_max) : pf;
+    } else {
+        const float pred = pa + rc.q;
+        const float gain = pred * rcp_approx_f(pred + pf);
+        nt = has_prior ? pt + gain * (tk - pt) : tk;
+        na = has_prior ? pf * gain : pf;  // == (1 - gain) * predicted, without the cancellation
+    }
+    const float at = fabsf(nt);
+    if (!(fabsf(at - rc.delta_f) > rc.echi)) return false;
+    out = at > rc.delta_f ? make_float2(INFINITY, 0.0f) : make_float2(nt, na);
+    return true;
+}
+
+// The reference's FP64 path for one voxel with a float prior (fusion.cpp:81-173, 237-272,
+// 313-318, 357-361): false when there is no measurement.
+template <int MODE>
+__device__ __noinline__ bool exact_voxel_f2(const VolParams& P, const FrameConsts* __restrict__ fc, const FuseParams& fp,
+                                            int key, int l, float2 prior, const double* __restrict__ pix_dm,
+                                            const double* __restrict__ pix_var, const double* __restrict__ pix_w,
+                                            float2& out) {
+    const int N = P.N, M = P.M;
+    const int bx = key % N, by = (key / N) % N, bz = key / (N * N);
+    const int lx = l % M, ly = (l / M) % M, lz = l / (M * M);
+    const d3 xc = apply(fc->inv, voxel_center(P, bx * M + lx, by * M + ly, bz * M + lz));
+    double pu, pv;
+    if (!project(fc->intr, xc, pu, pv)) return false;
+    const int u = ref_lround_int(pu), v = ref_lround_int(pv);
+    if (!(u >= 0 && v >= 0 && u < fc->intr.w && v < fc->intr.h)) return false;
+    const size_t pix = (size_t)v * fc->intr.w + u;
+    const double dm = pix_dm[pix];
+    if (!(dm > 0.0)) return false;
+    const double tsdf_k = dm - xc.z;
+    if (fabs(tsdf_k) > P.delta) return false;
+    const bool has_prior = prior.x < INFINITY;
+    double new_t, new_a, a_err;
+    filter_rule<MODE>(has_prior, has_prior ? (double)prior.x : 0.0, has_prior ? (double)prior.y : 0.0, tsdf_k,
+                      MODE == 2 ? pix_var[pix] : 0.0, MODE == 2 ? 0.0 : pix_w[pix], fp, false, new_t, new_a, a_err);
+    out = fabs(new_t) > P.delta ? make_float2(INFINITY, 0.0f) : make_float2((float)new_t, (float)new_a);
+    return true;
+}
+
 constexpr int kRowThreads = 256;
 constexpr int kRowCtasPerSm = 3;
 constexpr uint32_t kGrabUnits = 4;  // 32-row units a warp takes per atomic (before the tail)
@@ -888,14 +944,15 @@ struct RowRing {
     static constexpr size_t kBytes = (kRowThreads / 32) * kEntries * sizeof(uint4);
 };
 
-template <int MODE, int MS>
+// P2: the float2 {tsdf, aux} payload layout (SF_PAYLOAD_FLOAT2) instead of the 2-byte codes.
+template <int MODE, int MS, bool P2>
 __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
     k_integrate_rows(VolParams P, const FrameConsts* __restrict__ fc, FuseParams fp, const int2* __restrict__ work,
                      FrameCounters* __restrict__ ctr, const AuxTables* __restrict__ aux,
                      const float2* __restrict__ pix_f, const double* __restrict__ pix_dm,
                      const double* __restrict__ pix_var, const double* __restrict__ pix_w,
                      const int32_t* __restrict__ slot_key, uint16_t* __restrict__ payload,
-                     const uint32_t* __restrict__ uniq, uint32_t* __restrict__ keybits) {
+                     float2* __restrict__ fpay, const uint32_t* __restrict__ uniq, uint32_t* __restrict__ keybits) {
     pdl_wait();
     constexpr int M = 1 << MS, M3 = M * M * M, RPB = M * M;
     constexpr int kRing = RowRing<MS>::kEntries;
@@ -952,6 +1009,10 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
         sh.lg_scale = static_cast<float>(P.aux_lg_scale);
         sh.thr_lo = static_cast<float>(P.aux_p_min * 0.5);
         sh.thr_hi = static_cast<float>(P.aux_p_max * 2.0);
+        // float payload chi cut: T' carries the measurement's eT (gain <= 1) and the FP32 filter
+        // error (a few ulp of delta); float(delta) itself is within 2^-24 delta
+        sh.delta_f = static_cast<float>(delta);
+        sh.echi = static_cast<float>(2.0 * eT + 4e-6 * delta);
     }
     clear_keybits(ctr, uniq, keybits);
     __syncthreads();
@@ -967,18 +1028,34 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
         if (lane < n) {
             const uint4 e = ring[(head + lane) & (kRing - 1)];
             const uint32_t l = e.y & 0x1FF, cell = (e.y >> 9) & 0xFFFF;
-            uint32_t out;
-            int code = 0;
-            if ((e.y >> 31) ||
-                !approx_update<MODE>(cell, __uint_as_float(e.z), __uint_as_float(e.w), sh, s_tdec, s_adec, s_thr, out)) {
-                ++exact;
-                code = exact_voxel<MODE>(sP, fc, sFp, aux, slot_key[e.x], static_cast<int>(l), cell, pix_dm, pix_var,
-                                         pix_w);
-                out = static_cast<uint32_t>(code);
-            }
-            if (code >= 0) {
-                payload[(size_t)e.x * M3 + l] = static_cast<uint16_t>(out);
-                ++updated;
+            if constexpr (P2) {
+                float2* cellp = fpay + (size_t)e.x * M3 + l;
+                const float2 prior = *cellp;
+                float2 out;
+                bool have = true;
+                if ((e.y >> 31) || !approx_update_f2<MODE>(prior, __uint_as_float(e.z), __uint_as_float(e.w), sh, out)) {
+                    ++exact;
+                    have = exact_voxel_f2<MODE>(sP, fc, sFp, slot_key[e.x], static_cast<int>(l), prior, pix_dm, pix_var,
+                                                pix_w, out);
+                }
+                if (have) {
+                    *cellp = out;
+                    ++updated;
+                }
+            } else {
+                uint32_t out;
+                int code = 0;
+                if ((e.y >> 31) || !approx_update<MODE>(cell, __uint_as_float(e.z), __uint_as_float(e.w), sh, s_tdec,
+                                                        s_adec, s_thr, out)) {
+                    ++exact;
+                    code = exact_voxel<MODE>(sP, fc, sFp, aux, slot_key[e.x], static_cast<int>(l), cell, pix_dm,
+                                             pix_var, pix_w);
+                    out = static_cast<uint32_t>(code);
+                }
+                if (code >= 0) {
+                    payload[(size_t)e.x * M3 + l] = static_cast<uint16_t>(out);
+                    ++updated;
+                }
             }
         }
         head += n;
@@ -1025,9 +1102,17 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
                     bz = key / (N * N);
                 }
                 rbase = static_cast<uint32_t>(r * M);
-                typename RV::T* prow = reinterpret_cast<typename RV::T*>(payload + (size_t)slot * M3 + rbase);
-                if (fresh) *prow = RV::chi();  // newly allocated block: chi-initialised (grid.cpp:87-100)
-                else cells = *prow;
+                if constexpr (P2) {
+                    if (fresh) {  // newly allocated block: chi (+inf, 0) (grid.hpp:77-88)
+                        float4* frow = reinterpret_cast<float4*>(fpay + (size_t)slot * M3 + rbase);
+#pragma unroll
+                        for (int j = 0; j < M / 2; ++j) frow[j] = make_float4(INFINITY, 0.0f, INFINITY, 0.0f);
+                    }
+                } else {
+                    typename RV::T* prow = reinterpret_cast<typename RV::T*>(payload + (size_t)slot * M3 + rbase);
+                    if (fresh) *prow = RV::chi();  // newly allocated block: chi-initialised (grid.cpp:87-100)
+                    else cells = *prow;
+                }
                 const int ly = r & (M - 1), lz = r >> MS;
                 // row origin x_c = R (voxel_center) + t in FP64 (voxel_center, grid.cpp:271-273)
                 const double vx = sh.ox + (i2d_exact(bx << MS) + 0.5) * sh.voxel;
@@ -1078,7 +1163,8 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
                 const bool q = in || unc;
                 const unsigned bal = __ballot_sync(0xffffffffu, q);
                 if (q) {
-                    const uint32_t meta = (rbase + lx) | (RV::cell(cells, lx) << 9) | (unc ? 0x80000000u : 0u);
+                    const uint32_t meta =
+                        (rbase + lx) | (P2 ? 0u : (RV::cell(cells, lx) << 9)) | (unc ? 0x80000000u : 0u);
                     ring[(tail + __popc(bal & lt_mask)) & (kRing - 1)] =
                         make_uint4(slot, meta, __float_as_uint(t), __float_as_uint(px.y));
                 }
@@ -1399,18 +1485,18 @@ FuseParams resolve_fuse_params(const Volume& v, const sf_fusion_params& p, bool 
     return f;
 }
 
-template <int MODE, int MS>
+template <int MODE, int MS, bool P2>
 static void launch_integrate_rows(Volume& v, FrameBuffers& fb, const FuseParams& fp, cudaStream_t s) {
     static_assert(RowRing<MS>::kBytes <= 200 * 1024, "ring exceeds shared memory");
     static bool configured = false;  // per instantiation
     if (!configured) {
-        SF_CUDA(cudaFuncSetAttribute(k_integrate_rows<MODE, MS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SF_CUDA(cudaFuncSetAttribute(k_integrate_rows<MODE, MS, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)RowRing<MS>::kBytes));
         configured = true;
     }
-    launch_pdl(k_integrate_rows<MODE, MS>, dim3(148 * kRowCtasPerSm), dim3(kRowThreads), RowRing<MS>::kBytes, s,
+    launch_pdl(k_integrate_rows<MODE, MS, P2>, dim3(148 * kRowCtasPerSm), dim3(kRowThreads), RowRing<MS>::kBytes, s,
                v.P, fb.fc, fp, fb.work, fb.ctr, v.d_aux, fb.pix_f, fb.pix_dm, fb.pix_var, fb.pix_w, v.d_slot_key,
-               v.d_payload, fb.keys_unique, v.d_keybits);
+               v.d_payload, v.d_fpayload, fb.keys_unique, v.d_keybits);
 }
 
 // Frame prep of fuse_frame (depends only on the frame): normals with the fusion options
@@ -1490,9 +1576,22 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
                                                                fb.pix_q)
         const bool fpl = v.d_fpayload != nullptr;
         if (events && events->before_integrate) record_event(events->before_integrate, s);
-        const bool fast = !fpl && (P.mshift == 3 || P.mshift == 2) && v.h_aux.fp32_ok && fp.refine == 0;
-#define SF_INTEGRATE_ROWS(MODE, MS) launch_integrate_rows<MODE, MS>(v, fb, fp, s)
-        if (fast) {
+        const bool rows_ok = (P.mshift == 3 || P.mshift == 2) && v.h_aux.fp32_ok && fp.refine == 0;
+        const bool fast = v.layout == SF_PAYLOAD_CODES && rows_ok;
+        const bool fast_f2 = v.layout == SF_PAYLOAD_FLOAT2 && rows_ok;
+#define SF_INTEGRATE_ROWS(MODE, MS) launch_integrate_rows<MODE, MS, false>(v, fb, fp, s)
+#define SF_INTEGRATE_ROWS_F2(MODE, MS) launch_integrate_rows<MODE, MS, true>(v, fb, fp, s)
+        if (fast_f2) {
+            if (P.mshift == 3) {
+                if (fp.mode == 0) SF_INTEGRATE_ROWS_F2(0, 3);
+                else if (fp.mode == 1) SF_INTEGRATE_ROWS_F2(1, 3);
+                else SF_INTEGRATE_ROWS_F2(2, 3);
+            } else {
+                if (fp.mode == 0) SF_INTEGRATE_ROWS_F2(0, 2);
+                else if (fp.mode == 1) SF_INTEGRATE_ROWS_F2(1, 2);
+                else SF_INTEGRATE_ROWS_F2(2, 2);
+            }
+        } else if (fast) {
             if (P.mshift == 3) {
                 if (fp.mode == 0) SF_INTEGRATE_ROWS(0, 3);
                 else if (fp.mode == 1) SF_INTEGRATE_ROWS(1, 3);
@@ -1514,6 +1613,7 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
         }
 #undef SF_INTEGRATE
 #undef SF_INTEGRATE_ROWS
+#undef SF_INTEGRATE_ROWS_F2
         SF_LAUNCH_CHECK();
         if (events && events->after_integrate) record_event(events->after_integrate, s);
         n += 1;

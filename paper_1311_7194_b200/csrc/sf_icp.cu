@@ -728,18 +728,43 @@ __global__ void __launch_bounds__(32, 1)
     }
     const unsigned long long total = st->cur_count;
     double sum = 0.0, carry = 0.0;
-    if (lane < kSums) {
-        constexpr int kAhead = 8;  // loads in flight ahead of the dependent chain
-        unsigned long long m = 0;
-        for (; m + kAhead <= total; m += kAhead) {
-            double x[kAhead];
-#pragma unroll
-            for (int u = 0; u < kAhead; ++u) x[u] = __ldcg(&terms[(m + u) * kSums + lane]);
-#pragma unroll
-            for (int u = 0; u < kAhead; ++u) kahan_add(sum, carry, x[u]);
+    // The addends stream through shared memory in a cp.async pipeline (kStages batches of kB
+    // matches in flight), so the loop runs at the latency of the dependent Kahan chain.
+    constexpr int kB = 32, kStages = 4;
+    constexpr int kStageBytes = kB * kSums * 8;  // 7168 B, a multiple of 16
+    __shared__ __align__(16) double s_t[kStages][kB * kSums];
+    const unsigned long long nbatch = (total + kB - 1) / kB;
+    auto issue = [&](unsigned long long b) {
+        if (b < nbatch) {
+            const unsigned long long m0 = b * kB;
+            const int bytes = static_cast<int>(total - m0 < kB ? total - m0 : kB) * kSums * 8;
+            const char* g = reinterpret_cast<const char*>(terms + m0 * kSums);
+            const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(s_t[b % kStages]));
+            for (int off = lane * 16; off < bytes; off += 32 * 16)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sbase + off), "l"(g + off) : "memory");
         }
-        for (; m < total; ++m) kahan_add(sum, carry, __ldcg(&terms[m * kSums + lane]));
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    static_assert(kStageBytes % 16 == 0, "stage size");
+#pragma unroll
+    for (int b = 0; b < kStages - 1; ++b) issue(b);
+    for (unsigned long long b = 0; b < nbatch; ++b) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 2) : "memory");
+        __syncwarp();
+        const double* x = s_t[b % kStages];
+        const int nm = static_cast<int>(total - b * kB < kB ? total - b * kB : kB);
+        if (lane < kSums) {
+            if (nm == kB) {
+#pragma unroll
+                for (int j = 0; j < kB; ++j) kahan_add(sum, carry, x[j * kSums + lane]);
+            } else {
+                for (int j = 0; j < nm; ++j) kahan_add(sum, carry, x[j * kSums + lane]);
+            }
+        }
+        __syncwarp();  // stage b % kStages is free again
+        issue(b + kStages - 1);
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __shared__ double s_sum[kSums];
     __shared__ double s_A[36];
     __shared__ Eig6 s_eig;

@@ -163,6 +163,7 @@ struct sf_volume {
     int32_t* d_table = nullptr;      // N^3
     uint16_t* d_payload = nullptr;   // capacity * M^3
     float2* d_fpayload = nullptr;    // optional float payload {tsdf, aux}
+    int layout = SF_PAYLOAD_CODES;   // sf_payload_layout
     int32_t* d_free_list = nullptr;  // capacity (stack, bottom..top)
     int32_t* d_slot_key = nullptr;   // capacity: table index of the block in each slot, -1 free
     uint32_t* d_occ = nullptr;       // occupancy bitmap, N^3 bits
@@ -179,6 +180,11 @@ struct sf_volume {
 
 namespace sf {
 using Volume = ::sf_volume;
+// Operations that read or write the 2-byte codes fail loudly on a float2-only volume.
+inline void require_codes(const Volume& v, const char* what) {
+    if (v.layout == SF_PAYLOAD_FLOAT2)
+        throw Error(SF_UNSUPPORTED, std::string(what) + ": not available on a float2-payload volume (SF_PAYLOAD_FLOAT2)");
+}
 void ensure_frame_buffers(Volume& v, FrameBuffers& fb, int w, int h);
 void ensure_patch_order(Volume& v, int w, int h);
 

@@ -463,6 +463,7 @@ extern "C" {
 int sf_marching_cubes(sf_volume_t v, const double region_pose[12], const sf_intrinsics* region_intrinsics,
                       uint64_t batch_memory_budget, sf_mesh_t* out, void* stream) {
     return guarded([&]() -> int {
+        if (v) require_codes(*v, "marching_cubes");
         if (!v || !out) throw Error(SF_INVALID_ARGUMENT, "sf_marching_cubes: null argument");
         if ((region_pose == nullptr) != (region_intrinsics == nullptr))
             throw Error(SF_INVALID_ARGUMENT, "sf_marching_cubes: region needs both pose and intrinsics");

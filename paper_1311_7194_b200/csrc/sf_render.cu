@@ -944,6 +944,7 @@ int sf_ray_bounds(sf_volume_t v, const double pose[12], const sf_intrinsics* int
 int sf_raycast(sf_volume_t v, const double pose[12], const sf_intrinsics* intr, float* depth, float* normals_xyz,
                int32_t out_on_device, sf_raycast_stats* stats, void* stream) {
     return guarded([&]() -> int {
+        if (v) require_codes(*v, "raycast");
         SF_CUDA(cudaSetDevice(v->device));
         validate_intr(*intr);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -978,6 +979,7 @@ int sf_raycast_with_bounds(sf_volume_t v, const double pose[12], const sf_intrin
                            const float* t_end, float* depth, float* normals_xyz, int32_t on_device,
                            sf_raycast_stats* stats, void* stream) {
     return guarded([&]() -> int {
+        if (v) require_codes(*v, "raycast");
         if (!v || !pose || !intr || !t_start || !t_end || !depth || !normals_xyz)
             throw Error(SF_INVALID_ARGUMENT, "sf_raycast_with_bounds: null argument");
         SF_CUDA(cudaSetDevice(v->device));

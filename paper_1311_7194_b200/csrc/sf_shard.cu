@@ -125,6 +125,7 @@ extern "C" {
 int sf_shard_pack_halo(sf_volume_t v, int32_t* keys, uint16_t* payloads, uint64_t cap, uint32_t* count,
                        void* stream) {
     return guarded([&]() -> int {
+        if (v) require_codes(*v, "shard halo");
         if (!v || !count || (cap && (!keys || !payloads))) throw Error(SF_INVALID_ARGUMENT, "sf_shard_pack_halo: null");
         if (v->P.shard_world <= 1) throw Error(SF_LOGIC_ERROR, "sf_shard_pack_halo: volume is not sharded");
         if (v->P.M3 % 8 != 0) throw Error(SF_INVALID_ARGUMENT, "sf_shard_pack_halo: M^3 must be a multiple of 8");

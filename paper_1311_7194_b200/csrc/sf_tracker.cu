@@ -480,6 +480,7 @@ int sf_tracker_step(sf_tracker_t tr, const sf_frame* captured, int32_t mode, con
         if ((mode == 1 || mode == 2) && !gt_pose)
             throw Error(SF_INVALID_ARGUMENT, "sf_tracker_step: this mode needs a pose argument");
         if (mode < 0 || mode > 2) throw Error(SF_INVALID_ARGUMENT, "sf_tracker_step: unknown mode");
+        if (mode != 1 && tr->frames > 0) require_codes(*tr->vol, "tracking (raycast of the model)");
         SF_CUDA(cudaSetDevice(tr->vol->device));
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         const size_t n = static_cast<size_t>(tr->cam.w) * tr->cam.h;

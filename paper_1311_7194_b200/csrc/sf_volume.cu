@@ -521,6 +521,7 @@ int sf_volume_block_slot(sf_volume_t v, const int32_t bc[3], int32_t* slot_out) 
 // read_voxel (grid.cpp:121-130)
 int sf_volume_read_voxel(sf_volume_t v, const int32_t vc[3], int32_t* is_chi, double* tsdf, double* aux) {
     return guarded([&]() -> int {
+        if (v) require_codes(*v, "read_voxel");
         SF_CUDA(cudaSetDevice(v->device));
         for (int i = 0; i < 3; ++i)
             if (vc[i] < 0 || vc[i] >= v->P.res) throw Error(SF_OUT_OF_RANGE, "grid: voxel coordinate out of range");
@@ -550,6 +551,7 @@ int sf_volume_read_voxel(sf_volume_t v, const int32_t vc[3], int32_t* is_chi, do
 // write_voxel (grid.cpp:132-154)
 int sf_volume_write_voxel(sf_volume_t v, const int32_t vc[3], int32_t tsdf_is_chi, double tsdf, double aux) {
     return guarded([&]() -> int {
+        if (v) require_codes(*v, "write_voxel");
         SF_CUDA(cudaSetDevice(v->device));
         for (int i = 0; i < 3; ++i)
             if (vc[i] < 0 || vc[i] >= v->P.res) throw Error(SF_OUT_OF_RANGE, "grid: voxel coordinate out of range");
@@ -592,6 +594,7 @@ int sf_volume_read_table(sf_volume_t v, int32_t* host_table) {
 
 int sf_volume_read_payload(sf_volume_t v, uint64_t first, uint64_t count, uint16_t* out) {
     return guarded([&]() -> int {
+        if (v) require_codes(*v, "read_payload");
         SF_CUDA(cudaSetDevice(v->device));
         if (first + count > v->P.capacity) throw Error(SF_OUT_OF_RANGE, "payload range");
         SF_CUDA(cudaMemcpy(out, v->d_payload + first * v->P.M3, count * v->P.M3 * sizeof(uint16_t),
@@ -602,6 +605,7 @@ int sf_volume_read_payload(sf_volume_t v, uint64_t first, uint64_t count, uint16
 
 int sf_volume_write_payload(sf_volume_t v, uint64_t first, uint64_t count, const uint16_t* in) {
     return guarded([&]() -> int {
+        if (v) require_codes(*v, "write_payload");
         SF_CUDA(cudaSetDevice(v->device));
         if (first + count > v->P.capacity) throw Error(SF_OUT_OF_RANGE, "payload range");
         SF_CUDA(cudaMemcpy(v->d_payload + first * v->P.M3, in, count * v->P.M3 * sizeof(uint16_t),
@@ -624,8 +628,10 @@ int sf_volume_read_free_list(sf_volume_t v, int32_t* out, uint64_t* count_out) {
 
 int sf_volume_enable_float_payload(sf_volume_t v) {
     return guarded([&]() -> int {
+        if (!v) throw Error(SF_INVALID_ARGUMENT, "sf_volume_enable_float_payload: null volume");
         SF_CUDA(cudaSetDevice(v->device));
         if (v->d_fpayload) return SF_OK;
+        v->layout = SF_PAYLOAD_CODES_FLOAT_SHADOW;
         const uint64_t n = static_cast<uint64_t>(v->P.capacity) * v->P.M3;
         SF_CUDA(cudaMalloc(&v->d_fpayload, std::max<uint64_t>(n, 1) * sizeof(float2)));
         int blocks;
@@ -633,6 +639,38 @@ int sf_volume_enable_float_payload(sf_volume_t v) {
         k_fill_f2<<<blocks, 256>>>(v->d_fpayload, n, make_float2(INFINITY, 0.0f));
         SF_LAUNCH_CHECK();
         SF_CUDA(cudaDeviceSynchronize());
+        return SF_OK;
+    });
+}
+
+int sf_volume_set_payload_layout(sf_volume_t v, int32_t layout) {
+    return guarded([&]() -> int {
+        if (!v) throw Error(SF_INVALID_ARGUMENT, "sf_volume_set_payload_layout: null volume");
+        if (layout < SF_PAYLOAD_CODES || layout > SF_PAYLOAD_FLOAT2)
+            throw Error(SF_INVALID_ARGUMENT, "sf_volume_set_payload_layout: unknown layout");
+        if (layout == v->layout) return SF_OK;
+        if (layout == SF_PAYLOAD_CODES_FLOAT_SHADOW && v->layout == SF_PAYLOAD_CODES)
+            return sf_volume_enable_float_payload(v);
+        if (v->host_allocated() != 0)
+            throw Error(SF_LOGIC_ERROR, "sf_volume_set_payload_layout: the volume must be empty to change layout");
+        if (layout == SF_PAYLOAD_CODES) {
+            SF_CUDA(cudaSetDevice(v->device));
+            if (v->d_fpayload) SF_CUDA(cudaFree(v->d_fpayload));
+            v->d_fpayload = nullptr;
+            v->layout = SF_PAYLOAD_CODES;
+            return SF_OK;
+        }
+        const int rc = sf_volume_enable_float_payload(v);
+        if (rc != SF_OK) return rc;
+        v->layout = layout;
+        return SF_OK;
+    });
+}
+
+int sf_volume_get_payload_layout(sf_volume_t v, int32_t* layout) {
+    return guarded([&]() -> int {
+        if (!v || !layout) throw Error(SF_INVALID_ARGUMENT, "sf_volume_get_payload_layout: null argument");
+        *layout = v->layout;
         return SF_OK;
     });
 }
@@ -650,6 +688,7 @@ int sf_volume_read_float_payload(sf_volume_t v, uint64_t first, uint64_t count, 
 
 int sf_volume_save_snapshot(sf_volume_t v, const char* path) {
     return guarded([&]() -> int {
+        if (v) require_codes(*v, "save_snapshot");
         SF_CUDA(cudaSetDevice(v->device));
         std::vector<int32_t> table(v->P.table_size);
         SF_CUDA(cudaMemcpy(table.data(), v->d_table, table.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));

@@ -218,6 +218,86 @@ def test_float_payload_matches_reference_shadow(gpu, ref):
     assert compared > 50
 
 
+def _assert_float_close(a, b, what):
+    """Float payload bar (north star): chi pattern equal; TSDF within 1e-5 absolute; aux
+    (variance / weight) within 1e-5 relative."""
+    chi_a, chi_b = ~(a[:, 0] < np.inf), ~(b[:, 0] < np.inf)
+    assert np.array_equal(chi_a, chi_b), f"{what}: chi pattern differs at {np.flatnonzero(chi_a != chi_b)[:8]}"
+    live = ~chi_a
+    assert np.abs(a[live, 0].astype(np.float64) - b[live, 0]).max(initial=0) <= 1e-5, what
+    rel = np.abs(a[live, 1].astype(np.float64) - b[live, 1]) / np.maximum(np.abs(b[live, 1]), 1e-300)
+    assert rel.max(initial=0) <= 1e-5, f"{what}: aux rel diff {rel.max()}"
+    assert np.all(a[chi_a, 1] == 0)
+    return int(live.sum())
+
+
+@pytest.mark.parametrize("mode", [sf.FusionMode.Kalman, sf.FusionMode.Weighted, sf.FusionMode.Simple])
+def test_float2_payload_matches_reference_shadow(gpu, ref, mode):
+    """SF_PAYLOAD_FLOAT2 (P2: float {tsdf, aux} only, the FP32 row kernel with certified
+    decisions) against the reference's FloatShadowGrid (grid.hpp:77-88, fusion.cpp:313-318,
+    357-361): offset table bit-exact, chi pattern equal, values within 1e-5."""
+    cfg = sf.GridConfig(16, 8, (-1.0, -1.0, 0.25), 2.0, 0.0)  # 128^3: the reference shadow's limit
+    intr = scenes.camera(320, 240, 262.5)
+    poses = scenes.c1_trajectory(100)[::25]
+    frames = frames_for(gpu, scenes.sphere_plane_scene(), poses, intr, 2.0, sigma0=2.5e-4)
+    aux = sf.AuxMode.Variance if mode == sf.FusionMode.Kalman else sf.AuxMode.Weight
+    g, r = grids(gpu, ref, cfg, 4096, aux)
+    g.set_payload_layout(g.FLOAT2)
+    assert g.payload_layout == g.FLOAT2
+    assert ref.lib.volume_enable_shadow(r.handle) == 0
+    params = sf.FusionParams(mode=mode, sigma0=2.5e-4)
+    for f, p in zip(frames, poses):
+        assert gpu.fuse_frame(g, f, p, params) == ref.fuse_frame(r, f, p, params)
+    assert np.array_equal(g.read_table(), r.read_table())
+    res, n, m = 128, 16, 8
+    st = np.zeros(res ** 3, np.float32)
+    sa = np.zeros(res ** 3, np.float32)
+    ref.lib.volume_read_shadow(r.handle, st.ctypes.data_as(C.POINTER(C.c_float)),
+                               sa.ctypes.data_as(C.POINTER(C.c_float)))
+    fp = g.read_float_payload()
+    table = g.read_table()
+    ours, theirs = [], []
+    for ti in np.flatnonzero(table >= 0):
+        slot = table[ti]
+        bx, by, bz = ti % n, (ti // n) % n, ti // (n * n)
+        ours.append(fp[slot * 512:(slot + 1) * 512])
+        dt = st.reshape(res, res, res)[bz * m:(bz + 1) * m, by * m:(by + 1) * m, bx * m:(bx + 1) * m].reshape(-1)
+        da = sa.reshape(res, res, res)[bz * m:(bz + 1) * m, by * m:(by + 1) * m, bx * m:(bx + 1) * m].reshape(-1)
+        theirs.append(np.stack([dt, da], -1))
+    live = _assert_float_close(np.concatenate(ours), np.concatenate(theirs), "float2 vs shadow")
+    assert live > 20000
+    with pytest.raises(NotImplementedError):
+        gpu.raycast(g, poses[-1], intr)  # codes are not maintained on a float2 volume
+
+
+def test_float2_payload_c4_scale(gpu, workload_c4):
+    """P2 at the benchmarked C4 geometry (N = 512, 640x480 noisy frames, Kalman, p_min 1e-12):
+    the float2 row kernel against the FP64 float-shadow kernel (itself equal to the reference's
+    FloatShadowGrid above): same blocks, chi pattern, values within 1e-5."""
+    c, grid_cfg, intr, fusion, poses, frames = workload_c4
+    a = sf.SparseTsdfGrid(grid_cfg, c["pool"], sf.AuxMode.Variance, p_min=c["p_min"], backend=gpu)
+    b = sf.SparseTsdfGrid(grid_cfg, c["pool"], sf.AuxMode.Variance, p_min=c["p_min"], backend=gpu)
+    a.set_payload_layout(a.FLOAT2)
+    b.enable_float_payload()
+    for f, p in zip(frames, poses):
+        assert gpu.fuse_frame(a, f, p, fusion) == gpu.fuse_frame(b, f, p, fusion)
+    assert np.array_equal(a.read_table(), b.read_table())
+    n = b.allocated_count
+    live = _assert_float_close(a.read_float_payload(0, n), b.read_float_payload(0, n), "float2 C4")
+    assert live > 1_000_000
+
+
+@pytest.fixture(scope="module")
+def workload_c4(gpu):
+    import bench
+    import paper_1311_7194_b200 as sfp
+
+    c = bench.workload_config()
+    grid_cfg, intr, fusion, _ = bench.make_params(sfp, c)
+    poses, frames = bench.make_frames(sfp, c, 4, intr)
+    return c, grid_cfg, intr, fusion, poses, frames
+
+
 def test_pool_exhaustion_partial_state(gpu, oracle):
     """PoolExhausted mid-list: the allocate-list prefix is integrated, nothing else (fusion.cpp:369)."""
     intr = scenes.camera(320, 240, 262.5)
