@@ -176,6 +176,15 @@ int sf_dfrm_write(const char* path, const sf_frame* frame);
 int sf_dfrm_read(const char* path, sf_intrinsics* intrinsics, float* depth, float* sigma, int32_t* has_sigma,
                  int32_t out_on_device);
 
+/* ---- trajectory CSV (frame_io.hpp:18-28, frame_io.cpp:81-126) -------------------------
+ * Rows "frame_index,r00,...,r22,t0,t1,t2" printed with 17 significant digits (byte-identical
+ * to write_trajectory). read: 12 or 13 values per row ('#' lines and empty lines skipped; no
+ * frame index -> 0); a rotation that is not orthonormal within 1e-6 is replaced by its nearest
+ * rotation, as parse_trajectory_row does. frame_index / poses12 NULL: *count = rows (size
+ * query); otherwise *count is the capacity in and the row count out. */
+int sf_trajectory_write(const char* path, const int32_t* frame_index, const double* poses12, uint64_t count);
+int sf_trajectory_read(const char* path, int32_t* frame_index, double* poses12, uint64_t* count);
+
 /* ---- marching cubes (marching_cubes.hpp:37-44, marching_cubes.cpp:74-196) -----------
  * The reference's mesh exactly: same vertices (float, welded per batch by cube-edge id in
  * first-reference order), normals and triangles. region_pose / region_intrinsics: optional

@@ -591,4 +591,32 @@ int sfref_dfrm_read(const char* path, sf_intrinsics* intrinsics, float* depth, f
     });
 }
 
+// write_trajectory / read_trajectory (frame_io.cpp:81-126), same conventions as sf_trajectory_*
+int sfref_trajectory_write(const char* path, const int32_t* frame_index, const double* poses12, uint64_t count) {
+    return guarded([&]() -> int {
+        std::vector<TrajectoryEntry> t(count);
+        for (uint64_t i = 0; i < count; ++i) {
+            t[i].frame_index = frame_index[i];
+            t[i].pose = to_pose(poses12 + 12 * i);
+        }
+        write_trajectory(t, path);
+        return SF_OK;
+    });
+}
+
+int sfref_trajectory_read(const char* path, int32_t* frame_index, double* poses12, uint64_t* count) {
+    return guarded([&]() -> int {
+        const std::vector<TrajectoryEntry> t = read_trajectory(path);
+        if (frame_index && poses12) {
+            if (t.size() > *count) return SF_OUT_OF_RANGE;
+            for (size_t i = 0; i < t.size(); ++i) {
+                frame_index[i] = t[i].frame_index;
+                from_pose(t[i].pose, poses12 + 12 * i);
+            }
+        }
+        *count = t.size();
+        return SF_OK;
+    });
+}
+
 }  // extern "C"

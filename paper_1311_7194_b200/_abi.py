@@ -224,6 +224,8 @@ MESH = {
     "mesh_destroy": (C.c_int, [vp]),
     "dfrm_write": (C.c_int, [C.c_char_p, P(FrameC)]),
     "dfrm_read": (C.c_int, [C.c_char_p, P(IntrinsicsC), vp, vp, P(C.c_int32), i32]),
+    "trajectory_write": (C.c_int, [C.c_char_p, i32p, c_double_p, u64]),
+    "trajectory_read": (C.c_int, [C.c_char_p, i32p, c_double_p, u64p]),
 }
 
 PRODUCT_ONLY = {

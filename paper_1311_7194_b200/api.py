@@ -493,13 +493,38 @@ class Backend:
         fc = frame.c()
         self.check(self.lib.dfrm_write(path.encode(), C.byref(fc)))
 
-    def read_dfrm(self, path: str) -> DepthFrame:
+    def write_trajectory(self, entries, path: str):
+        """write_trajectory (frame_io.cpp:81-93): entries = [(frame_index, Pose), ...]."""
+        n = len(entries)
+        fi = np.array([int(e[0]) for e in entries], dtype=np.int32)
+        p = np.array([e[1].to12() for e in entries], dtype=np.float64).reshape(n, 12)
+        self.check(self.lib.trajectory_write(path.encode(), fi.ctypes.data_as(A.i32p), _dptr(p), n))
+
+    def read_trajectory(self, path: str):
+        """read_trajectory (frame_io.cpp:117-126) -> [(frame_index, Pose), ...]."""
+        cnt = C.c_uint64(0)
+        self.check(self.lib.trajectory_read(path.encode(), None, None, C.byref(cnt)))
+        fi = np.zeros(max(1, cnt.value), dtype=np.int32)
+        p = np.zeros((max(1, cnt.value), 12), dtype=np.float64)
+        self.check(self.lib.trajectory_read(path.encode(), fi.ctypes.data_as(A.i32p), _dptr(p), C.byref(cnt)))
+        return [(int(fi[i]), Pose.from12(p[i])) for i in range(cnt.value)]
+
+    def read_dfrm(self, path: str, device=None) -> DepthFrame:
+        """read_dfrm (frame_io.cpp:47-79). device: a CUDA device -> the depth (and sigma) planes are
+        read straight into device buffers (torch tensors, sf_frame.on_device = 1)."""
         ic = A.IntrinsicsC()
         self.check(self.lib.dfrm_read(path.encode(), C.byref(ic), None, None, None, 0))
         intr = Intrinsics(ic.width, ic.height, ic.fx, ic.fy, ic.cx, ic.cy, ic.near_plane, ic.far_plane)
+        hs = C.c_int32(0)
+        if device is not None:
+            import torch
+
+            d = torch.zeros((ic.height, ic.width), dtype=torch.float32, device=device)
+            s = torch.zeros_like(d)
+            self.check(self.lib.dfrm_read(path.encode(), C.byref(ic), d.data_ptr(), s.data_ptr(), C.byref(hs), 1))
+            return DepthFrame(intr, d, s if hs.value else None)
         d = np.zeros((ic.height, ic.width), dtype=np.float32)
         s = np.zeros_like(d)
-        hs = C.c_int32(0)
         self.check(self.lib.dfrm_read(path.encode(), C.byref(ic), d.ctypes.data, s.ctypes.data, C.byref(hs), 0))
         return DepthFrame(intr, d, s if hs.value else None)
 

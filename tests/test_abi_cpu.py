@@ -169,3 +169,36 @@ def test_dfrm_files_match_reference(tmp_path):
             assert np.array_equal(ra.sigma, rb.sigma)
         assert (ra.intrinsics.width, ra.intrinsics.height) == (40, 30)
         assert np.all((ra.depth == 0) | ((ra.depth >= np.float32(0.2)) & (ra.depth <= np.float32(3.0))))
+
+
+def test_trajectory_csv_matches_reference(tmp_path):
+    """Trajectory CSV (frame_io.cpp:81-126): write byte-identical to write_trajectory; read
+    equal bit for bit, incl. 12-value rows, '#' comments, empty lines and the nearest-rotation
+    repair of a non-orthonormal row. Host-side I/O: no GPU needed."""
+    from tests import oracle_backends
+
+    ref = oracle_backends.reference()
+    if ref is None:
+        pytest.skip("reference build absent")
+    gpu = sf.default_backend()
+    poses = sf.orbit_trajectory([0.1, -0.2, 1.3], 1.3, 7, (0.0, 1.0, 0.0), 0.3, 1.1)
+    entries = [(3 * k + 1, p) for k, p in enumerate(poses)]
+    a, b = str(tmp_path / "a.csv"), str(tmp_path / "b.csv")
+    gpu.write_trajectory(entries, a)
+    ref.write_trajectory(entries, b)
+    assert open(a, "rb").read() == open(b, "rb").read()
+    # hand-written rows: a comment, a blank line, a 12-value row, a slightly skewed rotation
+    skew = "0,1.0,1e-4,0,0,1,0,0,0,1,0.5,0.25,2"
+    text = "# frame,r00..r22,t\n\n" + open(a).read() + "1,0,0,0,1,0,0,0,1,-1,0,3\n" + skew + "\n"
+    c = tmp_path / "c.csv"
+    c.write_text(text)
+    ra, rb = gpu.read_trajectory(str(c)), ref.read_trajectory(str(c))
+    assert len(ra) == len(rb) == len(entries) + 2
+    for (fa, pa), (fb, pb) in zip(ra, rb):
+        assert fa == fb
+        assert np.array_equal(pa.to12(), pb.to12())
+    assert ra[-2][0] == 0 and ra[-1][1].rotation[0, 1] != 1e-4  # repaired by nearest_rotation
+    bad = tmp_path / "bad.csv"
+    bad.write_text("1,2,3\n")
+    with pytest.raises(RuntimeError):
+        gpu.read_trajectory(str(bad))

@@ -364,6 +364,56 @@ def test_snapshot_roundtrip_cross_implementation(gpu, ref, tmp_path):
     assert_same_volume(g2, r2)
 
 
+def test_dfrm_device_buffers(gpu, ref, tmp_path):
+    """DFRM (frame_io.cpp:28-79) from and into DEVICE buffers: writing a device-resident frame
+    gives the reference's bytes; reading into device buffers gives the host read's planes, and
+    fusing straight from them equals fusing the host frame."""
+    import torch
+
+    intr = scenes.camera(320, 240, 262.5)
+    pose = scenes.c1_trajectory(100)[20]
+    f = gpu.render_synthetic_depth(scenes.sphere_plane_scene(), pose, intr, sigma0=2.5e-4, seed=4, domain_size=2.0)
+    dev = torch.device("cuda", 0)
+    fd = sf.DepthFrame(intr, torch.from_numpy(f.depth).to(dev), torch.from_numpy(f.sigma).to(dev))
+    a, b = str(tmp_path / "dev.dfrm"), str(tmp_path / "ref.dfrm")
+    gpu.write_dfrm(fd, a)
+    ref.write_dfrm(f, b)
+    assert open(a, "rb").read() == open(b, "rb").read()
+    rd = gpu.read_dfrm(b, device=dev)
+    rh = ref.read_dfrm(b)
+    assert rd.depth.is_cuda and rd.sigma is not None
+    assert np.array_equal(rd.depth.cpu().numpy(), rh.depth) and np.array_equal(rd.sigma.cpu().numpy(), rh.sigma)
+    g1, r = grids(gpu, ref, scenes.c1_config(), 0, sf.AuxMode.Variance)
+    g2 = sf.SparseTsdfGrid(scenes.c1_config(), 0, sf.AuxMode.Variance, backend=gpu)
+    params = sf.FusionParams(mode=sf.FusionMode.Kalman, sigma0=2.5e-4)
+    assert gpu.fuse_frame(g1, rd, pose, params) == gpu.fuse_frame(g2, rh, pose, params) == ref.fuse_frame(r, rh, pose, params)
+    assert_same_volume(g1, r)
+    assert_same_volume(g2, r)
+
+
+def test_snapshot_resume_on_device(gpu, ref, tmp_path):
+    """Resume from an STSG snapshot (grid.cpp:333-408): the reference fuses and saves, the device
+    volume loads it and both keep fusing; volumes and re-saved snapshots stay identical."""
+    intr = scenes.camera(320, 240, 262.5)
+    poses = scenes.c1_trajectory(100)[10:50:10]
+    frames = frames_for(gpu, scenes.sphere_plane_scene(), poses, intr, 2.0, sigma0=2.5e-4)
+    params = sf.FusionParams(mode=sf.FusionMode.Kalman, sigma0=2.5e-4)
+    r = sf.SparseTsdfGrid(scenes.c1_config(), 3000, sf.AuxMode.Variance, backend=ref)
+    for f, p in zip(frames[:2], poses[:2]):
+        ref.fuse_frame(r, f, p, params)
+    path = str(tmp_path / "mid.stsg")
+    r.save_snapshot(path)
+    g = sf.SparseTsdfGrid.load_snapshot(path, pool_capacity=3000, backend=gpu)
+    assert_same_volume(g, r)
+    for f, p in zip(frames[2:], poses[2:]):
+        assert gpu.fuse_frame(g, f, p, params) == ref.fuse_frame(r, f, p, params)
+    assert_same_volume(g, r)
+    pg, pr = str(tmp_path / "g.stsg"), str(tmp_path / "r.stsg")
+    g.save_snapshot(pg)
+    r.save_snapshot(pr)
+    assert open(pg, "rb").read() == open(pr, "rb").read()
+
+
 # ---------------------------------------------------------------------------------
 # raycast
 # ---------------------------------------------------------------------------------
