@@ -10,7 +10,7 @@
 NVCC    ?= nvcc
 ARCH    := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -fmad=false -std=c++17 --expt-relaxed-constexpr \
-           -Xcompiler -fPIC,-ffp-contract=off,-O2 -Xptxas -warn-spills
+           -Xcompiler -fPIC,-ffp-contract=off,-O2 -Xptxas -warn-spills $(EXTRA)
 SRC_DIR := paper_1311_7194_b200/csrc
 OUT_DIR := paper_1311_7194_b200/_native
 OBJ_DIR := build/obj

@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_native", "libsf_gpu.so")
+# SF_GPU_LIB: an alternative build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("SF_GPU_LIB") or os.path.join(_HERE, "_native", "libsf_gpu.so")
 
 SF_OK = 0
 SF_INVALID_ARGUMENT = 1

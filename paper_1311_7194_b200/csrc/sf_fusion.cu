@@ -26,6 +26,8 @@
 #include "sf_internal.h"
 #include "sf_sample.cuh"
 
+#include <type_traits>
+
 namespace sf {
 
 constexpr int kThreads = 256;
@@ -762,6 +764,8 @@ struct RowShared {
     float q, w_max, k255w, lg_pmin, lg_scale;
     float thr_lo, thr_hi;     // clamp range of the variance code guess
     float delta_f, echi;      // float payload: chi cut |T'| > delta certain outside delta +- echi
+    double cx, cy;            // principal point (pixel-boundary planes of small-footprint rows)
+    int axis, lstep;          // row axis (0 x, 1 y, 2 z: the block axis closest to the optical axis), its l stride
 };
 
 // Phase-2 update of one in-band voxel in FP32; false when a decision is not certain.
@@ -913,8 +917,12 @@ __device__ __noinline__ bool exact_voxel_f2(const VolParams& P, const FrameConst
 }
 
 constexpr int kRowThreads = 256;
-constexpr int kRowCtasPerSm = 3;
+#ifndef SF_ROW_CTAS
+#define SF_ROW_CTAS 3
+#endif
+constexpr int kRowCtasPerSm = SF_ROW_CTAS;
 constexpr uint32_t kGrabUnits = 4;  // 32-row units a warp takes per atomic (before the tail)
+constexpr uint32_t kTailUnitsPerWarp = 8;  // single-unit grabs once this much work per warp remains
 
 template <int MS>
 struct RowVec;
@@ -926,6 +934,12 @@ struct RowVec<3> {
         return (lx & 1) ? (w >> 16) : (w & 0xFFFF);
     }
     __device__ static uint4 chi() { return make_uint4(0x00800080u, 0x00800080u, 0x00800080u, 0x00800080u); }
+    __device__ static uint4 gather(const uint16_t* c, int stride) {  // a row along y or z
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = c[(2 * k) * stride] | (static_cast<uint32_t>(c[(2 * k + 1) * stride]) << 16);
+        return make_uint4(w[0], w[1], w[2], w[3]);
+    }
 };
 template <>
 struct RowVec<2> {
@@ -935,12 +949,17 @@ struct RowVec<2> {
         return (lx & 1) ? (w >> 16) : (w & 0xFFFF);
     }
     __device__ static uint2 chi() { return make_uint2(0x00800080u, 0x00800080u); }
+    __device__ static uint2 gather(const uint16_t* c, int stride) {
+        return make_uint2(c[0] | (static_cast<uint32_t>(c[stride]) << 16),
+                          c[2 * stride] | (static_cast<uint32_t>(c[3 * stride]) << 16));
+    }
 };
 
 // Per-warp ring of queued voxels: >= 31 left over + 32 rows x M new entries, a power of two.
 template <int MS>
 struct RowRing {
-    static constexpr int kEntries = MS == 3 ? 512 : 256;
+    // >= 31 left over + the new entries between drains (M = 8 drains after each half-row)
+    static constexpr int kEntries = (MS == 3 && kRowCtasPerSm <= 3) ? 512 : 256;
     static constexpr size_t kBytes = (kRowThreads / 32) * kEntries * sizeof(uint4);
 };
 
@@ -984,9 +1003,17 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
         sh.oy = P.oy;
         sh.oz = P.oz;
         sh.voxel = P.voxel;
-        sh.Dxf = static_cast<float>(P.voxel * inv.R.m[0]);
-        sh.Dyf = static_cast<float>(P.voxel * inv.R.m[3]);
-        sh.Dzf = static_cast<float>(P.voxel * inv.R.m[6]);
+        // rows along the block axis with the largest camera-z component (x on ties)
+        int ax = 0;
+        if (fabs(inv.R.m[7]) > fabs(inv.R.m[6 + ax])) ax = 1;
+        if (fabs(inv.R.m[8]) > fabs(inv.R.m[6 + ax])) ax = 2;
+        sh.axis = ax;
+        sh.lstep = ax == 0 ? 1 : ax == 1 ? M : M * M;
+        sh.Dxf = static_cast<float>(P.voxel * inv.R.m[ax]);
+        sh.Dyf = static_cast<float>(P.voxel * inv.R.m[3 + ax]);
+        sh.Dzf = static_cast<float>(P.voxel * inv.R.m[6 + ax]);
+        sh.cx = intr.cx;
+        sh.cy = intr.cy;
         sh.fxf = static_cast<float>(intr.fx);
         sh.fyf = static_cast<float>(intr.fy);
         sh.cxf = static_cast<float>(intr.cx);
@@ -997,11 +1024,16 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
         // T error bound (m) for rows with z < 16 m: double-float row origin, lx * dz, and the
         // (Sterbenz-exact in the band) subtraction d - z_hi
         const double delta = P.delta;
-        const double eT = 0x1p-21 * (delta + 2.0 * M * P.voxel) + 0x1p-41;
+        // |T_f32 - T_ref| <= 2^-24 ((M-1) voxel [Dzf] + (M-1) voxel [fma] + |d - Azh| + |T| [two
+        // subtractions] + (M-1) voxel) + 2^-40 [the reference's own FP64 x_c vs the row model],
+        // with |d - Azh|, |T| <= delta + (M-1) voxel inside the decision region; x 1.25 slack
+        const double eT = 1.25 * 0x1p-23 * (delta + 1.5 * (M - 1) * P.voxel) + 0x1p-40;
         sh.thr_out = static_cast<float>((delta + eT) * 1.000001);
         sh.thr_in = static_cast<float>((delta - eT) * 0.999999);
         sh.k127 = static_cast<float>(kTsdfCodeRange / delta);
-        sh.ecode = static_cast<float>(1e-3 + 4.0 * eT * (kTsdfCodeRange / delta));
+        // code margin: the measurement's eT (gain <= 1) plus the FP32 filter's own error
+        // (<= 2.4e-4 code units: rounded inputs, rcp.approx, three roundings; x 1.5 slack)
+        sh.ecode = static_cast<float>(3.6e-4 + 1.5 * eT * (kTsdfCodeRange / delta));
         sh.q = static_cast<float>(fp.q);
         sh.w_max = static_cast<float>(P.aux_w_max);
         sh.k255w = static_cast<float>(255.0 / P.aux_w_max);
@@ -1063,7 +1095,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
     // Guided dynamic scheduling in units of 32 rows: kGrabUnits per atomic while plenty of work
     // remains, single units for the tail (the last grabs decide when the kernel ends).
     const uint32_t n_units = static_cast<uint32_t>((n_rows + 31) / 32);
-    const uint32_t tail_units = gridDim.x * (kRowThreads / 32) * 2 * kGrabUnits;
+    const uint32_t tail_units = gridDim.x * (kRowThreads / 32) * kTailUnitsPerWarp;
     uint32_t seen = 0;
     for (;;) {
         const uint32_t step = seen + tail_units < n_units ? kGrabUnits : 1u;
@@ -1075,15 +1107,22 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
         const uint32_t units = min(step, n_units - grab);
         const unsigned long long grab_row = (unsigned long long)grab * 32;
         for (uint32_t sub = 0; sub < units; ++sub) {
-            // ---------------- phase 1: one x-row per lane ----------------
-            // Row set-up (divergent), then a converged loop over the row's M voxels in which
-            // every lane evaluates its voxel and in-band / uncertain voxels are appended to the
-            // warp's ring right away (one ballot per voxel position: nothing held in registers).
+            // ---------------- phase 1: one row per lane ----------------
+            // Rows run along the block axis closest to the optical axis (sh.axis, chosen per
+            // frame), so a row's voxels project to a tiny pixel footprint. Row set-up
+            // (divergent), then a converged loop over the row's M voxels in which every lane
+            // evaluates its voxel and in-band / uncertain voxels are appended to the warp's ring
+            // right away (one ballot per voxel position: nothing held in registers).
             const unsigned long long row = grab_row + sub * 32 + lane;
             uint32_t slot = 0, rbase = 0;
             typename RV::T cells = RV::chi();
-            bool fast = false, exact_row = false;
+            bool fast = false, exact_row = false, small = false;
             float Axf = 0.f, Ayf = 0.f, Azh = 1.f, Azl = 0.f, half = -1.f;
+            // small-footprint rows: pixel-boundary planes s(l) = s0 + l ds (> 0: the upper
+            // column / row) with margins, and the (up to) 2 x 2 candidate pixels' {depth, p_k}
+            float su0 = -1e30f, dsu = 0.f, mu = 0.f, sv0 = -1e30f, dsv = 0.f, mv = 0.f;
+            float2 c00 = make_float2(0.f, 0.f), c10 = c00, c01 = c00, c11 = c00;
+            const int lstep = sh.lstep;
             if (row < n_rows) {
                 const uint32_t item = static_cast<uint32_t>(row >> (2 * MS));
                 const int r = static_cast<int>(row & (RPB - 1));
@@ -1101,23 +1140,46 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
                     by = (key / N) % N;
                     bz = key / (N * N);
                 }
-                rbase = static_cast<uint32_t>(r * M);
+                // the row's first voxel (local coordinates; the row coordinate is 0)
+                const int ri = r & (M - 1), rj = r >> MS;
+                int l0x, l0y, l0z;
+                if (sh.axis == 0) {
+                    l0x = 0, l0y = ri, l0z = rj;
+                } else if (sh.axis == 1) {
+                    l0x = ri, l0y = 0, l0z = rj;
+                } else {
+                    l0x = ri, l0y = rj, l0z = 0;
+                }
+                rbase = static_cast<uint32_t>(l0x + (l0y << MS) + (l0z << (2 * MS)));
                 if constexpr (P2) {
                     if (fresh) {  // newly allocated block: chi (+inf, 0) (grid.hpp:77-88)
-                        float4* frow = reinterpret_cast<float4*>(fpay + (size_t)slot * M3 + rbase);
+                        float2* f0 = fpay + (size_t)slot * M3 + rbase;
+                        if (lstep == 1) {
+                            float4* frow = reinterpret_cast<float4*>(f0);
 #pragma unroll
-                        for (int j = 0; j < M / 2; ++j) frow[j] = make_float4(INFINITY, 0.0f, INFINITY, 0.0f);
+                            for (int j = 0; j < M / 2; ++j) frow[j] = make_float4(INFINITY, 0.0f, INFINITY, 0.0f);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < M; ++j) f0[j * lstep] = make_float2(INFINITY, 0.0f);
+                        }
                     }
                 } else {
-                    typename RV::T* prow = reinterpret_cast<typename RV::T*>(payload + (size_t)slot * M3 + rbase);
-                    if (fresh) *prow = RV::chi();  // newly allocated block: chi-initialised (grid.cpp:87-100)
-                    else cells = *prow;
+                    uint16_t* c0 = payload + (size_t)slot * M3 + rbase;
+                    if (lstep == 1) {
+                        typename RV::T* prow = reinterpret_cast<typename RV::T*>(c0);
+                        if (fresh) *prow = RV::chi();  // newly allocated block: chi-initialised (grid.cpp:87-100)
+                        else cells = *prow;
+                    } else if (fresh) {
+#pragma unroll
+                        for (int j = 0; j < M; ++j) c0[j * lstep] = kChiPayload;
+                    } else {
+                        cells = RV::gather(c0, lstep);
+                    }
                 }
-                const int ly = r & (M - 1), lz = r >> MS;
                 // row origin x_c = R (voxel_center) + t in FP64 (voxel_center, grid.cpp:271-273)
-                const double vx = sh.ox + (i2d_exact(bx << MS) + 0.5) * sh.voxel;
-                const double vy = sh.oy + (i2d_exact((by << MS) + ly) + 0.5) * sh.voxel;
-                const double vz = sh.oz + (i2d_exact((bz << MS) + lz) + 0.5) * sh.voxel;
+                const double vx = sh.ox + (i2d_exact((bx << MS) + l0x) + 0.5) * sh.voxel;
+                const double vy = sh.oy + (i2d_exact((by << MS) + l0y) + 0.5) * sh.voxel;
+                const double vz = sh.oz + (i2d_exact((bz << MS) + l0z) + 0.5) * sh.voxel;
                 const double Ax = ((sh.R[0] * vx + sh.R[1] * vy) + sh.R[2] * vz) + sh.t[0];
                 const double Ay = ((sh.R[3] * vx + sh.R[4] * vy) + sh.R[5] * vz) + sh.t[1];
                 const double Az = ((sh.R[6] * vx + sh.R[7] * vy) + sh.R[8] * vz) + sh.t[2];
@@ -1132,43 +1194,125 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
                 const float Xq = sh.Fmax * X * rzlo;  // >= |u - cx|, |v - cy| over the row
                 fast = zlo > 1e-3f && zhi < 16.0f && Xq < 2097152.0f;
                 // pixel-rounding margin of the row; |u|, |v| < 2^22 guaranteed
-                if (fast) half = 0.5f - 1.6f * (0x1p-23f * Xq * (2.5f + Z * rzlo) + 0x1p-24f * sh.Wpix);
-                // row near / across the camera plane, or very far: exact path for all its voxels
-                else exact_row = !(zhi < -1e-3f);
+                if (fast) {
+                    const float eu = 1.6f * (0x1p-23f * Xq * (2.5f + Z * rzlo) + 0x1p-24f * sh.Wpix);
+                    half = 0.5f - eu;
+                    // Footprint: u, v are monotone along the row (z > 0), so every voxel's true
+                    // pixel column lies in lround([min(u0, u1) - eu, max(u0, u1) + eu]).
+                    const float r0 = rcp_approx_f(Azh), r1 = rcp_approx_f(zend);
+                    const float xe = fmaf(static_cast<float>(M - 1), sh.Dxf, Axf);
+                    const float ye = fmaf(static_cast<float>(M - 1), sh.Dyf, Ayf);
+                    const float u0 = fmaf(sh.fxf, Axf * r0, sh.cxf), u1 = fmaf(sh.fxf, xe * r1, sh.cxf);
+                    const float v0 = fmaf(sh.fyf, Ayf * r0, sh.cyf), v1 = fmaf(sh.fyf, ye * r1, sh.cyf);
+                    const float slack = eu + 1e-3f;
+                    const int cu0 = static_cast<int>(floorf(fminf(u0, u1) - slack + 0.5f));
+                    const int cu1 = static_cast<int>(floorf(fmaxf(u0, u1) + slack + 0.5f));
+                    const int cv0 = static_cast<int>(floorf(fminf(v0, v1) - slack + 0.5f));
+                    const int cv1 = static_cast<int>(floorf(fmaxf(v0, v1) + slack + 0.5f));
+                    small = cu1 - cu0 <= 1 && cv1 - cv0 <= 1;
+                    if (small) {
+                        // boundary between columns cu0 and cu0 + 1 at u = cu0 + 1/2: the sign of
+                        // s = fx x - (cu0 + 1/2 - cx) z (z > 0), affine along the row. Error of
+                        // its FP32 evaluation (inputs rounded once, products, the fma chain):
+                        // <= 2^-24 * 6 * (fx X + |b| Z + M voxel (fx + |b|)), plus 1e-9 for the
+                        // reference's own FP64 rounding of x_c and u.
+                        if (cu1 > cu0) {
+                            const float b = static_cast<float>((static_cast<double>(cu0) + 0.5) - sh.cx);
+                            su0 = fmaf(sh.fxf, Axf, -(b * Azh));
+                            dsu = fmaf(sh.fxf, sh.Dxf, -(b * sh.Dzf));
+                            mu = 0x1p-24f * 6.0f *
+                                     (sh.fxf * X + fabsf(b) * Z + sh.Mvox * (sh.fxf + fabsf(b))) + 1e-9f;
+                        }
+                        if (cv1 > cv0) {
+                            const float b = static_cast<float>((static_cast<double>(cv0) + 0.5) - sh.cy);
+                            sv0 = fmaf(sh.fyf, Ayf, -(b * Azh));
+                            dsv = fmaf(sh.fyf, sh.Dyf, -(b * sh.Dzf));
+                            mv = 0x1p-24f * 6.0f *
+                                     (sh.fyf * X + fabsf(b) * Z + sh.Mvox * (sh.fyf + fabsf(b))) + 1e-9f;
+                        }
+                        // candidate pixels (outside the image: no measurement, fusion.cpp:93-95)
+                        const bool u0in = cu0 >= 0 && cu0 < w, u1in = cu1 > cu0 && cu1 >= 0 && cu1 < w;
+                        const bool v0in = cv0 >= 0 && cv0 < h, v1in = cv1 > cv0 && cv1 >= 0 && cv1 < h;
+                        if (u0in && v0in) c00 = pix_f[cv0 * w + cu0];
+                        if (u1in && v0in) c10 = pix_f[cv0 * w + cu1];
+                        if (u0in && v1in) c01 = pix_f[cv1 * w + cu0];
+                        if (u1in && v1in) c11 = pix_f[cv1 * w + cu1];
+                    }
+                } else {
+                    // row near / across the camera plane, or very far: exact path for all its voxels
+                    exact_row = !(zhi < -1e-3f);
+                }
             }
             const float Dxf = sh.Dxf, Dyf = sh.Dyf, Dzf = sh.Dzf;
             const float fxf = sh.fxf, fyf = sh.fyf, cxf = sh.cxf, cyf = sh.cyf;
             const float thr_in = sh.thr_in, thr_out = sh.thr_out;
             const unsigned lt_mask = (1u << lane) - 1u;
+            // every lane small (or without work): the plane-test loop, else the general one
+            const bool warp_small = __all_sync(0xffffffffu, small || (!fast && !exact_row));
+            if (warp_small) {
 #pragma unroll
-            for (int lx = 0; lx < M; ++lx) {
-                // explicit fma: one rounding per coordinate (the bounds above assume <= 2)
-                const float xf = lx == 0 ? Axf : fmaf(static_cast<float>(lx), Dxf, Axf);
-                const float yf = lx == 0 ? Ayf : fmaf(static_cast<float>(lx), Dyf, Ayf);
-                const float zf = lx == 0 ? Azh : fmaf(static_cast<float>(lx), Dzf, Azh);
-                const float rz = rcp_approx_f(zf);
-                const float uf = fmaf(fxf, xf * rz, cxf), vf = fmaf(fyf, yf * rz, cyf);
-                const float tu = __fadd_rn(uf, kMagic23), tv = __fadd_rn(vf, kMagic23);
-                const bool cert = fabsf(__fsub_rn(uf, __fsub_rn(tu, kMagic23))) < half &&
-                                  fabsf(__fsub_rn(vf, __fsub_rn(tv, kMagic23))) < half;
-                const uint32_t u = static_cast<uint32_t>(__float_as_int(tu) - __float_as_int(kMagic23));
-                const uint32_t v = static_cast<uint32_t>(__float_as_int(tv) - __float_as_int(kMagic23));
-                const bool inimg = fast && cert && u < (uint32_t)w && v < (uint32_t)h;
-                const float2 px = pix_f[inimg ? v * (uint32_t)w + u : 0u];
-                const float t = (px.x - Azh) - (lx == 0 ? Azl : fmaf(static_cast<float>(lx), Dzf, Azl));
-                const float at = fabsf(t);
-                const bool meas = inimg && px.x > 0.0f;
-                const bool in = meas && at < thr_in;
-                const bool unc = exact_row || (fast && (!cert || (meas && !(at < thr_in) && !(at > thr_out))));
-                const bool q = in || unc;
-                const unsigned bal = __ballot_sync(0xffffffffu, q);
-                if (q) {
-                    const uint32_t meta =
-                        (rbase + lx) | (P2 ? 0u : (RV::cell(cells, lx) << 9)) | (unc ? 0x80000000u : 0u);
-                    ring[(tail + __popc(bal & lt_mask)) & (kRing - 1)] =
-                        make_uint4(slot, meta, __float_as_uint(t), __float_as_uint(px.y));
+                for (int lx = 0; lx < M; ++lx) {
+                    const float fl = static_cast<float>(lx);
+                    const float su = fmaf(fl, dsu, su0), sv = fmaf(fl, dsv, sv0);
+                    const bool iu = su > 0.0f, iv = sv > 0.0f;
+                    const bool cert = fabsf(su) > mu && fabsf(sv) > mv;
+                    const float2 px = iv ? (iu ? c11 : c01) : (iu ? c10 : c00);
+                    const float t = (px.x - Azh) - (lx == 0 ? Azl : fmaf(fl, Dzf, Azl));
+                    const float at = fabsf(t);
+                    const bool meas = small && px.x > 0.0f;
+                    const bool in = meas && cert && at < thr_in;
+                    const bool unc = small && (!cert || (meas && !(at < thr_in) && !(at > thr_out)));
+                    const bool q = in || unc;
+                    const unsigned bal = __ballot_sync(0xffffffffu, q);
+                    if (q) {
+                        const uint32_t meta = (rbase + lx * lstep) | (P2 ? 0u : (RV::cell(cells, lx) << 9)) |
+                                              (unc ? 0x80000000u : 0u);
+                        ring[(tail + __popc(bal & lt_mask)) & (kRing - 1)] =
+                            make_uint4(slot, meta, __float_as_uint(t), __float_as_uint(px.y));
+                    }
+                    tail += __popc(bal);
+                    if (kRing < 32 * M + 31 && lx == M / 2 - 1) {  // half-row drain (small ring)
+                        __syncwarp();
+                        while (tail - head >= 32) drain(32);
+                        __syncwarp();
+                    }
                 }
-                tail += __popc(bal);
+            } else {
+#pragma unroll
+                for (int lx = 0; lx < M; ++lx) {
+                    // explicit fma: one rounding per coordinate (the bounds above assume <= 2)
+                    const float xf = lx == 0 ? Axf : fmaf(static_cast<float>(lx), Dxf, Axf);
+                    const float yf = lx == 0 ? Ayf : fmaf(static_cast<float>(lx), Dyf, Ayf);
+                    const float zf = lx == 0 ? Azh : fmaf(static_cast<float>(lx), Dzf, Azh);
+                    const float rz = rcp_approx_f(zf);
+                    const float uf = fmaf(fxf, xf * rz, cxf), vf = fmaf(fyf, yf * rz, cyf);
+                    const float tu = __fadd_rn(uf, kMagic23), tv = __fadd_rn(vf, kMagic23);
+                    const bool cert = fabsf(__fsub_rn(uf, __fsub_rn(tu, kMagic23))) < half &&
+                                      fabsf(__fsub_rn(vf, __fsub_rn(tv, kMagic23))) < half;
+                    const uint32_t u = static_cast<uint32_t>(__float_as_int(tu) - __float_as_int(kMagic23));
+                    const uint32_t v = static_cast<uint32_t>(__float_as_int(tv) - __float_as_int(kMagic23));
+                    const bool inimg = fast && cert && u < (uint32_t)w && v < (uint32_t)h;
+                    const float2 px = pix_f[inimg ? v * (uint32_t)w + u : 0u];
+                    const float t = (px.x - Azh) - (lx == 0 ? Azl : fmaf(static_cast<float>(lx), Dzf, Azl));
+                    const float at = fabsf(t);
+                    const bool meas = inimg && px.x > 0.0f;
+                    const bool in = meas && at < thr_in;
+                    const bool unc = exact_row || (fast && (!cert || (meas && !(at < thr_in) && !(at > thr_out))));
+                    const bool q = in || unc;
+                    const unsigned bal = __ballot_sync(0xffffffffu, q);
+                    if (q) {
+                        const uint32_t meta = (rbase + lx * lstep) | (P2 ? 0u : (RV::cell(cells, lx) << 9)) |
+                                              (unc ? 0x80000000u : 0u);
+                        ring[(tail + __popc(bal & lt_mask)) & (kRing - 1)] =
+                            make_uint4(slot, meta, __float_as_uint(t), __float_as_uint(px.y));
+                    }
+                    tail += __popc(bal);
+                    if (kRing < 32 * M + 31 && lx == M / 2 - 1) {  // half-row drain (small ring)
+                        __syncwarp();
+                        while (tail - head >= 32) drain(32);
+                        __syncwarp();
+                    }
+                }
             }
             __syncwarp();  // ring entries and the fresh rows' chi stores before the drain
             // ---------------- phase 2: drain full rounds ----------------

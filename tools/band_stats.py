@@ -54,3 +54,26 @@ print(f"z slices (64 voxels) with an in-band voxel: {zsl.any(-1).mean():.3f}")
 q = inband.reshape(len(blocks), M, M, M)
 for name, ax in (("x", 3), ("y", 2), ("z", 1)):
     print(f"rows along {name} with in-band: {q.any(ax).mean():.3f}; in-band per such row {q.sum(ax)[q.any(ax)].mean():.2f}")
+
+# pixel footprint of rows along each axis: distinct lround(u) / lround(v) per row
+def footprint(axis):
+    res = []
+    for s0 in range(0, len(blocks), 2000):
+        b = blocks[s0:s0 + 2000]
+        vc = (b[:, None, :] * M + loc[None]).astype(np.float64)
+        x = org + (vc + 0.5) * vox
+        xc = (x - t) @ Rt.T
+        u = np.floor(525.0 * xc[..., 0] / xc[..., 2] + 319.5 + 0.5)
+        v = np.floor(525.0 * xc[..., 1] / xc[..., 2] + 239.5 + 0.5)
+        u = u.reshape(len(b), M, M, M); v = v.reshape(len(b), M, M, M)   # [z][y][x]
+        ax = {0: 3, 1: 2, 2: 1}[axis]
+        cu = u.max(ax) - u.min(ax) + 1
+        cv = v.max(ax) - v.min(ax) + 1
+        res.append(np.stack([cu.reshape(-1), cv.reshape(-1)], -1))
+    r = np.concatenate(res)
+    return r
+Rcam = P.rotation.T  # world -> camera rotation
+for a in range(3):
+    r = footprint(a)
+    print(f"axis {'xyz'[a]} (cam z comp {Rcam[2, a]:+.3f}): rows with cols<=2 & rows<=2: {((r[:,0]<=2)&(r[:,1]<=2)).mean():.3f}, "
+          f"single pixel {((r[:,0]==1)&(r[:,1]==1)).mean():.3f}, cols<=3&rows<=2 {((r[:,0]<=3)&(r[:,1]<=2)).mean():.3f}")
