@@ -45,3 +45,24 @@ $(CPPTEST): tests/cpp/test_gpu_api.cpp include/sparsefusion_gpu.hpp include/sf_g
 	@mkdir -p tests/cpp/_build
 	g++ -std=c++17 -O2 -ffp-contract=off -Iinclude -Ioracle/shim $< -L$(OUT_DIR) -lsf_gpu \
 	    -Wl,-rpath,'$$ORIGIN/../../../$(OUT_DIR)' -o $@
+
+# Conformance: the reference's own test suites (proj/tests/*.cpp, unmodified) linked against
+# the C++ drop-in layer (paper_1311_7194_b200/cpp/sparsefusion_adapter.cpp: fuse_frame,
+# select_update_blocks, compute_ray_bounds, raycast, icp, compute_normals, marching_cubes over
+# libsf_gpu.so) ahead of the reference's remaining objects (oracle/_ref/obj). Built only where
+# the reference headers exist; run on a GPU by tests/test_gpu_conformance.py.
+REF      ?= /root/reference/proj
+CONF_DIR := tests/cpp/_build
+CONF_TESTS := test_fusion test_render test_registration acceptance test_grid test_geometry test_pipeline
+REF_OBJS := $(wildcard oracle/_ref/obj/*.o)
+LDSTD    := $(if $(wildcard /usr/lib/gcc/x86_64-linux-gnu/13/libstdc++.so),-L/usr/lib/gcc/x86_64-linux-gnu/13)
+CONF_CXX := g++ -std=c++20 -O2 -DNDEBUG -ffp-contract=off -fPIC -w -Ioracle/shim -I$(REF)/include -Iinclude
+.PHONY: conformance
+conformance: $(addprefix $(CONF_DIR)/conf_,$(CONF_TESTS))
+$(CONF_DIR)/sparsefusion_adapter.o: paper_1311_7194_b200/cpp/sparsefusion_adapter.cpp include/sf_gpu.h
+	@mkdir -p $(CONF_DIR)
+	$(CONF_CXX) -c $< -o $@
+$(CONF_DIR)/conf_%: $(REF)/tests/%.cpp $(CONF_DIR)/sparsefusion_adapter.o $(LIB)
+	$(CONF_CXX) -I$(REF)/tests -DSPARSEFUSION_CLI_PATH='"/nonexistent/sparsefusion-cli"' $< \
+	    $(CONF_DIR)/sparsefusion_adapter.o $(REF_OBJS) $(LDSTD) -L$(OUT_DIR) -lsf_gpu \
+	    -Wl,--allow-multiple-definition -Wl,-rpath,'$$ORIGIN/../../../$(OUT_DIR)' -o $@

@@ -244,6 +244,12 @@ int sf_volume_write_voxel(sf_volume_t vol, const int32_t vc[3], int32_t tsdf_is_
 int sf_volume_read_table(sf_volume_t vol, int32_t* host_table);
 int sf_volume_read_payload(sf_volume_t vol, uint64_t first_slot, uint64_t slot_count, uint16_t* host_payload);
 int sf_volume_write_payload(sf_volume_t vol, uint64_t first_slot, uint64_t slot_count, const uint16_t* host_payload);
+/* Bulk import of a host grid's complete state into a freshly created (empty) volume: the
+ * N^3 offset table, payload slots [0, slot_count) and the free-list stack bottom to top
+ * (grid.hpp:189-191); allocated + free must equal the pool capacity. Used by the C++ drop-in
+ * layer, whose host SparseTsdfGrid stays the source of truth. */
+int sf_volume_import_state(sf_volume_t vol, const int32_t* table, const uint16_t* payload, uint64_t slot_count,
+                           const int32_t* free_list, uint64_t free_count);
 /* Free-list stack, bottom to top (grid.hpp:191); *count_out receives its length. */
 int sf_volume_read_free_list(sf_volume_t vol, int32_t* host_out, uint64_t* count_out);
 
@@ -275,6 +281,7 @@ typedef enum {
 int sf_volume_set_payload_layout(sf_volume_t vol, int32_t layout);
 int sf_volume_get_payload_layout(sf_volume_t vol, int32_t* layout);
 int sf_volume_read_float_payload(sf_volume_t vol, uint64_t first_slot, uint64_t slot_count, float* host_tsdf_aux);
+int sf_volume_write_float_payload(sf_volume_t vol, uint64_t first_slot, uint64_t slot_count, const float* host_tsdf_aux);
 
 /* ---- hot path ------------------------------------------------------------------------ */
 

@@ -235,6 +235,8 @@ PRODUCT_ONLY = {
     "volume_enable_float_payload": (C.c_int, [vp]),
     "volume_read_float_payload": (C.c_int, [vp, u64, u64, vp]),
     "volume_set_payload_layout": (C.c_int, [vp, i32]),
+    "volume_write_float_payload": (C.c_int, [vp, u64, u64, vp]),
+    "volume_import_state": (C.c_int, [vp, vp, vp, u64, vp, u64]),
     "volume_get_payload_layout": (C.c_int, [vp, i32p]),
     "tracker_create": (C.c_int, [vp, P(TrackerConfigC), c_double_p, P(vp)]),
     "tracker_destroy": (C.c_int, [vp]),

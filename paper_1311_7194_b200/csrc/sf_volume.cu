@@ -782,6 +782,59 @@ int sf_volume_load_snapshot(const char* path, uint64_t pool_capacity, int32_t de
     });
 }
 
+// Bulk import of a host grid's complete state into a FRESH volume (the C++ drop-in layer keeps
+// the reference's host SparseTsdfGrid as the source of truth and mirrors it per call):
+// offset table, payload slots [0, slot_count), the free-list stack (bottom to top).
+int sf_volume_import_state(sf_volume_t v, const int32_t* table, const uint16_t* payload, uint64_t slot_count,
+                           const int32_t* free_list, uint64_t free_count) {
+    return guarded([&]() -> int {
+        if (!v || !table || (slot_count && !payload) || (free_count && !free_list))
+            throw Error(SF_INVALID_ARGUMENT, "sf_volume_import_state: null argument");
+        SF_CUDA(cudaSetDevice(v->device));
+        if (v->host_allocated() != 0) throw Error(SF_LOGIC_ERROR, "sf_volume_import_state: volume not empty");
+        if (slot_count > v->P.capacity || free_count > v->P.capacity)
+            throw Error(SF_OUT_OF_RANGE, "sf_volume_import_state: more slots than the pool capacity");
+        uint64_t allocated = 0, high = 0;
+        for (uint64_t i = 0; i < v->P.table_size; ++i)
+            if (table[i] != kEmpty) {
+                if (table[i] < 0 || static_cast<uint64_t>(table[i]) >= v->P.capacity)
+                    throw Error(SF_OUT_OF_RANGE, "sf_volume_import_state: slot out of range");
+                ++allocated;
+                high = std::max<uint64_t>(high, static_cast<uint64_t>(table[i]) + 1);
+            }
+        if (allocated + free_count != v->P.capacity)
+            throw Error(SF_LOGIC_ERROR, "sf_volume_import_state: allocated + free != capacity");
+        SF_CUDA(cudaMemcpy(v->d_table, table, v->P.table_size * sizeof(int32_t), cudaMemcpyHostToDevice));
+        if (slot_count)
+            SF_CUDA(cudaMemcpy(v->d_payload, payload, slot_count * v->P.M3 * sizeof(uint16_t), cudaMemcpyHostToDevice));
+        if (free_count)
+            SF_CUDA(cudaMemcpy(v->d_free_list, free_list, free_count * sizeof(int32_t), cudaMemcpyHostToDevice));
+        VolCounters c{};
+        c.allocated_count = allocated;
+        c.free_top = free_count;
+        c.high_water = high;
+        SF_CUDA(cudaMemcpy(v->d_vc, &c, sizeof(c), cudaMemcpyHostToDevice));
+        int blocks;
+        grid_for(v->P.table_size, blocks);
+        k_rebuild_index<<<blocks, 256>>>(v->P, v->d_table, v->d_slot_key, v->d_occ);
+        SF_LAUNCH_CHECK();
+        SF_CUDA(cudaDeviceSynchronize());
+        return SF_OK;
+    });
+}
+
+int sf_volume_write_float_payload(sf_volume_t v, uint64_t first, uint64_t count, const float* in) {
+    return guarded([&]() -> int {
+        if (!v || (count && !in)) throw Error(SF_INVALID_ARGUMENT, "sf_volume_write_float_payload: null argument");
+        SF_CUDA(cudaSetDevice(v->device));
+        if (!v->d_fpayload) throw Error(SF_LOGIC_ERROR, "float payload not enabled");
+        if (first + count > v->P.capacity) throw Error(SF_OUT_OF_RANGE, "payload range");
+        SF_CUDA(cudaMemcpy(v->d_fpayload + first * v->P.M3, in, count * v->P.M3 * sizeof(float2),
+                           cudaMemcpyHostToDevice));
+        return SF_OK;
+    });
+}
+
 // Host-only introspection of the aux codec tables (used by the CPU test-suite to check the
 // threshold encode against the reference's log-based encode without a GPU).
 int sf_debug_aux_tables(const sf_aux_quant* aux, double delta, double* tsdf_decode, double* aux_decode,
