@@ -127,7 +127,8 @@ def cpu_info():
 
 C5 = dict(N=1024, M=8, voxel=0.15e-3, center=(0.0, 0.0, 0.0), r=0.08, bump=0.024, spacing=0.3,
           orbit_radius=0.9, orbit_arc=0.3, frames=100, width=640, height=480, focal=525.0, sigma0=4e-4,
-          p_min=1e-12, pool_total=2 * 1024 * 1024, max_distance=4e-3, reseed=16)
+          p_min=1e-12, pool_total=2 * 1024 * 1024, max_distance=4e-3, reseed=16, brick_shift=3,
+          halo_capacity=32768)
 
 
 def c5_config():
@@ -654,6 +655,15 @@ def run_ours(args, world, rank, local):
                                    "copy of the mesh into numpy arrays"},
         "clocks": clocks.summary(),
     }
+    if world == 1 and not args.no_c5:
+        # BASELINE configs[4] (C5, 8192^3) on this GPU through the sharded frame: one rank, and two
+        # ranks emulated in-process — the 1-GPU points of the multi-GPU curve (N > 1: run_sharded)
+        result["c5_sharded_one_gpu"] = {
+            "one_rank": sharded_c5(args, 1, 0, local, 1),
+            "two_ranks_emulated": sharded_c5(args, 1, 0, local, 2),
+            "note": "C5 workload of the N > 1 line; 'two_ranks_emulated' runs both ranks' kernels and the exchanges on "
+                    "this one GPU (its frame time is the sum of both ranks' work, not a multi-GPU time)",
+        }
     if rank == 0 and not args.no_cpu_baseline:
         nb = min(6, nframes - 1)
         cpu = reference_frames_per_s(sf, c, poses, frames, steps=nb, warmup=0, budget_s=30.0)
@@ -672,25 +682,21 @@ def run_ours(args, world, rank, local):
         dist.destroy_process_group()
 
 
-def run_sharded(args, world, rank, local):
-    """C5 over a block pool sharded across `world` GPUs (or --local-shards emulated ranks)."""
+def sharded_c5(args, world, rank, local, nshards, dist=None, icp_mode=0, clocks=None):
+    """C5 (8192^3 @ 0.15 mm, N = 1024) over a block pool sharded across `nshards` ranks through
+    the native sharded frame (one CUDA graph per frame, exchanges inside it):
+    this process's rank over NCCL when `dist` is set, else all ranks in this process. One step =
+    one fused frame of the whole job; device-timed like the C4 line (max over ranks)."""
     import torch
 
     import paper_1311_7194_b200 as sf
     from paper_1311_7194_b200 import shard
 
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist = None
-    if world > 1 or args.sharded_nccl:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=dev)
+    if dist is not None:
         comm = shard.DistComm()
         ranks = [rank]
-        nshards = world
     else:
-        nshards = args.local_shards
         comm = shard.LocalComm(nshards)
         ranks = list(range(nshards))
     c = c5_config()
@@ -700,20 +706,26 @@ def run_sharded(args, world, rank, local):
     poses, frames = make_frames(sf, c, nframes, intr, make_c5_scene(sf, c))
     dframes = [sf.DepthFrame(intr, torch.from_numpy(f.depth).to(dev), torch.from_numpy(f.sigma).to(dev))
                for f in frames]
-    pool = c["pool_total"] // nshards + 256 * 1024  # own blocks + mirrored halo
-    shards = [shard.ShardVolume(grid_cfg, pool, sf.AuxMode.Variance, r, nshards, device=local, p_min=c["p_min"])
-              for r in ranks]
-    tr = shard.ShardedTracker(shards, comm, intr, fusion, match, poses[0])
+    pool = c["pool_total"] // nshards + (256 * 1024 if nshards > 1 else 0)  # own blocks + mirrored halo
+    shards = [shard.ShardVolume(grid_cfg, pool, sf.AuxMode.Variance, r, nshards, device=local, p_min=c["p_min"],
+                                brick_shift=c["brick_shift"]) for r in ranks]
+    tr = shard.NativeShardedTracker(shards, comm, intr, fusion, match, poses[0], icp_mode=icp_mode,
+                                    halo_capacity=c["halo_capacity"])
     hooks = hook_deltas(sf, poses)
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    HOOK = tr.TRACK_WITH_HOOK
 
     def step(k):
         if reseed_due(c, k):
-            tr.current = poses[k - 1]
-        return tr.step(dframes[k], external=hooks[k] if k else None)
+            tr.set_pose(poses[k - 1], stream=sp)
+        tr.step(dframes[k], HOOK, hooks[k], stream=sp)
 
     for k in range(0, 1 + args.warmup):
         step(k)
-    stream = torch.cuda.current_stream()
+    m = tr.fetch(stream=sp)
+    if m.status:
+        raise RuntimeError(f"sharded warm-up failed with status {m.status}")
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     flush = torch.empty(400 * 1024 * 1024, dtype=torch.uint8, device=dev)
@@ -721,13 +733,14 @@ def run_sharded(args, world, rank, local):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
+    with (clocks if clocks is not None else contextlib.nullcontext()):
         for i in range(steps):
             k = 1 + args.warmup + i
             flush.fill_(i & 0xFF)
             ev0[i].record(stream)
-            metrics.append(step(k))
+            step(k)
             ev1[i].record(stream)
+            metrics.append(tr.fetch(stream=sp))  # synchronises (outside the events)
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -736,35 +749,73 @@ def run_sharded(args, world, rank, local):
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    vox = sum(m.voxels_updated for m in metrics)
+    if any(m.status for m in metrics):
+        raise RuntimeError(f"sharded run failed: {[m.status for m in metrics]}")
     gt = poses[nframes - 1]
-    pose_err = float(max(np.abs(metrics[-1].pose.rotation - gt.rotation).max(),
-                         np.abs(metrics[-1].pose.translation - gt.translation).max()))
+    out = {
+        "value": steps / (total_ms * 1e-3), "ms_per_step": total_ms / steps, "steps": steps, "frames": nframes,
+        "shards": nshards, "icp_mode": "replicas" if icp_mode == 0 else "partial sums + all-reduce",
+        "voxel_updates_per_s": sum(m.voxels_updated for m in metrics) / (total_ms * 1e-3),
+        "blocks_total_last": metrics[-1].blocks_total,
+        "icp_iterations_mean": sum(m.iterations for m in metrics) / steps,
+        "halo_records_mean": sum(m.halo_records for m in metrics) / steps,
+        "halo_overflow": sum(m.halo_overflow for m in metrics),
+        "kernel_launches_per_frame": sum(m.kernel_launches for m in metrics) / steps,
+        "tracking_error_last_frame": float(max(np.abs(metrics[-1].pose.rotation - gt.rotation).max(),
+                                               np.abs(metrics[-1].pose.translation - gt.translation).max())),
+        "transport": "NCCL (one rank per process)" if dist is not None else
+                     f"in-process ranks on one GPU ({nshards}; exchanges are kernels)",
+    }
+    del tr, shards
+    return out
+
+
+def run_sharded(args, world, rank, local):
+    """N > 1 (or --local-shards R emulated on one GPU): the C5 line, BASELINE configs[4]."""
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1 or args.sharded_nccl:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        nshards = world
+    else:
+        nshards = args.local_shards
+    clocks = ClockSampler(local)
+    res = {}
+    for mode in (0, 1):  # replicated ICP vs partial sums + all-reduce (SURVEY.md §8e: measure both)
+        res[mode] = sharded_c5(args, world, rank, local, nshards, dist, icp_mode=mode,
+                               clocks=clocks if mode == 0 else None)
+    r0 = res[0]
+    c = c5_config()
     result = {
         "metric": "fused depth frames/s (raycast+ICP+integrate, 640x480), 8192^3 sparse pool sharded",
-        "value": steps / (total_ms * 1e-3),
+        "value": r0["value"],
         "unit": "frames/s",
         "n_gpus": world,
-        "steps": steps,
+        "steps": r0["steps"],
         "warmup": args.warmup,
-        "ms_per_step": total_ms / steps,
+        "ms_per_step": r0["ms_per_step"],
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (GPU sphere-traced 3x3 grid of bumpy spheres, sigma0=4e-4 noise + sigma plane)",
         "config": {
-            "workload": "C5: 8192^3 sparse @ 0.15 mm (N=1024, M=8) block pool sharded by 8^3-block brick "
-                        f"across {nshards} ranks, halo exchange + global ray bounds + nearest-depth composite "
-                        "(NCCL), ICP on the composite, 640x480, Kalman, icp_with_hook",
-            "shards": nshards, "emulated_on_one_gpu": isinstance(comm, shard.LocalComm), "frames": nframes,
-            "pool_per_rank": pool, "l2": "flushed (400 MB write) between timed steps",
-            "parallelism": f"block-pool shards x{nshards}", "relocalise_every": c["reseed"],
+            "workload": "C5: 8192^3 sparse @ 0.15 mm (N=1024, M=8) block pool sharded by brick across the ranks, "
+                        "one CUDA graph per frame: global ray bounds, per-rank march, nearest-depth composite, "
+                        "replicated ICP, per-rank fuse, halo exchange; 640x480, Kalman, icp_with_hook",
+            "shards": nshards, "emulated_on_one_gpu": dist is None, "frames": r0["frames"],
+            "brick_blocks": 1 << c["brick_shift"], "halo_capacity": c["halo_capacity"],
+            "l2": "flushed (400 MB write) between timed steps", "parallelism": f"block-pool shards x{nshards}",
+            "relocalise_every": c["reseed"],
         },
-        "voxel_updates_per_s": vox / (total_ms * 1e-3),
-        "blocks_total_last": metrics[-1].blocks_total,
-        "icp_iterations_mean": sum(m.iterations for m in metrics) / steps,
-        "tracking_error_last_frame": pose_err,
+        "voxel_updates_per_s": r0["voxel_updates_per_s"],
+        "sharded": r0,
+        "icp_allreduce": res[1],
         "clocks": clocks.summary(),
     }
     if rank == 0:
@@ -901,6 +952,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 sharded sub-measurement of the N=1 line")
     ap.add_argument("--local-shards", type=int, default=0,
                     help="run the sharded C5 loop as this many emulated ranks on one GPU")
     ap.add_argument("--sharded-nccl", action="store_true",

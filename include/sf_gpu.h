@@ -415,6 +415,48 @@ int sf_tracker_last_launch_count(sf_tracker_t tr, uint64_t* count);
  * bytes sf_tracker_fetch reads back. */
 int sf_tracker_io_bytes(sf_tracker_t tr, int32_t has_sigma, uint64_t* h2d, uint64_t* d2h);
 
+/* ---- sharded fused frame --------------------------------
+ * run()'s per-frame body over a block pool partitioned across ranks, one CUDA graph per frame
+ * with the exchanges inside: ray bounds per rank -> MIN/MAX all-reduce (global bounds), each
+ * rank marches only the rays its own blocks meet, nearest-depth composite, ICP on the
+ * composite (icp_mode 0: replicated on every rank; 1: partial normal-equation sums over pixel
+ * slices combined by an all-reduce), pose update, per-rank fuse, halo exchange through
+ * fixed-capacity buffers. Ranks are in-process (create_local: `count` volumes of this GPU,
+ * volume i sharded as rank i of count; the exchanges are kernels) or one per process
+ * (create_nccl: NCCL on the stream, captured into the graph; rank 0 makes the id with
+ * sf_nccl_unique_id and the caller broadcasts it). No reference counterpart. */
+typedef struct sf_shard_tracker* sf_shard_tracker_t;
+typedef struct {
+    sf_tracker_config base;
+    int32_t icp_mode;       /* 0: replicas, 1: partial sums + all-reduce */
+    int32_t pad_;
+    uint64_t halo_capacity; /* halo records per rank per frame (0 -> 16384); overflow is reported */
+} sf_shard_tracker_config;
+typedef struct {
+    int32_t frame, registered, status, iterations;
+    double pose[12];
+    uint64_t matches;
+    uint64_t voxels_updated;  /* summed over ranks */
+    uint64_t blocks_total;    /* owned blocks summed over ranks (mirrored halo blocks excluded) */
+    uint64_t hit_pixels;      /* composite raycast */
+    uint64_t halo_records;    /* records packed this frame, all ranks */
+    uint64_t halo_overflow;   /* records beyond halo_capacity (not exchanged: raise the capacity) */
+    uint64_t kernel_launches; /* this process's kernels this frame */
+    int32_t icp_steps, pad_;
+} sf_shard_frame_metrics;
+int sf_nccl_unique_id(uint8_t out[128]);
+int sf_shard_tracker_create_local(sf_volume_t* volumes, int32_t count, const sf_shard_tracker_config* config,
+                                  const double initial_pose[12], sf_shard_tracker_t* out);
+int sf_shard_tracker_create_nccl(sf_volume_t volume, const uint8_t nccl_id[128], int32_t rank, int32_t world,
+                                 const sf_shard_tracker_config* config, const double initial_pose[12],
+                                 sf_shard_tracker_t* out);
+int sf_shard_tracker_destroy(sf_shard_tracker_t tr);
+/* modes as sf_tracker_step (0 track, 1 ground truth, 2 track with an external delta) */
+int sf_shard_tracker_step(sf_shard_tracker_t tr, const sf_frame* captured, int32_t mode, const double gt_pose[12],
+                          void* stream);
+int sf_shard_tracker_set_pose(sf_shard_tracker_t tr, const double pose[12], void* stream);
+int sf_shard_tracker_fetch(sf_shard_tracker_t tr, sf_shard_frame_metrics* out, void* stream);
+
 /* ---- synthetic input (scene.hpp:69-79, scene.cpp:101-177) --------------------------- */
 /* Analytic scene of spheres (cx,cy,cz,r), planes (nx,ny,nz,offset; normalised as
  * AnalyticScene::add_plane does) and axis-aligned boxes (cx,cy,cz,hx,hy,hz). Depth is

@@ -146,6 +146,34 @@ class TrackerConfigC(C.Structure):
     ]
 
 
+class ShardTrackerConfigC(C.Structure):
+    _fields_ = [
+        ("base", TrackerConfigC),
+        ("icp_mode", C.c_int32),
+        ("pad_", C.c_int32),
+        ("halo_capacity", C.c_uint64),
+    ]
+
+
+class ShardFrameMetricsC(C.Structure):
+    _fields_ = [
+        ("frame", C.c_int32),
+        ("registered", C.c_int32),
+        ("status", C.c_int32),
+        ("iterations", C.c_int32),
+        ("pose", C.c_double * 12),
+        ("matches", C.c_uint64),
+        ("voxels_updated", C.c_uint64),
+        ("blocks_total", C.c_uint64),
+        ("hit_pixels", C.c_uint64),
+        ("halo_records", C.c_uint64),
+        ("halo_overflow", C.c_uint64),
+        ("kernel_launches", C.c_uint64),
+        ("icp_steps", C.c_int32),
+        ("pad_", C.c_int32),
+    ]
+
+
 class FrameMetricsC(C.Structure):
     _fields_ = [
         ("frame", C.c_int32),
@@ -258,6 +286,13 @@ PRODUCT_ONLY = {
     "composite_select": (C.c_int, [vp, u64, i32, vp, vp, vp]),
     "shard_pack_halo": (C.c_int, [vp, vp, vp, u64, P(C.c_uint32), vp]),
     "shard_apply_halo": (C.c_int, [vp, vp, vp, u64, P(C.c_uint32), vp]),
+    "nccl_unique_id": (C.c_int, [vp]),
+    "shard_tracker_create_local": (C.c_int, [P(vp), i32, P(ShardTrackerConfigC), c_double_p, P(vp)]),
+    "shard_tracker_create_nccl": (C.c_int, [vp, vp, i32, i32, P(ShardTrackerConfigC), c_double_p, P(vp)]),
+    "shard_tracker_destroy": (C.c_int, [vp]),
+    "shard_tracker_step": (C.c_int, [vp, P(FrameC), i32, c_double_p, vp]),
+    "shard_tracker_set_pose": (C.c_int, [vp, c_double_p, vp]),
+    "shard_tracker_fetch": (C.c_int, [vp, P(ShardFrameMetricsC), vp]),
 }
 
 REF_ONLY = {

@@ -20,6 +20,7 @@
 // summation, and shrink applied to the sums instead of to each match (~1e-15 relative);
 // pose parity is asserted at 1e-6.
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstdlib>
 #include <string>
@@ -233,6 +234,99 @@ __host__ __device__ constexpr int packed_index(int i, int j) {  // upper triangl
     return i * 6 - i * (i - 1) / 2 + (j - i);
 }
 
+// The solve of one iteration from its merged unshrunk sums (one warp; lanes of warp 0).
+// st->center / scale / inv_scale / cur_count are set. Shrink as a linear map on the sums,
+// gated solve (certified Cholesky fast path, else the warp Jacobi), pose update,
+// convergence, and the loop condition. `counter` (the last-CTA ticket) is reset.
+template <bool COND>
+__device__ __noinline__ void solve_from_sums(IcpState* st, double* s_sum, double* s_fin, const IcpParamsDev& prm,
+                                             unsigned int* counter, cudaGraphConditionalHandle cond) {
+    const int lane = threadIdx.x & 31;
+    // ---- shrink as a linear map on the sums: A = L S6 L^T, b = -L t6, with
+    // L = [[D, -D C], [0, I]], D = diag(1/s), C = [c]x (one thread, fully unrolled: the 36
+    // entries are independent, so the latency overlaps).
+    if (lane == 0) {
+        const d3 c = st->center, inv = st->inv_scale;
+        const double C[3][3] = {{0.0, -c.z, c.y}, {c.z, 0.0, -c.x}, {-c.y, c.x, 0.0}};
+        const double D[3] = {inv.x, inv.y, inv.z};
+        double S[6][6];
+#pragma unroll
+        for (int i = 0; i < 6; ++i)
+#pragma unroll
+            for (int j = i; j < 6; ++j) S[i][j] = S[j][i] = s_sum[packed_index(i, j)];
+        // G = S L^T restricted to what is needed: G[k][j] = sum_l S[k][l] L[j][l]
+        double G[6][6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {  // L[j] = (D_j e_j, -D_j C[j])
+                double t = S[k][j];
+#pragma unroll
+                for (int l = 0; l < 3; ++l) t -= S[k][3 + l] * C[j][l];
+                G[k][j] = D[j] * t;
+            }
+#pragma unroll
+            for (int j = 3; j < 6; ++j) G[k][j] = S[k][j];
+        }
+#pragma unroll
+        for (int i = 0; i < 6; ++i)
+#pragma unroll
+            for (int j = i; j < 6; ++j) {
+                double a;
+                if (i < 3) {
+                    a = G[i][j];
+#pragma unroll
+                    for (int l = 0; l < 3; ++l) a -= C[i][l] * G[3 + l][j];
+                    a *= D[i];
+                } else {
+                    a = G[i][j];
+                }
+                s_fin[packed_index(i, j)] = a;
+            }
+        const double* T = s_sum + 21;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            double t = T[i];
+#pragma unroll
+            for (int l = 0; l < 3; ++l) t -= C[i][l] * T[3 + l];
+            s_fin[21 + i] = -(D[i] * t);
+        }
+#pragma unroll
+        for (int i = 3; i < 6; ++i) s_fin[21 + i] = -T[i];
+        s_fin[27] = s_sum[27];
+    }
+    __syncwarp();
+    __shared__ int s_fast;
+    if (lane == 0) {
+        double x[6];
+        s_fast = fast_gated_solve(s_fin, static_cast<double>(st->cur_count), prm.theta, x) ? 1 : 0;
+        if (s_fast) {
+            finalize_motion(st, s_fin, x, prm);
+            *counter = 0;
+            st->t_end = globaltimer_ns();
+            if constexpr (COND)
+                cudaGraphSetConditional(cond, (!st->done && st->iterations < prm.max_iterations) ? 1u : 0u);
+        }
+    }
+    __syncwarp();
+    if (s_fast) return;
+    __shared__ double s_A[36];
+    __shared__ Eig6 s_eig;
+    for (int i = lane; i < 36; i += 32) {
+        const int r = i / 6, cc = i % 6;
+        s_A[i] = s_fin[r <= cc ? packed_index(r, cc) : packed_index(cc, r)];
+    }
+    __syncwarp();
+    eigendecompose_sym6_warp_rr(s_A, &s_eig);
+    __syncwarp();
+    if (lane == 0) {
+        solve_finalize(st, s_fin, s_eig, prm);
+        *counter = 0;
+        st->t_end = globaltimer_ns();
+        if constexpr (COND)
+            cudaGraphSetConditional(cond, (!st->done && st->iterations < prm.max_iterations) ? 1u : 0u);
+    }}
+
 // One ICP iteration (registration.cpp:17-123 + 175-212) in one launch.
 //
 // The reference shrinks the matches (centre c, scale s from their bounding box) before it
@@ -244,29 +338,35 @@ __host__ __device__ constexpr int packed_index(int i, int j) {  // upper triangl
 // association, and the last CTA to finish merges the partials in a fixed order, forms c, s,
 // applies L (~1e-15 relative: the same result as shrinking first, up to rounding), runs the
 // warp-parallel Jacobi and the gated solve. No match records go through HBM.
-template <bool COND>
+//
+// PARTIAL (sharded ICP, north star "27-float allreduce"): the pass covers only the source
+// pixels [pix0, pix1) of this rank, and the last CTA writes the rank's merged partial sums,
+// box and count to `rec` instead of solving; the ranks' records are then all-reduced and
+// k_icp_solve_ranks solves (identically on every rank).
+template <bool COND, bool PARTIAL = false>
 __global__ void __launch_bounds__(kIcpThreads, 1)
     k_icp_step(const float* __restrict__ src, const float* __restrict__ src_n, const float* __restrict__ tgt,
                const float* __restrict__ tgt_n, Intr si, Intr ti, IcpParamsDev prm, IcpState* st,
                double* __restrict__ part_bbox, unsigned long long* __restrict__ part_count, DD* __restrict__ part,
-               unsigned int* counter, cudaGraphConditionalHandle cond) {
+               unsigned int* counter, cudaGraphConditionalHandle cond, int pix0 = 0, int pix1 = 0x7fffffff,
+               IcpRankPartial* rec = nullptr) {
     extern __shared__ DD s_red[];  // [kSums][kIcpThreads]
     if (threadIdx.x == 0 && st->bodies == 0) atomicCAS(&st->t_step0, 0ull, globaltimer_ns());
     if (st->done) {  // converged / lost: end the device-side loop
-        if constexpr (COND) {
+        if constexpr (COND && !PARTIAL) {
             if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0u);
         }
         return;
     }
     const Pose delta = st->delta;
-    const int n = si.w * si.h;
+    const int n = min(si.w * si.h, pix1);
     const int tid = threadIdx.x;
     DD acc[kSums];
 #pragma unroll
     for (int k = 0; k < kSums; ++k) acc[k] = DD{0.0, 0.0};
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
     unsigned long long cnt = 0;
-    for (int i = blockIdx.x * blockDim.x + tid; i < n; i += gridDim.x * blockDim.x) {
+    for (int i = pix0 + blockIdx.x * blockDim.x + tid; i < n; i += gridDim.x * blockDim.x) {
         d3 p, q, nn;
         if (!associate(i, src, src_n, tgt, tgt_n, si, ti, prm, delta, p, q, nn)) continue;
         const d3 pxn = cross(p, nn);
@@ -379,6 +479,16 @@ __global__ void __launch_bounds__(kIcpThreads, 1)
                 s_c[0] += s_c[w];
             }
             const unsigned long long total = s_c[0];
+            if constexpr (PARTIAL) {
+                rec->count = static_cast<double>(total);
+                for (int a = 0; a < 3; ++a) {
+                    rec->box[a] = s_b[0][a];
+                    rec->box[3 + a] = -s_b[0][3 + a];  // max as a min of the negation: one MIN all-reduce
+                }
+            }
+        }
+        if constexpr (!PARTIAL) if (tid == 0) {
+            const unsigned long long total = s_c[0];
             if (st->bodies == 0) st->t_assoc0 = globaltimer_ns();
             st->bodies += 1;
             s_lost = total < 10 ? 1 : 0;
@@ -430,12 +540,23 @@ __global__ void __launch_bounds__(kIcpThreads, 1)
         s_m[k][j] = a;
     }
     __syncthreads();
-    if (s_lost) {
-        if (tid == 0) {
-            *counter = 0;
-            if constexpr (COND) cudaGraphSetConditional(cond, 0u);
+    if constexpr (PARTIAL) {
+        if (tid < kSums) {
+            DD a = s_m[tid][0];
+            for (int j = 1; j < L; ++j) dd_merge(a, s_m[tid][j]);
+            rec->sums[2 * tid] = a.hi;
+            rec->sums[2 * tid + 1] = a.lo;
         }
+        if (tid == 0) *counter = 0;
         return;
+    } else {
+        if (s_lost) {
+            if (tid == 0) {
+                *counter = 0;
+                if constexpr (COND) cudaGraphSetConditional(cond, 0u);
+            }
+            return;
+        }
     }
     if (tid < kSums) {
         DD a = s_m[tid][0];
@@ -444,90 +565,65 @@ __global__ void __launch_bounds__(kIcpThreads, 1)
     }
     __syncthreads();
     if (tid >= 32) return;
-    // ---- shrink as a linear map on the sums: A = L S6 L^T, b = -L t6, with
-    // L = [[D, -D C], [0, I]], D = diag(1/s), C = [c]x (one thread, fully unrolled: the 36
-    // entries are independent, so the latency overlaps).
-    if (lane == 0) {
-        const d3 c = st->center, inv = st->inv_scale;
-        const double C[3][3] = {{0.0, -c.z, c.y}, {c.z, 0.0, -c.x}, {-c.y, c.x, 0.0}};
-        const double D[3] = {inv.x, inv.y, inv.z};
-        double S[6][6];
-#pragma unroll
-        for (int i = 0; i < 6; ++i)
-#pragma unroll
-            for (int j = i; j < 6; ++j) S[i][j] = S[j][i] = s_sum[packed_index(i, j)];
-        // G = S L^T restricted to what is needed: G[k][j] = sum_l S[k][l] L[j][l]
-        double G[6][6];
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {  // L[j] = (D_j e_j, -D_j C[j])
-                double t = S[k][j];
-#pragma unroll
-                for (int l = 0; l < 3; ++l) t -= S[k][3 + l] * C[j][l];
-                G[k][j] = D[j] * t;
-            }
-#pragma unroll
-            for (int j = 3; j < 6; ++j) G[k][j] = S[k][j];
+    solve_from_sums<COND>(st, s_sum, s_fin, prm, counter, cond);
+}
+
+// Sharded ICP: merge the ranks' records (local ranks in rank order; after an NCCL all-reduce
+// a single record holding the sums), then the same TrackingLost test, shrink and solve as
+// k_icp_step's last CTA. One warp.
+template <bool COND>
+__global__ void __launch_bounds__(32, 1)
+    k_icp_solve_ranks(IcpState* st, const IcpRankPartial* __restrict__ recs, int nrec, IcpParamsDev prm,
+                      unsigned int* counter, cudaGraphConditionalHandle cond) {
+    const int lane = threadIdx.x;
+    if (st->done) {
+        if constexpr (COND) {
+            if (lane == 0) cudaGraphSetConditional(cond, 0u);
         }
-#pragma unroll
-        for (int i = 0; i < 6; ++i)
-#pragma unroll
-            for (int j = i; j < 6; ++j) {
-                double a;
-                if (i < 3) {
-                    a = G[i][j];
-#pragma unroll
-                    for (int l = 0; l < 3; ++l) a -= C[i][l] * G[3 + l][j];
-                    a *= D[i];
-                } else {
-                    a = G[i][j];
-                }
-                s_fin[packed_index(i, j)] = a;
-            }
-        const double* T = s_sum + 21;
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            double t = T[i];
-#pragma unroll
-            for (int l = 0; l < 3; ++l) t -= C[i][l] * T[3 + l];
-            s_fin[21 + i] = -(D[i] * t);
-        }
-#pragma unroll
-        for (int i = 3; i < 6; ++i) s_fin[21 + i] = -T[i];
-        s_fin[27] = s_sum[27];
+        return;
     }
-    __syncwarp();
-    __shared__ int s_fast;
+    __shared__ double s_sum[kSums], s_fin[kSums];
+    __shared__ int s_lost;
+    if (lane < kSums) {
+        DD a{recs[0].sums[2 * lane], recs[0].sums[2 * lane + 1]};
+        for (int r = 1; r < nrec; ++r) dd_merge(a, DD{recs[r].sums[2 * lane], recs[r].sums[2 * lane + 1]});
+        s_sum[lane] = a.hi + a.lo;
+    }
     if (lane == 0) {
-        double x[6];
-        s_fast = fast_gated_solve(s_fin, static_cast<double>(st->cur_count), prm.theta, x) ? 1 : 0;
-        if (s_fast) {
-            finalize_motion(st, s_fin, x, prm);
-            *counter = 0;
-            st->t_end = globaltimer_ns();
-            if constexpr (COND)
-                cudaGraphSetConditional(cond, (!st->done && st->iterations < prm.max_iterations) ? 1u : 0u);
+        double b[6];
+        double cnt = 0.0;
+        for (int a = 0; a < 6; ++a) b[a] = INFINITY;
+        for (int r = 0; r < nrec; ++r) {
+            for (int a = 0; a < 6; ++a) b[a] = dmin(b[a], recs[r].box[a]);
+            cnt += recs[r].count;
+        }
+        const unsigned long long total = static_cast<unsigned long long>(cnt);
+        if (st->bodies == 0) st->t_assoc0 = globaltimer_ns();
+        st->bodies += 1;
+        s_lost = total < 10 ? 1 : 0;
+        if (total < 10) {  // TrackingLost (registration.cpp:202-204)
+            st->lost = 1;
+            st->lost_count = total;
+            st->done = 1;
+        } else {
+            st->matches = total;
+            st->cur_count = total;
+            const d3 l = mk(b[0], b[1], b[2]), hh = mk(-b[3], -b[4], -b[5]);
+            const d3 ext = sub(hh, l);
+            const d3 sc = mk(dmax(ext.x, prm.floor), dmax(ext.y, prm.floor), dmax(ext.z, prm.floor));
+            st->center = scale(0.5, add(l, hh));  // registration.cpp:60-63
+            st->scale = sc;
+            st->inv_scale = mk(1.0 / sc.x, 1.0 / sc.y, 1.0 / sc.z);
         }
     }
     __syncwarp();
-    if (s_fast) return;
-    __shared__ double s_A[36];
-    __shared__ Eig6 s_eig;
-    for (int i = lane; i < 36; i += 32) {
-        const int r = i / 6, cc = i % 6;
-        s_A[i] = s_fin[r <= cc ? packed_index(r, cc) : packed_index(cc, r)];
+    if (s_lost) {
+        if constexpr (COND) {
+            if (lane == 0) cudaGraphSetConditional(cond, 0u);
+        }
+        return;
     }
-    __syncwarp();
-    eigendecompose_sym6_warp_rr(s_A, &s_eig);
-    __syncwarp();
-    if (lane == 0) {
-        solve_finalize(st, s_fin, s_eig, prm);
-        *counter = 0;
-        st->t_end = globaltimer_ns();
-        if constexpr (COND)
-            cudaGraphSetConditional(cond, (!st->done && st->iterations < prm.max_iterations) ? 1u : 0u);
-    }
+    solve_from_sums<COND>(st, s_sum, s_fin, prm, counter, cond);
 }
 
 // ---------------------------------------------------------------------------------
@@ -908,6 +1004,82 @@ void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* 
     const cudaError_t ee = cudaStreamEndCapture(bs, &captured);
     SF_CUDA(le);
     SF_CUDA(ee);
+}
+
+// Sharded ICP (north star: "ICP partial sums combined with a 27-float allreduce"): per
+// iteration every local rank's PARTIAL pass over its slice of the source pixels, the reduction
+// of the ranks' records (`reduce`: nothing for in-process ranks, whose records the solve merges
+// in rank order; NCCL all-reduces for one rank per process), then k_icp_solve_ranks, identical
+// on every rank. Under capture with allow_loop the iterations are a conditional WHILE node as
+// in launch_icp; otherwise max_iterations bodies are issued and converged ones exit at once.
+void launch_icp_ranks(IcpWork& wk, const float* src, const float* src_n, const float* tgt, const float* tgt_n,
+                      const Intr& I, const double* d_initial, const IcpParamsDev& prm, int rank0, int nlocal,
+                      int world, IcpRankPartial* recs, int nrec, const std::function<void(cudaStream_t)>& reduce,
+                      bool allow_loop, cudaStream_t s, uint64_t* launches, const int* dead, bool* device_loop) {
+    SF_CUDA(cudaFuncSetAttribute(k_icp_step<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem));
+    SF_CUDA(cudaFuncSetAttribute(k_icp_step<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem));
+    const int n = I.w * I.h;
+    auto body = [&](cudaStream_t bs, bool cond_on, cudaGraphConditionalHandle cond) {
+        for (int i = 0; i < nlocal; ++i) {
+            const int r = rank0 + i;
+            const int p0 = static_cast<int>(static_cast<long long>(n) * r / world);
+            const int p1 = static_cast<int>(static_cast<long long>(n) * (r + 1) / world);
+            if (cond_on)
+                k_icp_step<true, true><<<kStepCtas, kIcpThreads, kStepSmem, bs>>>(
+                    src, src_n, tgt, tgt_n, I, I, prm, wk.st, wk.part_bbox, wk.part_count, wk.part, wk.counters + 2,
+                    cond, p0, p1, recs + i);
+            else
+                k_icp_step<false, true><<<kStepCtas, kIcpThreads, kStepSmem, bs>>>(
+                    src, src_n, tgt, tgt_n, I, I, prm, wk.st, wk.part_bbox, wk.part_count, wk.part, wk.counters + 2,
+                    0, p0, p1, recs + i);
+            SF_LAUNCH_CHECK();
+        }
+        reduce(bs);
+        if (cond_on) k_icp_solve_ranks<true><<<1, 32, 0, bs>>>(wk.st, recs, nrec, prm, wk.counters + 3, cond);
+        else k_icp_solve_ranks<false><<<1, 32, 0, bs>>>(wk.st, recs, nrec, prm, wk.counters + 3, 0);
+        SF_LAUNCH_CHECK();
+    };
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    SF_CUDA(cudaStreamIsCapturing(s, &cs));
+    const bool loop = allow_loop && cs == cudaStreamCaptureStatusActive && prm.max_iterations > 0;
+    if (device_loop) *device_loop = loop;
+    if (!loop) {
+        k_icp_init<false><<<1, 1, 0, s>>>(wk.st, d_initial, dead, prm.max_iterations, 0);
+        SF_LAUNCH_CHECK();
+        for (int it = 0; it < prm.max_iterations; ++it) body(s, false, 0);
+        if (launches) *launches += 1 + static_cast<uint64_t>(prm.max_iterations) * (nlocal + 1);
+        return;
+    }
+    cudaGraph_t g = nullptr;
+    SF_CUDA(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, nullptr, nullptr));
+    cudaGraphConditionalHandle cond;
+    SF_CUDA(cudaGraphConditionalHandleCreate(&cond, g, 0, 0));
+    k_icp_init<true><<<1, 1, 0, s>>>(wk.st, d_initial, dead, prm.max_iterations, cond);
+    SF_LAUNCH_CHECK();
+    if (launches) *launches += 1;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    SF_CUDA(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &ndeps));
+    cudaGraphNodeParams cp = {cudaGraphNodeTypeConditional};
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    SF_CUDA(cudaGraphAddNode(&node, g, deps, ndeps, &cp));
+    SF_CUDA(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+    if (!wk.body_stream) SF_CUDA(cudaStreamCreateWithFlags(&wk.body_stream, cudaStreamNonBlocking));
+    cudaStream_t bs = wk.body_stream;
+    SF_CUDA(cudaStreamBeginCaptureToGraph(bs, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeThreadLocal));
+    try {
+        body(bs, true, cond);
+    } catch (...) {
+        cudaGraph_t g2 = nullptr;
+        cudaStreamEndCapture(bs, &g2);
+        throw;
+    }
+    cudaGraph_t captured = nullptr;
+    SF_CUDA(cudaStreamEndCapture(bs, &captured));
 }
 
 void launch_icp_report(IcpWork& wk, cudaStream_t s, uint64_t* launches) {

@@ -1,6 +1,8 @@
 // sf_icp.cuh — ICP device state shared by sf_icp.cu and the tracker.
 #pragma once
 
+#include <functional>
+
 #include "sf_internal.h"
 
 namespace sf {
@@ -50,6 +52,16 @@ struct IcpState {
     double A_last[21];  // packed upper triangle of the last iteration's (shrunk) normal matrix
     unsigned long long t_begin, t_end;  // device clock (ns): state init, end of the last solve
     unsigned long long t_step0, t_assoc0;  // first step: first CTA start, association done (tail start)
+};
+
+// One rank's share of an iteration's normal equations (sharded ICP): the 28 unshrunk sums as
+// double-double pairs, the match count, the box as (lo, -hi) so that one MIN all-reduce
+// combines it. An NCCL SUM over sums[] + count and a MIN over box[] merge the ranks.
+struct IcpRankPartial {
+    double sums[2 * kSums];
+    double count;
+    double box[6];
+    double pad;
 };
 
 struct IcpParamsDev {
@@ -144,6 +156,13 @@ __device__ inline void icp_state_init(IcpState* st, const double* initial12, boo
     *st = z;
 }
 void fill_icp_result(const IcpState& st, sf_icp_result* out);
+// Sharded ICP: partial sums over pixel slices per local rank, `reduce` across processes (NCCL),
+// replicated solve (sf_icp.cu). recs: nlocal records (this process's ranks); nrec: records the
+// solve merges after `reduce` (nlocal in-process, 1 after an all-reduce across processes).
+void launch_icp_ranks(IcpWork& wk, const float* src, const float* src_n, const float* tgt, const float* tgt_n,
+                      const Intr& I, const double* d_initial, const IcpParamsDev& prm, int rank0, int nlocal,
+                      int world, IcpRankPartial* recs, int nrec, const std::function<void(cudaStream_t)>& reduce,
+                      bool allow_loop, cudaStream_t s, uint64_t* launches, const int* dead, bool* device_loop);
 // Eigenpairs of the last iteration when the fast gated solve deferred them (one warp).
 void launch_icp_report(IcpWork& wk, cudaStream_t s, uint64_t* launches);
 

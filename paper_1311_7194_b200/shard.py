@@ -225,6 +225,11 @@ class ShardFrameMetrics:
     voxels_updated: int = 0  # summed over ranks
     blocks_total: int = 0    # summed over ranks
     hit_pixels: int = 0      # composite
+    status: int = 0
+    halo_records: int = 0    # native tracker: records packed this frame (all ranks)
+    halo_overflow: int = 0   # records beyond the per-rank capacity (not exchanged)
+    kernel_launches: int = 0
+    icp_steps: int = 0
 
 
 class ShardedTracker:
@@ -268,6 +273,67 @@ class ShardedTracker:
         m = ShardFrameMetrics(self.k, reg, pose, it, nm_, vu, bt, hits)
         self.k += 1
         return m
+
+
+class NativeShardedTracker:
+    """The sharded fused frame as ONE CUDA graph per frame (sf_shard_tracker_*, csrc/sf_shard.cu):
+    global ray bounds, per-rank march of the rays its own blocks meet, nearest-depth composite,
+    ICP (``icp_mode`` 0: replicated; 1: partial sums over pixel slices + all-reduce), per-rank
+    fuse and halo exchange, with no host synchronisation inside a frame. ``comm`` is a
+    LocalComm (``shards`` = all ranks, in this process) or a DistComm (``shards`` = this rank;
+    NCCL communicator bootstrapped through torch.distributed)."""
+
+    TRACK, GROUND_TRUTH, TRACK_WITH_HOOK = 0, 1, 2
+
+    def __init__(self, shards: List[ShardVolume], comm, camera: Intrinsics, fusion: FusionParams,
+                 match: MatchParams, initial_pose: Pose, icp_mode: int = 0, halo_capacity: int = 0,
+                 use_graphs: bool = True):
+        self.shards, self.comm = shards, comm
+        be = default_backend()
+        self._lib = be.lib
+        self.backend = be
+        base = A.TrackerConfigC(fusion.c(), match.c(), camera.c(), 1 if use_graphs else 0, 0)
+        cfg = A.ShardTrackerConfigC(base, int(icp_mode), 0, int(halo_capacity))
+        p12 = initial_pose.to12()
+        h = C.c_void_p()
+        if isinstance(comm, DistComm):
+            import torch.distributed as dist
+
+            uid = torch.zeros(128, dtype=torch.uint8)
+            if comm.ranks[0] == 0:
+                be.check(self._lib.nccl_unique_id(uid.data_ptr()))
+            obj = [bytes(uid.numpy())]
+            dist.broadcast_object_list(obj, src=0, group=comm.group)
+            raw = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+            be.check(self._lib.shard_tracker_create_nccl(shards[0].grid.handle, raw, comm.ranks[0], comm.world,
+                                                         C.byref(cfg), _dptr(p12), C.byref(h)))
+        else:
+            vols = (C.c_void_p * len(shards))(*[s.grid.handle.value for s in shards])
+            be.check(self._lib.shard_tracker_create_local(vols, len(shards), C.byref(cfg), _dptr(p12), C.byref(h)))
+        self.handle = h
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            try:
+                self._lib.shard_tracker_destroy(self.handle)
+            except Exception:
+                pass
+            self.handle = None
+
+    def step(self, frame: DepthFrame, mode: int = 0, gt_pose: Optional[Pose] = None, stream=None):
+        fc = frame.c()
+        g = _dptr(gt_pose.to12()) if gt_pose is not None else None
+        self.backend.check(self._lib.shard_tracker_step(self.handle, C.byref(fc), mode, g, stream))
+
+    def set_pose(self, pose: Pose, stream=None):
+        self.backend.check(self._lib.shard_tracker_set_pose(self.handle, _dptr(pose.to12()), stream))
+
+    def fetch(self, stream=None) -> "ShardFrameMetrics":
+        m = A.ShardFrameMetricsC()
+        self.backend.check(self._lib.shard_tracker_fetch(self.handle, C.byref(m), stream))
+        return ShardFrameMetrics(m.frame, bool(m.registered), Pose.from12(list(m.pose)), m.iterations, m.matches,
+                                 m.voxels_updated, m.blocks_total, m.hit_pixels, m.status, m.halo_records,
+                                 m.halo_overflow, m.kernel_launches, m.icp_steps)
 
 
 def union_blocks(grids: List[SparseTsdfGrid], shards: Optional[List[ShardVolume]] = None):

@@ -141,3 +141,81 @@ def test_sharded_c5_full_scale(gpu):
         del tr, shards
     assert runs[0] == runs[1]
     assert runs[0][-1][2] > 10000
+
+
+@pytest.mark.parametrize("world,icp_mode", [(1, 0), (2, 0), (3, 0), (2, 1), (3, 1)])
+def test_native_sharded_tracker_matches_single_volume(gpu, world, icp_mode):
+    """The native sharded frame (one CUDA graph per frame: global bounds, per-rank march of the
+    rays its blocks meet, composite, ICP, per-rank fuse, in-graph halo exchange) against the
+    single-volume tracker on the C5 geometry. Replicated ICP (icp_mode 0): identical poses,
+    matches, blocks and voxel counts every frame. Partial sums + all-reduce (icp_mode 1): the
+    sums are merged per rank slice, so the pose agrees to ~1e-15 per call (tolerance 1e-6 over
+    the sequence) and the match counts are equal."""
+    cfg, shards = _small_c5(world)
+    intr = scenes.camera(320, 240, 262.5)
+    traj = scenes.c5_trajectory(100, radius=0.9)[:6]
+    frames = _frames(gpu, scenes.c5_scene(), traj, intr, cfg.box_side, sigma0=4e-4)
+    fusion = sf.FusionParams(mode=sf.FusionMode.Kalman)
+    match = sf.MatchParams.for_voxel_size(cfg.voxel_size)
+    tr = shard.NativeShardedTracker(shards, shard.LocalComm(world), intr, fusion, match, traj[0], icp_mode=icp_mode)
+    single = sf.SparseTsdfGrid(cfg, 220_000, sf.AuxMode.Variance, p_min=1e-12)
+    st = sf.Tracker(single, intr, fusion, match, traj[0])
+    for k, f in enumerate(frames):
+        ext = sf.compose(sf.invert(traj[k - 1]), traj[k]) if k else sf.Pose.identity()
+        tr.step(f, tr.TRACK_WITH_HOOK, ext)
+        st.step(f, sf.Tracker.TRACK_WITH_HOOK, ext)
+        m, ms = tr.fetch(), st.fetch()
+        assert m.status == 0 and m.halo_overflow == 0
+        dp = float(np.abs(m.pose.to12() - ms.pose.to12()).max())
+        if icp_mode == 0:
+            assert dp == 0.0, f"frame {k}: pose differs by {dp}"
+            assert m.voxels_updated == ms.fusion.voxels_updated and m.blocks_total == ms.fusion.blocks_total
+        else:
+            assert dp < 1e-6
+        if k:
+            assert m.registered and m.matches == ms.matches
+            # composite == single-volume raycast except for rays whose stage-1 bracket spans a chi
+            # gap reaching across owners (DESIGN.md §6, residual case): the previous valid sample
+            # lies outside the owner's blocks and halo; ~1 pixel in 10^4 here
+            assert abs(m.hit_pixels - ms.raycast.hit_pixels) <= max(1, ms.raycast.hit_pixels // 2000)
+            if world == 1:
+                assert m.hit_pixels == ms.raycast.hit_pixels
+        if world > 1 and k:
+            assert m.halo_records > 0
+    if icp_mode == 0:
+        got = shard.union_blocks([s.grid for s in shards], shards)
+        want = shard.union_blocks([single])
+        assert got.keys() == want.keys() and got == want
+
+
+def test_native_sharded_tracker_nccl_one_rank(gpu):
+    """The NCCL backend with a single rank (the collectives run, as identities) gives the same
+    frames as the in-process backend: the code path a multi-GPU run takes, on one GPU."""
+    import os
+
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29561")
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    cfg, _ = _small_c5(1)
+    intr = scenes.camera(320, 240, 262.5)
+    traj = scenes.c5_trajectory(100, radius=0.9)[:4]
+    frames = _frames(gpu, scenes.c5_scene(), traj, intr, cfg.box_side, sigma0=4e-4)
+    fusion = sf.FusionParams(mode=sf.FusionMode.Kalman)
+    match = sf.MatchParams.for_voxel_size(cfg.voxel_size)
+    runs = []
+    for comm in (shard.LocalComm(1), shard.DistComm()):
+        for icp_mode in (0, 1):
+            vol = shard.ShardVolume(cfg, 220_000, sf.AuxMode.Variance, 0, 1, p_min=1e-12)
+            tr = shard.NativeShardedTracker([vol], comm, intr, fusion, match, traj[0], icp_mode=icp_mode)
+            out = []
+            for k, f in enumerate(frames):
+                ext = sf.compose(sf.invert(traj[k - 1]), traj[k]) if k else sf.Pose.identity()
+                tr.step(f, tr.TRACK_WITH_HOOK, ext)
+                m = tr.fetch()
+                out.append((m.pose.to12().tobytes(), m.matches, m.blocks_total, m.voxels_updated, m.hit_pixels))
+            runs.append(out)
+            del tr, vol
+    assert runs[0] == runs[2] and runs[1] == runs[3]
