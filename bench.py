@@ -228,6 +228,16 @@ def aggregate_ranks(total_ms, e2e_ms, steps, world, device, dist=None):
     return total_ms, e2e_ms, world * steps / (total_ms * 1e-3), world * steps / (e2e_ms * 1e-3)
 
 
+def max_over_ranks(ms, device, dist=None):
+    """The slowest rank's device time (the contract's max over ranks)."""
+    import torch
+
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    if dist is not None and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def replicas_consistent(signature, device, dist=None, world=1):
     """Every rank runs the same synthetic sequence on its own GPU: their result signatures
     (final pose, block count, voxels updated) must agree bit for bit."""
@@ -744,11 +754,7 @@ def sharded_c5(args, world, rank, local, nshards, dist=None, icp_mode=0, clocks=
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    total_ms = sum(ev0[i].elapsed_time(ev1[i]) for i in range(steps))
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms = max_over_ranks(sum(ev0[i].elapsed_time(ev1[i]) for i in range(steps)), dev, dist)
     if any(m.status for m in metrics):
         raise RuntimeError(f"sharded run failed: {[m.status for m in metrics]}")
     gt = poses[nframes - 1]

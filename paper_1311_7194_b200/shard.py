@@ -275,6 +275,21 @@ class ShardedTracker:
         return m
 
 
+def broadcast_nccl_id(comm: "DistComm") -> bytes:
+    """NCCL bootstrap of the native sharded frame: rank 0 makes the 128-byte ncclUniqueId
+    (sf_nccl_unique_id) and the torch.distributed group broadcasts it to every rank."""
+    import torch.distributed as dist
+
+    obj = [None]
+    if comm.ranks[0] == 0:
+        uid = (C.c_uint8 * 128)()
+        be = default_backend()
+        be.check(be.lib.nccl_unique_id(uid))
+        obj = [bytes(uid)]
+    dist.broadcast_object_list(obj, src=0, group=comm.group)
+    return obj[0]
+
+
 class NativeShardedTracker:
     """The sharded fused frame as ONE CUDA graph per frame (sf_shard_tracker_*, csrc/sf_shard.cu):
     global ray bounds, per-rank march of the rays its own blocks meet, nearest-depth composite,
@@ -297,14 +312,7 @@ class NativeShardedTracker:
         p12 = initial_pose.to12()
         h = C.c_void_p()
         if isinstance(comm, DistComm):
-            import torch.distributed as dist
-
-            uid = torch.zeros(128, dtype=torch.uint8)
-            if comm.ranks[0] == 0:
-                be.check(self._lib.nccl_unique_id(uid.data_ptr()))
-            obj = [bytes(uid.numpy())]
-            dist.broadcast_object_list(obj, src=0, group=comm.group)
-            raw = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+            raw = (C.c_uint8 * 128).from_buffer_copy(broadcast_nccl_id(comm))
             be.check(self._lib.shard_tracker_create_nccl(shards[0].grid.handle, raw, comm.ranks[0], comm.world,
                                                          C.byref(cfg), _dptr(p12), C.byref(h)))
         else:

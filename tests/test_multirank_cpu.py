@@ -24,8 +24,12 @@ def _worker(rank, world, port, q):
     w, r, _ = bench.dist_setup()
     total, e2e, value, e2e_value = bench.aggregate_ranks(10.0 + rank, 20.0 - rank, 8, world, "cpu", dist)
     same = bench.replicas_consistent([1.0, 2.0, 3.0], "cpu", dist, world)
+    slowest = bench.max_over_ranks(3.0 + 4.0 * rank, "cpu", dist)  # the sharded (N > 1) line's timing
+    from paper_1311_7194_b200 import shard
+
+    uid = shard.broadcast_nccl_id(shard.DistComm())  # the sharded frame's NCCL bootstrap
     differ = bench.replicas_consistent([1.0, 2.0, float(rank)], "cpu", dist, world)
-    q.put((rank, w, r, total, e2e, value, e2e_value, same, differ))
+    q.put((rank, w, r, total, e2e, value, e2e_value, same, differ, slowest, uid))
     dist.destroy_process_group()
 
 
@@ -40,8 +44,10 @@ def test_two_rank_aggregation_gloo():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, w, r, total, e2e, value, e2e_value, same, differ in out:
+    assert out[0][-1] == out[1][-1] and len(out[0][-1]) == 128 and any(out[0][-1])  # same NCCL id on both ranks
+    for rank, w, r, total, e2e, value, e2e_value, same, differ, slowest, _ in out:
         assert (w, r) == (2, rank)
+        assert slowest == 7.0
         assert total == 11.0 and e2e == 20.0          # max over ranks
         assert value == pytest.approx(2 * 8 / 11e-3)  # whole-job aggregate
         assert e2e_value == pytest.approx(2 * 8 / 20e-3)
