@@ -543,6 +543,14 @@ def run_ours(args, world, rank, local):
     same_blocks = bool(np.array_equal(g_f2.read_table(), g_p1.read_table()))
     del g_f2, g_p1
 
+    # raycast stage (ray bounds + march + refine): the reference's block_slot
+    # reads of its DDA (4 B per cell walked), 20 B per trilinear sample (8 payload cells + the
+    # block's table entry) over stage 1 and stage 2 + gradient, and the 16 B/pixel depth + normal
+    ray_ms = [s[0] for s in stage]
+    ray_bytes = [mm.ray_dda_cells * 4 + (mm.raycast.sample_steps + mm.ray_refine_samples) * 20 + px * 16
+                 for mm in metrics_b]
+    ray_achieved = sum(ray_bytes) / (sum(ray_ms) * 1e-3) / 1e9
+
     # ICP stage (association is L2/HBM-bound: 32 B per pixel per iteration):
     # source depth + normals (16 B) and the projected target depth + normals (16 B)
     icp_ms = [s[1] for s in stage]
@@ -634,6 +642,14 @@ def run_ours(args, world, rank, local):
             "algorithmic_bytes": "per processed block M^3 x (read + write) of the payload (float2: 8 + 8 B, codes: "
                                  "2 + 2 B per voxel) + its 8 B work item; per launch the 8 B/pixel {depth, p_k} table",
         },
+        "raycast_roofline": {"bound": "hbm", "stage": "raycast (k_ray_bounds + k_raycast + k_raycast_refine)",
+                             "achieved": ray_achieved, "peak": peak, "unit": "GB/s", "frac": ray_achieved / peak,
+                             "bytes_per_frame_mean": sum(ray_bytes) / steps, "ms_per_frame_mean": sum(ray_ms) / steps,
+                             "dda_cells_mean": sum(mm.ray_dda_cells for mm in metrics_b) / steps,
+                             "samples_mean": sum(mm.raycast.sample_steps + mm.ray_refine_samples
+                                                 for mm in metrics_b) / steps,
+                             "algorithmic_bytes": "4 B per reference DDA cell (rays reaching the occupied box) + "
+                                                  "20 B per trilinear sample (stage 1, secant, gradient) + 16 B/pixel"},
         "icp_roofline": {"bound": "hbm", "stage": "ICP (source normals + k_icp_step iterations)",
                          "achieved": icp_achieved, "peak": peak, "unit": "GB/s",
                          "frac": icp_achieved / peak if icp_achieved else None,

@@ -370,6 +370,8 @@ typedef struct {
     uint64_t icp_ns;           /* ICP span on the device clock: first step start to the end of the last iteration's solve */
     int32_t icp_steps;         /* ICP step launches this frame (device-side loop: one per iteration) */
     int32_t pad_;
+    uint64_t ray_dda_cells;      /* reference DDA cells of the rays reaching the occupied box (roofline count) */
+    uint64_t ray_refine_samples; /* stage-2 secant + gradient samples of the raycast */
 } sf_frame_metrics;
 
 int sf_tracker_create(sf_volume_t vol, const sf_tracker_config* config, const double initial_pose[12],

@@ -195,6 +195,8 @@ class FrameMetricsC(C.Structure):
         ("icp_ns", C.c_uint64),
         ("icp_steps", C.c_int32),
         ("pad_", C.c_int32),
+        ("ray_dda_cells", C.c_uint64),
+        ("ray_refine_samples", C.c_uint64),
     ]
 
 

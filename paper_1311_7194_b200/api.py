@@ -761,6 +761,8 @@ class FrameMetrics:
     integrate_ns: int = 0  # integrate kernel span on the device clock (first CTA start .. last CTA end)
     icp_ns: int = 0  # ICP span on the device clock (first step start .. end of the last solve)
     icp_steps: int = 0  # ICP step launches (device-side loop: one per iteration)
+    ray_dda_cells: int = 0  # reference DDA cells of the rays reaching the occupied box (roofline count)
+    ray_refine_samples: int = 0  # raycast stage-2 secant + gradient samples
 
 
 class Tracker:
@@ -811,7 +813,7 @@ class Tracker:
                             FusionStats(f.voxels_updated, f.blocks_allocated_now, f.blocks_total, f.memory_bytes),
                             RaycastStats(r.sample_steps, r.hit_pixels, r.rays_with_bounds),
                             m.blocks_processed, m.voxels_visited, m.kernel_launches, m.exact_voxels,
-                            m.integrate_ns, m.icp_ns, m.icp_steps)
+                            m.integrate_ns, m.icp_ns, m.icp_steps, m.ray_dda_cells, m.ray_refine_samples)
 
     def fetch(self, stream=None) -> FrameMetrics:
         m = A.FrameMetricsC()

@@ -195,6 +195,11 @@ struct RayCounters {
     unsigned long long sample_steps, hit_pixels, rays_with_bounds;
     unsigned long long listed;    // length of the active-ray list written by the ray-bounds pass
     unsigned long long brackets;  // rays the stage-1 march bracketed (refine-pass list length)
+    // algorithmic work (raycast roofline): cells the reference DDA walks for the
+    // rays that reach the occupied box (entry to exit cell within [near, far]), and the secant +
+    // gradient samples of stage 2
+    unsigned long long dda_cells;
+    unsigned long long refine_samples;
 };
 // A stage-1 bracket [a, b] with TSDF values (va > 0 > vb) of pixel idx (render.cpp:207-208).
 struct RayBracket {

@@ -170,12 +170,10 @@ __device__ __forceinline__ bool bounds_pixel(const VolParams& P, const FrameCons
                                              const uint32_t* __restrict__ occ, const VolCounters* __restrict__ vc,
                                              const uint32_t* __restrict__ s_coarse, float* __restrict__ t_start,
                                              float* __restrict__ t_end, int w, double jump_cells,
-                                             unsigned long long* __restrict__ dbg, int u, int v, double inv_fx,
-                                             double inv_fy) {
+                                             int u, int v, double inv_fx,
+                                             double inv_fy, unsigned long long& cells) {
     const size_t idx = (size_t)v * w + u;
     float ts = INFINITY, te = -INFINITY;
-    unsigned long long dbg_t0 = dbg ? globaltimer_ns() : 0ull;
-    unsigned dbg_steps = 0;
     if (vc->allocated_count != 0 && may_meet_occupied(P, fc, occ, u, v, inv_fx, inv_fy)) {
         const Intr& intr = fc->intr;
         const Pose& pose = fc->pose;
@@ -258,6 +256,16 @@ __device__ __forceinline__ bool bounds_pixel(const VolParams& P, const FrameCons
                     td = INFINITY;
                 }
             };
+            {
+                // cells of the reference DDA (render.cpp:103-144) from the entry cell to the cell
+                // at min(hi, box exit): one per plane crossing + 1 (for the roofline count only)
+                const double hx = org[0] + hi * dir[0], hy = org[1] + hi * dir[1], hz = org[2] + hi * dir[2];
+                const int qx = clampc(ref_floor_int((hx - box_lo[0]) / side));
+                const int qy = clampc(ref_floor_int((hy - box_lo[1]) / side));
+                const int qz = clampc(ref_floor_int((hz - box_lo[2]) / side));
+                cells += 1ull + static_cast<unsigned>(abs(qx - cx)) + static_cast<unsigned>(abs(qy - cy)) +
+                         static_cast<unsigned>(abs(qz - cz));
+            }
             Dda s;
             s.cx = cx;
             s.cy = cy;
@@ -270,7 +278,7 @@ __device__ __forceinline__ bool bounds_pixel(const VolParams& P, const FrameCons
             const double td_min = dmin(s.tdx, dmin(s.tdy, s.tdz));
             // Skip the run-up to the occupied box: every cell entered before the ray reaches
             // the box grown by one block lies outside the occupied box.
-            if (t_grown > lo + 4.0 * td_min) { dda_jump(s, t_grown); dbg_steps += 1u << 16; }
+            if (t_grown > lo + 4.0 * td_min) dda_jump(s, t_grown);
             const double sb_side = side * (1 << kCoarseShift);
             int declined_cc = -1;  // coarse cell whose skip was judged too short to jump
             // Loop state derived from the cells (recomputed after a jump, stepped otherwise):
@@ -306,7 +314,6 @@ __device__ __forceinline__ bool bounds_pixel(const VolParams& P, const FrameCons
             uint32_t pend_word = 0, pend_bit = 0;  // occupancy probe of the previous step
         double pend_tin = 0.0, pend_tout = 0.0;
         while (live && s.t_in <= hi) {
-                ++dbg_steps;
                 const int axis = s.tmx <= s.tmy ? (s.tmx <= s.tmz ? 0 : 2) : (s.tmy <= s.tmz ? 1 : 2);
                 const double tm = axis == 0 ? s.tmx : (axis == 1 ? s.tmy : s.tmz);
                 if (!cbit && cc != declined_cc) {
@@ -323,7 +330,7 @@ __device__ __forceinline__ bool bounds_pixel(const VolParams& P, const FrameCons
                     if (s.sz != 0) t_exit = dmin(t_exit, ((s.sz > 0 ? oz_ + sb_side : oz_) - org[2]) * inv_dir[2]);
                     const double T = dmin(t_exit, hi) - 0.25 * td_min;
                     // a jump costs a few hundred instructions: worth it past ~16 plain steps
-                    if (T > tm + jump_cells * td_min && (dbg_steps += 1u << 16, dda_jump(s, T))) {
+                    if (T > tm + jump_cells * td_min && dda_jump(s, T)) {
                         if (s.cx < 0 || s.cx >= n || s.cy < 0 || s.cy >= n || s.cz < 0 || s.cz >= n) break;
                         derive();
                         if (outside()) break;
@@ -380,11 +387,6 @@ __device__ __forceinline__ bool bounds_pixel(const VolParams& P, const FrameCons
     }
     t_start[idx] = ts;
     t_end[idx] = te;
-    if (dbg) {
-        dbg[3 * idx] = dbg_t0;
-        dbg[3 * idx + 1] = globaltimer_ns();
-        dbg[3 * idx + 2] = dbg_steps | ((unsigned long long)(blockIdx.x) << 32);
-    }
     return ts <= te;
 }
 
@@ -408,8 +410,7 @@ __global__ void __launch_bounds__(256, 2) k_ray_bounds(VolParams P, const FrameC
                              const VolCounters* __restrict__ vc, float* __restrict__ t_start,
                              float* __restrict__ t_end, int w, int h, const int* dead, int* __restrict__ ray_list,
                              RayCounters* list_ctr, float* __restrict__ depth_out, float* __restrict__ normals_out,
-                             double jump_cells, uint32_t* __restrict__ sched, const uint32_t* __restrict__ order,
-                             unsigned long long* __restrict__ dbg) {
+                             double jump_cells, uint32_t* __restrict__ sched, const uint32_t* __restrict__ order) {
     pdl_wait();
     extern __shared__ uint32_t s_coarse[];
     if (dead && *dead) return;
@@ -422,6 +423,7 @@ __global__ void __launch_bounds__(256, 2) k_ray_bounds(VolParams P, const FrameC
     const int ln = threadIdx.x & 31;
     const int pw = (w + 7) >> 3, n_patches = pw * ((h + 3) >> 2);
     const double inv_fx = 1.0 / fc->intr.fx, inv_fy = 1.0 / fc->intr.fy;
+    unsigned long long cells = 0;
     for (;;) {
         int patch = 0;
         if (ln == 0) patch = static_cast<int>(atomicAdd(&sched[0], 1u));
@@ -431,8 +433,8 @@ __global__ void __launch_bounds__(256, 2) k_ray_bounds(VolParams P, const FrameC
         const int u = (patch % pw) * 8 + (ln & 7);
         const int v = (patch / pw) * 4 + (ln >> 3);
         if (u >= w || v >= h) continue;
-        const bool act =
-            bounds_pixel(P, fc, occ, vc, s_coarse, t_start, t_end, w, jump_cells, dbg, u, v, inv_fx, inv_fy);
+        const bool act = bounds_pixel(P, fc, occ, vc, s_coarse, t_start, t_end, w, jump_cells, u, v, inv_fx,
+                                      inv_fy, cells);
         if (ray_list) {
             // Active-ray list for the march (warp-aggregated append); inactive pixels get the
             // empty raycast result here.
@@ -448,6 +450,10 @@ __global__ void __launch_bounds__(256, 2) k_ray_bounds(VolParams P, const FrameC
             }
             if (act) ray_list[base + __popc(bal & ((1u << ln) - 1u))] = idx;
         }
+    }
+    if (list_ctr) {
+        for (int off = 16; off > 0; off >>= 1) cells += __shfl_down_sync(0xffffffffu, cells, off);
+        if (ln == 0 && cells) atomicAdd(&list_ctr->dda_cells, cells);
     }
     // last CTA out resets the counters for the next launch
     __syncthreads();
@@ -570,8 +576,11 @@ __device__ __forceinline__ void march_ray(const VolParams& P, const FrameConsts*
     }
 }
 
+#ifndef SF_RAYCAST_CTAS
+#define SF_RAYCAST_CTAS 3
+#endif
 template <int G>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, SF_RAYCAST_CTAS)
     k_raycast(VolParams P, const FrameConsts* __restrict__ fc, const int32_t* __restrict__ table,
               const uint16_t* __restrict__ payload, const uint32_t* __restrict__ occ, const AuxTables* __restrict__ aux,
               const float* __restrict__ t_start, const float* __restrict__ t_end, float* __restrict__ depth_out,
@@ -609,8 +618,8 @@ __global__ void __launch_bounds__(256, 3)
 // Stage 2 + gradient normal of one bracketed ray (render.cpp:209-246); returns 1 for a hit.
 __device__ __forceinline__ unsigned refine_ray(const Sampler& S, const VolParams& P, const FrameConsts* __restrict__ fc,
                                                const RayBracket& b, float* __restrict__ depth_out,
-                                               float* __restrict__ normals_out, int w, int* iters = nullptr,
-                                               unsigned long long* t_mid = nullptr) {
+                                               float* __restrict__ normals_out, int w,
+                                               unsigned long long& samples) {
     const Intr& intr = fc->intr;
     const Pose& pose = fc->pose;
     const double vox = P.voxel;
@@ -624,12 +633,20 @@ __device__ __forceinline__ unsigned refine_ray(const Sampler& S, const VolParams
     float out_d = 0.0f, nx = 0.f, ny = 0.f, nz = 0.f;
     int64_t ckey = -1;
     int32_t cslot = kEmpty;
+    Sampler::CellCache cell;
     int iter = 0;
     for (; iter < 48 && hit_b - hit_a > fine_tol; ++iter) {
         double t_new = hit_b - val_b * (hit_b - hit_a) / (val_b - val_a);
         if (!(t_new > hit_a) || !(t_new < hit_b)) t_new = 0.5 * (hit_a + hit_b);
         double val;
+#ifndef SF_REFINE_CACHE
+#define SF_REFINE_CACHE 1
+#endif
+#if SF_REFINE_CACHE
+        if (!S.sample_cached(add(pose.t, scale(t_new, dir)), val, ckey, cslot, cell)) {
+#else
         if (!S.sample_near(add(pose.t, scale(t_new, dir)), val, ckey, cslot)) {
+#endif
             hit_a = t_new;
             val_a = dmax(val_a, 1e-12);
             continue;
@@ -642,8 +659,7 @@ __device__ __forceinline__ unsigned refine_ray(const Sampler& S, const VolParams
             val_b = val;
         }
     }
-    if (iters) *iters = iter;
-    if (t_mid) *t_mid = globaltimer_ns();
+    samples += iter;
     double root;
     if (val_b != val_a) {
         const double interp = hit_b - val_b * (hit_b - hit_a) / (val_b - val_a);
@@ -655,10 +671,18 @@ __device__ __forceinline__ unsigned refine_ray(const Sampler& S, const VolParams
     if (!(dd < intr.near_plane || dd > intr.far_plane)) {
         out_d = (float)dd;
         hits += 1;
+        samples += 6;
         // sample_tsdf_gradient (render.cpp:50-63)
         const d3 p = add(pose.t, scale(root, dir));
         d3 gr;
+#ifndef SF_GRAD_PAR
+#define SF_GRAD_PAR 0
+#endif
+#if SF_GRAD_PAR
+        if (S.gradient_par(p, vox, gr, ckey, cslot) && sqnorm(gr) > 0.0) {
+#else
         if (S.gradient_near(p, vox, gr, ckey, cslot) && sqnorm(gr) > 0.0) {
+#endif
             // world_to_cam * grad.normalized()  (render.cpp:242-245)
             const d3 n_cam = mv(mt(pose.R), normalized(gr));
             nx = (float)n_cam.x;
@@ -681,7 +705,7 @@ __global__ void __launch_bounds__(256)
                      const uint16_t* __restrict__ payload, const uint32_t* __restrict__ occ,
                      const AuxTables* __restrict__ aux, const RayBracket* __restrict__ brackets,
                      float* __restrict__ depth_out, float* __restrict__ normals_out, RayCounters* stats, int w,
-                     const int* dead, unsigned long long* __restrict__ dbg) {
+                     const int* dead) {
     pdl_wait();
     __shared__ double s_tdec[256];
     if (dead && *dead) return;
@@ -689,55 +713,22 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     const Sampler S{P, table, payload, occ, s_tdec};
     const unsigned long long n = stats->brackets;
-    unsigned long long hits = 0;
+    unsigned long long hits = 0, samples = 0;
     for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
          i += (unsigned long long)gridDim.x * blockDim.x) {
-        const RayBracket b = brackets[i];
-        if (dbg) {  // SF_RF_DEBUG: per-ray {start, end of the secant loop, end, iterations | idx}
-            const unsigned long long t0 = globaltimer_ns();
-            int it = 0;
-            unsigned long long tm = 0;
-            hits += refine_ray(S, P, fc, b, depth_out, normals_out, w, &it, &tm);
-            dbg[4 * i] = t0;
-            dbg[4 * i + 1] = tm;
-            dbg[4 * i + 2] = globaltimer_ns();
-            dbg[4 * i + 3] = static_cast<unsigned long long>(it) | (static_cast<unsigned long long>(b.idx) << 32);
-        } else {
-            hits += refine_ray(S, P, fc, b, depth_out, normals_out, w);
-        }
+        hits += refine_ray(S, P, fc, brackets[i], depth_out, normals_out, w, samples);
     }
-    for (int off = 16; off > 0; off >>= 1) hits += __shfl_down_sync(0xffffffffu, hits, off);
+    for (int off = 16; off > 0; off >>= 1) {
+        hits += __shfl_down_sync(0xffffffffu, hits, off);
+        samples += __shfl_down_sync(0xffffffffu, samples, off);
+    }
     if ((threadIdx.x & 31) == 0 && hits) atomicAdd(&stats->hit_pixels, hits);
+    if ((threadIdx.x & 31) == 0 && samples) atomicAdd(&stats->refine_samples, samples);
 }
 
 // Minimum number of DDA cells an exact skip must save (a jump costs a few hundred
 // instructions; shorter crossings of empty super-blocks are stepped without occupancy reads).
-static double ray_jump_cells() {
-    static const double j = [] {
-        const char* e = std::getenv("SF_RAY_JUMP_CELLS");
-        return e ? std::atof(e) : 16.0;
-    }();
-    return j;
-}
-
-// Debug (SF_RB_DEBUG=<path>): per-ray start/end device times and DDA step counts of every
-// ray-bounds launch appended to <path> (synchronises the stream; never in a captured graph).
-static unsigned long long* rb_debug_buffer(size_t n) {
-    static unsigned long long* buf = nullptr;
-    if (!std::getenv("SF_RB_DEBUG")) return nullptr;
-    if (!buf) SF_CUDA(cudaMalloc(&buf, 3 * n * sizeof(unsigned long long)));
-    return buf;
-}
-static void rb_debug_dump(unsigned long long* buf, size_t n, cudaStream_t s) {
-    if (!buf) return;
-    std::vector<unsigned long long> h(3 * n);
-    SF_CUDA(cudaMemcpyAsync(h.data(), buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    SF_CUDA(cudaStreamSynchronize(s));
-    if (FILE* f = std::fopen(std::getenv("SF_RB_DEBUG"), "ab")) {
-        std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
-        std::fclose(f);
-    }
-}
+constexpr double kRayJumpCells = 16.0;
 
 // Patch order of k_ray_bounds: 8x4 patches sorted by the distance of their centre to the
 // image centre (built once per image size, outside graph capture: ensure_frame_buffers).
@@ -764,16 +755,14 @@ void ensure_patch_order(Volume& v, int w, int h) {
 void launch_ray_bounds(Volume& v, const FrameConsts* d_fc, const Intr& intr, float* t_start, float* t_end,
                        cudaStream_t s, uint64_t* launches, const int* dead_flag, int* ray_list,
                        RayCounters* list_ctr, float* depth, float* normals) {
-    unsigned long long* rb_dbg = rb_debug_buffer((size_t)intr.w * intr.h);
     ensure_patch_order(v, intr.w, intr.h);
     const dim3 blk(256), grd(148 * 2);
     const uint64_t nc = v.P.Nc;
     const size_t smem = ((nc * nc * nc + 31) / 32) * sizeof(uint32_t);
     if (smem > 48 * 1024) SF_CUDA(cudaFuncSetAttribute(k_ray_bounds, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     launch_pdl(k_ray_bounds, grd, blk, smem, s, v.P, d_fc, v.d_occ, v.d_vc, t_start, t_end, intr.w, intr.h,
-               dead_flag, ray_list, list_ctr, depth, normals, ray_jump_cells(), v.d_sched, v.d_patch_order, rb_dbg);
+               dead_flag, ray_list, list_ctr, depth, normals, kRayJumpCells, v.d_sched, v.d_patch_order);
     SF_LAUNCH_CHECK();
-    rb_debug_dump(rb_dbg, (size_t)intr.w * intr.h, s);
     if (launches) *launches += 1;
 }
 
@@ -839,24 +828,9 @@ void launch_raycast(Volume& v, const FrameConsts* d_fc, const Intr& intr, const 
                depth, normals, d_stats, intr.w, intr.h, dead_flag, ray_list, brackets);
     SF_LAUNCH_CHECK();
     // one warp per CTA: the ~30 k bracketed rays spread over all SMs (latency-bound, few warps)
-    static unsigned long long* rf_dbg = nullptr;  // SF_RF_DEBUG=<path>: per-ray refine timing (graph-less runs)
-    const char* rf_path = std::getenv("SF_RF_DEBUG");
-    if (rf_path && !rf_dbg) SF_CUDA(cudaMalloc(&rf_dbg, 4ull * intr.w * intr.h * sizeof(unsigned long long)));
     launch_pdl(k_raycast_refine, dim3(148 * 16), dim3(32), 0, s, v.P, d_fc, v.d_table, v.d_payload, v.d_occ,
-               v.d_aux, brackets, depth, normals, d_stats, intr.w, dead_flag, rf_path ? rf_dbg : nullptr);
+               v.d_aux, brackets, depth, normals, d_stats, intr.w, dead_flag);
     SF_LAUNCH_CHECK();
-    if (rf_path) {
-        unsigned long long nb = 0;
-        SF_CUDA(cudaMemcpyAsync(&nb, &d_stats->brackets, sizeof(nb), cudaMemcpyDeviceToHost, s));
-        SF_CUDA(cudaStreamSynchronize(s));
-        std::vector<unsigned long long> hb(4 * nb + 1);
-        hb[0] = nb;
-        if (nb) SF_CUDA(cudaMemcpy(hb.data() + 1, rf_dbg, 4 * nb * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-        if (FILE* f = std::fopen(rf_path, "ab")) {
-            std::fwrite(hb.data(), sizeof(unsigned long long), hb.size(), f);
-            std::fclose(f);
-        }
-    }
     if (launches) *launches += 2;
 }
 

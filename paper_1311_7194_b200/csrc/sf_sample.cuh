@@ -174,6 +174,90 @@ struct Sampler {
         return true;
     }
 
+    // The 8 decoded corners of the last voxel cell sampled by sample_cached (or its nullopt).
+    struct CellCache {
+        int bx = -1, by = -1, bz = -1;
+        bool ok = false;
+        double c[8];
+    };
+    // sample_near for the secant iterations of one ray: once the bracket is inside one voxel
+    // cell, successive samples share the cell's 8 corners, which are reused instead of
+    // reloaded (same corner values, same fractions, same arithmetic: bit-identical).
+    __device__ bool sample_cached(d3 p, double& out, int64_t& ckey, int32_t& cslot, CellCache& cc) const {
+        if (P.mshift < 0) return sample(p, out);
+        const double gx = div_voxel(p.x - P.ox) - 0.5;
+        const double gy = div_voxel(p.y - P.oy) - 0.5;
+        const double gz = div_voxel(p.z - P.oz) - 0.5;
+        constexpr double kLim = 1073741824.0;
+        if (!(fabs(gx) < kLim && fabs(gy) < kLim && fabs(gz) < kLim)) return false;
+        int bx, by, bz;
+        const double flx = floor_exact(gx, bx), fly = floor_exact(gy, by), flz = floor_exact(gz, bz);
+        const int res = P.res;
+        if (bx < 0 || by < 0 || bz < 0 || bx + 1 >= res || by + 1 >= res || bz + 1 >= res) return false;
+        const double fx = gx - flx, fy = gy - fly, fz = gz - flz;
+        if (bx != cc.bx || by != cc.by || bz != cc.bz) {
+            const int ms = P.mshift, mm = P.M - 1, N = P.N;
+            const int lx = bx & mm, ly = by & mm, lz = bz & mm;
+            const bool cx = lx == mm, cy = ly == mm, cz = lz == mm;
+            const int kb = ((bz >> ms) * N + (by >> ms)) * N + (bx >> ms);
+            const int32_t sb = kb == ckey ? cslot : __ldg(&table[kb]);
+            const int NN = N * N;
+            bool ok = true;
+            uint16_t pl[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const bool ox = (i & 1) && cx, oy = ((i >> 1) & 1) && cy, oz = (i >> 2) && cz;
+                const int32_t sl =
+                    (ox || oy || oz) ? __ldg(&table[kb + (ox ? 1 : 0) + (oy ? N : 0) + (oz ? NN : 0)]) : sb;
+                const int vx = ox ? 0 : lx + (i & 1), vy = oy ? 0 : ly + ((i >> 1) & 1), vz = oz ? 0 : lz + (i >> 2);
+                ok = ok && sl != kEmpty;
+                pl[i] = sl != kEmpty ? __ldg(&payload[((size_t)sl << (3 * ms)) + (((vz << ms) + vy) << ms) + vx])
+                                     : static_cast<uint16_t>(kChiPayload);
+            }
+            ckey = kb;
+            cslot = sb;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int8_t code = static_cast<int8_t>(pl[i] & 0xFF);
+                ok = ok && code != kChiCode;
+                cc.c[i] = tdec[(int)code + 128];
+            }
+            cc.bx = bx;
+            cc.by = by;
+            cc.bz = bz;
+            cc.ok = ok;
+        }
+        if (!cc.ok) return false;
+        const double* c = cc.c;
+        const double x0 = c[0] + (c[1] - c[0]) * fx;
+        const double x1 = c[2] + (c[3] - c[2]) * fx;
+        const double x2 = c[4] + (c[5] - c[4]) * fx;
+        const double x3 = c[6] + (c[7] - c[6]) * fx;
+        const double y0 = x0 + (x1 - x0) * fy;
+        const double y1 = x2 + (x3 - x2) * fy;
+        out = y0 + (y1 - y0) * fz;
+        return true;
+    }
+
+    // sample_tsdf_gradient (render.cpp:50-63) with the six samples independent of each other
+    // (issued together instead of one after the other; the reference's early exit on a
+    // nullopt only skips samples whose values would be discarded: same result).
+    __device__ bool gradient_par(d3 p, double h, d3& g, int64_t ckey, int32_t cslot) const {
+        double v[6];
+        bool ok[6];
+        const d3 q[6] = {mk(p.x + h, p.y, p.z), mk(p.x - h, p.y, p.z), mk(p.x, p.y + h, p.z),
+                         mk(p.x, p.y - h, p.z), mk(p.x, p.y, p.z + h), mk(p.x, p.y, p.z - h)};
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            int64_t k = ckey;
+            int32_t sl = cslot;
+            ok[i] = sample_near(q[i], v[i], k, sl);
+        }
+        if (!(ok[0] && ok[1] && ok[2] && ok[3] && ok[4] && ok[5])) return false;
+        g = mk((v[0] - v[1]) / (2.0 * h), (v[2] - v[3]) / (2.0 * h), (v[4] - v[5]) / (2.0 * h));
+        return true;
+    }
+
     // sample_tsdf_gradient (render.cpp:50-63) with the near-surface sampler
     __device__ bool gradient_near(d3 p, double h, d3& g, int64_t& ckey, int32_t& cslot) const {
         double a, b;

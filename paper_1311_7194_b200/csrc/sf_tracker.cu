@@ -609,6 +609,8 @@ void sf_tracker::decode(const Fetch* f, int frame, int mode, uint64_t launches, 
     out->raycast.sample_steps = f->rs.sample_steps;
     out->raycast.hit_pixels = f->rs.hit_pixels;
     out->raycast.rays_with_bounds = f->rs.rays_with_bounds;
+    out->ray_dda_cells = f->rs.dda_cells;
+    out->ray_refine_samples = f->rs.refine_samples;
     out->blocks_processed = static_cast<uint64_t>(f->ctr.limit) + f->ctr.n_update;
     if (f->ctr.skip) out->blocks_processed = 0;
     out->voxels_visited = out->blocks_processed * m * m * m;
