@@ -495,12 +495,13 @@ def run_ours(args, world, rank, local):
     integ_bytes = [mm.blocks_processed * (m3 * 4 + 8) + px * 8 for mm in metrics_b]
     achieved = sum(integ_bytes) / (sum(integ_ms) * 1e-3) / 1e9
     peak, peak_kind = hbm_peak()
-    traffic = None  # DRAM bytes per launch of the roofline kernel from the committed ncu capture
-    tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_integrate_traffic.json")
+    # DRAM bytes per launch of the roofline kernel from the committed ncu capture
+    traffic = {"codes": None, "float2": None}
+    tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r2_integrate_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             t = json.load(f)
-        traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
+        traffic = {k: t[k]["dram_read_bytes"] + t[k]["dram_write_bytes"] for k in ("codes", "float2")}
 
     def integrate_only(layout):
         """Ground-truth poses (the integrate-only configuration of BASELINE configs[0], at C4):
@@ -525,11 +526,11 @@ def run_ours(args, world, rank, local):
             raise RuntimeError(f"integrate-only run failed: {[mm.status for mm in ms_]}")
         return g, ms_, kern_ms
 
-    def integrate_roofline(ms_, kern_ms, bytes_per_voxel, kernel):
+    def integrate_roofline(ms_, kern_ms, bytes_per_voxel, kernel, layout):
         b = [mm.blocks_processed * (m3 * bytes_per_voxel + 8) + px * 8 for mm in ms_]
         ach = sum(b) / (sum(kern_ms) * 1e-3) / 1e9
         return {"bound": "hbm", "kernel": kernel, "achieved": ach, "peak": peak, "peak_kind": peak_kind,
-                "unit": "GB/s", "frac": ach / peak, "bytes_per_launch_mean": sum(b) / steps,
+                "unit": "GB/s", "frac": ach / peak, "traffic": traffic[layout], "bytes_per_launch_mean": sum(b) / steps,
                 "ms_per_launch_mean": sum(kern_ms) / steps,
                 "kernel_span_ms_mean": sum(mm.integrate_ns for mm in ms_) / steps * 1e-6,
                 "blocks_processed_mean": sum(mm.blocks_processed for mm in ms_) / steps,
@@ -629,15 +630,15 @@ def run_ours(args, world, rank, local):
         "icp_device_ms_mean": sum(mm.icp_ns for mm in metrics) / steps * 1e-6,
         "tracking_error_last_frame": pose_err,
         "roofline": {"bound": "hbm", "kernel": "k_integrate_rows<Kalman>", "achieved": achieved, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic["codes"],
                      "bytes_per_launch_mean": sum(integ_bytes) / steps,
                      "ms_per_launch_mean": sum(integ_ms) / steps,
                      "kernel_span_ms_mean": sum(mm.integrate_ns for mm in metrics) / steps * 1e-6},
         "integrate_only": {
             "workload": "C4 frames fused at their ground-truth poses (integrate-only, BASELINE configs[0] style); "
                         "same frames, fresh volumes",
-            "float2_payload": integrate_roofline(ms_f2, kern_f2, 16, "k_integrate_rows<Kalman, M=8, float2>"),
-            "codes_payload": integrate_roofline(ms_p1, kern_p1, 4, "k_integrate_rows<Kalman, M=8, codes>"),
+            "float2_payload": integrate_roofline(ms_f2, kern_f2, 16, "k_integrate_rows<Kalman, M=8, float2>", "float2"),
+            "codes_payload": integrate_roofline(ms_p1, kern_p1, 4, "k_integrate_rows<Kalman, M=8, codes>", "codes"),
             "same_block_tables": same_blocks,
             "algorithmic_bytes": "per processed block M^3 x (read + write) of the payload (float2: 8 + 8 B, codes: "
                                  "2 + 2 B per voxel) + its 8 B work item; per launch the 8 B/pixel {depth, p_k} table",
