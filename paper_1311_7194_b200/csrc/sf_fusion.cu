@@ -768,6 +768,67 @@ struct RowShared {
     int axis, lstep;          // row axis (0 x, 1 y, 2 z: the block axis closest to the optical axis), its l stride
 };
 
+// Per-frame constants of the row kernels (one thread).
+template <int M>
+__device__ void row_kernel_init(const VolParams& P, const FrameConsts* __restrict__ fc, const FuseParams& fp,
+                                RowShared& sh, VolParams& sP, FuseParams& sFp, float* s_thr) {
+    s_thr[0] = -INFINITY;
+    s_thr[257] = s_thr[258] = s_thr[259] = INFINITY;
+    sP = P;
+    sFp = fp;
+    const Pose inv = fc->inv;
+    const Intr intr = fc->intr;
+    for (int i = 0; i < 9; ++i) sh.R[i] = inv.R.m[i];
+    sh.t[0] = inv.t.x;
+    sh.t[1] = inv.t.y;
+    sh.t[2] = inv.t.z;
+    sh.ox = P.ox;
+    sh.oy = P.oy;
+    sh.oz = P.oz;
+    sh.voxel = P.voxel;
+    // rows along the block axis with the largest camera-z component (x on ties)
+    int ax = 0;
+    if (fabs(inv.R.m[7]) > fabs(inv.R.m[6 + ax])) ax = 1;
+    if (fabs(inv.R.m[8]) > fabs(inv.R.m[6 + ax])) ax = 2;
+    sh.axis = ax;
+    sh.lstep = ax == 0 ? 1 : ax == 1 ? M : M * M;
+    sh.Dxf = static_cast<float>(P.voxel * inv.R.m[ax]);
+    sh.Dyf = static_cast<float>(P.voxel * inv.R.m[3 + ax]);
+    sh.Dzf = static_cast<float>(P.voxel * inv.R.m[6 + ax]);
+    sh.cx = intr.cx;
+    sh.cy = intr.cy;
+    sh.fxf = static_cast<float>(intr.fx);
+    sh.fyf = static_cast<float>(intr.fy);
+    sh.cxf = static_cast<float>(intr.cx);
+    sh.cyf = static_cast<float>(intr.cy);
+    sh.Fmax = static_cast<float>(dmax(intr.fx, intr.fy));
+    sh.Wpix = static_cast<float>(intr.w > intr.h ? intr.w : intr.h) + 2.0f;
+    sh.Mvox = static_cast<float>(M * P.voxel);
+    // T error bound (m) for rows with z < 16 m: double-float row origin, lx * dz, and the
+    // (Sterbenz-exact in the band) subtraction d - z_hi
+    const double delta = P.delta;
+    // |T_f32 - T_ref| <= 2^-24 ((M-1) voxel [Dzf] + (M-1) voxel [fma] + |d - Azh| + |T| [two
+    // subtractions] + (M-1) voxel) + 2^-40 [the reference's own FP64 x_c vs the row model],
+    // with |d - Azh|, |T| <= delta + (M-1) voxel inside the decision region; x 1.25 slack
+    const double eT = 1.25 * 0x1p-23 * (delta + 1.5 * (M - 1) * P.voxel) + 0x1p-40;
+    sh.thr_out = static_cast<float>((delta + eT) * 1.000001);
+    sh.thr_in = static_cast<float>((delta - eT) * 0.999999);
+    sh.k127 = static_cast<float>(kTsdfCodeRange / delta);
+    // code margin: the measurement's eT (gain <= 1) plus the FP32 filter's own error
+    // (<= 2.4e-4 code units: rounded inputs, rcp.approx, three roundings; x 1.5 slack)
+    sh.ecode = static_cast<float>(3.6e-4 + 1.5 * eT * (kTsdfCodeRange / delta));
+    sh.q = static_cast<float>(fp.q);
+    sh.w_max = static_cast<float>(P.aux_w_max);
+    sh.k255w = static_cast<float>(255.0 / P.aux_w_max);
+    sh.lg_pmin = static_cast<float>(P.aux_lg_pmin);
+    sh.lg_scale = static_cast<float>(P.aux_lg_scale);
+    sh.thr_lo = static_cast<float>(P.aux_p_min * 0.5);
+    sh.thr_hi = static_cast<float>(P.aux_p_max * 2.0);
+    // float payload chi cut: T' carries the measurement's eT (gain <= 1) and the FP32 filter
+    // error (a few ulp of delta); float(delta) itself is within 2^-24 delta
+    sh.delta_f = static_cast<float>(delta);
+    sh.echi = static_cast<float>(2.0 * eT + 4e-6 * delta);
+}
 // Phase-2 update of one in-band voxel in FP32; false when a decision is not certain.
 template <int MODE>
 __device__ __forceinline__ bool approx_update(uint32_t cell, float tk, float pf, const RowShared& rc,
@@ -923,6 +984,19 @@ constexpr int kRowThreads = 256;
 constexpr int kRowCtasPerSm = SF_ROW_CTAS;
 constexpr uint32_t kGrabUnits = 4;  // 32-row units a warp takes per atomic (before the tail)
 constexpr uint32_t kTailUnitsPerWarp = 8;  // single-unit grabs once this much work per warp remains
+#ifndef SF_STATIC_PCT
+#define SF_STATIC_PCT 0
+#endif
+constexpr uint32_t kStaticPct = SF_STATIC_PCT;
+#ifndef SF_SLAB  // M = 8: half-block slab kernel (k_integrate_slab) instead of k_integrate_rows
+#define SF_SLAB 1
+#endif
+#ifndef SF_DIAG_NODRAIN  // timing diagnostics only (wrong results): skip phase 2 / the ring
+#define SF_DIAG_NODRAIN 0
+#endif
+#ifndef SF_DIAG_NOENQ
+#define SF_DIAG_NOENQ 0
+#endif  // share of the row units dealt out statically
 
 template <int MS>
 struct RowVec;
@@ -988,64 +1062,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
         s_adec[i] = aux->aux_decode_f[i];
         s_thr[i + 1] = aux->aux_thresh_f[i];
     }
-    if (threadIdx.x == 0) {
-        s_thr[0] = -INFINITY;
-        s_thr[257] = s_thr[258] = s_thr[259] = INFINITY;
-        sP = P;
-        sFp = fp;
-        const Pose inv = fc->inv;
-        const Intr intr = fc->intr;
-        for (int i = 0; i < 9; ++i) sh.R[i] = inv.R.m[i];
-        sh.t[0] = inv.t.x;
-        sh.t[1] = inv.t.y;
-        sh.t[2] = inv.t.z;
-        sh.ox = P.ox;
-        sh.oy = P.oy;
-        sh.oz = P.oz;
-        sh.voxel = P.voxel;
-        // rows along the block axis with the largest camera-z component (x on ties)
-        int ax = 0;
-        if (fabs(inv.R.m[7]) > fabs(inv.R.m[6 + ax])) ax = 1;
-        if (fabs(inv.R.m[8]) > fabs(inv.R.m[6 + ax])) ax = 2;
-        sh.axis = ax;
-        sh.lstep = ax == 0 ? 1 : ax == 1 ? M : M * M;
-        sh.Dxf = static_cast<float>(P.voxel * inv.R.m[ax]);
-        sh.Dyf = static_cast<float>(P.voxel * inv.R.m[3 + ax]);
-        sh.Dzf = static_cast<float>(P.voxel * inv.R.m[6 + ax]);
-        sh.cx = intr.cx;
-        sh.cy = intr.cy;
-        sh.fxf = static_cast<float>(intr.fx);
-        sh.fyf = static_cast<float>(intr.fy);
-        sh.cxf = static_cast<float>(intr.cx);
-        sh.cyf = static_cast<float>(intr.cy);
-        sh.Fmax = static_cast<float>(dmax(intr.fx, intr.fy));
-        sh.Wpix = static_cast<float>(intr.w > intr.h ? intr.w : intr.h) + 2.0f;
-        sh.Mvox = static_cast<float>(M * P.voxel);
-        // T error bound (m) for rows with z < 16 m: double-float row origin, lx * dz, and the
-        // (Sterbenz-exact in the band) subtraction d - z_hi
-        const double delta = P.delta;
-        // |T_f32 - T_ref| <= 2^-24 ((M-1) voxel [Dzf] + (M-1) voxel [fma] + |d - Azh| + |T| [two
-        // subtractions] + (M-1) voxel) + 2^-40 [the reference's own FP64 x_c vs the row model],
-        // with |d - Azh|, |T| <= delta + (M-1) voxel inside the decision region; x 1.25 slack
-        const double eT = 1.25 * 0x1p-23 * (delta + 1.5 * (M - 1) * P.voxel) + 0x1p-40;
-        sh.thr_out = static_cast<float>((delta + eT) * 1.000001);
-        sh.thr_in = static_cast<float>((delta - eT) * 0.999999);
-        sh.k127 = static_cast<float>(kTsdfCodeRange / delta);
-        // code margin: the measurement's eT (gain <= 1) plus the FP32 filter's own error
-        // (<= 2.4e-4 code units: rounded inputs, rcp.approx, three roundings; x 1.5 slack)
-        sh.ecode = static_cast<float>(3.6e-4 + 1.5 * eT * (kTsdfCodeRange / delta));
-        sh.q = static_cast<float>(fp.q);
-        sh.w_max = static_cast<float>(P.aux_w_max);
-        sh.k255w = static_cast<float>(255.0 / P.aux_w_max);
-        sh.lg_pmin = static_cast<float>(P.aux_lg_pmin);
-        sh.lg_scale = static_cast<float>(P.aux_lg_scale);
-        sh.thr_lo = static_cast<float>(P.aux_p_min * 0.5);
-        sh.thr_hi = static_cast<float>(P.aux_p_max * 2.0);
-        // float payload chi cut: T' carries the measurement's eT (gain <= 1) and the FP32 filter
-        // error (a few ulp of delta); float(delta) itself is within 2^-24 delta
-        sh.delta_f = static_cast<float>(delta);
-        sh.echi = static_cast<float>(2.0 * eT + 4e-6 * delta);
-    }
+    if (threadIdx.x == 0) row_kernel_init<M>(P, fc, fp, sh, sP, sFp, s_thr);
     clear_keybits(ctr, uniq, keybits);
     __syncthreads();
     const uint32_t limit = ctr->limit, upd_base = ctr->upd_base;
@@ -1057,7 +1074,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
     uint32_t updated = 0, exact = 0;
     // Phase 2 on ring entries [head, head + n): lanes take one entry each.
     auto drain = [&](uint32_t n) {
-        if (lane < n) {
+        if (!SF_DIAG_NODRAIN && lane < n) {
             const uint4 e = ring[(head + lane) & (kRing - 1)];
             const uint32_t l = e.y & 0x1FF, cell = (e.y >> 9) & 0xFFFF;
             if constexpr (P2) {
@@ -1096,15 +1113,31 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
     // remains, single units for the tail (the last grabs decide when the kernel ends).
     const uint32_t n_units = static_cast<uint32_t>((n_rows + 31) / 32);
     const uint32_t tail_units = gridDim.x * (kRowThreads / 32) * kTailUnitsPerWarp;
-    uint32_t seen = 0;
+    // The first kStaticPct % of the units are dealt out statically (contiguous runs per warp,
+    // no atomics); the rest is grabbed dynamically.
+    const uint32_t n_warps = gridDim.x * (kRowThreads / 32);
+    const uint32_t gwarp = blockIdx.x * (kRowThreads / 32) + (threadIdx.x >> 5);
+    const uint32_t s_per_warp = static_cast<uint32_t>((static_cast<unsigned long long>(n_units) * kStaticPct) /
+                                                      (100ull * n_warps));
+    const uint32_t dyn_base = s_per_warp * n_warps;
+    uint32_t s_next = gwarp * s_per_warp;
+    const uint32_t s_end = s_next + s_per_warp;
+    uint32_t seen = dyn_base;
     for (;;) {
-        const uint32_t step = seen + tail_units < n_units ? kGrabUnits : 1u;
-        uint32_t grab = 0;
-        if (lane == 0) grab = atomicAdd(&ctr->row_chunks, step);
-        grab = __shfl_sync(0xffffffffu, grab, 0);
-        seen = grab + step;
-        if (grab >= n_units) break;
-        const uint32_t units = min(step, n_units - grab);
+        uint32_t grab, units;
+        if (s_next < s_end) {
+            grab = s_next;
+            units = min(kGrabUnits, s_end - s_next);
+            s_next += units;
+        } else {
+            const uint32_t step = seen + tail_units < n_units ? kGrabUnits : 1u;
+            uint32_t g = 0;
+            if (lane == 0) g = atomicAdd(&ctr->row_chunks, step);
+            grab = dyn_base + __shfl_sync(0xffffffffu, g, 0);
+            seen = grab + step;
+            if (grab >= n_units) break;
+            units = min(step, n_units - grab);
+        }
         const unsigned long long grab_row = (unsigned long long)grab * 32;
         for (uint32_t sub = 0; sub < units; ++sub) {
             // ---------------- phase 1: one row per lane ----------------
@@ -1270,7 +1303,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
                         ring[(tail + __popc(bal & lt_mask)) & (kRing - 1)] =
                             make_uint4(slot, meta, __float_as_uint(t), __float_as_uint(px.y));
                     }
-                    tail += __popc(bal);
+                    if (!SF_DIAG_NOENQ) tail += __popc(bal);
                     if (kRing < 32 * M + 31 && lx == M / 2 - 1) {  // half-row drain (small ring)
                         __syncwarp();
                         while (tail - head >= 32) drain(32);
@@ -1306,7 +1339,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
                         ring[(tail + __popc(bal & lt_mask)) & (kRing - 1)] =
                             make_uint4(slot, meta, __float_as_uint(t), __float_as_uint(px.y));
                     }
-                    tail += __popc(bal);
+                    if (!SF_DIAG_NOENQ) tail += __popc(bal);
                     if (kRing < 32 * M + 31 && lx == M / 2 - 1) {  // half-row drain (small ring)
                         __syncwarp();
                         while (tail - head >= 32) drain(32);
@@ -1321,6 +1354,365 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
         }
     }
     drain(tail - head);
+    for (int off = 16; off > 0; off >>= 1) {
+        updated += __shfl_down_sync(0xffffffffu, updated, off);
+        exact += __shfl_down_sync(0xffffffffu, exact, off);
+    }
+    if (lane == 0 && updated) atomicAdd(&ctr->voxels_updated, (unsigned long long)updated);
+    if (lane == 0 && exact) atomicAdd(&ctr->exact_voxels, (unsigned long long)exact);
+    if (lane == 0) atomicMax(&ctr->t_end, globaltimer_ns());
+}
+
+// ---------------------------------------------------------------------------------
+// Half-block slab integrate (M = 8): the roofline kernel.
+//
+// Same certified decisions and FP32 evaluation as k_integrate_rows; what
+// changes is the data movement. A warp's unit of work is 32 rows of one block = a half-block
+// slab of 256 voxels, which is 32 contiguous x-rows of the payload (16 B each for codes, 64 B
+// for float2). The slab is copied HBM -> shared memory with cp.async one unit ahead (work
+// items two units ahead), phase 1 classifies voxels from registers and queues in-band ones by
+// slab position, phase 2 updates them in shared memory (no global latency in the update), and
+// the slab goes back to HBM as coalesced 16-byte stores. Fresh blocks are filled with chi in
+// shared memory instead of being read.
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr int kSlabVox = 256;   // voxels per unit (32 rows of M = 8)
+constexpr int kSlabRing = 256;  // queued voxels per warp: one unit's worth, drained per unit
+template <bool P2>
+struct SlabSmem {
+    using Cell = typename std::conditional<P2, float2, uint16_t>::type;
+    static constexpr size_t kRingBytes = (kRowThreads / 32) * kSlabRing * sizeof(uint4);
+    static constexpr size_t kSlabBytes = (kRowThreads / 32) * 2 * kSlabVox * sizeof(Cell);
+    static constexpr size_t kBytes = kRingBytes + kSlabBytes;
+};
+
+// Offset (voxels, inside the block) of x-row q of unit half h: the slab is z in [4h, 4h + 4)
+// for rows along x or y, y in [4h, 4h + 4) for rows along z.
+__device__ __forceinline__ int slab_xrow(int axis, int h, int q) {
+    return axis == 2 ? 64 * (q >> 2) + 32 * h + 8 * (q & 3) : 256 * h + 8 * q;
+}
+
+template <int MODE, bool P2>
+__global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
+    k_integrate_slab(VolParams P, const FrameConsts* __restrict__ fc, FuseParams fp, const int2* __restrict__ work,
+                     FrameCounters* __restrict__ ctr, const AuxTables* __restrict__ aux,
+                     const float2* __restrict__ pix_f, const double* __restrict__ pix_dm,
+                     const double* __restrict__ pix_var, const double* __restrict__ pix_w,
+                     uint16_t* __restrict__ payload, float2* __restrict__ fpay, const uint32_t* __restrict__ uniq,
+                     uint32_t* __restrict__ keybits) {
+    pdl_wait();
+    constexpr int M = 8, MS = 3, M3 = 512;
+    using Cell = typename SlabSmem<P2>::Cell;
+    __shared__ float s_tdec[256], s_adec[256], s_thr[260];  // s_thr[k + 1] = thresh[k]; +-inf sentinels
+    extern __shared__ uint4 s_dyn[];  // rings (uint4 {pos | exact << 31, T, p, 0}), then the slabs
+    __shared__ RowShared sh;
+    __shared__ VolParams sP;
+    __shared__ FuseParams sFp;
+    if (ctr->skip) return;
+    if (threadIdx.x == 0) atomicMin(&ctr->t_begin, globaltimer_ns());
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        s_tdec[i] = aux->tsdf_decode_f[i];
+        s_adec[i] = aux->aux_decode_f[i];
+        s_thr[i + 1] = aux->aux_thresh_f[i];
+    }
+    if (threadIdx.x == 0) row_kernel_init<M>(P, fc, fp, sh, sP, sFp, s_thr);
+    clear_keybits(ctr, uniq, keybits);
+    __syncthreads();
+    const uint32_t limit = ctr->limit, upd_base = ctr->upd_base;
+    const uint32_t n_units = (limit + ctr->n_update) * 2u;
+    const int w = fc->intr.w, h = fc->intr.h, N = P.N;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint4* ring = s_dyn + warp * kSlabRing;
+    Cell* slabs = reinterpret_cast<Cell*>(reinterpret_cast<char*>(s_dyn) + SlabSmem<P2>::kRingBytes) +
+                  warp * 2 * kSlabVox;
+    const int axis = sh.axis;
+    // slab position of this lane's row: voxel l at pos0 + l * pstride (x-row q holds 8 voxels)
+    const int pstride = axis == 0 ? 1 : axis == 1 ? 8 : 32;
+    const int pos0 = axis == 0 ? 8 * lane : axis == 1 ? 64 * (lane >> 3) + (lane & 7) : 8 * (lane >> 3) + (lane & 7);
+    uint32_t updated = 0, exact = 0;
+
+    // ---- unit supply: a static share per warp, then guided dynamic grabs ----
+    const uint32_t n_warps = gridDim.x * (kRowThreads / 32);
+    const uint32_t gwarp = blockIdx.x * (kRowThreads / 32) + warp;
+    const uint32_t s_per_warp =
+        static_cast<uint32_t>((static_cast<unsigned long long>(n_units) * kStaticPct) / (100ull * n_warps));
+    const uint32_t dyn_base = s_per_warp * n_warps;
+    const uint32_t tail_units = n_warps * kTailUnitsPerWarp;
+    uint32_t s_next = gwarp * s_per_warp;
+    const uint32_t s_end = s_next + s_per_warp;
+    uint32_t d_lo = 0, d_hi = 0, seen = dyn_base;
+    bool done = false;
+    auto take = [&]() -> uint32_t {
+        if (s_next < s_end) return s_next++;
+        if (d_lo < d_hi) return d_lo++;
+        if (done) return n_units;
+        const uint32_t step = seen + tail_units < n_units ? kGrabUnits : 1u;
+        uint32_t g = 0;
+        if (lane == 0) g = atomicAdd(&ctr->row_chunks, step);
+        g = dyn_base + __shfl_sync(0xffffffffu, g, 0);
+        seen = g + step;
+        if (g >= n_units) {
+            done = true;
+            return n_units;
+        }
+        d_lo = g + 1;
+        d_hi = min(g + step, n_units);
+        return g;
+    };
+    auto load_item = [&](uint32_t u) -> int2 {
+        return u < n_units ? work_at(work, limit, upd_base, u >> 1) : make_int2(0, 0);
+    };
+    // Slab of unit u into buffer b: cp.async of this lane's x-row, or chi for a fresh block.
+    auto issue_slab = [&](uint32_t u, int2 wk, int b) {
+        if (u >= n_units) return;
+        Cell* dst = slabs + b * kSlabVox + 8 * lane;
+        const uint32_t slot = static_cast<uint32_t>(wk.x) & 0x7fffffffu;
+        if (static_cast<uint32_t>(wk.x) >> 31) {  // newly allocated block: chi (grid.cpp:87-100, grid.hpp:77-88)
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+            if constexpr (P2) {
+                const uint4 c = make_uint4(__float_as_uint(INFINITY), 0u, __float_as_uint(INFINITY), 0u);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) d4[j] = c;
+            } else {
+                d4[0] = make_uint4(0x00800080u, 0x00800080u, 0x00800080u, 0x00800080u);
+            }
+            return;
+        }
+        const size_t src = (size_t)slot * M3 + slab_xrow(axis, static_cast<int>(u & 1), lane);
+        if constexpr (P2) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) cp_async16(dst + 2 * j, fpay + src + 2 * j);
+        } else {
+            cp_async16(dst, payload + src);
+        }
+    };
+
+    uint32_t u0 = take();
+    int2 wk0 = load_item(u0);
+    uint32_t u1 = take();
+    int2 wk1 = load_item(u1);
+    issue_slab(u0, wk0, 0);
+    cp_async_commit();
+    for (int it = 0; u0 < n_units; ++it) {
+        const uint32_t u2 = take();
+        const int2 wk2 = load_item(u2);  // consumed by the next iteration's issue
+        issue_slab(u1, wk1, (it + 1) & 1);
+        cp_async_commit();
+        cp_async_wait<1>();  // this unit's slab has landed (the next one may still be in flight)
+        __syncwarp();
+        Cell* slab = slabs + (it & 1) * kSlabVox;
+        const uint32_t slot = static_cast<uint32_t>(wk0.x) & 0x7fffffffu;
+        const bool fresh = (static_cast<uint32_t>(wk0.x) >> 31) != 0;
+        const int key = wk0.y;
+        const int hh = static_cast<int>(u0 & 1);
+        // ---------------- phase 1: one row per lane (as k_integrate_rows) ----------------
+        uint32_t tail = 0;
+        {
+            bool fast = false, exact_row = false, small = false;
+            float Axf = 0.f, Ayf = 0.f, Azh = 1.f, Azl = 0.f, half = -1.f;
+            float su0 = -1e30f, dsu = 0.f, mu = 0.f, sv0 = -1e30f, dsv = 0.f, mv = 0.f;
+            float2 c00 = make_float2(0.f, 0.f), c10 = c00, c01 = c00, c11 = c00;
+            int bx, by, bz;
+            if (P.nshift >= 0) {
+                bx = key & (N - 1);
+                by = (key >> P.nshift) & (N - 1);
+                bz = key >> (2 * P.nshift);
+            } else {
+                bx = key % N;
+                by = (key / N) % N;
+                bz = key / (N * N);
+            }
+            const int r = 32 * hh + lane;
+            const int ri = r & (M - 1), rj = r >> MS;
+            int l0x, l0y, l0z;
+            if (axis == 0) {
+                l0x = 0, l0y = ri, l0z = rj;
+            } else if (axis == 1) {
+                l0x = ri, l0y = 0, l0z = rj;
+            } else {
+                l0x = ri, l0y = rj, l0z = 0;
+            }
+            // row origin x_c = R (voxel_center) + t in FP64 (voxel_center, grid.cpp:271-273)
+            const double vx = sh.ox + (i2d_exact((bx << MS) + l0x) + 0.5) * sh.voxel;
+            const double vy = sh.oy + (i2d_exact((by << MS) + l0y) + 0.5) * sh.voxel;
+            const double vz = sh.oz + (i2d_exact((bz << MS) + l0z) + 0.5) * sh.voxel;
+            const double Ax = ((sh.R[0] * vx + sh.R[1] * vy) + sh.R[2] * vz) + sh.t[0];
+            const double Ay = ((sh.R[3] * vx + sh.R[4] * vy) + sh.R[5] * vz) + sh.t[1];
+            const double Az = ((sh.R[6] * vx + sh.R[7] * vy) + sh.R[8] * vz) + sh.t[2];
+            Axf = static_cast<float>(Ax);
+            Ayf = static_cast<float>(Ay);
+            Azh = static_cast<float>(Az);
+            Azl = static_cast<float>(Az - static_cast<double>(Azh));
+            const float zend = fmaf(static_cast<float>(M - 1), sh.Dzf, Azh);
+            const float zlo = fminf(Azh, zend) - 1e-6f, zhi = fmaxf(Azh, zend) + 1e-6f;
+            const float rzlo = rcp_approx_f(zlo);
+            const float X = fmaxf(fabsf(Axf), fabsf(Ayf)) + sh.Mvox, Z = fabsf(Azh) + sh.Mvox;
+            const float Xq = sh.Fmax * X * rzlo;  // >= |u - cx|, |v - cy| over the row
+            fast = zlo > 1e-3f && zhi < 16.0f && Xq < 2097152.0f;
+            if (fast) {
+                // pixel-rounding margin of the row and its pixel footprint
+                const float eu = 1.6f * (0x1p-23f * Xq * (2.5f + Z * rzlo) + 0x1p-24f * sh.Wpix);
+                half = 0.5f - eu;
+                const float r0 = rcp_approx_f(Azh), r1 = rcp_approx_f(zend);
+                const float xe = fmaf(static_cast<float>(M - 1), sh.Dxf, Axf);
+                const float ye = fmaf(static_cast<float>(M - 1), sh.Dyf, Ayf);
+                const float u0f = fmaf(sh.fxf, Axf * r0, sh.cxf), u1f = fmaf(sh.fxf, xe * r1, sh.cxf);
+                const float v0f = fmaf(sh.fyf, Ayf * r0, sh.cyf), v1f = fmaf(sh.fyf, ye * r1, sh.cyf);
+                const float slack = eu + 1e-3f;
+                const int cu0 = static_cast<int>(floorf(fminf(u0f, u1f) - slack + 0.5f));
+                const int cu1 = static_cast<int>(floorf(fmaxf(u0f, u1f) + slack + 0.5f));
+                const int cv0 = static_cast<int>(floorf(fminf(v0f, v1f) - slack + 0.5f));
+                const int cv1 = static_cast<int>(floorf(fmaxf(v0f, v1f) + slack + 0.5f));
+                small = cu1 - cu0 <= 1 && cv1 - cv0 <= 1;
+                if (small) {
+                    // pixel-boundary planes (see k_integrate_rows)
+                    if (cu1 > cu0) {
+                        const float b = static_cast<float>((static_cast<double>(cu0) + 0.5) - sh.cx);
+                        su0 = fmaf(sh.fxf, Axf, -(b * Azh));
+                        dsu = fmaf(sh.fxf, sh.Dxf, -(b * sh.Dzf));
+                        mu = 0x1p-24f * 6.0f * (sh.fxf * X + fabsf(b) * Z + sh.Mvox * (sh.fxf + fabsf(b))) + 1e-9f;
+                    }
+                    if (cv1 > cv0) {
+                        const float b = static_cast<float>((static_cast<double>(cv0) + 0.5) - sh.cy);
+                        sv0 = fmaf(sh.fyf, Ayf, -(b * Azh));
+                        dsv = fmaf(sh.fyf, sh.Dyf, -(b * sh.Dzf));
+                        mv = 0x1p-24f * 6.0f * (sh.fyf * X + fabsf(b) * Z + sh.Mvox * (sh.fyf + fabsf(b))) + 1e-9f;
+                    }
+                    const bool u0in = cu0 >= 0 && cu0 < w, u1in = cu1 > cu0 && cu1 >= 0 && cu1 < w;
+                    const bool v0in = cv0 >= 0 && cv0 < h, v1in = cv1 > cv0 && cv1 >= 0 && cv1 < h;
+                    if (u0in && v0in) c00 = pix_f[cv0 * w + cu0];
+                    if (u1in && v0in) c10 = pix_f[cv0 * w + cu1];
+                    if (u0in && v1in) c01 = pix_f[cv1 * w + cu0];
+                    if (u1in && v1in) c11 = pix_f[cv1 * w + cu1];
+                }
+            } else {
+                exact_row = !(zhi < -1e-3f);
+            }
+            const float Dxf = sh.Dxf, Dyf = sh.Dyf, Dzf = sh.Dzf;
+            const float fxf = sh.fxf, fyf = sh.fyf, cxf = sh.cxf, cyf = sh.cyf;
+            const float thr_in = sh.thr_in, thr_out = sh.thr_out;
+            const unsigned lt_mask = (1u << lane) - 1u;
+            const bool warp_small = __all_sync(0xffffffffu, small || (!fast && !exact_row));
+            if (warp_small) {
+#pragma unroll
+                for (int lx = 0; lx < M; ++lx) {
+                    const float fl = static_cast<float>(lx);
+                    const float su = fmaf(fl, dsu, su0), sv = fmaf(fl, dsv, sv0);
+                    const bool iu = su > 0.0f, iv = sv > 0.0f;
+                    const bool cert = fabsf(su) > mu && fabsf(sv) > mv;
+                    const float2 px = iv ? (iu ? c11 : c01) : (iu ? c10 : c00);
+                    const float t = (px.x - Azh) - (lx == 0 ? Azl : fmaf(fl, Dzf, Azl));
+                    const float at = fabsf(t);
+                    const bool meas = small && px.x > 0.0f;
+                    const bool in = meas && cert && at < thr_in;
+                    const bool unc = small && (!cert || (meas && !(at < thr_in) && !(at > thr_out)));
+                    const bool q = in || unc;
+                    const unsigned bal = __ballot_sync(0xffffffffu, q);
+                    if (q)
+                        ring[tail + __popc(bal & lt_mask)] =
+                            make_uint4(static_cast<uint32_t>(pos0 + lx * pstride) | (unc ? 0x80000000u : 0u),
+                                       __float_as_uint(t), __float_as_uint(px.y), 0u);
+                    tail += __popc(bal);
+                }
+            } else {
+#pragma unroll
+                for (int lx = 0; lx < M; ++lx) {
+                    const float xf = lx == 0 ? Axf : fmaf(static_cast<float>(lx), Dxf, Axf);
+                    const float yf = lx == 0 ? Ayf : fmaf(static_cast<float>(lx), Dyf, Ayf);
+                    const float zf = lx == 0 ? Azh : fmaf(static_cast<float>(lx), Dzf, Azh);
+                    const float rz = rcp_approx_f(zf);
+                    const float uf = fmaf(fxf, xf * rz, cxf), vf = fmaf(fyf, yf * rz, cyf);
+                    const float tu = __fadd_rn(uf, kMagic23), tv = __fadd_rn(vf, kMagic23);
+                    const bool cert = fabsf(__fsub_rn(uf, __fsub_rn(tu, kMagic23))) < half &&
+                                      fabsf(__fsub_rn(vf, __fsub_rn(tv, kMagic23))) < half;
+                    const uint32_t u = static_cast<uint32_t>(__float_as_int(tu) - __float_as_int(kMagic23));
+                    const uint32_t v = static_cast<uint32_t>(__float_as_int(tv) - __float_as_int(kMagic23));
+                    const bool inimg = fast && cert && u < (uint32_t)w && v < (uint32_t)h;
+                    const float2 px = pix_f[inimg ? v * (uint32_t)w + u : 0u];
+                    const float t = (px.x - Azh) - (lx == 0 ? Azl : fmaf(static_cast<float>(lx), Dzf, Azl));
+                    const float at = fabsf(t);
+                    const bool meas = inimg && px.x > 0.0f;
+                    const bool in = meas && at < thr_in;
+                    const bool unc = exact_row || (fast && (!cert || (meas && !(at < thr_in) && !(at > thr_out))));
+                    const bool q = in || unc;
+                    const unsigned bal = __ballot_sync(0xffffffffu, q);
+                    if (q)
+                        ring[tail + __popc(bal & lt_mask)] =
+                            make_uint4(static_cast<uint32_t>(pos0 + lx * pstride) | (unc ? 0x80000000u : 0u),
+                                       __float_as_uint(t), __float_as_uint(px.y), 0u);
+                    tail += __popc(bal);
+                }
+            }
+        }
+        __syncwarp();  // ring entries before the drain
+        // ---------------- phase 2: update the queued voxels in shared memory ----------------
+        bool wrote = false;
+        for (uint32_t head = 0; head < tail; head += 32) {
+            if (head + lane < tail) {
+                const uint4 e = ring[head + lane];
+                const int pos = static_cast<int>(e.x & 0xFFu);
+                Cell* cellp = slab + pos;
+                const bool unc = (e.x >> 31) != 0;
+                if constexpr (P2) {
+                    const float2 prior = *cellp;
+                    float2 out;
+                    bool have = true;
+                    if (unc || !approx_update_f2<MODE>(prior, __uint_as_float(e.y), __uint_as_float(e.z), sh, out)) {
+                        ++exact;
+                        const int l = slab_xrow(axis, hh, pos >> 3) + (pos & 7);
+                        have = exact_voxel_f2<MODE>(sP, fc, sFp, key, l, prior, pix_dm, pix_var, pix_w, out);
+                    }
+                    if (have) {
+                        *cellp = out;
+                        ++updated;
+                        wrote = true;
+                    }
+                } else {
+                    const uint32_t cell = *cellp;
+                    uint32_t out;
+                    int code = 0;
+                    if (unc || !approx_update<MODE>(cell, __uint_as_float(e.y), __uint_as_float(e.z), sh, s_tdec,
+                                                    s_adec, s_thr, out)) {
+                        ++exact;
+                        const int l = slab_xrow(axis, hh, pos >> 3) + (pos & 7);
+                        code = exact_voxel<MODE>(sP, fc, sFp, aux, key, l, cell, pix_dm, pix_var, pix_w);
+                        out = static_cast<uint32_t>(code);
+                    }
+                    if (code >= 0) {
+                        *cellp = static_cast<uint16_t>(out);
+                        ++updated;
+                        wrote = true;
+                    }
+                }
+            }
+        }
+        // ---------------- write-back: 32 x-rows, coalesced 16-byte stores ----------------
+        if (__any_sync(0xffffffffu, wrote) || fresh) {
+            __syncwarp();
+            const size_t dst = (size_t)slot * M3 + slab_xrow(axis, hh, lane);
+            const uint4* s4 = reinterpret_cast<const uint4*>(slab + 8 * lane);
+            if constexpr (P2) {
+                uint4* g4 = reinterpret_cast<uint4*>(fpay + dst);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) g4[j] = s4[j];
+            } else {
+                *reinterpret_cast<uint4*>(payload + dst) = s4[0];
+            }
+        }
+        __syncwarp();  // ring and slab reuse
+        u0 = u1;
+        wk0 = wk1;
+        u1 = u2;
+        wk1 = wk2;
+    }
+    cp_async_wait<0>();
     for (int off = 16; off > 0; off >>= 1) {
         updated += __shfl_down_sync(0xffffffffu, updated, off);
         exact += __shfl_down_sync(0xffffffffu, exact, off);
@@ -1643,6 +2035,19 @@ static void launch_integrate_rows(Volume& v, FrameBuffers& fb, const FuseParams&
                v.d_payload, v.d_fpayload, fb.keys_unique, v.d_keybits);
 }
 
+template <int MODE, bool P2>
+static void launch_integrate_slab(Volume& v, FrameBuffers& fb, const FuseParams& fp, cudaStream_t s) {
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+        SF_CUDA(cudaFuncSetAttribute(k_integrate_slab<MODE, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)SlabSmem<P2>::kBytes));
+        configured = true;
+    }
+    launch_pdl(k_integrate_slab<MODE, P2>, dim3(148 * kRowCtasPerSm), dim3(kRowThreads), SlabSmem<P2>::kBytes, s,
+               v.P, fb.fc, fp, fb.work, fb.ctr, v.d_aux, fb.pix_f, fb.pix_dm, fb.pix_var, fb.pix_w, v.d_payload,
+               v.d_fpayload, fb.keys_unique, v.d_keybits);
+}
+
 // Frame prep of fuse_frame (depends only on the frame): normals with the fusion options
 // (sigma0, spatial_scale = 0.25 * delta; fusion.cpp:33-36), edge mask, per-pixel measurement
 // factors (fusion.cpp:40-72, 148-171).
@@ -1723,8 +2128,15 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
         const bool rows_ok = (P.mshift == 3 || P.mshift == 2) && v.h_aux.fp32_ok && fp.refine == 0;
         const bool fast = v.layout == SF_PAYLOAD_CODES && rows_ok;
         const bool fast_f2 = v.layout == SF_PAYLOAD_FLOAT2 && rows_ok;
+#if SF_SLAB
+#define SF_INTEGRATE_ROWS(MODE, MS) \
+    (MS == 3 ? launch_integrate_slab<MODE, false>(v, fb, fp, s) : launch_integrate_rows<MODE, MS, false>(v, fb, fp, s))
+#define SF_INTEGRATE_ROWS_F2(MODE, MS) \
+    (MS == 3 ? launch_integrate_slab<MODE, true>(v, fb, fp, s) : launch_integrate_rows<MODE, MS, true>(v, fb, fp, s))
+#else
 #define SF_INTEGRATE_ROWS(MODE, MS) launch_integrate_rows<MODE, MS, false>(v, fb, fp, s)
 #define SF_INTEGRATE_ROWS_F2(MODE, MS) launch_integrate_rows<MODE, MS, true>(v, fb, fp, s)
+#endif
         if (fast_f2) {
             if (P.mshift == 3) {
                 if (fp.mode == 0) SF_INTEGRATE_ROWS_F2(0, 3);

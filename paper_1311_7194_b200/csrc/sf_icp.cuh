@@ -106,6 +106,7 @@ struct IcpWork {
         SF_CUDA(cudaMalloc(&part_count, kIcpCtas * sizeof(unsigned long long)));
         SF_CUDA(cudaMalloc(&part, kIcpCtas * kSums * sizeof(DD)));
         SF_CUDA(cudaMalloc(&st, sizeof(IcpState)));
+        SF_CUDA(cudaMemset(st, 0, sizeof(IcpState)));  // fields a path never writes are snapshotted whole
         SF_CUDA(cudaMalloc(&src_normals, 3 * n * sizeof(float)));
         SF_CUDA(cudaMalloc(&src, n * sizeof(float)));
         SF_CUDA(cudaMalloc(&tgt, n * sizeof(float)));

@@ -441,6 +441,7 @@ int sf_tracker_create(sf_volume_t vol, const sf_tracker_config* config, const do
         const TrackerDev td0{0, 0, 0, 0, -1, 0};
         SF_CUDA(cudaMemcpy(t->d_td, &td0, sizeof(TrackerDev), cudaMemcpyHostToDevice));
         SF_CUDA(cudaMemset(t->d_rstats, 0, sizeof(RayCounters)));
+        SF_CUDA(cudaMemset(t->d_init_delta, 0, 12 * sizeof(double)));
         SF_CUDA(cudaMemcpy(t->d_cur, initial_pose, 12 * sizeof(double), cudaMemcpyHostToDevice));
         SF_CUDA(cudaMallocHost(&t->h, sizeof(sf_tracker::Fetch)));
         for (auto& e : t->ev) SF_CUDA(cudaEventCreate(&e));
