@@ -765,9 +765,17 @@ struct RowShared {
     float thr_lo, thr_hi;     // clamp range of the variance code guess
     float delta_f, echi;      // float payload: chi cut |T'| > delta certain outside delta +- echi
     double cx, cy;            // principal point (pixel-boundary planes of small-footprint rows)
+    double eT;                // |T_f32 - T_ref| bound (m) of the phase-1 measurement
     int axis, lstep;          // row axis (0 x, 1 y, 2 z: the block axis closest to the optical axis), its l stride
 };
 
+// Row axis of a frame: the block axis with the largest camera-z component (x on ties).
+__device__ __forceinline__ int row_axis(const Pose& inv) {
+    int ax = 0;
+    if (fabs(inv.R.m[7]) > fabs(inv.R.m[6 + ax])) ax = 1;
+    if (fabs(inv.R.m[8]) > fabs(inv.R.m[6 + ax])) ax = 2;
+    return ax;
+}
 // Per-frame constants of the row kernels (one thread).
 template <int M>
 __device__ void row_kernel_init(const VolParams& P, const FrameConsts* __restrict__ fc, const FuseParams& fp,
@@ -787,9 +795,7 @@ __device__ void row_kernel_init(const VolParams& P, const FrameConsts* __restric
     sh.oz = P.oz;
     sh.voxel = P.voxel;
     // rows along the block axis with the largest camera-z component (x on ties)
-    int ax = 0;
-    if (fabs(inv.R.m[7]) > fabs(inv.R.m[6 + ax])) ax = 1;
-    if (fabs(inv.R.m[8]) > fabs(inv.R.m[6 + ax])) ax = 2;
+    const int ax = row_axis(inv);
     sh.axis = ax;
     sh.lstep = ax == 0 ? 1 : ax == 1 ? M : M * M;
     sh.Dxf = static_cast<float>(P.voxel * inv.R.m[ax]);
@@ -811,6 +817,7 @@ __device__ void row_kernel_init(const VolParams& P, const FrameConsts* __restric
     // subtractions] + (M-1) voxel) + 2^-40 [the reference's own FP64 x_c vs the row model],
     // with |d - Azh|, |T| <= delta + (M-1) voxel inside the decision region; x 1.25 slack
     const double eT = 1.25 * 0x1p-23 * (delta + 1.5 * (M - 1) * P.voxel) + 0x1p-40;
+    sh.eT = eT;
     sh.thr_out = static_cast<float>((delta + eT) * 1.000001);
     sh.thr_in = static_cast<float>((delta - eT) * 0.999999);
     sh.k127 = static_cast<float>(kTsdfCodeRange / delta);
@@ -887,6 +894,47 @@ __device__ __forceinline__ bool approx_update(uint32_t cell, float tk, float pf,
         if (!certain_lround_f(fminf(fmaxf(na, 0.0f), rc.w_max) * rc.k255w, 1e-3f, ac)) return false;
     }
     out = static_cast<uint32_t>(static_cast<uint8_t>(tc)) | (static_cast<uint32_t>(ac) << 8);
+    return true;
+}
+
+// Second chance for a voxel whose FP32 update was not certain (codes): the filter rule in FP64
+// on the same phase-1 inputs (T with its bound eT, p_k / w_k rounded to float), the decisions
+// certified against that input error only (no FP32 filter error): ~4x fewer voxels reach the
+// full FP64 path (exact_voxel), which re-derives the measurement from the projection.
+// Errors of the FP64 results vs the reference's: new_t <= eT (gain <= 1) + 2 delta 2^-25 (p_k
+// rounding through the gain, |T - prior| <= 2 delta) + FP64 rounding; new_a relative <= 2^-24
+// (d ln new_a / d ln p_k <= 1) + the reference's own cancellation a_err (filter_rule).
+template <int MODE>
+__device__ __noinline__ bool refine_update(const VolParams& P, const FuseParams& fp, const AuxTables* __restrict__ aux,
+                                           uint32_t cell, float tk, float pf, double eT, uint32_t& out) {
+    const int code = static_cast<int>(static_cast<int8_t>(cell & 0xFF));
+    const bool has_prior = code != kChiCode;
+    const double pt = has_prior ? aux->tsdf_decode[code + 128] : 0.0;
+    const double pa = has_prior ? aux->aux_decode[cell >> 8] : 0.0;
+    double nt, na, a_err;
+    if (!filter_rule<MODE>(has_prior, pt, pa, static_cast<double>(tk), MODE == 2 ? static_cast<double>(pf) : 0.0,
+                           MODE == 2 ? 0.0 : static_cast<double>(pf), fp, true, nt, na, a_err))
+        return false;
+    const double delta = P.delta;
+    const double et = 1.5 * (eT + 0x1p-24 * delta) + 1e-15 * delta;
+    const double at = fabs(nt);
+    if (!(fabs(at - delta) > et)) return false;
+    if (at > delta) {
+        out = kChiPayload;
+        return true;
+    }
+    int tc, ac;
+    if (!certain_lround_fast(nt * (kTsdfCodeRange / delta), et * (kTsdfCodeRange / delta) + 1e-9, tc)) return false;
+    const double ea = 1.5 * (0x1p-23 * fabs(na) + a_err) + 1e-300;
+    if (P.aux_mode == 0) {
+        const double k = 255.0 / P.aux_w_max;
+        if (!certain_lround_fast(dclamp(na, 0.0, P.aux_w_max) * k, ea * k + 1e-9, ac)) return false;
+    } else {
+        ac = aux_var_code(P, aux->aux_thresh, na);
+        if (ac > 0 && !(na - ea >= aux->aux_thresh[ac])) return false;
+        if (ac < 255 && !(na + ea < aux->aux_thresh[ac + 1])) return false;
+    }
+    out = static_cast<uint32_t>(static_cast<uint8_t>(static_cast<int8_t>(tc))) | (static_cast<uint32_t>(ac) << 8);
     return true;
 }
 
@@ -985,11 +1033,20 @@ constexpr int kRowCtasPerSm = SF_ROW_CTAS;
 constexpr uint32_t kGrabUnits = 4;  // 32-row units a warp takes per atomic (before the tail)
 constexpr uint32_t kTailUnitsPerWarp = 8;  // single-unit grabs once this much work per warp remains
 #ifndef SF_STATIC_PCT
-#define SF_STATIC_PCT 0
+#define SF_STATIC_PCT 50
 #endif
 constexpr uint32_t kStaticPct = SF_STATIC_PCT;
 #ifndef SF_SLAB  // M = 8: half-block slab kernel (k_integrate_slab) instead of k_integrate_rows
 #define SF_SLAB 1
+#endif
+#ifndef SF_DIAG_TIMES
+#define SF_DIAG_TIMES 0
+#endif
+#ifndef SF_DIAG_UNCONLY  // diagnostics: count only the phase-1 uncertain voxels as exact
+#define SF_DIAG_UNCONLY 0
+#endif
+#ifndef SF_DIAG_NOEXACT  // timing diagnostics only (wrong results): no FP64 fallback
+#define SF_DIAG_NOEXACT 0
 #endif
 #ifndef SF_DIAG_NODRAIN  // timing diagnostics only (wrong results): skip phase 2 / the ring
 #define SF_DIAG_NODRAIN 0
@@ -1383,6 +1440,17 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+#if SF_DIAG_TIMES  // timing diagnostics: per warp {kernel entry, first unit, last unit end, units}
+__device__ unsigned long long g_slab_dbg[148 * 4 * 8 * 4];
+#endif
+#ifndef SF_SLAB_PF
+#define SF_SLAB_PF 1
+#endif
+constexpr bool kSlabPrefetch = SF_SLAB_PF;
+#ifndef SF_REFINE
+#define SF_REFINE 1
+#endif
+constexpr bool kRefine = SF_REFINE;  // FP64 filter on the phase-1 inputs before the full FP64 path  // work items two units ahead (else one)
 constexpr int kSlabVox = 256;   // voxels per unit (32 rows of M = 8)
 constexpr int kSlabRing = 256;  // queued voxels per warp: one unit's worth, drained per unit
 template <bool P2>
@@ -1416,15 +1484,13 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
     __shared__ VolParams sP;
     __shared__ FuseParams sFp;
     if (ctr->skip) return;
+#if SF_DIAG_TIMES
+    const unsigned long long t_entry = globaltimer_ns();
+    unsigned long long t_first = 0, n_done = 0;
+#endif
     if (threadIdx.x == 0) atomicMin(&ctr->t_begin, globaltimer_ns());
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-        s_tdec[i] = aux->tsdf_decode_f[i];
-        s_adec[i] = aux->aux_decode_f[i];
-        s_thr[i + 1] = aux->aux_thresh_f[i];
-    }
-    if (threadIdx.x == 0) row_kernel_init<M>(P, fc, fp, sh, sP, sFp, s_thr);
-    clear_keybits(ctr, uniq, keybits);
-    __syncthreads();
+    // The first units' work items and slab copies are issued before the per-frame constants are
+    // set up (they need only the row axis), so their latency overlaps the prologue.
     const uint32_t limit = ctr->limit, upd_base = ctr->upd_base;
     const uint32_t n_units = (limit + ctr->n_update) * 2u;
     const int w = fc->intr.w, h = fc->intr.h, N = P.N;
@@ -1432,7 +1498,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
     uint4* ring = s_dyn + warp * kSlabRing;
     Cell* slabs = reinterpret_cast<Cell*>(reinterpret_cast<char*>(s_dyn) + SlabSmem<P2>::kRingBytes) +
                   warp * 2 * kSlabVox;
-    const int axis = sh.axis;
+    const int axis = row_axis(fc->inv);
     // slab position of this lane's row: voxel l at pos0 + l * pstride (x-row q holds 8 voxels)
     const int pstride = axis == 0 ? 1 : axis == 1 ? 8 : 32;
     const int pos0 = axis == 0 ? 8 * lane : axis == 1 ? 64 * (lane >> 3) + (lane & 7) : 8 * (lane >> 3) + (lane & 7);
@@ -1500,14 +1566,29 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
     int2 wk1 = load_item(u1);
     issue_slab(u0, wk0, 0);
     cp_async_commit();
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        s_tdec[i] = aux->tsdf_decode_f[i];
+        s_adec[i] = aux->aux_decode_f[i];
+        s_thr[i + 1] = aux->aux_thresh_f[i];
+    }
+    if (threadIdx.x == 0) row_kernel_init<M>(P, fc, fp, sh, sP, sFp, s_thr);
+    __syncthreads();
     for (int it = 0; u0 < n_units; ++it) {
-        const uint32_t u2 = take();
-        const int2 wk2 = load_item(u2);  // consumed by the next iteration's issue
+        uint32_t u2 = n_units;
+        int2 wk2 = make_int2(0, 0);
+        if (kSlabPrefetch) {
+            u2 = take();
+            wk2 = load_item(u2);  // consumed by the next iteration's issue
+        }
         issue_slab(u1, wk1, (it + 1) & 1);
         cp_async_commit();
         cp_async_wait<1>();  // this unit's slab has landed (the next one may still be in flight)
         __syncwarp();
         Cell* slab = slabs + (it & 1) * kSlabVox;
+#if SF_DIAG_TIMES
+        if (it == 0) t_first = globaltimer_ns();
+        ++n_done;
+#endif
         const uint32_t slot = static_cast<uint32_t>(wk0.x) & 0x7fffffffu;
         const bool fresh = (static_cast<uint32_t>(wk0.x) >> 31) != 0;
         const int key = wk0.y;
@@ -1665,7 +1746,8 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
                     float2 out;
                     bool have = true;
                     if (unc || !approx_update_f2<MODE>(prior, __uint_as_float(e.y), __uint_as_float(e.z), sh, out)) {
-                        ++exact;
+                        exact += (SF_DIAG_UNCONLY && !unc) ? 0 : 1;
+                        if (SF_DIAG_NOEXACT) continue;
                         const int l = slab_xrow(axis, hh, pos >> 3) + (pos & 7);
                         have = exact_voxel_f2<MODE>(sP, fc, sFp, key, l, prior, pix_dm, pix_var, pix_w, out);
                     }
@@ -1678,9 +1760,12 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
                     const uint32_t cell = *cellp;
                     uint32_t out;
                     int code = 0;
-                    if (unc || !approx_update<MODE>(cell, __uint_as_float(e.y), __uint_as_float(e.z), sh, s_tdec,
-                                                    s_adec, s_thr, out)) {
-                        ++exact;
+                    if (unc || (!approx_update<MODE>(cell, __uint_as_float(e.y), __uint_as_float(e.z), sh, s_tdec,
+                                                     s_adec, s_thr, out) &&
+                                !(kRefine && refine_update<MODE>(sP, sFp, aux, cell, __uint_as_float(e.y),
+                                                                 __uint_as_float(e.z), sh.eT, out)))) {
+                        exact += (SF_DIAG_UNCONLY && !unc) ? 0 : 1;
+                        if (SF_DIAG_NOEXACT) continue;
                         const int l = slab_xrow(axis, hh, pos >> 3) + (pos & 7);
                         code = exact_voxel<MODE>(sP, fc, sFp, aux, key, l, cell, pix_dm, pix_var, pix_w);
                         out = static_cast<uint32_t>(code);
@@ -1709,10 +1794,25 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
         __syncwarp();  // ring and slab reuse
         u0 = u1;
         wk0 = wk1;
-        u1 = u2;
-        wk1 = wk2;
+        if (kSlabPrefetch) {
+            u1 = u2;
+            wk1 = wk2;
+        } else {
+            u1 = take();
+            wk1 = load_item(u1);
+        }
     }
     cp_async_wait<0>();
+    clear_keybits(ctr, uniq, keybits);  // in the tail, where warps run out of units
+#if SF_DIAG_TIMES
+    if (lane == 0 && gwarp < 148 * 4 * 8) {
+        unsigned long long* d = g_slab_dbg + 4 * gwarp;
+        d[0] = t_entry;
+        d[1] = t_first;
+        d[2] = globaltimer_ns();
+        d[3] = n_done;
+    }
+#endif
     for (int off = 16; off > 0; off >>= 1) {
         updated += __shfl_down_sync(0xffffffffu, updated, off);
         exact += __shfl_down_sync(0xffffffffu, exact, off);
@@ -1721,6 +1821,11 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
     if (lane == 0 && exact) atomicAdd(&ctr->exact_voxels, (unsigned long long)exact);
     if (lane == 0) atomicMax(&ctr->t_end, globaltimer_ns());
 }
+#if SF_DIAG_TIMES
+extern "C" int sf_debug_slab_times(unsigned long long* out, int n) {
+    return (int)cudaMemcpyFromSymbol(out, g_slab_dbg, n * sizeof(unsigned long long));
+}
+#endif
 
 // ---- measurement refinement (fusion.cpp:99-143) ---------------------------------------
 // glibc's hypot (dbl-64, the non-FMA build of Borges' corrected algorithm used by the
