@@ -30,6 +30,16 @@
 
 namespace sf {
 
+#ifdef SF_DIAG_ICP_TAIL  // timing diagnostics: timestamps of the last step's tail
+__device__ unsigned long long g_icp_dbg[8];
+#define SF_ICP_STAMP(i) (g_icp_dbg[i] = globaltimer_ns())
+extern "C" int sf_debug_icp_tail(unsigned long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, g_icp_dbg, 8 * sizeof(unsigned long long));
+}
+#else
+#define SF_ICP_STAMP(i) ((void)0)
+#endif
+
 // COND: the launch sits in a graph with the device-side iteration loop and drives its
 // condition. (Separate instantiations: kernels that call the device graph API are not
 // profiled by Nsight Compute, so the eager / fixed-sequence form must not contain the call.)
@@ -107,39 +117,42 @@ __device__ __noinline__ void solve_finalize(IcpState* st, const double* s_sum, c
 // reference's own eigenvalue rounding, so the reference gates every direction in too. Then
 // x = A^-1 b by a second Cholesky (same solution up to rounding). Returns false (Jacobi path)
 // otherwise. One thread.
-__device__ __noinline__ bool fast_gated_solve(const double* s_fin, double n_pairs, double theta, double* x) {
+// The two factorisations run on two lanes: pass 0 the shifted one (the certificate), pass 1
+// the unshifted one and the two triangular solves (x). The fast path holds when both succeed.
+__device__ __noinline__ bool fast_gated_solve(const double* s_fin, double n_pairs, double theta, int pass, double* x) {
     double A[6][6];
 #pragma unroll
     for (int i = 0; i < 6; ++i)
 #pragma unroll
         for (int j = i; j < 6; ++j) A[i][j] = A[j][i] = s_fin[i * 6 - i * (i - 1) / 2 + (j - i)];
-    double fro = 0.0;
+    double sh = 0.0;
+    if (pass == 0) {
+        double fro = 0.0;
 #pragma unroll
-    for (int i = 0; i < 6; ++i)
+        for (int i = 0; i < 6; ++i)
 #pragma unroll
-        for (int j = 0; j < 6; ++j) fro += A[i][j] * A[i][j];
-    fro = sqrt(fro);
-    const double shift = theta * n_pairs * (1.0 + 1e-9) + 64.0 * 2.220446049250313e-16 * fro;
+            for (int j = 0; j < 6; ++j) fro += A[i][j] * A[i][j];
+        fro = sqrt(fro);
+        sh = theta * n_pairs * (1.0 + 1e-9) + 64.0 * 2.220446049250313e-16 * fro;
+    }
     double L[6][6];
-    for (int pass = 0; pass < 2; ++pass) {
-        const double sh = pass == 0 ? shift : 0.0;
 #pragma unroll
-        for (int j = 0; j < 6; ++j) {
-            double s = A[j][j] - sh;
+    for (int j = 0; j < 6; ++j) {
+        double s = A[j][j] - sh;
 #pragma unroll
-            for (int k = 0; k < j; ++k) s -= L[j][k] * L[j][k];
-            if (!(s > 0.0)) return false;
-            const double d = sqrt(s), inv = 1.0 / d;
-            L[j][j] = d;
+        for (int k = 0; k < j; ++k) s -= L[j][k] * L[j][k];
+        if (!(s > 0.0)) return false;
+        const double d = sqrt(s), inv = 1.0 / d;
+        L[j][j] = d;
 #pragma unroll
-            for (int i = j + 1; i < 6; ++i) {
-                double t = A[i][j];
+        for (int i = j + 1; i < 6; ++i) {
+            double t = A[i][j];
 #pragma unroll
-                for (int k = 0; k < j; ++k) t -= L[i][k] * L[j][k];
-                L[i][j] = t * inv;
-            }
+            for (int k = 0; k < j; ++k) t -= L[i][k] * L[j][k];
+            L[i][j] = t * inv;
         }
     }
+    if (pass == 0) return true;
     double y[6];
 #pragma unroll
     for (int i = 0; i < 6; ++i) {  // L y = b
@@ -201,8 +214,8 @@ __global__ void k_icp_report(IcpState* st) {
     if (lane == 0) st->eig_pending = 0;
 }
 
-constexpr int kStepCtas = 148;  // one CTA per SM (double-double accumulators); fixed => deterministic
-constexpr int kStepSmem = kSums * kIcpThreads * static_cast<int>(sizeof(DD));  // CTA-reduction transpose
+constexpr int kStepCtas = 296;  // two CTAs per SM; fixed => deterministic reduction tree
+constexpr int kStepSmem = kSums * kIcpThreads * static_cast<int>(sizeof(double));  // CTA-reduction transpose
 constexpr int kMergeLanes = kIcpThreads / kSums;  // threads per sum in the final merge (252 of 256 busy)
 
 // match_points association for source pixel i (registration.cpp:17-50).
@@ -296,12 +309,15 @@ __device__ __noinline__ void solve_from_sums(IcpState* st, double* s_sum, double
         s_fin[27] = s_sum[27];
     }
     __syncwarp();
-    __shared__ int s_fast;
-    if (lane == 0) {
-        double x[6];
-        s_fast = fast_gated_solve(s_fin, static_cast<double>(st->cur_count), prm.theta, x) ? 1 : 0;
+    if (lane == 0) SF_ICP_STAMP(2);
+    double x[6];
+    const bool ok = lane < 2 && fast_gated_solve(s_fin, static_cast<double>(st->cur_count), prm.theta, lane, x);
+    const bool s_fast = (__ballot_sync(0xffffffffu, ok) & 3u) == 3u;
+    if (lane == 1) {
+        SF_ICP_STAMP(3);
         if (s_fast) {
             finalize_motion(st, s_fin, x, prm);
+            SF_ICP_STAMP(4);
             *counter = 0;
             st->t_end = globaltimer_ns();
             if constexpr (COND)
@@ -344,13 +360,13 @@ __device__ __noinline__ void solve_from_sums(IcpState* st, double* s_sum, double
 // box and count to `rec` instead of solving; the ranks' records are then all-reduced and
 // k_icp_solve_ranks solves (identically on every rank).
 template <bool COND, bool PARTIAL = false>
-__global__ void __launch_bounds__(kIcpThreads, 1)
+__global__ void __launch_bounds__(kIcpThreads, 2)
     k_icp_step(const float* __restrict__ src, const float* __restrict__ src_n, const float* __restrict__ tgt,
                const float* __restrict__ tgt_n, Intr si, Intr ti, IcpParamsDev prm, IcpState* st,
                double* __restrict__ part_bbox, unsigned long long* __restrict__ part_count, DD* __restrict__ part,
                unsigned int* counter, cudaGraphConditionalHandle cond, int pix0 = 0, int pix1 = 0x7fffffff,
                IcpRankPartial* rec = nullptr) {
-    extern __shared__ DD s_red[];  // [kSums][kIcpThreads]
+    extern __shared__ double s_red[];  // [kSums][kIcpThreads]
     if (threadIdx.x == 0 && st->bodies == 0) atomicCAS(&st->t_step0, 0ull, globaltimer_ns());
     if (st->done) {  // converged / lost: end the device-side loop
         if constexpr (COND && !PARTIAL) {
@@ -361,9 +377,11 @@ __global__ void __launch_bounds__(kIcpThreads, 1)
     const Pose delta = st->delta;
     const int n = min(si.w * si.h, pix1);
     const int tid = threadIdx.x;
-    DD acc[kSums];
+    // per-thread partial sums in plain FP64 (a thread adds ~4 matches); double-double from the
+    // CTA reduction on
+    double acc[kSums];
 #pragma unroll
-    for (int k = 0; k < kSums; ++k) acc[k] = DD{0.0, 0.0};
+    for (int k = 0; k < kSums; ++k) acc[k] = 0.0;
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
     unsigned long long cnt = 0;
     for (int i = pix0 + blockIdx.x * blockDim.x + tid; i < n; i += gridDim.x * blockDim.x) {
@@ -376,10 +394,10 @@ __global__ void __launch_bounds__(kIcpThreads, 1)
 #pragma unroll
         for (int a = 0; a < 6; ++a)
 #pragma unroll
-            for (int b = a; b < 6; ++b, ++k) dd_add(acc[k], r[a] * r[b]);
+            for (int b = a; b < 6; ++b, ++k) acc[k] += r[a] * r[b];
 #pragma unroll
-        for (int a = 0; a < 6; ++a) dd_add(acc[21 + a], r[a] * d);
-        dd_add(acc[27], d * d);
+        for (int a = 0; a < 6; ++a) acc[21 + a] += r[a] * d;
+        acc[27] += d * d;
         const double pp[3] = {p.x, p.y, p.z}, qq[3] = {q.x, q.y, q.z};
 #pragma unroll
         for (int a = 0; a < 3; ++a) {  // shrink's bounding box (registration.cpp:54-59)
@@ -414,14 +432,13 @@ __global__ void __launch_bounds__(kIcpThreads, 1)
     for (int k = 0; k < kSums; ++k) s_red[k * kIcpThreads + tid] = acc[k];
     __syncthreads();
     constexpr int kSeg = kIcpThreads / 32;  // 8 segments of 32 threads per sum
-    DD seg{0.0, 0.0};
+    __shared__ DD s_seg[kSums][kSeg];
     if (tid < kSums * kSeg) {
-        const DD* row = s_red + (tid / kSeg) * kIcpThreads + (tid % kSeg) * 32;
-        seg = row[0];
-        for (int t = 1; t < 32; ++t) dd_merge(seg, row[t]);
+        const double* row = s_red + (tid / kSeg) * kIcpThreads + (tid % kSeg) * 32;
+        DD seg{row[0], 0.0};
+        for (int t = 1; t < 32; ++t) dd_add(seg, row[t]);
+        s_seg[tid / kSeg][tid % kSeg] = seg;
     }
-    __syncthreads();
-    if (tid < kSums * kSeg) s_red[(tid / kSeg) * kIcpThreads + (tid % kSeg)] = seg;
     if (tid == 0) {
         for (int w = 1; w < kIcpThreads / 32; ++w) {
             for (int a = 0; a < 3; ++a) {
@@ -435,11 +452,12 @@ __global__ void __launch_bounds__(kIcpThreads, 1)
     }
     __syncthreads();
     if (tid < kSums) {
-        DD a = s_red[tid * kIcpThreads];
-        for (int j = 1; j < kSeg; ++j) dd_merge(a, s_red[tid * kIcpThreads + j]);
+        DD a = s_seg[tid][0];
+        for (int j = 1; j < kSeg; ++j) dd_merge(a, s_seg[tid][j]);
         part[blockIdx.x * kSums + tid] = a;
     }
     if (!last_cta(counter)) return;
+    if (tid == 0) SF_ICP_STAMP(0);
 
     // ---- last CTA: merge the partials (fixed order) --------------------------------------
     const int nparts = gridDim.x;
@@ -510,7 +528,7 @@ __global__ void __launch_bounds__(kIcpThreads, 1)
             }
         }
     }
-    constexpr int L = kMergeLanes, kBatch = (kStepCtas + kMergeLanes - 1) / kMergeLanes;  // one L2 round trip
+    constexpr int L = kMergeLanes, kBatch = 17;  // partials in flight per thread (two L2 round trips)
     __shared__ DD s_m[kSums][L];
     __shared__ double s_sum[kSums], s_fin[kSums];
     if (tid < kSums * L) {
@@ -564,6 +582,7 @@ __global__ void __launch_bounds__(kIcpThreads, 1)
         s_sum[tid] = a.hi + a.lo;
     }
     __syncthreads();
+    if (tid == 0) SF_ICP_STAMP(1);
     if (tid >= 32) return;
     solve_from_sums<COND>(st, s_sum, s_fin, prm, counter, cond);
 }

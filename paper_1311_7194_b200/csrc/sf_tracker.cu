@@ -617,7 +617,11 @@ void sf_tracker::decode(const Fetch* f, int frame, int mode, uint64_t launches, 
     out->voxels_visited = out->blocks_processed * m * m * m;
     out->exact_voxels = f->ctr.exact_voxels;
     out->integrate_ns = f->ctr.t_end > f->ctr.t_begin ? f->ctr.t_end - f->ctr.t_begin : 0;
+#ifdef SF_DIAG_ICP_ASSOC  // timing diagnostics: the first step's association phase only
+    out->icp_ns = f->icp.t_step0 && f->icp.t_assoc0 > f->icp.t_step0 ? f->icp.t_assoc0 - f->icp.t_step0 : 0;
+#else
     out->icp_ns = f->icp.t_step0 && f->icp.t_end > f->icp.t_step0 ? f->icp.t_end - f->icp.t_step0 : 0;
+#endif
     out->icp_steps = f->icp.bodies;
     out->kernel_launches = launches;
     // device-side ICP loop: one launch per iteration body (three in the reference-order mode)

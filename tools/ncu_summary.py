@@ -1,5 +1,5 @@
 """Summarise one kernel of an .ncu-rep: SOL, occupancy, stall reasons, instruction mix.
-usage: python tools/ncu_summary.py report.ncu-rep"""
+usage: python tools/ncu_summary.py report.ncu-rep [row]  (row: which launch of the report, default 0)"""
 import csv
 import io
 import subprocess
@@ -9,7 +9,7 @@ from collections import Counter
 rep = sys.argv[1]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(io.StringIO(raw)))
-h, v = r[0], r[2]
+h, v = r[0], r[2 + (int(sys.argv[2]) if len(sys.argv) > 2 else 0)]
 d = dict(zip(h, v))
 keys = ["Kernel Name", "gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
