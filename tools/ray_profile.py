@@ -24,7 +24,8 @@ s = torch.cuda.current_stream()
 flush = torch.empty(400 << 20, dtype=torch.uint8, device=dev)
 ms = []
 for r in range(R + 3):
-    flush.fill_(r & 255)
+    if not os.environ.get("NOFLUSH"):
+        flush.fill_(r & 255)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
     _, _, st = gpu.raycast_result(g, poses[K], intr, out_depth=d, out_normals=n, stream=s.cuda_stream)
@@ -34,3 +35,13 @@ for r in range(R + 3):
         ms.append(e0.elapsed_time(e1))
 ms.sort()
 print(f"raycast: median {ms[len(ms)//2]*1e3:.1f} us, min {ms[0]*1e3:.1f} us; stats {st}")
+if os.environ.get("SF_DIAG_RB"):
+    import ctypes
+    lib = ctypes.CDLL(os.environ["SF_GPU_LIB"])
+    buf = (ctypes.c_ulonglong * 8)()
+    lib.sf_debug_rb(buf)
+    gpu.raycast_result(g, poses[K], intr, out_depth=d, out_normals=n, stream=s.cuda_stream)
+    torch.cuda.synchronize()
+    lib.sf_debug_rb(buf)
+    print(f"DDA rays {buf[4]} (with bounds {buf[5]}): loop iterations before first occupied {buf[0]}, after {buf[1]}; "
+          f"jumps before {buf[2]}, after {buf[3]}")
