@@ -25,12 +25,16 @@ for lay in sys.argv[2].split(",") if len(sys.argv) > 2 else ["codes", "float2"]:
     a = np.frombuffer(buf, dtype=np.uint64).reshape(W, 4).astype(np.int64)
     a = a[a[:, 0] > 0]
     t0 = a[:, 0].min()
-    e, f1, end, units = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3, (a[:, 2] - t0) / 1e3, a[:, 3]
+    e, f1, end, units = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3, (a[:, 2] - t0) / 1e3, a[:, 3] & 0xFFFF
+    last = e + (a[:, 3] >> 16) / 1e3
     q = lambda x: " ".join(f"{v:6.1f}" for v in np.percentile(x, [0, 10, 50, 90, 100]))
     print(f"{lay}: warps {len(a)}  (percentiles 0/10/50/90/100, us from first entry)")
     print(f"  entry      {q(e)}")
     print(f"  first unit {q(f1)}")
     print(f"  end        {q(end)}")
     print(f"  units      {q(units)}  total {units.sum()}")
+    o = np.argsort(-end)[:12]
+    print("  latest warps (gwarp: units, last unit start, end):",
+          "; ".join(f"{int(i)}: {int(units[i])}, {last[i]:.1f}, {end[i]:.1f}" for i in o))
     busy = end - f1
     print(f"  busy/unit  {q(busy / np.maximum(units, 1))}")
