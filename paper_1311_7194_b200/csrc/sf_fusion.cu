@@ -766,6 +766,7 @@ struct RowShared {
     float delta_f, echi;      // float payload: chi cut |T'| > delta certain outside delta +- echi
     double cx, cy;            // principal point (pixel-boundary planes of small-footprint rows)
     double eT;                // |T_f32 - T_ref| bound (m) of the phase-1 measurement
+    int lut_shift, lut_base, lut_n;  // variance-code lookup (AuxTables::lut; lut_n = 0: log-scale guess)
     int axis, lstep;          // row axis (0 x, 1 y, 2 z: the block axis closest to the optical axis), its l stride
 };
 
@@ -779,7 +780,11 @@ __device__ __forceinline__ int row_axis(const Pose& inv) {
 // Per-frame constants of the row kernels (one thread).
 template <int M>
 __device__ void row_kernel_init(const VolParams& P, const FrameConsts* __restrict__ fc, const FuseParams& fp,
-                                RowShared& sh, VolParams& sP, FuseParams& sFp, float* s_thr) {
+                                const AuxTables* __restrict__ aux, RowShared& sh, VolParams& sP, FuseParams& sFp,
+                                float* s_thr) {
+    sh.lut_shift = aux->lut_shift;
+    sh.lut_base = aux->lut_base;
+    sh.lut_n = aux->lut_n;
     s_thr[0] = -INFINITY;
     s_thr[257] = s_thr[258] = s_thr[259] = INFINITY;
     sP = P;
@@ -840,7 +845,7 @@ __device__ void row_kernel_init(const VolParams& P, const FrameConsts* __restric
 template <int MODE>
 __device__ __forceinline__ bool approx_update(uint32_t cell, float tk, float pf, const RowShared& rc,
                                               const float* s_tdec, const float* s_adec, const float* s_thr,
-                                              uint32_t& out) {
+                                              const uint2* s_lut, uint32_t& out) {
     const int code = static_cast<int>(static_cast<int8_t>(cell & 0xFF));
     const bool has_prior = code != kChiCode;
     const float pt = s_tdec[code + 128], pa = s_adec[cell >> 8];
@@ -874,6 +879,17 @@ __device__ __forceinline__ bool approx_update(uint32_t cell, float tk, float pf,
         // FP32 evaluation (<= 2e-6 relative) + the reference's own cancellation in
         // (1 - gain) * predicted (<= 1e-15 * predicted) + float thresholds (2^-24).
         const float m = 3e-6f * na + 1e-15f * pred;
+        if (rc.lut_n > 0) {
+            // the bucket of na's float bits holds at most one threshold: code = #below + (na >= it)
+            if (!(na >= 0.0f)) return false;
+            const int b = min(max(static_cast<int>(__float_as_uint(na) >> rc.lut_shift) - rc.lut_base, 0), rc.lut_n - 1);
+            const uint2 e = s_lut[b];
+            const int g = static_cast<int>(e.y) + (na >= __uint_as_float(e.x) ? 1 : 0);
+            if (!(na - m >= s_thr[g + 1]) && g > 0) return false;   // thresh[g]
+            if (!(na + m < s_thr[g + 2]) && g < 255) return false;  // thresh[g + 1]
+            out = static_cast<uint32_t>(static_cast<uint8_t>(tc)) | (static_cast<uint32_t>(g) << 8);
+            return true;
+        }
         // The log-scale guess is within 0.1 code of the encode formula, so the code is one of
         // round(guess) - 1 .. + 1: two comparisons settle it (s_thr is shifted by one with
         // -inf / +inf sentinels so every index below is in range).
@@ -1108,6 +1124,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
     constexpr int kRing = RowRing<MS>::kEntries;
     using RV = RowVec<MS>;
     __shared__ float s_tdec[256], s_adec[256], s_thr[260];  // s_thr[k + 1] = thresh[k]; +-inf sentinels
+    __shared__ uint2 s_lut[(P2 || MODE != 2) ? 1 : kAuxLut];  // variance-code lookup (codes, Kalman)
     extern __shared__ uint4 s_ring[];  // per warp kRing entries: {slot, l | cell << 9 | exact << 31, T, p}
     __shared__ RowShared sh;
     __shared__ VolParams sP;  // by reference into the (noinline) exact path without a stack copy
@@ -1119,7 +1136,9 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
         s_adec[i] = aux->aux_decode_f[i];
         s_thr[i + 1] = aux->aux_thresh_f[i];
     }
-    if (threadIdx.x == 0) row_kernel_init<M>(P, fc, fp, sh, sP, sFp, s_thr);
+    if (!P2 && MODE == 2)
+        for (int i = threadIdx.x; i < aux->lut_n; i += blockDim.x) s_lut[i] = aux->lut[i];
+    if (threadIdx.x == 0) row_kernel_init<M>(P, fc, fp, aux, sh, sP, sFp, s_thr);
     clear_keybits(ctr, uniq, keybits);
     __syncthreads();
     const uint32_t limit = ctr->limit, upd_base = ctr->upd_base;
@@ -1152,7 +1171,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
                 uint32_t out;
                 int code = 0;
                 if ((e.y >> 31) || !approx_update<MODE>(cell, __uint_as_float(e.z), __uint_as_float(e.w), sh, s_tdec,
-                                                        s_adec, s_thr, out)) {
+                                                        s_adec, s_thr, s_lut, out)) {
                     ++exact;
                     code = exact_voxel<MODE>(sP, fc, sFp, aux, slot_key[e.x], static_cast<int>(l), cell, pix_dm,
                                              pix_var, pix_w);
@@ -1479,6 +1498,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
     constexpr int M = 8, MS = 3, M3 = 512;
     using Cell = typename SlabSmem<P2>::Cell;
     __shared__ float s_tdec[256], s_adec[256], s_thr[260];  // s_thr[k + 1] = thresh[k]; +-inf sentinels
+    __shared__ uint2 s_lut[(P2 || MODE != 2) ? 1 : kAuxLut];  // variance-code lookup (codes, Kalman)
     extern __shared__ uint4 s_dyn[];  // rings (uint4 {pos | exact << 31, T, p, 0}), then the slabs
     __shared__ RowShared sh;
     __shared__ VolParams sP;
@@ -1571,7 +1591,9 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
         s_adec[i] = aux->aux_decode_f[i];
         s_thr[i + 1] = aux->aux_thresh_f[i];
     }
-    if (threadIdx.x == 0) row_kernel_init<M>(P, fc, fp, sh, sP, sFp, s_thr);
+    if (!P2 && MODE == 2)
+        for (int i = threadIdx.x; i < aux->lut_n; i += blockDim.x) s_lut[i] = aux->lut[i];
+    if (threadIdx.x == 0) row_kernel_init<M>(P, fc, fp, aux, sh, sP, sFp, s_thr);
     __syncthreads();
     for (int it = 0; u0 < n_units; ++it) {
         uint32_t u2 = n_units;
@@ -1761,7 +1783,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
                     uint32_t out;
                     int code = 0;
                     if (unc || (!approx_update<MODE>(cell, __uint_as_float(e.y), __uint_as_float(e.z), sh, s_tdec,
-                                                     s_adec, s_thr, out) &&
+                                                     s_adec, s_thr, s_lut, out) &&
                                 !(kRefine && refine_update<MODE>(sP, sFp, aux, cell, __uint_as_float(e.y),
                                                                  __uint_as_float(e.z), sh.eT, out)))) {
                         exact += (SF_DIAG_UNCONLY && !unc) ? 0 : 1;

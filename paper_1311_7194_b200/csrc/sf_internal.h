@@ -107,6 +107,7 @@ struct FrameCounters {
 };
 
 // Device-side aux codec tables (host-computed with the reference's libm).
+constexpr int kAuxLut = 1024;  // max buckets of the variance-code lookup
 struct AuxTables {
     double tsdf_decode[256];  // dequantize_tsdf(code)        (grid.cpp:25-27), index code+128
     double aux_decode[256];   // AuxQuantization::decode(code) (grid.cpp:48-51)
@@ -115,6 +116,11 @@ struct AuxTables {
     // their rounding error is part of that path's decision margins (sf_fusion.cu).
     float tsdf_decode_f[256], aux_decode_f[256], aux_thresh_f[256];
     int fp32_ok;  // all codec values representable as normal floats (else the FP64 kernel runs)
+    // Variance-mode code lookup on the float bits (lut_n > 0): bucket b = (bits(v) >> lut_shift)
+    // - lut_base (clamped to [0, lut_n)) holds at most one float threshold; lut[b] = {bits of that
+    // threshold (+inf if none), #thresholds below the bucket}, so code = lut[b].y + (v >= T).
+    int lut_shift, lut_base, lut_n;
+    uint2 lut[kAuxLut];
 };
 void build_aux_tables(const VolParams& P, AuxTables* t);
 uint8_t host_aux_encode(const VolParams& P, double value);  // reference encode (grid.cpp:38-46)

@@ -76,6 +76,16 @@ static double bitsd(uint64_t b) {
 // encode(v) == #{k : v >= thresh[k]}. Each threshold is located by bisection over the
 // ordered bit patterns of positive doubles, with the reference's own libm log: exact.
 static void build_aux_thresholds(const VolParams& P, AuxTables* t);
+static uint32_t f_bits(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    return u;
+}
+static float bits_f(uint32_t u) {
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
 void build_aux_tables(const VolParams& P, AuxTables* t) {
     for (int c = -128; c < 128; ++c) t->tsdf_decode[c + 128] = dequantize_tsdf(static_cast<int8_t>(c), P.delta);
     for (int c = 0; c < 256; ++c) t->aux_decode[c] = host_aux_decode(P, static_cast<uint8_t>(c));
@@ -93,6 +103,50 @@ void build_aux_tables(const VolParams& P, AuxTables* t) {
         if (!fits(t->tsdf_decode[c]) || !fits(t->aux_decode[c]) || !fits(t->aux_thresh[c])) t->fp32_ok = 0;
     }
     if (P.aux_mode == 0 && !fits(P.aux_w_max)) t->fp32_ok = 0;
+    // variance-code lookup over the float thresholds (see AuxTables)
+    t->lut_n = 0;
+    t->lut_shift = 0;
+    t->lut_base = 0;
+#ifndef SF_AUX_LUT
+#define SF_AUX_LUT 1
+#endif
+    if (SF_AUX_LUT && P.aux_mode == 1 && t->fp32_ok) {
+        std::vector<uint32_t> fin;  // bit patterns of the finite (positive) float thresholds, ascending
+        int n_neg = 0;
+        bool ok = true;
+        for (int k = 1; k < 256; ++k) {
+            const float f = t->aux_thresh_f[k];
+            if (f == -INFINITY) {
+                if (!fin.empty()) ok = false;  // -inf thresholds precede every finite one
+                ++n_neg;
+            } else if (std::isfinite(f)) {
+                if (!(f > 0.0f) || (!fin.empty() && !(f > bits_f(fin.back())))) ok = false;
+                fin.push_back(f_bits(f));
+            }
+        }
+        if (ok && !fin.empty()) {
+            int sh = 23;
+            for (; sh > 0; --sh) {  // coarsest buckets holding at most one threshold each
+                bool distinct = true;
+                for (size_t i = 1; i < fin.size(); ++i) distinct = distinct && (fin[i] >> sh) != (fin[i - 1] >> sh);
+                if (distinct) break;
+            }
+            const uint32_t base = fin.front() >> sh, n = (fin.back() >> sh) - base + 1;
+            bool distinct = true;
+            for (size_t i = 1; i < fin.size(); ++i) distinct = distinct && (fin[i] >> sh) != (fin[i - 1] >> sh);
+            if (distinct && n <= static_cast<uint32_t>(kAuxLut)) {
+                size_t j = 0;  // next finite threshold
+                for (uint32_t b = 0; b < n; ++b) {
+                    uint2 e = make_uint2(f_bits(INFINITY), static_cast<uint32_t>(n_neg + j));
+                    if (j < fin.size() && (fin[j] >> sh) == base + b) e.x = fin[j++];
+                    t->lut[b] = e;
+                }
+                t->lut_shift = sh;
+                t->lut_base = static_cast<int>(base);
+                t->lut_n = static_cast<int>(n);
+            }
+        }
+    }
 }
 
 static void build_aux_thresholds(const VolParams& P, AuxTables* t) {
