@@ -1704,24 +1704,31 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
             const unsigned lt_mask = (1u << lane) - 1u;
             const bool warp_small = __all_sync(0xffffffffu, small || (!fast && !exact_row));
             if (warp_small) {
+                // d - z_hi per candidate pixel; no measurement (no depth, or a lane without a
+                // small row) -> +1e30, which every voxel finds out of band
+                const float tb00 = small && c00.x > 0.0f ? c00.x - Azh : 1e30f;
+                const float tb10 = small && c10.x > 0.0f ? c10.x - Azh : 1e30f;
+                const float tb01 = small && c01.x > 0.0f ? c01.x - Azh : 1e30f;
+                const float tb11 = small && c11.x > 0.0f ? c11.x - Azh : 1e30f;
 #pragma unroll
                 for (int lx = 0; lx < M; ++lx) {
                     const float fl = static_cast<float>(lx);
                     const float su = fmaf(fl, dsu, su0), sv = fmaf(fl, dsv, sv0);
                     const bool iu = su > 0.0f, iv = sv > 0.0f;
-                    const bool cert = fabsf(su) > mu && fabsf(sv) > mv;
-                    const float2 px = iv ? (iu ? c11 : c01) : (iu ? c10 : c00);
-                    const float t = (px.x - Azh) - (lx == 0 ? Azl : fmaf(fl, Dzf, Azl));
-                    const float at = fabsf(t);
-                    const bool meas = small && px.x > 0.0f;
-                    const bool in = meas && cert && at < thr_in;
-                    const bool unc = small && (!cert || (meas && !(at < thr_in) && !(at > thr_out)));
-                    const bool q = in || unc;
+                    const bool cert = fabsf(su) > mu && fabsf(sv) > mv;  // lanes without a small row: su0, sv0 = -1e30
+                    const float tb = iv ? (iu ? tb11 : tb01) : (iu ? tb10 : tb00);
+                    const float t = tb - (lx == 0 ? Azl : fmaf(fl, Dzf, Azl));
+                    const bool gt = fabsf(t) > thr_out;
+                    // in: cert && |t| < thr_in; uncertain: !cert, or |t| between the thresholds
+                    const bool q = !cert || !gt;
                     const unsigned bal = __ballot_sync(0xffffffffu, q);
-                    if (q)
+                    if (q) {
+                        const bool unc = !cert || !(fabsf(t) < thr_in);
+                        const float pk = iv ? (iu ? c11.y : c01.y) : (iu ? c10.y : c00.y);
                         ring[tail + __popc(bal & lt_mask)] =
                             make_uint4(static_cast<uint32_t>(pos0 + lx * pstride) | (unc ? 0x80000000u : 0u),
-                                       __float_as_uint(t), __float_as_uint(px.y), 0u);
+                                       __float_as_uint(t), __float_as_uint(pk), 0u);
+                    }
                     tail += __popc(bal);
                 }
             } else {
