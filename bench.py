@@ -497,7 +497,7 @@ def run_ours(args, world, rank, local):
     peak, peak_kind = hbm_peak()
     # DRAM bytes per launch of the roofline kernel from the committed ncu capture
     traffic = {"codes": None, "float2": None}
-    tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r2_integrate_traffic.json")
+    tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r2_slab_integrate_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             t = json.load(f)
@@ -629,7 +629,7 @@ def run_ours(args, world, rank, local):
         "icp_steps_mean": sum(mm.icp_steps for mm in metrics) / steps,
         "icp_device_ms_mean": sum(mm.icp_ns for mm in metrics) / steps * 1e-6,
         "tracking_error_last_frame": pose_err,
-        "roofline": {"bound": "hbm", "kernel": "k_integrate_rows<Kalman>", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": "k_integrate_slab<Kalman, M=8, codes>", "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic["codes"],
                      "bytes_per_launch_mean": sum(integ_bytes) / steps,
                      "ms_per_launch_mean": sum(integ_ms) / steps,
@@ -637,8 +637,8 @@ def run_ours(args, world, rank, local):
         "integrate_only": {
             "workload": "C4 frames fused at their ground-truth poses (integrate-only, BASELINE configs[0] style); "
                         "same frames, fresh volumes",
-            "float2_payload": integrate_roofline(ms_f2, kern_f2, 16, "k_integrate_rows<Kalman, M=8, float2>", "float2"),
-            "codes_payload": integrate_roofline(ms_p1, kern_p1, 4, "k_integrate_rows<Kalman, M=8, codes>", "codes"),
+            "float2_payload": integrate_roofline(ms_f2, kern_f2, 16, "k_integrate_slab<Kalman, M=8, float2>", "float2"),
+            "codes_payload": integrate_roofline(ms_p1, kern_p1, 4, "k_integrate_slab<Kalman, M=8, codes>", "codes"),
             "same_block_tables": same_blocks,
             "algorithmic_bytes": "per processed block M^3 x (read + write) of the payload (float2: 8 + 8 B, codes: "
                                  "2 + 2 B per voxel) + its 8 B work item; per launch the 8 B/pixel {depth, p_k} table",

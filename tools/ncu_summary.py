@@ -9,15 +9,16 @@ from collections import Counter
 rep = sys.argv[1]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(io.StringIO(raw)))
-h, v = r[0], r[2 + (int(sys.argv[2]) if len(sys.argv) > 2 else 0)]
+h, u, v = r[0], r[1], r[2 + (int(sys.argv[2]) if len(sys.argv) > 2 else 0)]
 d = dict(zip(h, v))
+units = dict(zip(h, u))
 keys = ["Kernel Name", "gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "sm__cycles_active.avg", "gpc__cycles_elapsed.max", "launch__registers_per_thread",
         "lts__t_sector_hit_rate.pct"]
 for k in keys:
-    print(f"{k:60s} {d.get(k, '?')[:120]}")
+    print(f"{k:60s} {d.get(k, '?')[:120]} {units.get(k, '') if k != 'Kernel Name' else ''}")
 st = {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): float(x.replace(",", "") or 0)
       for k, x in d.items() if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")}
 tot = sum(st.values()) or 1
