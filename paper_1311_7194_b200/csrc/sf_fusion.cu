@@ -1051,25 +1051,13 @@ constexpr uint32_t kTailUnitsPerWarp = 8;  // single-unit grabs once this much w
 #ifndef SF_STATIC_PCT
 #define SF_STATIC_PCT 50
 #endif
-constexpr uint32_t kStaticPct = SF_STATIC_PCT;
+constexpr uint32_t kStaticPct = SF_STATIC_PCT;  // share of the row units dealt out statically
 #ifndef SF_SLAB  // M = 8: half-block slab kernel (k_integrate_slab) instead of k_integrate_rows
 #define SF_SLAB 1
 #endif
-#ifndef SF_DIAG_TIMES
+#ifndef SF_DIAG_TIMES  // timing diagnostics (tools/slab_times.py): per-warp timeline of k_integrate_slab
 #define SF_DIAG_TIMES 0
 #endif
-#ifndef SF_DIAG_UNCONLY  // diagnostics: count only the phase-1 uncertain voxels as exact
-#define SF_DIAG_UNCONLY 0
-#endif
-#ifndef SF_DIAG_NOEXACT  // timing diagnostics only (wrong results): no FP64 fallback
-#define SF_DIAG_NOEXACT 0
-#endif
-#ifndef SF_DIAG_NODRAIN  // timing diagnostics only (wrong results): skip phase 2 / the ring
-#define SF_DIAG_NODRAIN 0
-#endif
-#ifndef SF_DIAG_NOENQ
-#define SF_DIAG_NOENQ 0
-#endif  // share of the row units dealt out statically
 
 template <int MS>
 struct RowVec;
@@ -1150,7 +1138,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
     uint32_t updated = 0, exact = 0;
     // Phase 2 on ring entries [head, head + n): lanes take one entry each.
     auto drain = [&](uint32_t n) {
-        if (!SF_DIAG_NODRAIN && lane < n) {
+        if (lane < n) {
             const uint4 e = ring[(head + lane) & (kRing - 1)];
             const uint32_t l = e.y & 0x1FF, cell = (e.y >> 9) & 0xFFFF;
             if constexpr (P2) {
@@ -1379,7 +1367,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
                         ring[(tail + __popc(bal & lt_mask)) & (kRing - 1)] =
                             make_uint4(slot, meta, __float_as_uint(t), __float_as_uint(px.y));
                     }
-                    if (!SF_DIAG_NOENQ) tail += __popc(bal);
+                    tail += __popc(bal);
                     if (kRing < 32 * M + 31 && lx == M / 2 - 1) {  // half-row drain (small ring)
                         __syncwarp();
                         while (tail - head >= 32) drain(32);
@@ -1415,7 +1403,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
                         ring[(tail + __popc(bal & lt_mask)) & (kRing - 1)] =
                             make_uint4(slot, meta, __float_as_uint(t), __float_as_uint(px.y));
                     }
-                    if (!SF_DIAG_NOENQ) tail += __popc(bal);
+                    tail += __popc(bal);
                     if (kRing < 32 * M + 31 && lx == M / 2 - 1) {  // half-row drain (small ring)
                         __syncwarp();
                         while (tail - head >= 32) drain(32);
@@ -1775,8 +1763,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
                     float2 out;
                     bool have = true;
                     if (unc || !approx_update_f2<MODE>(prior, __uint_as_float(e.y), __uint_as_float(e.z), sh, out)) {
-                        exact += (SF_DIAG_UNCONLY && !unc) ? 0 : 1;
-                        if (SF_DIAG_NOEXACT) continue;
+                        ++exact;
                         const int l = slab_xrow(axis, hh, pos >> 3) + (pos & 7);
                         have = exact_voxel_f2<MODE>(sP, fc, sFp, key, l, prior, pix_dm, pix_var, pix_w, out);
                     }
@@ -1793,8 +1780,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
                                                      s_adec, s_thr, s_lut, out) &&
                                 !(kRefine && refine_update<MODE>(sP, sFp, aux, cell, __uint_as_float(e.y),
                                                                  __uint_as_float(e.z), sh.eT, out)))) {
-                        exact += (SF_DIAG_UNCONLY && !unc) ? 0 : 1;
-                        if (SF_DIAG_NOEXACT) continue;
+                        ++exact;
                         const int l = slab_xrow(axis, hh, pos >> 3) + (pos & 7);
                         code = exact_voxel<MODE>(sP, fc, sFp, aux, key, l, cell, pix_dm, pix_var, pix_w);
                         out = static_cast<uint32_t>(code);
