@@ -1544,27 +1544,29 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
         return u < n_units ? work_at(work, limit, upd_base, u >> 1) : make_int2(0, 0);
     };
     // Slab of unit u into buffer b: cp.async of this lane's x-row, or chi for a fresh block.
+    // float2: 16-byte chunk c = lane + 32 j of the slab is quarter (c & 3) of x-row c >> 2, so a
+    // warp's accesses are consecutive in shared memory (no bank conflicts) and in global memory.
     auto issue_slab = [&](uint32_t u, int2 wk, int b) {
         if (u >= n_units) return;
-        Cell* dst = slabs + b * kSlabVox + 8 * lane;
         const uint32_t slot = static_cast<uint32_t>(wk.x) & 0x7fffffffu;
-        if (static_cast<uint32_t>(wk.x) >> 31) {  // newly allocated block: chi (grid.cpp:87-100, grid.hpp:77-88)
-            uint4* d4 = reinterpret_cast<uint4*>(dst);
-            if constexpr (P2) {
-                const uint4 c = make_uint4(__float_as_uint(INFINITY), 0u, __float_as_uint(INFINITY), 0u);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) d4[j] = c;
-            } else {
-                d4[0] = make_uint4(0x00800080u, 0x00800080u, 0x00800080u, 0x00800080u);
-            }
-            return;
-        }
-        const size_t src = (size_t)slot * M3 + slab_xrow(axis, static_cast<int>(u & 1), lane);
+        const bool fresh_blk = (static_cast<uint32_t>(wk.x) >> 31) != 0;  // chi (grid.cpp:87-100, grid.hpp:77-88)
         if constexpr (P2) {
+            uint4* d4 = reinterpret_cast<uint4*>(slabs + b * kSlabVox);
+            const float2* g = fpay + (size_t)slot * M3;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) cp_async16(dst + 2 * j, fpay + src + 2 * j);
+            for (int j = 0; j < 4; ++j) {
+                const int c = lane + 32 * j;
+                if (fresh_blk)
+                    d4[c] = make_uint4(__float_as_uint(INFINITY), 0u, __float_as_uint(INFINITY), 0u);
+                else
+                    cp_async16(d4 + c, g + slab_xrow(axis, static_cast<int>(u & 1), c >> 2) + 2 * (c & 3));
+            }
         } else {
-            cp_async16(dst, payload + src);
+            Cell* dst = slabs + b * kSlabVox + 8 * lane;
+            if (fresh_blk)
+                *reinterpret_cast<uint4*>(dst) = make_uint4(0x00800080u, 0x00800080u, 0x00800080u, 0x00800080u);
+            else
+                cp_async16(dst, payload + (size_t)slot * M3 + slab_xrow(axis, static_cast<int>(u & 1), lane));
         }
     };
 
@@ -1796,14 +1798,17 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
         // ---------------- write-back: 32 x-rows, coalesced 16-byte stores ----------------
         if (__any_sync(0xffffffffu, wrote) || fresh) {
             __syncwarp();
-            const size_t dst = (size_t)slot * M3 + slab_xrow(axis, hh, lane);
-            const uint4* s4 = reinterpret_cast<const uint4*>(slab + 8 * lane);
             if constexpr (P2) {
-                uint4* g4 = reinterpret_cast<uint4*>(fpay + dst);
+                const uint4* s4 = reinterpret_cast<const uint4*>(slab);
+                float2* g = fpay + (size_t)slot * M3;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) g4[j] = s4[j];
+                for (int j = 0; j < 4; ++j) {
+                    const int c = lane + 32 * j;
+                    *reinterpret_cast<uint4*>(g + slab_xrow(axis, hh, c >> 2) + 2 * (c & 3)) = s4[c];
+                }
             } else {
-                *reinterpret_cast<uint4*>(payload + dst) = s4[0];
+                const uint4* s4 = reinterpret_cast<const uint4*>(slab + 8 * lane);
+                *reinterpret_cast<uint4*>(payload + (size_t)slot * M3 + slab_xrow(axis, hh, lane)) = s4[0];
             }
         }
         __syncwarp();  // ring and slab reuse
