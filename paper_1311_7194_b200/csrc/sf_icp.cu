@@ -215,7 +215,10 @@ __global__ void k_icp_report(IcpState* st) {
 }
 
 constexpr int kStepCtas = 296;  // two CTAs per SM; fixed => deterministic reduction tree
-constexpr int kStepSmem = kSums * kIcpThreads * static_cast<int>(sizeof(double));  // CTA-reduction transpose
+// CTA-reduction transpose [kSums][kIcpThreads / 32 segments][33]: the padding puts the 32-value
+// segments that the merge threads of one warp walk in lockstep on different banks
+constexpr int kSegStride = 33, kSumStride = (kIcpThreads / 32) * kSegStride;
+constexpr int kStepSmem = kSums * kSumStride * static_cast<int>(sizeof(double));
 constexpr int kMergeLanes = kIcpThreads / kSums;  // threads per sum in the final merge (252 of 256 busy)
 
 // match_points association for source pixel i (registration.cpp:17-50).
@@ -366,7 +369,7 @@ __global__ void __launch_bounds__(kIcpThreads, 2)
                double* __restrict__ part_bbox, unsigned long long* __restrict__ part_count, DD* __restrict__ part,
                unsigned int* counter, cudaGraphConditionalHandle cond, int pix0 = 0, int pix1 = 0x7fffffff,
                IcpRankPartial* rec = nullptr) {
-    extern __shared__ double s_red[];  // [kSums][kIcpThreads]
+    extern __shared__ double s_red[];  // [kSums][segments][kSegStride]
     if (threadIdx.x == 0 && st->bodies == 0) atomicCAS(&st->t_step0, 0ull, globaltimer_ns());
     if (st->done) {  // converged / lost: end the device-side loop
         if constexpr (COND && !PARTIAL) {
@@ -429,12 +432,12 @@ __global__ void __launch_bounds__(kIcpThreads, 2)
         s_c[wid] = cnt;
     }
 #pragma unroll
-    for (int k = 0; k < kSums; ++k) s_red[k * kIcpThreads + tid] = acc[k];
+    for (int k = 0; k < kSums; ++k) s_red[k * kSumStride + (tid >> 5) * kSegStride + (tid & 31)] = acc[k];
     __syncthreads();
     constexpr int kSeg = kIcpThreads / 32;  // 8 segments of 32 threads per sum
     __shared__ DD s_seg[kSums][kSeg];
     if (tid < kSums * kSeg) {
-        const double* row = s_red + (tid / kSeg) * kIcpThreads + (tid % kSeg) * 32;
+        const double* row = s_red + (tid / kSeg) * kSumStride + (tid % kSeg) * kSegStride;
         DD seg{row[0], 0.0};
         for (int t = 1; t < 32; ++t) dd_add(seg, row[t]);
         s_seg[tid / kSeg][tid % kSeg] = seg;
