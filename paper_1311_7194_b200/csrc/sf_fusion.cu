@@ -1487,7 +1487,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
     using Cell = typename SlabSmem<P2>::Cell;
     __shared__ float s_tdec[256], s_adec[256], s_thr[260];  // s_thr[k + 1] = thresh[k]; +-inf sentinels
     __shared__ uint2 s_lut[(P2 || MODE != 2) ? 1 : kAuxLut];  // variance-code lookup (codes, Kalman)
-    extern __shared__ uint4 s_dyn[];  // rings (uint4 {pos | exact << 31, T, p, 0}), then the slabs
+    extern __shared__ __align__(128) uint4 s_dyn[];  // rings (uint4 {pos | exact << 31, T, p, 0}), then the slabs
     __shared__ RowShared sh;
     __shared__ VolParams sP;
     __shared__ FuseParams sFp;

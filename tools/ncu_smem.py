@@ -20,7 +20,8 @@ ix = {h: i for i, h in enumerate(hdr)}
 acc = collections.Counter(); tot = collections.Counter()
 for r in rows:
     if len(r) != len(hdr) or not r[0].startswith("0x"): continue
-    ex = float(r[ix["L1 Wavefronts Shared Excessive"]] or 0); wf = float(r[ix["L1 Wavefronts Shared"]] or 0)
+    num = lambda v: float(v) if v.replace(".", "", 1).isdigit() else 0.0
+    ex = num(r[ix["L1 Wavefronts Shared Excessive"]]); wf = num(r[ix["L1 Wavefronts Shared"]])
     if wf == 0: continue
     key = amap.get(r[0], ("?", 0, r[1][:60]))
     acc[key] += ex; tot[key] += wf
