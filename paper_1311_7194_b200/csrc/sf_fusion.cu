@@ -1551,15 +1551,18 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
         const uint32_t slot = static_cast<uint32_t>(wk.x) & 0x7fffffffu;
         const bool fresh_blk = (static_cast<uint32_t>(wk.x) >> 31) != 0;  // chi (grid.cpp:87-100, grid.hpp:77-88)
         if constexpr (P2) {
-            uint4* d4 = reinterpret_cast<uint4*>(slabs + b * kSlabVox);
-            const float2* g = fpay + (size_t)slot * M3;
+            uint4* d4 = reinterpret_cast<uint4*>(slabs + b * kSlabVox) + lane;
+            // chunk j: x-row (lane >> 2) + 8 j, whose offset is linear in j (64 voxels per step
+            // for rows along x or y, 128 for rows along z)
+            const float2* g = fpay + (size_t)slot * M3 + slab_xrow(axis, static_cast<int>(u & 1), lane >> 2) +
+                              2 * (lane & 3);
+            const int gstep = axis == 2 ? 128 : 64;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const int c = lane + 32 * j;
                 if (fresh_blk)
-                    d4[c] = make_uint4(__float_as_uint(INFINITY), 0u, __float_as_uint(INFINITY), 0u);
+                    d4[32 * j] = make_uint4(__float_as_uint(INFINITY), 0u, __float_as_uint(INFINITY), 0u);
                 else
-                    cp_async16(d4 + c, g + slab_xrow(axis, static_cast<int>(u & 1), c >> 2) + 2 * (c & 3));
+                    cp_async16(d4 + 32 * j, g + j * gstep);
             }
         } else {
             Cell* dst = slabs + b * kSlabVox + 8 * lane;
@@ -1799,13 +1802,11 @@ __global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
         if (__any_sync(0xffffffffu, wrote) || fresh) {
             __syncwarp();
             if constexpr (P2) {
-                const uint4* s4 = reinterpret_cast<const uint4*>(slab);
-                float2* g = fpay + (size_t)slot * M3;
+                const uint4* s4 = reinterpret_cast<const uint4*>(slab) + lane;
+                float2* g = fpay + (size_t)slot * M3 + slab_xrow(axis, hh, lane >> 2) + 2 * (lane & 3);
+                const int gstep = axis == 2 ? 128 : 64;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int c = lane + 32 * j;
-                    *reinterpret_cast<uint4*>(g + slab_xrow(axis, hh, c >> 2) + 2 * (c & 3)) = s4[c];
-                }
+                for (int j = 0; j < 4; ++j) *reinterpret_cast<uint4*>(g + j * gstep) = s4[32 * j];
             } else {
                 const uint4* s4 = reinterpret_cast<const uint4*>(slab + 8 * lane);
                 *reinterpret_cast<uint4*>(payload + (size_t)slot * M3 + slab_xrow(axis, hh, lane)) = s4[0];
