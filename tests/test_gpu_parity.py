@@ -287,6 +287,65 @@ def test_float2_payload_c4_scale(gpu, workload_c4):
     assert live > 1_000_000
 
 
+def _axis_poses():
+    """Cameras whose optical axes are closest to x, y and z in turn, so the integrate kernel's
+    rows (along the block axis with the largest camera-z component) run along each axis: the
+    half-block slab layouts of all three row axes are exercised."""
+    import math
+    around_x = sf.orbit_trajectory([0.0, 0.0, 1.3], 1.3, 4, (1.0, 0.0, 0.0), 0.05, math.pi / 2)  # +y .. +z
+    around_y = sf.orbit_trajectory([0.0, 0.0, 1.3], 1.3, 2, (0.0, 1.0, 0.0), 0.1, 0.4)  # -x
+    poses = around_x + around_y
+    axes = {int(np.argmax(np.abs(p.rotation[:, 2]))) for p in poses}  # world axis of the camera's z
+    assert axes == {0, 1, 2}, axes
+    return poses
+
+
+@pytest.mark.parametrize("mode", [sf.FusionMode.Kalman, sf.FusionMode.Weighted, sf.FusionMode.Simple])
+def test_fuse_all_row_axes_bit_exact(gpu, oracle, mode):
+    """Codes layout, every row axis of the slab kernel: stats, table and payload bit-exact."""
+    intr = scenes.camera(320, 240, 262.5)
+    poses = _axis_poses()
+    frames = frames_for(gpu, scenes.sphere_plane_scene(), poses, intr, 2.0, sigma0=2.5e-4)
+    aux = sf.AuxMode.Variance if mode == sf.FusionMode.Kalman else sf.AuxMode.Weight
+    g, r = grids(gpu, oracle, scenes.c1_config(), 20000, aux)
+    params = sf.FusionParams(mode=mode, sigma0=2.5e-4)
+    for f, p in zip(frames, poses):
+        assert gpu.fuse_frame(g, f, p, params) == oracle.fuse_frame(r, f, p, params)
+        assert_same_volume(g, r)
+
+
+def test_float2_all_row_axes_match_reference_shadow(gpu, ref):
+    """Float2 layout, every row axis of the slab kernel, against the reference's FloatShadowGrid."""
+    cfg = sf.GridConfig(16, 8, (-1.0, -1.0, 0.25), 2.0, 0.0)  # 128^3: the reference shadow's limit
+    intr = scenes.camera(320, 240, 262.5)
+    poses = _axis_poses()
+    frames = frames_for(gpu, scenes.sphere_plane_scene(), poses, intr, 2.0, sigma0=2.5e-4)
+    g, r = grids(gpu, ref, cfg, 4096, sf.AuxMode.Variance)
+    g.set_payload_layout(g.FLOAT2)
+    assert ref.lib.volume_enable_shadow(r.handle) == 0
+    params = sf.FusionParams(mode=sf.FusionMode.Kalman, sigma0=2.5e-4)
+    for f, p in zip(frames, poses):
+        assert gpu.fuse_frame(g, f, p, params) == ref.fuse_frame(r, f, p, params)
+    assert np.array_equal(g.read_table(), r.read_table())
+    res, n, m = 128, 16, 8
+    st = np.zeros(res ** 3, np.float32)
+    sa = np.zeros(res ** 3, np.float32)
+    ref.lib.volume_read_shadow(r.handle, st.ctypes.data_as(C.POINTER(C.c_float)),
+                               sa.ctypes.data_as(C.POINTER(C.c_float)))
+    fp = g.read_float_payload()
+    table = g.read_table()
+    ours, theirs = [], []
+    for ti in np.flatnonzero(table >= 0):
+        slot = table[ti]
+        bx, by, bz = ti % n, (ti // n) % n, ti // (n * n)
+        ours.append(fp[slot * 512:(slot + 1) * 512])
+        dt = st.reshape(res, res, res)[bz * m:(bz + 1) * m, by * m:(by + 1) * m, bx * m:(bx + 1) * m].reshape(-1)
+        da = sa.reshape(res, res, res)[bz * m:(bz + 1) * m, by * m:(by + 1) * m, bx * m:(bx + 1) * m].reshape(-1)
+        theirs.append(np.stack([dt, da], -1))
+    live = _assert_float_close(np.concatenate(ours), np.concatenate(theirs), "float2 vs shadow, all axes")
+    assert live > 10000
+
+
 @pytest.fixture(scope="module")
 def workload_c4(gpu):
     import bench
