@@ -32,6 +32,10 @@ namespace sf {
 
 constexpr int kThreads = 256;
 constexpr int kPersistentCtas = 148 * 8;
+#ifndef SF_ALLOC_CTAS
+#define SF_ALLOC_CTAS (148 * 4)
+#endif
+constexpr int kAllocCtas = SF_ALLOC_CTAS;  // k_alloc_visible: rank CTAs + visibility CTAs (last-CTA epilogue)
 
 // ---------------------------------------------------------------------------------
 // frame setup (one warp: hull points, corner rays and SAT axes computed lane-parallel)
@@ -2236,7 +2240,7 @@ void launch_fuse(Volume& v, FrameBuffers& fb, const Intr& intr, const float* dep
                    w, h, fb.stride, su, sv, v.d_keybits, fb.keys_unique, fb.ctr, v.d_table, fb.ranks, fb.flags,
                    fb.work);
         SF_LAUNCH_CHECK();
-        launch_pdl(k_alloc_visible, dim3(kPersistentCtas), dim3(kThreads), 0, s, P, fb.fc, fb.ctr, v.d_vc, fb.ranks,
+        launch_pdl(k_alloc_visible, dim3(kAllocCtas), dim3(kThreads), 0, s, P, fb.fc, fb.ctr, v.d_vc, fb.ranks,
                    fb.flags, v.d_table, v.d_free_list, v.d_slot_key, v.d_occ, fb.keys_unique, v.d_keybits, depth, w,
                    h, fb.work);
         SF_LAUNCH_CHECK();
