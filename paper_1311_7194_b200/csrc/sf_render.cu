@@ -823,12 +823,18 @@ void launch_raycast(Volume& v, const FrameConsts* d_fc, const Intr& intr, const 
                     float* depth, float* normals, RayCounters* d_stats, cudaStream_t s, uint64_t* launches,
                     const int* dead_flag, const int* ray_list, RayBracket* brackets) {
     constexpr int G = 8;  // lanes per ray: 32 rays per 256-thread CTA, persistent over the list
-    const dim3 blk(256), grd(148 * 3);
+    const dim3 blk(256), grd(148 * SF_RAYCAST_CTAS);
     launch_pdl(k_raycast<G>, grd, blk, 0, s, v.P, d_fc, v.d_table, v.d_payload, v.d_occ, v.d_aux, t_start, t_end,
                depth, normals, d_stats, intr.w, intr.h, dead_flag, ray_list, brackets);
     SF_LAUNCH_CHECK();
     // one warp per CTA: the ~30 k bracketed rays spread over all SMs (latency-bound, few warps)
-    launch_pdl(k_raycast_refine, dim3(148 * 16), dim3(32), 0, s, v.P, d_fc, v.d_table, v.d_payload, v.d_occ,
+#ifndef SF_REFINE_CTAS
+#define SF_REFINE_CTAS 16
+#endif
+#ifndef SF_REFINE_THREADS
+#define SF_REFINE_THREADS 32
+#endif
+    launch_pdl(k_raycast_refine, dim3(148 * SF_REFINE_CTAS), dim3(SF_REFINE_THREADS), 0, s, v.P, d_fc, v.d_table, v.d_payload, v.d_occ,
                v.d_aux, brackets, depth, normals, d_stats, intr.w, dead_flag);
     SF_LAUNCH_CHECK();
     if (launches) *launches += 2;
