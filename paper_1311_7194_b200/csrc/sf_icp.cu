@@ -135,7 +135,7 @@ __device__ __noinline__ bool fast_gated_solve(const double* s_fin, double n_pair
         fro = sqrt(fro);
         sh = theta * n_pairs * (1.0 + 1e-9) + 64.0 * 2.220446049250313e-16 * fro;
     }
-    double L[6][6];
+    double L[6][6], invd[6];
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
         double s = A[j][j] - sh;
@@ -144,6 +144,7 @@ __device__ __noinline__ bool fast_gated_solve(const double* s_fin, double n_pair
         if (!(s > 0.0)) return false;
         const double d = sqrt(s), inv = 1.0 / d;
         L[j][j] = d;
+        invd[j] = inv;
 #pragma unroll
         for (int i = j + 1; i < 6; ++i) {
             double t = A[i][j];
@@ -159,14 +160,14 @@ __device__ __noinline__ bool fast_gated_solve(const double* s_fin, double n_pair
         double t = s_fin[21 + i];
 #pragma unroll
         for (int k = 0; k < i; ++k) t -= L[i][k] * y[k];
-        y[i] = t / L[i][i];
+        y[i] = t * invd[i];  // reciprocal of the pivot from the factorisation (ulp-level vs t / L[i][i])
     }
 #pragma unroll
     for (int i = 5; i >= 0; --i) {  // L^T x = y
         double t = y[i];
 #pragma unroll
         for (int k = i + 1; k < 6; ++k) t -= L[k][i] * x[k];
-        x[i] = t / L[i][i];
+        x[i] = t * invd[i];
     }
     return true;
 }
@@ -184,8 +185,8 @@ __device__ __noinline__ void finalize_motion(IcpState* st, const double* s_fin, 
 #pragma unroll
     for (int r = 1; r < 6; ++r) xn = xn + x[r] * x[r];
     st->shrunk_norm = sqrt(xn);
-    const d3 s = st->scale, c = st->center;
-    const d3 r = mk((1.0 / s.x) * x[0], (1.0 / s.y) * x[1], (1.0 / s.z) * x[2]);
+    const d3 is = st->inv_scale, c = st->center;  // inv_scale = 1.0 / scale (set with it)
+    const d3 r = mk(is.x * x[0], is.y * x[1], is.z * x[2]);
     const d3 t = sub(mk(x[3], x[4], x[5]), cross(r, c));
     st->motion_r = r;
     st->motion_t = t;
