@@ -466,53 +466,81 @@ __global__ void __launch_bounds__(kIcpThreads, 2)
     if (tid == 0) SF_ICP_STAMP(0);
 
     // ---- last CTA: merge the partials (fixed order) --------------------------------------
+    // The box / count partials and the 28 double-double sums are loaded and reduced in one pass
+    // (independent loads in flight together), then thread 0 finishes the box while 28 threads
+    // finish the sums.
     const int nparts = gridDim.x;
     __shared__ int s_lost;
-    {
-        double b[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
-        unsigned long long c = 0;
-        for (int p = tid; p < nparts; p += blockDim.x) {
+    constexpr int L = kMergeLanes, kBatch = 17;  // partials in flight per thread (two L2 round trips)
+    __shared__ DD s_m[kSums][L];
+    __shared__ double s_sum[kSums], s_fin[kSums];
+    double b[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    unsigned long long c = 0;
+    for (int p = tid; p < nparts; p += blockDim.x) {
 #pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                b[a] = dmin(b[a], __ldcg(&part_bbox[p * 6 + a]));
-                b[3 + a] = dmax(b[3 + a], __ldcg(&part_bbox[p * 6 + 3 + a]));
-            }
-            c += __ldcg(&part_count[p]);
+        for (int a = 0; a < 3; ++a) {
+            b[a] = dmin(b[a], __ldcg(&part_bbox[p * 6 + a]));
+            b[3 + a] = dmax(b[3 + a], __ldcg(&part_bbox[p * 6 + 3 + a]));
         }
+        c += __ldcg(&part_count[p]);
+    }
+    if (tid < kSums * L) {
+        const int k = tid % kSums, j = tid / kSums;
+        const double2* vp = reinterpret_cast<const double2*>(part);
+        DD a{0.0, 0.0};
+        bool first = true;
+        for (int p0 = j; p0 < nparts; p0 += kBatch * L) {
+            double2 v[kBatch];
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
+            for (int u = 0; u < kBatch; ++u) {
+                const int p = p0 + u * L;
+                v[u] = p < nparts ? __ldcg(&vp[p * kSums + k]) : make_double2(0.0, 0.0);
+            }
 #pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                b[a] = dmin(b[a], __shfl_down_sync(0xffffffffu, b[a], off));
-                b[3 + a] = dmax(b[3 + a], __shfl_down_sync(0xffffffffu, b[3 + a], off));
-            }
-            c += __shfl_down_sync(0xffffffffu, c, off);
-        }
-        __syncthreads();  // s_b / s_c reuse
-        if (lane == 0) {
-            for (int a = 0; a < 6; ++a) s_b[wid][a] = b[a];
-            s_c[wid] = c;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            for (int w = 1; w < kIcpThreads / 32; ++w) {
-                for (int a = 0; a < 3; ++a) {
-                    s_b[0][a] = dmin(s_b[0][a], s_b[w][a]);
-                    s_b[0][3 + a] = dmax(s_b[0][3 + a], s_b[w][3 + a]);
-                }
-                s_c[0] += s_c[w];
-            }
-            const unsigned long long total = s_c[0];
-            if constexpr (PARTIAL) {
-                rec->count = static_cast<double>(total);
-                for (int a = 0; a < 3; ++a) {
-                    rec->box[a] = s_b[0][a];
-                    rec->box[3 + a] = -s_b[0][3 + a];  // max as a min of the negation: one MIN all-reduce
+            for (int u = 0; u < kBatch; ++u) {
+                if (p0 + u * L >= nparts) break;
+                const DD x{v[u].x, v[u].y};
+                if (first) {
+                    a = x;
+                    first = false;
+                } else {
+                    dd_merge(a, x);
                 }
             }
         }
-        if constexpr (!PARTIAL) if (tid == 0) {
-            const unsigned long long total = s_c[0];
+        s_m[k][j] = a;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            b[a] = dmin(b[a], __shfl_down_sync(0xffffffffu, b[a], off));
+            b[3 + a] = dmax(b[3 + a], __shfl_down_sync(0xffffffffu, b[3 + a], off));
+        }
+        c += __shfl_down_sync(0xffffffffu, c, off);
+    }
+    __syncthreads();  // s_b / s_c reuse; s_m complete
+    if (lane == 0) {
+        for (int a = 0; a < 6; ++a) s_b[wid][a] = b[a];
+        s_c[wid] = c;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int w = 1; w < kIcpThreads / 32; ++w) {
+            for (int a = 0; a < 3; ++a) {
+                s_b[0][a] = dmin(s_b[0][a], s_b[w][a]);
+                s_b[0][3 + a] = dmax(s_b[0][3 + a], s_b[w][3 + a]);
+            }
+            s_c[0] += s_c[w];
+        }
+        const unsigned long long total = s_c[0];
+        if constexpr (PARTIAL) {
+            rec->count = static_cast<double>(total);
+            for (int a = 0; a < 3; ++a) {
+                rec->box[a] = s_b[0][a];
+                rec->box[3 + a] = -s_b[0][3 + a];  // max as a min of the negation: one MIN all-reduce
+            }
+        } else {
             if (st->bodies == 0) st->t_assoc0 = globaltimer_ns();
             st->bodies += 1;
             s_lost = total < 10 ? 1 : 0;
@@ -534,43 +562,19 @@ __global__ void __launch_bounds__(kIcpThreads, 2)
             }
         }
     }
-    constexpr int L = kMergeLanes, kBatch = 17;  // partials in flight per thread (two L2 round trips)
-    __shared__ DD s_m[kSums][L];
-    __shared__ double s_sum[kSums], s_fin[kSums];
-    if (tid < kSums * L) {
-        const int k = tid % kSums, j = tid / kSums;
-        const double2* vp = reinterpret_cast<const double2*>(part);
-        DD a{0.0, 0.0};
-        bool first = true;
-        for (int p0 = j; p0 < nparts; p0 += kBatch * L) {
-            double2 b[kBatch];
-#pragma unroll
-            for (int u = 0; u < kBatch; ++u) {
-                const int p = p0 + u * L;
-                b[u] = p < nparts ? __ldcg(&vp[p * kSums + k]) : make_double2(0.0, 0.0);
-            }
-#pragma unroll
-            for (int u = 0; u < kBatch; ++u) {
-                if (p0 + u * L >= nparts) break;
-                const DD x{b[u].x, b[u].y};
-                if (first) {
-                    a = x;
-                    first = false;
-                } else {
-                    dd_merge(a, x);
-                }
-            }
+    if (tid >= 32 && tid < 32 + kSums) {  // a warp other than thread 0's: overlaps the box work
+        const int k = tid - 32;
+        DD a = s_m[k][0];
+        for (int j = 1; j < L; ++j) dd_merge(a, s_m[k][j]);
+        if constexpr (PARTIAL) {
+            rec->sums[2 * k] = a.hi;
+            rec->sums[2 * k + 1] = a.lo;
+        } else {
+            s_sum[k] = a.hi + a.lo;
         }
-        s_m[k][j] = a;
     }
     __syncthreads();
     if constexpr (PARTIAL) {
-        if (tid < kSums) {
-            DD a = s_m[tid][0];
-            for (int j = 1; j < L; ++j) dd_merge(a, s_m[tid][j]);
-            rec->sums[2 * tid] = a.hi;
-            rec->sums[2 * tid + 1] = a.lo;
-        }
         if (tid == 0) *counter = 0;
         return;
     } else {
@@ -582,12 +586,6 @@ __global__ void __launch_bounds__(kIcpThreads, 2)
             return;
         }
     }
-    if (tid < kSums) {
-        DD a = s_m[tid][0];
-        for (int j = 1; j < L; ++j) dd_merge(a, s_m[tid][j]);
-        s_sum[tid] = a.hi + a.lo;
-    }
-    __syncthreads();
     if (tid == 0) SF_ICP_STAMP(1);
     if (tid >= 32) return;
     solve_from_sums<COND>(st, s_sum, s_fin, prm, counter, cond);
