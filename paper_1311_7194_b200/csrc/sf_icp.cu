@@ -217,12 +217,20 @@ __global__ void k_icp_report(IcpState* st) {
     if (lane == 0) st->eig_pending = 0;
 }
 
-constexpr int kStepCtas = 296;  // two CTAs per SM; fixed => deterministic reduction tree
-// CTA-reduction transpose [kSums][kIcpThreads / 32 segments][33]: the padding puts the 32-value
+#ifndef SF_ICP_STEP_THREADS
+#define SF_ICP_STEP_THREADS 256
+#endif
+#ifndef SF_ICP_STEP_CTAS
+#define SF_ICP_STEP_CTAS 296
+#endif
+constexpr int kStepThreads = SF_ICP_STEP_THREADS;  // k_icp_step: threads per CTA
+constexpr int kStepCtas = SF_ICP_STEP_CTAS;  // fixed => deterministic reduction tree
+static_assert(kStepCtas <= kIcpCtas, "partial buffers hold kIcpCtas CTAs");
+// CTA-reduction transpose [kSums][kStepThreads / 32 segments][33]: the padding puts the 32-value
 // segments that the merge threads of one warp walk in lockstep on different banks
-constexpr int kSegStride = 33, kSumStride = (kIcpThreads / 32) * kSegStride;
+constexpr int kSegStride = 33, kSumStride = (kStepThreads / 32) * kSegStride;
 constexpr int kStepSmem = kSums * kSumStride * static_cast<int>(sizeof(double));
-constexpr int kMergeLanes = kIcpThreads / kSums;  // threads per sum in the final merge (252 of 256 busy)
+constexpr int kMergeLanes = kStepThreads / kSums;  // threads per sum in the final merge (252 of 256 busy)
 
 // match_points association for source pixel i (registration.cpp:17-50).
 __device__ __forceinline__ bool associate(int i, const float* __restrict__ src, const float* __restrict__ src_n,
@@ -366,7 +374,7 @@ __device__ __noinline__ void solve_from_sums(IcpState* st, double* s_sum, double
 // box and count to `rec` instead of solving; the ranks' records are then all-reduced and
 // k_icp_solve_ranks solves (identically on every rank).
 template <bool COND, bool PARTIAL = false>
-__global__ void __launch_bounds__(kIcpThreads, 2)
+__global__ void __launch_bounds__(kStepThreads, 512 / kStepThreads)
     k_icp_step(const float* __restrict__ src, const float* __restrict__ src_n, const float* __restrict__ tgt,
                const float* __restrict__ tgt_n, Intr si, Intr ti, IcpParamsDev prm, IcpState* st,
                double* __restrict__ part_bbox, unsigned long long* __restrict__ part_count, DD* __restrict__ part,
@@ -423,8 +431,8 @@ __global__ void __launch_bounds__(kIcpThreads, 2)
         }
         cnt += __shfl_down_sync(0xffffffffu, cnt, off);
     }
-    __shared__ double s_b[kIcpThreads / 32][6];
-    __shared__ unsigned long long s_c[kIcpThreads / 32];
+    __shared__ double s_b[kStepThreads / 32][6];
+    __shared__ unsigned long long s_c[kStepThreads / 32];
     const int lane = tid & 31, wid = tid >> 5;
     if (lane == 0) {
 #pragma unroll
@@ -437,7 +445,7 @@ __global__ void __launch_bounds__(kIcpThreads, 2)
 #pragma unroll
     for (int k = 0; k < kSums; ++k) s_red[k * kSumStride + (tid >> 5) * kSegStride + (tid & 31)] = acc[k];
     __syncthreads();
-    constexpr int kSeg = kIcpThreads / 32;  // 8 segments of 32 threads per sum
+    constexpr int kSeg = kStepThreads / 32;  // 8 segments of 32 threads per sum
     __shared__ DD s_seg[kSums][kSeg];
     if (tid < kSums * kSeg) {
         const double* row = s_red + (tid / kSeg) * kSumStride + (tid % kSeg) * kSegStride;
@@ -446,7 +454,7 @@ __global__ void __launch_bounds__(kIcpThreads, 2)
         s_seg[tid / kSeg][tid % kSeg] = seg;
     }
     if (tid == 0) {
-        for (int w = 1; w < kIcpThreads / 32; ++w) {
+        for (int w = 1; w < kStepThreads / 32; ++w) {
             for (int a = 0; a < 3; ++a) {
                 s_b[0][a] = dmin(s_b[0][a], s_b[w][a]);
                 s_b[0][3 + a] = dmax(s_b[0][3 + a], s_b[w][3 + a]);
@@ -526,7 +534,7 @@ __global__ void __launch_bounds__(kIcpThreads, 2)
     }
     __syncthreads();
     if (tid == 0) {
-        for (int w = 1; w < kIcpThreads / 32; ++w) {
+        for (int w = 1; w < kStepThreads / 32; ++w) {
             for (int a = 0; a < 3; ++a) {
                 s_b[0][a] = dmin(s_b[0][a], s_b[w][a]);
                 s_b[0][3 + a] = dmax(s_b[0][3 + a], s_b[w][3 + a]);
@@ -670,7 +678,7 @@ __global__ void __launch_bounds__(32, 1)
 // The Kahan chains are sequential (4 dependent FP64 adds per match and sum), so an iteration
 // costs ~matches x the FP64 add latency; the tree path (default) is the fast one.
 // ---------------------------------------------------------------------------------
-constexpr int kExactCtas = kStepCtas;
+constexpr int kExactCtas = kIcpCtas;
 
 __host__ __device__ inline int exact_chunk(int n) {  // pixels per CTA range (multiple of 32)
     return ((n + kExactCtas - 1) / kExactCtas + 31) & ~31;
@@ -968,7 +976,7 @@ void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* 
                 cnt += 3;
                 continue;
             }
-            k_icp_step<false><<<kStepCtas, kIcpThreads, kStepSmem, s>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st,
+            k_icp_step<false><<<kStepCtas, kStepThreads, kStepSmem, s>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st,
                                                                         wk.part_bbox, wk.part_count, wk.part,
                                                                         wk.counters, 0);
             SF_LAUNCH_CHECK();
@@ -987,7 +995,7 @@ void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* 
         if (prm.exact)
             issue_exact_iteration<true>(wk, src, src_n, tgt, tgt_n, si, ti, prm, s, cond);
         else
-            k_icp_step<true><<<kStepCtas, kIcpThreads, kStepSmem, s>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st,
+            k_icp_step<true><<<kStepCtas, kStepThreads, kStepSmem, s>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st,
                                                                        wk.part_bbox, wk.part_count, wk.part,
                                                                        wk.counters, cond);
     } else {
@@ -1018,7 +1026,7 @@ void launch_icp(IcpWork& wk, const float* src, const float* src_n, const float* 
             throw;
         }
     } else {
-        k_icp_step<true><<<kStepCtas, kIcpThreads, kStepSmem, bs>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st,
+        k_icp_step<true><<<kStepCtas, kStepThreads, kStepSmem, bs>>>(src, src_n, tgt, tgt_n, si, ti, prm, wk.st,
                                                                     wk.part_bbox, wk.part_count, wk.part,
                                                                     wk.counters, cond);
     }
@@ -1048,11 +1056,11 @@ void launch_icp_ranks(IcpWork& wk, const float* src, const float* src_n, const f
             const int p0 = static_cast<int>(static_cast<long long>(n) * r / world);
             const int p1 = static_cast<int>(static_cast<long long>(n) * (r + 1) / world);
             if (cond_on)
-                k_icp_step<true, true><<<kStepCtas, kIcpThreads, kStepSmem, bs>>>(
+                k_icp_step<true, true><<<kStepCtas, kStepThreads, kStepSmem, bs>>>(
                     src, src_n, tgt, tgt_n, I, I, prm, wk.st, wk.part_bbox, wk.part_count, wk.part, wk.counters + 2,
                     cond, p0, p1, recs + i);
             else
-                k_icp_step<false, true><<<kStepCtas, kIcpThreads, kStepSmem, bs>>>(
+                k_icp_step<false, true><<<kStepCtas, kStepThreads, kStepSmem, bs>>>(
                     src, src_n, tgt, tgt_n, I, I, prm, wk.st, wk.part_bbox, wk.part_count, wk.part, wk.counters + 2,
                     0, p0, p1, recs + i);
             SF_LAUNCH_CHECK();
