@@ -1463,6 +1463,10 @@ constexpr bool kSlabPrefetch = SF_SLAB_PF;
 #endif
 constexpr bool kRefine = SF_REFINE;  // FP64 filter on the phase-1 inputs before the full FP64 path  // work items two units ahead (else one)
 constexpr int kSlabVox = 256;   // voxels per unit (32 rows of M = 8)
+// CTAs per SM of the slab kernel: codes 3 (80 registers; issue-bound, more warps pay), float2 2
+// (128 registers: no rematerialisation; the smaller instruction stream is latency-bound anyway)
+template <bool P2>
+constexpr int kSlabCtas = P2 ? 2 : kRowCtasPerSm;
 constexpr int kSlabRing = 256;  // queued voxels per warp: one unit's worth, drained per unit
 template <bool P2>
 struct SlabSmem {
@@ -1479,7 +1483,7 @@ __device__ __forceinline__ int slab_xrow(int axis, int h, int q) {
 }
 
 template <int MODE, bool P2>
-__global__ void __launch_bounds__(kRowThreads, kRowCtasPerSm)
+__global__ void __launch_bounds__(kRowThreads, kSlabCtas<P2>)
     k_integrate_slab(VolParams P, const FrameConsts* __restrict__ fc, FuseParams fp, const int2* __restrict__ work,
                      FrameCounters* __restrict__ ctr, const AuxTables* __restrict__ aux,
                      const float2* __restrict__ pix_f, const double* __restrict__ pix_dm,
@@ -2173,7 +2177,7 @@ static void launch_integrate_slab(Volume& v, FrameBuffers& fb, const FuseParams&
                                      (int)SlabSmem<P2>::kBytes));
         configured = true;
     }
-    launch_pdl(k_integrate_slab<MODE, P2>, dim3(148 * kRowCtasPerSm), dim3(kRowThreads), SlabSmem<P2>::kBytes, s,
+    launch_pdl(k_integrate_slab<MODE, P2>, dim3(148 * kSlabCtas<P2>), dim3(kRowThreads), SlabSmem<P2>::kBytes, s,
                v.P, fb.fc, fp, fb.work, fb.ctr, v.d_aux, fb.pix_f, fb.pix_dm, fb.pix_var, fb.pix_w, v.d_payload,
                v.d_fpayload, fb.keys_unique, v.d_keybits);
 }
